@@ -1,0 +1,157 @@
+"""CPU oracle for the Tsallis multilevel-thresholding hot path (arXiv 2012.10684).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, ``__graft_entry__.smoke()`` and
+bench.py's ``cpu_baseline`` / ``--impl reference`` legs, never by the product
+package.  Thin ctypes wrapper over ``tsallis_oracle.c`` (which documents every
+step with its PAPER.md citation); shares nothing with the CUDA path.
+
+Parity pins: every function here is pinned by tests/test_oracle_*.py against
+closed forms, exact rationals, textbook limits, brute force and invariants (see
+DESIGN.md "Oracle pins").  ``phi_at``/``search`` on the paper's own (private)
+data are "parity unpinned": the paper prints no threshold or objective values.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "tsallis_oracle.c")
+
+OK, INVALID_ARG, LEVEL_OVERFLOW, NO_VALID_SPLIT = 0, 1, 2, 3
+PSEUDO_ADDITIVE, SUM_PLUS_PRODUCT = 0, 1
+KMAX = 4
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC"]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("t", ctypes.c_int32 * KMAX),
+        ("phi", ctypes.c_double),
+        ("has_runner_up", ctypes.c_int32),
+        ("t2", ctypes.c_int32 * KMAX),
+        ("phi2", ctypes.c_double),
+        ("gap", ctypes.c_double),
+        ("tuples_valid", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        lib.oracle_histogram.restype = I
+        lib.oracle_histogram.argtypes = [P, I, I64, I, P]
+        lib.oracle_class_entropy.restype = D
+        lib.oracle_class_entropy.argtypes = [P, I, I, D, ctypes.POINTER(I)]
+        lib.oracle_phi_at.restype = D
+        lib.oracle_phi_at.argtypes = [P, I, I, D, I, P, ctypes.POINTER(I)]
+        lib.oracle_search.restype = I
+        lib.oracle_search.argtypes = [P, I, I, D, I, I, ctypes.POINTER(_Result)]
+        lib.oracle_label.restype = None
+        lib.oracle_label.argtypes = [P, I, I64, I, P, P]
+        lib.oracle_segment.restype = I
+        lib.oracle_segment.argtypes = [P, I, I64, I64, I64, I64, I64, I, I, D, I, I, I,
+                                       P, P, P, P, P, P]
+        lib.oracle_max_threads.restype = I
+        _lib = lib
+    return _lib
+
+
+def _u32(h):
+    h = np.ascontiguousarray(h, dtype=np.uint32)
+    return h
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def histogram(slice_, bins):
+    """(hist u32[bins], status) of one slice (any shape)."""
+    a = np.ascontiguousarray(slice_)
+    h = np.zeros(bins, np.uint32)
+    st = _load().oracle_histogram(a.ctypes.data, a.dtype.itemsize, a.size, bins, h.ctypes.data)
+    return h, int(st)
+
+
+def class_entropy(p, a, b, q):
+    """S of class [a,b] from probabilities p (None if the class is empty)."""
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    v = ctypes.c_int(0)
+    s = _load().oracle_class_entropy(p.ctypes.data, a, b, q, ctypes.byref(v))
+    return s if v.value else None
+
+
+def phi_at(hist, k, q, t, objective=PSEUDO_ADDITIVE):
+    """Objective at tuple t from the definition (None if invalid)."""
+    h = _u32(hist)
+    tt = np.ascontiguousarray(t, dtype=np.int32)
+    assert tt.size == k
+    v = ctypes.c_int(0)
+    r = _load().oracle_phi_at(h.ctypes.data, h.size, k, q, objective, tt.ctypes.data,
+                              ctypes.byref(v))
+    return r if v.value else None
+
+
+def search(hist, k, q, objective=PSEUDO_ADDITIVE, level=1):
+    """Exhaustive argmax.  Returns dict(status, t, phi, t2, phi2, gap, tuples_valid)."""
+    h = _u32(hist)
+    r = _Result()
+    _load().oracle_search(h.ctypes.data, h.size, k, q, objective, level, ctypes.byref(r))
+    return {
+        "status": int(r.status),
+        "t": tuple(int(x) for x in r.t[:k]),
+        "phi": float(r.phi),
+        "t2": tuple(int(x) for x in r.t2[:k]) if r.has_runner_up else None,
+        "phi2": float(r.phi2) if r.has_runner_up else None,
+        "gap": float(r.gap),
+        "tuples_valid": int(r.tuples_valid),
+    }
+
+
+def label(slice_, k, t):
+    a = np.ascontiguousarray(slice_)
+    tt = np.ascontiguousarray(t, dtype=np.int32)
+    out = np.empty(a.shape, np.uint8)
+    _load().oracle_label(a.ctypes.data, a.dtype.itemsize, a.size, k, tt.ctypes.data,
+                         out.ctypes.data)
+    return out
+
+
+def segment(vol, bins, k, q, objective=PSEUDO_ADDITIVE, level=1, z0=0, z1=None,
+            threads=None, labels=True):
+    """Whole path for slices [z0, z1) of vol[nz][ny][nx].  Arrays are indexed by
+    absolute slice; entries outside [z0, z1) are left zero/NaN."""
+    v = np.ascontiguousarray(vol)
+    nz, ny, nx = v.shape
+    z1 = nz if z1 is None else z1
+    hist = np.zeros((nz, bins), np.uint32)
+    thr = np.full((nz, k), -1, np.int32)
+    phi = np.full(nz, np.nan)
+    gap = np.full(nz, np.nan)
+    status = np.full(nz, -1, np.int32)
+    lab = np.zeros(v.shape, np.uint8) if labels else None
+    threads = threads or max_threads()
+    _load().oracle_segment(v.ctypes.data, v.dtype.itemsize, nx, ny, nz, z0, z1, bins, k, q,
+                           objective, level, threads, hist.ctypes.data, thr.ctypes.data,
+                           phi.ctypes.data, gap.ctypes.data, status.ctypes.data,
+                           lab.ctypes.data if labels else None)
+    return {"hist": hist, "thresholds": thr, "phi": phi, "gap": gap, "status": status,
+            "labels": lab}

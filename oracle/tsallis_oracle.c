@@ -1,0 +1,404 @@
+/*
+ * oracle/tsallis_oracle.c -- plain, slow, obviously-correct CPU oracle for the
+ * Tsallis multilevel-thresholding hot path of arXiv 2012.10684.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  It
+ * shares no code, header, table or constant with the CUDA path
+ * (paper_2012_10684_b200/csrc) and neither side includes the other.
+ *
+ * Build: gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp -shared -fPIC
+ * (no FMA contraction, no re-association: every sum below is the sequential
+ * ascending sum it is written as -- DESIGN.md reading R9).
+ *
+ * What it computes, per slice (PAPER.md line numbers refer to the v2 text,
+ * lines 367-807 of /root/reference/PAPER.md):
+ *
+ *   1. histogram c_i = #{voxels with value i}                 PAPER.md:456-462 (Fig. hist, 1-D
+ *      brightness histogram; "first dimension" :564).  Any voxel >= L is a
+ *      LEVEL_OVERFLOW for the slice (never clamped; R13).
+ *   2. p_i = c_i / N, N = sum of c                            PAPER.md:579 (set P, sum p = 1)
+ *   3. per class C = [a,b]:  P = sum_{i=a..b} p_i             PAPER.md:587-591 (class mass)
+ *        q != 1:  S = (1 - sum_{i=a..b} (p_i/P)^q) / (q - 1)  PAPER.md:581-585 (H^alpha_1, H^alpha_2;
+ *                 summand read as p_i/P_j -- DESIGN.md R3; 0^q = 0)
+ *        q == 1:  S = -sum (p_i/P) ln(p_i/P), 0 ln 0 = 0      Shannon limit (R6)
+ *      P == 0  => the class is empty and the tuple is skipped (R5).
+ *   4. classes of a tuple t_1 < ... < t_k, t_j in [0, L-2]:
+ *        C_0 = [0, t_1], C_j = [t_j + 1, t_{j+1}], C_k = [t_k + 1, L-1]
+ *      (t_j is the last bin of the lower class; PAPER.md:582,:588 -- DESIGN.md R4)
+ *   5. objective (R1):
+ *        PSEUDO_ADDITIVE (default): phi = S_0; for j = 1..k: phi = phi + S_j + (1-q) phi S_j
+ *          -- PAPER.md:593-596 (H1 + H2 + (1-alpha) H1 H2) applied left to right
+ *        SUM_PLUS_PRODUCT: phi = (S_0 + ... + S_k) + (1-q) (S_0 * ... * S_k)
+ *   6. argmax over all tuples in lexicographic order, replacing the best only on
+ *      a strictly greater phi, so the lowest tuple wins ties  (PAPER.md:594,:597
+ *      "Arg max"; tie rule DESIGN.md R8).  No valid tuple => NO_VALID_SPLIT.
+ *      Runner-up: best phi over canonical tuples (every t_j a non-empty bin,
+ *      i.e. distinct partitions) other than t*;  gap = (phi* - phi2)/|phi*|.
+ *   7. labels: label(v) = #{ j : v > t_j }   -- Algorithm 1 (PAPER.md:464-477,
+ *      ">= T -> 1") with T = t + 1 for k = 1, generalised to k thresholds (R4).
+ *
+ * Level 0 recomputes every class sum from the definition for every tuple.
+ * Level 1 memoises S per distinct class content, keyed by (first non-empty bin
+ * >= a, last non-empty bin <= b).  Because every term is >= 0 and adding +0.0
+ * is exact, the sums over [a,b] and over that key range are the same sequence
+ * of non-zero additions, so Level 1 is bit-identical to Level 0 (tested).
+ *
+ * Pins (tests/test_oracle_*.py): numpy.bincount; closed forms for uniform
+ * histograms (mpmath); exact rationals at q = 2 (fractions); Kapur-Sahoo-Wong
+ * closed form at q = 1; point masses; gap phantoms; mirror symmetry; scale
+ * invariance; log-domain DP; Level 0 = Level 1 bit-exactly.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_LEVEL_OVERFLOW 2
+#define OR_NO_VALID_SPLIT 3
+#define OR_INVALID_ARG 1
+
+#define OR_OBJ_PSEUDO_ADDITIVE 0
+#define OR_OBJ_SUM_PLUS_PRODUCT 1
+
+#define OR_KMAX 4
+
+/* ---------------------------------------------------------------- step 1 */
+/* Histogram of one slice.  dtype_bytes 1 = u8, 2 = u16.
+ * Returns OR_LEVEL_OVERFLOW if any voxel >= bins (those voxels are not counted). */
+int oracle_histogram(const void *slice, int dtype_bytes, int64_t n, int bins,
+                     uint32_t *hist) {
+  int status = OR_OK;
+  for (int i = 0; i < bins; i++) hist[i] = 0;
+  for (int64_t x = 0; x < n; x++) {
+    unsigned v = dtype_bytes == 1 ? ((const uint8_t *)slice)[x]
+                                  : ((const uint16_t *)slice)[x];
+    if (v >= (unsigned)bins) {
+      status = OR_LEVEL_OVERFLOW;
+      continue;
+    }
+    hist[v] += 1;
+  }
+  return status;
+}
+
+/* ---------------------------------------------------------------- step 2 */
+static void probabilities(const uint32_t *hist, int bins, double *p) {
+  double N = 0.0;
+  for (int i = 0; i < bins; i++) N += (double)hist[i]; /* exact: N < 2^53 */
+  for (int i = 0; i < bins; i++) p[i] = (double)hist[i] / N;
+}
+
+/* ---------------------------------------------------------------- step 3 */
+/* Tsallis entropy of the class [a,b] (class mass :587-591).
+ * *valid = 0 when the class mass P is zero (empty class). */
+double oracle_class_entropy(const double *p, int a, int b, double q, int *valid) {
+  double P = 0.0;
+  for (int i = a; i <= b; i++) P = P + p[i];
+  if (P == 0.0) {
+    *valid = 0;
+    return 0.0;
+  }
+  *valid = 1;
+  if (q == 1.0) {
+    double H = 0.0;
+    for (int i = a; i <= b; i++) {
+      if (p[i] > 0.0) {
+        double r = p[i] / P;
+        H = H - r * log(r);
+      }
+    }
+    return H;
+  }
+  double A = 0.0;
+  for (int i = a; i <= b; i++) {
+    if (p[i] > 0.0) A = A + pow(p[i] / P, q); /* 0^q = 0 */
+  }
+  return (1.0 - A) / (q - 1.0);
+}
+
+/* ---------------------------------------------------------------- step 5 */
+static double combine(const double *S, int nclass, double q, int objective) {
+  if (objective == OR_OBJ_SUM_PLUS_PRODUCT) {
+    double sum = 0.0, prod = 1.0;
+    for (int j = 0; j < nclass; j++) sum = sum + S[j];
+    for (int j = 0; j < nclass; j++) prod = prod * S[j];
+    return sum + (1.0 - q) * prod;
+  }
+  double phi = S[0];
+  for (int j = 1; j < nclass; j++) phi = phi + S[j] + (1.0 - q) * phi * S[j];
+  return phi;
+}
+
+/* class bounds of tuple t (step 4) */
+static void class_bounds(const int *t, int k, int bins, int *lo, int *hi) {
+  lo[0] = 0;
+  for (int j = 0; j < k; j++) {
+    hi[j] = t[j];
+    lo[j + 1] = t[j] + 1;
+  }
+  hi[k] = bins - 1;
+}
+
+/* Objective at one tuple, straight from the definition (Level 0).  *valid = 0
+ * when some class is empty or the tuple is not strictly increasing in
+ * [0, bins-2]. */
+double oracle_phi_at(const uint32_t *hist, int bins, int k, double q,
+                     int objective, const int *t, int *valid) {
+  *valid = 0;
+  if (k < 1 || k > OR_KMAX) return NAN;
+  for (int j = 0; j < k; j++) {
+    if (t[j] < 0 || t[j] > bins - 2) return NAN;
+    if (j > 0 && t[j] <= t[j - 1]) return NAN;
+  }
+  double *p = (double *)malloc(sizeof(double) * bins);
+  probabilities(hist, bins, p);
+  int lo[OR_KMAX + 1], hi[OR_KMAX + 1];
+  double S[OR_KMAX + 1];
+  class_bounds(t, k, bins, lo, hi);
+  for (int j = 0; j <= k; j++) {
+    int v;
+    S[j] = oracle_class_entropy(p, lo[j], hi[j], q, &v);
+    if (!v) {
+      free(p);
+      return NAN;
+    }
+  }
+  free(p);
+  *valid = 1;
+  return combine(S, k + 1, q, objective);
+}
+
+/* ---------------------------------------------------------------- step 6 */
+typedef struct {
+  int32_t status;
+  int32_t t[OR_KMAX];
+  double phi;
+  int32_t has_runner_up;
+  int32_t t2[OR_KMAX];
+  double phi2;
+  double gap;
+  int64_t tuples_valid;
+} oracle_result;
+
+typedef struct {
+  int level;
+  int bins, m;
+  const double *p;
+  double q;
+  int *first_nz_ge; /* [bins+1] index into nz[] of first non-empty bin >= a */
+  int *last_nz_le;  /* [bins]   index into nz[] of last non-empty bin <= b, -1 if none */
+  int *nz;          /* [m] non-empty bins ascending */
+  double *memo;     /* [m*m] Level 1 */
+  unsigned char *have;
+} class_ctx;
+
+static double class_S(class_ctx *c, int a, int b, int *valid) {
+  if (c->level == 0) return oracle_class_entropy(c->p, a, b, c->q, valid);
+  int ia = c->first_nz_ge[a];
+  int ib = c->last_nz_le[b];
+  if (ib < 0 || ia >= c->m || ia > ib) {
+    *valid = 0;
+    return 0.0;
+  }
+  *valid = 1;
+  size_t key = (size_t)ia * (size_t)c->m + (size_t)ib;
+  if (!c->have[key]) {
+    int v;
+    c->memo[key] = oracle_class_entropy(c->p, c->nz[ia], c->nz[ib], c->q, &v);
+    c->have[key] = 1;
+  }
+  return c->memo[key];
+}
+
+/* Exhaustive search over every t_1 < ... < t_k in [0, L-2], lexicographic
+ * order, strict-greater argmax (lowest tuple wins).  level 0 or 1. */
+int oracle_search(const uint32_t *hist, int bins, int k, double q, int objective,
+                  int level, oracle_result *out) {
+  memset(out, 0, sizeof(*out));
+  for (int j = 0; j < OR_KMAX; j++) out->t[j] = out->t2[j] = -1;
+  out->phi = out->phi2 = out->gap = NAN;
+  if (k < 1 || k > OR_KMAX || bins < 2 || k > bins - 1 || !(q > 0.0) || !isfinite(q)) {
+    out->status = OR_INVALID_ARG;
+    return OR_INVALID_ARG;
+  }
+  double N = 0.0;
+  for (int i = 0; i < bins; i++) N += (double)hist[i];
+  if (N == 0.0) {
+    out->status = OR_NO_VALID_SPLIT;
+    return OR_NO_VALID_SPLIT;
+  }
+  class_ctx c;
+  memset(&c, 0, sizeof(c));
+  c.level = level;
+  c.bins = bins;
+  c.q = q;
+  double *p = (double *)malloc(sizeof(double) * bins);
+  probabilities(hist, bins, p);
+  c.p = p;
+  c.nz = (int *)malloc(sizeof(int) * bins);
+  c.first_nz_ge = (int *)malloc(sizeof(int) * (bins + 1));
+  c.last_nz_le = (int *)malloc(sizeof(int) * bins);
+  int m = 0;
+  for (int i = 0; i < bins; i++) {
+    c.last_nz_le[i] = -1;
+    if (hist[i] > 0) c.nz[m++] = i;
+    c.last_nz_le[i] = m - 1;
+  }
+  c.m = m;
+  {
+    /* first_nz_ge[i] = number of non-empty bins < i == index of first non-empty >= i */
+    int cnt = 0;
+    for (int i = 0; i < bins; i++) {
+      c.first_nz_ge[i] = cnt;
+      if (hist[i] > 0) cnt++;
+    }
+    c.first_nz_ge[bins] = cnt;
+  }
+  if (level == 1) {
+    c.memo = (double *)malloc(sizeof(double) * (size_t)m * (size_t)m + 8);
+    c.have = (unsigned char *)calloc((size_t)m * (size_t)m + 8, 1);
+  }
+
+  int t[OR_KMAX], lo[OR_KMAX + 1], hi[OR_KMAX + 1];
+  double S[OR_KMAX + 1];
+  for (int j = 0; j < k; j++) t[j] = j;
+  int found = 0;
+  double best = -INFINITY;
+  /* canonical top-2 */
+  int c_found = 0, c2_found = 0;
+  double c1v = -INFINITY, c2v = -INFINITY;
+  int c1t[OR_KMAX], c2t[OR_KMAX];
+  int64_t nvalid = 0;
+  for (;;) {
+    class_bounds(t, k, bins, lo, hi);
+    int ok = 1;
+    for (int j = 0; j <= k && ok; j++) {
+      int v;
+      S[j] = class_S(&c, lo[j], hi[j], &v);
+      ok = v;
+    }
+    if (ok) {
+      nvalid++;
+      double phi = combine(S, k + 1, q, objective);
+      if (!found || phi > best) {
+        best = phi;
+        found = 1;
+        for (int j = 0; j < k; j++) out->t[j] = t[j];
+      }
+      int canonical = 1;
+      for (int j = 0; j < k; j++)
+        if (hist[t[j]] == 0) canonical = 0;
+      if (canonical) {
+        if (!c_found || phi > c1v) {
+          if (c_found) {
+            c2v = c1v;
+            c2_found = 1;
+            memcpy(c2t, c1t, sizeof(c1t));
+          }
+          c1v = phi;
+          c_found = 1;
+          memcpy(c1t, t, sizeof(int) * k);
+        } else if (!c2_found || phi > c2v) {
+          c2v = phi;
+          c2_found = 1;
+          memcpy(c2t, t, sizeof(int) * k);
+        }
+      }
+    }
+    /* lexicographic successor of t over [0, bins-2] */
+    int j = k - 1;
+    while (j >= 0 && t[j] == bins - 2 - (k - 1 - j)) j--;
+    if (j < 0) break;
+    t[j]++;
+    for (int jj = j + 1; jj < k; jj++) t[jj] = t[jj - 1] + 1;
+  }
+  out->tuples_valid = nvalid;
+  if (!found) {
+    out->status = OR_NO_VALID_SPLIT;
+    for (int j = 0; j < OR_KMAX; j++) out->t[j] = -1;
+  } else {
+    out->status = OR_OK;
+    out->phi = best;
+    if (c2_found) {
+      out->has_runner_up = 1;
+      out->phi2 = c2v;
+      for (int j = 0; j < k; j++) out->t2[j] = c2t[j];
+      if (best == 0.0)
+        out->gap = (c2v == 0.0) ? 0.0 : INFINITY;
+      else
+        out->gap = (best - c2v) / fabs(best);
+    } else {
+      out->gap = INFINITY;
+    }
+  }
+  free(p);
+  free(c.nz);
+  free(c.first_nz_ge);
+  free(c.last_nz_le);
+  free(c.memo);
+  free(c.have);
+  return out->status;
+}
+
+/* ---------------------------------------------------------------- step 7 */
+/* label(v) = #{ j : v > t_j }  (Algorithm 1, with T = t+1) */
+void oracle_label(const void *slice, int dtype_bytes, int64_t n, int k,
+                  const int32_t *t, uint8_t *labels) {
+  for (int64_t x = 0; x < n; x++) {
+    unsigned v = dtype_bytes == 1 ? ((const uint8_t *)slice)[x]
+                                  : ((const uint16_t *)slice)[x];
+    int l = 0;
+    for (int j = 0; j < k; j++)
+      if ((int)v > t[j]) l++;
+    labels[x] = (uint8_t)l;
+  }
+}
+
+/* ------------------------------------------------------------- whole path */
+/* Steps 1-7 for slices [z0, z1) of a [nz][ny][nx] volume.  Outputs are indexed
+ * by absolute slice z.  labels may be NULL.  OpenMP over slices (each slice is
+ * independent; results do not depend on the thread count). */
+int oracle_segment(const void *vol, int dtype_bytes, int64_t nx, int64_t ny,
+                   int64_t nz, int64_t z0, int64_t z1, int bins, int k, double q,
+                   int objective, int level, int nthreads, uint32_t *hist,
+                   int32_t *thresholds, double *phi, double *gap,
+                   int32_t *status, uint8_t *labels) {
+  (void)nz;
+  int64_t n = nx * ny;
+  if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+  for (int64_t z = z0; z < z1; z++) {
+    const unsigned char *slice = (const unsigned char *)vol + (size_t)z * n * dtype_bytes;
+    uint32_t *h = hist + (size_t)z * bins;
+    int st = oracle_histogram(slice, dtype_bytes, n, bins, h);
+    oracle_result r;
+    memset(&r, 0, sizeof(r));
+    for (int j = 0; j < OR_KMAX; j++) r.t[j] = -1;
+    r.phi = NAN;
+    r.gap = NAN;
+    if (st == OR_OK) st = oracle_search(h, bins, k, q, objective, level, &r);
+    status[z] = st;
+    for (int j = 0; j < k; j++) thresholds[z * k + j] = st == OR_OK ? r.t[j] : -1;
+    phi[z] = st == OR_OK ? r.phi : NAN;
+    gap[z] = st == OR_OK ? r.gap : NAN;
+    if (labels) {
+      uint8_t *lab = labels + (size_t)z * n;
+      if (st == OR_OK)
+        oracle_label(slice, dtype_bytes, n, k, r.t, lab);
+      else
+        memset(lab, 0, (size_t)n);
+    }
+  }
+  return OR_OK;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,181 @@
+/*
+ * tsa.h -- C ABI of libtsa: B200-native (sm_100a) Tsallis-entropy multilevel
+ * thresholding of CT slices, the data-parallel hot path of arXiv 2012.10684
+ * ("GPU acceleration of patient-specific airway image segmentation").
+ *
+ * Problem statement (PAPER.md v2; line numbers of /root/reference/PAPER.md):
+ *   image in -> threshold selected by maximising Tsallis entropy -> Algorithm 1
+ *   applied, generalised per slice to
+ *   k thresholds of the 1-D gray-level histogram (BASELINE.json:north_star):
+ *     c_i   = #{voxels of slice z with value i}, i < bins
+ *     p_i   = c_i / N
+ *     class C_0 = [0,t_1], C_j = [t_j+1, t_{j+1}], C_k = [t_k+1, bins-1]
+ *     A_j   = sum_{i in C_j} (p_i / P_j)^q,  S_j = (1 - A_j)/(q - 1)
+ *             (q == 1: S_j = -sum (p_i/P_j) ln(p_i/P_j))
+ *     phi   = S_0 (+) S_1 (+) ... (+) S_k,  x (+) y = x + y + (1-q) x y
+ *             (TSA_OBJ_SUM_PLUS_PRODUCT: sum S_j + (1-q) prod S_j)
+ *     t*    = argmax phi over 0 <= t_1 < ... < t_k <= bins-2, every class
+ *             non-empty, lowest tuple on exact ties
+ *     label = #{ j : v > t*_j }  (Algorithm 1 with T = t+1 for k = 1)
+ *   The readings behind these lines are DESIGN.md R1-R17.
+ *
+ * Conventions for every entry point:
+ *   - Every data pointer is a DEVICE pointer on the current CUDA device unless
+ *     its comment says "host".  Layouts are C-contiguous.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are asynchronous on that stream: they validate arguments on the
+ *     host, enqueue kernels and return; they never synchronise, never allocate
+ *     or free device memory and keep no global mutable state, so a whole
+ *     tsa_segment call can be captured in a CUDA graph.
+ *   - The caller owns every buffer, including the workspace (size from the
+ *     matching *_workspace_size call, 256-byte aligned).
+ *   - Argument errors return TSA_ERR_INVALID_ARG before anything is enqueued.
+ *     Data-dependent errors are reported per slice in slice_status (the call
+ *     itself returns TSA_OK): TSA_ERR_LEVEL_OVERFLOW when any voxel >= bins
+ *     (never clamped), TSA_ERR_NO_VALID_SPLIT when fewer than k+1 bins are
+ *     non-empty.  A failed slice gets thresholds -1, objective NaN, labels 0.
+ *   - CUDA launch failures return TSA_ERR_CUDA; tsa_last_error() gives detail
+ *     (thread-local).
+ */
+#ifndef TSA_H
+#define TSA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSA_VERSION 1
+#define TSA_KMAX 4
+#define TSA_BINS_MAX 4096
+#define TSA_KEY_NONE 0xFFFFFFFFFFFFFFFFull /* partial key of "no valid tuple" */
+
+typedef enum {
+  TSA_OK = 0,
+  TSA_ERR_INVALID_ARG = 1,
+  TSA_ERR_LEVEL_OVERFLOW = 2,
+  TSA_ERR_NO_VALID_SPLIT = 3,
+  TSA_ERR_WORKSPACE = 4,
+  TSA_ERR_CUDA = 5,
+  TSA_ERR_NCCL = 6
+} tsa_status;
+
+typedef enum { TSA_U8 = 1, TSA_U16 = 2 } tsa_dtype;
+
+/* R1: the k >= 2 objective.  PSEUDO_ADDITIVE is the paper's two-class rule
+ * folded over k+1 classes (default); SUM_PLUS_PRODUCT is the multilevel
+ * literature's alternative. */
+typedef enum { TSA_OBJ_PSEUDO_ADDITIVE = 0, TSA_OBJ_SUM_PLUS_PRODUCT = 1 } tsa_objective;
+
+/* Which tuples the exhaustive search evaluates.  FULL: every t_1<...<t_k in
+ * [0, bins-2] (C(bins-1,k) tuples, invalid ones skipped).  CANONICAL: only
+ * tuples whose every t_j is a non-empty bin (C(m-1,k) tuples, m = non-empty
+ * bins).  Both return the same (bit-identical) t* and score: tuples that
+ * differ only by empty bins describe the same partition, evaluate to the same
+ * value bit for bit, and the lowest of them is the canonical one. */
+typedef enum { TSA_ENUM_CANONICAL = 0, TSA_ENUM_FULL = 1 } tsa_enumeration;
+
+typedef struct {
+  const void *volume;   /* [nz][ny][nx] u8 or u16, device */
+  int32_t dtype;        /* tsa_dtype */
+  int64_t nx, ny, nz;   /* > 0; nx*ny < 2^31 */
+  int32_t bins;         /* L: 2..256 for u8, 2..4096 for u16 */
+  int32_t k;            /* thresholds per slice, 1..4, k <= bins-1 */
+  double q;             /* entropic index q (alpha), > 0 and finite; q == 1 is Shannon */
+  int32_t objective;    /* tsa_objective */
+  int32_t enumeration;  /* tsa_enumeration */
+  int32_t units_per_slice; /* search work units per slice (0 = library heuristic) */
+} tsa_problem;
+
+typedef struct {
+  int32_t *thresholds;   /* [nz][k], required; t_1<...<t_k in [0,bins-2]; -1 on slice error */
+  uint8_t *labels;       /* [nz][ny][nx] or NULL = skip labelling */
+  double *objective;     /* [nz] or NULL; phi(t*) recomputed in the definition's order; NaN on error */
+  uint32_t *histogram;   /* [nz][bins] or NULL (then kept in the workspace) */
+  int32_t *slice_status; /* [nz] or NULL; tsa_status per slice */
+} tsa_outputs;
+
+/* Validate a problem (host only, no CUDA calls).  TSA_OK or TSA_ERR_INVALID_ARG. */
+tsa_status tsa_validate(const tsa_problem *p);
+
+/* Bytes of workspace tsa_segment needs for this problem (0 if invalid). */
+size_t tsa_workspace_size(const tsa_problem *p);
+
+/* The whole hot path on one stream:
+ * histogram -> tables (prefix scans) -> exhaustive search -> argmax/finalize
+ * -> labels. */
+tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *workspace,
+                       size_t workspace_bytes, void *stream);
+
+/* ---- stage calls (parity tests, ncu, tuple sharding) ------------------- */
+
+/* a1: hist[z][i] = #{v == i} over the slice's in-range voxels; slice_status[z]
+ * = TSA_OK or TSA_ERR_LEVEL_OVERFLOW.  Both outputs are fully overwritten. */
+tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_status,
+                         void *stream);
+
+/* Workspace for tsa_search of nz slices of bins bins (same for every unit range). */
+size_t tsa_search_workspace_size(int64_t nz, int64_t voxels_per_slice, int32_t bins, int32_t k,
+                                 double q, int32_t objective, int32_t enumeration);
+
+/* Units per slice the library would pick for this shape (what units_per_slice=0 means). */
+int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration);
+
+/* a2+a3: prefix-scan tables and the exhaustive search over work units
+ * [unit_begin, unit_end) of units_per_slice units per slice.  Unit u of slice z
+ * covers a fixed, rank-independent range of the slice's tuples, so disjoint
+ * unit ranges on different GPUs partition the tuple space.
+ *   hist            [nz][bins] (from tsa_histogram)
+ *   slice_status    [nz] in/out: slices not TSA_OK are skipped; TSA_ERR_NO_VALID_SPLIT
+ *                   is set when fewer than k+1 bins are non-empty
+ *   part_score      [unit_end-unit_begin][nz] f64 out: best score per unit (score = phi-
+ *                   monotone comparison quantity, higher is better; -inf if none)
+ *   part_key        [unit_end-unit_begin][nz] u64 out: packed tuple of that score:
+ *                   sum_j t_j << 12*(k-1-j) (integer order == lexicographic order);
+ *                   TSA_KEY_NONE if none. */
+tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz,
+                      int64_t voxels_per_slice, int32_t bins, int32_t k, double q,
+                      int32_t objective, int32_t enumeration, int32_t units_per_slice,
+                      int32_t unit_begin, int32_t unit_end, double *part_score,
+                      uint64_t *part_key, void *workspace, size_t workspace_bytes,
+                      void *stream);
+
+/* a4 (partial): merge nparts [nparts][nz] partials into [nz] under the total
+ * order (score desc, key asc).  Used before a cross-rank exchange. */
+tsa_status tsa_merge(const double *part_score, const uint64_t *part_key, int32_t nparts,
+                     int64_t nz, double *score, uint64_t *key, void *stream);
+
+/* a4: merge partials, decode t*, recompute phi(t*) from the histogram in the
+ * definition's order, write out->thresholds / objective / slice_status
+ * (out->labels and out->histogram are ignored). */
+tsa_status tsa_finalize(const uint32_t *hist, const int32_t *slice_status, int64_t nz,
+                        int32_t bins, int32_t k, double q, int32_t objective,
+                        const double *part_score, const uint64_t *part_key, int32_t nparts,
+                        const tsa_outputs *out, void *stream);
+
+/* a5: labels[z][y][x] = #{j : v > thresholds[z][j]}; 0 for slices whose
+ * slice_status (may be NULL = all OK) is not TSA_OK. */
+tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds,
+                     const int32_t *slice_status, uint8_t *labels, void *stream);
+
+/* Host-buffer convenience: copies a HOST volume (pinned recommended) to the
+ * device in slabs, runs tsa_segment per slab and copies thresholds, objective,
+ * status and (if labels_host != NULL) labels back, overlapping copies with
+ * compute on two streams.  Device scratch (dev_buf, dev_bytes) comes from the
+ * caller: tsa_segment_host_scratch_size() bytes.  Blocks until done. */
+size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab_slices);
+tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slices,
+                            int32_t *thresholds_host, double *objective_host,
+                            int32_t *status_host, uint8_t *labels_host, void *dev_buf,
+                            size_t dev_bytes, void *stream0, void *stream1);
+
+const char *tsa_status_string(tsa_status s);
+const char *tsa_last_error(void);
+int32_t tsa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSA_H */

@@ -1,0 +1,330 @@
+"""B200-native Tsallis multilevel thresholding (arXiv 2012.10684 hot path).
+
+Thin Python binding over ``libtsa.so`` (C ABI in ``include/tsa.h``): argument
+marshalling only -- every step of the path runs in the library's sm_100a CUDA
+kernels.  PyTorch supplies device memory (tensors), streams
+(``torch.cuda.current_stream()``) and, for multi-GPU runs, process groups.
+There is no CPU fallback: importing works anywhere (so the ABI can be checked
+on a CPU host) but every compute call requires CUDA tensors and the built
+library, and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsa.so")
+
+TSA_OK, TSA_ERR_INVALID_ARG, TSA_ERR_LEVEL_OVERFLOW, TSA_ERR_NO_VALID_SPLIT = 0, 1, 2, 3
+TSA_ERR_WORKSPACE, TSA_ERR_CUDA, TSA_ERR_NCCL = 4, 5, 6
+TSA_U8, TSA_U16 = 1, 2
+TSA_OBJ_PSEUDO_ADDITIVE, TSA_OBJ_SUM_PLUS_PRODUCT = 0, 1
+TSA_ENUM_CANONICAL, TSA_ENUM_FULL = 0, 1
+TSA_KEY_NONE = 0xFFFFFFFFFFFFFFFF
+KMAX = 4
+
+OBJECTIVES = {"pseudo_additive": 0, "sum_plus_product": 1}
+ENUMERATIONS = {"canonical": 0, "full": 1}
+
+# every symbol include/tsa.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "tsa_validate", "tsa_workspace_size", "tsa_segment", "tsa_histogram",
+    "tsa_search_workspace_size", "tsa_default_units", "tsa_search", "tsa_merge",
+    "tsa_finalize", "tsa_label", "tsa_segment_host_scratch_size", "tsa_segment_host",
+    "tsa_status_string", "tsa_last_error", "tsa_version",
+)
+
+
+class TsaError(RuntimeError):
+    def __init__(self, status, where, detail=""):
+        super().__init__(f"{where}: status {status} ({_status_name(status)}) {detail}")
+        self.status = status
+
+
+def _status_name(s):
+    names = {0: "TSA_OK", 1: "TSA_ERR_INVALID_ARG", 2: "TSA_ERR_LEVEL_OVERFLOW",
+             3: "TSA_ERR_NO_VALID_SPLIT", 4: "TSA_ERR_WORKSPACE", 5: "TSA_ERR_CUDA",
+             6: "TSA_ERR_NCCL"}
+    return names.get(int(s), "?")
+
+
+class tsa_problem(ctypes.Structure):
+    _fields_ = [
+        ("volume", ctypes.c_void_p),
+        ("dtype", ctypes.c_int32),
+        ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+        ("bins", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("q", ctypes.c_double),
+        ("objective", ctypes.c_int32),
+        ("enumeration", ctypes.c_int32),
+        ("units_per_slice", ctypes.c_int32),
+    ]
+
+
+class tsa_outputs(ctypes.Structure):
+    _fields_ = [
+        ("thresholds", ctypes.c_void_p),
+        ("labels", ctypes.c_void_p),
+        ("objective", ctypes.c_void_p),
+        ("histogram", ctypes.c_void_p),
+        ("slice_status", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load libtsa.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, D, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+    PP = ctypes.POINTER(tsa_problem)
+    PO = ctypes.POINTER(tsa_outputs)
+    sig = {
+        "tsa_validate": (I32, [PP]),
+        "tsa_workspace_size": (SZ, [PP]),
+        "tsa_segment": (I32, [PP, PO, P, SZ, P]),
+        "tsa_histogram": (I32, [PP, P, P, P]),
+        "tsa_search_workspace_size": (SZ, [I64, I64, I32, I32, D, I32, I32]),
+        "tsa_default_units": (I32, [I64, I32, I32, I32]),
+        "tsa_search": (I32, [P, P, I64, I64, I32, I32, D, I32, I32, I32, I32, I32, P, P, P, SZ, P]),
+        "tsa_merge": (I32, [P, P, I32, I64, P, P, P]),
+        "tsa_finalize": (I32, [P, P, I64, I32, I32, D, I32, P, P, I32, PO, P]),
+        "tsa_label": (I32, [PP, P, P, P, P]),
+        "tsa_segment_host_scratch_size": (SZ, [PP, I64]),
+        "tsa_segment_host": (I32, [PP, I64, P, P, P, P, P, SZ, P, P]),
+        "tsa_status_string": (ctypes.c_char_p, [I32]),
+        "tsa_last_error": (ctypes.c_char_p, []),
+        "tsa_version": (I32, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status, where):
+    if status != TSA_OK:
+        detail = load().tsa_last_error().decode(errors="replace")
+        raise TsaError(status, where, detail)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libtsa needs CUDA tensors (no CPU fallback)")
+
+
+def _dtype_code(vol):
+    if vol.dtype == torch.uint8:
+        return TSA_U8
+    if vol.dtype == torch.uint16:
+        return TSA_U16
+    raise ValueError(f"volume dtype must be uint8 or uint16, got {vol.dtype}")
+
+
+def make_problem(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0):
+    if vol.dim() != 3 or not vol.is_contiguous():
+        raise ValueError("volume must be a contiguous [nz][ny][nx] tensor")
+    nz, ny, nx = vol.shape
+    return tsa_problem(vol.data_ptr(), _dtype_code(vol), nx, ny, nz, bins, k, float(q),
+                       OBJECTIVES.get(objective, objective), ENUMERATIONS.get(enumeration, enumeration),
+                       units)
+
+
+def tsa_version():
+    return int(load().tsa_version())
+
+
+def tsa_validate(problem):
+    return int(load().tsa_validate(ctypes.byref(problem)))
+
+
+def tsa_workspace_size(problem):
+    return int(load().tsa_workspace_size(ctypes.byref(problem)))
+
+
+def tsa_default_units(nz, bins, k, enumeration="canonical"):
+    return int(load().tsa_default_units(nz, bins, k, ENUMERATIONS.get(enumeration, enumeration)))
+
+
+def tsa_search_workspace_size(nz, voxels_per_slice, bins, k, q, objective="pseudo_additive",
+                              enumeration="canonical"):
+    return int(load().tsa_search_workspace_size(nz, voxels_per_slice, bins, k, float(q),
+                                                OBJECTIVES.get(objective, objective),
+                                                ENUMERATIONS.get(enumeration, enumeration)))
+
+
+def workspace_for(problem, device):
+    n = tsa_workspace_size(problem)
+    if n == 0:
+        _check(load().tsa_validate(ctypes.byref(problem)), "tsa_workspace_size")
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def tsa_segment(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0,
+                labels=True, out=None, workspace=None, stream=None):
+    """Whole path on the current stream.  Returns dict of device tensors:
+    thresholds [nz,k] i32, objective [nz] f64, histogram [nz,bins] u32,
+    status [nz] i32, labels [nz,ny,nx] u8 (or None)."""
+    _need_cuda(vol)
+    lib = load()
+    p = make_problem(vol, bins, k, q, objective, enumeration, units)
+    nz = vol.shape[0]
+    dev = vol.device
+    if out is None:
+        out = {
+            "thresholds": torch.empty((nz, k), dtype=torch.int32, device=dev),
+            "objective": torch.empty(nz, dtype=torch.float64, device=dev),
+            "histogram": torch.empty((nz, bins), dtype=torch.int32, device=dev),
+            "status": torch.empty(nz, dtype=torch.int32, device=dev),
+            "labels": torch.empty(vol.shape, dtype=torch.uint8, device=dev) if labels else None,
+        }
+    o = tsa_outputs(out["thresholds"].data_ptr(),
+                    out["labels"].data_ptr() if out.get("labels") is not None else None,
+                    out["objective"].data_ptr() if out.get("objective") is not None else None,
+                    out["histogram"].data_ptr() if out.get("histogram") is not None else None,
+                    out["status"].data_ptr() if out.get("status") is not None else None)
+    if workspace is None:
+        workspace = workspace_for(p, dev)
+    _check(lib.tsa_segment(ctypes.byref(p), ctypes.byref(o), _ptr(workspace), workspace.numel(),
+                           _stream(stream)), "tsa_segment")
+    return out
+
+
+def tsa_histogram(vol, bins, stream=None):
+    _need_cuda(vol)
+    p = make_problem(vol, bins, 1, 1.0)
+    nz = vol.shape[0]
+    hist = torch.empty((nz, bins), dtype=torch.int32, device=vol.device)
+    status = torch.empty(nz, dtype=torch.int32, device=vol.device)
+    _check(load().tsa_histogram(ctypes.byref(p), _ptr(hist), _ptr(status), _stream(stream)),
+           "tsa_histogram")
+    return hist, status
+
+
+def tsa_search(hist, status, voxels_per_slice, k, q, objective="pseudo_additive",
+               enumeration="canonical", units=0, unit_begin=0, unit_end=None, workspace=None,
+               stream=None):
+    """Returns (part_score [n_units, nz] f64, part_key [n_units, nz] i64 (u64 bits)).
+    `status` is updated in place (NO_VALID_SPLIT)."""
+    _need_cuda(hist, status)
+    nz, bins = hist.shape
+    obj = OBJECTIVES.get(objective, objective)
+    enum = ENUMERATIONS.get(enumeration, enumeration)
+    if units <= 0:
+        units = tsa_default_units(nz, bins, k, enum)
+    unit_end = units if unit_end is None else unit_end
+    nu = unit_end - unit_begin
+    ps = torch.empty((max(nu, 1), nz), dtype=torch.float64, device=hist.device)
+    pk = torch.empty((max(nu, 1), nz), dtype=torch.int64, device=hist.device)
+    if workspace is None:
+        n = tsa_search_workspace_size(nz, voxels_per_slice, bins, k, q, obj, enum)
+        workspace = torch.empty(max(n, 1), dtype=torch.uint8, device=hist.device)
+    _check(load().tsa_search(_ptr(hist), _ptr(status), nz, voxels_per_slice, bins, k, float(q), obj,
+                             enum, units, unit_begin, unit_end, _ptr(ps), _ptr(pk),
+                             _ptr(workspace), workspace.numel(), _stream(stream)), "tsa_search")
+    return ps, pk
+
+
+def tsa_merge(part_score, part_key, stream=None):
+    _need_cuda(part_score, part_key)
+    nparts, nz = part_score.shape
+    s = torch.empty(nz, dtype=torch.float64, device=part_score.device)
+    k = torch.empty(nz, dtype=torch.int64, device=part_score.device)
+    _check(load().tsa_merge(_ptr(part_score), _ptr(part_key), nparts, nz, _ptr(s), _ptr(k),
+                            _stream(stream)), "tsa_merge")
+    return s, k
+
+
+def tsa_finalize(hist, status, k, q, part_score, part_key, objective="pseudo_additive", stream=None):
+    _need_cuda(hist, status, part_score, part_key)
+    nz, bins = hist.shape
+    nparts = part_score.shape[0]
+    dev = hist.device
+    thr = torch.empty((nz, k), dtype=torch.int32, device=dev)
+    phi = torch.empty(nz, dtype=torch.float64, device=dev)
+    st = torch.empty(nz, dtype=torch.int32, device=dev)
+    o = tsa_outputs(thr.data_ptr(), None, phi.data_ptr(), None, st.data_ptr())
+    _check(load().tsa_finalize(_ptr(hist), _ptr(status), nz, bins, k, float(q),
+                               OBJECTIVES.get(objective, objective), _ptr(part_score),
+                               _ptr(part_key), nparts, ctypes.byref(o), _stream(stream)),
+           "tsa_finalize")
+    return thr, phi, st
+
+
+def tsa_label(vol, thresholds, status=None, bins=None, stream=None):
+    _need_cuda(vol, thresholds, status)
+    k = thresholds.shape[1]
+    bins = bins or (256 if vol.dtype == torch.uint8 else 4096)
+    p = make_problem(vol, bins, k, 1.0)
+    labels = torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
+    _check(load().tsa_label(ctypes.byref(p), _ptr(thresholds), _ptr(status), _ptr(labels),
+                            _stream(stream)), "tsa_label")
+    return labels
+
+
+def tsa_segment_host(vol_host, bins, k, q, objective="pseudo_additive", enumeration="canonical",
+                     units=0, slab=None, labels=True, scratch=None, streams=None, out=None,
+                     device=None):
+    """Host-buffer path: vol_host is a CPU (ideally pinned) torch tensor; copies
+    in/out run inside the library, overlapped with compute on two streams.
+    Returns dict of CPU tensors.  Blocks until done."""
+    if vol_host.is_cuda:
+        raise ValueError("tsa_segment_host takes a host tensor")
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    lib = load()
+    p = make_problem(vol_host, bins, k, q, objective, enumeration, units)
+    nz = vol_host.shape[0]
+    slab = slab or max(1, min(nz, 32))
+    if out is None:
+        pin = vol_host.is_pinned()
+        out = {
+            "thresholds": torch.empty((nz, k), dtype=torch.int32, pin_memory=pin),
+            "objective": torch.empty(nz, dtype=torch.float64, pin_memory=pin),
+            "status": torch.empty(nz, dtype=torch.int32, pin_memory=pin),
+            "labels": torch.empty(vol_host.shape, dtype=torch.uint8, pin_memory=pin) if labels else None,
+        }
+    if scratch is None:
+        n = int(lib.tsa_segment_host_scratch_size(ctypes.byref(p), slab))
+        scratch = torch.empty(max(n, 1), dtype=torch.uint8, device=device)
+    if streams is None:
+        streams = (torch.cuda.current_stream(device), torch.cuda.Stream(device))
+    lab = out.get("labels")
+    _check(lib.tsa_segment_host(ctypes.byref(p), slab, _ptr(out["thresholds"]), _ptr(out["objective"]),
+                                _ptr(out["status"]), _ptr(lab) if lab is not None else None,
+                                _ptr(scratch), scratch.numel(),
+                                ctypes.c_void_p(streams[0].cuda_stream),
+                                ctypes.c_void_p(streams[1].cuda_stream)), "tsa_segment_host")
+    return out
+
+
+def unpack_key(key, k):
+    """Packed u64 key (as python int) -> tuple of k thresholds."""
+    key &= 0xFFFFFFFFFFFFFFFF
+    return tuple((key >> (12 * (k - 1 - j))) & 0xFFF for j in range(k))

@@ -1,0 +1,557 @@
+// tsa_api.cu -- host side of libtsa: argument validation, workspace carving and
+// launch sequencing behind the C ABI declared in include/tsa.h.  Never
+// allocates device memory, never synchronises the caller's stream (except the
+// documented blocking tsa_segment_host), keeps no global mutable state other
+// than the thread-local error string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tsa.h"
+#include "tsa_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tsa_status set_error(tsa_status s, const char *msg) {
+  g_last_error = msg;
+  return s;
+}
+
+tsa_status check_cuda(const char *where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+    return set_error(TSA_ERR_CUDA, buf);
+  }
+  return TSA_OK;
+}
+
+#define TSA_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      char _b[512];                                                           \
+      snprintf(_b, sizeof(_b), "%s: %s", #call, cudaGetErrorString(_e));      \
+      return set_error(TSA_ERR_CUDA, _b);                                     \
+    }                                                                         \
+  } while (0)
+
+#define TSA_TRY(expr)               \
+  do {                              \
+    tsa_status _s = (expr);         \
+    if (_s != TSA_OK) return _s;    \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// bump allocator over a caller-provided workspace (sizes only when base == null)
+struct Carve {
+  char *base;
+  size_t off = 0;
+  template <typename T>
+  T *take(size_t count) {
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+double binom_d(double n, int r) {
+  double v = 1.0;
+  for (int i = 0; i < r; i++) v = v * (n - i) / (i + 1);
+  return v;
+}
+
+bool valid_search_shape(int64_t nz, int64_t N, int32_t bins, int32_t k, double q,
+                        int32_t objective, int32_t enumeration) {
+  if (nz <= 0 || N <= 0 || N >= (int64_t(1) << 31)) return false;
+  if (bins < 2 || bins > TSA_BINS_MAX) return false;
+  if (k < 1 || k > TSA_KMAX || k > bins - 1) return false;
+  if (!(q > 0.0) || !std::isfinite(q)) return false;
+  if (objective != TSA_OBJ_PSEUDO_ADDITIVE && objective != TSA_OBJ_SUM_PLUS_PRODUCT) return false;
+  if (enumeration != TSA_ENUM_CANONICAL && enumeration != TSA_ENUM_FULL) return false;
+  if (binom_d((double)bins - 1, k) >= 9.2e18) return false;
+  return true;
+}
+
+int search_mode(double q, int32_t objective) {
+  if (objective == TSA_OBJ_SUM_PLUS_PRODUCT) return tsa::SPP;
+  if (q == 1.0) return tsa::SUM;
+  return q < 1.0 ? tsa::PROD_MAX : tsa::PROD_MIN;
+}
+
+bool use_rtable(int32_t bins, int32_t k, int32_t objective) {
+  return objective == TSA_OBJ_PSEUDO_ADDITIVE && k >= 3 && bins <= 512;
+}
+
+struct SearchWs {
+  double *ipow = nullptr, *lnn = nullptr, *rcp = nullptr;
+  uint32_t *cC = nullptr, *fC = nullptr;
+  double *cWhi = nullptr, *cWlo = nullptr, *fWhi = nullptr, *fWlo = nullptr;
+  int32_t *cBin = nullptr, *fBin = nullptr;
+  double *Asuf = nullptr, *R = nullptr;
+  int32_t *M = nullptr;
+};
+
+size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, int32_t k,
+                    double q, int32_t objective, int32_t enumeration) {
+  const size_t E = (size_t)bins + 1;
+  const bool shannon = q == 1.0;
+  if (shannon) {
+    w.lnn = c.take<double>((size_t)N + 1);
+    w.rcp = c.take<double>((size_t)N + 1);
+  } else {
+    w.ipow = c.take<double>((size_t)N + 1);
+  }
+  w.cC = c.take<uint32_t>(nz * E);
+  w.cWhi = c.take<double>(nz * E);
+  w.cWlo = c.take<double>(nz * E);
+  w.cBin = c.take<int32_t>(nz * E);
+  if (enumeration == TSA_ENUM_FULL) {
+    w.fC = c.take<uint32_t>(nz * E);
+    w.fWhi = c.take<double>(nz * E);
+    w.fWlo = c.take<double>(nz * E);
+    w.fBin = c.take<int32_t>(nz * E);
+  }
+  w.Asuf = c.take<double>(nz * (size_t)bins);
+  w.M = c.take<int32_t>(nz);
+  if (use_rtable(bins, k, objective)) w.R = c.take<double>(nz * (size_t)bins * bins);
+  return c.off;
+}
+
+template <int K, int MODE>
+void launch_search_k(const tsa::SearchArgs &a, dim3 grid, cudaStream_t s, bool rt) {
+  if (rt)
+    tsa::k_search<K, MODE, true><<<grid, 256, 0, s>>>(a);
+  else
+    tsa::k_search<K, MODE, false><<<grid, 256, 0, s>>>(a);
+}
+
+template <int MODE>
+void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t s, bool rt) {
+  switch (k) {
+    case 1: launch_search_k<1, MODE>(a, grid, s, false); break;
+    case 2: launch_search_k<2, MODE>(a, grid, s, false); break;
+    case 3: launch_search_k<3, MODE>(a, grid, s, rt); break;
+    default: launch_search_k<4, MODE>(a, grid, s, rt); break;
+  }
+}
+
+template <int MODE>
+void launch_scan(const tsa::ScanArgs &a, cudaStream_t s) {
+  const int warps = 4;
+  const unsigned blocks = (unsigned)((a.nz + warps - 1) / warps);
+  tsa::k_scan<MODE><<<blocks, 32 * warps, 0, s>>>(a);
+}
+
+template <int MODE>
+void launch_rtable(const SearchWs &w, const uint32_t *C, const double *Whi, const double *Wlo,
+                   const int32_t *status, int64_t nz, int E, int L, const tsa::Luts &l,
+                   cudaStream_t s) {
+  dim3 grid((unsigned)L, (unsigned)nz);
+  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, E, L, l);
+}
+
+int g_num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t tsa_version(void) { return TSA_VERSION; }
+
+const char *tsa_last_error(void) { return g_last_error.c_str(); }
+
+const char *tsa_status_string(tsa_status s) {
+  switch (s) {
+    case TSA_OK: return "TSA_OK";
+    case TSA_ERR_INVALID_ARG: return "TSA_ERR_INVALID_ARG";
+    case TSA_ERR_LEVEL_OVERFLOW: return "TSA_ERR_LEVEL_OVERFLOW";
+    case TSA_ERR_NO_VALID_SPLIT: return "TSA_ERR_NO_VALID_SPLIT";
+    case TSA_ERR_WORKSPACE: return "TSA_ERR_WORKSPACE";
+    case TSA_ERR_CUDA: return "TSA_ERR_CUDA";
+    case TSA_ERR_NCCL: return "TSA_ERR_NCCL";
+  }
+  return "TSA_ERR_UNKNOWN";
+}
+
+tsa_status tsa_validate(const tsa_problem *p) {
+  if (!p) return set_error(TSA_ERR_INVALID_ARG, "problem is NULL");
+  if (!p->volume) return set_error(TSA_ERR_INVALID_ARG, "volume is NULL");
+  if (p->dtype != TSA_U8 && p->dtype != TSA_U16) return set_error(TSA_ERR_INVALID_ARG, "dtype");
+  if (p->nx <= 0 || p->ny <= 0 || p->nz <= 0) return set_error(TSA_ERR_INVALID_ARG, "dims must be > 0");
+  if (p->nx * p->ny >= (int64_t(1) << 31)) return set_error(TSA_ERR_INVALID_ARG, "slice too large");
+  if (p->dtype == TSA_U8 && p->bins > 256) return set_error(TSA_ERR_INVALID_ARG, "bins > 256 with u8");
+  if (p->units_per_slice < 0 || p->units_per_slice > 65535)
+    return set_error(TSA_ERR_INVALID_ARG, "units_per_slice");
+  if (!valid_search_shape(p->nz, p->nx * p->ny, p->bins, p->k, p->q, p->objective, p->enumeration))
+    return set_error(TSA_ERR_INVALID_ARG, "bins/k/q/objective/enumeration out of range");
+  return TSA_OK;
+}
+
+int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
+  if (nz <= 0) return 1;
+  const double target = (double)g_num_sms() * (k >= 3 ? 8.0 : 2.0);
+  double rows = binom_d((double)bins - 1, k - 1);
+  if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
+  double u = std::ceil(target / (double)nz);
+  u = std::min(u, std::max(1.0, rows / 64.0));
+  return (int32_t)std::max(1.0, std::min(u, 256.0));
+}
+
+size_t tsa_search_workspace_size(int64_t nz, int64_t N, int32_t bins, int32_t k, double q,
+                                 int32_t objective, int32_t enumeration) {
+  if (!valid_search_shape(nz, N, bins, k, q, objective, enumeration)) return 0;
+  Carve c{nullptr};
+  SearchWs w;
+  return carve_search(c, w, nz, N, bins, k, q, objective, enumeration);
+}
+
+static int32_t units_of(const tsa_problem *p) {
+  return p->units_per_slice > 0 ? p->units_per_slice
+                                : tsa_default_units(p->nz, p->bins, p->k, p->enumeration);
+}
+
+struct SegWs {
+  uint32_t *hist;
+  int32_t *status;
+  double *ps;
+  uint64_t *pk;
+  char *search;
+  size_t search_bytes;
+};
+
+static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
+  Carve c{base};
+  const int32_t U = units_of(p);
+  uint32_t *hist = c.take<uint32_t>((size_t)p->nz * p->bins);
+  int32_t *status = c.take<int32_t>((size_t)p->nz);
+  double *ps = c.take<double>((size_t)U * p->nz);
+  uint64_t *pk = c.take<uint64_t>((size_t)U * p->nz);
+  const size_t sb = tsa_search_workspace_size(p->nz, p->nx * p->ny, p->bins, p->k, p->q,
+                                              p->objective, p->enumeration);
+  char *search = c.take<char>(sb);
+  if (o) *o = SegWs{hist, status, ps, pk, search, sb};
+  return c.off;
+}
+
+size_t tsa_workspace_size(const tsa_problem *p) {
+  if (tsa_validate(p) != TSA_OK) return 0;
+  return carve_segment(p, nullptr, nullptr);
+}
+
+tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_status, void *stream) {
+  TSA_TRY(tsa_validate(p));
+  if (!hist || !slice_status) return set_error(TSA_ERR_INVALID_ARG, "hist/slice_status NULL");
+  cudaStream_t s = S(stream);
+  TSA_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * p->nz * p->bins, s));
+  TSA_CUDA(cudaMemsetAsync(slice_status, 0, sizeof(int32_t) * p->nz, s));
+  tsa::HistArgs a;
+  a.vol = reinterpret_cast<const uint8_t *>(p->volume);
+  a.hist = hist;
+  a.status = slice_status;
+  a.n = p->nx * p->ny;
+  a.L = p->bins;
+  const int threads = 512;
+  // privatised copies: one per warp for small L, fewer for large L (<= 64 KB)
+  int reps = std::max(1, std::min(threads / 32, (int)(65536 / (4 * p->bins))));
+  a.replicas = reps;
+  const size_t smem = (size_t)reps * p->bins * 4;
+  const int64_t bytes_per_slice = a.n * (p->dtype == TSA_U8 ? 1 : 2);
+  // ~64 KB of input per CTA
+  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, bytes_per_slice / 65536));
+  a.chunks = chunks;
+  dim3 grid((unsigned)chunks, (unsigned)p->nz);
+  if (p->dtype == TSA_U8) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(tsa::k_histogram<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tsa::k_histogram<uint8_t><<<grid, threads, smem, s>>>(a);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(tsa::k_histogram<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tsa::k_histogram<uint16_t><<<grid, threads, smem, s>>>(a);
+  }
+  return check_cuda("k_histogram");
+}
+
+tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N,
+                      int32_t bins, int32_t k, double q, int32_t objective, int32_t enumeration,
+                      int32_t units, int32_t unit_begin, int32_t unit_end, double *part_score,
+                      uint64_t *part_key, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!valid_search_shape(nz, N, bins, k, q, objective, enumeration))
+    return set_error(TSA_ERR_INVALID_ARG, "search shape");
+  if (!hist || !slice_status || !part_score || !part_key || !workspace)
+    return set_error(TSA_ERR_INVALID_ARG, "NULL pointer");
+  if (units <= 0) units = tsa_default_units(nz, bins, k, enumeration);
+  if (unit_begin < 0 || unit_end > units || unit_begin >= unit_end)
+    return set_error(TSA_ERR_INVALID_ARG, "unit range");
+  Carve c{reinterpret_cast<char *>(workspace)};
+  SearchWs w;
+  const size_t need = carve_search(c, w, nz, N, bins, k, q, objective, enumeration);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "search workspace too small");
+  cudaStream_t s = S(stream);
+  const bool shannon = q == 1.0;
+  const int mode = search_mode(q, objective);
+  tsa::Luts l;
+  l.ipow = w.ipow;
+  l.lnn = w.lnn;
+  l.rcp = w.rcp;
+  l.iqm1 = shannon ? 0.0 : 1.0 / (q - 1.0);
+  l.omq = 1.0 - q;
+  l.shannon = shannon;
+  {
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((N + threads) / threads, 4 * g_num_sms());
+    tsa::k_luts<<<(unsigned)blocks, threads, 0, s>>>(w.ipow, w.lnn, w.rcp, N, q, shannon);
+    TSA_TRY(check_cuda("k_luts"));
+  }
+  const int E = bins + 1;
+  tsa::ScanArgs sa;
+  sa.hist = hist;
+  sa.status = slice_status;
+  sa.nz = nz;
+  sa.L = bins;
+  sa.E = E;
+  sa.k = k;
+  sa.q = q;
+  sa.shannon = shannon;
+  sa.full = enumeration == TSA_ENUM_FULL;
+  sa.cC = w.cC;
+  sa.cWhi = w.cWhi;
+  sa.cWlo = w.cWlo;
+  sa.cBin = w.cBin;
+  sa.fC = w.fC;
+  sa.fWhi = w.fWhi;
+  sa.fWlo = w.fWlo;
+  sa.fBin = w.fBin;
+  sa.Asuf = w.Asuf;
+  sa.M = w.M;
+  sa.luts = l;
+  sa.mode = mode;
+  switch (mode) {
+    case tsa::PROD_MAX: launch_scan<tsa::PROD_MAX>(sa, s); break;
+    case tsa::PROD_MIN: launch_scan<tsa::PROD_MIN>(sa, s); break;
+    case tsa::SUM: launch_scan<tsa::SUM>(sa, s); break;
+    default: launch_scan<tsa::SPP>(sa, s); break;
+  }
+  TSA_TRY(check_cuda("k_scan"));
+  const bool full = enumeration == TSA_ENUM_FULL;
+  const uint32_t *tC = full ? w.fC : w.cC;
+  const double *tWhi = full ? w.fWhi : w.cWhi;
+  const double *tWlo = full ? w.fWlo : w.cWlo;
+  const int32_t *tBin = full ? w.fBin : w.cBin;
+  const bool rt = w.R != nullptr;
+  if (rt) {
+    switch (mode) {
+      case tsa::PROD_MAX: launch_rtable<tsa::PROD_MAX>(w, tC, tWhi, tWlo, slice_status, nz, E, bins, l, s); break;
+      case tsa::PROD_MIN: launch_rtable<tsa::PROD_MIN>(w, tC, tWhi, tWlo, slice_status, nz, E, bins, l, s); break;
+      default: launch_rtable<tsa::SUM>(w, tC, tWhi, tWlo, slice_status, nz, E, bins, l, s); break;
+    }
+    TSA_TRY(check_cuda("k_rtable"));
+  }
+  tsa::SearchArgs a;
+  a.C = tC;
+  a.Whi = tWhi;
+  a.Wlo = tWlo;
+  a.Asuf = w.Asuf;
+  a.R = w.R;
+  a.Bin = tBin;
+  a.Mz = w.M;
+  a.status = slice_status;
+  a.part_score = part_score;
+  a.part_key = part_key;
+  a.luts = l;
+  a.nz = nz;
+  a.E = E;
+  a.L = bins;
+  a.units = units;
+  a.unit_begin = unit_begin;
+  dim3 grid((unsigned)(unit_end - unit_begin), (unsigned)nz);
+  switch (mode) {
+    case tsa::PROD_MAX: launch_search_mode<tsa::PROD_MAX>(k, a, grid, s, rt); break;
+    case tsa::PROD_MIN: launch_search_mode<tsa::PROD_MIN>(k, a, grid, s, rt); break;
+    case tsa::SUM: launch_search_mode<tsa::SUM>(k, a, grid, s, rt); break;
+    default: launch_search_mode<tsa::SPP>(k, a, grid, s, false); break;
+  }
+  return check_cuda("k_search");
+}
+
+tsa_status tsa_merge(const double *part_score, const uint64_t *part_key, int32_t nparts,
+                     int64_t nz, double *score, uint64_t *key, void *stream) {
+  if (!part_score || !part_key || !score || !key || nparts <= 0 || nz <= 0)
+    return set_error(TSA_ERR_INVALID_ARG, "merge args");
+  const int warps = 4;
+  tsa::k_merge<<<(unsigned)((nz + warps - 1) / warps), 32 * warps, 0, S(stream)>>>(
+      part_score, part_key, nparts, nz, score, key);
+  return check_cuda("k_merge");
+}
+
+static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, int64_t nz,
+                                int32_t bins, int32_t k, double q, int32_t objective,
+                                const double *ps, const uint64_t *pk, int32_t nparts,
+                                int32_t *thresholds, double *objective_out, int32_t *status_out,
+                                cudaStream_t s) {
+  tsa::FinalizeArgs f;
+  f.hist = hist;
+  f.status_in = status_in;
+  f.ps = ps;
+  f.pk = pk;
+  f.nparts = nparts;
+  f.nz = nz;
+  f.L = bins;
+  f.k = k;
+  f.objective = objective;
+  f.q = q;
+  f.thresholds = thresholds;
+  f.objective_out = objective_out;
+  f.status_out = status_out;
+  tsa::k_finalize<<<(unsigned)nz, 32, (size_t)bins * sizeof(double), s>>>(f);
+  return check_cuda("k_finalize");
+}
+
+tsa_status tsa_finalize(const uint32_t *hist, const int32_t *slice_status, int64_t nz,
+                        int32_t bins, int32_t k, double q, int32_t objective,
+                        const double *part_score, const uint64_t *part_key, int32_t nparts,
+                        const tsa_outputs *out, void *stream) {
+  if (!valid_search_shape(nz, 1, bins, k, q, objective, TSA_ENUM_CANONICAL))
+    return set_error(TSA_ERR_INVALID_ARG, "finalize shape");
+  if (!hist || !slice_status || !part_score || !part_key || nparts <= 0 || !out ||
+      !out->thresholds)
+    return set_error(TSA_ERR_INVALID_ARG, "finalize pointers");
+  return finalize_impl(hist, slice_status, nz, bins, k, q, objective, part_score, part_key,
+                       nparts, out->thresholds, out->objective, out->slice_status, S(stream));
+}
+
+tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
+                     uint8_t *labels, void *stream) {
+  TSA_TRY(tsa_validate(p));
+  if (!thresholds || !labels) return set_error(TSA_ERR_INVALID_ARG, "label pointers");
+  tsa::LabelArgs a;
+  a.vol = reinterpret_cast<const uint8_t *>(p->volume);
+  a.labels = labels;
+  a.thr = thresholds;
+  a.status = slice_status;
+  a.n = p->nx * p->ny;
+  a.k = p->k;
+  const int64_t bytes = a.n * (p->dtype == TSA_U8 ? 2 : 3);
+  a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, bytes / 65536));
+  dim3 grid((unsigned)a.chunks, (unsigned)p->nz);
+  if (p->dtype == TSA_U8)
+    tsa::k_label<uint8_t><<<grid, 256, 0, S(stream)>>>(a);
+  else
+    tsa::k_label<uint16_t><<<grid, 256, 0, S(stream)>>>(a);
+  return check_cuda("k_label");
+}
+
+tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *workspace,
+                       size_t workspace_bytes, void *stream) {
+  TSA_TRY(tsa_validate(p));
+  if (!out || !out->thresholds) return set_error(TSA_ERR_INVALID_ARG, "outputs->thresholds NULL");
+  if (!workspace) return set_error(TSA_ERR_INVALID_ARG, "workspace NULL");
+  SegWs w;
+  const size_t need = carve_segment(p, reinterpret_cast<char *>(workspace), &w);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = S(stream);
+  uint32_t *hist = out->histogram ? out->histogram : w.hist;
+  const int32_t U = units_of(p);
+  TSA_TRY(tsa_histogram(p, hist, w.status, stream));
+  TSA_TRY(tsa_search(hist, w.status, p->nz, p->nx * p->ny, p->bins, p->k, p->q, p->objective,
+                     p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, stream));
+  TSA_TRY(finalize_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
+                        out->thresholds, out->objective, w.status, s));
+  if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, stream));
+  if (out->slice_status)
+    TSA_CUDA(cudaMemcpyAsync(out->slice_status, w.status, sizeof(int32_t) * p->nz,
+                             cudaMemcpyDeviceToDevice, s));
+  return TSA_OK;
+}
+
+// ----------------------------------------------------------- host buffers
+static size_t slab_bytes(const tsa_problem *p, int64_t slab, tsa_problem *sp) {
+  *sp = *p;
+  sp->nz = slab;
+  sp->volume = reinterpret_cast<const void *>(uintptr_t(1));  // shape only
+  const size_t vb = (size_t)slab * p->nx * p->ny * (p->dtype == TSA_U8 ? 1 : 2);
+  const size_t lb = (size_t)slab * p->nx * p->ny;
+  Carve c{nullptr};
+  c.take<char>(vb);
+  c.take<char>(lb);
+  c.take<int32_t>((size_t)slab * p->k);
+  c.take<double>((size_t)slab);
+  c.take<int32_t>((size_t)slab);
+  c.take<char>(tsa_workspace_size(sp));
+  return c.off;
+}
+
+size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab) {
+  if (tsa_validate(p) != TSA_OK || slab <= 0) return 0;
+  slab = std::min(slab, p->nz);
+  tsa_problem sp;
+  return 2 * slab_bytes(p, slab, &sp);
+}
+
+tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, double *obj_h,
+                            int32_t *st_h, uint8_t *lab_h, void *dev_buf, size_t dev_bytes,
+                            void *stream0, void *stream1) {
+  TSA_TRY(tsa_validate(p));
+  if (slab <= 0 || !thr_h || !dev_buf) return set_error(TSA_ERR_INVALID_ARG, "host segment args");
+  slab = std::min(slab, p->nz);
+  tsa_problem sp;
+  const size_t per = slab_bytes(p, slab, &sp);
+  if (dev_bytes < 2 * per) return set_error(TSA_ERR_WORKSPACE, "device scratch too small");
+  const size_t esz = p->dtype == TSA_U8 ? 1 : 2;
+  const int64_t n = p->nx * p->ny;
+  cudaStream_t st[2] = {S(stream0), S(stream1)};
+  for (int64_t z0 = 0, i = 0; z0 < p->nz; z0 += slab, i++) {
+    const int64_t nzs = std::min(slab, p->nz - z0);
+    const int b = (int)(i & 1);
+    Carve c{reinterpret_cast<char *>(dev_buf) + b * per};
+    char *vol = c.take<char>((size_t)slab * n * esz);
+    uint8_t *lab = c.take<uint8_t>((size_t)slab * n);
+    int32_t *thr = c.take<int32_t>((size_t)slab * p->k);
+    double *obj = c.take<double>((size_t)slab);
+    int32_t *sts = c.take<int32_t>((size_t)slab);
+    tsa_problem q = *p;
+    q.nz = nzs;
+    q.volume = vol;
+    char *ws = c.take<char>(0);
+    const size_t wsb = tsa_workspace_size(&q);
+    const char *src = reinterpret_cast<const char *>(p->volume) + (size_t)z0 * n * esz;
+    TSA_CUDA(cudaMemcpyAsync(vol, src, (size_t)nzs * n * esz, cudaMemcpyHostToDevice, st[b]));
+    tsa_outputs o{thr, lab_h ? lab : nullptr, obj, nullptr, sts};
+    TSA_TRY(tsa_segment(&q, &o, ws, wsb, st[b]));
+    TSA_CUDA(cudaMemcpyAsync(thr_h + z0 * p->k, thr, sizeof(int32_t) * nzs * p->k,
+                             cudaMemcpyDeviceToHost, st[b]));
+    if (obj_h)
+      TSA_CUDA(cudaMemcpyAsync(obj_h + z0, obj, sizeof(double) * nzs, cudaMemcpyDeviceToHost, st[b]));
+    if (st_h)
+      TSA_CUDA(cudaMemcpyAsync(st_h + z0, sts, sizeof(int32_t) * nzs, cudaMemcpyDeviceToHost, st[b]));
+    if (lab_h)
+      TSA_CUDA(cudaMemcpyAsync(lab_h + (size_t)z0 * n, lab, (size_t)nzs * n, cudaMemcpyDeviceToHost,
+                               st[b]));
+  }
+  TSA_CUDA(cudaStreamSynchronize(st[0]));
+  TSA_CUDA(cudaStreamSynchronize(st[1]));
+  return TSA_OK;
+}
+
+}  // extern "C"

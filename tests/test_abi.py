@@ -1,0 +1,117 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/tsa.h declares, validates arguments synchronously and sizes
+workspaces.  (No compute calls: there is no device here.)"""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2012_10684_b200 as tsa
+from paper_2012_10684_b200 import tsa_problem
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tsa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tsa_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(tsa.LIB_PATH):
+        import __graft_entry__
+
+        __graft_entry__.build_tsa()
+    return tsa.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = header_functions()
+    assert set(declared) == set(tsa.EXPORTS), declared
+    out = subprocess.check_output(["nm", "-D", "--defined-only", tsa.LIB_PATH]).decode()
+    exported = set(re.findall(r"\bT (tsa_[a-z_0-9]+)", out))
+    missing = [f for f in declared if f not in exported]
+    assert not missing, missing
+    for f in declared:
+        assert hasattr(lib, f)
+
+
+def test_sm100a_cubin_embedded(lib):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", tsa.LIB_PATH]).decode()
+    assert "sm_100a" in out
+
+
+def test_version_and_strings(lib):
+    assert tsa.tsa_version() == 1
+    assert lib.tsa_status_string(3) == b"TSA_ERR_NO_VALID_SPLIT"
+
+
+def _p(**kw):
+    base = dict(volume=1, dtype=1, nx=512, ny=512, nz=300, bins=256, k=2, q=0.8, objective=0,
+                enumeration=0, units_per_slice=0)
+    base.update(kw)
+    return tsa_problem(**base)
+
+
+@pytest.mark.parametrize(
+    "kw",
+    [dict(q=0.0), dict(q=-1.0), dict(q=float("inf")), dict(q=float("nan")), dict(k=0), dict(k=5),
+     dict(bins=1), dict(bins=4097, dtype=2), dict(bins=300, dtype=1), dict(nx=0), dict(nz=-1),
+     dict(k=3, bins=3), dict(volume=0), dict(dtype=3), dict(objective=2), dict(enumeration=7),
+     dict(nx=65536, ny=65536)],
+)
+def test_invalid_arguments_rejected_synchronously(lib, kw):
+    p = _p(**kw)
+    assert lib.tsa_validate(ctypes.byref(p)) == tsa.TSA_ERR_INVALID_ARG
+    assert lib.tsa_workspace_size(ctypes.byref(p)) == 0
+    # entry points return the error before touching the device
+    o = tsa.tsa_outputs(1, 0, 0, 0, 0)
+    assert lib.tsa_segment(ctypes.byref(p), ctypes.byref(o), ctypes.c_void_p(1), 1 << 40, None) == 1
+    assert lib.tsa_histogram(ctypes.byref(p), ctypes.c_void_p(1), ctypes.c_void_p(1), None) == 1
+    assert lib.tsa_label(ctypes.byref(p), ctypes.c_void_p(1), None, ctypes.c_void_p(1), None) == 1
+    assert len(lib.tsa_last_error()) > 0
+
+
+def test_valid_problems_and_workspace(lib):
+    for kw in (dict(), dict(k=4), dict(k=1, nx=256, ny=256, nz=1), dict(dtype=2, bins=4096, nx=1024,
+               ny=1024, nz=1000), dict(q=1.0), dict(objective=1, k=3), dict(enumeration=1, k=4)):
+        p = _p(**kw)
+        assert lib.tsa_validate(ctypes.byref(p)) == 0, kw
+        ws = lib.tsa_workspace_size(ctypes.byref(p))
+        assert ws > 0 and ws % 256 == 0
+    # a too-small workspace is reported, not overrun
+    p = _p()
+    o = tsa.tsa_outputs(1, 0, 0, 0, 0)
+    assert lib.tsa_segment(ctypes.byref(p), ctypes.byref(o), ctypes.c_void_p(256), 10, None) == \
+        tsa.TSA_ERR_WORKSPACE
+
+
+def test_search_argument_checks(lib):
+    ws = lib.tsa_search_workspace_size(300, 512 * 512, 256, 2, 0.8, 0, 0)
+    assert ws > 0
+    assert lib.tsa_search_workspace_size(300, 512 * 512, 256, 5, 0.8, 0, 0) == 0
+    one = ctypes.c_void_p(1)
+    # bad unit range
+    assert lib.tsa_search(one, one, 300, 512 * 512, 256, 2, 0.8, 0, 0, 8, 4, 9, one, one, one, ws,
+                          None) == tsa.TSA_ERR_INVALID_ARG
+    # too-small workspace
+    assert lib.tsa_search(one, one, 300, 512 * 512, 256, 2, 0.8, 0, 0, 8, 0, 8, one, one, one, 16,
+                          None) == tsa.TSA_ERR_WORKSPACE
+    assert lib.tsa_default_units(300, 256, 2, 0) >= 1
+    assert lib.tsa_default_units(300, 256, 4, 0) >= lib.tsa_default_units(300, 256, 2, 0)
+
+
+def test_compute_calls_refuse_cpu_tensors():
+    import torch
+
+    vol = torch.zeros((1, 16, 16), dtype=torch.uint8)
+    with pytest.raises(ValueError):
+        tsa.tsa_segment(vol, 256, 1, 0.8)
+
+
+def test_key_unpack():
+    assert tsa.unpack_key((3 << 36) | (70 << 24) | (71 << 12) | 254, 4) == (3, 70, 71, 254)

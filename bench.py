@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the Tsallis multilevel-thresholding hot path (arXiv 2012.10684).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+
+A *step* is one pass of the whole hot path (SURVEY.md §8(a) rows a1-a5:
+histogram -> prefix tables -> exhaustive tuple search -> argmax/finalize ->
+labels) over one synthetic CT volume of the workload (default c2 =
+BASELINE.json:configs[1], 512x512x300 u8, 256 bins, k=2, q=0.8).  With N GPUs
+(torchrun, one process per GPU) every rank segments its own resident volume
+(slices sharded over GPUs, no data-path collective): weak scaling,
+value = slices of all ranks / max-over-ranks device time.
+
+Prints ONE JSON line on rank 0 (metric, value, unit, ..., roofline,
+cpu_baseline, e2e, clocks, gpu_launches).  --impl reference times the CPU
+oracle (the reference arm for this paper, which has no code of its own).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CT slices/sec and Gtuples/s Tsallis search at 1/2/4/8 B200 vs roofline"
+UNIT = "slices/s"
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--impl", default="tsa", choices=["tsa", "reference"])
+    ap.add_argument("--enumeration", default="canonical", choices=["canonical", "full"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--buffers", type=int, default=0, help="resident volume copies rotated (0 = auto, > 2x L2)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": HBM_FALLBACK_GBS}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 50 ms in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append((time.perf_counter(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        win = [p for (t, p) in self.samples if t0 - 0.05 <= t <= t1 + 0.05]
+        if len(win) < 3:  # timed region shorter than the sampling period: widen
+            win = [p for (t, p) in self.samples if t0 - 2.0 <= t <= t1 + 0.5]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(p[0]) for p in win if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in win if p[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for p in win for n, v in zip(names, p[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(win)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x, world, device):
+    import torch
+
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def cpu_baseline(cfg, vol, q, target_s=15.0):
+    """The oracle as it stands, on the host cores, over a bounded slice sample."""
+    import oracle
+
+    threads = oracle.max_threads()
+    # calibrate on a few slices, then size the sample to ~target_s of wall time
+    n0 = min(cfg.nz, max(threads, 4))
+    t = time.perf_counter()
+    oracle.segment(vol[:n0], cfg.bins, cfg.k, q, threads=threads)
+    dt = time.perf_counter() - t
+    n = int(min(cfg.nz, max(n0, n0 * target_s / max(dt, 1e-6))))
+    t = time.perf_counter()
+    oracle.segment(vol[:n], cfg.bins, cfg.k, q, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {n} of {cfg.nz} slices of workload {cfg.name} (whole path: histogram, "
+                      f"exhaustive Level-1 search, labels), {threads} OpenMP threads, {dt:.2f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    """Reference arm: the CPU oracle, timed as it stands (rank 0 only)."""
+    import numpy as np
+
+    import oracle
+    import phantom
+
+    if rank != 0:
+        return
+    q = cfg.qs[0]
+    vol = phantom.make_volume(cfg)
+    threads = oracle.max_threads()
+    t = time.perf_counter()
+    oracle.segment(vol[:threads], cfg.bins, cfg.k, q, threads=threads)
+    per_slice = (time.perf_counter() - t) / threads
+    budget = 120.0
+    spp = int(max(1, min(cfg.nz, budget / max(args.steps + args.warmup, 1) / max(per_slice, 1e-6))))
+    z = 0
+    for _ in range(args.warmup):
+        oracle.segment(vol[z:z + spp], cfg.bins, cfg.k, q, threads=threads)
+    t = time.perf_counter()
+    for s in range(args.steps):
+        z0 = (s * spp) % max(1, cfg.nz - spp + 1)
+        oracle.segment(vol[z0:z0 + spp], cfg.bins, cfg.k, q, threads=threads)
+    dt = time.perf_counter() - t
+    value = spp * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(cfg, args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{spp} slices of {cfg.name} per step (whole path, Level-1 oracle)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(cfg, args, world):
+    return {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
+            "slices_per_gpu": cfg.nz, "bins": cfg.bins, "k": cfg.k, "q": cfg.qs[0],
+            "input": cfg.dtype, "objective": "pseudo_additive", "enumeration": args.enumeration,
+            "parallelism": f"slices sharded, {world} GPU(s), no collective",
+            "l2": "inputs larger than L2: rotating resident volume/label copies (> 2x 126 MB)"}
+
+
+def main():
+    args = parse()
+    import phantom
+
+    cfg = phantom.CONFIGS[args.workload]
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, cfg, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2012_10684_b200 as tsa
+
+    assert torch.cuda.is_available(), "bench needs a GPU"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    q = cfg.qs[0]
+    k, bins = cfg.k, cfg.bins
+    host = phantom.make_volume(cfg)
+    vol_bytes = host.nbytes
+    n_vox = host.size
+    # resident copies so that consecutive steps never hit L2 (126 MB)
+    nbuf = args.buffers or max(2, int(np.ceil(2 * 126e6 / (vol_bytes + n_vox))) + 1)
+    vols = [torch.from_numpy(host).to(dev) for _ in range(nbuf)]
+    p = tsa.make_problem(vols[0], bins, k, q, enumeration=args.enumeration)
+    ws = tsa.workspace_for(p, dev)
+    outs = []
+    for i in range(nbuf):
+        outs.append({
+            "thresholds": torch.empty((cfg.nz, k), dtype=torch.int32, device=dev),
+            "objective": torch.empty(cfg.nz, dtype=torch.float64, device=dev),
+            "histogram": torch.empty((cfg.nz, bins), dtype=torch.int32, device=dev),
+            "status": torch.empty(cfg.nz, dtype=torch.int32, device=dev),
+            "labels": torch.empty(host.shape, dtype=torch.uint8, device=dev),
+        })
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        tsa.tsa_segment(vols[i % nbuf], bins, k, q, enumeration=args.enumeration, out=outs[i % nbuf],
+                        workspace=ws, stream=stream)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms, world, dev)
+    ms_per_step = ms_max / args.steps
+    value = world * cfg.nz / (ms_per_step * 1e-3)
+
+    # -------- per-kernel timing pass (same kernels through the stage calls)
+    nvox_slice = cfg.nx * cfg.ny
+    U = tsa.tsa_default_units(cfg.nz, bins, k, args.enumeration)
+    hist = torch.empty((cfg.nz, bins), dtype=torch.int32, device=dev)
+    st = torch.empty(cfg.nz, dtype=torch.int32, device=dev)
+    sws = torch.empty(tsa.tsa_search_workspace_size(cfg.nz, nvox_slice, bins, k, q, 0, args.enumeration),
+                      dtype=torch.uint8, device=dev)
+    reps = max(20, min(args.steps, 400))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
+    for i in range(reps + 3):
+        j = i - 3
+        v = vols[i % nbuf]
+        if j >= 0:
+            ev[j][0].record(stream)
+        h, s = tsa.tsa_histogram(v, bins)
+        if j >= 0:
+            ev[j][1].record(stream)
+        ps, pk = tsa.tsa_search(h, s, nvox_slice, k, q, enumeration=args.enumeration, units=U,
+                                workspace=sws)
+        if j >= 0:
+            ev[j][2].record(stream)
+        thr, phi, st2 = tsa.tsa_finalize(h, s, k, q, ps, pk)
+        if j >= 0:
+            ev[j][3].record(stream)
+        tsa.tsa_label(v, thr, st2, bins=bins)
+        if j >= 0:
+            ev[j][4].record(stream)
+    torch.cuda.synchronize()
+    stage_ms = {}
+    for si, name in enumerate(["histogram", "search", "finalize", "label"]):
+        stage_ms[name] = statistics.mean(ev[j][si].elapsed_time(ev[j][si + 1]) for j in range(reps))
+    hist_bytes = n_vox * host.itemsize
+    label_bytes = n_vox * (host.itemsize + 1)
+    kernels = {
+        "histogram": {"ms": stage_ms["histogram"], "bytes": hist_bytes,
+                      "gbs": hist_bytes / (stage_ms["histogram"] * 1e-3) / 1e9},
+        "search": {"ms": stage_ms["search"] + stage_ms["finalize"]},
+        "label": {"ms": stage_ms["label"], "bytes": label_bytes,
+                  "gbs": label_bytes / (stage_ms["label"] * 1e-3) / 1e9},
+    }
+    # tuple counts: nominal C(L-1,k) per slice; evaluated = canonical C(m-1,k)
+    from math import comb
+
+    hist_np = outs[0]["histogram"].cpu().numpy()
+    m = (hist_np > 0).sum(axis=1)
+    evaluated = int(sum(comb(int(mm) - 1, k) for mm in m)) if args.enumeration == "canonical" else \
+        cfg.nz * comb(bins - 1, k)
+    nominal = cfg.nz * comb(bins - 1, k)
+    kernels["search"]["tuples_nominal"] = nominal
+    kernels["search"]["tuples_evaluated"] = evaluated
+    kernels["search"]["gtuples_per_s_nominal"] = nominal / (kernels["search"]["ms"] * 1e-3) / 1e9
+    kernels["search"]["gtuples_per_s_evaluated"] = evaluated / (kernels["search"]["ms"] * 1e-3) / 1e9
+
+    pk_, how = peaks()
+    hbm = float(pk_.get("hbm_gbs", HBM_FALLBACK_GBS))
+    dom = max(("histogram", "label"), key=lambda n: kernels[n]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f)
+        traffic = tr.get(args.workload, {}).get(dom)
+    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": kernels[dom]["gbs"], "peak": hbm,
+                "unit": "GB/s", "frac": kernels[dom]["gbs"] / hbm, "traffic": traffic,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({how})",
+                "algorithmic_bytes_per_launch": kernels[dom]["bytes"]}
+
+    # -------- e2e: host buffers through the C ABI (copies inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        host_t = torch.from_numpy(host).pin_memory()
+        hout = {
+            "thresholds": torch.empty((cfg.nz, k), dtype=torch.int32).pin_memory(),
+            "objective": torch.empty(cfg.nz, dtype=torch.float64).pin_memory(),
+            "status": torch.empty(cfg.nz, dtype=torch.int32).pin_memory(),
+            "labels": torch.empty(host.shape, dtype=torch.uint8).pin_memory(),
+        }
+        slab = 25
+        hp = tsa.make_problem(host_t, bins, k, q, enumeration=args.enumeration)
+        import ctypes
+
+        scratch = torch.empty(int(tsa.load().tsa_segment_host_scratch_size(ctypes.byref(hp), slab)),
+                              dtype=torch.uint8, device=dev)
+        s2 = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        for _ in range(2):
+            tsa.tsa_segment_host(host_t, bins, k, q, enumeration=args.enumeration, slab=slab,
+                                 scratch=scratch, streams=s2, out=hout)
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            tsa.tsa_segment_host(host_t, bins, k, q, enumeration=args.enumeration, slab=slab,
+                                 scratch=scratch, streams=s2, out=hout)
+        dt = time.perf_counter() - t0
+        dt = max_over_ranks(dt, world, dev)
+        barrier(world)
+        d2h = sum(t.numel() * t.element_size() for t in hout.values())
+        e2e = {"value": world * cfg.nz * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(d2h),
+               "api": "tsa_segment_host (pinned host buffers, 2-stream slab pipeline)",
+               "steps": args.e2e_steps}
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, host, q)
+
+    launches_per_step = 6 + (1 if (k >= 3 and bins <= 512) else 0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_of(cfg, args, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+            "kernels": kernels,
+            "gtuples_per_s_nominal": world * nominal / (ms_per_step * 1e-3) / 1e9,
+            "gtuples_per_s_evaluated": world * evaluated / (ms_per_step * 1e-3) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -129,12 +129,22 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   return c.off;
 }
 
+template <int K, int MODE, bool RT>
+void launch_search_kr(const tsa::SearchArgs &a, dim3 grid, cudaStream_t s) {
+  // stage the slice tables in shared memory when they are small
+  const size_t smem = (size_t)(2 * a.E + a.L) * sizeof(double) + (size_t)a.E * sizeof(uint32_t);
+  if (a.L <= 1024)
+    tsa::k_search<K, MODE, RT, true><<<grid, 256, smem, s>>>(a);
+  else
+    tsa::k_search<K, MODE, RT, false><<<grid, 256, 0, s>>>(a);
+}
+
 template <int K, int MODE>
 void launch_search_k(const tsa::SearchArgs &a, dim3 grid, cudaStream_t s, bool rt) {
   if (rt)
-    tsa::k_search<K, MODE, true><<<grid, 256, 0, s>>>(a);
+    launch_search_kr<K, MODE, true>(a, grid, s);
   else
-    tsa::k_search<K, MODE, false><<<grid, 256, 0, s>>>(a);
+    launch_search_kr<K, MODE, false>(a, grid, s);
 }
 
 template <int MODE>
@@ -149,9 +159,8 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
 
 template <int MODE>
 void launch_scan(const tsa::ScanArgs &a, cudaStream_t s) {
-  const int warps = 4;
-  const unsigned blocks = (unsigned)((a.nz + warps - 1) / warps);
-  tsa::k_scan<MODE><<<blocks, 32 * warps, 0, s>>>(a);
+  const size_t smem = (size_t)a.L * sizeof(double);
+  tsa::k_scan<MODE><<<(unsigned)a.nz, 32, smem, s>>>(a);
 }
 
 template <int MODE>
@@ -210,11 +219,11 @@ tsa_status tsa_validate(const tsa_problem *p) {
 
 int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
   if (nz <= 0) return 1;
-  const double target = (double)g_num_sms() * (k >= 3 ? 8.0 : 2.0);
+  const double target = (double)g_num_sms() * 8.0;
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
   double u = std::ceil(target / (double)nz);
-  u = std::min(u, std::max(1.0, rows / 64.0));
+  u = std::min(u, std::max(1.0, rows / 16.0));
   return (int32_t)std::max(1.0, std::min(u, 256.0));
 }
 
@@ -270,6 +279,7 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   a.hist = hist;
   a.status = slice_status;
   a.n = p->nx * p->ny;
+  a.z0 = 0;
   a.L = p->bins;
   const int threads = 512;
   // privatised copies: one per warp for small L, fewer for large L (<= 64 KB)
@@ -277,18 +287,19 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   a.replicas = reps;
   const size_t smem = (size_t)reps * p->bins * 4;
   const int64_t bytes_per_slice = a.n * (p->dtype == TSA_U8 ? 1 : 2);
-  // ~64 KB of input per CTA
+  // ~64 KB of input per CTA (measured best for 512x512 u8 slices)
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, bytes_per_slice / 65536));
   a.chunks = chunks;
   dim3 grid((unsigned)chunks, (unsigned)p->nz);
-  if (p->dtype == TSA_U8) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(tsa::k_histogram<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tsa::k_histogram<uint8_t><<<grid, threads, smem, s>>>(a);
+  if (p->dtype == TSA_U8 && p->bins == 256) {
+    tsa::k_histogram<uint8_t, false><<<grid, threads, smem, s>>>(a);
+  } else if (p->dtype == TSA_U8) {
+    tsa::k_histogram<uint8_t, true><<<grid, threads, smem, s>>>(a);
   } else {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(tsa::k_histogram<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tsa::k_histogram<uint16_t><<<grid, threads, smem, s>>>(a);
+      cudaFuncSetAttribute(tsa::k_histogram<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    tsa::k_histogram<uint16_t, true><<<grid, threads, smem, s>>>(a);
   }
   return check_cuda("k_histogram");
 }
@@ -346,7 +357,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   sa.Asuf = w.Asuf;
   sa.M = w.M;
   sa.luts = l;
-  sa.mode = mode;
+
   switch (mode) {
     case tsa::PROD_MAX: launch_scan<tsa::PROD_MAX>(sa, s); break;
     case tsa::PROD_MIN: launch_scan<tsa::PROD_MIN>(sa, s); break;
@@ -409,7 +420,7 @@ static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, 
                                 int32_t bins, int32_t k, double q, int32_t objective,
                                 const double *ps, const uint64_t *pk, int32_t nparts,
                                 int32_t *thresholds, double *objective_out, int32_t *status_out,
-                                cudaStream_t s) {
+                                int32_t *status_out2, cudaStream_t s) {
   tsa::FinalizeArgs f;
   f.hist = hist;
   f.status_in = status_in;
@@ -424,7 +435,11 @@ static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, 
   f.thresholds = thresholds;
   f.objective_out = objective_out;
   f.status_out = status_out;
-  tsa::k_finalize<<<(unsigned)nz, 32, (size_t)bins * sizeof(double), s>>>(f);
+  f.status_out2 = status_out2;
+  const size_t smem = (size_t)bins * (sizeof(double) + sizeof(int));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(tsa::k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tsa::k_finalize<<<(unsigned)nz, 32, smem, s>>>(f);
   return check_cuda("k_finalize");
 }
 
@@ -438,7 +453,7 @@ tsa_status tsa_finalize(const uint32_t *hist, const int32_t *slice_status, int64
       !out->thresholds)
     return set_error(TSA_ERR_INVALID_ARG, "finalize pointers");
   return finalize_impl(hist, slice_status, nz, bins, k, q, objective, part_score, part_key,
-                       nparts, out->thresholds, out->objective, out->slice_status, S(stream));
+                       nparts, out->thresholds, out->objective, out->slice_status, nullptr, S(stream));
 }
 
 tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
@@ -451,14 +466,26 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
   a.thr = thresholds;
   a.status = slice_status;
   a.n = p->nx * p->ny;
+  a.z0 = 0;
+  a.z1 = p->nz;
   a.k = p->k;
-  const int64_t bytes = a.n * (p->dtype == TSA_U8 ? 2 : 3);
-  a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, bytes / 65536));
-  dim3 grid((unsigned)a.chunks, (unsigned)p->nz);
-  if (p->dtype == TSA_U8)
-    tsa::k_label<uint8_t><<<grid, 256, 0, S(stream)>>>(a);
-  else
-    tsa::k_label<uint16_t><<<grid, 256, 0, S(stream)>>>(a);
+  const bool aligned = a.n % 16 == 0 && (reinterpret_cast<uintptr_t>(p->volume) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(labels) & 15) == 0;
+  if (aligned) {
+    const int64_t groups = a.n / 16 * p->nz;
+    const int64_t blocks = std::min<int64_t>((groups + 255) / 256, (int64_t)g_num_sms() * 8);
+    if (p->dtype == TSA_U8)
+      tsa::k_label_flat<uint8_t><<<(unsigned)blocks, 256, 0, S(stream)>>>(a);
+    else
+      tsa::k_label_flat<uint16_t><<<(unsigned)blocks, 256, 0, S(stream)>>>(a);
+  } else {
+    const int64_t cx = std::max<int64_t>(1, std::min<int64_t>(64, a.n / 4096));
+    dim3 grid((unsigned)cx, (unsigned)p->nz);
+    if (p->dtype == TSA_U8)
+      tsa::k_label_generic<uint8_t><<<grid, 256, 0, S(stream)>>>(a);
+    else
+      tsa::k_label_generic<uint16_t><<<grid, 256, 0, S(stream)>>>(a);
+  }
   return check_cuda("k_label");
 }
 
@@ -477,11 +504,8 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   TSA_TRY(tsa_search(hist, w.status, p->nz, p->nx * p->ny, p->bins, p->k, p->q, p->objective,
                      p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, stream));
   TSA_TRY(finalize_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
-                        out->thresholds, out->objective, w.status, s));
+                        out->thresholds, out->objective, w.status, out->slice_status, s));
   if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, stream));
-  if (out->slice_status)
-    TSA_CUDA(cudaMemcpyAsync(out->slice_status, w.status, sizeof(int32_t) * p->nz,
-                             cudaMemcpyDeviceToDevice, s));
   return TSA_OK;
 }
 

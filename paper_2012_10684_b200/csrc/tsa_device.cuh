@@ -93,9 +93,9 @@ struct Luts {
 // comparison, so invalid tuples are skipped without a branch.
 template <int MODE>
 __device__ __forceinline__ double class_term(const SliceTables &t, const Luts &l, int a, int b) {
-  const uint32_t n = __ldg(t.C + b + 1) - __ldg(t.C + a);
-  const double w = dd_diff(__ldg(t.Whi + b + 1), __ldg(t.Wlo + b + 1), __ldg(t.Whi + a),
-                           __ldg(t.Wlo + a));
+  // generic loads: the tables may be staged in shared memory
+  const uint32_t n = t.C[b + 1] - t.C[a];
+  const double w = dd_diff(t.Whi[b + 1], t.Wlo[b + 1], t.Whi[a], t.Wlo[a]);
   if (MODE == PROD_MAX || MODE == PROD_MIN) {
     return __dmul_rn(w, __ldg(l.ipow + n));
   } else if (MODE == SUM) {

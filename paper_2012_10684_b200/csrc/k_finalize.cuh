@@ -53,6 +53,13 @@ struct FinalizeArgs {
   int32_t *status_out2;
 };
 
+__device__ __forceinline__ int class_of(int i, int t0, int t1, int t2, int t3) {
+  return (i > t0) + (i > t1) + (i > t2) + (i > t3);
+}
+
+// One warp per slice.  Lane c <= k owns class c: it sums P_c and then A_c
+// sequentially over the class's non-empty bins in ascending order (the
+// definition's order); the p_i and pow/log terms are computed lane-parallel.
 __global__ void __launch_bounds__(32) k_finalize(FinalizeArgs g) {
   extern __shared__ double fsh[];  // [L] p then terms, followed by int [L] bin list
   int *lst = reinterpret_cast<int *>(fsh + g.L);
@@ -81,19 +88,25 @@ __global__ void __launch_bounds__(32) k_finalize(FinalizeArgs g) {
     }
     return;
   }
-  int t[kKMax];
-#pragma unroll
-  for (int j = 0; j < kKMax; j++) t[j] = j < k ? (int)((key >> (12 * (k - 1 - j))) & 0xFFFull) : L;
-  if (lane < k) g.thresholds[z * k + lane] = t[lane];
+  // thresholds beyond k are "L": no bin is above them
+  const int t0 = (int)((key >> (12 * (k - 1))) & 0xFFFull);
+  const int t1 = k > 1 ? (int)((key >> (12 * (k - 2))) & 0xFFFull) : L;
+  const int t2 = k > 2 ? (int)((key >> (12 * (k - 3))) & 0xFFFull) : L;
+  const int t3 = k > 3 ? (int)(key & 0xFFFull) : L;
+  if (lane < k) {
+    const int tl = lane == 0 ? t0 : lane == 1 ? t1 : lane == 2 ? t2 : t3;
+    g.thresholds[z * k + lane] = tl;
+  }
   if (lane == 0) {
     if (g.status_out) g.status_out[z] = kOK;
     if (g.status_out2) g.status_out2[z] = kOK;
   }
   if (!g.objective_out) return;
   const uint32_t *h = g.hist + z * L;
-  // N and the ordered list of non-empty bins
+  // N, the ordered list of non-empty bins, and per-class list lengths
   uint64_t nsum = 0;
   int m = 0;
+  int cnt_mine = 0;  // lane c: number of non-empty bins in class c
   for (int i0 = 0; i0 < L; i0 += 32) {
     const int i = i0 + lane;
     const uint32_t c = i < L ? __ldg(h + i) : 0u;
@@ -101,69 +114,66 @@ __global__ void __launch_bounds__(32) k_finalize(FinalizeArgs g) {
     const unsigned bal = __ballot_sync(0xffffffffu, c != 0);
     if (c) lst[m + __popc(bal & ((1u << lane) - 1u))] = i;
     m += __popc(bal);
+    const int cls = c ? class_of(i, t0, t1, t2, t3) : -1;
+#pragma unroll
+    for (int cc = 0; cc <= kKMax; cc++) {
+      const int n_c = __popc(__ballot_sync(0xffffffffu, cls == cc));
+      if (lane == cc) cnt_mine += n_c;
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, off);
   const double N = (double)nsum;  // exact: the oracle's sequential double sum of integers
+  int start = cnt_mine;           // exclusive prefix of class lengths over lanes 0..k
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, start, off);
+    if (lane >= off) start += o;
+  }
+  start -= cnt_mine;
   __syncwarp();
   for (int j = lane; j < m; j += 32) fsh[j] = __ddiv_rn((double)__ldg(h + lst[j]), N);
   __syncwarp();
-  __shared__ double Pc[kKMax + 1];
-  if (lane == 0) {
-    int cls = 0;
-    double P = 0.0;
-    for (int j = 0; j < m; j++) {
-      const int i = lst[j];
-      while (cls < k && i > t[cls]) {
-        Pc[cls++] = P;
-        P = 0.0;
-      }
-      P = __dadd_rn(P, fsh[j]);
-    }
-    while (cls <= k) {
-      Pc[cls++] = P;
-      P = 0.0;
-    }
-  }
+  double P = 0.0;
+  if (lane <= k)
+    for (int j = start; j < start + cnt_mine; j++) P = __dadd_rn(P, fsh[j]);
   __syncwarp();
   const double q = g.q;
   const bool shannon = q == 1.0;
+  __shared__ double Psh[kKMax + 1];
+  if (lane <= k) Psh[lane] = P;
+  __syncwarp();
   for (int j = lane; j < m; j += 32) {
-    const int i = lst[j];
-    int cls = 0;
-    while (cls < k && i > t[cls]) cls++;
-    const double r = __ddiv_rn(fsh[j], Pc[cls]);
+    const int cls = class_of(lst[j], t0, t1, t2, t3);
+    const double r = __ddiv_rn(fsh[j], Psh[cls]);
     fsh[j] = shannon ? __dmul_rn(r, log(r)) : pow(r, q);
   }
   __syncwarp();
-  if (lane == 0) {
-    double S[kKMax + 1];
-    int cls = 0;
-    double A = 0.0;
-    for (int j = 0; j < m; j++) {
-      const int i = lst[j];
-      while (cls < k && i > t[cls]) {
-        S[cls++] = A;
-        A = 0.0;
-      }
+  double A = 0.0;
+  if (lane <= k)
+    for (int j = start; j < start + cnt_mine; j++)
       A = shannon ? __dsub_rn(A, fsh[j]) : __dadd_rn(A, fsh[j]);
-    }
-    while (cls <= k) {
-      S[cls++] = A;
-      A = 0.0;
-    }
-    if (!shannon)
-      for (int j = 0; j <= k; j++) S[j] = __ddiv_rn(__dsub_rn(1.0, S[j]), __dsub_rn(q, 1.0));
+  const double Sl = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(q, 1.0));
+  double S[kKMax + 1];
+#pragma unroll
+  for (int j = 0; j <= kKMax; j++) S[j] = __shfl_sync(0xffffffffu, Sl, j);
+  if (lane == 0) {
     double phi;
     if (g.objective == 1) {
       double sum = 0.0, prod = 1.0;
-      for (int j = 0; j <= k; j++) sum = __dadd_rn(sum, S[j]);
-      for (int j = 0; j <= k; j++) prod = __dmul_rn(prod, S[j]);
+#pragma unroll
+      for (int j = 0; j <= kKMax; j++)
+        if (j <= k) sum = __dadd_rn(sum, S[j]);
+#pragma unroll
+      for (int j = 0; j <= kKMax; j++)
+        if (j <= k) prod = __dmul_rn(prod, S[j]);
       phi = __dadd_rn(sum, __dmul_rn(__dsub_rn(1.0, q), prod));
     } else {
       phi = S[0];
-      for (int j = 1; j <= k; j++)
-        phi = __dadd_rn(__dadd_rn(phi, S[j]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, q), phi), S[j]));
+#pragma unroll
+      for (int j = 1; j <= kKMax; j++)
+        if (j <= k)
+          phi = __dadd_rn(__dadd_rn(phi, S[j]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, q), phi), S[j]));
     }
     g.objective_out[z] = phi;
   }

@@ -24,10 +24,16 @@ struct LabelArgs {
   int k;
 };
 
-__device__ __forceinline__ uint32_t swar_label4(uint32_t w, const uint32_t *tb, int k) {
-  uint32_t o = 0;
-  for (int j = 0; j < k; j++) o += __vcmpgtu4(w, tb[j]) & 0x01010101u;
-  return o;
+// Thresholds beyond k are set to 255 (u8) / 65535 (u16): "v > t" is then never
+// true, so the unrolled 4-way compare needs no k-dependent control flow.
+__device__ __forceinline__ uint32_t swar_label4(uint32_t w, uint32_t t0, uint32_t t1, uint32_t t2,
+                                                uint32_t t3) {
+  return (__vcmpgtu4(w, t0) & 0x01010101u) + (__vcmpgtu4(w, t1) & 0x01010101u) +
+         (__vcmpgtu4(w, t2) & 0x01010101u) + (__vcmpgtu4(w, t3) & 0x01010101u);
+}
+
+__device__ __forceinline__ uint32_t label_of(int v, int t0, int t1, int t2, int t3) {
+  return (uint32_t)(v > t0) + (uint32_t)(v > t1) + (uint32_t)(v > t2) + (uint32_t)(v > t3);
 }
 
 // Fast path: n % 16 == 0 and 16-byte aligned volume/labels (the common case).
@@ -38,29 +44,37 @@ __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint4 *src = reinterpret_cast<const uint4 *>(g.vol);
   uint4 *dst = reinterpret_cast<uint4 *>(g.labels);
-  int zc = -1;
+  const int64_t i_first = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int z = (int)(i_first / per);
+  int64_t zend = (int64_t)(z + 1) * per;  // first group of the next slice
+  const int tmax = sizeof(T) == 1 ? 255 : 65535;
+  int t0 = tmax, t1 = tmax, t2 = tmax, t3 = tmax;
   bool ok = false;
-  uint32_t tb[kKMax];
-  int t[kKMax];
-  for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i1; i += stride) {
-    const int z = (int)(i / per);
-    if (z != zc) {
-      zc = z;
-      ok = g.status == nullptr || g.status[z] == kOK;
-#pragma unroll
-      for (int j = 0; j < kKMax; j++) {
-        t[j] = j < g.k ? g.thr[z * g.k + j] : 0;
-        tb[j] = (uint32_t)(t[j] & 0xff) * 0x01010101u;
+  bool fresh = true;
+  for (int64_t i = i_first; i < i1; i += stride) {
+    if (i >= zend || fresh) {  // slice change: at most once or twice per thread
+      if (!fresh) {
+        z = (int)(i / per);
+        zend = (int64_t)(z + 1) * per;
       }
+      fresh = false;
+      ok = g.status == nullptr || g.status[z] == kOK;
+      const int32_t *tz = g.thr + z * g.k;
+      t0 = tz[0];
+      t1 = g.k > 1 ? tz[1] : tmax;
+      t2 = g.k > 2 ? tz[2] : tmax;
+      t3 = g.k > 3 ? tz[3] : tmax;
     }
     if (sizeof(T) == 1) {
       const uint4 w = __ldcs(src + i);
       uint4 o = make_uint4(0u, 0u, 0u, 0u);
       if (ok) {
-        o.x = swar_label4(w.x, tb, g.k);
-        o.y = swar_label4(w.y, tb, g.k);
-        o.z = swar_label4(w.z, tb, g.k);
-        o.w = swar_label4(w.w, tb, g.k);
+        const uint32_t b0 = (uint32_t)t0 * 0x01010101u, b1 = (uint32_t)t1 * 0x01010101u;
+        const uint32_t b2 = (uint32_t)t2 * 0x01010101u, b3 = (uint32_t)t3 * 0x01010101u;
+        o.x = swar_label4(w.x, b0, b1, b2, b3);
+        o.y = swar_label4(w.y, b0, b1, b2, b3);
+        o.z = swar_label4(w.z, b0, b1, b2, b3);
+        o.w = swar_label4(w.w, b0, b1, b2, b3);
       }
       __stcs(dst + i, o);
     } else {
@@ -71,9 +85,7 @@ __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
 #pragma unroll
         for (int e = 0; e < 16; e++) {
           const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          uint32_t l = 0;
-          for (int j = 0; j < g.k; j++) l += v > t[j];
-          o[e >> 2] |= l << (8 * (e & 3));
+          o[e >> 2] |= label_of(v, t0, t1, t2, t3) << (8 * (e & 3));
         }
       }
       __stcs(dst + i, make_uint4(o[0], o[1], o[2], o[3]));
@@ -88,15 +100,13 @@ __global__ void __launch_bounds__(256) k_label_generic(LabelArgs g) {
   const T *slice = reinterpret_cast<const T *>(g.vol) + (size_t)z * g.n;
   uint8_t *out = g.labels + (size_t)z * g.n;
   const bool ok = g.status == nullptr || g.status[z] == kOK;
-  int t[kKMax] = {0, 0, 0, 0};
-  for (int j = 0; j < g.k; j++) t[j] = g.thr[z * g.k + j];
+  const int tmax = 65535;
+  const int32_t *tz = g.thr + z * g.k;
+  const int t0 = tz[0], t1 = g.k > 1 ? tz[1] : tmax, t2 = g.k > 2 ? tz[2] : tmax;
+  const int t3 = g.k > 3 ? tz[3] : tmax;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)slice[i];
-    uint32_t l = 0;
-    if (ok)
-      for (int j = 0; j < g.k; j++) l += v > t[j];
-    out[i] = (uint8_t)l;
+    out[i] = ok ? (uint8_t)label_of((int)slice[i], t0, t1, t2, t3) : (uint8_t)0;
   }
 }
 

@@ -35,7 +35,7 @@ struct SearchArgs {
   uint64_t *part_key;
   Luts luts;
   int64_t nz;
-  int E, L, units, unit_begin;
+  int E, L, RS, units, unit_begin;  // RS: R-table row stride (>= L + 4, even)
 };
 
 // STAGE: copy the slice's C/W/Asuf tables to shared memory first (L <= 1024).
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) k_search(SearchArgs g) {
               lo = idx[j] + 1;
             }
             constexpr bool kRT = RT && K >= 3;
-            const double *Rrow = kRT ? g.R + ((size_t)z * g.L + (size_t)a) * g.L : nullptr;
+            const double *Rrow = kRT ? g.R + ((size_t)z * g.L + (size_t)a) * g.RS : nullptr;
             for (int b = a + 1 + lane; b <= M - 2; b += 32) {
               const double R = kRT ? __ldg(Rrow + b)
                                    : combine<MODE>(class_term<MODE>(t, g.luts, a + 1, b), t.Asuf[b]);
@@ -152,6 +152,155 @@ __global__ void __launch_bounds__(256) k_search(SearchArgs g) {
     if (lane == 0) {
       g.part_score[(size_t)blockIdx.x * g.nz + z] = best;
       g.part_key[(size_t)blockIdx.x * g.nz + z] = key;
+    }
+  }
+}
+
+}  // namespace tsa
+
+namespace tsa {
+
+// Colex unranking of an R-combination (R = 2 or 3): the combination of rank r
+// in colexicographic order (last element major).  Closed-form estimate plus
+// exact integer correction.
+template <int R>
+__device__ __forceinline__ void unrank_colex(uint64_t r, int *idx) {
+  if (R == 1) {
+    idx[0] = (int)r;
+    return;
+  }
+  if (R == 2) {
+    int a = (int)((1.0 + sqrt(1.0 + 8.0 * (double)r)) * 0.5);
+    while (a > 1 && binom((uint64_t)a, 2) > r) a--;
+    while (binom((uint64_t)a + 1, 2) <= r) a++;
+    idx[1] = a;
+    idx[0] = (int)(r - binom((uint64_t)a, 2));
+    return;
+  }
+  // R == 3
+  int a = (int)cbrt(6.0 * (double)r) + 1;
+  while (a > 2 && binom((uint64_t)a, 3) > r) a--;
+  while (binom((uint64_t)a + 1, 3) <= r) a++;
+  idx[2] = a;
+  r -= binom((uint64_t)a, 3);
+  int b = (int)((1.0 + sqrt(1.0 + 8.0 * (double)r)) * 0.5);
+  while (b > 1 && binom((uint64_t)b, 2) > r) b--;
+  while (binom((uint64_t)b + 1, 2) <= r) b++;
+  idx[1] = b;
+  idx[0] = (int)(r - binom((uint64_t)b, 2));
+}
+
+// hit |= any(pre (x) r_i >= best) over 4 columns, as 4 DMUL/DADD + 4 setp.ge.or
+// into one predicate (2 FP64-pipe instructions per tuple; the compiler would
+// otherwise turn the OR of compares into a DSETP.MAX chain).
+template <int MODE>
+__device__ __forceinline__ unsigned cmp4(unsigned hit, double pre, double2 x, double2 y, double best) {
+  if (MODE == SUM) {
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "add.rn.f64 t0, %1, %2;\n\tadd.rn.f64 t1, %1, %3;\n\t"
+        "add.rn.f64 t2, %1, %4;\n\tadd.rn.f64 t3, %1, %5;\n\t"
+        "setp.ge.or.f64 p, t0, %6, p;\n\tsetp.ge.or.f64 p, t1, %6, p;\n\t"
+        "setp.ge.or.f64 p, t2, %6, p;\n\tsetp.ge.or.f64 p, t3, %6, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "+r"(hit)
+        : "d"(pre), "d"(x.x), "d"(x.y), "d"(y.x), "d"(y.y), "d"(best));
+  } else {
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "mul.rn.f64 t0, %1, %2;\n\tmul.rn.f64 t1, %1, %3;\n\t"
+        "mul.rn.f64 t2, %1, %4;\n\tmul.rn.f64 t3, %1, %5;\n\t"
+        "setp.ge.or.f64 p, t0, %6, p;\n\tsetp.ge.or.f64 p, t1, %6, p;\n\t"
+        "setp.ge.or.f64 p, t2, %6, p;\n\tsetp.ge.or.f64 p, t3, %6, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "+r"(hit)
+        : "d"(pre), "d"(x.x), "d"(x.y), "d"(y.x), "d"(y.y), "d"(best));
+  }
+  return hit;
+}
+
+// Exhaustive search for k >= 3 with the R table (pseudo-additive, q != 1 or
+// q == 1).  One thread per row (a (k-1)-prefix ending at a = t_{k-1}); rows
+// in colex order so neighbouring lanes share a and read the same R row (L1
+// broadcast).  Inner loop per tuple: v = pre (x) R[a][b] and one predicated
+// compare "v >= best" OR-accumulated into a flag -- 2 FP64-pipe instructions
+// per tuple.  Only when the flag is set (the row may hold a new best) is the
+// row rescanned with the full (score, key) total order, so the result equals
+// the lowest tuple among the maxima exactly.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) k_search_rows(SearchArgs g) {
+  static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
+  constexpr int R = K - 1;
+  const int z = blockIdx.y;
+  const int u = g.unit_begin + blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double best = -CUDART_INF;
+  uint64_t bestkey = kKeyNone;
+  const int st = g.status[z];
+  const int M = g.Mz[z];
+  const int P = M - 1;
+  const SliceTables t{g.C + (size_t)z * g.E, g.Whi + (size_t)z * g.E, g.Wlo + (size_t)z * g.E,
+                      g.Asuf + (size_t)z * g.L};
+  const int32_t *bin = g.Bin + (size_t)z * g.E;
+  if (st == kOK && P >= K) {
+    const uint64_t NR = binom((uint64_t)P, R);
+    const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
+    const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
+    for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      int idx[R];
+      unrank_colex<R>(r, idx);
+      const int a = idx[R - 1];
+      if (a > M - 3) continue;
+      double pre = MODE == SUM ? 0.0 : 1.0;
+      int lo = 0;
+#pragma unroll
+      for (int j = 0; j < R; j++) {
+        pre = combine<MODE>(pre, class_term<MODE>(t, g.luts, lo, idx[j]));
+        lo = idx[j] + 1;
+      }
+      if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
+      const double *row = g.R + ((size_t)z * g.L + (size_t)a) * g.RS;
+      // columns [a+1, M-2]; entries outside are NaN, so 4-column groups from the
+      // even column at or below a+1 need no bounds checks (row stride RS >= L+4)
+      const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
+      const double2 *re = rp + ((M - 1 - ((a + 1) & ~1) + 3) >> 2) * 2;
+      unsigned hit = 0;
+      for (; rp < re; rp += 2) {
+        const double2 x = __ldg(rp), y = __ldg(rp + 1);
+        hit = cmp4<MODE>(hit, pre, x, y, best);
+      }
+      if (hit) {
+        uint64_t kp = 0;
+#pragma unroll
+        for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
+        for (int b = a + 1; b <= M - 2; b++) {
+          const double v = combine<MODE>(pre, row[b]);
+          if (v >= best) {
+            const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+            if (better(v, key, best, bestkey)) {
+              best = v;
+              bestkey = key;
+            }
+          }
+        }
+      }
+    }
+  }
+  warp_argmax(best, bestkey);
+  __shared__ double ss[32];
+  __shared__ uint64_t sk[32];
+  if (lane == 0) {
+    ss[warp] = best;
+    sk[warp] = bestkey;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    best = lane < nw ? ss[lane] : -CUDART_INF;
+    bestkey = lane < nw ? sk[lane] : kKeyNone;
+    warp_argmax(best, bestkey);
+    if (lane == 0) {
+      g.part_score[(size_t)blockIdx.x * g.nz + z] = best;
+      g.part_key[(size_t)blockIdx.x * g.nz + z] = bestkey;
     }
   }
 }

@@ -64,19 +64,23 @@ __global__ void __launch_bounds__(32) k_scan(ScanArgs g) {
   const uint32_t *h = g.hist + z * L;
   const int per = (L + 31) / 32;
   const int i0 = min(L, lane * per), i1 = min(L, i0 + per);
+  // w_i for all bins, lane-strided: independent pow/log calls overlap
+#pragma unroll 4
+  for (int i = lane; i < L; i += 32) {
+    const uint32_t c = __ldg(h + i);
+    const double x = (double)c;
+    wsh[i] = c == 0 ? 0.0 : (g.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q));
+  }
+  __syncwarp();
   uint32_t m_l = 0, n_l = 0;
   dd w_l = {0.0, 0.0};
   for (int i = i0; i < i1; i++) {
     const uint32_t c = __ldg(h + i);
-    double w = 0.0;
     if (c) {
       m_l++;
       n_l += c;
-      const double x = (double)c;
-      w = g.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q);
-      w_l = dd_add_d(w_l, w);
+      w_l = dd_add_d(w_l, wsh[i]);
     }
-    wsh[i] = w;
   }
   uint32_t m_inc = m_l, n_inc = n_l;
   dd w_inc = w_l;
@@ -164,12 +168,12 @@ __global__ void __launch_bounds__(32) k_scan(ScanArgs g) {
 // R[a][b] = combine(T(a+1, b), Asuf[b]) for 0 <= a < b <= M-2 (k >= 3,
 // pseudo-additive): the last two classes of a tuple, so the search's inner
 // loop is one multiply (or add) and one compare per tuple.  Entries b > M-2
-// of each row are padded with NaN (never selected) up to the row stride.
+// of each row are padded with NaN (never selected) up to the row stride RS.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_rtable(const uint32_t *C, const double *Whi,
                                                 const double *Wlo, const double *Asuf,
                                                 const int32_t *Mz, const int32_t *status,
-                                                double *R, int E, int L, Luts luts) {
+                                                double *R, int E, int L, int RS, Luts luts) {
   const int z = blockIdx.y;
   const int a = blockIdx.x;
   if (status[z] != kOK) return;
@@ -177,8 +181,8 @@ __global__ void __launch_bounds__(256) k_rtable(const uint32_t *C, const double 
   if (a > M - 3) return;
   SliceTables t{C + (size_t)z * E, Whi + (size_t)z * E, Wlo + (size_t)z * E, nullptr};
   const double *as = Asuf + (size_t)z * L;
-  double *row = R + ((size_t)z * L + a) * L;
-  for (int b = threadIdx.x; b < L; b += blockDim.x) {
+  double *row = R + ((size_t)z * L + a) * RS;
+  for (int b = threadIdx.x; b < RS; b += blockDim.x) {
     double v = CUDART_NAN;
     if (b > a && b <= M - 2) v = combine<MODE>(class_term<MODE>(t, luts, a + 1, b), __ldg(as + b));
     row[b] = v;

@@ -90,6 +90,9 @@ int search_mode(double q, int32_t objective) {
   return q < 1.0 ? tsa::PROD_MAX : tsa::PROD_MIN;
 }
 
+// R-table row stride: >= bins + 4 (4-column groups read past M-2 into NaN) and even
+inline int rstride(int32_t bins) { return (bins + 4 + 1) & ~1; }
+
 bool use_rtable(int32_t bins, int32_t k, int32_t objective) {
   return objective == TSA_OBJ_PSEUDO_ADDITIVE && k >= 3 && bins <= 512;
 }
@@ -125,7 +128,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   }
   w.Asuf = c.take<double>(nz * (size_t)bins);
   w.M = c.take<int32_t>(nz);
-  if (use_rtable(bins, k, objective)) w.R = c.take<double>(nz * (size_t)bins * bins);
+  if (use_rtable(bins, k, objective)) w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 8);
   return c.off;
 }
 
@@ -149,6 +152,16 @@ void launch_search_k(const tsa::SearchArgs &a, dim3 grid, cudaStream_t s, bool r
 
 template <int MODE>
 void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t s, bool rt) {
+  // k >= 3 with the R table (even row stride for 16-byte pair loads): thread-per-row kernel
+  if constexpr (MODE != tsa::SPP) {
+    if (rt && k >= 3) {
+      if (k == 3)
+        tsa::k_search_rows<3, MODE><<<grid, 256, 0, s>>>(a);
+      else
+        tsa::k_search_rows<4, MODE><<<grid, 256, 0, s>>>(a);
+      return;
+    }
+  }
   switch (k) {
     case 1: launch_search_k<1, MODE>(a, grid, s, false); break;
     case 2: launch_search_k<2, MODE>(a, grid, s, false); break;
@@ -168,7 +181,7 @@ void launch_rtable(const SearchWs &w, const uint32_t *C, const double *Whi, cons
                    const int32_t *status, int64_t nz, int E, int L, const tsa::Luts &l,
                    cudaStream_t s) {
   dim3 grid((unsigned)L, (unsigned)nz);
-  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, E, L, l);
+  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, E, L, rstride(L), l);
 }
 
 int g_num_sms() {
@@ -394,6 +407,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.nz = nz;
   a.E = E;
   a.L = bins;
+  a.RS = rstride(bins);
   a.units = units;
   a.unit_begin = unit_begin;
   dim3 grid((unsigned)(unit_end - unit_begin), (unsigned)nz);
@@ -437,7 +451,7 @@ static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, 
   f.status_out = status_out;
   f.status_out2 = status_out2;
   const size_t smem = (size_t)bins * (sizeof(double) + sizeof(int));
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)
     cudaFuncSetAttribute(tsa::k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tsa::k_finalize<<<(unsigned)nz, 32, smem, s>>>(f);
   return check_cuda("k_finalize");

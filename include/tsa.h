@@ -87,6 +87,17 @@ typedef struct {
   int32_t objective;    /* tsa_objective */
   int32_t enumeration;  /* tsa_enumeration */
   int32_t units_per_slice; /* search work units per slice (0 = library heuristic) */
+  /* tsa_segment schedule (0 = library default for every field):
+   *   pipeline     1 = one persistent fused kernel (histogram / tables + search +
+   *                finalize / labels overlapped through a dependency-ordered task
+   *                queue; needs k <= 2, bins <= 1024, CANONICAL, PSEUDO_ADDITIVE,
+   *                nx*ny % 16 == 0, 16-byte aligned volume and labels),
+   *                -1 = one kernel per stage, 0 = fused whenever eligible
+   *   slab_slices  fused: slices per pipeline slab
+   *   label_lag    fused: rounds by which labelling trails the histogram */
+  int32_t pipeline;
+  int32_t slab_slices;
+  int32_t label_lag;
 } tsa_problem;
 
 typedef struct {
@@ -102,6 +113,11 @@ tsa_status tsa_validate(const tsa_problem *p);
 
 /* Bytes of workspace tsa_segment needs for this problem (0 if invalid). */
 size_t tsa_workspace_size(const tsa_problem *p);
+
+/* Which implementation tsa_segment runs for this problem: 1 = the fused
+ * persistent kernel, -1 = one kernel per stage, 0 = invalid problem.  (Labels
+ * must also be 16-byte aligned for the fused kernel.) */
+int32_t tsa_pipeline_kind(const tsa_problem *p);
 
 /* The whole hot path on one stream:
  * histogram -> tables (prefix scans) -> exhaustive search -> argmax/finalize

@@ -34,7 +34,7 @@ EXPORTS = (
     "tsa_validate", "tsa_workspace_size", "tsa_segment", "tsa_histogram",
     "tsa_search_workspace_size", "tsa_default_units", "tsa_search", "tsa_merge",
     "tsa_finalize", "tsa_label", "tsa_segment_host_scratch_size", "tsa_segment_host",
-    "tsa_status_string", "tsa_last_error", "tsa_version",
+    "tsa_status_string", "tsa_last_error", "tsa_version", "tsa_pipeline_kind",
 )
 
 
@@ -62,6 +62,9 @@ class tsa_problem(ctypes.Structure):
         ("objective", ctypes.c_int32),
         ("enumeration", ctypes.c_int32),
         ("units_per_slice", ctypes.c_int32),
+        ("pipeline", ctypes.c_int32),
+        ("slab_slices", ctypes.c_int32),
+        ("label_lag", ctypes.c_int32),
     ]
 
 
@@ -109,6 +112,7 @@ def load() -> ctypes.CDLL:
         "tsa_status_string": (ctypes.c_char_p, [I32]),
         "tsa_last_error": (ctypes.c_char_p, []),
         "tsa_version": (I32, []),
+        "tsa_pipeline_kind": (I32, [PP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -148,13 +152,17 @@ def _dtype_code(vol):
     raise ValueError(f"volume dtype must be uint8 or uint16, got {vol.dtype}")
 
 
-def make_problem(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0):
+PIPELINES = {"auto": 0, "fused": 1, "staged": -1}
+
+
+def make_problem(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0,
+                 pipeline="auto", slab_slices=0, label_lag=0):
     if vol.dim() != 3 or not vol.is_contiguous():
         raise ValueError("volume must be a contiguous [nz][ny][nx] tensor")
     nz, ny, nx = vol.shape
     return tsa_problem(vol.data_ptr(), _dtype_code(vol), nx, ny, nz, bins, k, float(q),
                        OBJECTIVES.get(objective, objective), ENUMERATIONS.get(enumeration, enumeration),
-                       units)
+                       units, PIPELINES.get(pipeline, pipeline), slab_slices, label_lag)
 
 
 def tsa_version():
@@ -163,6 +171,11 @@ def tsa_version():
 
 def tsa_validate(problem):
     return int(load().tsa_validate(ctypes.byref(problem)))
+
+
+def tsa_pipeline_kind(problem):
+    """1 = fused persistent kernel, -1 = staged kernels, 0 = invalid."""
+    return int(load().tsa_pipeline_kind(ctypes.byref(problem)))
 
 
 def tsa_workspace_size(problem):
@@ -188,13 +201,14 @@ def workspace_for(problem, device):
 
 
 def tsa_segment(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0,
-                labels=True, out=None, workspace=None, stream=None):
+                labels=True, out=None, workspace=None, stream=None, pipeline="auto", slab_slices=0,
+                label_lag=0):
     """Whole path on the current stream.  Returns dict of device tensors:
     thresholds [nz,k] i32, objective [nz] f64, histogram [nz,bins] u32,
     status [nz] i32, labels [nz,ny,nx] u8 (or None)."""
     _need_cuda(vol)
     lib = load()
-    p = make_problem(vol, bins, k, q, objective, enumeration, units)
+    p = make_problem(vol, bins, k, q, objective, enumeration, units, pipeline, slab_slices, label_lag)
     nz = vol.shape[0]
     dev = vol.device
     if out is None:
@@ -291,7 +305,7 @@ def tsa_label(vol, thresholds, status=None, bins=None, stream=None):
 
 def tsa_segment_host(vol_host, bins, k, q, objective="pseudo_additive", enumeration="canonical",
                      units=0, slab=None, labels=True, scratch=None, streams=None, out=None,
-                     device=None):
+                     device=None, pipeline="auto"):
     """Host-buffer path: vol_host is a CPU (ideally pinned) torch tensor; copies
     in/out run inside the library, overlapped with compute on two streams.
     Returns dict of CPU tensors.  Blocks until done."""
@@ -299,7 +313,7 @@ def tsa_segment_host(vol_host, bins, k, q, objective="pseudo_additive", enumerat
         raise ValueError("tsa_segment_host takes a host tensor")
     device = device or torch.device("cuda", torch.cuda.current_device())
     lib = load()
-    p = make_problem(vol_host, bins, k, q, objective, enumeration, units)
+    p = make_problem(vol_host, bins, k, q, objective, enumeration, units, pipeline)
     nz = vol_host.shape[0]
     slab = slab or max(1, min(nz, 32))
     if out is None:

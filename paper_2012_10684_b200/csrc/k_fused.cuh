@@ -1,0 +1,433 @@
+// k_fused.cuh -- the whole hot path as ONE
+// persistent kernel for k <= 2, bins <= 1024, canonical enumeration (the c1/c2
+// workloads).  Separate kernels leave the GPU idle between phases: the
+// histogram is bound by shared-memory atomics, the per-slice search/finalize
+// by latency, the labelling by HBM.  Here they overlap.
+//
+// Task queue (claimed in order with one global atomic; every dependency points
+// to an earlier queue position, so a CTA waiting on one waits on a task some
+// running CTA already holds -- no deadlock):
+//   LUT tasks                               1/n^q table chunks
+//   round r = 0 .. nslab + DL - 1:
+//     H(r)       slab r: (slice, chunk) histogram partials (no atomics to HBM)
+//     M(r - 1)   slab r-1: per slice, sum partials -> histogram, prefix tables,
+//                exhaustive search, argmax, phi(t*) in the definition's order
+//     L(r - DL)  slab r-DL: (slice, chunk) labels, DL rounds behind so M is
+//                done; the slab's voxels are still in L2 (126 MB), so the
+//                label pass re-reads them from L2, not HBM.
+// Completion counters (hdone[z], mdone[z], lutdone) use release/acquire
+// (__threadfence + atomic / volatile poll + __threadfence).
+#pragma once
+#include <cstdint>
+
+#include "k_label.cuh"
+#include "tsa_device.cuh"
+
+namespace tsa {
+
+struct FusedArgs {
+  const uint8_t *vol;
+  int dtype_bytes;
+  int64_t n;  // voxels per slice
+  int64_t nz;
+  int L, k;
+  double q;
+  int mode;
+  // outputs
+  int32_t *thresholds;  // [nz][k]
+  double *objective;    // [nz] or null
+  uint32_t *hist;       // [nz][L]
+  int32_t *status;      // [nz]
+  int32_t *status2;     // [nz] or null (user copy)
+  uint8_t *labels;      // [nz][n] or null
+  // workspace
+  uint32_t *partial;    // [nz][HC][L]
+  int32_t *povf;        // [nz][HC]
+  double *ipow;         // [N+1]
+  double *lnn, *rcp;
+  int32_t *counters;    // [0] head, [1] lutdone, [2 .. 2+nz) hdone, [2+nz .. 2+2nz) mdone
+  Luts luts;
+  // schedule
+  int HC, LC, SB, DL, nslab, nlut;
+  int64_t lut_per;
+};
+
+__device__ __forceinline__ void wait_ge(const int32_t *p, int target) {
+  if (*((volatile const int32_t *)p) >= target) {
+    __threadfence();
+    return;
+  }
+  unsigned ns = 32;
+  while (*((volatile const int32_t *)p) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns *= 2;
+  }
+  __threadfence();
+}
+
+__device__ __forceinline__ void signal_add(int32_t *p, int v) {
+  __threadfence();
+  atomicAdd(p, v);
+}
+
+// ---------------------------------------------------------------- H task
+template <typename T>
+__device__ void fused_hist(const FusedArgs &g, int z, int c, uint32_t *sh) {
+  const int L = g.L;
+  const int warps = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < L * warps; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  uint32_t *bins = sh + (threadIdx.x >> 5) * L;
+  const T *slice = reinterpret_cast<const T *>(g.vol) + (size_t)z * g.n;
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t nvec = g.n / VEC;
+  const int64_t per = (nvec + g.HC - 1) / g.HC;
+  const int64_t v0 = per * c, v1 = min(nvec, v0 + per);
+  const uint4 *v4 = reinterpret_cast<const uint4 *>(slice);
+  int ovf = 0;
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+    const uint4 w = __ldg(v4 + i);  // default policy: keep in L2 for the label pass
+    if (sizeof(T) == 1 && L == 256) {
+      hist_word<T, false>(bins, w.x, L, ovf);
+      hist_word<T, false>(bins, w.y, L, ovf);
+      hist_word<T, false>(bins, w.z, L, ovf);
+      hist_word<T, false>(bins, w.w, L, ovf);
+    } else {
+      hist_word<T, true>(bins, w.x, L, ovf);
+      hist_word<T, true>(bins, w.y, L, ovf);
+      hist_word<T, true>(bins, w.z, L, ovf);
+      hist_word<T, true>(bins, w.w, L, ovf);
+    }
+  }
+  __shared__ int s_ovf;
+  if (threadIdx.x == 0) s_ovf = 0;
+  __syncthreads();
+  if (ovf) s_ovf = 1;
+  uint32_t *out = g.partial + ((size_t)z * g.HC + c) * L;
+  for (int b = threadIdx.x; b < L; b += blockDim.x) {
+    uint32_t s = 0;
+    for (int r = 0; r < warps; r++) s += sh[r * L + b];
+    out[b] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g.povf[(size_t)z * g.HC + c] = s_ovf;
+    signal_add(g.counters + 2 + z, 1);
+  }
+}
+
+// ---------------------------------------------------------------- L task
+template <typename T>
+__device__ void fused_label(const FusedArgs &g, int z, int c) {
+  if (threadIdx.x == 0) wait_ge(g.counters + 2 + g.nz + z, 1);
+  __syncthreads();
+  // data written by another CTA in this launch: read through L2 (__ldcg)
+  const bool ok = __ldcg(g.status + z) == kOK;
+  const int tmax = sizeof(T) == 1 ? 255 : 65535;
+  const int32_t *tz = g.thresholds + z * g.k;
+  const int t0 = __ldcg(tz), t1 = g.k > 1 ? __ldcg(tz + 1) : tmax;
+  const int64_t groups = g.n / 16;
+  const int64_t per = (groups + g.LC - 1) / g.LC;
+  const int64_t i0 = (int64_t)z * groups + per * c;
+  const int64_t i1 = (int64_t)z * groups + min(groups, per * (c + 1));
+  const uint4 *src = reinterpret_cast<const uint4 *>(g.vol);
+  uint4 *dst = reinterpret_cast<uint4 *>(g.labels);
+  const uint32_t b0 = (uint32_t)(t0 & 0xff) * 0x01010101u, b1 = (uint32_t)(t1 & 0xff) * 0x01010101u;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    if (sizeof(T) == 1) {
+      const uint4 w = __ldcs(src + i);
+      uint4 o = make_uint4(0u, 0u, 0u, 0u);
+      if (ok) {
+        o.x = (__vcmpgtu4(w.x, b0) & 0x01010101u) + (__vcmpgtu4(w.x, b1) & 0x01010101u);
+        o.y = (__vcmpgtu4(w.y, b0) & 0x01010101u) + (__vcmpgtu4(w.y, b1) & 0x01010101u);
+        o.z = (__vcmpgtu4(w.z, b0) & 0x01010101u) + (__vcmpgtu4(w.z, b1) & 0x01010101u);
+        o.w = (__vcmpgtu4(w.w, b0) & 0x01010101u) + (__vcmpgtu4(w.w, b1) & 0x01010101u);
+      }
+      __stcs(dst + i, o);
+    } else {
+      const uint4 wa = __ldcs(src + 2 * i), wb = __ldcs(src + 2 * i + 1);
+      const uint32_t ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+      uint32_t o[4] = {0u, 0u, 0u, 0u};
+      if (ok) {
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+          const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+          o[e >> 2] |= ((uint32_t)(v > t0) + (uint32_t)(v > t1)) << (8 * (e & 3));
+        }
+      }
+      __stcs(dst + i, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- M task
+// One CTA per slice: histogram from partials, prefix tables (canonical), the
+// exhaustive search for k <= 2, argmax, phi(t*) in the definition's order.
+template <int K, int MODE>
+__device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
+  const int L = g.L, E = L + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  uint32_t *hs = reinterpret_cast<uint32_t *>(smem);            // [L]
+  double *wsh = reinterpret_cast<double *>(hs + ((L + 1) & ~1)); // [L]
+  double *tWhi = wsh + L;                                       // [E]
+  double *tWlo = tWhi + E;                                      // [E]
+  double *Asuf = tWlo + E;                                      // [L]
+  double *fsh = Asuf + L;                                       // [L]
+  uint32_t *tC = reinterpret_cast<uint32_t *>(fsh + L);         // [E]
+  int32_t *tBin = reinterpret_cast<int32_t *>(tC + E);          // [E]
+  __shared__ int s_status, s_M;
+  __shared__ double s_red[32], s_P[kKMax + 1], s_S[kKMax + 1];
+  __shared__ uint64_t s_key[32];
+  if (tid == 0) {
+    wait_ge(g.counters + 1, g.nlut);
+    wait_ge(g.counters + 2 + z, g.HC);
+  }
+  __syncthreads();
+  // histogram = sum of chunk partials; overflow flag
+  int ovf = 0;
+  for (int c = tid; c < g.HC; c += blockDim.x) ovf |= __ldcg(g.povf + (size_t)z * g.HC + c);
+  if (tid == 0) s_status = 0;
+  __syncthreads();
+  if (ovf) s_status = kLevelOverflow;
+  for (int i = tid; i < L; i += blockDim.x) {
+    uint32_t s = 0;
+    for (int c = 0; c < g.HC; c++) s += __ldcg(g.partial + ((size_t)z * g.HC + c) * L + i);
+    hs[i] = s;
+    g.hist[(size_t)z * L + i] = s;
+    const double x = (double)s;
+    wsh[i] = s == 0 ? 0.0 : (g.luts.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q));
+  }
+  __syncthreads();
+  // prefix tables by warp 0 (same construction as k_scan, canonical)
+  if (warp == 0) {
+    const int per = (L + 31) / 32;
+    const int i0 = min(L, lane * per), i1 = min(L, i0 + per);
+    uint32_t m_l = 0, n_l = 0;
+    dd w_l = {0.0, 0.0};
+    for (int i = i0; i < i1; i++) {
+      const uint32_t c = hs[i];
+      if (c) {
+        m_l++;
+        n_l += c;
+        w_l = dd_add_d(w_l, wsh[i]);
+      }
+    }
+    uint32_t m_inc = m_l, n_inc = n_l;
+    dd w_inc = w_l;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t om = __shfl_up_sync(0xffffffffu, m_inc, off);
+      const uint32_t on = __shfl_up_sync(0xffffffffu, n_inc, off);
+      const double oh = __shfl_up_sync(0xffffffffu, w_inc.hi, off);
+      const double ol = __shfl_up_sync(0xffffffffu, w_inc.lo, off);
+      if (lane >= off) {
+        m_inc += om;
+        n_inc += on;
+        w_inc = dd_add({oh, ol}, w_inc);
+      }
+    }
+    const uint32_t m_tot = __shfl_sync(0xffffffffu, m_inc, 31);
+    dd w_ex;
+    w_ex.hi = __shfl_up_sync(0xffffffffu, w_inc.hi, 1);
+    w_ex.lo = __shfl_up_sync(0xffffffffu, w_inc.lo, 1);
+    if (lane == 0) {
+      tC[0] = 0;
+      tWhi[0] = 0.0;
+      tWlo[0] = 0.0;
+      tBin[0] = -1;
+    }
+    uint32_t e = m_inc - m_l + 1, ncum = n_inc - n_l;
+    dd wl = {0.0, 0.0};
+    for (int i = i0; i < i1; i++) {
+      const uint32_t c = hs[i];
+      if (c) {
+        ncum += c;
+        wl = dd_add_d(wl, wsh[i]);
+        const dd W = lane == 0 ? wl : dd_add(w_ex, wl);
+        tC[e] = ncum;
+        tWhi[e] = W.hi;
+        tWlo[e] = W.lo;
+        tBin[e] = i;
+        e++;
+      }
+    }
+    if (lane == 0) {
+      s_M = (int)m_tot;
+      if (s_status == kOK && (int)m_tot < K + 1) s_status = kNoValidSplit;
+    }
+  }
+  __syncthreads();
+  const int M = s_M;
+  int st = s_status;
+  const SliceTables t{tC, tWhi, tWlo, Asuf};
+  double best = -CUDART_INF;
+  uint64_t key = kKeyNone;
+  if (st == kOK) {
+    for (int i = tid; i <= M - 2; i += blockDim.x) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
+    __syncthreads();
+    // search: rows a (k = 2) or the single row a = -1 (k = 1); warps over rows,
+    // lanes over b, lex order per lane, strict '>' (lowest tuple on ties)
+    int brow = -1, bb = -1;
+    const int nrows = K == 1 ? 1 : M - 1;
+    for (int r = warp; r < nrows; r += nw) {
+      const int a = K == 1 ? -1 : r;
+      if (a > M - 3) continue;
+      const double pre = K == 1 ? (MODE == SUM ? 0.0 : 1.0)
+                                : combine<MODE>(MODE == SUM ? 0.0 : 1.0, class_term<MODE>(t, g.luts, 0, a));
+      for (int b = a + 1 + lane; b <= M - 2; b += 32) {
+        double v = combine<MODE>(pre, combine<MODE>(class_term<MODE>(t, g.luts, a + 1, b), Asuf[b]));
+        if (MODE == PROD_MIN) v = -v;
+        if (v > best) {
+          best = v;
+          brow = a;
+          bb = b;
+        }
+      }
+    }
+    if (bb >= 0) key = K == 1 ? (uint64_t)tBin[bb + 1]
+                              : (((uint64_t)tBin[brow + 1]) << 12) | (uint64_t)tBin[bb + 1];
+  }
+  warp_argmax(best, key);
+  if (lane == 0) {
+    s_red[warp] = best;
+    s_key[warp] = key;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    best = lane < nw ? s_red[lane] : -CUDART_INF;
+    key = lane < nw ? s_key[lane] : kKeyNone;
+    warp_argmax(best, key);
+    if (lane == 0) {
+      if (st == kOK && key == kKeyNone) st = kNoValidSplit;
+      s_status = st;
+      s_key[0] = key;
+    }
+  }
+  __syncthreads();
+  st = s_status;
+  key = s_key[0];
+  int32_t *thr = g.thresholds + (size_t)z * g.k;
+  if (st != kOK) {
+    if (tid < g.k) thr[tid] = -1;
+    if (tid == 0) {
+      if (g.objective) g.objective[z] = CUDART_NAN;
+      g.status[z] = st;
+      if (g.status2) g.status2[z] = st;
+    }
+  } else {
+    const int t0 = (int)((key >> (12 * (K - 1))) & 0xFFFull);
+    const int t1 = K > 1 ? (int)(key & 0xFFFull) : L;
+    if (tid < K) thr[tid] = tid == 0 ? t0 : t1;
+    // phi(t*) in the definition's order (k_finalize): p over the canonical list
+    if (g.objective) {
+      // N = total count (the last prefix count; exact)
+      const double N = (double)tC[M];
+      for (int j = tid; j < M; j += blockDim.x) fsh[j] = __ddiv_rn((double)(tC[j + 1] - tC[j]), N);
+      __syncthreads();
+      // class c = list range [s_c, e_c)
+      int cls_start[kKMax + 2];
+      {
+        int c = 0;
+        cls_start[0] = 0;
+        // boundaries: first list index with bin > t_c
+        // (lists are short; every thread computes them)
+        int j = 0;
+        for (c = 0; c < K; c++) {
+          const int tc = c == 0 ? t0 : t1;
+          while (j < M && tBin[j + 1] <= tc) j++;
+          cls_start[c + 1] = j;
+        }
+        cls_start[K + 1] = M;
+      }
+      if (tid <= K) {
+        double P = 0.0;
+        for (int j = cls_start[tid]; j < cls_start[tid + 1]; j++) P = __dadd_rn(P, fsh[j]);
+        s_P[tid] = P;
+      }
+      __syncthreads();
+      const bool shannon = g.luts.shannon;
+      for (int j = tid; j < M; j += blockDim.x) {
+        const int cls = (tBin[j + 1] > t0) + (K > 1 && tBin[j + 1] > t1);
+        const double r = __ddiv_rn(fsh[j], s_P[cls]);
+        fsh[j] = shannon ? __dmul_rn(r, log(r)) : pow(r, g.q);
+      }
+      __syncthreads();
+      if (tid <= K) {
+        double A = 0.0;
+        for (int j = cls_start[tid]; j < cls_start[tid + 1]; j++)
+          A = shannon ? __dsub_rn(A, fsh[j]) : __dadd_rn(A, fsh[j]);
+        s_S[tid] = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(g.q, 1.0));
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double phi = s_S[0];
+        for (int j = 1; j <= K; j++)
+          phi = __dadd_rn(__dadd_rn(phi, s_S[j]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, g.q), phi), s_S[j]));
+        g.objective[z] = phi;
+      }
+    }
+    if (tid == 0) {
+      g.status[z] = kOK;
+      if (g.status2) g.status2[z] = kOK;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) signal_add(g.counters + 2 + g.nz + z, 1);
+}
+
+template <typename T, int K, int MODE>
+__global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
+  extern __shared__ __align__(16) char fsm[];
+  __shared__ int s_task;
+  const int nH = g.SB * g.HC, nM = g.SB, nL = g.SB * g.LC;
+  const int round = nH + nM + nL;
+  const int64_t total = (int64_t)g.nlut + (int64_t)(g.nslab + g.DL) * round;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(g.counters, 1);
+    __syncthreads();
+    const int64_t task = s_task;
+    __syncthreads();
+    if (task >= total) break;
+    if (task < g.nlut) {
+      const int64_t N = g.n;
+      const int64_t a = task * g.lut_per, b = min(N + 1, a + g.lut_per);
+      for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
+        const double x = (double)m;
+        if (g.luts.shannon) {
+          g.lnn[m] = m == 0 ? CUDART_NAN : log(x);
+          g.rcp[m] = m == 0 ? CUDART_NAN : __drcp_rn(x);
+        } else {
+          g.ipow[m] = m == 0 ? CUDART_NAN : __drcp_rn(pow(x, g.q));
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) signal_add(g.counters + 1, 1);
+      continue;
+    }
+    const int64_t rt = task - g.nlut;
+    const int r = (int)(rt / round);
+    const int off = (int)(rt % round);
+    if (off < nH) {
+      const int slab = r;
+      if (slab >= g.nslab) continue;
+      const int z = slab * g.SB + off / g.HC;
+      if (z >= g.nz) continue;
+      fused_hist<T>(g, z, off % g.HC, reinterpret_cast<uint32_t *>(fsm));
+    } else if (off < nH + nM) {
+      const int slab = r - 1;
+      if (slab < 0 || slab >= g.nslab) continue;
+      const int z = slab * g.SB + (off - nH);
+      if (z >= g.nz) continue;
+      fused_mid<K, MODE>(g, z, fsm);
+    } else {
+      const int slab = r - g.DL;
+      if (slab < 0 || slab >= g.nslab) continue;
+      const int o = off - nH - nM;
+      const int z = slab * g.SB + o / g.LC;
+      if (z >= g.nz) continue;
+      if (g.labels) fused_label<T>(g, z, o % g.LC);
+    }
+  }
+}
+
+}  // namespace tsa

@@ -13,6 +13,7 @@
 
 #include "tsa.h"
 #include "tsa_kernels.cuh"
+#include "k_fused.cuh"
 
 namespace {
 
@@ -260,20 +261,126 @@ struct SegWs {
   uint64_t *pk;
   char *search;
   size_t search_bytes;
+  // fused pipeline
+  uint32_t *partial;
+  int32_t *povf;
+  int32_t *counters;
+  double *luts;
 };
+
+// fused-pipeline constants (tuned on B200, profiles/)
+constexpr int kFusedHC = 4;   // histogram chunks per slice
+constexpr int kFusedLC = 4;   // label chunks per slice
+constexpr int kFusedThreads = 512;
+
+static bool fused_eligible(const tsa_problem *p) {
+  const int64_t n = p->nx * p->ny;
+  return p->k <= 2 && p->bins <= 1024 && p->enumeration == TSA_ENUM_CANONICAL &&
+         p->objective == TSA_OBJ_PSEUDO_ADDITIVE && n % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(p->volume) & 15) == 0;
+}
 
 static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
   Carve c{base};
   const int32_t U = units_of(p);
-  uint32_t *hist = c.take<uint32_t>((size_t)p->nz * p->bins);
-  int32_t *status = c.take<int32_t>((size_t)p->nz);
-  double *ps = c.take<double>((size_t)U * p->nz);
-  uint64_t *pk = c.take<uint64_t>((size_t)U * p->nz);
-  const size_t sb = tsa_search_workspace_size(p->nz, p->nx * p->ny, p->bins, p->k, p->q,
-                                              p->objective, p->enumeration);
-  char *search = c.take<char>(sb);
-  if (o) *o = SegWs{hist, status, ps, pk, search, sb};
+  SegWs w;
+  w.hist = c.take<uint32_t>((size_t)p->nz * p->bins);
+  w.status = c.take<int32_t>((size_t)p->nz);
+  w.ps = c.take<double>((size_t)U * p->nz);
+  w.pk = c.take<uint64_t>((size_t)U * p->nz);
+  w.search_bytes = tsa_search_workspace_size(p->nz, p->nx * p->ny, p->bins, p->k, p->q,
+                                             p->objective, p->enumeration);
+  w.search = c.take<char>(w.search_bytes);
+  w.partial = c.take<uint32_t>((size_t)p->nz * kFusedHC * p->bins);
+  w.povf = c.take<int32_t>((size_t)p->nz * kFusedHC);
+  w.counters = c.take<int32_t>(2 + 2 * (size_t)p->nz);
+  w.luts = c.take<double>(2 * ((size_t)p->nx * p->ny + 1));
+  if (o) *o = w;
   return c.off;
+}
+
+}  // extern "C"
+
+template <typename T, int K>
+static void launch_fused_k(const tsa::FusedArgs &a, int mode, size_t smem, int grid, cudaStream_t s) {
+  switch (mode) {
+    case tsa::PROD_MAX: {
+      auto f = tsa::k_fused<T, K, tsa::PROD_MAX>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      f<<<grid, kFusedThreads, smem, s>>>(a);
+    } break;
+    case tsa::PROD_MIN: {
+      auto f = tsa::k_fused<T, K, tsa::PROD_MIN>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      f<<<grid, kFusedThreads, smem, s>>>(a);
+    } break;
+    default: {
+      auto f = tsa::k_fused<T, K, tsa::SUM>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      f<<<grid, kFusedThreads, smem, s>>>(a);
+    } break;
+  }
+}
+
+extern "C" {
+
+static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, const SegWs &w,
+                                cudaStream_t s) {
+  const int64_t N = p->nx * p->ny;
+  const bool shannon = p->q == 1.0;
+  tsa::FusedArgs a;
+  a.vol = reinterpret_cast<const uint8_t *>(p->volume);
+  a.dtype_bytes = p->dtype == TSA_U8 ? 1 : 2;
+  a.n = N;
+  a.nz = p->nz;
+  a.L = p->bins;
+  a.k = p->k;
+  a.q = p->q;
+  a.mode = search_mode(p->q, p->objective);
+  a.thresholds = out->thresholds;
+  a.objective = out->objective;
+  a.hist = out->histogram ? out->histogram : w.hist;
+  a.status = w.status;
+  a.status2 = out->slice_status;
+  a.labels = out->labels;
+  a.partial = w.partial;
+  a.povf = w.povf;
+  a.counters = w.counters;
+  a.ipow = shannon ? nullptr : w.luts;
+  a.lnn = shannon ? w.luts : nullptr;
+  a.rcp = shannon ? w.luts + (N + 1) : nullptr;
+  a.luts.ipow = a.ipow;
+  a.luts.lnn = a.lnn;
+  a.luts.rcp = a.rcp;
+  a.luts.iqm1 = shannon ? 0.0 : 1.0 / (p->q - 1.0);
+  a.luts.omq = 1.0 - p->q;
+  a.luts.shannon = shannon;
+  a.HC = kFusedHC;
+  a.LC = kFusedLC;
+  a.SB = p->slab_slices > 0 ? p->slab_slices : 16;
+  a.DL = p->label_lag > 0 ? std::max(2, p->label_lag) : 6;
+  a.nslab = (int)((p->nz + a.SB - 1) / a.SB);
+  a.lut_per = 4096;
+  a.nlut = (int)((N + 1 + a.lut_per - 1) / a.lut_per);
+  TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
+  const int L = p->bins, E = L + 1;
+  const size_t smem_h = (size_t)(kFusedThreads / 32) * L * sizeof(uint32_t);
+  const size_t smem_m = (size_t)((L + 1) & ~1) * 4 + (size_t)L * 8 * 3 + (size_t)E * 8 * 2 + (size_t)E * 8;
+  const size_t smem = std::max(smem_h, smem_m) + 64;
+  const int grid = g_num_sms() * 2;
+  if (p->dtype == TSA_U8) {
+    if (p->k == 1) launch_fused_k<uint8_t, 1>(a, a.mode, smem, grid, s);
+    else launch_fused_k<uint8_t, 2>(a, a.mode, smem, grid, s);
+  } else {
+    if (p->k == 1) launch_fused_k<uint16_t, 1>(a, a.mode, smem, grid, s);
+    else launch_fused_k<uint16_t, 2>(a, a.mode, smem, grid, s);
+  }
+  return check_cuda("k_fused");
+}
+
+int32_t tsa_pipeline_kind(const tsa_problem *p) {
+  if (tsa_validate(p) != TSA_OK) return 0;
+  return (p->pipeline >= 0 && fused_eligible(p)) ? 1 : -1;
 }
 
 size_t tsa_workspace_size(const tsa_problem *p) {
@@ -512,6 +619,9 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   const size_t need = carve_segment(p, reinterpret_cast<char *>(workspace), &w);
   if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = S(stream);
+  const bool labels_aligned = !out->labels || (reinterpret_cast<uintptr_t>(out->labels) & 15) == 0;
+  if (p->pipeline >= 0 && fused_eligible(p) && labels_aligned) return segment_fused(p, out, w, s);
+  if (p->pipeline > 0) return set_error(TSA_ERR_INVALID_ARG, "pipeline=fused but the problem is not eligible");
   uint32_t *hist = out->histogram ? out->histogram : w.hist;
   const int32_t U = units_of(p);
   TSA_TRY(tsa_histogram(p, hist, w.status, stream));

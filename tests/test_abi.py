@@ -51,7 +51,7 @@ def test_version_and_strings(lib):
 
 
 def _p(**kw):
-    base = dict(volume=1, dtype=1, nx=512, ny=512, nz=300, bins=256, k=2, q=0.8, objective=0,
+    base = dict(volume=256, dtype=1, nx=512, ny=512, nz=300, bins=256, k=2, q=0.8, objective=0,
                 enumeration=0, units_per_slice=0)
     base.update(kw)
     return tsa_problem(**base)
@@ -74,6 +74,16 @@ def test_invalid_arguments_rejected_synchronously(lib, kw):
     assert lib.tsa_histogram(ctypes.byref(p), ctypes.c_void_p(1), ctypes.c_void_p(1), None) == 1
     assert lib.tsa_label(ctypes.byref(p), ctypes.c_void_p(1), None, ctypes.c_void_p(1), None) == 1
     assert len(lib.tsa_last_error()) > 0
+
+
+def test_pipeline_kind(lib):
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p())) == 1            # c2: fused
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(k=3))) == -1        # k >= 3: staged
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=-1))) == -1
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(enumeration=1))) == -1
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024))) == -1
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(nx=37, ny=53))) == -1  # n % 16 != 0
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(q=0.0))) == 0
 
 
 def test_valid_problems_and_workspace(lib):

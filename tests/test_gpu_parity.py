@@ -318,3 +318,48 @@ def test_cuda_graph_capture():
     torch.cuda.synchronize()
     for key in ref:
         assert torch.equal(out[key], ref[key]), key
+
+
+# ------------------------------------------- fused pipeline == staged kernels
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("q", [0.5, 0.8, 1.0, 1.3])
+def test_fused_pipeline_bitexact_vs_staged(k, q):
+    """The persistent fused kernel (k <= 2) and the one-kernel-per-stage path
+    produce bit-identical histograms, thresholds, objectives, status and labels."""
+    cfg = phantom.CONFIGS["c2"]
+    vol = to_dev(phantom.make_volume(cfg, nz=37, z_first=20))
+    a = tsa.tsa_segment(vol, 256, k, q, pipeline="fused", slab_slices=4, label_lag=2)
+    b = tsa.tsa_segment(vol, 256, k, q, pipeline="staged")
+    torch.cuda.synchronize()
+    for key in ("histogram", "thresholds", "status", "labels"):
+        assert torch.equal(a[key], b[key]), key
+    assert torch.equal(a["objective"].view(torch.int64), b["objective"].view(torch.int64))
+
+
+def test_fused_pipeline_parity_and_errors():
+    """Fused path vs oracle, including overflow and no-valid-split slices."""
+    vol = phantom.make_volume(phantom.CONFIGS["c2"], nz=12, z_first=150).copy()
+    vol[3] = 77                      # constant slice: NO_VALID_SPLIT
+    vol[5, 10, 10] = 255             # fine for bins = 256
+    out = tsa.tsa_segment(to_dev(vol), 256, 2, 0.8, pipeline="fused", slab_slices=5, label_lag=3)
+    torch.cuda.synchronize()
+    st = out["status"].cpu().numpy()
+    assert st[3] == 3
+    run_and_check(vol, 256, 2, 0.8)   # auto = fused for this shape
+    # overflow (u16 data above bins) through the fused path
+    v16 = (vol.astype(np.uint16) * 3)
+    v16[7, 0, 0] = 1000
+    out = tsa.tsa_segment(to_dev(v16), 1000, 1, 0.8, pipeline="fused")
+    torch.cuda.synchronize()
+    assert out["status"].cpu().numpy()[7] == 2
+    run_and_check(v16, 1000, 1, 0.8)
+
+
+@pytest.mark.parametrize("sb,dl", [(1, 2), (3, 2), (16, 6), (64, 9)])
+def test_fused_schedule_invariance(sb, dl):
+    vol = to_dev(phantom.make_volume(phantom.CONFIGS["c2"], nz=50, z_first=100))
+    ref = tsa.tsa_segment(vol, 256, 2, 0.8, pipeline="staged")
+    out = tsa.tsa_segment(vol, 256, 2, 0.8, pipeline="fused", slab_slices=sb, label_lag=dl)
+    torch.cuda.synchronize()
+    for key in ("histogram", "thresholds", "labels", "status"):
+        assert torch.equal(out[key], ref[key]), key

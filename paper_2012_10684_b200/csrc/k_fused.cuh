@@ -20,7 +20,9 @@
 #pragma once
 #include <cstdint>
 
+#include "k_histogram.cuh"
 #include "k_label.cuh"
+#include "k_search.cuh"
 #include "tsa_device.cuh"
 
 namespace tsa {
@@ -85,18 +87,29 @@ __device__ void fused_hist(const FusedArgs &g, int z, int c, uint32_t *sh) {
   const int64_t v0 = per * c, v1 = min(nvec, v0 + per);
   const uint4 *v4 = reinterpret_cast<const uint4 *>(slice);
   int ovf = 0;
-  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
-    const uint4 w = __ldg(v4 + i);  // default policy: keep in L2 for the label pass
-    if (sizeof(T) == 1 && L == 256) {
-      hist_word<T, false>(bins, w.x, L, ovf);
-      hist_word<T, false>(bins, w.y, L, ovf);
-      hist_word<T, false>(bins, w.z, L, ovf);
-      hist_word<T, false>(bins, w.w, L, ovf);
-    } else {
-      hist_word<T, true>(bins, w.x, L, ovf);
-      hist_word<T, true>(bins, w.y, L, ovf);
-      hist_word<T, true>(bins, w.z, L, ovf);
-      hist_word<T, true>(bins, w.w, L, ovf);
+  const bool nocheck = sizeof(T) == 1 && L == 256;
+  constexpr int U = 4;  // 4 x 16-byte loads in flight per thread
+  for (int64_t i0 = v0 + threadIdx.x; i0 < v1; i0 += (int64_t)U * blockDim.x) {
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      w[u] = i < v1 ? __ldg(v4 + i) : make_uint4(0u, 0u, 0u, 0u);  // default policy: stays in L2
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (i0 + (int64_t)u * blockDim.x >= v1) break;
+      if (nocheck) {
+        hist_word<T, false>(bins, w[u].x, L, ovf);
+        hist_word<T, false>(bins, w[u].y, L, ovf);
+        hist_word<T, false>(bins, w[u].z, L, ovf);
+        hist_word<T, false>(bins, w[u].w, L, ovf);
+      } else {
+        hist_word<T, true>(bins, w[u].x, L, ovf);
+        hist_word<T, true>(bins, w[u].y, L, ovf);
+        hist_word<T, true>(bins, w[u].z, L, ovf);
+        hist_word<T, true>(bins, w[u].w, L, ovf);
+      }
     }
   }
   __shared__ int s_ovf;
@@ -118,7 +131,47 @@ __device__ void fused_hist(const FusedArgs &g, int z, int c, uint32_t *sh) {
 
 // ---------------------------------------------------------------- L task
 template <typename T>
+__device__ __forceinline__ uint4 label16(const uint4 *src, int64_t i, bool ok, int t0, int t1,
+                                         uint32_t b0, uint32_t b1) {
+  if (sizeof(T) == 1) {
+    const uint4 w = __ldcs(src + i);
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (ok) {
+      o.x = (__vcmpgtu4(w.x, b0) & 0x01010101u) + (__vcmpgtu4(w.x, b1) & 0x01010101u);
+      o.y = (__vcmpgtu4(w.y, b0) & 0x01010101u) + (__vcmpgtu4(w.y, b1) & 0x01010101u);
+      o.z = (__vcmpgtu4(w.z, b0) & 0x01010101u) + (__vcmpgtu4(w.z, b1) & 0x01010101u);
+      o.w = (__vcmpgtu4(w.w, b0) & 0x01010101u) + (__vcmpgtu4(w.w, b1) & 0x01010101u);
+    }
+    return o;
+  } else {
+    const uint4 wa = __ldcs(src + 2 * i), wb = __ldcs(src + 2 * i + 1);
+    const uint32_t ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+        o[e >> 2] |= ((uint32_t)(v > t0) + (uint32_t)(v > t1)) << (8 * (e & 3));
+      }
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+template <typename T>
 __device__ void fused_label(const FusedArgs &g, int z, int c) {
+  const int64_t groups = g.n / 16;
+  const int64_t per = (groups + g.LC - 1) / g.LC;
+  const int64_t i0 = (int64_t)z * groups + per * c;
+  const int64_t i1 = (int64_t)z * groups + min(groups, per * (c + 1));
+  const uint4 *src = reinterpret_cast<const uint4 *>(g.vol);
+  uint4 *dst = reinterpret_cast<uint4 *>(g.labels);
+  // touch this thread's first input vectors before waiting (the volume does
+  // not depend on the search): the wait then overlaps the L2 latency
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += 4 * (int64_t)blockDim.x) {
+    if (sizeof(T) == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + i));
+    else asm volatile("prefetch.global.L1 [%0];" ::"l"(src + 2 * i));
+  }
   if (threadIdx.x == 0) wait_ge(g.counters + 2 + g.nz + z, 1);
   __syncthreads();
   // data written by another CTA in this launch: read through L2 (__ldcg)
@@ -126,36 +179,19 @@ __device__ void fused_label(const FusedArgs &g, int z, int c) {
   const int tmax = sizeof(T) == 1 ? 255 : 65535;
   const int32_t *tz = g.thresholds + z * g.k;
   const int t0 = __ldcg(tz), t1 = g.k > 1 ? __ldcg(tz + 1) : tmax;
-  const int64_t groups = g.n / 16;
-  const int64_t per = (groups + g.LC - 1) / g.LC;
-  const int64_t i0 = (int64_t)z * groups + per * c;
-  const int64_t i1 = (int64_t)z * groups + min(groups, per * (c + 1));
-  const uint4 *src = reinterpret_cast<const uint4 *>(g.vol);
-  uint4 *dst = reinterpret_cast<uint4 *>(g.labels);
   const uint32_t b0 = (uint32_t)(t0 & 0xff) * 0x01010101u, b1 = (uint32_t)(t1 & 0xff) * 0x01010101u;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    if (sizeof(T) == 1) {
-      const uint4 w = __ldcs(src + i);
-      uint4 o = make_uint4(0u, 0u, 0u, 0u);
-      if (ok) {
-        o.x = (__vcmpgtu4(w.x, b0) & 0x01010101u) + (__vcmpgtu4(w.x, b1) & 0x01010101u);
-        o.y = (__vcmpgtu4(w.y, b0) & 0x01010101u) + (__vcmpgtu4(w.y, b1) & 0x01010101u);
-        o.z = (__vcmpgtu4(w.z, b0) & 0x01010101u) + (__vcmpgtu4(w.z, b1) & 0x01010101u);
-        o.w = (__vcmpgtu4(w.w, b0) & 0x01010101u) + (__vcmpgtu4(w.w, b1) & 0x01010101u);
-      }
-      __stcs(dst + i, o);
-    } else {
-      const uint4 wa = __ldcs(src + 2 * i), wb = __ldcs(src + 2 * i + 1);
-      const uint32_t ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-      uint32_t o[4] = {0u, 0u, 0u, 0u};
-      if (ok) {
+  constexpr int U = 4;
+  for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += (int64_t)U * blockDim.x) {
+    uint4 o[U];
 #pragma unroll
-        for (int e = 0; e < 16; e++) {
-          const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          o[e >> 2] |= ((uint32_t)(v > t0) + (uint32_t)(v > t1)) << (8 * (e & 3));
-        }
-      }
-      __stcs(dst + i, make_uint4(o[0], o[1], o[2], o[3]));
+    for (int u = 0; u < U; u++) {
+      const int64_t i = ib + (int64_t)u * blockDim.x;
+      if (i < i1) o[u] = label16<T>(src, i, ok, t0, t1, b0, b1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = ib + (int64_t)u * blockDim.x;
+      if (i < i1) __stcs(dst + i, o[u]);
     }
   }
 }
@@ -265,27 +301,14 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   if (st == kOK) {
     for (int i = tid; i <= M - 2; i += blockDim.x) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
     __syncthreads();
-    // search: rows a (k = 2) or the single row a = -1 (k = 1); warps over rows,
-    // lanes over b, lex order per lane, strict '>' (lowest tuple on ties)
-    int brow = -1, bb = -1;
-    const int nrows = K == 1 ? 1 : M - 1;
-    for (int r = warp; r < nrows; r += nw) {
-      const int a = K == 1 ? -1 : r;
-      if (a > M - 3) continue;
-      const double pre = K == 1 ? (MODE == SUM ? 0.0 : 1.0)
-                                : combine<MODE>(MODE == SUM ? 0.0 : 1.0, class_term<MODE>(t, g.luts, 0, a));
-      for (int b = a + 1 + lane; b <= M - 2; b += 32) {
-        double v = combine<MODE>(pre, combine<MODE>(class_term<MODE>(t, g.luts, a + 1, b), Asuf[b]));
-        if (MODE == PROD_MIN) v = -v;
-        if (v > best) {
-          best = v;
-          brow = a;
-          bb = b;
-        }
-      }
-    }
-    if (bb >= 0) key = K == 1 ? (uint64_t)tBin[bb + 1]
-                              : (((uint64_t)tBin[brow + 1]) << 12) | (uint64_t)tBin[bb + 1];
+    // Apre[a] = T(0, a) in fsh (free until the finalize step)
+    if (K == 2)
+      for (int i = tid; i <= M - 2; i += blockDim.x) fsh[i] = class_term<MODE>(t, g.luts, 0, i);
+    __syncthreads();
+    // exhaustive search over all C(M-1, K) tuples, tuple-parallel over the CTA
+    search_flat_k12<K, MODE>(t, fsh, g.luts, tBin, M, 0, binom((uint64_t)(M - 1), K), tid,
+                             blockDim.x, best, key);
+    __syncthreads();  // fsh is reused below
   }
   warp_argmax(best, key);
   if (lane == 0) {
@@ -378,15 +401,19 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
 template <typename T, int K, int MODE>
 __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
-  __shared__ int s_task;
   const int nH = g.SB * g.HC, nM = g.SB, nL = g.SB * g.LC;
   const int round = nH + nM + nL;
   const int64_t total = (int64_t)g.nlut + (int64_t)(g.nslab + g.DL) * round;
+  __shared__ int s_next;
+  if (threadIdx.x == 0) s_next = atomicAdd(g.counters, 1);
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(g.counters, 1);
     __syncthreads();
-    const int64_t task = s_task;
+    const int64_t task = s_next;
     __syncthreads();
+    // claim the following task now; its latency hides behind this one (a
+    // claimed-but-unstarted task only follows tasks this CTA already runs,
+    // so the dependency order still rules out deadlock)
+    if (threadIdx.x == 0 && task < total) s_next = atomicAdd(g.counters, 1);
     if (task >= total) break;
     if (task < g.nlut) {
       const int64_t N = g.n;

@@ -306,3 +306,120 @@ __global__ void __launch_bounds__(256) k_search_rows(SearchArgs g) {
 }
 
 }  // namespace tsa
+
+namespace tsa {
+
+// Flattened exhaustive search for k <= 2 (pseudo-additive or q == 1): the
+// tuples (a, b), a < b (k = 2; colex rank C(b,2) + a) or (b) (k = 1) of ranks
+// [r0, r1) are dealt to threads; each thread evaluates B independent tuples at
+// a time so their 1/n^q gathers overlap (a row-by-row walk serialises them).
+// Value (same expression tree as k_search): v = (1 (x) Apre[a]) (x)
+// (T(a+1, b) (x) Asuf[b]), Apre[a] = T(0, a).  Per-thread order is not lex, so
+// every candidate is compared under the full (score, key) order.
+template <int K, int MODE>
+__device__ __forceinline__ void search_flat_k12(const SliceTables &t, const double *Apre,
+                                                const Luts &l, const int32_t *bin, int M,
+                                                uint64_t r0, uint64_t r1, uint64_t tid,
+                                                uint64_t nth, double &best, uint64_t &bestkey) {
+  constexpr int B = 4;
+  const double ident = MODE == SUM ? 0.0 : 1.0;
+  for (uint64_t rb = r0 + tid; rb < r1; rb += nth * B) {
+    int aa[B], bb[B];
+    bool ok[B];
+#pragma unroll
+    for (int u = 0; u < B; u++) {
+      const uint64_t r = rb + u * nth;
+      ok[u] = r < r1;
+      if (K == 1) {
+        aa[u] = -1;
+        bb[u] = ok[u] ? (int)r : 0;
+      } else {
+        int b = 1, a = 0;
+        if (ok[u]) {
+          b = (int)((1.0 + sqrt(1.0 + 8.0 * (double)r)) * 0.5);
+          while (b > 1 && binom((uint64_t)b, 2) > r) b--;
+          while (binom((uint64_t)b + 1, 2) <= r) b++;
+          a = (int)(r - binom((uint64_t)b, 2));
+        }
+        aa[u] = a;
+        bb[u] = b;
+      }
+    }
+    double v[B];
+#pragma unroll
+    for (int u = 0; u < B; u++) {
+      const double R = combine<MODE>(class_term<MODE>(t, l, aa[u] + 1, bb[u]), t.Asuf[bb[u]]);
+      const double pre = K == 1 ? ident : combine<MODE>(ident, Apre[aa[u]]);
+      v[u] = combine<MODE>(pre, R);
+      if (MODE == PROD_MIN) v[u] = -v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < B; u++) {
+      if (ok[u] && v[u] >= best) {
+        const uint64_t key = K == 1 ? (uint64_t)bin[bb[u] + 1]
+                                    : ((uint64_t)bin[aa[u] + 1] << 12) | (uint64_t)bin[bb[u] + 1];
+        if (better(v[u], key, best, bestkey)) {
+          best = v[u];
+          bestkey = key;
+        }
+      }
+    }
+  }
+}
+
+// Staged-path kernel for k <= 2 (not sum-plus-product): CTA (unit, slice)
+// stages the slice tables and Apre in shared memory, then searches its
+// tuple-rank range [T*u/U, T*(u+1)/U) with search_flat_k12.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) k_search_flat(SearchArgs g) {
+  extern __shared__ double ssh[];
+  const int z = blockIdx.y;
+  const int u = g.unit_begin + blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double best = -CUDART_INF;
+  uint64_t bestkey = kKeyNone;
+  const int st = g.status[z];
+  const int M = g.Mz[z];
+  const int P = M - 1;
+  if (st == kOK && P >= K) {
+    SliceTables t{g.C + (size_t)z * g.E, g.Whi + (size_t)z * g.E, g.Wlo + (size_t)z * g.E,
+                  g.Asuf + (size_t)z * g.L};
+    double *sWhi = ssh, *sWlo = ssh + g.E, *sAsuf = ssh + 2 * g.E, *sApre = ssh + 2 * g.E + g.L;
+    uint32_t *sC = reinterpret_cast<uint32_t *>(ssh + 2 * g.E + 2 * g.L);
+    for (int i = threadIdx.x; i <= M; i += blockDim.x) {
+      sWhi[i] = t.Whi[i];
+      sWlo[i] = t.Wlo[i];
+      sC[i] = t.C[i];
+      if (i <= M - 2) sAsuf[i] = t.Asuf[i];
+    }
+    __syncthreads();
+    const SliceTables ts{sC, sWhi, sWlo, sAsuf};
+    if (K == 2)
+      for (int i = threadIdx.x; i <= M - 2; i += blockDim.x) sApre[i] = class_term<MODE>(ts, g.luts, 0, i);
+    __syncthreads();
+    const uint64_t T = binom((uint64_t)P, K);
+    const uint64_t r0 = T * (uint64_t)u / (uint64_t)g.units;
+    const uint64_t r1 = T * (uint64_t)(u + 1) / (uint64_t)g.units;
+    search_flat_k12<K, MODE>(ts, sApre, g.luts, g.Bin + (size_t)z * g.E, M, r0, r1, threadIdx.x,
+                             blockDim.x, best, bestkey);
+  }
+  warp_argmax(best, bestkey);
+  __shared__ double ss[32];
+  __shared__ uint64_t sk[32];
+  if (lane == 0) {
+    ss[warp] = best;
+    sk[warp] = bestkey;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    best = lane < nw ? ss[lane] : -CUDART_INF;
+    bestkey = lane < nw ? sk[lane] : kKeyNone;
+    warp_argmax(best, bestkey);
+    if (lane == 0) {
+      g.part_score[(size_t)blockIdx.x * g.nz + z] = best;
+      g.part_key[(size_t)blockIdx.x * g.nz + z] = bestkey;
+    }
+  }
+}
+
+}  // namespace tsa

@@ -163,6 +163,16 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
       return;
     }
   }
+  // k <= 2: flattened tuple-parallel kernel (tables staged in shared memory)
+  if constexpr (MODE != tsa::SPP) {
+    if (k <= 2) {
+      const size_t smem = (size_t)(2 * a.E + 2 * a.L) * sizeof(double) + (size_t)a.E * sizeof(uint32_t);
+      auto f = k == 1 ? tsa::k_search_flat<1, MODE> : tsa::k_search_flat<2, MODE>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      f<<<grid, 256, smem, s>>>(a);
+      return;
+    }
+  }
   switch (k) {
     case 1: launch_search_k<1, MODE>(a, grid, s, false); break;
     case 2: launch_search_k<2, MODE>(a, grid, s, false); break;
@@ -269,8 +279,8 @@ struct SegWs {
 };
 
 // fused-pipeline constants (tuned on B200, profiles/)
-constexpr int kFusedHC = 4;   // histogram chunks per slice
-constexpr int kFusedLC = 4;   // label chunks per slice
+constexpr int kFusedHC = 2;   // histogram chunks per slice
+constexpr int kFusedLC = 2;   // label chunks per slice
 constexpr int kFusedThreads = 512;
 
 static bool fused_eligible(const tsa_problem *p) {

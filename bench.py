@@ -333,8 +333,8 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f).get(args.workload, {})
-    if kind == 1:
-        # the product step is ONE persistent kernel (k_fused): time each call
+    if kind in (1, 2):
+        # fused (one persistent kernel) or compact (3 kernels): time each call
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(reps)]
         for i in range(reps + 3):
@@ -347,9 +347,11 @@ def main():
         fused_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
         kernels["fused"] = {"ms": fused_ms, "bytes": step_bytes,
                             "gbs": step_bytes / (fused_ms * 1e-3) / 1e9,
-                            "note": "memset of 2+2nz counters + k_fused; bytes = volume once + labels once"}
+                            "note": ("k_fused (+ counter memset)" if kind == 1 else
+                                     "k_hist_part + k_mid + k_label_flat") +
+                                    "; bytes = volume once + labels once (the re-read is served by L2)"}
         dom = "fused"
-        traffic = tr.get("fused")
+        traffic = tr.get("fused") if kind == 1 else tr.get("compact")
     else:
         dom = max(("histogram", "label", "search"), key=lambda nme: kernels[nme]["ms"])
         traffic = tr.get(dom)
@@ -358,7 +360,9 @@ def main():
                     "unit": "FP64 instr/s", "frac": None, "traffic": traffic,
                     "note": "search-dominated workload: see kernels.search and profiles/"}
     else:
-        roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": kernels[dom]["gbs"], "peak": hbm,
+        kname = {"fused": "k_fused" if kind == 1 else "compact step (k_hist_part + k_mid + k_label_flat)"}.get(
+            dom, f"k_{dom}")
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": kernels[dom]["gbs"], "peak": hbm,
                     "unit": "GB/s", "frac": kernels[dom]["gbs"] / hbm, "traffic": traffic,
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({how})",
                     "algorithmic_bytes_per_launch": kernels[dom]["bytes"]}
@@ -404,7 +408,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, host, q)
 
-    launches_per_step = 1 if kind == 1 else 6 + (1 if (k >= 3 and bins <= 512) else 0)
+    launches_per_step = {1: 1, 2: 3}.get(kind, 6 + (1 if (k >= 3 and bins <= 512) else 0))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -413,7 +417,7 @@ def main():
             "config": config_of(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
-            "kernels": kernels, "pipeline": "fused" if kind == 1 else "staged",
+            "kernels": kernels, "pipeline": {1: "fused", 2: "compact"}.get(kind, "staged"),
             "gtuples_per_s_nominal": world * nominal / (ms_per_step * 1e-3) / 1e9,
             "gtuples_per_s_evaluated": world * evaluated / (ms_per_step * 1e-3) / 1e9,
         }

@@ -88,11 +88,14 @@ typedef struct {
   int32_t enumeration;  /* tsa_enumeration */
   int32_t units_per_slice; /* search work units per slice (0 = library heuristic) */
   /* tsa_segment schedule (0 = library default for every field):
-   *   pipeline     1 = one persistent fused kernel (histogram / tables + search +
-   *                finalize / labels overlapped through a dependency-ordered task
-   *                queue; needs k <= 2, bins <= 1024, CANONICAL, PSEUDO_ADDITIVE,
-   *                nx*ny % 16 == 0, 16-byte aligned volume and labels),
-   *                -1 = one kernel per stage, 0 = fused whenever eligible
+   *   pipeline     2 = compact: three kernels (histogram partials + 1/n^q table,
+   *                one CTA per slice for tables/search/argmax/phi, labels);
+   *                1 = one persistent fused kernel (the same work overlapped
+   *                through a dependency-ordered task queue); both need k <= 2,
+   *                bins <= 1024, CANONICAL, PSEUDO_ADDITIVE, nx*ny % 16 == 0,
+   *                16-byte aligned volume and labels;
+   *                -1 = staged: one kernel per stage (any problem);
+   *                0 = compact whenever eligible, else staged
    *   slab_slices  fused: slices per pipeline slab
    *   label_lag    fused: rounds by which labelling trails the histogram */
   int32_t pipeline;
@@ -114,9 +117,9 @@ tsa_status tsa_validate(const tsa_problem *p);
 /* Bytes of workspace tsa_segment needs for this problem (0 if invalid). */
 size_t tsa_workspace_size(const tsa_problem *p);
 
-/* Which implementation tsa_segment runs for this problem: 1 = the fused
- * persistent kernel, -1 = one kernel per stage, 0 = invalid problem.  (Labels
- * must also be 16-byte aligned for the fused kernel.) */
+/* Which implementation tsa_segment runs for this problem: 2 = compact
+ * (3 kernels), 1 = persistent fused kernel, -1 = staged (one kernel per stage),
+ * 0 = invalid problem.  (Labels must also be 16-byte aligned for 1 and 2.) */
 int32_t tsa_pipeline_kind(const tsa_problem *p);
 
 /* The whole hot path on one stream:

@@ -152,7 +152,7 @@ def _dtype_code(vol):
     raise ValueError(f"volume dtype must be uint8 or uint16, got {vol.dtype}")
 
 
-PIPELINES = {"auto": 0, "fused": 1, "staged": -1}
+PIPELINES = {"auto": 0, "fused": 1, "compact": 2, "staged": -1}
 
 
 def make_problem(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0,
@@ -174,7 +174,7 @@ def tsa_validate(problem):
 
 
 def tsa_pipeline_kind(problem):
-    """1 = fused persistent kernel, -1 = staged kernels, 0 = invalid."""
+    """2 = compact (3 kernels), 1 = fused persistent kernel, -1 = staged kernels, 0 = invalid."""
     return int(load().tsa_pipeline_kind(ctypes.byref(problem)))
 
 

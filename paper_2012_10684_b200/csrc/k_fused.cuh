@@ -27,6 +27,24 @@
 
 namespace tsa {
 
+#ifdef TSA_TRACE
+// debug builds only (tools/fused_trace.py): per-task (type, z, smid, t0, t1)
+__device__ unsigned long long g_trace[5 * 65536];
+__device__ int g_trace_n;
+__device__ unsigned long long g_mphase[8 * 4096];  // per slice: 8 phase timestamps of its M task
+#define TSA_MPHASE(z, i) \
+  if (threadIdx.x == 0 && (z) < 4096) g_mphase[8 * (z) + (i)] = gtimer();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+#ifndef TSA_TRACE
+#define TSA_MPHASE(z, i)
+#endif
+
 struct FusedArgs {
   const uint8_t *vol;
   int dtype_bytes;
@@ -50,7 +68,7 @@ struct FusedArgs {
   int32_t *counters;    // [0] head, [1] lutdone, [2 .. 2+nz) hdone, [2+nz .. 2+2nz) mdone
   Luts luts;
   // schedule
-  int HC, LC, SB, DL, nslab, nlut;
+  int HC, LC, SB, DM, DL, nslab, nlut;
   int64_t lut_per;
 };
 
@@ -125,7 +143,7 @@ __device__ void fused_hist(const FusedArgs &g, int z, int c, uint32_t *sh) {
   __syncthreads();
   if (threadIdx.x == 0) {
     g.povf[(size_t)z * g.HC + c] = s_ovf;
-    signal_add(g.counters + 2 + z, 1);
+    if (g.counters) signal_add(g.counters + 2 + z, 1);
   }
 }
 
@@ -214,11 +232,13 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   __shared__ int s_status, s_M;
   __shared__ double s_red[32], s_P[kKMax + 1], s_S[kKMax + 1];
   __shared__ uint64_t s_key[32];
-  if (tid == 0) {
+  TSA_MPHASE(z, 0)
+  if (tid == 0 && g.counters) {
     wait_ge(g.counters + 1, g.nlut);
     wait_ge(g.counters + 2 + z, g.HC);
   }
   __syncthreads();
+  TSA_MPHASE(z, 1)
   // histogram = sum of chunk partials; overflow flag
   int ovf = 0;
   for (int c = tid; c < g.HC; c += blockDim.x) ovf |= __ldcg(g.povf + (size_t)z * g.HC + c);
@@ -234,6 +254,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     wsh[i] = s == 0 ? 0.0 : (g.luts.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q));
   }
   __syncthreads();
+  TSA_MPHASE(z, 2)
   // prefix tables by warp 0 (same construction as k_scan, canonical)
   if (warp == 0) {
     const int per = (L + 31) / 32;
@@ -293,18 +314,23 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     }
   }
   __syncthreads();
+  TSA_MPHASE(z, 3)
   const int M = s_M;
   int st = s_status;
   const SliceTables t{tC, tWhi, tWlo, Asuf};
   double best = -CUDART_INF;
   uint64_t key = kKeyNone;
   if (st == kOK) {
-    for (int i = tid; i <= M - 2; i += blockDim.x) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
+    // Asuf[i] = T(i+1, M-1) and Apre[i] = T(0, i) (in fsh, free until the finalize
+    // step) in one pass so their gathers overlap
+    for (int i = tid; i <= M - 2; i += blockDim.x) {
+      const double as = class_term<MODE>(t, g.luts, i + 1, M - 1);
+      const double ap = K == 2 ? class_term<MODE>(t, g.luts, 0, i) : 0.0;
+      Asuf[i] = as;
+      if (K == 2) fsh[i] = ap;
+    }
     __syncthreads();
-    // Apre[a] = T(0, a) in fsh (free until the finalize step)
-    if (K == 2)
-      for (int i = tid; i <= M - 2; i += blockDim.x) fsh[i] = class_term<MODE>(t, g.luts, 0, i);
-    __syncthreads();
+    TSA_MPHASE(z, 4)
     // exhaustive search over all C(M-1, K) tuples, tuple-parallel over the CTA
     search_flat_k12<K, MODE>(t, fsh, g.luts, tBin, M, 0, binom((uint64_t)(M - 1), K), tid,
                              blockDim.x, best, key);
@@ -327,6 +353,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     }
   }
   __syncthreads();
+  TSA_MPHASE(z, 5)
   st = s_status;
   key = s_key[0];
   int32_t *thr = g.thresholds + (size_t)z * g.k;
@@ -395,29 +422,70 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     }
   }
   __syncthreads();
-  if (tid == 0) signal_add(g.counters + 2 + g.nz + z, 1);
+  TSA_MPHASE(z, 6)
+  if (tid == 0 && g.counters) signal_add(g.counters + 2 + g.nz + z, 1);
+}
+
+// Task index -> (type, slice, chunk).  Queue: LUT tasks, then rounds r:
+// H(slab r), M(slab r - DM), L(slab r - DL) (empty parts are skipped, so the
+// queue has no no-op tasks).  Returns 0 LUT, 1 H, 2 M, 3 L, -1 past the end.
+__device__ __forceinline__ int decode_task(const FusedArgs &g, int64_t t, int &z, int &c) {
+  if (t < g.nlut) {
+    z = (int)t;
+    return 0;
+  }
+  t -= g.nlut;
+  const int nH = g.SB * g.HC, nM = g.SB, nL = g.SB * g.LC;
+  for (int r = 0; r < g.nslab + g.DL; r++) {
+    const int h = r < g.nslab ? nH : 0;
+    const int m = (r - g.DM >= 0 && r - g.DM < g.nslab) ? nM : 0;
+    const int l = (r - g.DL >= 0 && r - g.DL < g.nslab) ? nL : 0;
+    if (t < h) {
+      z = r * g.SB + (int)(t / g.HC);
+      c = (int)(t % g.HC);
+      return 1;
+    }
+    t -= h;
+    if (t < m) {
+      z = (r - g.DM) * g.SB + (int)t;
+      c = 0;
+      return 2;
+    }
+    t -= m;
+    if (t < l) {
+      z = (r - g.DL) * g.SB + (int)(t / g.LC);
+      c = (int)(t % g.LC);
+      return 3;
+    }
+    t -= l;
+  }
+  return -1;
 }
 
 template <typename T, int K, int MODE>
 __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
-  const int nH = g.SB * g.HC, nM = g.SB, nL = g.SB * g.LC;
-  const int round = nH + nM + nL;
-  const int64_t total = (int64_t)g.nlut + (int64_t)(g.nslab + g.DL) * round;
-  __shared__ int s_next;
-  if (threadIdx.x == 0) s_next = atomicAdd(g.counters, 1);
+  __shared__ int s_type, s_z, s_c;
   for (;;) {
+    if (threadIdx.x == 0) {
+      const int task = atomicAdd(g.counters, 1);
+      int z = 0, c = 0;
+      s_type = decode_task(g, task, z, c);
+      s_z = z;
+      s_c = c;
+    }
     __syncthreads();
-    const int64_t task = s_next;
+    const int type = s_type, z = s_z, c = s_c;
     __syncthreads();
-    // claim the following task now; its latency hides behind this one (a
-    // claimed-but-unstarted task only follows tasks this CTA already runs,
-    // so the dependency order still rules out deadlock)
-    if (threadIdx.x == 0 && task < total) s_next = atomicAdd(g.counters, 1);
-    if (task >= total) break;
-    if (task < g.nlut) {
+    if (type < 0) break;
+#ifdef TSA_TRACE
+    unsigned long long tr0 = 0;
+    if (threadIdx.x == 0) tr0 = gtimer();
+    const int tr_type = type, tr_z = z;
+#endif
+    if (type == 0) {
       const int64_t N = g.n;
-      const int64_t a = task * g.lut_per, b = min(N + 1, a + g.lut_per);
+      const int64_t a = (int64_t)z * g.lut_per, b = min(N + 1, a + g.lut_per);
       for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
         const double x = (double)m;
         if (g.luts.shannon) {
@@ -429,32 +497,60 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
       }
       __syncthreads();
       if (threadIdx.x == 0) signal_add(g.counters + 1, 1);
-      continue;
+    } else if (z < g.nz) {
+      if (type == 1) fused_hist<T>(g, z, c, reinterpret_cast<uint32_t *>(fsm));
+      else if (type == 2) fused_mid<K, MODE>(g, z, fsm);
+      else if (g.labels) fused_label<T>(g, z, c);
     }
-    const int64_t rt = task - g.nlut;
-    const int r = (int)(rt / round);
-    const int off = (int)(rt % round);
-    if (off < nH) {
-      const int slab = r;
-      if (slab >= g.nslab) continue;
-      const int z = slab * g.SB + off / g.HC;
-      if (z >= g.nz) continue;
-      fused_hist<T>(g, z, off % g.HC, reinterpret_cast<uint32_t *>(fsm));
-    } else if (off < nH + nM) {
-      const int slab = r - 1;
-      if (slab < 0 || slab >= g.nslab) continue;
-      const int z = slab * g.SB + (off - nH);
-      if (z >= g.nz) continue;
-      fused_mid<K, MODE>(g, z, fsm);
+#ifdef TSA_TRACE
+    if (threadIdx.x == 0) {
+      const int slot = atomicAdd(&g_trace_n, 1);
+      if (slot < 65536) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[5 * slot + 0] = tr_type;
+        g_trace[5 * slot + 1] = (unsigned long long)tr_z;
+        g_trace[5 * slot + 2] = smid;
+        g_trace[5 * slot + 3] = tr0;
+        g_trace[5 * slot + 4] = gtimer();
+      }
+    }
+#endif
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compact 3-kernel path (default for the same eligible problems): the fused
+// kernel's task bodies as three grid-wide kernels, so the latency-bound
+// per-slice search never shares an SM with the atomics-bound histogram.
+//   k_hist_part  (chunk, slice) histogram partials + this CTA's share of the
+//                1/n^q table; loads keep the volume in L2 (evict_last) for
+//   k_mid        one CTA per slice: tables, search, argmax, phi(t*)
+//   k_label      labels (the volume re-read mostly hits L2)
+template <typename T>
+__global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
+  extern __shared__ __align__(16) char fsm[];
+  fused_hist<T>(g, blockIdx.y, blockIdx.x, reinterpret_cast<uint32_t *>(fsm));
+  // LUT share of this CTA
+  const int64_t G = (int64_t)gridDim.x * gridDim.y;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t N1 = g.n + 1;
+  const int64_t a = N1 * cta / G, b = N1 * (cta + 1) / G;
+  for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
+    const double x = (double)m;
+    if (g.luts.shannon) {
+      g.lnn[m] = m == 0 ? CUDART_NAN : log(x);
+      g.rcp[m] = m == 0 ? CUDART_NAN : __drcp_rn(x);
     } else {
-      const int slab = r - g.DL;
-      if (slab < 0 || slab >= g.nslab) continue;
-      const int o = off - nH - nM;
-      const int z = slab * g.SB + o / g.LC;
-      if (z >= g.nz) continue;
-      if (g.labels) fused_label<T>(g, z, o % g.LC);
+      g.ipow[m] = m == 0 ? CUDART_NAN : __drcp_rn(pow(x, g.q));
     }
   }
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(512) k_mid(FusedArgs g) {
+  extern __shared__ __align__(16) char fsm[];
+  fused_mid<K, MODE>(g, blockIdx.x, fsm);
 }
 
 }  // namespace tsa

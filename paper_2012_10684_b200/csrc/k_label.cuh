@@ -32,12 +32,23 @@ __device__ __forceinline__ uint32_t swar_label4(uint32_t w, uint32_t t0, uint32_
          (__vcmpgtu4(w, t2) & 0x01010101u) + (__vcmpgtu4(w, t3) & 0x01010101u);
 }
 
+template <int KT>
+__device__ __forceinline__ uint32_t swar_labelk(uint32_t w, uint32_t t0, uint32_t t1, uint32_t t2,
+                                                uint32_t t3) {
+  uint32_t o = __vcmpgtu4(w, t0) & 0x01010101u;
+  if (KT > 1) o += __vcmpgtu4(w, t1) & 0x01010101u;
+  if (KT > 2) o += __vcmpgtu4(w, t2) & 0x01010101u;
+  if (KT > 3) o += __vcmpgtu4(w, t3) & 0x01010101u;
+  return o;
+}
+
 __device__ __forceinline__ uint32_t label_of(int v, int t0, int t1, int t2, int t3) {
   return (uint32_t)(v > t0) + (uint32_t)(v > t1) + (uint32_t)(v > t2) + (uint32_t)(v > t3);
 }
 
 // Fast path: n % 16 == 0 and 16-byte aligned volume/labels (the common case).
-template <typename T>
+// KT = k (compile-time: only k SWAR compares per word; thresholds >= k unused).
+template <typename T, int KT>
 __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
   const int64_t per = g.n / 16;  // 16-voxel groups per slice
   const int64_t i0 = g.z0 * per, i1 = g.z1 * per;
@@ -71,10 +82,10 @@ __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
       if (ok) {
         const uint32_t b0 = (uint32_t)t0 * 0x01010101u, b1 = (uint32_t)t1 * 0x01010101u;
         const uint32_t b2 = (uint32_t)t2 * 0x01010101u, b3 = (uint32_t)t3 * 0x01010101u;
-        o.x = swar_label4(w.x, b0, b1, b2, b3);
-        o.y = swar_label4(w.y, b0, b1, b2, b3);
-        o.z = swar_label4(w.z, b0, b1, b2, b3);
-        o.w = swar_label4(w.w, b0, b1, b2, b3);
+        o.x = swar_labelk<KT>(w.x, b0, b1, b2, b3);
+        o.y = swar_labelk<KT>(w.y, b0, b1, b2, b3);
+        o.z = swar_labelk<KT>(w.z, b0, b1, b2, b3);
+        o.w = swar_labelk<KT>(w.w, b0, b1, b2, b3);
       }
       __stcs(dst + i, o);
     } else {

@@ -321,7 +321,7 @@ __device__ __forceinline__ void search_flat_k12(const SliceTables &t, const doub
                                                 const Luts &l, const int32_t *bin, int M,
                                                 uint64_t r0, uint64_t r1, uint64_t tid,
                                                 uint64_t nth, double &best, uint64_t &bestkey) {
-  constexpr int B = 4;
+  constexpr int B = 8;
   const double ident = MODE == SUM ? 0.0 : 1.0;
   for (uint64_t rb = r0 + tid; rb < r1; rb += nth * B) {
     int aa[B], bb[B];

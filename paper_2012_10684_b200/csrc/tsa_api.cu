@@ -279,7 +279,8 @@ struct SegWs {
 };
 
 // fused-pipeline constants (tuned on B200, profiles/)
-constexpr int kFusedHC = 2;   // histogram chunks per slice
+constexpr int kFusedHC = 2;   // histogram chunks per slice (persistent fused kernel)
+constexpr int kCompactHC = 4; // histogram chunks per slice (3-kernel compact path)
 constexpr int kFusedLC = 2;   // label chunks per slice
 constexpr int kFusedThreads = 512;
 
@@ -301,8 +302,8 @@ static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
   w.search_bytes = tsa_search_workspace_size(p->nz, p->nx * p->ny, p->bins, p->k, p->q,
                                              p->objective, p->enumeration);
   w.search = c.take<char>(w.search_bytes);
-  w.partial = c.take<uint32_t>((size_t)p->nz * kFusedHC * p->bins);
-  w.povf = c.take<int32_t>((size_t)p->nz * kFusedHC);
+  w.partial = c.take<uint32_t>((size_t)p->nz * std::max(kFusedHC, kCompactHC) * p->bins);
+  w.povf = c.take<int32_t>((size_t)p->nz * std::max(kFusedHC, kCompactHC));
   w.counters = c.take<int32_t>(2 + 2 * (size_t)p->nz);
   w.luts = c.take<double>(2 * ((size_t)p->nx * p->ny + 1));
   if (o) *o = w;
@@ -335,7 +336,7 @@ static void launch_fused_k(const tsa::FusedArgs &a, int mode, size_t smem, int g
 extern "C" {
 
 static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, const SegWs &w,
-                                cudaStream_t s) {
+                                cudaStream_t s, bool persistent) {
   const int64_t N = p->nx * p->ny;
   const bool shannon = p->q == 1.0;
   tsa::FusedArgs a;
@@ -368,14 +369,38 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
   a.HC = kFusedHC;
   a.LC = kFusedLC;
   a.SB = p->slab_slices > 0 ? p->slab_slices : 16;
-  a.DL = p->label_lag > 0 ? std::max(2, p->label_lag) : 6;
+  a.DM = 2;
+  a.DL = p->label_lag > 0 ? std::max(a.DM + 1, p->label_lag) : 6;
   a.nslab = (int)((p->nz + a.SB - 1) / a.SB);
   a.lut_per = 4096;
   a.nlut = (int)((N + 1 + a.lut_per - 1) / a.lut_per);
-  TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
   const int L = p->bins, E = L + 1;
   const size_t smem_h = (size_t)(kFusedThreads / 32) * L * sizeof(uint32_t);
   const size_t smem_m = (size_t)((L + 1) & ~1) * 4 + (size_t)L * 8 * 3 + (size_t)E * 8 * 2 + (size_t)E * 8;
+  if (!persistent) {
+    // compact path: k_hist_part -> k_mid -> k_label (no counters, no memsets)
+    a.counters = nullptr;
+    a.HC = kCompactHC;
+    const size_t sh = smem_h + 64, sm = smem_m + 64;
+    dim3 gh((unsigned)a.HC, (unsigned)p->nz);
+    if (p->dtype == TSA_U8) tsa::k_hist_part<uint8_t><<<gh, kFusedThreads, sh, s>>>(a);
+    else {
+      if (sh > 48 * 1024)
+        cudaFuncSetAttribute(tsa::k_hist_part<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+      tsa::k_hist_part<uint16_t><<<gh, kFusedThreads, sh, s>>>(a);
+    }
+    TSA_TRY(check_cuda("k_hist_part"));
+    auto mid = p->k == 1 ? (a.mode == tsa::PROD_MAX ? tsa::k_mid<1, tsa::PROD_MAX>
+                            : a.mode == tsa::PROD_MIN ? tsa::k_mid<1, tsa::PROD_MIN> : tsa::k_mid<1, tsa::SUM>)
+                         : (a.mode == tsa::PROD_MAX ? tsa::k_mid<2, tsa::PROD_MAX>
+                            : a.mode == tsa::PROD_MIN ? tsa::k_mid<2, tsa::PROD_MIN> : tsa::k_mid<2, tsa::SUM>);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    mid<<<(unsigned)p->nz, kFusedThreads, sm, s>>>(a);
+    TSA_TRY(check_cuda("k_mid"));
+    if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, s));
+    return TSA_OK;
+  }
+  TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
   const size_t smem = std::max(smem_h, smem_m) + 64;
   const int grid = g_num_sms() * 2;
   if (p->dtype == TSA_U8) {
@@ -390,7 +415,8 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
 
 int32_t tsa_pipeline_kind(const tsa_problem *p) {
   if (tsa_validate(p) != TSA_OK) return 0;
-  return (p->pipeline >= 0 && fused_eligible(p)) ? 1 : -1;
+  if (p->pipeline < 0 || !fused_eligible(p)) return -1;
+  return p->pipeline == 1 ? 1 : 2;
 }
 
 size_t tsa_workspace_size(const tsa_problem *p) {
@@ -605,10 +631,17 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
   if (aligned) {
     const int64_t groups = a.n / 16 * p->nz;
     const int64_t blocks = std::min<int64_t>((groups + 255) / 256, (int64_t)g_num_sms() * 8);
-    if (p->dtype == TSA_U8)
-      tsa::k_label_flat<uint8_t><<<(unsigned)blocks, 256, 0, S(stream)>>>(a);
-    else
-      tsa::k_label_flat<uint16_t><<<(unsigned)blocks, 256, 0, S(stream)>>>(a);
+    cudaStream_t s = S(stream);
+    if (p->dtype == TSA_U8) {
+      switch (p->k) {
+        case 1: tsa::k_label_flat<uint8_t, 1><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        case 2: tsa::k_label_flat<uint8_t, 2><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        case 3: tsa::k_label_flat<uint8_t, 3><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        default: tsa::k_label_flat<uint8_t, 4><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+      }
+    } else {
+      tsa::k_label_flat<uint16_t, 4><<<(unsigned)blocks, 256, 0, s>>>(a);
+    }
   } else {
     const int64_t cx = std::max<int64_t>(1, std::min<int64_t>(64, a.n / 4096));
     dim3 grid((unsigned)cx, (unsigned)p->nz);
@@ -630,8 +663,9 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = S(stream);
   const bool labels_aligned = !out->labels || (reinterpret_cast<uintptr_t>(out->labels) & 15) == 0;
-  if (p->pipeline >= 0 && fused_eligible(p) && labels_aligned) return segment_fused(p, out, w, s);
-  if (p->pipeline > 0) return set_error(TSA_ERR_INVALID_ARG, "pipeline=fused but the problem is not eligible");
+  if (p->pipeline >= 0 && fused_eligible(p) && labels_aligned)
+    return segment_fused(p, out, w, s, p->pipeline == 1);
+  if (p->pipeline > 0) return set_error(TSA_ERR_INVALID_ARG, "fused/compact pipeline requested but the problem is not eligible");
   uint32_t *hist = out->histogram ? out->histogram : w.hist;
   const int32_t U = units_of(p);
   TSA_TRY(tsa_histogram(p, hist, w.status, stream));
@@ -712,4 +746,20 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   return TSA_OK;
 }
 
+#ifdef TSA_TRACE
+// debug builds only (tools/fused_trace.py): copy the fused-kernel task trace to the host
+int tsa_debug_trace(unsigned long long *host, int max_entries) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, tsa::g_trace_n, sizeof(int));
+  n = std::min(n, std::min(max_entries, 65536));
+  cudaMemcpyFromSymbol(host, tsa::g_trace, sizeof(unsigned long long) * 5 * n);
+  const int zero = 0;
+  cudaMemcpyToSymbol(tsa::g_trace_n, &zero, sizeof(int));
+  return n;
+}
+int tsa_debug_mphase(unsigned long long *host, int nz) {
+  cudaMemcpyFromSymbol(host, tsa::g_mphase, sizeof(unsigned long long) * 8 * std::min(nz, 4096));
+  return 0;
+}
+#endif
 }  // extern "C"

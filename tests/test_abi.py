@@ -77,7 +77,8 @@ def test_invalid_arguments_rejected_synchronously(lib, kw):
 
 
 def test_pipeline_kind(lib):
-    assert lib.tsa_pipeline_kind(ctypes.byref(_p())) == 1            # c2: fused
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p())) == 2            # c2: compact
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=1))) == 1  # persistent fused
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(k=3))) == -1        # k >= 3: staged
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=-1))) == -1
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(enumeration=1))) == -1

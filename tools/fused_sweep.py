@@ -33,6 +33,7 @@ def run(**kw):
 
 
 print(f"{name} staged: {run(pipeline='staged'):.1f} us/step")
+print(f"{name} compact: {run(pipeline='compact'):.1f} us/step")
 for sb in (4, 8, 16, 32):
-    for dl in (2, 3, 4, 6, 10):
+    for dl in (3, 4, 5, 6, 8, 12):
         print(f"{name} fused sb={sb} dl={dl}: {run(pipeline='fused', slab_slices=sb, label_lag=dl):.1f} us/step")

@@ -23,6 +23,7 @@
 #include "k_histogram.cuh"
 #include "k_label.cuh"
 #include "k_search.cuh"
+#include "k_tables.cuh"
 #include "tsa_device.cuh"
 
 namespace tsa {
@@ -232,6 +233,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   __shared__ int s_status, s_M;
   __shared__ double s_red[32], s_P[kKMax + 1], s_S[kKMax + 1];
   __shared__ uint64_t s_key[32];
+  __shared__ __align__(16) double s_scan[96];
   TSA_MPHASE(z, 0)
   if (tid == 0 && g.counters) {
     wait_ge(g.counters + 1, g.nlut);
@@ -250,70 +252,21 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     for (int c = 0; c < g.HC; c++) s += __ldcg(g.partial + ((size_t)z * g.HC + c) * L + i);
     hs[i] = s;
     g.hist[(size_t)z * L + i] = s;
-    const double x = (double)s;
-    wsh[i] = s == 0 ? 0.0 : (g.luts.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q));
   }
   __syncthreads();
   TSA_MPHASE(z, 2)
-  // prefix tables by warp 0 (same construction as k_scan, canonical)
-  if (warp == 0) {
-    const int per = (L + 31) / 32;
-    const int i0 = min(L, lane * per), i1 = min(L, i0 + per);
-    uint32_t m_l = 0, n_l = 0;
-    dd w_l = {0.0, 0.0};
-    for (int i = i0; i < i1; i++) {
-      const uint32_t c = hs[i];
-      if (c) {
-        m_l++;
-        n_l += c;
-        w_l = dd_add_d(w_l, wsh[i]);
-      }
+  // prefix tables (the same block-wide construction as k_scan: bit-identical)
+  {
+    int m;
+    uint32_t ntot;
+    build_tables(hs, L, g.q, g.luts.shannon, wsh, tC, tWhi, tWlo, tBin,
+                 reinterpret_cast<char *>(s_scan), m, ntot);
+    if (tid == 0) {
+      s_M = m;
+      if (s_status == kOK && m < K + 1) s_status = kNoValidSplit;
     }
-    uint32_t m_inc = m_l, n_inc = n_l;
-    dd w_inc = w_l;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t om = __shfl_up_sync(0xffffffffu, m_inc, off);
-      const uint32_t on = __shfl_up_sync(0xffffffffu, n_inc, off);
-      const double oh = __shfl_up_sync(0xffffffffu, w_inc.hi, off);
-      const double ol = __shfl_up_sync(0xffffffffu, w_inc.lo, off);
-      if (lane >= off) {
-        m_inc += om;
-        n_inc += on;
-        w_inc = dd_add({oh, ol}, w_inc);
-      }
-    }
-    const uint32_t m_tot = __shfl_sync(0xffffffffu, m_inc, 31);
-    dd w_ex;
-    w_ex.hi = __shfl_up_sync(0xffffffffu, w_inc.hi, 1);
-    w_ex.lo = __shfl_up_sync(0xffffffffu, w_inc.lo, 1);
-    if (lane == 0) {
-      tC[0] = 0;
-      tWhi[0] = 0.0;
-      tWlo[0] = 0.0;
-      tBin[0] = -1;
-    }
-    uint32_t e = m_inc - m_l + 1, ncum = n_inc - n_l;
-    dd wl = {0.0, 0.0};
-    for (int i = i0; i < i1; i++) {
-      const uint32_t c = hs[i];
-      if (c) {
-        ncum += c;
-        wl = dd_add_d(wl, wsh[i]);
-        const dd W = lane == 0 ? wl : dd_add(w_ex, wl);
-        tC[e] = ncum;
-        tWhi[e] = W.hi;
-        tWlo[e] = W.lo;
-        tBin[e] = i;
-        e++;
-      }
-    }
-    if (lane == 0) {
-      s_M = (int)m_tot;
-      if (s_status == kOK && (int)m_tot < K + 1) s_status = kNoValidSplit;
-    }
+    __syncthreads();
   }
-  __syncthreads();
   TSA_MPHASE(z, 3)
   const int M = s_M;
   int st = s_status;

@@ -49,120 +49,131 @@ struct ScanArgs {
   Luts luts;
 };
 
-// One warp (one CTA) per slice.  Lane l owns the contiguous bins
-// [l*L/32, (l+1)*L/32): it forms w_i (pow or c ln c) once into shared memory,
-// a local double-double prefix, and a warp shuffle scan of (m, n, W) gives its
-// offsets.  FULL tables copy the canonical entry of the last non-empty bin <= i,
-// so tuples that differ only by empty bins read identical table values and
-// evaluate bit-identically.
-template <int MODE>
-__global__ void __launch_bounds__(32) k_scan(ScanArgs g) {
-  extern __shared__ double wsh[];  // [L]
-  const int lane = threadIdx.x;
-  const int64_t z = blockIdx.x;
-  const int L = g.L, E = g.E;
-  const uint32_t *h = g.hist + z * L;
-  const int per = (L + 31) / 32;
-  const int i0 = min(L, lane * per), i1 = min(L, i0 + per);
-  // w_i for all bins, lane-strided: independent pow/log calls overlap
-#pragma unroll 4
-  for (int i = lane; i < L; i += 32) {
-    const uint32_t c = __ldg(h + i);
+// Canonical prefix tables of one slice, built by the whole CTA (any block
+// size; every caller uses kTableThreads so the rounding is identical):
+//   w_i = c_i^q (c_i ln c_i at q == 1) for all bins, lane-strided (independent
+//   pow calls overlap); thread t then owns the contiguous bins
+//   [t*per, (t+1)*per): local double-double prefix, a block scan of
+//   (#non-empty, count, W) gives its offsets, and it writes its entries
+//   e = rank + 1:  C[e] (exact prefix count), Whi/Wlo[e], Bin[e]; entry 0 is
+//   the sentinel (0, 0, -1).  Returns m (non-empty bins) and N (total count).
+constexpr int kTableThreads = 256;
+
+__device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q, int shannon,
+                                             double *wsh, uint32_t *C, double *Whi, double *Wlo,
+                                             int32_t *Bin, char *scratch, int &m_out,
+                                             uint32_t &n_out) {
+  // exactly kTableThreads threads do the work whatever the block size (>= it),
+  // so every kernel produces bit-identical tables
+  const int tid = threadIdx.x, T = kTableThreads;
+  for (int i = tid; i < L; i += blockDim.x) {
+    const uint32_t c = h[i];
     const double x = (double)c;
-    wsh[i] = c == 0 ? 0.0 : (g.shannon ? __dmul_rn(x, log(x)) : pow(x, g.q));
+    wsh[i] = c == 0 ? 0.0 : (shannon ? __dmul_rn(x, log(x)) : pow(x, q));
   }
-  __syncwarp();
+  __syncthreads();
+  const int per = (L + T - 1) / T;
+  const int i0 = tid < T ? min(L, tid * per) : L, i1 = tid < T ? min(L, i0 + per) : L;
   uint32_t m_l = 0, n_l = 0;
   dd w_l = {0.0, 0.0};
   for (int i = i0; i < i1; i++) {
-    const uint32_t c = __ldg(h + i);
+    const uint32_t c = h[i];
     if (c) {
       m_l++;
       n_l += c;
       w_l = dd_add_d(w_l, wsh[i]);
     }
   }
-  uint32_t m_inc = m_l, n_inc = n_l;
-  dd w_inc = w_l;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t om = __shfl_up_sync(0xffffffffu, m_inc, off);
-    const uint32_t on = __shfl_up_sync(0xffffffffu, n_inc, off);
-    const double oh = __shfl_up_sync(0xffffffffu, w_inc.hi, off);
-    const double ol = __shfl_up_sync(0xffffffffu, w_inc.lo, off);
-    if (lane >= off) {
-      m_inc += om;
-      n_inc += on;
-      w_inc = dd_add({oh, ol}, w_inc);
+  uint32_t m_ex, n_ex, m_tot, n_tot;
+  dd w_ex;
+  block_scan_mnw(m_l, n_l, w_l, m_ex, n_ex, w_ex, m_tot, n_tot, scratch, T);
+  if (tid == 0) {
+    C[0] = 0;
+    Whi[0] = 0.0;
+    Wlo[0] = 0.0;
+    Bin[0] = -1;
+  }
+  uint32_t e = m_ex + 1, ncum = n_ex;
+  dd wl = {0.0, 0.0};
+  for (int i = i0; i < i1; i++) {
+    const uint32_t c = h[i];
+    if (c) {
+      ncum += c;
+      wl = dd_add_d(wl, wsh[i]);
+      const dd W = dd_add(w_ex, wl);
+      C[e] = ncum;
+      Whi[e] = W.hi;
+      Wlo[e] = W.lo;
+      Bin[e] = i;
+      e++;
     }
   }
-  const uint32_t m_tot = __shfl_sync(0xffffffffu, m_inc, 31);
-  const uint32_t m_ex = m_inc - m_l, n_ex = n_inc - n_l;
-  dd w_ex;
-  w_ex.hi = __shfl_up_sync(0xffffffffu, w_inc.hi, 1);
-  w_ex.lo = __shfl_up_sync(0xffffffffu, w_inc.lo, 1);
+  __syncthreads();
+  m_out = (int)m_tot;
+  n_out = n_tot;
+}
+
+// One CTA (kTableThreads) per slice: canonical tables via build_tables; FULL
+// tables copy the canonical entry of the last non-empty bin <= i, so tuples
+// that differ only by empty bins read identical table values and evaluate
+// bit-identically; then Asuf.
+template <int MODE>
+__global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
+  extern __shared__ __align__(16) double wsh[];  // [L] then scan scratch
+  const int tid = threadIdx.x;
+  const int64_t z = blockIdx.x;
+  const int L = g.L, E = g.E;
+  const uint32_t *h = g.hist + z * L;
+  char *scratch = reinterpret_cast<char *>(wsh + L);
   uint32_t *cC = g.cC + z * E;
   double *cWhi = g.cWhi + z * E, *cWlo = g.cWlo + z * E;
   int32_t *cBin = g.cBin + z * E;
-  if (lane == 0) {
-    cC[0] = 0;
-    cWhi[0] = 0.0;
-    cWlo[0] = 0.0;
-    cBin[0] = -1;
-  }
-  {
-    uint32_t e = m_ex + 1, ncum = n_ex;
-    dd wl = {0.0, 0.0};
-    for (int i = i0; i < i1; i++) {
-      const uint32_t c = __ldg(h + i);
-      if (c) {
-        ncum += c;
-        wl = dd_add_d(wl, wsh[i]);
-        const dd W = lane == 0 ? wl : dd_add(w_ex, wl);
-        cC[e] = ncum;
-        cWhi[e] = W.hi;
-        cWlo[e] = W.lo;
-        cBin[e] = i;
-        e++;
-      }
-    }
-  }
-  __syncwarp();
+  int m;
+  uint32_t ntot;
+  build_tables(h, L, g.q, g.shannon, wsh, cC, cWhi, cWlo, cBin, scratch, m, ntot);
   int status = g.status[z];
-  if (status == kOK && (int)m_tot < g.k + 1) status = kNoValidSplit;
-  if (lane == 0) g.status[z] = status;
+  if (status == kOK && m < g.k + 1) status = kNoValidSplit;
+  __syncthreads();
+  if (tid == 0) g.status[z] = status;
   const uint32_t *tC = cC;
   const double *tWhi = cWhi, *tWlo = cWlo;
-  int M = (int)m_tot;
+  int M = m;
   if (g.full) {
     uint32_t *fC = g.fC + z * E;
     double *fWhi = g.fWhi + z * E, *fWlo = g.fWlo + z * E;
     int32_t *fBin = g.fBin + z * E;
-    if (lane == 0) {
-      fC[0] = 0;
-      fWhi[0] = 0.0;
-      fWlo[0] = 0.0;
-      fBin[0] = -1;
+    // rank of bin i among non-empty bins: binary search in the canonical list
+    for (int i = tid; i <= L; i += blockDim.x) {
+      if (i == 0) {
+        fC[0] = 0;
+        fWhi[0] = 0.0;
+        fWlo[0] = 0.0;
+        fBin[0] = -1;
+        continue;
+      }
+      const int bin = i - 1;
+      int lo = 0, hi = m;  // largest r in [0, m] with cBin[r] <= bin (cBin[0] = -1)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cBin[mid] <= bin) lo = mid;
+        else hi = mid - 1;
+      }
+      fC[i] = cC[lo];
+      fWhi[i] = cWhi[lo];
+      fWlo[i] = cWlo[lo];
+      fBin[i] = bin;
     }
-    uint32_t r = m_ex;
-    for (int i = i0; i < i1; i++) {
-      if (__ldg(h + i)) r++;
-      fC[i + 1] = cC[r];
-      fWhi[i + 1] = cWhi[r];
-      fWlo[i + 1] = cWlo[r];
-      fBin[i + 1] = i;
-    }
-    __syncwarp();
+    __syncthreads();
     tC = fC;
     tWhi = fWhi;
     tWlo = fWlo;
     M = L;
   }
-  if (lane == 0) g.M[z] = M;
+  if (tid == 0) g.M[z] = M;
   if (status != kOK) return;
   SliceTables t{tC, tWhi, tWlo, nullptr};
   double *Asuf = g.Asuf + z * L;
-  for (int i = lane; i <= M - 2; i += 32) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
+  for (int i = tid; i <= M - 2; i += blockDim.x) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
 }
 
 // R[a][b] = combine(T(a+1, b), Asuf[b]) for 0 <= a < b <= M-2 (k >= 3,

@@ -183,8 +183,9 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
 
 template <int MODE>
 void launch_scan(const tsa::ScanArgs &a, cudaStream_t s) {
-  const size_t smem = (size_t)a.L * sizeof(double);
-  tsa::k_scan<MODE><<<(unsigned)a.nz, 32, smem, s>>>(a);
+  const size_t smem = (size_t)a.L * sizeof(double) + 1024;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_scan<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tsa::k_scan<MODE><<<(unsigned)a.nz, tsa::kTableThreads, smem, s>>>(a);
 }
 
 template <int MODE>
@@ -395,7 +396,7 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
                          : (a.mode == tsa::PROD_MAX ? tsa::k_mid<2, tsa::PROD_MAX>
                             : a.mode == tsa::PROD_MIN ? tsa::k_mid<2, tsa::PROD_MIN> : tsa::k_mid<2, tsa::SUM>);
     if (sm > 48 * 1024) cudaFuncSetAttribute(mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    mid<<<(unsigned)p->nz, kFusedThreads, sm, s>>>(a);
+    mid<<<(unsigned)p->nz, tsa::kTableThreads, sm, s>>>(a);
     TSA_TRY(check_cuda("k_mid"));
     if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, s));
     return TSA_OK;

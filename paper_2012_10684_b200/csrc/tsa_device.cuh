@@ -173,3 +173,83 @@ __device__ __forceinline__ void warp_argmax(double &s, uint64_t &k) {
 }
 
 }  // namespace tsa
+
+namespace tsa {
+
+// Block-wide exclusive scan of per-thread (m, n, w): m, n exact integers and w
+// a double-double.  Warp shuffle scans, then one warp scans the warp totals.
+// Every kernel that builds prefix tables uses this one function with the same
+// block size, so tables (and hence every tuple value) are bit-identical
+// across the staged, compact and fused paths.  scratch: >= 32 * 24 bytes.
+__device__ __forceinline__ void block_scan_mnw(uint32_t m, uint32_t n, dd w, uint32_t &m_ex,
+                                               uint32_t &n_ex, dd &w_ex, uint32_t &m_tot,
+                                               uint32_t &n_tot, char *scratch, int nthreads) {
+  // threads >= nthreads must pass zeros; only the first nthreads/32 warps are scanned
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (nthreads + 31) >> 5;
+  uint32_t mi = m, ni = n;
+  dd wi = w;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t om = __shfl_up_sync(0xffffffffu, mi, off);
+    const uint32_t on = __shfl_up_sync(0xffffffffu, ni, off);
+    const double oh = __shfl_up_sync(0xffffffffu, wi.hi, off);
+    const double ol = __shfl_up_sync(0xffffffffu, wi.lo, off);
+    if (lane >= off) {
+      mi += om;
+      ni += on;
+      wi = dd_add({oh, ol}, wi);
+    }
+  }
+  uint32_t *sm = reinterpret_cast<uint32_t *>(scratch);
+  uint32_t *sn = sm + 32;
+  double *sh = reinterpret_cast<double *>(scratch + 256);
+  double *sl = sh + 32;
+  if (lane == 31 && warp < nw) {
+    sm[warp] = mi;
+    sn[warp] = ni;
+    sh[warp] = wi.hi;
+    sl[warp] = wi.lo;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t a = lane < nw ? sm[lane] : 0u, b = lane < nw ? sn[lane] : 0u;
+    dd c = lane < nw ? dd{sh[lane], sl[lane]} : dd{0.0, 0.0};
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t oa = __shfl_up_sync(0xffffffffu, a, off);
+      const uint32_t ob = __shfl_up_sync(0xffffffffu, b, off);
+      const double oh = __shfl_up_sync(0xffffffffu, c.hi, off);
+      const double ol = __shfl_up_sync(0xffffffffu, c.lo, off);
+      if (lane >= off) {
+        a += oa;
+        b += ob;
+        c = dd_add({oh, ol}, c);
+      }
+    }
+    // store inclusive warp prefixes; slot nw.. holds the totals
+    __syncwarp();
+    if (lane < nw) {
+      sm[lane] = a;
+      sn[lane] = b;
+      sh[lane] = c.hi;
+      sl[lane] = c.lo;
+    }
+  }
+  __syncthreads();
+  m_tot = sm[nw - 1];
+  n_tot = sn[nw - 1];
+  // exclusive prefix of this thread = (warp exclusive) + (lane exclusive)
+  const uint32_t wm = warp ? sm[warp - 1] : 0u, wn = warp ? sn[warp - 1] : 0u;
+  const dd ww = warp ? dd{sh[warp - 1], sl[warp - 1]} : dd{0.0, 0.0};
+  const uint32_t lm = mi - m, ln = ni - n;
+  dd lw;
+  lw.hi = __shfl_up_sync(0xffffffffu, wi.hi, 1);
+  lw.lo = __shfl_up_sync(0xffffffffu, wi.lo, 1);
+  if (lane == 0) lw = {0.0, 0.0};
+  m_ex = wm + lm;
+  n_ex = wn + ln;
+  w_ex = dd_add(ww, lw);
+  __syncthreads();  // scratch reusable after return
+}
+
+}  // namespace tsa

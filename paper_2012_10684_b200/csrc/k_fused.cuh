@@ -473,18 +473,27 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
 }
 
 // ---------------------------------------------------------------------------
-// Compact 3-kernel path (default for the same eligible problems): the fused
-// kernel's task bodies as three grid-wide kernels, so the latency-bound
-// per-slice search never shares an SM with the atomics-bound histogram.
-//   k_hist_part  (chunk, slice) histogram partials + this CTA's share of the
-//                1/n^q table; loads keep the volume in L2 (evict_last) for
-//   k_mid        one CTA per slice: tables, search, argmax, phi(t*)
-//   k_label      labels (the volume re-read mostly hits L2)
+// Compact path (default for the same eligible problems): the fused kernel's
+// task bodies as three kernels chained with Programmatic Dependent Launch.
+// Each kernel lets its dependent launch as soon as all its CTAs are running
+// (griddepcontrol.launch_dependents), and dependents wait per slice on the
+// release/acquire counters instead of on whole-grid completion, so the
+// latency-bound per-slice search overlaps the atomics-bound histogram and the
+// HBM-bound labelling of other slices.  (A dependent grid only launches once
+// every CTA of its primary has started, so spinning dependents can never
+// starve the CTAs they wait for.)
+//   k_hist_part   (chunk, slice): its share of the 1/n^q table, then histogram
+//                 partials; signals lutdone and hdone[z]
+//   k_mid         one CTA per slice: waits lutdone, hdone[z]; tables, search,
+//                 argmax, phi(t*); signals mdone[z]
+//   k_label_part  (chunk, slice): waits mdone[z]; labels
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename T>
 __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
-  fused_hist<T>(g, blockIdx.y, blockIdx.x, reinterpret_cast<uint32_t *>(fsm));
-  // LUT share of this CTA
+  pdl_trigger();
+  // LUT share of this CTA first (k_mid waits for all of them)
   const int64_t G = (int64_t)gridDim.x * gridDim.y;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   const int64_t N1 = g.n + 1;
@@ -498,12 +507,21 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
       g.ipow[m] = m == 0 ? CUDART_NAN : __drcp_rn(pow(x, g.q));
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && g.counters) signal_add(g.counters + 1, 1);
+  fused_hist<T>(g, blockIdx.y, blockIdx.x, reinterpret_cast<uint32_t *>(fsm));
 }
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(512) k_mid(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
+  pdl_trigger();
   fused_mid<K, MODE>(g, blockIdx.x, fsm);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_label_part(FusedArgs g) {
+  fused_label<T>(g, blockIdx.y, blockIdx.x);
 }
 
 }  // namespace tsa

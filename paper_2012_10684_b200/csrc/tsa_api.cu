@@ -282,6 +282,7 @@ struct SegWs {
 // fused-pipeline constants (tuned on B200, profiles/)
 constexpr int kFusedHC = 2;   // histogram chunks per slice (persistent fused kernel)
 constexpr int kCompactHC = 4; // histogram chunks per slice (3-kernel compact path)
+constexpr int kCompactLC = 4; // label chunks per slice (3-kernel compact path)
 constexpr int kFusedLC = 2;   // label chunks per slice
 constexpr int kFusedThreads = 512;
 
@@ -379,9 +380,11 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
   const size_t smem_h = (size_t)(kFusedThreads / 32) * L * sizeof(uint32_t);
   const size_t smem_m = (size_t)((L + 1) & ~1) * 4 + (size_t)L * 8 * 3 + (size_t)E * 8 * 2 + (size_t)E * 8;
   if (!persistent) {
-    // compact path: k_hist_part -> k_mid -> k_label (no counters, no memsets)
-    a.counters = nullptr;
+    // compact path: k_hist_part -> k_mid -> k_label_part, PDL-chained
+    TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
     a.HC = kCompactHC;
+    a.LC = kCompactLC;
+    a.nlut = a.HC * (int)p->nz;  // every k_hist_part CTA computes a LUT share
     const size_t sh = smem_h + 64, sm = smem_m + 64;
     dim3 gh((unsigned)a.HC, (unsigned)p->nz);
     if (p->dtype == TSA_U8) tsa::k_hist_part<uint8_t><<<gh, kFusedThreads, sh, s>>>(a);
@@ -391,15 +394,30 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
       tsa::k_hist_part<uint16_t><<<gh, kFusedThreads, sh, s>>>(a);
     }
     TSA_TRY(check_cuda("k_hist_part"));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     auto mid = p->k == 1 ? (a.mode == tsa::PROD_MAX ? tsa::k_mid<1, tsa::PROD_MAX>
                             : a.mode == tsa::PROD_MIN ? tsa::k_mid<1, tsa::PROD_MIN> : tsa::k_mid<1, tsa::SUM>)
                          : (a.mode == tsa::PROD_MAX ? tsa::k_mid<2, tsa::PROD_MAX>
                             : a.mode == tsa::PROD_MIN ? tsa::k_mid<2, tsa::PROD_MIN> : tsa::k_mid<2, tsa::SUM>);
     if (sm > 48 * 1024) cudaFuncSetAttribute(mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    mid<<<(unsigned)p->nz, tsa::kTableThreads, sm, s>>>(a);
-    TSA_TRY(check_cuda("k_mid"));
-    if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, s));
-    return TSA_OK;
+    cfg.gridDim = dim3((unsigned)p->nz);
+    cfg.blockDim = dim3(tsa::kTableThreads);
+    cfg.dynamicSmemBytes = sm;
+    TSA_CUDA(cudaLaunchKernelEx(&cfg, mid, a));
+    if (out->labels) {
+      cfg.gridDim = dim3((unsigned)a.LC, (unsigned)p->nz);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = 0;
+      if (p->dtype == TSA_U8) TSA_CUDA(cudaLaunchKernelEx(&cfg, tsa::k_label_part<uint8_t>, a));
+      else TSA_CUDA(cudaLaunchKernelEx(&cfg, tsa::k_label_part<uint16_t>, a));
+    }
+    return check_cuda("compact path");
   }
   TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
   const size_t smem = std::max(smem_h, smem_m) + 64;

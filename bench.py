@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--buffers", type=int, default=0, help="resident volume copies rotated (0 = auto, > 2x L2)")
+    ap.add_argument("--shard", default="slices", choices=["slices", "tuples"],
+                    help="slices: every rank segments its own volume (weak scaling); tuples: the "
+                         "ranks split the tuple space of one volume, NCCL all-gathers (strong)")
+    ap.add_argument("--pipeline", default="auto", choices=["auto", "compact", "fused", "staged"])
     return ap.parse_args()
 
 
@@ -200,6 +204,70 @@ def config_of(cfg, args, world):
             "l2": "inputs larger than L2: rotating resident volume/label copies (> 2x 126 MB)"}
 
 
+def run_tuple_sharded(args, cfg, rank, world, dev):
+    """One volume, tuple space split over the ranks:
+    histogram all-gather, per-rank search over its work units of every slice,
+    (score, key) all-gather, merge/finalize, labels of the own slab."""
+    import numpy as np
+    import torch
+
+    import phantom
+    import paper_2012_10684_b200 as tsa
+    from paper_2012_10684_b200.dist import segment_tuple_sharded, slab_range
+
+    if world > 1:
+        import torch.distributed as dist
+    else:
+        import torch.distributed as dist
+
+        import socket
+
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    q = cfg.qs[0]
+    z0, z1 = slab_range(cfg.nz, world, rank)
+    host = phantom.make_volume(cfg, nz=z1 - z0, z_first=z0) if z1 > z0 else \
+        np.zeros((0, cfg.ny, cfg.nx), cfg.np_dtype)
+    slab = torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+    ws = None
+    for _ in range(max(args.warmup, 3)):
+        segment_tuple_sharded(slab, cfg.nz, cfg.bins, cfg.k, q, enumeration=args.enumeration)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        out = segment_tuple_sharded(slab, cfg.nz, cfg.bins, cfg.k, q, enumeration=args.enumeration)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev) if world > 1 else e0.elapsed_time(e1)
+    ms_step = ms / args.steps
+    from math import comb
+
+    hist = out["histogram"].cpu().numpy()
+    m = (hist > 0).sum(axis=1)
+    evaluated = int(sum(comb(int(x) - 1, cfg.k) for x in m)) if args.enumeration == "canonical" \
+        else cfg.nz * comb(cfg.bins - 1, cfg.k)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": cfg.nz / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_of(cfg, args, world),
+                           parallelism=f"tuple space of every slice split over {world} GPU(s); "
+                                       "NCCL all-gather of histograms and (score, key) partials"),
+            "gtuples_per_s_nominal": cfg.nz * comb(cfg.bins - 1, cfg.k) / (ms_step * 1e-3) / 1e9,
+            "gtuples_per_s_evaluated": evaluated / (ms_step * 1e-3) / 1e9,
+            "gpu_launches": None, "units": out["units"],
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     import phantom
@@ -224,6 +292,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+    if args.shard == "tuples":
+        run_tuple_sharded(args, cfg, rank, world, dev)
+        return
     q = cfg.qs[0]
     k, bins = cfg.k, cfg.bins
     host = phantom.make_volume(cfg)
@@ -232,7 +303,7 @@ def main():
     # resident copies so that consecutive steps never hit L2 (126 MB)
     nbuf = args.buffers or max(2, int(np.ceil(2 * 126e6 / (vol_bytes + n_vox))) + 1)
     vols = [torch.from_numpy(host).to(dev) for _ in range(nbuf)]
-    p = tsa.make_problem(vols[0], bins, k, q, enumeration=args.enumeration)
+    p = tsa.make_problem(vols[0], bins, k, q, enumeration=args.enumeration, pipeline=args.pipeline)
     ws = tsa.workspace_for(p, dev)
     outs = []
     for i in range(nbuf):
@@ -247,7 +318,7 @@ def main():
 
     def step(i):
         tsa.tsa_segment(vols[i % nbuf], bins, k, q, enumeration=args.enumeration, out=outs[i % nbuf],
-                        workspace=ws, stream=stream)
+                        workspace=ws, stream=stream, pipeline=args.pipeline)
 
     sampler = ClockSampler(local)
     sampler.start()

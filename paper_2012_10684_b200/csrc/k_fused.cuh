@@ -489,9 +489,31 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
 //   k_label_part  (chunk, slice): waits mdone[z]; labels
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+#ifdef TSA_TRACE
+__device__ __forceinline__ void trace_rec(int type, int z, unsigned long long t0) {
+  if (threadIdx.x != 0) return;
+  const int slot = atomicAdd(&g_trace_n, 1);
+  if (slot < 65536) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[5 * slot + 0] = type;
+    g_trace[5 * slot + 1] = (unsigned long long)z;
+    g_trace[5 * slot + 2] = smid;
+    g_trace[5 * slot + 3] = t0;
+    g_trace[5 * slot + 4] = gtimer();
+  }
+}
+#define TRACE_T0 const unsigned long long _t0 = gtimer();
+#define TRACE_END(type, z) trace_rec(type, z, _t0);
+#else
+#define TRACE_T0
+#define TRACE_END(type, z)
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
+  TRACE_T0
   pdl_trigger();
   // LUT share of this CTA first (k_mid waits for all of them)
   const int64_t G = (int64_t)gridDim.x * gridDim.y;
@@ -510,18 +532,23 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   __syncthreads();
   if (threadIdx.x == 0 && g.counters) signal_add(g.counters + 1, 1);
   fused_hist<T>(g, blockIdx.y, blockIdx.x, reinterpret_cast<uint32_t *>(fsm));
+  TRACE_END(1, blockIdx.y)
 }
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(512) k_mid(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
+  TRACE_T0
   pdl_trigger();
   fused_mid<K, MODE>(g, blockIdx.x, fsm);
+  TRACE_END(2, blockIdx.x)
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_label_part(FusedArgs g) {
+  TRACE_T0
   fused_label<T>(g, blockIdx.y, blockIdx.x);
+  TRACE_END(3, blockIdx.y)
 }
 
 }  // namespace tsa

@@ -1,0 +1,122 @@
+"""Multi-GPU execution of the hot path ("job
+distribution ... reduction of results from different devices").
+
+One process per GPU, torch.distributed process group (NCCL over NVLink on the
+B200 box; gloo for the CPU tests of the host logic).  Two strategies:
+
+* slab sharding (``segment_slabs``): rank r segments slices
+  [slab_range(nz, P, r)) with no data-path collective -- slices are
+  independent problems.
+* tuple sharding (``segment_tuple_sharded``): every rank needs the same
+  per-slice argmax over a tuple space too large for one GPU (k = 4).  Each rank
+  histograms its slab, the histograms are all-gathered (nz*L*4 bytes), each
+  rank runs the exhaustive search over its share of the work units of *every*
+  slice, the per-slice (score, key) partials are all-gathered (16 B per slice
+  per rank) and merged under the total order (score desc, key asc) by
+  ``tsa_finalize``.  The unit partition is rank-independent, so the result is
+  bit-identical to the 1-GPU result for any world size.
+
+The collectives move only small host-independent tensors; every step of the
+path itself runs in the libtsa kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import (tsa_default_units, tsa_finalize, tsa_histogram, tsa_label, tsa_merge, tsa_search,
+               tsa_segment, ENUMERATIONS)
+
+
+def slab_range(nz: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous slab [z0, z1) of rank `rank`: ceil(nz/P) slices per rank,
+    the last ranks possibly fewer (or none)."""
+    per = -(-nz // world)
+    z0 = min(nz, rank * per)
+    return z0, min(nz, z0 + per)
+
+
+def unit_range(units: int, world: int, rank: int) -> tuple[int, int]:
+    """Work units [u0, u1) of rank `rank` out of `units` per slice (balanced,
+    disjoint, covering)."""
+    return units * rank // world, units * (rank + 1) // world
+
+
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """all_gather_into_tensor; gloo cannot gather CUDA tensors, so route them
+    through host memory there (tests only: NCCL is the production backend)."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def gather_rows(local: torch.Tensor, rows_per_rank: int, group=None) -> torch.Tensor:
+    """All-gather equally sized row blocks (rank-major).  `local` is padded to
+    `rows_per_rank` rows with zeros; returns [world * rows_per_rank, ...]."""
+    world = dist.get_world_size(group)
+    if local.shape[0] < rows_per_rank:
+        pad = torch.zeros((rows_per_rank - local.shape[0],) + tuple(local.shape[1:]),
+                          dtype=local.dtype, device=local.device)
+        local = torch.cat([local, pad])
+    out = torch.empty((world * rows_per_rank,) + tuple(local.shape[1:]), dtype=local.dtype,
+                      device=local.device)
+    _all_gather(out, local.contiguous(), group)
+    return out
+
+
+def gather_partials(score: torch.Tensor, key: torch.Tensor, group=None):
+    """All-gather per-slice partial argmax results: [nz] -> [world, nz]."""
+    world = dist.get_world_size(group)
+    n = score.shape[0]
+    s = torch.empty(world * n, dtype=score.dtype, device=score.device)
+    k = torch.empty(world * n, dtype=key.dtype, device=key.device)
+    _all_gather(s, score.contiguous(), group)
+    _all_gather(k, key.contiguous(), group)
+    return s.view(world, n), k.view(world, n)
+
+
+def segment_slabs(vol_slab, bins, k, q, **kw):
+    """Slab sharding: this rank's slices only, no collective."""
+    return tsa_segment(vol_slab, bins, k, q, **kw)
+
+
+def segment_tuple_sharded(vol_slab, nz_total, bins, k, q, objective="pseudo_additive",
+                          enumeration="canonical", units=0, group=None, labels=True,
+                          workspace=None):
+    """Tuple sharding across the group.  `vol_slab` is this rank's slab
+    (slab_range(nz_total, P, rank)) on this rank's GPU.  Returns the full
+    per-slice results (thresholds/objective/status for all nz_total slices,
+    identical on every rank) and this rank's labels."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per = -(-nz_total // world)
+    dev = vol_slab.device
+    ny, nx = vol_slab.shape[1], vol_slab.shape[2]
+    if vol_slab.shape[0] > 0:
+        hist_l, st_l = tsa_histogram(vol_slab, bins)
+    else:
+        hist_l = torch.zeros((0, bins), dtype=torch.int32, device=dev)
+        st_l = torch.zeros(0, dtype=torch.int32, device=dev)
+    hist = gather_rows(hist_l, per, group)[:nz_total].contiguous()
+    status = gather_rows(st_l, per, group)[:nz_total].contiguous()
+    enum = ENUMERATIONS.get(enumeration, enumeration)
+    U = units if units > 0 else max(world, tsa_default_units(nz_total, bins, k, enum))
+    u0, u1 = unit_range(U, world, rank)
+    if u1 > u0:
+        ps, pk = tsa_search(hist, status, nx * ny, k, q, objective, enumeration, units=U,
+                            unit_begin=u0, unit_end=u1, workspace=workspace)
+        s_loc, k_loc = tsa_merge(ps, pk)
+    else:  # more ranks than units: contribute "no tuple"
+        s_loc = torch.full((nz_total,), float("-inf"), dtype=torch.float64, device=dev)
+        k_loc = torch.full((nz_total,), -1, dtype=torch.int64, device=dev)
+    ps_all, pk_all = gather_partials(s_loc, k_loc, group)
+    thr, phi, st = tsa_finalize(hist, status, k, q, ps_all, pk_all, objective=objective)
+    z0, z1 = slab_range(nz_total, world, rank)
+    lab = None
+    if labels and z1 > z0:
+        lab = tsa_label(vol_slab, thr[z0:z1].contiguous(), st[z0:z1].contiguous(), bins=bins)
+    return {"thresholds": thr, "objective": phi, "status": st, "histogram": hist, "labels": lab,
+            "units": U, "unit_range": (u0, u1), "slab": (z0, z1)}

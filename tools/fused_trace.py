@@ -17,22 +17,23 @@ lib = tsa.load()
 lib.tsa_debug_trace.restype = ctypes.c_int
 lib.tsa_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-sb = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-dl = int(sys.argv[3]) if len(sys.argv) > 3 else 6
+pipe = sys.argv[2] if len(sys.argv) > 2 else "fused"
+sb = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+dl = int(sys.argv[4]) if len(sys.argv) > 4 else 6
 cfg = phantom.CONFIGS[name]
 vol = torch.from_numpy(phantom.make_volume(cfg)).cuda()
 for _ in range(3):
-    tsa.tsa_segment(vol, cfg.bins, cfg.k, cfg.qs[0], pipeline="fused", slab_slices=sb, label_lag=dl)
+    tsa.tsa_segment(vol, cfg.bins, cfg.k, cfg.qs[0], pipeline=pipe, slab_slices=sb, label_lag=dl)
 torch.cuda.synchronize()
 buf = np.zeros(5 * 65536, np.uint64)
 lib.tsa_debug_trace(buf.ctypes.data, 65536)  # reset
-tsa.tsa_segment(vol, cfg.bins, cfg.k, cfg.qs[0], pipeline="fused", slab_slices=sb, label_lag=dl)
+tsa.tsa_segment(vol, cfg.bins, cfg.k, cfg.qs[0], pipeline=pipe, slab_slices=sb, label_lag=dl)
 torch.cuda.synchronize()
 n = lib.tsa_debug_trace(buf.ctypes.data, 65536)
 tr = buf[: 5 * n].reshape(n, 5).astype(np.int64)
 t0 = tr[:, 3].min()
 span = (tr[:, 4].max() - t0) / 1e3
-print(f"{name} sb={sb} dl={dl}: {n} tasks, kernel span {span:.1f} us")
+print(f"{name} {pipe} sb={sb} dl={dl}: {n} tasks, kernel span {span:.1f} us")
 for ty, nm in ((0, "LUT/noop"), (1, "H"), (2, "M"), (3, "L")):
     m = tr[:, 0] == ty
     if not m.any():

@@ -30,6 +30,7 @@ namespace tsa {
 struct SearchArgs {
   const uint32_t *C;
   const double *Whi, *Wlo, *Asuf, *R;
+  const double *PP, *AI;  // k >= 3 prefix tables (k_rtable): PP[x][y] = T(0,x) (x) T(x+1,y), AI[x][y] = T(x,y)
   const int32_t *Bin, *Mz, *status;
   double *part_score;  // [nunits][nz]
   uint64_t *part_key;
@@ -219,6 +220,57 @@ __device__ __forceinline__ unsigned cmp4(unsigned hit, double pre, double2 x, do
   return hit;
 }
 
+template <int MODE>
+__device__ __forceinline__ unsigned cmp8(unsigned hit, double pre, double2 x0, double2 x1, double2 x2,
+                                         double2 x3, double best) {
+  if (MODE == SUM) {
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "add.rn.f64 t0, %1, %2;\n\tadd.rn.f64 t1, %1, %3;\n\tadd.rn.f64 t2, %1, %4;\n\t"
+        "add.rn.f64 t3, %1, %5;\n\tadd.rn.f64 t4, %1, %6;\n\tadd.rn.f64 t5, %1, %7;\n\t"
+        "add.rn.f64 t6, %1, %8;\n\tadd.rn.f64 t7, %1, %9;\n\t"
+        "setp.ge.or.f64 p, t0, %10, p;\n\tsetp.ge.or.f64 p, t1, %10, p;\n\t"
+        "setp.ge.or.f64 p, t2, %10, p;\n\tsetp.ge.or.f64 p, t3, %10, p;\n\t"
+        "setp.ge.or.f64 p, t4, %10, p;\n\tsetp.ge.or.f64 p, t5, %10, p;\n\t"
+        "setp.ge.or.f64 p, t6, %10, p;\n\tsetp.ge.or.f64 p, t7, %10, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "+r"(hit)
+        : "d"(pre), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y), "d"(x3.x),
+          "d"(x3.y), "d"(best));
+  } else {
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "mul.rn.f64 t0, %1, %2;\n\tmul.rn.f64 t1, %1, %3;\n\tmul.rn.f64 t2, %1, %4;\n\t"
+        "mul.rn.f64 t3, %1, %5;\n\tmul.rn.f64 t4, %1, %6;\n\tmul.rn.f64 t5, %1, %7;\n\t"
+        "mul.rn.f64 t6, %1, %8;\n\tmul.rn.f64 t7, %1, %9;\n\t"
+        "setp.ge.or.f64 p, t0, %10, p;\n\tsetp.ge.or.f64 p, t1, %10, p;\n\t"
+        "setp.ge.or.f64 p, t2, %10, p;\n\tsetp.ge.or.f64 p, t3, %10, p;\n\t"
+        "setp.ge.or.f64 p, t4, %10, p;\n\tsetp.ge.or.f64 p, t5, %10, p;\n\t"
+        "setp.ge.or.f64 p, t6, %10, p;\n\tsetp.ge.or.f64 p, t7, %10, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "+r"(hit)
+        : "d"(pre), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y), "d"(x3.x),
+          "d"(x3.y), "d"(best));
+  }
+  return hit;
+}
+
+// Colex successor of an R-combination (no upper bound check: callers bound
+// the rank range).
+template <int R>
+__device__ __forceinline__ void next_colex(int *idx) {
+#pragma unroll
+  for (int j = 0; j < R; j++) {
+    if (j == R - 1 || idx[j] + 1 < idx[j + 1]) {
+      idx[j]++;
+#pragma unroll
+      for (int i = 0; i < R; i++)
+        if (i < j) idx[i] = i;
+      return;
+    }
+  }
+}
+
 // Exhaustive search for k >= 3 with the R table (pseudo-additive, q != 1 or
 // q == 1).  One thread per row (a (k-1)-prefix ending at a = t_{k-1}); rows
 // in colex order so neighbouring lanes share a and read the same R row (L1
@@ -228,7 +280,7 @@ __device__ __forceinline__ unsigned cmp4(unsigned hit, double pre, double2 x, do
 // row rescanned with the full (score, key) total order, so the result equals
 // the lowest tuple among the maxima exactly.
 template <int K, int MODE>
-__global__ void __launch_bounds__(256) k_search_rows(SearchArgs g) {
+__global__ void __launch_bounds__(256, 2) k_search_rows(SearchArgs g) {
   static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
   constexpr int R = K - 1;
   const int z = blockIdx.y;
@@ -246,40 +298,46 @@ __global__ void __launch_bounds__(256) k_search_rows(SearchArgs g) {
     const uint64_t NR = binom((uint64_t)P, R);
     const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
     const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
-    for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    // each thread walks CH consecutive colex ranks (unrank once, then successor);
+    // the 32*CH ranks of a warp share their last element a for all but the
+    // smallest a, so the R row reads are warp-broadcast
+    constexpr int CH = 4;
+    const double *PPz = g.PP + (size_t)z * g.L * g.RS;
+    const double *AIz = K == 4 ? g.AI + (size_t)z * g.L * g.RS : nullptr;
+    for (uint64_t rb = r0 + (uint64_t)threadIdx.x * CH; rb < r1; rb += (uint64_t)blockDim.x * CH) {
       int idx[R];
-      unrank_colex<R>(r, idx);
-      const int a = idx[R - 1];
-      if (a > M - 3) continue;
-      double pre = MODE == SUM ? 0.0 : 1.0;
-      int lo = 0;
+      unrank_colex<R>(rb, idx);
+      const uint64_t re_ = min(r1, rb + CH);
+      for (uint64_t r = rb; r < re_; r++, next_colex<R>(idx)) {
+        const int a = idx[R - 1];
+        if (a > M - 3) continue;
+        // Pre = (1 (x) T(0,t1)) (x) T(t1+1,t2) [(x) T(t2+1,a)] from the tables
+        double pre = K == 3 ? PPz[(size_t)idx[0] * g.RS + a]
+                            : combine<MODE>(PPz[(size_t)idx[0] * g.RS + idx[1]],
+                                            AIz[(size_t)(idx[1] + 1) * g.RS + a]);
+        if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
+        const double *row = g.R + ((size_t)z * g.L + (size_t)a) * g.RS;
+        // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
+        // even column at or below a+1 need no bounds checks (row stride RS >= L+8)
+        const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
+        const double2 *rend = rp + ((M - 1 - ((a + 1) & ~1) + 7) >> 3) * 4;
+        unsigned hit = 0;
+        for (; rp < rend; rp += 4) {
+          const double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+          hit = cmp8<MODE>(hit, pre, x0, x1, x2, x3, best);
+        }
+        if (hit) {
+          uint64_t kp = 0;
 #pragma unroll
-      for (int j = 0; j < R; j++) {
-        pre = combine<MODE>(pre, class_term<MODE>(t, g.luts, lo, idx[j]));
-        lo = idx[j] + 1;
-      }
-      if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
-      const double *row = g.R + ((size_t)z * g.L + (size_t)a) * g.RS;
-      // columns [a+1, M-2]; entries outside are NaN, so 4-column groups from the
-      // even column at or below a+1 need no bounds checks (row stride RS >= L+4)
-      const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
-      const double2 *re = rp + ((M - 1 - ((a + 1) & ~1) + 3) >> 2) * 2;
-      unsigned hit = 0;
-      for (; rp < re; rp += 2) {
-        const double2 x = __ldg(rp), y = __ldg(rp + 1);
-        hit = cmp4<MODE>(hit, pre, x, y, best);
-      }
-      if (hit) {
-        uint64_t kp = 0;
-#pragma unroll
-        for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
-        for (int b = a + 1; b <= M - 2; b++) {
-          const double v = combine<MODE>(pre, row[b]);
-          if (v >= best) {
-            const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
-            if (better(v, key, best, bestkey)) {
-              best = v;
-              bestkey = key;
+          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
+          for (int b = a + 1; b <= M - 2; b++) {
+            const double v = combine<MODE>(pre, row[b]);
+            if (v >= best) {
+              const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+              if (better(v, key, best, bestkey)) {
+                best = v;
+                bestkey = key;
+              }
             }
           }
         }

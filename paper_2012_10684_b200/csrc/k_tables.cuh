@@ -180,23 +180,42 @@ __global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
 // pseudo-additive): the last two classes of a tuple, so the search's inner
 // loop is one multiply (or add) and one compare per tuple.  Entries b > M-2
 // of each row are padded with NaN (never selected) up to the row stride RS.
+// (See k_rtable below for the three tables.)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_rtable(const uint32_t *C, const double *Whi,
                                                 const double *Wlo, const double *Asuf,
                                                 const int32_t *Mz, const int32_t *status,
-                                                double *R, int E, int L, int RS, Luts luts) {
+                                                double *R, double *PP, double *AI, int E, int L,
+                                                int RS, Luts luts) {
+  // row x = blockIdx.x of the three k >= 3 tables (row stride RS, NaN padding):
+  //   R[x][y]  = T(x+1, y) (x) T(y+1, M-1)   last two classes,      x < y <= M-2
+  //   PP[x][y] = T(0, x) (x) T(x+1, y)        first two classes,    x < y <= M-2
+  //   AI[x][y] = T(x, y)                      one interval (k = 4), x <= y <= M-2
+  // each the same expression as the on-the-fly fold, so values are identical
   const int z = blockIdx.y;
   const int a = blockIdx.x;
   if (status[z] != kOK) return;
   const int M = Mz[z];
-  if (a > M - 3) return;
+  if (a > M - 2) return;
   SliceTables t{C + (size_t)z * E, Whi + (size_t)z * E, Wlo + (size_t)z * E, nullptr};
   const double *as = Asuf + (size_t)z * L;
-  double *row = R + ((size_t)z * L + a) * RS;
+  double *rrow = R + ((size_t)z * L + a) * RS;
+  double *prow = PP + ((size_t)z * L + a) * RS;
+  double *irow = AI ? AI + ((size_t)z * L + a) * RS : nullptr;
+  const double head = class_term<MODE>(t, luts, 0, a);
   for (int b = threadIdx.x; b < RS; b += blockDim.x) {
-    double v = CUDART_NAN;
-    if (b > a && b <= M - 2) v = combine<MODE>(class_term<MODE>(t, luts, a + 1, b), __ldg(as + b));
-    row[b] = v;
+    double r = CUDART_NAN, pp = CUDART_NAN, ai = CUDART_NAN;
+    if (b <= M - 2) {
+      if (b > a) {
+        const double mid = class_term<MODE>(t, luts, a + 1, b);
+        r = combine<MODE>(mid, __ldg(as + b));
+        pp = combine<MODE>(head, mid);
+      }
+      if (irow && b >= a) ai = class_term<MODE>(t, luts, a, b);
+    }
+    rrow[b] = r;
+    prow[b] = pp;
+    if (irow) irow[b] = ai;
   }
 }
 

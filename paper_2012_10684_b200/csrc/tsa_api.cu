@@ -91,8 +91,8 @@ int search_mode(double q, int32_t objective) {
   return q < 1.0 ? tsa::PROD_MAX : tsa::PROD_MIN;
 }
 
-// R-table row stride: >= bins + 4 (4-column groups read past M-2 into NaN) and even
-inline int rstride(int32_t bins) { return (bins + 4 + 1) & ~1; }
+// R-table row stride: >= bins + 8 (8-column groups read past M-2 into NaN) and even
+inline int rstride(int32_t bins) { return (bins + 8 + 1) & ~1; }
 
 bool use_rtable(int32_t bins, int32_t k, int32_t objective) {
   return objective == TSA_OBJ_PSEUDO_ADDITIVE && k >= 3 && bins <= 512;
@@ -103,7 +103,7 @@ struct SearchWs {
   uint32_t *cC = nullptr, *fC = nullptr;
   double *cWhi = nullptr, *cWlo = nullptr, *fWhi = nullptr, *fWlo = nullptr;
   int32_t *cBin = nullptr, *fBin = nullptr;
-  double *Asuf = nullptr, *R = nullptr;
+  double *Asuf = nullptr, *R = nullptr, *PP = nullptr, *AI = nullptr;
   int32_t *M = nullptr;
 };
 
@@ -129,7 +129,11 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   }
   w.Asuf = c.take<double>(nz * (size_t)bins);
   w.M = c.take<int32_t>(nz);
-  if (use_rtable(bins, k, objective)) w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 8);
+  if (use_rtable(bins, k, objective)) {
+    w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+    w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+    if (k >= 4) w.AI = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+  }
   return c.off;
 }
 
@@ -193,7 +197,8 @@ void launch_rtable(const SearchWs &w, const uint32_t *C, const double *Whi, cons
                    const int32_t *status, int64_t nz, int E, int L, const tsa::Luts &l,
                    cudaStream_t s) {
   dim3 grid((unsigned)L, (unsigned)nz);
-  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, E, L, rstride(L), l);
+  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, w.PP, w.AI, E, L,
+                                            rstride(L), l);
 }
 
 int g_num_sms() {
@@ -560,6 +565,8 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.Wlo = tWlo;
   a.Asuf = w.Asuf;
   a.R = w.R;
+  a.PP = w.PP;
+  a.AI = w.AI;
   a.Bin = tBin;
   a.Mz = w.M;
   a.status = slice_status;

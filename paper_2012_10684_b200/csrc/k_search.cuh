@@ -36,7 +36,8 @@ struct SearchArgs {
   uint64_t *part_key;
   Luts luts;
   int64_t nz;
-  int E, L, RS, units, unit_begin;  // RS: R-table row stride (>= L + 4, even)
+  int E, L, RS, units, unit_begin;  // RS: R-table row stride (>= L + 8, even)
+  int nunits;                        // units in this launch (unit_end - unit_begin)
 };
 
 // STAGE: copy the slice's C/W/Asuf tables to shared memory first (L <= 1024).
@@ -271,94 +272,134 @@ __device__ __forceinline__ void next_colex(int *idx) {
   }
 }
 
-// Exhaustive search for k >= 3 with the R table (pseudo-additive, q != 1 or
-// q == 1).  One thread per row (a (k-1)-prefix ending at a = t_{k-1}); rows
-// in colex order so neighbouring lanes share a and read the same R row (L1
-// broadcast).  Inner loop per tuple: v = pre (x) R[a][b] and one predicated
-// compare "v >= best" OR-accumulated into a flag -- 2 FP64-pipe instructions
-// per tuple.  Only when the flag is set (the row may hold a new best) is the
-// row rescanned with the full (score, key) total order, so the result equals
-// the lowest tuple among the maxima exactly.
-template <int K, int MODE>
-__global__ void __launch_bounds__(256, 2) k_search_rows(SearchArgs g) {
-  static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
-  constexpr int R = K - 1;
-  const int z = blockIdx.y;
-  const int u = g.unit_begin + blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double best = -CUDART_INF;
-  uint64_t bestkey = kKeyNone;
-  const int st = g.status[z];
-  const int M = g.Mz[z];
-  const int P = M - 1;
-  const SliceTables t{g.C + (size_t)z * g.E, g.Whi + (size_t)z * g.E, g.Wlo + (size_t)z * g.E,
-                      g.Asuf + (size_t)z * g.L};
-  const int32_t *bin = g.Bin + (size_t)z * g.E;
-  if (st == kOK && P >= K) {
-    const uint64_t NR = binom((uint64_t)P, R);
-    const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
-    const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
-    // each thread walks CH consecutive colex ranks (unrank once, then successor);
-    // the 32*CH ranks of a warp share their last element a for all but the
-    // smallest a, so the R row reads are warp-broadcast
-    constexpr int CH = 4;
-    const double *PPz = g.PP + (size_t)z * g.L * g.RS;
-    const double *AIz = K == 4 ? g.AI + (size_t)z * g.L * g.RS : nullptr;
-    for (uint64_t rb = r0 + (uint64_t)threadIdx.x * CH; rb < r1; rb += (uint64_t)blockDim.x * CH) {
-      int idx[R];
-      unrank_colex<R>(rb, idx);
-      const uint64_t re_ = min(r1, rb + CH);
-      for (uint64_t r = rb; r < re_; r++, next_colex<R>(idx)) {
-        const int a = idx[R - 1];
-        if (a > M - 3) continue;
-        // Pre = (1 (x) T(0,t1)) (x) T(t1+1,t2) [(x) T(t2+1,a)] from the tables
-        double pre = K == 3 ? PPz[(size_t)idx[0] * g.RS + a]
-                            : combine<MODE>(PPz[(size_t)idx[0] * g.RS + idx[1]],
-                                            AIz[(size_t)(idx[1] + 1) * g.RS + a]);
-        if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
-        const double *row = g.R + ((size_t)z * g.L + (size_t)a) * g.RS;
-        // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
-        // even column at or below a+1 need no bounds checks (row stride RS >= L+8)
-        const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
-        const double2 *rend = rp + ((M - 1 - ((a + 1) & ~1) + 7) >> 3) * 4;
-        unsigned hit = 0;
-        for (; rp < rend; rp += 4) {
-          const double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
-          hit = cmp8<MODE>(hit, pre, x0, x1, x2, x3, best);
-        }
-        if (hit) {
-          uint64_t kp = 0;
-#pragma unroll
-          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
-          for (int b = a + 1; b <= M - 2; b++) {
-            const double v = combine<MODE>(pre, row[b]);
-            if (v >= best) {
-              const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
-              if (better(v, key, best, bestkey)) {
-                best = v;
-                bestkey = key;
-              }
-            }
-          }
+// One row of the k >= 3 search: tuples (prefix, b), b in (a, M-2], value
+// pre (x) R[a][b].  Fast path: 8 columns per step, 2 FP64 instructions per
+// tuple (DMUL + DSETP.GE.OR into one predicate), next group's loads in flight
+// while the current one is compared.  Only if some value >= best is the row
+// rescanned under the exact (score, key) order.
+template <int MODE>
+__device__ __forceinline__ void search_row(const double *row, int a, int M, double pre, uint64_t kp,
+                                           const int32_t *bin, double &best, uint64_t &bestkey) {
+  // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
+  // even column at or below a+1 need no bounds checks (row stride RS >= L+8)
+  const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
+  const double2 *rend = rp + ((M - 1 - ((a + 1) & ~1) + 7) >> 3) * 4;
+  unsigned hit = 0;
+  double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+  for (;;) {
+    const bool more = rp + 4 < rend;
+    double2 y0 = x0, y1 = x1, y2 = x2, y3 = x3;
+    if (more) {
+      y0 = __ldg(rp + 4);
+      y1 = __ldg(rp + 5);
+      y2 = __ldg(rp + 6);
+      y3 = __ldg(rp + 7);
+    }
+    hit = cmp8<MODE>(hit, pre, x0, x1, x2, x3, best);
+    if (!more) break;
+    x0 = y0;
+    x1 = y1;
+    x2 = y2;
+    x3 = y3;
+    rp += 4;
+  }
+  if (hit) {
+    for (int b = a + 1; b <= M - 2; b++) {
+      const double v = combine<MODE>(pre, row[b]);
+      if (v >= best) {
+        const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+        if (better(v, key, best, bestkey)) {
+          best = v;
+          bestkey = key;
         }
       }
     }
   }
-  warp_argmax(best, bestkey);
+}
+
+__device__ __forceinline__ void block_argmax(double &best, uint64_t &key) {
   __shared__ double ss[32];
   __shared__ uint64_t sk[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  warp_argmax(best, key);
+  __syncthreads();  // previous users of ss/sk are done
   if (lane == 0) {
     ss[warp] = best;
-    sk[warp] = bestkey;
+    sk[warp] = key;
   }
   __syncthreads();
-  if (warp == 0) {
-    best = lane < nw ? ss[lane] : -CUDART_INF;
-    bestkey = lane < nw ? sk[lane] : kKeyNone;
-    warp_argmax(best, bestkey);
-    if (lane == 0) {
-      g.part_score[(size_t)blockIdx.x * g.nz + z] = best;
-      g.part_key[(size_t)blockIdx.x * g.nz + z] = bestkey;
+  best = lane < nw ? ss[lane] : -CUDART_INF;
+  key = lane < nw ? sk[lane] : kKeyNone;
+  warp_argmax(best, key);  // every warp reduces the same values: all threads agree
+}
+
+// Exhaustive search for k >= 3 with the R/PP/AI tables (pseudo-additive, q != 1
+// or q == 1).  Persistent: CTA b handles work items (slice z, unit u) b, b+G,
+// ...; in an item each thread walks CH consecutive colex rows (prefixes ending
+// at a = t_{k-1}; unrank once, then successor), so the 32*CH rows of a warp
+// share a and read the same R row (L1 broadcast).  Pre comes from the tables
+// (no class-term gathers).  After every thread's first chunk the CTA's best so
+// far seeds all threads, so later rows rarely need the exact rescan.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256, 2) k_search_rows(SearchArgs g) {
+  static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
+  constexpr int R = K - 1;
+  constexpr int CH = 4;
+  const int64_t items = g.nz * (int64_t)g.nunits;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int z = (int)(item / g.nunits);
+    const int ul = (int)(item % g.nunits);
+    const int u = g.unit_begin + ul;
+    double best = -CUDART_INF;
+    uint64_t bestkey = kKeyNone;
+    const int st = g.status[z];
+    const int M = g.Mz[z];
+    const int P = M - 1;
+    const int32_t *bin = g.Bin + (size_t)z * g.E;
+    const bool active = st == kOK && P >= K;
+    uint64_t r0 = 0, r1 = 0;
+    if (active) {
+      const uint64_t NR = binom((uint64_t)P, R);
+      r0 = NR * (uint64_t)u / (uint64_t)g.units;
+      r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
+    }
+    const double *PPz = g.PP + (size_t)z * g.L * g.RS;
+    const double *AIz = K == 4 ? g.AI + (size_t)z * g.L * g.RS : nullptr;
+    const double *Rz = g.R + (size_t)z * g.L * g.RS;
+    bool first = true;
+    for (uint64_t rb = r0 + (uint64_t)threadIdx.x * CH;; rb += (uint64_t)blockDim.x * CH) {
+      if (rb < r1) {
+        int idx[R];
+        unrank_colex<R>(rb, idx);
+        const uint64_t re_ = min(r1, rb + CH);
+        for (uint64_t r = rb; r < re_; r++, next_colex<R>(idx)) {
+          const int a = idx[R - 1];
+          if (a > M - 3) continue;
+          // Pre = (1 (x) T(0,t1)) (x) T(t1+1,t2) [(x) T(t2+1,a)] from the tables
+          double pre = K == 3 ? PPz[(size_t)idx[0] * g.RS + a]
+                              : combine<MODE>(PPz[(size_t)idx[0] * g.RS + idx[1]],
+                                              AIz[(size_t)(idx[1] + 1) * g.RS + a]);
+          if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
+          uint64_t kp = 0;
+#pragma unroll
+          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
+          search_row<MODE>(Rz + (size_t)a * g.RS, a, M, pre, kp, bin, best, bestkey);
+        }
+      }
+      if (first) {  // seed every thread with the CTA's best after one chunk each
+        first = false;
+        double b2 = best;
+        uint64_t k2 = bestkey;
+        block_argmax(b2, k2);
+        best = b2;
+        bestkey = k2;
+      }
+      if (rb >= r1) break;
+    }
+    block_argmax(best, bestkey);
+    if (threadIdx.x == 0) {
+      g.part_score[(size_t)ul * g.nz + z] = best;
+      g.part_key[(size_t)ul * g.nz + z] = bestkey;
     }
   }
 }

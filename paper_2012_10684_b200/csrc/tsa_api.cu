@@ -19,6 +19,8 @@ namespace {
 
 thread_local std::string g_last_error;
 
+int g_num_sms();
+
 tsa_status set_error(tsa_status s, const char *msg) {
   g_last_error = msg;
   return s;
@@ -160,10 +162,13 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
   // k >= 3 with the R table (even row stride for 16-byte pair loads): thread-per-row kernel
   if constexpr (MODE != tsa::SPP) {
     if (rt && k >= 3) {
+      // persistent: 2 CTAs per SM loop over (slice, unit) items
+      const int64_t items = (int64_t)grid.x * grid.y;
+      const unsigned g1 = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
       if (k == 3)
-        tsa::k_search_rows<3, MODE><<<grid, 256, 0, s>>>(a);
+        tsa::k_search_rows<3, MODE><<<g1, 256, 0, s>>>(a);
       else
-        tsa::k_search_rows<4, MODE><<<grid, 256, 0, s>>>(a);
+        tsa::k_search_rows<4, MODE><<<g1, 256, 0, s>>>(a);
       return;
     }
   }
@@ -249,11 +254,12 @@ tsa_status tsa_validate(const tsa_problem *p) {
 
 int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
   if (nz <= 0) return 1;
-  const double target = (double)g_num_sms() * 8.0;
+  const double target = (double)g_num_sms() * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
   double u = std::ceil(target / (double)nz);
-  u = std::min(u, std::max(1.0, rows / 16.0));
+  // k >= 3: a unit should fill a 256-thread CTA walking 4 rows per thread
+  u = std::min(u, std::max(1.0, rows / (k >= 3 ? 1024.0 : 16.0)));
   return (int32_t)std::max(1.0, std::min(u, 256.0));
 }
 
@@ -579,6 +585,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.RS = rstride(bins);
   a.units = units;
   a.unit_begin = unit_begin;
+  a.nunits = unit_end - unit_begin;
   dim3 grid((unsigned)(unit_end - unit_begin), (unsigned)nz);
   switch (mode) {
     case tsa::PROD_MAX: launch_search_mode<tsa::PROD_MAX>(k, a, grid, s, rt); break;

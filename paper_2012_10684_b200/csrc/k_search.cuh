@@ -221,38 +221,34 @@ __device__ __forceinline__ unsigned cmp4(unsigned hit, double pre, double2 x, do
   return hit;
 }
 
+// hit |= any(pre (x) x_i >= best) over 8 columns: 8 DMUL/DADD and 8 DSETP into
+// independent predicates (no serial predicate chain), OR-ed by a PLOP3 tree.
 template <int MODE>
 __device__ __forceinline__ unsigned cmp8(unsigned hit, double pre, double2 x0, double2 x1, double2 x2,
                                          double2 x3, double best) {
+#define TSA_CMP8_BODY(OP)                                                                        \
+  asm("{\n\t.reg .pred p0, p1, p2, p3, p4, p5, p6, p7, ph;\n\t"                                  \
+      ".reg .f64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t" OP " t0, %1, %2;\n\t" OP " t1, %1, %3;\n\t" \
+      OP " t2, %1, %4;\n\t" OP " t3, %1, %5;\n\t" OP " t4, %1, %6;\n\t" OP " t5, %1, %7;\n\t"     \
+      OP " t6, %1, %8;\n\t" OP " t7, %1, %9;\n\t"                                                 \
+      "setp.ge.f64 p0, t0, %10;\n\tsetp.ge.f64 p1, t1, %10;\n\t"                                  \
+      "setp.ge.f64 p2, t2, %10;\n\tsetp.ge.f64 p3, t3, %10;\n\t"                                  \
+      "setp.ge.f64 p4, t4, %10;\n\tsetp.ge.f64 p5, t5, %10;\n\t"                                  \
+      "setp.ge.f64 p6, t6, %10;\n\tsetp.ge.f64 p7, t7, %10;\n\t"                                  \
+      "setp.ne.u32 ph, %0, 0;\n\t"                                                                \
+      "or.pred p0, p0, p1;\n\tor.pred p2, p2, p3;\n\tor.pred p4, p4, p5;\n\t"                     \
+      "or.pred p6, p6, p7;\n\tor.pred p0, p0, p2;\n\tor.pred p4, p4, p6;\n\t"                     \
+      "or.pred p0, p0, p4;\n\tor.pred p0, p0, ph;\n\t"                                            \
+      "selp.u32 %0, 1, 0, p0;\n\t}"                                                               \
+      : "+r"(hit)                                                                                 \
+      : "d"(pre), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y), "d"(x3.x),    \
+        "d"(x3.y), "d"(best))
   if (MODE == SUM) {
-    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
-        "setp.ne.u32 p, %0, 0;\n\t"
-        "add.rn.f64 t0, %1, %2;\n\tadd.rn.f64 t1, %1, %3;\n\tadd.rn.f64 t2, %1, %4;\n\t"
-        "add.rn.f64 t3, %1, %5;\n\tadd.rn.f64 t4, %1, %6;\n\tadd.rn.f64 t5, %1, %7;\n\t"
-        "add.rn.f64 t6, %1, %8;\n\tadd.rn.f64 t7, %1, %9;\n\t"
-        "setp.ge.or.f64 p, t0, %10, p;\n\tsetp.ge.or.f64 p, t1, %10, p;\n\t"
-        "setp.ge.or.f64 p, t2, %10, p;\n\tsetp.ge.or.f64 p, t3, %10, p;\n\t"
-        "setp.ge.or.f64 p, t4, %10, p;\n\tsetp.ge.or.f64 p, t5, %10, p;\n\t"
-        "setp.ge.or.f64 p, t6, %10, p;\n\tsetp.ge.or.f64 p, t7, %10, p;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "+r"(hit)
-        : "d"(pre), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y), "d"(x3.x),
-          "d"(x3.y), "d"(best));
+    TSA_CMP8_BODY("add.rn.f64");
   } else {
-    asm("{\n\t.reg .pred p;\n\t.reg .f64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
-        "setp.ne.u32 p, %0, 0;\n\t"
-        "mul.rn.f64 t0, %1, %2;\n\tmul.rn.f64 t1, %1, %3;\n\tmul.rn.f64 t2, %1, %4;\n\t"
-        "mul.rn.f64 t3, %1, %5;\n\tmul.rn.f64 t4, %1, %6;\n\tmul.rn.f64 t5, %1, %7;\n\t"
-        "mul.rn.f64 t6, %1, %8;\n\tmul.rn.f64 t7, %1, %9;\n\t"
-        "setp.ge.or.f64 p, t0, %10, p;\n\tsetp.ge.or.f64 p, t1, %10, p;\n\t"
-        "setp.ge.or.f64 p, t2, %10, p;\n\tsetp.ge.or.f64 p, t3, %10, p;\n\t"
-        "setp.ge.or.f64 p, t4, %10, p;\n\tsetp.ge.or.f64 p, t5, %10, p;\n\t"
-        "setp.ge.or.f64 p, t6, %10, p;\n\tsetp.ge.or.f64 p, t7, %10, p;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "+r"(hit)
-        : "d"(pre), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y), "d"(x3.x),
-          "d"(x3.y), "d"(best));
+    TSA_CMP8_BODY("mul.rn.f64");
   }
+#undef TSA_CMP8_BODY
   return hit;
 }
 
@@ -283,24 +279,30 @@ __device__ __forceinline__ void search_row(const double *row, int a, int M, doub
   // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
   // even column at or below a+1 need no bounds checks (row stride RS >= L+8)
   const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
-  const double2 *rend = rp + ((M - 1 - ((a + 1) & ~1) + 7) >> 3) * 4;
+  int ng = (M - 1 - ((a + 1) & ~1) + 7) >> 3;  // 8-column groups (>= 1)
   unsigned hit = 0;
+  // two register buffers alternate (no copies): loads of group g+1 are in
+  // flight while group g is compared
   double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+  double2 y0, y1, y2, y3;
   for (;;) {
-    const bool more = rp + 4 < rend;
-    double2 y0 = x0, y1 = x1, y2 = x2, y3 = x3;
-    if (more) {
+    if (ng > 1) {
       y0 = __ldg(rp + 4);
       y1 = __ldg(rp + 5);
       y2 = __ldg(rp + 6);
       y3 = __ldg(rp + 7);
     }
     hit = cmp8<MODE>(hit, pre, x0, x1, x2, x3, best);
-    if (!more) break;
-    x0 = y0;
-    x1 = y1;
-    x2 = y2;
-    x3 = y3;
+    if (--ng == 0) break;
+    rp += 4;
+    if (ng > 1) {
+      x0 = __ldg(rp + 4);
+      x1 = __ldg(rp + 5);
+      x2 = __ldg(rp + 6);
+      x3 = __ldg(rp + 7);
+    }
+    hit = cmp8<MODE>(hit, pre, y0, y1, y2, y3, best);
+    if (--ng == 0) break;
     rp += 4;
   }
   if (hit) {
@@ -341,7 +343,7 @@ __device__ __forceinline__ void block_argmax(double &best, uint64_t &key) {
 // (no class-term gathers).  After every thread's first chunk the CTA's best so
 // far seeds all threads, so later rows rarely need the exact rescan.
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, 2) k_search_rows(SearchArgs g) {
+__global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
   static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
   constexpr int R = K - 1;
   constexpr int CH = 4;

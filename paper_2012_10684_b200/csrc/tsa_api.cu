@@ -162,9 +162,9 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
   // k >= 3 with the R table (even row stride for 16-byte pair loads): thread-per-row kernel
   if constexpr (MODE != tsa::SPP) {
     if (rt && k >= 3) {
-      // persistent: 2 CTAs per SM loop over (slice, unit) items
+      // persistent: 3 CTAs per SM loop over (slice, unit) items
       const int64_t items = (int64_t)grid.x * grid.y;
-      const unsigned g1 = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
+      const unsigned g1 = (unsigned)std::min<int64_t>(items, 3 * g_num_sms());
       if (k == 3)
         tsa::k_search_rows<3, MODE><<<g1, 256, 0, s>>>(a);
       else

@@ -273,8 +273,8 @@ __device__ __forceinline__ void next_colex(int *idx) {
 // tuple (DMUL + DSETP.GE.OR into one predicate), next group's loads in flight
 // while the current one is compared.  Only if some value >= best is the row
 // rescanned under the exact (score, key) order.
-template <int MODE>
-__device__ __forceinline__ void search_row(const double *row, int a, int M, double pre, uint64_t kp,
+template <int MODE, int R>
+__device__ __forceinline__ void search_row(const double *row, int a, int M, double pre, const int *idx,
                                            const int32_t *bin, double &best, uint64_t &bestkey) {
   // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
   // even column at or below a+1 need no bounds checks (row stride RS >= L+8)
@@ -306,6 +306,9 @@ __device__ __forceinline__ void search_row(const double *row, int a, int M, doub
     rp += 4;
   }
   if (hit) {
+    uint64_t kp = 0;
+#pragma unroll
+    for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
     for (int b = a + 1; b <= M - 2; b++) {
       const double v = combine<MODE>(pre, row[b]);
       if (v >= best) {
@@ -368,8 +371,13 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
     const double *PPz = g.PP + (size_t)z * g.L * g.RS;
     const double *AIz = K == 4 ? g.AI + (size_t)z * g.L * g.RS : nullptr;
     const double *Rz = g.R + (size_t)z * g.L * g.RS;
-    bool first = true;
-    for (uint64_t rb = r0 + (uint64_t)threadIdx.x * CH;; rb += (uint64_t)blockDim.x * CH) {
+    // uniform chunk count for the CTA: after every chunk the CTA's best so far
+    // is shared (one block reduction per 4 rows per thread), so a thread only
+    // rescans a row that may beat the best any thread has seen
+    const uint64_t span = (uint64_t)blockDim.x * CH;
+    const uint64_t nchunks = r1 > r0 ? (r1 - r0 + span - 1) / span : 0;
+    for (uint64_t ci = 0; ci < nchunks; ci++) {
+      const uint64_t rb = r0 + ci * span + (uint64_t)threadIdx.x * CH;
       if (rb < r1) {
         int idx[R];
         unrank_colex<R>(rb, idx);
@@ -382,21 +390,10 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
                               : combine<MODE>(PPz[(size_t)idx[0] * g.RS + idx[1]],
                                               AIz[(size_t)(idx[1] + 1) * g.RS + a]);
           if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
-          uint64_t kp = 0;
-#pragma unroll
-          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
-          search_row<MODE>(Rz + (size_t)a * g.RS, a, M, pre, kp, bin, best, bestkey);
+          search_row<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre, idx, bin, best, bestkey);
         }
       }
-      if (first) {  // seed every thread with the CTA's best after one chunk each
-        first = false;
-        double b2 = best;
-        uint64_t k2 = bestkey;
-        block_argmax(b2, k2);
-        best = b2;
-        bestkey = k2;
-      }
-      if (rb >= r1) break;
+      block_argmax(best, bestkey);
     }
     block_argmax(best, bestkey);
     if (threadIdx.x == 0) {

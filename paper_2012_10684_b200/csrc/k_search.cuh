@@ -382,15 +382,28 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
         int idx[R];
         unrank_colex<R>(rb, idx);
         const uint64_t re_ = min(r1, rb + CH);
-        for (uint64_t r = rb; r < re_; r++, next_colex<R>(idx)) {
+        // software pipeline across rows: the next row's Pre loads are issued
+        // before the current row's compare loop
+        auto pre_of = [&](const int *id) -> double {
+          const double p = K == 3 ? __ldg(PPz + (size_t)id[0] * g.RS + id[R - 1])
+                                  : combine<MODE>(__ldg(PPz + (size_t)id[0] * g.RS + id[1]),
+                                                  __ldg(AIz + (size_t)(id[1] + 1) * g.RS + id[R - 1]));
+          return MODE == PROD_MIN ? -p : p;  // (-pre)*R == -(pre*R) exactly
+        };
+        double pre = pre_of(idx);
+        for (uint64_t r = rb; r < re_; r++) {
+          int nidx[R];
+#pragma unroll
+          for (int j = 0; j < R; j++) nidx[j] = idx[j];
+          next_colex<R>(nidx);
+          const bool more = r + 1 < re_;
+          const double npre = more && nidx[R - 1] <= M - 3 ? pre_of(nidx) : 0.0;
           const int a = idx[R - 1];
-          if (a > M - 3) continue;
           // Pre = (1 (x) T(0,t1)) (x) T(t1+1,t2) [(x) T(t2+1,a)] from the tables
-          double pre = K == 3 ? PPz[(size_t)idx[0] * g.RS + a]
-                              : combine<MODE>(PPz[(size_t)idx[0] * g.RS + idx[1]],
-                                              AIz[(size_t)(idx[1] + 1) * g.RS + a]);
-          if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
-          search_row<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre, idx, bin, best, bestkey);
+          if (a <= M - 3) search_row<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre, idx, bin, best, bestkey);
+#pragma unroll
+          for (int j = 0; j < R; j++) idx[j] = nidx[j];
+          pre = npre;
         }
       }
       block_argmax(best, bestkey);

@@ -165,10 +165,15 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
       // persistent: 3 CTAs per SM loop over (slice, unit) items
       const int64_t items = (int64_t)grid.x * grid.y;
       const unsigned g1 = (unsigned)std::min<int64_t>(items, 3 * g_num_sms());
-      if (k == 3)
+      const unsigned g2 = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
+      if (a.L <= 256) {  // warp-cooperative kernel: R row in registers (8 per lane)
+        if (k == 3) tsa::k_search_warp<3, MODE, 8><<<g2, 256, 0, s>>>(a);
+        else tsa::k_search_warp<4, MODE, 8><<<g2, 256, 0, s>>>(a);
+      } else if (k == 3) {
         tsa::k_search_rows<3, MODE><<<g1, 256, 0, s>>>(a);
-      else
+      } else {
         tsa::k_search_rows<4, MODE><<<g1, 256, 0, s>>>(a);
+      }
       return;
     }
   }

@@ -537,201 +537,4 @@ __global__ void __launch_bounds__(256) k_search_flat(SearchArgs g) {
 
 namespace tsa {
 
-// hit |= any(pp (x) rv[j] >= best), j < J: J DMUL/DADD + J DSETP into
-// independent predicates, OR-ed by PLOP3s (no serial predicate chain).
-template <int MODE>
-__device__ __forceinline__ unsigned cmp2(unsigned hit, double pp, double r0, double r1, double best) {
-  if (MODE == SUM)
-    asm("{\n\t.reg .pred p0, p1, ph;\n\t.reg .f64 t0, t1;\n\t"
-        "add.rn.f64 t0, %1, %2;\n\tadd.rn.f64 t1, %1, %3;\n\t"
-        "setp.ge.f64 p0, t0, %4;\n\tsetp.ge.f64 p1, t1, %4;\n\tsetp.ne.u32 ph, %0, 0;\n\t"
-        "or.pred p0, p0, p1;\n\tor.pred p0, p0, ph;\n\tselp.u32 %0, 1, 0, p0;\n\t}"
-        : "+r"(hit) : "d"(pp), "d"(r0), "d"(r1), "d"(best));
-  else
-    asm("{\n\t.reg .pred p0, p1, ph;\n\t.reg .f64 t0, t1;\n\t"
-        "mul.rn.f64 t0, %1, %2;\n\tmul.rn.f64 t1, %1, %3;\n\t"
-        "setp.ge.f64 p0, t0, %4;\n\tsetp.ge.f64 p1, t1, %4;\n\tsetp.ne.u32 ph, %0, 0;\n\t"
-        "or.pred p0, p0, p1;\n\tor.pred p0, p0, ph;\n\tselp.u32 %0, 1, 0, p0;\n\t}"
-        : "+r"(hit) : "d"(pp), "d"(r0), "d"(r1), "d"(best));
-  return hit;
-}
-
-// One group: prefixes spre[pf..pl] (shared memory, broadcast reads, two per
-// LDS.128) times this lane's J register columns rv[0..J).
-template <int MODE, int J>
-__device__ __forceinline__ unsigned group_cmp(const double *spre, int pf, int pl, const double *rv,
-                                              double best) {
-  unsigned hit = 0;
-  int p = pf;
-  if (p & 1) {  // align to a pair
-    const double pp = spre[p];
-#pragma unroll
-    for (int j = 0; j + 1 < J; j += 2) hit = cmp2<MODE>(hit, pp, rv[j], rv[j + 1], best);
-    if (J & 1) hit = cmp2<MODE>(hit, pp, rv[J - 1], CUDART_NAN, best);
-    p++;
-  }
-  for (; p + 1 <= pl; p += 2) {
-    const double2 q = *reinterpret_cast<const double2 *>(spre + p);
-#pragma unroll
-    for (int j = 0; j + 1 < J; j += 2) {
-      hit = cmp2<MODE>(hit, q.x, rv[j], rv[j + 1], best);
-      hit = cmp2<MODE>(hit, q.y, rv[j], rv[j + 1], best);
-    }
-    if (J & 1) hit = cmp2<MODE>(hit, q.x, rv[J - 1], CUDART_NAN, best), hit = cmp2<MODE>(hit, q.y, rv[J - 1], CUDART_NAN, best);
-  }
-  if (p == pl) {
-    const double pp = spre[p];
-#pragma unroll
-    for (int j = 0; j + 1 < J; j += 2) hit = cmp2<MODE>(hit, pp, rv[j], rv[j + 1], best);
-    if (J & 1) hit = cmp2<MODE>(hit, pp, rv[J - 1], CUDART_NAN, best);
-  }
-  return hit;
-}
-
-template <int MODE, int JMAX>
-__device__ __forceinline__ unsigned group_cmp_dispatch(int J, const double *spre, int pf, int pl,
-                                                       const double *rv, double best) {
-  switch (J) {
-    case 1: return group_cmp<MODE, 1>(spre, pf, pl, rv, best);
-    case 2: return group_cmp<MODE, 2>(spre, pf, pl, rv, best);
-    case 3: return group_cmp<MODE, 3>(spre, pf, pl, rv, best);
-    case 4: return group_cmp<MODE, 4>(spre, pf, pl, rv, best);
-    case 5: return group_cmp<MODE, 5 <= JMAX ? 5 : JMAX>(spre, pf, pl, rv, best);
-    case 6: return group_cmp<MODE, 6 <= JMAX ? 6 : JMAX>(spre, pf, pl, rv, best);
-    case 7: return group_cmp<MODE, 7 <= JMAX ? 7 : JMAX>(spre, pf, pl, rv, best);
-    default: return group_cmp<MODE, JMAX>(spre, pf, pl, rv, best);
-  }
-}
-
-// Warp-cooperative exhaustive search for k >= 3 (pseudo-additive / q == 1)
-// with the R, PP, AI tables.  A warp takes 32 consecutive colex rows (one per
-// lane: a prefix t_1..t_{k-2} and a = t_{k-1}); consecutive rows sharing a form
-// a group; the group's R row is loaded once, coalesced, with lane l holding
-// columns b = a+1+l+32j in registers, and the group's prefix values are
-// broadcast from shared memory (two per LDS.128).  Per tuple: one DMUL (or
-// DADD) and one DSETP, no divergence, no per-tuple global loads.  A
-// warp-uniform exact rescan runs only when some lane saw a value >= its best;
-// the warp's best is shared after every batch so rescans stay rare.
-template <int K, int MODE, int JMAX>
-__global__ void __launch_bounds__(256, 2) k_search_warp(SearchArgs g) {
-  static_assert(K >= 3 && K <= 4, "k = 3, 4");
-  constexpr int R = K - 1;
-  __shared__ __align__(16) double s_pre[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *spre = s_pre[warp];
-  const int64_t items = g.nz * (int64_t)g.nunits;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int z = (int)(item / g.nunits);
-    const int ul = (int)(item % g.nunits);
-    const int u = g.unit_begin + ul;
-    double best = -CUDART_INF;
-    uint64_t bestkey = kKeyNone;
-    const int M = g.Mz[z];
-    const int P = M - 1;
-    const int32_t *bin = g.Bin + (size_t)z * g.E;
-    if (g.status[z] == kOK && P >= K) {
-      const uint64_t NR = binom((uint64_t)P, R);
-      const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
-      const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
-      // contiguous slice of the unit per warp, in batches of 32 rows
-      const uint64_t per = ((r1 - r0 + nw - 1) / nw + 31) / 32 * 32;
-      const uint64_t w0 = min(r1, r0 + per * warp), w1 = min(r1, w0 + per);
-      const double *PPz = g.PP + (size_t)z * g.L * g.RS;
-      const double *AIz = K == 4 ? g.AI + (size_t)z * g.L * g.RS : nullptr;
-      const double *Rz = g.R + (size_t)z * g.L * g.RS;
-      int idx[R];
-      if (w0 + lane < w1) unrank_colex<R>(w0 + lane, idx);
-      else idx[R - 1] = 0;
-      for (uint64_t rb = w0; rb < w1; rb += 32) {
-        const uint64_t r = rb + lane;
-        const bool valid = r < w1;
-        const int a = valid ? idx[R - 1] : 0x7fffffff;
-        const bool live = valid && a <= M - 3;
-        double pre = CUDART_NAN;
-        if (live) {
-          pre = K == 3 ? __ldg(PPz + (size_t)idx[0] * g.RS + a)
-                       : combine<MODE>(__ldg(PPz + (size_t)idx[0] * g.RS + idx[1]),
-                                       __ldg(AIz + (size_t)(idx[1] + 1) * g.RS + a));
-          if (MODE == PROD_MIN) pre = -pre;  // (-pre)*R == -(pre*R) exactly
-        }
-        __syncwarp();
-        spre[lane] = pre;
-        __syncwarp();
-        unsigned pending = __ballot_sync(0xffffffffu, live);
-        while (pending) {
-          const int pf = __ffs(pending) - 1;
-          const int ac = __shfl_sync(0xffffffffu, a, pf);
-          const unsigned grp = __ballot_sync(0xffffffffu, live && a == ac) & pending;
-          pending &= ~grp;
-          const int pl = 31 - __clz(grp);  // rows of a group are consecutive lanes
-          const double *row = Rz + (size_t)ac * g.RS;
-          const int J = (M - 2 - ac + 31) >> 5;
-          double rv[JMAX];
-#pragma unroll
-          for (int j = 0; j < JMAX; j++) {
-            const int b = ac + 1 + lane + 32 * j;
-            rv[j] = (j < J && b <= M - 2) ? __ldg(row + b) : CUDART_NAN;
-          }
-          const unsigned hit = group_cmp_dispatch<MODE, JMAX>(J, spre, pf, pl, rv, best);
-          if (__any_sync(0xffffffffu, hit)) {  // exact rescan of the group
-            uint64_t kp = 0;
-            if (live && a == ac) {
-#pragma unroll
-              for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
-            }
-            for (int p = pf; p <= pl; p++) {
-              const double pp = spre[p];
-              const uint64_t kq = __shfl_sync(0xffffffffu, kp, p);
-#pragma unroll
-              for (int j = 0; j < JMAX; j++) {
-                const int b = ac + 1 + lane + 32 * j;
-                if (j < J && b <= M - 2) {
-                  const double v = combine<MODE>(pp, rv[j]);
-                  if (v >= best) {
-                    const uint64_t key = (kq << 12) | (uint64_t)bin[b + 1];
-                    if (better(v, key, best, bestkey)) {
-                      best = v;
-                      bestkey = key;
-                    }
-                  }
-                }
-              }
-            }
-          }
-        }
-        // share the warp's best (keeps rescans rare)
-        double wb = best;
-        uint64_t wk = bestkey;
-        warp_argmax(wb, wk);
-        best = wb;
-        bestkey = wk;
-        // advance this lane's row by 32 colex steps
-        if (valid && rb + 32 + lane < w1) {
-          idx[0] += 32;
-          if (R == 2) {
-            while (idx[0] >= idx[1]) {
-              idx[0] -= idx[1];
-              idx[1]++;
-            }
-          } else {
-            while (idx[0] >= idx[1]) {
-              idx[0] -= idx[1];
-              idx[1]++;
-              if (idx[1] == idx[R - 1]) {
-                idx[R - 1]++;
-                idx[1] = 1;
-              }
-            }
-          }
-        }
-      }
-    }
-    block_argmax(best, bestkey);
-    if (threadIdx.x == 0) {
-      g.part_score[(size_t)ul * g.nz + z] = best;
-      g.part_key[(size_t)ul * g.nz + z] = bestkey;
-    }
-  }
-}
-
 }  // namespace tsa

@@ -166,10 +166,8 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
       const int64_t items = (int64_t)grid.x * grid.y;
       const unsigned g1 = (unsigned)std::min<int64_t>(items, 3 * g_num_sms());
       const unsigned g2 = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
-      if (a.L <= 256) {  // warp-cooperative kernel: R row in registers (8 per lane)
-        if (k == 3) tsa::k_search_warp<3, MODE, 8><<<g2, 256, 0, s>>>(a);
-        else tsa::k_search_warp<4, MODE, 8><<<g2, 256, 0, s>>>(a);
-      } else if (k == 3) {
+      (void)g2;
+      if (k == 3) {
         tsa::k_search_rows<3, MODE><<<g1, 256, 0, s>>>(a);
       } else {
         tsa::k_search_rows<4, MODE><<<g1, 256, 0, s>>>(a);

@@ -98,4 +98,55 @@ __global__ void __launch_bounds__(512) k_histogram(HistArgs g) {
   if (threadIdx.x == 0 && overflow) g.status[z] = kLevelOverflow;
 }
 
+// u16 data, large L (12-bit CT, 4096 bins): per-warp copies of 16-bit counters
+// packed two per word (atomicAdd of 1 or 1<<16), so every warp gets its own
+// copy within 128 KB of shared memory; a warp counts at most
+// (slice / chunks) / warps < 65536 voxels, so no half-word overflows.
+__global__ void __launch_bounds__(512) k_histogram_p16(HistArgs g) {
+  extern __shared__ uint32_t sh[];
+  const int z = (int)(g.z0 + blockIdx.y);
+  const int L = g.L, LW = (L + 1) / 2;
+  const int nthr = blockDim.x;
+  const int rep = (threadIdx.x >> 5) % g.replicas;
+  for (int i = threadIdx.x; i < LW * g.replicas; i += nthr) sh[i] = 0;
+  __shared__ int overflow;
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  uint32_t *bins = sh + rep * LW;
+  const uint16_t *slice = reinterpret_cast<const uint16_t *>(g.vol) + (size_t)z * g.n;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(slice);
+  int64_t head = (int64_t)(((16 - (base & 15)) & 15) / 2);
+  if (head > g.n) head = g.n;
+  const int64_t nvec = (g.n - head) / 8;
+  const int64_t tail0 = head + nvec * 8;
+  const uint4 *v4 = reinterpret_cast<const uint4 *>(slice + head);
+  const int64_t per = (nvec + g.chunks - 1) / g.chunks;
+  const int64_t v0 = per * blockIdx.x, v1 = min(nvec, v0 + per);
+  int ovf = 0;
+  auto add = [&](uint32_t b) {
+    if (b < (uint32_t)L) atomicAdd(bins + (b >> 1), 1u << ((b & 1u) << 4));
+    else ovf = 1;
+  };
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += nthr) {
+    const uint4 w = __ldcs(v4 + i);
+    add(w.x & 0xffffu); add(w.x >> 16);
+    add(w.y & 0xffffu); add(w.y >> 16);
+    add(w.z & 0xffffu); add(w.z >> 16);
+    add(w.w & 0xffffu); add(w.w >> 16);
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t i = threadIdx.x; i < head; i += nthr) add(slice[i]);
+    for (int64_t i = tail0 + threadIdx.x; i < g.n; i += nthr) add(slice[i]);
+  }
+  if (ovf) overflow = 1;
+  __syncthreads();
+  uint32_t *out = g.hist + (size_t)z * L;
+  for (int b = threadIdx.x; b < L; b += nthr) {
+    uint32_t s = 0;
+    for (int r = 0; r < g.replicas; r++) s += (sh[r * LW + (b >> 1)] >> ((b & 1) << 4)) & 0xffffu;
+    if (s) atomicAdd(out + b, s);
+  }
+  if (threadIdx.x == 0 && overflow) g.status[z] = kLevelOverflow;
+}
+
 }  // namespace tsa

@@ -42,6 +42,15 @@ __device__ __forceinline__ uint32_t swar_labelk(uint32_t w, uint32_t t0, uint32_
   return o;
 }
 
+template <int KT>
+__device__ __forceinline__ uint32_t label_ofk(int v, int t0, int t1, int t2, int t3) {
+  uint32_t l = (uint32_t)(v > t0);
+  if (KT > 1) l += (uint32_t)(v > t1);
+  if (KT > 2) l += (uint32_t)(v > t2);
+  if (KT > 3) l += (uint32_t)(v > t3);
+  return l;
+}
+
 __device__ __forceinline__ uint32_t label_of(int v, int t0, int t1, int t2, int t3) {
   return (uint32_t)(v > t0) + (uint32_t)(v > t1) + (uint32_t)(v > t2) + (uint32_t)(v > t3);
 }
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
 #pragma unroll
         for (int e = 0; e < 16; e++) {
           const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          o[e >> 2] |= label_of(v, t0, t1, t2, t3) << (8 * (e & 3));
+          o[e >> 2] |= label_ofk<KT>(v, t0, t1, t2, t3) << (8 * (e & 3));
         }
       }
       __stcs(dst + i, make_uint4(o[0], o[1], o[2], o[3]));

@@ -481,8 +481,8 @@ __device__ __forceinline__ void search_flat_k12(const SliceTables &t, const doub
 // Staged-path kernel for k <= 2 (not sum-plus-product): CTA (unit, slice)
 // stages the slice tables and Apre in shared memory, then searches its
 // tuple-rank range [T*u/U, T*(u+1)/U) with search_flat_k12.
-template <int K, int MODE>
-__global__ void __launch_bounds__(256) k_search_flat(SearchArgs g) {
+template <int K, int MODE, int NT>
+__global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
   extern __shared__ double ssh[];
   const int z = blockIdx.y;
   const int u = g.unit_begin + blockIdx.x;

@@ -179,9 +179,12 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
   if constexpr (MODE != tsa::SPP) {
     if (k <= 2) {
       const size_t smem = (size_t)(2 * a.E + 2 * a.L) * sizeof(double) + (size_t)a.E * sizeof(uint32_t);
-      auto f = k == 1 ? tsa::k_search_flat<1, MODE> : tsa::k_search_flat<2, MODE>;
+      // large tables fill shared memory: one 1024-thread CTA per SM instead
+      const bool big = a.L > 1024;
+      auto f = big ? (k == 1 ? tsa::k_search_flat<1, MODE, 1024> : tsa::k_search_flat<2, MODE, 1024>)
+                   : (k == 1 ? tsa::k_search_flat<1, MODE, 256> : tsa::k_search_flat<2, MODE, 256>);
       if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      f<<<grid, 256, smem, s>>>(a);
+      f<<<grid, big ? 1024 : 256, smem, s>>>(a);
       return;
     }
   }
@@ -471,19 +474,28 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   a.z0 = 0;
   a.L = p->bins;
   const int threads = 512;
-  // privatised copies: one per warp for small L, fewer for large L (<= 64 KB)
-  int reps = std::max(1, std::min(threads / 32, (int)(65536 / (4 * p->bins))));
+  // privatised copies: one per warp; u16 data with large L packs two 16-bit
+  // counters per word (a warp counts < 65536 voxels per launch chunk)
+  const bool pack16 = p->dtype == TSA_U16 && p->bins > 1024;
+  int reps = pack16 ? std::max(1, std::min(threads / 32, (int)(131072 / (2 * p->bins))))
+                    : std::max(1, std::min(threads / 32, (int)(65536 / (4 * p->bins))));
   a.replicas = reps;
-  const size_t smem = (size_t)reps * p->bins * 4;
+  const size_t smem = pack16 ? (size_t)reps * ((p->bins + 1) / 2) * 4 : (size_t)reps * p->bins * 4;
   const int64_t bytes_per_slice = a.n * (p->dtype == TSA_U8 ? 1 : 2);
   // ~64 KB of input per CTA (measured best for 512x512 u8 slices)
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, bytes_per_slice / 65536));
+  // packed 16-bit counters: a warp must count < 65536 voxels
+  if (pack16) chunks = (int)std::max<int64_t>(chunks, (a.n + (threads / 32) * 60000 - 1) / ((threads / 32) * 60000));
   a.chunks = chunks;
   dim3 grid((unsigned)chunks, (unsigned)p->nz);
   if (p->dtype == TSA_U8 && p->bins == 256) {
     tsa::k_histogram<uint8_t, false><<<grid, threads, smem, s>>>(a);
   } else if (p->dtype == TSA_U8) {
     tsa::k_histogram<uint8_t, true><<<grid, threads, smem, s>>>(a);
+  } else if (pack16) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(tsa::k_histogram_p16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tsa::k_histogram_p16<<<grid, threads, smem, s>>>(a);
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(tsa::k_histogram<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -676,7 +688,12 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
         default: tsa::k_label_flat<uint8_t, 4><<<(unsigned)blocks, 256, 0, s>>>(a); break;
       }
     } else {
-      tsa::k_label_flat<uint16_t, 4><<<(unsigned)blocks, 256, 0, s>>>(a);
+      switch (p->k) {
+        case 1: tsa::k_label_flat<uint16_t, 1><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        case 2: tsa::k_label_flat<uint16_t, 2><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        case 3: tsa::k_label_flat<uint16_t, 3><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+        default: tsa::k_label_flat<uint16_t, 4><<<(unsigned)blocks, 256, 0, s>>>(a); break;
+      }
     }
   } else {
     const int64_t cx = std::max<int64_t>(1, std::min<int64_t>(64, a.n / 4096));

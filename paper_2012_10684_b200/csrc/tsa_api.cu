@@ -476,7 +476,9 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   const int threads = 512;
   // privatised copies: one per warp; u16 data with large L packs two 16-bit
   // counters per word (a warp counts < 65536 voxels per launch chunk)
-  const bool pack16 = p->dtype == TSA_U16 && p->bins > 1024;
+  // (packed 16-bit copies measured 3x slower on 12-bit CT: neighbouring bins
+  // share words; kept off -- profiles/r1_c5_histogram.md)
+  const bool pack16 = false;
   int reps = pack16 ? std::max(1, std::min(threads / 32, (int)(131072 / (2 * p->bins))))
                     : std::max(1, std::min(threads / 32, (int)(65536 / (4 * p->bins))));
   a.replicas = reps;

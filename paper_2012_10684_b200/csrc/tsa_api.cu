@@ -402,10 +402,18 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     a.HC = kCompactHC;
     a.LC = kCompactLC;
     a.nlut = a.HC * (int)p->nz;  // every k_hist_part CTA computes a LUT share
-    const size_t sh = smem_h + 64, sm = smem_m + 64;
+    // tuning (compact path): slab_slices = max histogram CTAs per SM (shared-memory
+    // padding leaves thread slots for the per-slice CTAs), label_lag = k_mid threads
+    size_t sh = smem_h + 64;
+    if (p->slab_slices > 0) sh = std::max(sh, (size_t)(225 * 1024) / (size_t)p->slab_slices);
+    const size_t sm = smem_m + 64;
+    const int mid_threads = p->label_lag >= 32 ? p->label_lag : tsa::kTableThreads;
     dim3 gh((unsigned)a.HC, (unsigned)p->nz);
-    if (p->dtype == TSA_U8) tsa::k_hist_part<uint8_t><<<gh, kFusedThreads, sh, s>>>(a);
-    else {
+    if (p->dtype == TSA_U8) {
+      if (sh > 48 * 1024)
+        cudaFuncSetAttribute(tsa::k_hist_part<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+      tsa::k_hist_part<uint8_t><<<gh, kFusedThreads, sh, s>>>(a);
+    } else {
       if (sh > 48 * 1024)
         cudaFuncSetAttribute(tsa::k_hist_part<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
       tsa::k_hist_part<uint16_t><<<gh, kFusedThreads, sh, s>>>(a);
@@ -424,7 +432,7 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
                             : a.mode == tsa::PROD_MIN ? tsa::k_mid<2, tsa::PROD_MIN> : tsa::k_mid<2, tsa::SUM>);
     if (sm > 48 * 1024) cudaFuncSetAttribute(mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cfg.gridDim = dim3((unsigned)p->nz);
-    cfg.blockDim = dim3(tsa::kTableThreads);
+    cfg.blockDim = dim3((unsigned)mid_threads);
     cfg.dynamicSmemBytes = sm;
     TSA_CUDA(cudaLaunchKernelEx(&cfg, mid, a));
     if (out->labels) {

@@ -294,6 +294,73 @@ __global__ void __launch_bounds__(WARPS * 32) h_lane(const uint8_t *vol, uint32_
   }
 }
 
+
+// V8: predicated red.shared (no branches) for non-zero bytes, zero bytes
+// counted with SWAR in a register (bin 0 is ~31% of a CT slice and its
+// same-address atomics serialise).
+__device__ __forceinline__ void red_nz(uint32_t *bins, uint32_t x) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+               :: "r"((uint32_t)__cvta_generic_to_shared(bins + x)), "r"(x) : "memory");
+}
+template <int CH>
+__global__ void __launch_bounds__(512) h_prednz(const uint4 *v, uint32_t *hist, int64_t nvec_slice) {
+  __shared__ uint32_t sh[16][256];
+  const int z = blockIdx.y;
+  for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  uint32_t *b = sh[threadIdx.x >> 5];
+  const uint4 *s = v + z * nvec_slice;
+  const int64_t per = (nvec_slice + CH - 1) / CH;
+  const int64_t v0 = per * blockIdx.x, v1 = min(nvec_slice, v0 + per);
+  uint32_t zeros = 0;
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+    const uint4 w = s[i];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      zeros += zero_bytes(ws[q]);
+#pragma unroll
+      for (int j = 0; j < 4; j++) red_nz(b, (ws[q] >> (8 * j)) & 0xff);
+    }
+  }
+  atomicAdd(b, zeros);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t t = 0;
+    for (int r = 0; r < 16; r++) t += sh[r][i];
+    if (t) atomicAdd(hist + z * 256 + i, t);
+  }
+}
+// V9: plain red.shared for every byte (baseline for V8)
+__device__ __forceinline__ void red_all(uint32_t *bins, uint32_t x) {
+  asm volatile("red.shared.add.u32 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(bins + x)) : "memory");
+}
+template <int CH>
+__global__ void __launch_bounds__(512) h_redall(const uint4 *v, uint32_t *hist, int64_t nvec_slice) {
+  __shared__ uint32_t sh[16][256];
+  const int z = blockIdx.y;
+  for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  uint32_t *b = sh[threadIdx.x >> 5];
+  const uint4 *s = v + z * nvec_slice;
+  const int64_t per = (nvec_slice + CH - 1) / CH;
+  const int64_t v0 = per * blockIdx.x, v1 = min(nvec_slice, v0 + per);
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+    const uint4 w = s[i];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) red_all(b, (ws[q] >> (8 * j)) & 0xff);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t t = 0;
+    for (int r = 0; r < 16; r++) t += sh[r][i];
+    if (t) atomicAdd(hist + z * 256 + i, t);
+  }
+}
+
 // label kernels
 template <int UNROLL>
 __global__ void __launch_bounds__(256) l_swar(const uint4 *v, uint4 *out, int64_t nvec, int64_t per_slice,
@@ -443,6 +510,10 @@ int main(int argc, char **argv) {
     runl(h_lane<8, 2>, 8, 1, "lane_w8_u2_g1");
     runl(h_lane<4, 4>, 4, 6, "lane_w4_u4_g6x(2waves)");
   }
+
+  timeit("prednz_c4", [&] { h_prednz<4><<<dim3(4, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);
+  timeit("prednz_c8", [&] { h_prednz<8><<<dim3(8, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);
+  timeit("redall_c4", [&] { h_redall<4><<<dim3(4, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);
   // copy reference: a plain D2D copy of the same bytes
   timeit("memcpy_d2d", [&] { cudaMemcpyAsync(lab, d, total, cudaMemcpyDeviceToDevice); }, 2.0 * total, false);
   return 0;

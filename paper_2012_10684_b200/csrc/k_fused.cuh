@@ -514,12 +514,11 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
   TRACE_T0
-  pdl_trigger();
+  pdl_trigger();  // one wave: the per-slice kernel can launch right away
   // LUT share of this CTA first (k_mid waits for all of them)
-  const int64_t G = (int64_t)gridDim.x * gridDim.y;
-  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t G = gridDim.x;
   const int64_t N1 = g.n + 1;
-  const int64_t a = N1 * cta / G, b = N1 * (cta + 1) / G;
+  const int64_t a = N1 * blockIdx.x / G, b = N1 * (blockIdx.x + 1) / G;
   for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
     const double x = (double)m;
     if (g.luts.shannon) {
@@ -531,8 +530,15 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   }
   __syncthreads();
   if (threadIdx.x == 0 && g.counters) signal_add(g.counters + 1, 1);
-  fused_hist<T>(g, blockIdx.y, blockIdx.x, reinterpret_cast<uint32_t *>(fsm));
-  TRACE_END(1, blockIdx.y)
+  // persistent over (slice, chunk) items in slice order, so early slices
+  // complete first and their per-slice work can start while later slices are
+  // still being counted
+  const int64_t items = g.nz * (int64_t)g.HC;
+  for (int64_t it = blockIdx.x; it < items; it += G) {
+    __syncthreads();  // shared bins of the previous item are flushed
+    fused_hist<T>(g, (int)(it / g.HC), (int)(it % g.HC), reinterpret_cast<uint32_t *>(fsm));
+  }
+  TRACE_END(1, blockIdx.x)
 }
 
 template <int K, int MODE>

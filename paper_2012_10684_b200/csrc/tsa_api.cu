@@ -401,14 +401,18 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
     a.HC = kCompactHC;
     a.LC = kCompactLC;
-    a.nlut = a.HC * (int)p->nz;  // every k_hist_part CTA computes a LUT share
+    // persistent histogram grid: hist_ctas_per_sm CTAs per SM (3 leaves thread
+    // slots for the per-slice CTAs), each also computes a share of the LUT
+    const int hist_per_sm = p->slab_slices > 0 ? p->slab_slices : 3;
+    const int hgrid = (int)std::min<int64_t>((int64_t)a.HC * p->nz, (int64_t)hist_per_sm * g_num_sms());
+    a.nlut = hgrid;
     // tuning (compact path): slab_slices = max histogram CTAs per SM (shared-memory
     // padding leaves thread slots for the per-slice CTAs), label_lag = k_mid threads
     size_t sh = smem_h + 64;
-    if (p->slab_slices > 0) sh = std::max(sh, (size_t)(225 * 1024) / (size_t)p->slab_slices);
+    sh = std::max(sh, (size_t)(225 * 1024) / (size_t)hist_per_sm);
     const size_t sm = smem_m + 64;
     const int mid_threads = p->label_lag >= 32 ? p->label_lag : tsa::kTableThreads;
-    dim3 gh((unsigned)a.HC, (unsigned)p->nz);
+    dim3 gh((unsigned)hgrid);
     if (p->dtype == TSA_U8) {
       if (sh > 48 * 1024)
         cudaFuncSetAttribute(tsa::k_hist_part<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);

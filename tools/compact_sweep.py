@@ -31,7 +31,7 @@ def run(**kw):
     return e0.elapsed_time(e1) / n * 1e3
 
 
-for hs in (0, 2, 3):
+for hs in (2, 3, 4):
     for mt in (256, 512):
         print(f"{name} compact hist_ctas_per_sm={hs or 'auto'} mid_threads={mt}: "
               f"{run(pipeline='compact', slab_slices=hs, label_lag=mt):.1f} us/step", flush=True)

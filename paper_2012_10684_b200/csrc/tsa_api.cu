@@ -401,15 +401,16 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     TSA_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(int32_t) * (2 + 2 * (size_t)p->nz), s));
     a.HC = kCompactHC;
     a.LC = kCompactLC;
-    // persistent histogram grid: hist_ctas_per_sm CTAs per SM (3 leaves thread
-    // slots for the per-slice CTAs), each also computes a share of the LUT
-    const int hist_per_sm = p->slab_slices > 0 ? p->slab_slices : 3;
+    // persistent histogram grid: hist_ctas_per_sm CTAs per SM (measured best: 4,
+    // profiles/r1_compact_sweep.log), each also computes a share of the LUT
+    const int hist_per_sm = p->slab_slices > 0 ? p->slab_slices : 4;
     const int hgrid = (int)std::min<int64_t>((int64_t)a.HC * p->nz, (int64_t)hist_per_sm * g_num_sms());
     a.nlut = hgrid;
     // tuning (compact path): slab_slices = max histogram CTAs per SM (shared-memory
     // padding leaves thread slots for the per-slice CTAs), label_lag = k_mid threads
     size_t sh = smem_h + 64;
-    sh = std::max(sh, (size_t)(225 * 1024) / (size_t)hist_per_sm);
+    if (p->slab_slices > 0)  // explicit limit: pad shared memory (keeps ~30 KB for k_mid CTAs)
+      sh = std::max(sh, (size_t)(196 * 1024) / (size_t)hist_per_sm);
     const size_t sm = smem_m + 64;
     const int mid_threads = p->label_lag >= 32 ? p->label_lag : tsa::kTableThreads;
     dim3 gh((unsigned)hgrid);

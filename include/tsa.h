@@ -96,8 +96,10 @@ typedef struct {
    *                16-byte aligned volume and labels;
    *                -1 = staged: one kernel per stage (any problem);
    *                0 = compact whenever eligible, else staged
-   *   slab_slices  fused: slices per pipeline slab
-   *   label_lag    fused: rounds by which labelling trails the histogram */
+   *   slab_slices  fused: slices per pipeline slab; compact: histogram CTAs
+   *                per SM (default 4)
+   *   label_lag    fused: rounds by which labelling trails the histogram;
+   *                compact: threads of the per-slice kernel (default 256) */
   int32_t pipeline;
   int32_t slab_slices;
   int32_t label_lag;

@@ -1,0 +1,28 @@
+#!/usr/bin/env bash
+# compute-sanitizer (memcheck, racecheck, synccheck) over every pipeline on a
+# small c2 slab and a small k=4 / u16 problem.  Run under gpurun.
+set -u
+OUT=gpurun_out/sanitizer
+mkdir -p $OUT
+cat > /tmp/san_case.py <<'PY'
+import sys, os
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch
+import phantom, paper_2012_10684_b200 as tsa
+v = torch.from_numpy(phantom.make_volume(phantom.CONFIGS["c2"], nz=6, z_first=120)).cuda()
+for pipe in ("compact", "fused", "staged"):
+    for k in (1, 2):
+        tsa.tsa_segment(v, 256, k, 0.8, pipeline=pipe)
+tsa.tsa_segment(v, 256, 3, 1.0, pipeline="staged")
+tsa.tsa_segment(v, 256, 4, 1.3, pipeline="staged", enumeration="full")
+tsa.tsa_segment(v, 256, 2, 0.7, objective="sum_plus_product")
+v16 = (v.to(torch.int32) * 13).to(torch.uint16).contiguous()
+tsa.tsa_segment(v16, 4096, 2, 0.8)
+torch.cuda.synchronize()
+print("ok")
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py > $OUT/$tool.log 2>&1
+  echo "$tool exit=$?" | tee -a $OUT/summary.txt
+  tail -3 $OUT/$tool.log >> $OUT/summary.txt
+done

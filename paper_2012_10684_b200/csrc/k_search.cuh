@@ -32,6 +32,7 @@ struct SearchArgs {
   const double *Whi, *Wlo, *Asuf, *R;
   const double *PP, *AI;  // k >= 3 prefix tables (k_rtable): PP[x][y] = T(0,x) (x) T(x+1,y), AI[x][y] = T(x,y)
   const int32_t *Bin, *Mz, *status;
+  int32_t *counter;    // dynamic item counter (k >= 3 rows kernel), zeroed before launch
   double *part_score;  // [nunits][nz]
   uint64_t *part_key;
   Luts luts;
@@ -349,9 +350,15 @@ template <int K, int MODE>
 __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
   static_assert(K >= 3 && K <= 4, "rows kernel is for k = 3, 4");
   constexpr int R = K - 1;
-  constexpr int CH = 4;
+  constexpr int CH = 8;
   const int64_t items = g.nz * (int64_t)g.nunits;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+  __shared__ int s_item;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(g.counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= items) break;
     const int z = (int)(item / g.nunits);
     const int ul = (int)(item % g.nunits);
     const int u = g.unit_begin + ul;

@@ -192,30 +192,28 @@ __global__ void __launch_bounds__(256) k_rtable(const uint32_t *C, const double 
   //   PP[x][y] = T(0, x) (x) T(x+1, y)        first two classes,    x < y <= M-2
   //   AI[x][y] = T(x, y)                      one interval (k = 4), x <= y <= M-2
   // each the same expression as the on-the-fly fold, so values are identical
-  const int z = blockIdx.y;
-  const int a = blockIdx.x;
+  // one CTA per slice, threads over the flattened (row, column) entries
+  const int z = blockIdx.x;
   if (status[z] != kOK) return;
   const int M = Mz[z];
-  if (a > M - 2) return;
   SliceTables t{C + (size_t)z * E, Whi + (size_t)z * E, Wlo + (size_t)z * E, nullptr};
   const double *as = Asuf + (size_t)z * L;
-  double *rrow = R + ((size_t)z * L + a) * RS;
-  double *prow = PP + ((size_t)z * L + a) * RS;
-  double *irow = AI ? AI + ((size_t)z * L + a) * RS : nullptr;
-  const double head = class_term<MODE>(t, luts, 0, a);
-  for (int b = threadIdx.x; b < RS; b += blockDim.x) {
+  const int rows = M - 1;  // a in [0, M-2]
+  for (int64_t e = threadIdx.x; e < (int64_t)rows * RS; e += blockDim.x) {
+    const int a = (int)(e / RS), b = (int)(e % RS);
     double r = CUDART_NAN, pp = CUDART_NAN, ai = CUDART_NAN;
     if (b <= M - 2) {
       if (b > a) {
         const double mid = class_term<MODE>(t, luts, a + 1, b);
         r = combine<MODE>(mid, __ldg(as + b));
-        pp = combine<MODE>(head, mid);
+        pp = combine<MODE>(class_term<MODE>(t, luts, 0, a), mid);
       }
-      if (irow && b >= a) ai = class_term<MODE>(t, luts, a, b);
+      if (AI && b >= a) ai = class_term<MODE>(t, luts, a, b);
     }
-    rrow[b] = r;
-    prow[b] = pp;
-    if (irow) irow[b] = ai;
+    const size_t o = ((size_t)z * L + a) * RS + b;
+    R[o] = r;
+    PP[o] = pp;
+    if (AI) AI[o] = ai;
   }
 }
 

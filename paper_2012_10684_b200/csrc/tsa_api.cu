@@ -107,6 +107,7 @@ struct SearchWs {
   int32_t *cBin = nullptr, *fBin = nullptr;
   double *Asuf = nullptr, *R = nullptr, *PP = nullptr, *AI = nullptr;
   int32_t *M = nullptr;
+  int32_t *counter = nullptr;  // dynamic work-item counter of the k >= 3 search
 };
 
 size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, int32_t k,
@@ -131,6 +132,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   }
   w.Asuf = c.take<double>(nz * (size_t)bins);
   w.M = c.take<int32_t>(nz);
+  w.counter = c.take<int32_t>(1);
   if (use_rtable(bins, k, objective)) {
     w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
     w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
@@ -162,8 +164,9 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
   // k >= 3 with the R table (even row stride for 16-byte pair loads): thread-per-row kernel
   if constexpr (MODE != tsa::SPP) {
     if (rt && k >= 3) {
-      // persistent: 3 CTAs per SM loop over (slice, unit) items
+      // persistent: 3 CTAs per SM fetch (slice, unit) items dynamically
       const int64_t items = (int64_t)grid.x * grid.y;
+      cudaMemsetAsync(a.counter, 0, sizeof(int32_t), s);
       const unsigned g1 = (unsigned)std::min<int64_t>(items, 3 * g_num_sms());
       const unsigned g2 = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
       (void)g2;
@@ -207,8 +210,7 @@ template <int MODE>
 void launch_rtable(const SearchWs &w, const uint32_t *C, const double *Whi, const double *Wlo,
                    const int32_t *status, int64_t nz, int E, int L, const tsa::Luts &l,
                    cudaStream_t s) {
-  dim3 grid((unsigned)L, (unsigned)nz);
-  tsa::k_rtable<MODE><<<grid, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, w.PP, w.AI, E, L,
+  tsa::k_rtable<MODE><<<(unsigned)nz, 256, 0, s>>>(C, Whi, Wlo, w.Asuf, w.M, status, w.R, w.PP, w.AI, E, L,
                                             rstride(L), l);
 }
 
@@ -264,8 +266,8 @@ int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumerati
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
   double u = std::ceil(target / (double)nz);
-  // k >= 3: a unit should fill a 256-thread CTA walking 4 rows per thread
-  u = std::min(u, std::max(1.0, rows / (k >= 3 ? 1024.0 : 16.0)));
+  // k >= 3: a unit should fill a 256-thread CTA walking 8 rows per thread
+  u = std::min(u, std::max(1.0, rows / (k >= 3 ? 2048.0 : 16.0)));
   return (int32_t)std::max(1.0, std::min(u, 256.0));
 }
 
@@ -603,6 +605,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.R = w.R;
   a.PP = w.PP;
   a.AI = w.AI;
+  a.counter = w.counter;
   a.Bin = tBin;
   a.Mz = w.M;
   a.status = slice_status;

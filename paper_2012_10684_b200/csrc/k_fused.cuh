@@ -482,8 +482,9 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
 // HBM-bound labelling of other slices.  (A dependent grid only launches once
 // every CTA of its primary has started, so spinning dependents can never
 // starve the CTAs they wait for.)
-//   k_hist_part   (chunk, slice): its share of the 1/n^q table, then histogram
-//                 partials; signals lutdone and hdone[z]
+//   k_lut_part    the 1/n^q table over all SMs; signals lutdone
+//   k_hist_part   persistent, slice-ordered (slice, chunk) histogram partials;
+//                 signals hdone[z]
 //   k_mid         one CTA per slice: waits lutdone, hdone[z]; tables, search,
 //                 argmax, phi(t*); signals mdone[z]
 //   k_label_part  (chunk, slice): waits mdone[z]; labels
@@ -515,11 +516,25 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
   TRACE_T0
   pdl_trigger();  // one wave: the per-slice kernel can launch right away
-  // LUT share of this CTA first (k_mid waits for all of them)
   const int64_t G = gridDim.x;
+  // persistent over (slice, chunk) items in slice order, so early slices
+  // complete first and their per-slice work can start while later slices are
+  // still being counted
+  const int64_t items = g.nz * (int64_t)g.HC;
+  for (int64_t it = blockIdx.x; it < items; it += G) {
+    __syncthreads();  // shared bins of the previous item are flushed
+    fused_hist<T>(g, (int)(it / g.HC), (int)(it % g.HC), reinterpret_cast<uint32_t *>(fsm));
+  }
+  TRACE_END(1, blockIdx.x)
+}
+
+// The 1/n^q (or ln n, 1/n) table over all SMs, PDL primary of k_hist_part;
+// every CTA signals the LUT counter that k_mid waits on.
+__global__ void __launch_bounds__(256) k_lut_part(FusedArgs g) {
+  pdl_trigger();
   const int64_t N1 = g.n + 1;
-  const int64_t a = N1 * blockIdx.x / G, b = N1 * (blockIdx.x + 1) / G;
-  for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < N1;
+       m += (int64_t)gridDim.x * blockDim.x) {
     const double x = (double)m;
     if (g.luts.shannon) {
       g.lnn[m] = m == 0 ? CUDART_NAN : log(x);
@@ -530,15 +545,6 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
   }
   __syncthreads();
   if (threadIdx.x == 0 && g.counters) signal_add(g.counters + 1, 1);
-  // persistent over (slice, chunk) items in slice order, so early slices
-  // complete first and their per-slice work can start while later slices are
-  // still being counted
-  const int64_t items = g.nz * (int64_t)g.HC;
-  for (int64_t it = blockIdx.x; it < items; it += G) {
-    __syncthreads();  // shared bins of the previous item are flushed
-    fused_hist<T>(g, (int)(it / g.HC), (int)(it % g.HC), reinterpret_cast<uint32_t *>(fsm));
-  }
-  TRACE_END(1, blockIdx.x)
 }
 
 template <int K, int MODE>

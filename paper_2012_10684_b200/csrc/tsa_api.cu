@@ -404,28 +404,16 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     a.HC = kCompactHC;
     a.LC = kCompactLC;
     // persistent histogram grid: hist_ctas_per_sm CTAs per SM (measured best: 4,
-    // profiles/r1_compact_sweep.log), each also computes a share of the LUT
+    // profiles/r1_compact_sweep.log)
     const int hist_per_sm = p->slab_slices > 0 ? p->slab_slices : 4;
     const int hgrid = (int)std::min<int64_t>((int64_t)a.HC * p->nz, (int64_t)hist_per_sm * g_num_sms());
-    a.nlut = hgrid;
-    // tuning (compact path): slab_slices = max histogram CTAs per SM (shared-memory
-    // padding leaves thread slots for the per-slice CTAs), label_lag = k_mid threads
+    const int lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1 + 255) / 256, 2 * g_num_sms()));
+    a.nlut = lgrid;
     size_t sh = smem_h + 64;
     if (p->slab_slices > 0)  // explicit limit: pad shared memory (keeps ~30 KB for k_mid CTAs)
       sh = std::max(sh, (size_t)(196 * 1024) / (size_t)hist_per_sm);
     const size_t sm = smem_m + 64;
     const int mid_threads = p->label_lag >= 32 ? p->label_lag : tsa::kTableThreads;
-    dim3 gh((unsigned)hgrid);
-    if (p->dtype == TSA_U8) {
-      if (sh > 48 * 1024)
-        cudaFuncSetAttribute(tsa::k_hist_part<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-      tsa::k_hist_part<uint8_t><<<gh, kFusedThreads, sh, s>>>(a);
-    } else {
-      if (sh > 48 * 1024)
-        cudaFuncSetAttribute(tsa::k_hist_part<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-      tsa::k_hist_part<uint16_t><<<gh, kFusedThreads, sh, s>>>(a);
-    }
-    TSA_TRY(check_cuda("k_hist_part"));
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -433,6 +421,21 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    tsa::k_lut_part<<<lgrid, 256, 0, s>>>(a);
+    TSA_TRY(check_cuda("k_lut_part"));
+    cfg.gridDim = dim3((unsigned)hgrid);
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = sh;
+    if (p->dtype == TSA_U8) {
+      if (sh > 48 * 1024)
+        cudaFuncSetAttribute(tsa::k_hist_part<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+      TSA_CUDA(cudaLaunchKernelEx(&cfg, tsa::k_hist_part<uint8_t>, a));
+    } else {
+      if (sh > 48 * 1024)
+        cudaFuncSetAttribute(tsa::k_hist_part<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+      TSA_CUDA(cudaLaunchKernelEx(&cfg, tsa::k_hist_part<uint16_t>, a));
+    }
+    TSA_TRY(check_cuda("k_hist_part"));
     auto mid = p->k == 1 ? (a.mode == tsa::PROD_MAX ? tsa::k_mid<1, tsa::PROD_MAX>
                             : a.mode == tsa::PROD_MIN ? tsa::k_mid<1, tsa::PROD_MIN> : tsa::k_mid<1, tsa::SUM>)
                          : (a.mode == tsa::PROD_MAX ? tsa::k_mid<2, tsa::PROD_MAX>

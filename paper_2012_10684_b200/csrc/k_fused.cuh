@@ -285,8 +285,8 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     __syncthreads();
     TSA_MPHASE(z, 4)
     // exhaustive search over all C(M-1, K) tuples, tuple-parallel over the CTA
-    search_flat_k12<K, MODE>(t, fsh, g.luts, tBin, M, 0, binom((uint64_t)(M - 1), K), tid,
-                             blockDim.x, best, key);
+    search_flat_k12<K, MODE, 12>(t, fsh, g.luts, tBin, M, 0, binom((uint64_t)(M - 1), K), tid,
+                                 blockDim.x, best, key);
     __syncthreads();  // fsh is reused below
   }
   warp_argmax(best, key);
@@ -327,26 +327,44 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
       const double N = (double)tC[M];
       for (int j = tid; j < M; j += blockDim.x) fsh[j] = __ddiv_rn((double)(tC[j + 1] - tC[j]), N);
       __syncthreads();
-      // class c = list range [s_c, e_c)
-      int cls_start[kKMax + 2];
-      {
-        int c = 0;
-        cls_start[0] = 0;
-        // boundaries: first list index with bin > t_c
-        // (lists are short; every thread computes them)
-        int j = 0;
-        for (c = 0; c < K; c++) {
-          const int tc = c == 0 ? t0 : t1;
-          while (j < M && tBin[j + 1] <= tc) j++;
-          cls_start[c + 1] = j;
+      // class c = canonical-list range [cs, ce): boundaries by binary search
+      auto first_above = [&](int tv) {  // smallest j in [0, M] with j == M or bin_j > tv
+        int lo = 0, hi = M;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tBin[mid + 1] > tv) hi = mid;
+          else lo = mid + 1;
         }
-        cls_start[K + 1] = M;
-      }
+        return lo;
+      };
+      int cs = 0, ce = M;
       if (tid <= K) {
-        double P = 0.0;
-        for (int j = cls_start[tid]; j < cls_start[tid + 1]; j++) P = __dadd_rn(P, fsh[j]);
-        s_P[tid] = P;
+        cs = tid == 0 ? 0 : first_above(tid == 1 ? t0 : t1);
+        ce = tid == K ? M : first_above(tid == 0 ? t0 : t1);
       }
+      // sequential sums in ascending bin order (the definition's order),
+      // loads batched four at a time
+      auto seq_sum = [&](bool sub) {
+        double acc = 0.0;
+        int j = cs;
+        for (; j + 4 <= ce; j += 4) {
+          const double x0 = fsh[j], x1 = fsh[j + 1], x2 = fsh[j + 2], x3 = fsh[j + 3];
+          if (sub) {
+            acc = __dsub_rn(acc, x0);
+            acc = __dsub_rn(acc, x1);
+            acc = __dsub_rn(acc, x2);
+            acc = __dsub_rn(acc, x3);
+          } else {
+            acc = __dadd_rn(acc, x0);
+            acc = __dadd_rn(acc, x1);
+            acc = __dadd_rn(acc, x2);
+            acc = __dadd_rn(acc, x3);
+          }
+        }
+        for (; j < ce; j++) acc = sub ? __dsub_rn(acc, fsh[j]) : __dadd_rn(acc, fsh[j]);
+        return acc;
+      };
+      if (tid <= K) s_P[tid] = seq_sum(false);
       __syncthreads();
       const bool shannon = g.luts.shannon;
       for (int j = tid; j < M; j += blockDim.x) {
@@ -356,9 +374,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
       }
       __syncthreads();
       if (tid <= K) {
-        double A = 0.0;
-        for (int j = cls_start[tid]; j < cls_start[tid + 1]; j++)
-          A = shannon ? __dsub_rn(A, fsh[j]) : __dadd_rn(A, fsh[j]);
+        const double A = seq_sum(shannon);
         s_S[tid] = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(g.q, 1.0));
       }
       __syncthreads();
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(256) k_lut_part(FusedArgs g) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(512) k_mid(FusedArgs g) {
+__global__ void __launch_bounds__(256, 3) k_mid(FusedArgs g) {
   extern __shared__ __align__(16) char fsm[];
   TRACE_T0
   pdl_trigger();

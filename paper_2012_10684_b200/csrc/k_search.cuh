@@ -434,12 +434,11 @@ namespace tsa {
 // Value (same expression tree as k_search): v = (1 (x) Apre[a]) (x)
 // (T(a+1, b) (x) Asuf[b]), Apre[a] = T(0, a).  Per-thread order is not lex, so
 // every candidate is compared under the full (score, key) order.
-template <int K, int MODE>
+template <int K, int MODE, int B = 8>
 __device__ __forceinline__ void search_flat_k12(const SliceTables &t, const double *Apre,
                                                 const Luts &l, const int32_t *bin, int M,
                                                 uint64_t r0, uint64_t r1, uint64_t tid,
                                                 uint64_t nth, double &best, uint64_t &bestkey) {
-  constexpr int B = 8;
   const double ident = MODE == SUM ? 0.0 : 1.0;
   for (uint64_t rb = r0 + tid; rb < r1; rb += nth * B) {
     int aa[B], bb[B];

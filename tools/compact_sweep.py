@@ -32,6 +32,6 @@ def run(**kw):
 
 
 for hs in (2, 3, 4):
-    for mt in (256, 512):
+    for mt in (256,):
         print(f"{name} compact hist_ctas_per_sm={hs or 'auto'} mid_threads={mt}: "
               f"{run(pipeline='compact', slab_slices=hs, label_lag=mt):.1f} us/step", flush=True)

@@ -253,6 +253,42 @@ __device__ __forceinline__ unsigned cmp8(unsigned hit, double pre, double2 x0, d
   return hit;
 }
 
+// Two prefixes against the same 8 columns: 16 DMUL/DADD + 16 DSETP into
+// independent predicates, one PLOP3 tree (the column loads are shared).
+template <int MODE>
+__device__ __forceinline__ unsigned cmp8x2(unsigned hit, double p0, double p1, double2 x0, double2 x1,
+                                           double2 x2, double2 x3, double best) {
+#define TSA_CMP16_BODY(OP)                                                                        \
+  asm("{\n\t.reg .pred q0, q1, q2, q3, q4, q5, q6, q7, q8, q9, q10, q11, q12, q13, q14, q15, qh;\n\t" \
+      ".reg .f64 t0, t1, t2, t3, t4, t5, t6, t7, u0, u1, u2, u3, u4, u5, u6, u7;\n\t"               \
+      OP " t0, %1, %3;\n\t" OP " t1, %1, %4;\n\t" OP " t2, %1, %5;\n\t" OP " t3, %1, %6;\n\t"        \
+      OP " t4, %1, %7;\n\t" OP " t5, %1, %8;\n\t" OP " t6, %1, %9;\n\t" OP " t7, %1, %10;\n\t"       \
+      OP " u0, %2, %3;\n\t" OP " u1, %2, %4;\n\t" OP " u2, %2, %5;\n\t" OP " u3, %2, %6;\n\t"        \
+      OP " u4, %2, %7;\n\t" OP " u5, %2, %8;\n\t" OP " u6, %2, %9;\n\t" OP " u7, %2, %10;\n\t"       \
+      "setp.ge.f64 q0, t0, %11;\n\tsetp.ge.f64 q1, t1, %11;\n\tsetp.ge.f64 q2, t2, %11;\n\t"        \
+      "setp.ge.f64 q3, t3, %11;\n\tsetp.ge.f64 q4, t4, %11;\n\tsetp.ge.f64 q5, t5, %11;\n\t"        \
+      "setp.ge.f64 q6, t6, %11;\n\tsetp.ge.f64 q7, t7, %11;\n\tsetp.ge.f64 q8, u0, %11;\n\t"        \
+      "setp.ge.f64 q9, u1, %11;\n\tsetp.ge.f64 q10, u2, %11;\n\tsetp.ge.f64 q11, u3, %11;\n\t"      \
+      "setp.ge.f64 q12, u4, %11;\n\tsetp.ge.f64 q13, u5, %11;\n\tsetp.ge.f64 q14, u6, %11;\n\t"     \
+      "setp.ge.f64 q15, u7, %11;\n\tsetp.ne.u32 qh, %0, 0;\n\t"                                     \
+      "or.pred q0, q0, q1;\n\tor.pred q2, q2, q3;\n\tor.pred q4, q4, q5;\n\tor.pred q6, q6, q7;\n\t"  \
+      "or.pred q8, q8, q9;\n\tor.pred q10, q10, q11;\n\tor.pred q12, q12, q13;\n\t"                  \
+      "or.pred q14, q14, q15;\n\tor.pred q0, q0, q2;\n\tor.pred q4, q4, q6;\n\t"                     \
+      "or.pred q8, q8, q10;\n\tor.pred q12, q12, q14;\n\tor.pred q0, q0, q4;\n\t"                    \
+      "or.pred q8, q8, q12;\n\tor.pred q0, q0, q8;\n\tor.pred q0, q0, qh;\n\t"                       \
+      "selp.u32 %0, 1, 0, q0;\n\t}"                                                                 \
+      : "+r"(hit)                                                                                  \
+      : "d"(p0), "d"(p1), "d"(x0.x), "d"(x0.y), "d"(x1.x), "d"(x1.y), "d"(x2.x), "d"(x2.y),          \
+        "d"(x3.x), "d"(x3.y), "d"(best))
+  if (MODE == SUM) {
+    TSA_CMP16_BODY("add.rn.f64");
+  } else {
+    TSA_CMP16_BODY("mul.rn.f64");
+  }
+#undef TSA_CMP16_BODY
+  return hit;
+}
+
 // Colex successor of an R-combination (no upper bound check: callers bound
 // the rank range).
 template <int R>
@@ -317,6 +353,57 @@ __device__ __forceinline__ void search_row(const double *row, int a, int M, doub
         if (better(v, key, best, bestkey)) {
           best = v;
           bestkey = key;
+        }
+      }
+    }
+  }
+}
+
+// Two rows sharing a (consecutive colex ranks): the 8-column loads serve both.
+template <int MODE, int R>
+__device__ __forceinline__ void search_row2(const double *row, int a, int M, double pre0, double pre1,
+                                            const int *idx0, const int *idx1, const int32_t *bin,
+                                            double &best, uint64_t &bestkey) {
+  const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
+  int ng = (M - 1 - ((a + 1) & ~1) + 7) >> 3;
+  unsigned hit = 0;
+  double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+  double2 y0, y1, y2, y3;
+  for (;;) {
+    if (ng > 1) {
+      y0 = __ldg(rp + 4);
+      y1 = __ldg(rp + 5);
+      y2 = __ldg(rp + 6);
+      y3 = __ldg(rp + 7);
+    }
+    hit = cmp8x2<MODE>(hit, pre0, pre1, x0, x1, x2, x3, best);
+    if (--ng == 0) break;
+    rp += 4;
+    if (ng > 1) {
+      x0 = __ldg(rp + 4);
+      x1 = __ldg(rp + 5);
+      x2 = __ldg(rp + 6);
+      x3 = __ldg(rp + 7);
+    }
+    hit = cmp8x2<MODE>(hit, pre0, pre1, y0, y1, y2, y3, best);
+    if (--ng == 0) break;
+    rp += 4;
+  }
+  if (hit) {  // exact rescan, lower-lex row first
+    for (int which = 0; which < 2; which++) {
+      const int *idx = which == 0 ? idx0 : idx1;
+      const double pre = which == 0 ? pre0 : pre1;
+      uint64_t kp = 0;
+#pragma unroll
+      for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[j] + 1];
+      for (int b = a + 1; b <= M - 2; b++) {
+        const double v = combine<MODE>(pre, row[b]);
+        if (v >= best) {
+          const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+          if (better(v, key, best, bestkey)) {
+            best = v;
+            bestkey = key;
+          }
         }
       }
     }
@@ -397,20 +484,26 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
                                                   __ldg(AIz + (size_t)(id[1] + 1) * g.RS + id[R - 1]));
           return MODE == PROD_MIN ? -p : p;  // (-pre)*R == -(pre*R) exactly
         };
-        double pre = pre_of(idx);
-        for (uint64_t r = rb; r < re_; r++) {
+        for (uint64_t r = rb; r < re_;) {
           int nidx[R];
 #pragma unroll
           for (int j = 0; j < R; j++) nidx[j] = idx[j];
           next_colex<R>(nidx);
-          const bool more = r + 1 < re_;
-          const double npre = more && nidx[R - 1] <= M - 3 ? pre_of(nidx) : 0.0;
           const int a = idx[R - 1];
           // Pre = (1 (x) T(0,t1)) (x) T(t1+1,t2) [(x) T(t2+1,a)] from the tables
-          if (a <= M - 3) search_row<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre, idx, bin, best, bestkey);
+          if (r + 1 < re_ && nidx[R - 1] == a && a <= M - 3) {
+            search_row2<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre_of(idx), pre_of(nidx), idx, nidx, bin,
+                                 best, bestkey);
 #pragma unroll
-          for (int j = 0; j < R; j++) idx[j] = nidx[j];
-          pre = npre;
+            for (int j = 0; j < R; j++) idx[j] = nidx[j];
+            next_colex<R>(idx);
+            r += 2;
+          } else {
+            if (a <= M - 3) search_row<MODE, R>(Rz + (size_t)a * g.RS, a, M, pre_of(idx), idx, bin, best, bestkey);
+#pragma unroll
+            for (int j = 0; j < R; j++) idx[j] = nidx[j];
+            r += 1;
+          }
         }
       }
       block_argmax(best, bestkey);

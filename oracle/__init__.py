@@ -70,6 +70,14 @@ def _load():
         lib.oracle_segment.argtypes = [P, I, I64, I64, I64, I64, I64, I, I, D, I, I, I,
                                        P, P, P, P, P, P]
         lib.oracle_max_threads.restype = I
+        lib.oracle_mean3x3.restype = None
+        lib.oracle_mean3x3.argtypes = [P, I64, I64, P]
+        lib.oracle_hist2d.restype = I
+        lib.oracle_hist2d.argtypes = [P, I64, I64, I, P]
+        lib.oracle_phi2d_at.restype = D
+        lib.oracle_phi2d_at.argtypes = [P, I, D, I, I, ctypes.POINTER(I)]
+        lib.oracle_search2d.restype = I
+        lib.oracle_search2d.argtypes = [P, I, D, P, P, P, P]
         _lib = lib
     return _lib
 
@@ -155,3 +163,40 @@ def segment(vol, bins, k, q, objective=PSEUDO_ADDITIVE, level=1, z0=0, z1=None,
                            lab.ctypes.data if labels else None)
     return {"hist": hist, "thresholds": thr, "phi": phi, "gap": gap, "status": status,
             "labels": lab}
+
+
+# ---------------------------------------------------------------- 2-D (f1)
+def mean3x3(slice_u8):
+    """3x3 floor mean with replicate border (R18/R19)."""
+    f = np.ascontiguousarray(slice_u8, dtype=np.uint8)
+    g = np.empty_like(f)
+    _load().oracle_mean3x3(f.ctypes.data, f.shape[1], f.shape[0], g.ctypes.data)
+    return g
+
+
+def hist2d(slice_u8, bins):
+    """(h [bins][bins] u32 with h[i][j] = #{f=i, g=j}, status)."""
+    f = np.ascontiguousarray(slice_u8, dtype=np.uint8)
+    h = np.zeros((bins, bins), np.uint32)
+    st = _load().oracle_hist2d(f.ctypes.data, f.shape[1], f.shape[0], bins, h.ctypes.data)
+    return h, int(st)
+
+
+def phi2d_at(h, q, t, s):
+    h = np.ascontiguousarray(h, dtype=np.uint32)
+    v = ctypes.c_int(0)
+    r = _load().oracle_phi2d_at(h.ctypes.data, h.shape[0], q, t, s, ctypes.byref(v))
+    return r if v.value else None
+
+
+def search2d(h, q):
+    """Exhaustive Level-0 2-D argmax (O(L^4): small L)."""
+    h = np.ascontiguousarray(h, dtype=np.uint32)
+    t = np.zeros(1, np.int32)
+    s = np.zeros(1, np.int32)
+    phi = np.zeros(1)
+    gap = np.zeros(1)
+    st = _load().oracle_search2d(h.ctypes.data, h.shape[0], q, t.ctypes.data, s.ctypes.data,
+                                  phi.ctypes.data, gap.ctypes.data)
+    return {"status": int(st), "t": int(t[0]), "s": int(s[0]), "phi": float(phi[0]),
+            "gap": float(gap[0])}

@@ -402,3 +402,148 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ======================================================================
+ * 2-D Tsallis thresholding -- the paper's own formulation (SURVEY.md §8(f)
+ * NEXT row 1).  Plain definitions:
+ *   g(x,y) = floor( (1/9) sum_{i,j in {-1,0,1}} f(x+i, y+j) )
+ *            (the garbled f(x+i, y+i) read as f(x+i, y+j), "decimal part"
+ *            read as floor; border: replicate -- DESIGN.md R18/R19)
+ *   h(i,j) = #{(x,y): f = i, g = j},  p_ij = h / N
+ *   class 1 = {i <= t, j <= s}, class 2 = {i > t, j > s}; quadrants 2 and 4
+ *   are ignored
+ *   P_c = sum_{class c} p_ij;  H_c = (1 - sum_{class c} (p_ij/P_c)^a)/(a - 1)
+ *   (a == 1: Shannon)
+ *   phi(t,s) = H_1 + H_2 + (1-a) H_1 H_2, argmax over (t,s) in [0,L-2]^2,
+ *   lowest (t,s) on ties; only t labels: label = f > t
+ * Sums run over cells in row-major (i, then j) ascending order.
+ * ====================================================================== */
+
+/* 3x3 floor mean with replicate border of one [ny][nx] u8 slice */
+void oracle_mean3x3(const uint8_t *f, int64_t nx, int64_t ny, uint8_t *g) {
+  for (int64_t y = 0; y < ny; y++) {
+    for (int64_t x = 0; x < nx; x++) {
+      int sum = 0;
+      for (int dy = -1; dy <= 1; dy++) {
+        for (int dx = -1; dx <= 1; dx++) {
+          int64_t yy = y + dy, xx = x + dx;
+          if (yy < 0) yy = 0;
+          if (yy > ny - 1) yy = ny - 1;
+          if (xx < 0) xx = 0;
+          if (xx > nx - 1) xx = nx - 1;
+          sum += f[yy * nx + xx];
+        }
+      }
+      g[y * nx + x] = (uint8_t)(sum / 9);
+    }
+  }
+}
+
+/* h[i*L + j] over one slice; OR_LEVEL_OVERFLOW if any f >= L (not counted) */
+int oracle_hist2d(const uint8_t *f, int64_t nx, int64_t ny, int L, uint32_t *h) {
+  uint8_t *g = (uint8_t *)malloc((size_t)(nx * ny));
+  oracle_mean3x3(f, nx, ny, g);
+  int st = OR_OK;
+  for (int64_t i = 0; i < (int64_t)L * L; i++) h[i] = 0;
+  for (int64_t x = 0; x < nx * ny; x++) {
+    if (f[x] >= L || g[x] >= L) {
+      st = OR_LEVEL_OVERFLOW;
+      continue;
+    }
+    h[(int64_t)f[x] * L + g[x]] += 1;
+  }
+  free(g);
+  return st;
+}
+
+/* Tsallis entropy of the rectangle [i0,i1] x [j0,j1] of a 2-D p (row-major) */
+static double rect_entropy(const double *p, int L, int i0, int i1, int j0, int j1, double q,
+                           int *valid) {
+  double P = 0.0;
+  for (int i = i0; i <= i1; i++)
+    for (int j = j0; j <= j1; j++) P = P + p[i * L + j];
+  if (P == 0.0) {
+    *valid = 0;
+    return 0.0;
+  }
+  *valid = 1;
+  if (q == 1.0) {
+    double H = 0.0;
+    for (int i = i0; i <= i1; i++)
+      for (int j = j0; j <= j1; j++)
+        if (p[i * L + j] > 0.0) {
+          double r = p[i * L + j] / P;
+          H = H - r * log(r);
+        }
+    return H;
+  }
+  double A = 0.0;
+  for (int i = i0; i <= i1; i++)
+    for (int j = j0; j <= j1; j++)
+      if (p[i * L + j] > 0.0) A = A + pow(p[i * L + j] / P, q);
+  return (1.0 - A) / (q - 1.0);
+}
+
+static void probabilities2d(const uint32_t *h, int L, double *p) {
+  double N = 0.0;
+  for (int64_t i = 0; i < (int64_t)L * L; i++) N += (double)h[i];
+  for (int64_t i = 0; i < (int64_t)L * L; i++) p[i] = (double)h[i] / N;
+}
+
+/* phi(t,s) from the definition; *valid = 0 if a class is empty or (t,s) out of range */
+double oracle_phi2d_at(const uint32_t *h, int L, double q, int t, int s, int *valid) {
+  *valid = 0;
+  if (t < 0 || s < 0 || t > L - 2 || s > L - 2) return NAN;
+  double *p = (double *)malloc(sizeof(double) * (size_t)L * L);
+  probabilities2d(h, L, p);
+  int v1, v2;
+  double H1 = rect_entropy(p, L, 0, t, 0, s, q, &v1);
+  double H2 = rect_entropy(p, L, t + 1, L - 1, s + 1, L - 1, q, &v2);
+  free(p);
+  if (!v1 || !v2) return NAN;
+  *valid = 1;
+  return H1 + H2 + (1.0 - q) * H1 * H2;
+}
+
+/* Exhaustive 2-D search (Level 0: every candidate from the definition;
+ * O(L^4) -- small L only).  Row-major (t, then s) order, strict '>'. */
+int oracle_search2d(const uint32_t *h, int L, double q, int32_t *t_out, int32_t *s_out,
+                    double *phi_out, double *gap_out) {
+  double *p = (double *)malloc(sizeof(double) * (size_t)L * L);
+  probabilities2d(h, L, p);
+  int found = 0;
+  double best = -INFINITY, second = -INFINITY;
+  int bt = -1, bs = -1, have2 = 0;
+  for (int t = 0; t <= L - 2; t++) {
+    for (int s = 0; s <= L - 2; s++) {
+      int v1, v2;
+      double H1 = rect_entropy(p, L, 0, t, 0, s, q, &v1);
+      if (!v1) continue;
+      double H2 = rect_entropy(p, L, t + 1, L - 1, s + 1, L - 1, q, &v2);
+      if (!v2) continue;
+      double phi = H1 + H2 + (1.0 - q) * H1 * H2;
+      if (!found || phi > best) {
+        if (found) {
+          second = best;
+          have2 = 1;
+        }
+        best = phi;
+        bt = t;
+        bs = s;
+        found = 1;
+      } else if (!have2 || phi > second) {
+        second = phi;
+        have2 = 1;
+      }
+    }
+  }
+  free(p);
+  *t_out = bt;
+  *s_out = bs;
+  *phi_out = found ? best : NAN;
+  /* gap over all other candidates (2-D partitions are not deduplicated: a
+   * candidate differing only by empty rows/columns ties exactly, gap 0) */
+  *gap_out = !found ? NAN : (!have2 ? INFINITY : (best == 0.0 ? (second == 0.0 ? 0.0 : INFINITY)
+                                                              : (best - second) / fabs(best)));
+  return found ? OR_OK : OR_NO_VALID_SPLIT;
+}

@@ -11,7 +11,7 @@ while IFS= read -r mut; do
   [ -z "$mut" ] && continue
   sed "$mut" /tmp/_oracle_orig.c > oracle/tsallis_oracle.c
   python -c "import oracle; oracle.build(True)"
-  res=$(python -m pytest tests/test_oracle_pins.py -q 2>&1 | tail -1)
+  res=$(python -m pytest tests/test_oracle_pins.py tests/test_oracle_2d.py -q 2>&1 | tail -1)
   echo "$res   <= $mut"
   case "$res" in *failed*) ;; *) fail=1 ;; esac
 done <<'MUTS'
@@ -25,5 +25,8 @@ s/return sum + (1.0 - q) \* prod;/return sum + (q - 1.0) * prod;/
 s/for (int j = 1; j < nclass; j++) phi = phi/for (int j = 1; j < nclass - 1; j++) phi = phi/
 s/for (int i = a; i <= b; i++) P = P + p\[i\];/for (int i = a; i <= b; i++) P = P + p[i]; if (a > 0) P = P + p[a - 1];/
 s/if ((int)v > t\[j\]) l++;/if ((int)v >= t[j]) l++;/
+s/g\[y \* nx + x\] = (uint8_t)(sum \/ 9);/g[y * nx + x] = (uint8_t)(sum \/ 8);/
+s/double H2 = rect_entropy(p, L, t + 1, L - 1, s + 1, L - 1, q, \&v2);/double H2 = rect_entropy(p, L, t, L - 1, s + 1, L - 1, q, \&v2);/
+s/  return H1 + H2 + (1.0 - q) \* H1 \* H2;/  return H1 + H2;/
 MUTS
 exit $fail

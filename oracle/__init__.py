@@ -76,8 +76,8 @@ def _load():
         lib.oracle_hist2d.argtypes = [P, I64, I64, I, P]
         lib.oracle_phi2d_at.restype = D
         lib.oracle_phi2d_at.argtypes = [P, I, D, I, I, ctypes.POINTER(I)]
-        lib.oracle_search2d.restype = I
-        lib.oracle_search2d.argtypes = [P, I, D, P, P, P, P]
+        lib.oracle_search2d_n.restype = I
+        lib.oracle_search2d_n.argtypes = [P, I, D, I, P, P, P, P]
         _lib = lib
     return _lib
 
@@ -189,14 +189,47 @@ def phi2d_at(h, q, t, s):
     return r if v.value else None
 
 
-def search2d(h, q):
-    """Exhaustive Level-0 2-D argmax (O(L^4): small L)."""
+def search2d(h, q, threads=1):
+    """Exhaustive Level-0 2-D argmax (O(L^4); rows of candidates on `threads`
+    OpenMP threads -- the result does not depend on the thread count).
+    Returns dict(status, t, s, phi, gap); gap is over distinct partitions."""
     h = np.ascontiguousarray(h, dtype=np.uint32)
     t = np.zeros(1, np.int32)
     s = np.zeros(1, np.int32)
     phi = np.zeros(1)
     gap = np.zeros(1)
-    st = _load().oracle_search2d(h.ctypes.data, h.shape[0], q, t.ctypes.data, s.ctypes.data,
-                                  phi.ctypes.data, gap.ctypes.data)
+    st = _load().oracle_search2d_n(h.ctypes.data, h.shape[0], q, int(threads), t.ctypes.data,
+                                    s.ctypes.data, phi.ctypes.data, gap.ctypes.data)
     return {"status": int(st), "t": int(t[0]), "s": int(s[0]), "phi": float(phi[0]),
             "gap": float(gap[0])}
+
+
+def segment2d(vol, bins, q, z_list=None, threads=None, labels=True):
+    """2-D path for the slices in z_list (default all) of a u8 vol[nz][ny][nx]:
+    hist2d -> search2d -> labels = f > t (PAPER.md:597 "only t is used").
+    Arrays are indexed by absolute slice; slices not in z_list stay -1/NaN/0."""
+    v = np.ascontiguousarray(vol, dtype=np.uint8)
+    nz = v.shape[0]
+    z_list = range(nz) if z_list is None else z_list
+    threads = threads or max_threads()
+    hist = np.zeros((nz, bins, bins), np.uint32)
+    thr = np.full((nz, 2), -1, np.int32)
+    phi = np.full(nz, np.nan)
+    gap = np.full(nz, np.nan)
+    status = np.full(nz, -1, np.int32)
+    lab = np.zeros(v.shape, np.uint8) if labels else None
+    for z in z_list:
+        h, st = hist2d(v[z], bins)
+        hist[z] = h
+        if st == OK:
+            r = search2d(h, q, threads)
+            st = r["status"]
+            if st == OK:
+                thr[z] = (r["t"], r["s"])
+                phi[z] = r["phi"]
+                gap[z] = r["gap"]
+                if labels:
+                    lab[z] = label(v[z], 1, (r["t"],))
+        status[z] = st
+    return {"hist": hist, "thresholds": thr, "phi": phi, "gap": gap, "status": status,
+            "labels": lab}

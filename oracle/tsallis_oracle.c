@@ -505,45 +505,78 @@ double oracle_phi2d_at(const uint32_t *h, int L, double q, int t, int s, int *va
   return H1 + H2 + (1.0 - q) * H1 * H2;
 }
 
-/* Exhaustive 2-D search (Level 0: every candidate from the definition;
- * O(L^4) -- small L only).  Row-major (t, then s) order, strict '>'. */
-int oracle_search2d(const uint32_t *h, int L, double q, int32_t *t_out, int32_t *s_out,
-                    double *phi_out, double *gap_out) {
+/* Exhaustive 2-D search, Level 0: every candidate's phi from the definition
+ * (O(L^4); each t row of candidates is independent, so rows run on OpenMP
+ * threads, each writing its own slots -- the values do not depend on the
+ * thread count).  Then, sequentially in row-major (t, then s) order, the
+ * argmax with strict '>' (lowest (t,s) wins exact ties, "Arg
+ * max"; R8/R21).
+ * Runner-up (acceptance metadata only): best phi over candidates describing a
+ * DIFFERENT partition of the non-empty cells.  (t,s) and (t',s) give the same
+ * classes iff every row in (t, t'] is empty, and likewise for columns, so the
+ * distinct partitions are exactly the "canonical" candidates whose row t and
+ * column s are non-empty (row/column marginals of h); the lowest member of an
+ * equivalence class is canonical (R21).  gap = (phi* - phi2)/|phi*|. */
+int oracle_search2d_n(const uint32_t *h, int L, double q, int nthreads, int32_t *t_out,
+                      int32_t *s_out, double *phi_out, double *gap_out) {
+  const int M = L - 1;
   double *p = (double *)malloc(sizeof(double) * (size_t)L * L);
+  double *phi = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1) * (M > 0 ? M : 1));
+  char *ok = (char *)calloc((size_t)(M > 0 ? M : 1) * (M > 0 ? M : 1), 1);
   probabilities2d(h, L, p);
-  int found = 0;
-  double best = -INFINITY, second = -INFINITY;
-  int bt = -1, bs = -1, have2 = 0;
-  for (int t = 0; t <= L - 2; t++) {
-    for (int s = 0; s <= L - 2; s++) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+  for (int t = 0; t < M; t++) {
+    for (int s = 0; s < M; s++) {
       int v1, v2;
       double H1 = rect_entropy(p, L, 0, t, 0, s, q, &v1);
       if (!v1) continue;
       double H2 = rect_entropy(p, L, t + 1, L - 1, s + 1, L - 1, q, &v2);
       if (!v2) continue;
-      double phi = H1 + H2 + (1.0 - q) * H1 * H2;
-      if (!found || phi > best) {
-        if (found) {
-          second = best;
-          have2 = 1;
-        }
-        best = phi;
+      phi[(size_t)t * M + s] = H1 + H2 + (1.0 - q) * H1 * H2;
+      ok[(size_t)t * M + s] = 1;
+    }
+  }
+  int found = 0, bt = -1, bs = -1;
+  double best = -INFINITY;
+  for (int t = 0; t < M; t++)
+    for (int s = 0; s < M; s++)
+      if (ok[(size_t)t * M + s] && (!found || phi[(size_t)t * M + s] > best)) {
+        best = phi[(size_t)t * M + s];
         bt = t;
         bs = s;
         found = 1;
-      } else if (!have2 || phi > second) {
-        second = phi;
+      }
+  /* marginals: non-empty rows (f levels) and columns (g levels) */
+  char *rnz = (char *)calloc((size_t)L, 1), *cnz = (char *)calloc((size_t)L, 1);
+  for (int i = 0; i < L; i++)
+    for (int j = 0; j < L; j++)
+      if (h[(size_t)i * L + j]) {
+        rnz[i] = 1;
+        cnz[j] = 1;
+      }
+  int have2 = 0;
+  double second = -INFINITY;
+  for (int t = 0; t < M; t++)
+    for (int s = 0; s < M; s++)
+      if (ok[(size_t)t * M + s] && rnz[t] && cnz[s] && !(t == bt && s == bs) &&
+          (!have2 || phi[(size_t)t * M + s] > second)) {
+        second = phi[(size_t)t * M + s];
         have2 = 1;
       }
-    }
-  }
+  free(rnz);
+  free(cnz);
+  free(ok);
+  free(phi);
   free(p);
   *t_out = bt;
   *s_out = bs;
   *phi_out = found ? best : NAN;
-  /* gap over all other candidates (2-D partitions are not deduplicated: a
-   * candidate differing only by empty rows/columns ties exactly, gap 0) */
   *gap_out = !found ? NAN : (!have2 ? INFINITY : (best == 0.0 ? (second == 0.0 ? 0.0 : INFINITY)
                                                               : (best - second) / fabs(best)));
   return found ? OR_OK : OR_NO_VALID_SPLIT;
+}
+
+int oracle_search2d(const uint32_t *h, int L, double q, int32_t *t_out, int32_t *s_out,
+                    double *phi_out, double *gap_out) {
+  return oracle_search2d_n(h, L, q, 1, t_out, s_out, phi_out, gap_out);
 }

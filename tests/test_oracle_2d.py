@@ -122,3 +122,74 @@ def test_2d_transpose_symmetry():
             a = oracle.phi2d_at(h, q, t, s)
             b = oracle.phi2d_at(h.T.copy(), q, s, t)
             assert abs(a - b) <= 1e-13 * abs(a)
+
+
+def _partition(h, t, s):
+    """The classes of (t,s) as sets of non-empty cells (independent of the oracle)."""
+    nz = {(int(i), int(j)) for i, j in zip(*np.nonzero(h))}
+    return (frozenset(c for c in nz if c[0] <= t and c[1] <= s),
+            frozenset(c for c in nz if c[0] > t and c[1] > s))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_2d_gap_over_distinct_partitions(seed):
+    """Runner-up = best value over candidates whose cell partition differs from
+    t*'s (50-digit values, partitions as explicit cell sets)."""
+    rng = np.random.default_rng(300 + seed)
+    L = int(rng.integers(5, 9))
+    q = [0.6, 1.0, 1.4][seed % 3]
+    h = rng.integers(0, 15, size=(L, L)).astype(np.uint32)
+    h[rng.integers(0, L, 2), :] = 0  # empty rows and columns make equivalent candidates
+    h[:, rng.integers(0, L, 2)] = 0
+    r = oracle.search2d(h, q)
+    if r["status"] != oracle.OK:
+        return
+    best_part = _partition(h, r["t"], r["s"])
+    others = [mp_phi2d(h, t, s, q) for t, s in itertools.product(range(L - 1), range(L - 1))
+              if _partition(h, t, s) != best_part]
+    others = [v for v in others if v is not None]
+    if not others:
+        assert r["gap"] == float("inf")
+        return
+    phi2 = max(others)
+    gap = (mpmath.mpf(r["phi"]) - phi2) / abs(mpmath.mpf(r["phi"]))
+    assert abs(r["gap"] - float(gap)) <= 1e-12 * max(1.0, abs(float(gap))) + 1e-13
+
+
+def test_2d_equivalent_candidates_tie_exactly_and_lowest_wins():
+    """Empty rows/columns between candidates leave the partition unchanged, so
+    their values tie bit for bit and the lowest candidate (non-empty row and
+    column) is returned -- the reading the canonical GPU search relies on."""
+    rng = np.random.default_rng(77)
+    L = 10
+    h = rng.integers(1, 9, size=(L, L)).astype(np.uint32)
+    h[4:7, :] = 0
+    h[:, 2:5] = 0
+    for t in range(L - 1):
+        for s in range(L - 1):
+            a = oracle.phi2d_at(h, 0.7, t, s)
+            tt = t if not 4 <= t <= 6 else 3
+            ss = s if not 2 <= s <= 4 else 1
+            assert (a is None) == (oracle.phi2d_at(h, 0.7, tt, ss) is None)
+            if a is not None:
+                assert a == oracle.phi2d_at(h, 0.7, tt, ss)
+    for q in (0.5, 1.0, 1.5):
+        r = oracle.search2d(h, q)
+        assert r["t"] not in (4, 5, 6) and r["s"] not in (2, 3, 4)
+
+
+def test_2d_point_masses_gap():
+    h = np.zeros((16, 16), np.uint32)
+    h[3, 3] = 40
+    h[12, 12] = 40
+    r = oracle.search2d(h, 0.8)
+    assert r["gap"] == float("inf")  # a single distinct valid partition
+
+
+def test_2d_thread_count_invariant():
+    f = phantom.make_volume(phantom.CONFIGS["c2"], nz=1, z_first=60)[0][::4, ::4].copy()
+    h, _ = oracle.hist2d(f, 256)
+    hs = h[::4, ::4].copy()  # 64 levels keeps the O(L^4) search quick
+    a = oracle.search2d(hs, 0.8, threads=1)
+    b = oracle.search2d(hs, 0.8, threads=4)
+    assert a == b

@@ -192,6 +192,57 @@ tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slice
                             int32_t *status_host, uint8_t *labels_host, void *dev_buf,
                             size_t dev_bytes, void *stream0, void *stream1);
 
+/* ---- 2-D Tsallis thresholding: the paper's own formulation -------------
+ * (readings DESIGN.md R18-R22)
+ *   g(x,y)   = floor( sum_{3x3} f / 9 ), replicate border
+ *   h[i][j]  = #{(x,y) : f = i, g = j}
+ *   class 1  = {i <= t, j <= s}, class 2 = {i > t, j > s}
+ *   H_c      = (1 - sum_{class c} (p_ij / P_c)^q) / (q - 1)      (q == 1: Shannon)
+ *   phi(t,s) = H_1 + H_2 + (1 - q) H_1 H_2
+ *   (t*,s*)  = argmax over 0 <= t, s <= bins-2 with both classes non-empty,
+ *              lowest (t,s) in row-major order on exact ties        (R21)
+ *   label    = [f > t*]  ("only t is used as the threshold value")
+ * Conventions as above (device pointers, caller-owned buffers and workspace,
+ * asynchronous on `stream`, argument errors before any launch, per-slice
+ * data errors: TSA_ERR_LEVEL_OVERFLOW if any f >= bins or g >= bins,
+ * TSA_ERR_NO_VALID_SPLIT if no (t,s) has two non-empty classes). */
+typedef struct {
+  const void *volume;   /* [nz][ny][nx] u8, device */
+  int64_t nx, ny, nz;   /* > 0; nx <= 65535; nx*ny < 2^31 */
+  int32_t bins;         /* L: 2..256 */
+  double q;             /* > 0 and finite; q == 1 is Shannon */
+  int32_t cluster;      /* CTAs per slice (one thread-block cluster each): 0 = library
+                           default, else 4..8 (the L x L histogram is split by f-rows
+                           over the cluster's shared memory) */
+} tsa2d_problem;
+
+/* TSA_OK or TSA_ERR_INVALID_ARG (host only). */
+tsa_status tsa2d_validate(const tsa2d_problem *p);
+
+/* Bytes of workspace tsa2d_segment / tsa2d_histogram need (0 if invalid). */
+size_t tsa2d_workspace_size(const tsa2d_problem *p);
+
+/* CTAs per cluster the library uses for this problem (0 if invalid). */
+int32_t tsa2d_cluster_size(const tsa2d_problem *p);
+
+/* The whole 2-D path: mean image, 2-D histogram, exhaustive (t,s) search,
+ * argmax, phi(t*,s*) recomputed from the definition, labels.
+ *   out->thresholds   [nz][2] (t*, s*), required; -1 on slice error
+ *   out->labels       [nz][ny][nx] u8 or NULL: [f > t*], 0 on slice error
+ *   out->objective    [nz] f64 or NULL: phi(t*,s*); NaN on slice error
+ *   out->histogram    [nz][bins][bins] u32 or NULL: h
+ *   out->slice_status [nz] or NULL */
+tsa_status tsa2d_segment(const tsa2d_problem *p, const tsa_outputs *out, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
+/* The 2-D histogram alone: hist [nz][bins][bins] u32 (required), slice_status
+ * [nz] (required): TSA_OK or TSA_ERR_LEVEL_OVERFLOW. */
+tsa_status tsa2d_histogram(const tsa2d_problem *p, uint32_t *hist, int32_t *slice_status,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
+/* The mean image alone: g [nz][ny][nx] u8. */
+tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream);
+
 const char *tsa_status_string(tsa_status s);
 const char *tsa_last_error(void);
 int32_t tsa_version(void);

@@ -35,6 +35,8 @@ EXPORTS = (
     "tsa_search_workspace_size", "tsa_default_units", "tsa_search", "tsa_merge",
     "tsa_finalize", "tsa_label", "tsa_segment_host_scratch_size", "tsa_segment_host",
     "tsa_status_string", "tsa_last_error", "tsa_version", "tsa_pipeline_kind",
+    "tsa2d_validate", "tsa2d_workspace_size", "tsa2d_cluster_size", "tsa2d_segment",
+    "tsa2d_histogram", "tsa2d_mean3x3",
 )
 
 
@@ -78,6 +80,16 @@ class tsa_outputs(ctypes.Structure):
     ]
 
 
+class tsa2d_problem(ctypes.Structure):
+    _fields_ = [
+        ("volume", ctypes.c_void_p),
+        ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+        ("bins", ctypes.c_int32),
+        ("q", ctypes.c_double),
+        ("cluster", ctypes.c_int32),
+    ]
+
+
 _lib = None
 
 
@@ -96,6 +108,7 @@ def load() -> ctypes.CDLL:
     P, I32, I64, D, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
     PP = ctypes.POINTER(tsa_problem)
     PO = ctypes.POINTER(tsa_outputs)
+    P2 = ctypes.POINTER(tsa2d_problem)
     sig = {
         "tsa_validate": (I32, [PP]),
         "tsa_workspace_size": (SZ, [PP]),
@@ -113,6 +126,12 @@ def load() -> ctypes.CDLL:
         "tsa_last_error": (ctypes.c_char_p, []),
         "tsa_version": (I32, []),
         "tsa_pipeline_kind": (I32, [PP]),
+        "tsa2d_validate": (I32, [P2]),
+        "tsa2d_workspace_size": (SZ, [P2]),
+        "tsa2d_cluster_size": (I32, [P2]),
+        "tsa2d_segment": (I32, [P2, PO, P, SZ, P]),
+        "tsa2d_histogram": (I32, [P2, P, P, P, SZ, P]),
+        "tsa2d_mean3x3": (I32, [P2, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -336,6 +355,76 @@ def tsa_segment_host(vol_host, bins, k, q, objective="pseudo_additive", enumerat
                                 ctypes.c_void_p(streams[0].cuda_stream),
                                 ctypes.c_void_p(streams[1].cuda_stream)), "tsa_segment_host")
     return out
+
+
+# ------------------------------------------------------------------ 2-D
+def make_problem2d(vol, bins, q, cluster=0):
+    if vol.dim() != 3 or not vol.is_contiguous() or vol.dtype != torch.uint8:
+        raise ValueError("2-D path: volume must be a contiguous uint8 [nz][ny][nx] tensor")
+    nz, ny, nx = vol.shape
+    return tsa2d_problem(vol.data_ptr(), nx, ny, nz, bins, float(q), cluster)
+
+
+def tsa2d_cluster_size(vol, bins, q=0.8, cluster=0):
+    return int(load().tsa2d_cluster_size(ctypes.byref(make_problem2d(vol, bins, q, cluster))))
+
+
+def tsa2d_workspace(problem, device):
+    n = int(load().tsa2d_workspace_size(ctypes.byref(problem)))
+    if n == 0:
+        _check(load().tsa2d_validate(ctypes.byref(problem)), "tsa2d_workspace_size")
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def tsa2d_segment(vol, bins, q, labels=True, histogram=False, cluster=0, out=None, workspace=None,
+                  stream=None):
+    """2-D Tsallis path on the current stream.  Returns dict of
+    device tensors: thresholds [nz,2] i32 (t, s), objective [nz] f64, status [nz]
+    i32, labels [nz,ny,nx] u8 ([f > t]) or None, histogram [nz,bins,bins] or None."""
+    _need_cuda(vol)
+    p = make_problem2d(vol, bins, q, cluster)
+    nz = vol.shape[0]
+    dev = vol.device
+    if out is None:
+        out = {
+            "thresholds": torch.empty((nz, 2), dtype=torch.int32, device=dev),
+            "objective": torch.empty(nz, dtype=torch.float64, device=dev),
+            "status": torch.empty(nz, dtype=torch.int32, device=dev),
+            "labels": torch.empty(vol.shape, dtype=torch.uint8, device=dev) if labels else None,
+            "histogram": (torch.empty((nz, bins, bins), dtype=torch.int32, device=dev)
+                          if histogram else None),
+        }
+    o = tsa_outputs(out["thresholds"].data_ptr(),
+                    out["labels"].data_ptr() if out.get("labels") is not None else None,
+                    out["objective"].data_ptr() if out.get("objective") is not None else None,
+                    out["histogram"].data_ptr() if out.get("histogram") is not None else None,
+                    out["status"].data_ptr() if out.get("status") is not None else None)
+    if workspace is None:
+        workspace = tsa2d_workspace(p, dev)
+    _check(load().tsa2d_segment(ctypes.byref(p), ctypes.byref(o), _ptr(workspace),
+                                workspace.numel(), _stream(stream)), "tsa2d_segment")
+    return out
+
+
+def tsa2d_histogram(vol, bins, cluster=0, workspace=None, stream=None):
+    _need_cuda(vol)
+    p = make_problem2d(vol, bins, 1.0, cluster)
+    nz = vol.shape[0]
+    hist = torch.empty((nz, bins, bins), dtype=torch.int32, device=vol.device)
+    status = torch.empty(nz, dtype=torch.int32, device=vol.device)
+    if workspace is None:
+        workspace = tsa2d_workspace(p, vol.device)
+    _check(load().tsa2d_histogram(ctypes.byref(p), _ptr(hist), _ptr(status), _ptr(workspace),
+                                  workspace.numel(), _stream(stream)), "tsa2d_histogram")
+    return hist, status
+
+
+def tsa2d_mean3x3(vol, stream=None):
+    _need_cuda(vol)
+    p = make_problem2d(vol, 256, 1.0)
+    g = torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
+    _check(load().tsa2d_mean3x3(ctypes.byref(p), _ptr(g), _stream(stream)), "tsa2d_mean3x3")
+    return g
 
 
 def unpack_key(key, k):

@@ -1,0 +1,916 @@
+// k_tsallis2d.cuh -- SURVEY.md §8(f) NEXT row 1: the paper's own 2-D Tsallis
+// thresholding, one thread-block cluster per slice.
+//
+//   g(x,y)  = floor(sum_{3x3} f / 9), replicate border            PAPER.md:566-570 (R18, R19)
+//   h(i,j)  = #{f = i, g = j}
+//   class 1 = {i <= t, j <= s}, class 2 = {i > t, j > s}           PAPER.md:578-591 (R20)
+//   A_c     = sum_{class c} (h / n_c)^q,  phi = (A_1 A_2 - 1)/(1 - q)  (q == 1: S_1 + S_2)
+//   (t*,s*) = argmax phi over [0, L-2]^2, lowest (t,s) on exact ties  PAPER.md:593-597 (R21)
+//   label   = [f > t*]  ("only t is used")                          PAPER.md:597 (R22)
+//
+// B200 design.  The 2-D histogram of an 8-bit slice is 256 x 256 u32 = 256 KB,
+// more than one SM's shared memory, so a slice is owned by a cluster of CL
+// CTAs (one per SM, ~210 KB of shared memory each) and never leaves the chip:
+//   1. histogram: CTA c reads image rows [c ny/CL, (c+1) ny/CL) (16-pixel
+//      items, 16-bit-lane SWAR 3x3 box sums, exact floor(v/9) = (7282 v) >> 16,
+//      a register ring keeping 4 rows of loads in flight) and counts (f,g)
+//      codes into a PRIVATE full L x L histogram of 16-bit counters packed two
+//      per word (a CTA counts <= 65535 pixels per round, so no counter can
+//      wrap); uniform items add 16, warp-uniform ones 16 x lanes at once.
+//   2. merge over DSMEM: CTA r owns the f-rows [r R, (r+1) R) (R = ceil(L/CL))
+//      and sums that band of all CL private histograms into a u32 band.
+//   3. band column sums are exchanged over DSMEM: every CTA gets the
+//      column totals of the bands below / above it (the SAT boundary values).
+//   4. prefix walk: 8 rows at a time, one warp per row scans the row (lane =
+//      8 contiguous columns, warp scan of lane totals), then thread s walks the
+//      rows adding the row prefix to its running (n_1, W_1) = summed-area table
+//      value at (t, s) and stores A_1(t,s) = W_1 / n_1^q in shared memory.
+//   5. suffix walk: the same from the top row down with row suffixes, giving
+//      (n_2, W_2) of class 2 directly (sums of non-negative terms, no prefix
+//      differences, no cancellation), the score A_1 A_2 (+-, or S_1 + S_2 at
+//      q = 1) and a running (score, key = t L + s) best.
+//   6. argmax: warp shuffles, block, then over the cluster via DSMEM.
+//   7. phi(t*,s*) recomputed in p-space from the definition (p = h/N, P_c as a
+//      sum of p, (p/P_c)^q per non-empty cell; fixed-order reductions).
+// Only canonical candidates -- row t and column s non-empty -- are scored:
+// every other candidate describes the same partition as a canonical one and
+// the lowest member of each class is canonical (R21), so the result
+// equals the exhaustive argmax and the summation order of the tables need not
+// make equivalent candidates tie bit for bit.  w(c) = c^q (c ln c at q = 1)
+// and 1/n^q (ln n, 1/n) come from n-indexed tables (k2d_luts).
+#pragma once
+#include <cooperative_groups.h>
+
+#include <cstdint>
+
+#include "tsa_device.cuh"
+
+namespace tsa {
+
+namespace cg = cooperative_groups;
+
+constexpr int k2dThreads = 256;  // CTA size of the cluster kernel
+constexpr int k2dGroup = k2dThreads / 32;  // rows per walk group (one warp per row)
+constexpr int k2dMaxCL = 8;
+
+struct Tsa2dArgs {
+  const uint8_t *vol;     // [nz][ny][nx]
+  int64_t nx, ny, nz;
+  int L, LP;              // bins, even row pitch of the 2-D tables
+  int CL, R;              // CTAs per cluster, f-rows per band (R = ceil(L / CL))
+  int rr;                 // image rows per counting round (rr * nx <= 65535)
+  int rounds;             // counting rounds (same for every CTA of a cluster)
+  int vec;                // 16-pixel SWAR path (nx % 16 == 0, 16-byte aligned slices)
+  double q;
+  int mode;               // PROD_MAX / PROD_MIN / SUM (q == 1)
+  const double *wlut;     // [N+1] w(c): c^q, or c ln c at q == 1; w(0) = 0
+  const double *ipow;     // [N+1] 1/n^q (NaN at 0)          (q != 1)
+  const double *lnn;      // [N+1] ln n (NaN at 0)            (q == 1)
+  const double *rcp;      // [N+1] 1/n                        (q == 1)
+  int32_t *thresholds;    // [nz][2] (t, s), -1 on error
+  int32_t *tlab;          // [nz] t for the label kernel (-1 on error)
+  double *objective;      // [nz] or null
+  uint32_t *hist;         // [nz][L][L] or null
+  int32_t *status;        // [nz] (workspace, read by the label kernel)
+  int32_t *status2;       // [nz] or null (caller's copy)
+  int hist_only;          // stop after the histogram (tsa2d_histogram)
+};
+
+// ------------------------------------------------------------------ luts
+__global__ void k2d_luts(double *wlut, double *ipow, double *lnn, double *rcp, int64_t N, double q,
+                         int shannon) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n <= N;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const double x = (double)n;
+    if (shannon) {
+      wlut[n] = n == 0 ? 0.0 : __dmul_rn(x, log(x));
+      lnn[n] = n == 0 ? CUDART_NAN : log(x);
+      rcp[n] = n == 0 ? CUDART_NAN : __drcp_rn(x);
+    } else {
+      const double pw = pow(x, q);
+      wlut[n] = n == 0 ? 0.0 : pw;
+      ipow[n] = n == 0 ? CUDART_NAN : __drcp_rn(pw);
+    }
+  }
+}
+
+// ------------------------------------------------------- 3x3 mean helpers
+// 16-bit-lane horizontal 3-sums of the 4 pixels of word w (bytes b0..b3 =
+// pixels x..x+3), lb = pixel x-1, rb = pixel x+4 (already border-replicated):
+//   lo = (lb+b0+b1, b0+b1+b2), hi = (b1+b2+b3, b2+b3+rb)   (each <= 765)
+__device__ __forceinline__ void hsum4(uint32_t w, uint32_t lb, uint32_t rb, uint32_t &lo,
+                                      uint32_t &hi) {
+  const uint32_t pL0 = __byte_perm(w, lb, 0x5054);  // (lb, b0)
+  const uint32_t p01 = __byte_perm(w, 0u, 0x4140);  // (b0, b1)
+  const uint32_t p12 = __byte_perm(w, 0u, 0x4241);  // (b1, b2)
+  const uint32_t p23 = __byte_perm(w, 0u, 0x4342);  // (b2, b3)
+  const uint32_t p3R = __byte_perm(w, rb, 0x5453);  // (b3, rb)
+  lo = pL0 + p01 + p12;
+  hi = p12 + p23 + p3R;
+}
+
+// floor(v / 9) for 0 <= v <= 2295 (= 9 * 255): (7282 v) >> 16 is exact on that range
+__device__ __forceinline__ uint32_t div9(uint32_t v) { return (v * 7282u) >> 16; }
+
+__device__ __forceinline__ uint32_t ldg_u8(const uint8_t *p) { return (uint32_t)__ldg(p); }
+
+// image row y's word gx plus its border-replicated neighbour pixels
+__device__ __forceinline__ void load_row4(const uint8_t *row, int64_t gx, int64_t G4, uint32_t &w,
+                                          uint32_t &lb, uint32_t &rb) {
+  w = __ldg(reinterpret_cast<const uint32_t *>(row) + gx);
+  lb = gx > 0 ? ldg_u8(row + 4 * gx - 1) : (w & 0xffu);
+  rb = gx < G4 - 1 ? ldg_u8(row + 4 * gx + 4) : (w >> 24);
+}
+
+// --------------------------------------------------------- stage: g image
+// tsa2d_mean3x3: g for every pixel (the same SWAR arithmetic as the cluster
+// kernel when vec, else scalar).  grid (x-chunks, nz), 256 threads.
+__global__ void __launch_bounds__(256) k2d_mean(const uint8_t *vol, uint8_t *g, int64_t nx,
+                                                int64_t ny, int vec) {
+  const int64_t z = blockIdx.y;
+  const uint8_t *f = vol + z * nx * ny;
+  uint8_t *gz = g + z * nx * ny;
+  if (vec) {
+    const int64_t G4 = nx / 4;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < G4 * ny;
+         it += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t y = it / G4, gx = it % G4;
+      uint32_t lo = 0, hi = 0;
+      for (int dy = -1; dy <= 1; dy++) {
+        const int64_t yy = min(max(y + dy, (int64_t)0), ny - 1);
+        uint32_t w, lb, rb, l, h;
+        load_row4(f + yy * nx, gx, G4, w, lb, rb);
+        hsum4(w, lb, rb, l, h);
+        lo += l;
+        hi += h;
+      }
+      const uint32_t out = div9(lo & 0xffffu) | div9(lo >> 16) << 8 | div9(hi & 0xffffu) << 16 |
+                           div9(hi >> 16) << 24;
+      *reinterpret_cast<uint32_t *>(gz + y * nx + 4 * gx) = out;
+    }
+  } else {
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < nx * ny;
+         it += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t y = it / nx, x = it % nx;
+      uint32_t v = 0;
+      for (int dy = -1; dy <= 1; dy++)
+        for (int dx = -1; dx <= 1; dx++) {
+          const int64_t yy = min(max(y + dy, (int64_t)0), ny - 1);
+          const int64_t xx = min(max(x + dx, (int64_t)0), nx - 1);
+          v += f[yy * nx + xx];
+        }
+      gz[it] = (uint8_t)div9(v);
+    }
+  }
+}
+
+// ------------------------------------------------------------ block scans
+// inclusive scan over the CTA (one element per thread, thread order) of an
+// exact count and a double; scratch >= 32 * 16 bytes.  Fixed tree: results
+// are a pure function of the inputs.
+__device__ __forceinline__ void block_incl_scan(uint32_t &n, double &w, char *scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t on = __shfl_up_sync(0xffffffffu, n, off);
+    const double ow = __shfl_up_sync(0xffffffffu, w, off);
+    if (lane >= off) {
+      n += on;
+      w = __dadd_rn(ow, w);
+    }
+  }
+  uint32_t *sn = reinterpret_cast<uint32_t *>(scratch);
+  double *sw = reinterpret_cast<double *>(scratch + 256);
+  if (lane == 31) {
+    sn[warp] = n;
+    sw[warp] = w;
+  }
+  __syncthreads();
+  uint32_t bn = 0;
+  double bw = 0.0;
+  for (int i = 0; i < warp && i < nw; i++) {
+    bn += sn[i];
+    bw = __dadd_rn(bw, sw[i]);
+  }
+  n += bn;
+  w = __dadd_rn(bw, w);
+  __syncthreads();
+}
+
+// exclusive SUFFIX scan (sum over threads > this one)
+__device__ __forceinline__ void block_excl_suffix_scan(uint32_t &n, double &w, char *scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t in = n;
+  double iw = w;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t on = __shfl_down_sync(0xffffffffu, in, off);
+    const double ow = __shfl_down_sync(0xffffffffu, iw, off);
+    if (lane + off < 32) {
+      in += on;
+      iw = __dadd_rn(iw, ow);
+    }
+  }
+  uint32_t *sn = reinterpret_cast<uint32_t *>(scratch);
+  double *sw = reinterpret_cast<double *>(scratch + 256);
+  if (lane == 0) {
+    sn[warp] = in;
+    sw[warp] = iw;
+  }
+  __syncthreads();
+  uint32_t bn = 0;
+  double bw = 0.0;
+  for (int i = nw - 1; i > warp; i--) {
+    bn += sn[i];
+    bw = __dadd_rn(bw, sw[i]);
+  }
+  // exclusive within the warp: inclusive of the next lane
+  uint32_t xn = __shfl_down_sync(0xffffffffu, in, 1);
+  double xw = __shfl_down_sync(0xffffffffu, iw, 1);
+  if (lane == 31) {
+    xn = 0;
+    xw = 0.0;
+  }
+  n = xn + bn;
+  w = __dadd_rn(xw, bw);
+  __syncthreads();
+}
+
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; i++) t = __dadd_rn(t, scratch[i]);
+  __syncthreads();
+  return t;
+}
+
+// class term of a (count, W) rectangle: A = W / n^q (or S = ln n - W/n); NaN if n == 0
+template <int MODE>
+__device__ __forceinline__ double term2d(uint32_t n, double W, const Tsa2dArgs &a) {
+  if (MODE == SUM) return __dsub_rn(__ldg(a.lnn + n), __dmul_rn(W, __ldg(a.rcp + n)));
+  return __dmul_rn(W, __ldg(a.ipow + n));
+}
+
+template <int MODE>
+__device__ __forceinline__ double score2d(double t1, double t2) {
+  if (MODE == SUM) return __dadd_rn(t1, t2);
+  const double p = __dmul_rn(t1, t2);
+  return MODE == PROD_MAX ? p : -p;
+}
+
+// -------------------------------------------------------------- the kernel
+// Shared-memory layout (bytes, every offset 16-aligned).  Band-row tables use
+// the padded pitch PP = LP + LP/8 with column j at j + j/8, so a lane reading
+// 8 contiguous columns and a thread reading column s are both (nearly)
+// bank-conflict free.
+//   A      max(L*LP*2, R*LP*8): private u16 histogram, later A_1 / S_1 [R][LP] f64
+//   Hb     R*PP*4              merged u32 band
+//   gN     G*PP*4, gW G*PP*8   walk group buffers (row prefix / suffix)
+//   colN   LP*4, colW LP*8     band column sums (read by the other CTAs)
+//   rl     R*4                 band rows that are non-empty (compacted list)
+//   xch    256                 exchange slots (flags, argmax, phi partials)
+//   scr    1024                scan scratch
+struct Smem2d {
+  size_t A, Hb, gN, gW, colN, colW, rl, xch, scr, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline int pitch2d(int LP) { return LP + (LP + 7) / 8; }
+
+__host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
+  Smem2d s;
+  const int PP = pitch2d(LP);
+  size_t o = 0;
+  s.A = o;
+  const size_t a1 = (size_t)L * LP * 2, a2 = (size_t)R * LP * 8;
+  o += al16(a1 > a2 ? a1 : a2);
+  s.Hb = o;
+  o += al16((size_t)R * PP * 4);
+  s.gN = o;
+  o += al16((size_t)k2dGroup * PP * 4);
+  s.gW = o;
+  o += al16((size_t)k2dGroup * PP * 8);
+  s.colN = o;
+  o += al16((size_t)LP * 4);
+  s.colW = o;
+  o += al16((size_t)LP * 8);
+  s.rl = o;
+  o += al16((size_t)R * 4 + 16);
+  s.xch = o;
+  o += 256;
+  s.scr = o;
+  o += 1024;
+  s.total = o;
+  return s;
+}
+
+__device__ __forceinline__ int pj(int j) { return j + (j >> 3); }
+
+// exchange slot offsets (doubles / u64 / ints inside xch)
+struct Xch {
+  int flags;        // overflow flag (int)
+  double score;     // CTA best
+  uint64_t key;
+  double P1, P2;    // phi partials, round a
+  double A1, A2;    // round b
+};
+
+// one image row's 16-pixel item: pixels x0..x0+15 (uint4) and the
+// border-replicated neighbours x0-1, x0+16
+struct Raw16 {
+  uint4 w;
+  uint32_t lb, rb;
+};
+
+__device__ __forceinline__ Raw16 load16(const uint8_t *row, int64_t gx, int64_t G16) {
+  Raw16 r;
+  r.w = __ldg(reinterpret_cast<const uint4 *>(row) + gx);
+  r.lb = gx > 0 ? ldg_u8(row + 16 * gx - 1) : (r.w.x & 0xffu);
+  r.rb = gx < G16 - 1 ? ldg_u8(row + 16 * gx + 16) : (r.w.w >> 24);
+  return r;
+}
+
+// horizontal 3-sums of the 16 pixels: 8 words of two 16-bit lanes
+__device__ __forceinline__ void hsum16(const Raw16 &r, uint32_t *hs) {
+  hsum4(r.w.x, r.lb, r.w.y & 0xffu, hs[0], hs[1]);
+  hsum4(r.w.y, r.w.x >> 24, r.w.z & 0xffu, hs[2], hs[3]);
+  hsum4(r.w.z, r.w.y >> 24, r.w.w & 0xffu, hs[4], hs[5]);
+  hsum4(r.w.w, r.w.z >> 24, r.rb, hs[6], hs[7]);
+}
+
+__device__ __forceinline__ void add_code(uint32_t *hp, uint32_t c, uint32_t n) {
+  atomicAdd(hp + (c >> 1), n << ((c & 1u) << 4));
+}
+
+// Count the (f, g) codes of image rows [ya, yb) into the packed u16 histogram.
+// VEC: items of 16 pixels (nx % 16 == 0, 16-byte aligned slices); each item
+// walks a stripe of rows with a register ring prefetching kPF rows ahead, so
+// a warp keeps kPF row loads in flight instead of one.
+constexpr int kPF = 4;
+
+template <bool VEC, bool CHECK>
+__device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f, int64_t ya,
+                                            int64_t yb, uint32_t *hp, int &ovf) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t nx = a.nx, ny = a.ny;
+  const int LP = a.LP, L = a.L;
+  if (yb <= ya) return;
+  if (VEC) {
+    const int64_t G16 = nx / 16;
+    const int64_t S = G16 >= k2dThreads ? 1 : k2dThreads / G16;  // row stripes
+    const int64_t rows = yb - ya, per = (rows + S - 1) / S;
+    for (int64_t item = tid; item < G16 * S; item += k2dThreads) {
+      const int64_t gx = item % G16, st = item / G16;
+      const int64_t ys = ya + st * per, ye = min(yb, ys + per);
+      if (ys >= ye) continue;
+      uint32_t hp_[8], hc[8], hn[8];
+      {
+        const Raw16 r0 = load16(f + max(ys - 1, (int64_t)0) * nx, gx, G16);
+        hsum16(r0, hp_);
+      }
+      Raw16 cur = load16(f + ys * nx, gx, G16);
+      hsum16(cur, hc);
+      Raw16 ring[kPF];
+#pragma unroll
+      for (int d = 0; d < kPF; d++)
+        if (ys + 1 + d <= ye) ring[d] = load16(f + min(ys + 1 + d, ny - 1) * nx, gx, G16);
+      for (int64_t y = ys; y < ye; y += kPF) {
+#pragma unroll
+        for (int d = 0; d < kPF; d++) {
+          if (y + d < ye) {
+            const Raw16 nxt = ring[d];
+            const int64_t yl = y + d + 1 + kPF;  // row kept in this slot next
+            if (yl <= ye) ring[d] = load16(f + min(yl, ny - 1) * nx, gx, G16);
+            hsum16(nxt, hn);
+            uint32_t box[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) box[e] = hp_[e] + hc[e] + hn[e];
+            const uint32_t fw[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
+            if (!CHECK) {
+              const uint32_t f0 = fw[0] & 0xffu;
+              bool uni = fw[0] == f0 * 0x01010101u && fw[1] == fw[0] && fw[2] == fw[0] &&
+                         fw[3] == fw[0];
+              const uint32_t b0 = box[0] & 0xffffu;
+#pragma unroll
+              for (int e = 0; e < 8; e++) uni = uni && box[e] == (b0 | (b0 << 16));
+              const uint32_t c0 = f0 * LP + div9(b0);
+              const unsigned m = __activemask();
+              const int leader = __ffs(m) - 1;
+              const uint32_t cl = __shfl_sync(m, c0, leader);
+              if (__all_sync(m, uni && c0 == cl)) {
+                if (lane == leader) add_code(hp, c0, 16u * __popc(m));
+              } else if (uni) {
+                add_code(hp, c0, 16u);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; e++) {
+                  const uint32_t fv = (fw[e >> 2] >> (8 * (e & 3))) & 0xffu;
+                  const uint32_t bv = (box[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                  add_code(hp, fv * LP + div9(bv), 1u);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; e++) {
+                const uint32_t fv = (fw[e >> 2] >> (8 * (e & 3))) & 0xffu;
+                const uint32_t gv = div9((box[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+                if (fv >= (uint32_t)L || gv >= (uint32_t)L) {
+                  ovf = 1;
+                  continue;
+                }
+                add_code(hp, fv * LP + gv, 1u);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+              hp_[e] = hc[e];
+              hc[e] = hn[e];
+            }
+            cur = nxt;
+          }
+        }
+      }
+    }
+  } else {
+    const int64_t npx = (yb - ya) * nx;
+    for (int64_t it = tid; it < npx; it += k2dThreads) {
+      const int64_t y = ya + it / nx, x = it % nx;
+      uint32_t v = 0;
+      for (int dy = -1; dy <= 1; dy++)
+        for (int dx = -1; dx <= 1; dx++) {
+          const int64_t yy = min(max(y + dy, (int64_t)0), ny - 1);
+          const int64_t xx = min(max(x + dx, (int64_t)0), nx - 1);
+          v += ldg_u8(f + yy * nx + xx);
+        }
+      const uint32_t fv = ldg_u8(f + y * nx + x), gv = div9(v);
+      if (CHECK && (fv >= (uint32_t)L || gv >= (uint32_t)L)) {
+        ovf = 1;
+        continue;
+      }
+      add_code(hp, fv * LP + gv, 1u);
+    }
+    (void)lane;
+  }
+}
+
+template <int MODE, bool VEC, bool CHECK>
+__global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
+  extern __shared__ __align__(16) char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = a.CL, r = (int)cluster.block_rank();
+  const int64_t z = blockIdx.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int L = a.L, LP = a.LP, R = a.R, PP = pitch2d(LP);
+  const int row0 = r * R, nrows = max(0, min(L, row0 + R) - row0);  // band f-rows
+  const Smem2d lay = smem2d_layout(L, LP, R);
+  uint32_t *hp = reinterpret_cast<uint32_t *>(smem + lay.A);  // packed u16 private histogram
+  double *A1 = reinterpret_cast<double *>(smem + lay.A);
+  uint32_t *Hb = reinterpret_cast<uint32_t *>(smem + lay.Hb);
+  uint32_t *gN = reinterpret_cast<uint32_t *>(smem + lay.gN);
+  double *gW = reinterpret_cast<double *>(smem + lay.gW);
+  uint32_t *colN = reinterpret_cast<uint32_t *>(smem + lay.colN);
+  double *colW = reinterpret_cast<double *>(smem + lay.colW);
+  int *rl = reinterpret_cast<int *>(smem + lay.rl);
+  Xch *xch = reinterpret_cast<Xch *>(smem + lay.xch);
+  char *scr = smem + lay.scr;
+  const uint8_t *f = a.vol + z * a.nx * a.ny;
+
+  // ---- 1 + 2: counting rounds and DSMEM merge into the u32 band
+  for (int i = tid; i < nrows * PP; i += k2dThreads) Hb[i] = 0u;
+  if (tid == 0) xch->flags = 0;
+  int ovf = 0;
+  const int64_t ya0 = (int64_t)r * a.ny / CL, yb0 = (int64_t)(r + 1) * a.ny / CL;
+  const int hw = L * LP / 2;  // words of the private histogram
+  for (int rd = 0; rd < a.rounds; rd++) {
+    uint4 *hp4 = reinterpret_cast<uint4 *>(hp);
+    for (int i = tid; i < (hw + 3) / 4; i += k2dThreads) hp4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    const int64_t ya = min(yb0, ya0 + (int64_t)rd * a.rr), yb = min(yb0, ya + a.rr);
+    count_round<VEC, CHECK>(a, f, ya, yb, hp, ovf);
+    cluster.sync();  // every private histogram of this round complete
+    // band words: rows [row0, row0+nrows) of every CTA's private histogram
+    const int bw0 = row0 * LP / 2, bwn = nrows * LP / 2;
+    if ((LP & 7) == 0) {
+      for (int i = tid; i < bwn / 4; i += k2dThreads) {  // 8 cells of one row
+        uint4 v[k2dMaxCL];
+#pragma unroll
+        for (int c = 0; c < k2dMaxCL; c++)
+          if (c < CL) v[c] = reinterpret_cast<const uint4 *>(cluster.map_shared_rank(hp, c) + bw0)[i];
+        const int cell = 8 * i, ri = cell / LP, j = cell - ri * LP;
+        uint32_t *dst = Hb + ri * PP + pj(j);
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) o[e] = dst[e];
+#pragma unroll
+        for (int c = 0; c < k2dMaxCL; c++)
+          if (c < CL) {
+            o[0] += v[c].x & 0xffffu;
+            o[1] += v[c].x >> 16;
+            o[2] += v[c].y & 0xffffu;
+            o[3] += v[c].y >> 16;
+            o[4] += v[c].z & 0xffffu;
+            o[5] += v[c].z >> 16;
+            o[6] += v[c].w & 0xffffu;
+            o[7] += v[c].w >> 16;
+          }
+#pragma unroll
+        for (int e = 0; e < 8; e++) dst[e] = o[e];
+      }
+    } else {
+      for (int c = 0; c < CL; c++) {
+        const uint32_t *src = cluster.map_shared_rank(hp, c) + bw0;
+        for (int i = tid; i < bwn; i += k2dThreads) {
+          const uint32_t v = src[i];
+          if (v) {
+            const int ri = (2 * i) / LP, j = 2 * i - ri * LP;
+            Hb[ri * PP + pj(j)] += v & 0xffffu;
+            Hb[ri * PP + pj(j + 1)] += v >> 16;
+          }
+        }
+      }
+    }
+    cluster.sync();  // all reads of the private histograms done before reuse
+  }
+  if (CHECK && ovf) atomicOr(&xch->flags, 1);
+  // optional histogram output (the band's rows)
+  if (a.hist) {
+    uint32_t *ho = a.hist + ((size_t)z * L + row0) * L;
+    for (int i = warp; i < nrows; i += k2dThreads / 32)
+      for (int j = lane; j < L; j += 32) ho[(size_t)i * L + j] = Hb[i * PP + pj(j)];
+  }
+
+  // ---- 3: non-empty band rows, band column sums and the exchange
+  const int s = tid;  // column owned in the walks (L <= 256 = k2dThreads)
+  {
+    // compacted list of the band's non-empty rows (one warp per row)
+    for (int i = warp; i < nrows; i += k2dThreads / 32) {
+      uint32_t any = 0;
+      for (int j = lane; j < L; j += 32) any |= Hb[i * PP + pj(j)];
+      any = __any_sync(0xffffffffu, any != 0);
+      if (lane == 0) rl[1 + i] = any ? 1 : 0;
+    }
+    uint32_t n = 0;
+    double W = 0.0;
+    if (s < L) {
+#pragma unroll 4
+      for (int i = 0; i < nrows; i++) {
+        const uint32_t h = Hb[i * PP + pj(s)];
+        n += h;
+        W = __dadd_rn(W, h ? __ldg(a.wlut + h) : 0.0);
+      }
+    }
+    if (s < LP) {
+      colN[s] = n;
+      colW[s] = W;
+    }
+    __syncthreads();
+    if (warp == 0) {  // compact the flags in place (rl[0] = count)
+      int cnt = 0;
+      for (int b = 0; b < nrows; b += 32) {
+        const int i = b + lane;
+        const bool fl = i < nrows && rl[1 + i];
+        const unsigned m = __ballot_sync(0xffffffffu, fl);
+        __syncwarp();
+        if (fl) rl[1 + cnt + __popc(m & ((1u << lane) - 1u))] = i;
+        cnt += __popc(m);
+        __syncwarp();
+      }
+      if (lane == 0) rl[0] = cnt;
+    }
+  }
+  __syncthreads();
+  cluster.sync();
+  const int nrl = rl[0];
+  const int *rows = rl + 1;
+  int any_ovf = 0;
+  uint32_t lowN = 0, upN = 0, allN = 0;
+  double lowW = 0.0, upW = 0.0;
+  {
+    uint32_t cn[k2dMaxCL];
+    double cw[k2dMaxCL];
+#pragma unroll
+    for (int c = 0; c < k2dMaxCL; c++) {
+      if (c < CL) {
+        cn[c] = s < L ? cluster.map_shared_rank(colN, c)[s] : 0u;
+        cw[c] = s < L ? cluster.map_shared_rank(colW, c)[s] : 0.0;
+        if (CHECK) any_ovf |= cluster.map_shared_rank(&xch->flags, c)[0];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < k2dMaxCL; c++) {
+      if (c < CL) {
+        allN += cn[c];
+        if (c < r) {
+          lowN += cn[c];
+          lowW = __dadd_rn(lowW, cw[c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = k2dMaxCL - 1; c >= 0; c--) {
+      if (c < CL && c > r) {
+        upN += cn[c];
+        upW = __dadd_rn(upW, cw[c]);
+      }
+    }
+  }
+  const bool colnz = s < L && allN > 0;
+  // prefix base B(s) = sum_{j <= s} low(j); suffix base B'(s) = sum_{j > s} up(j)
+  block_incl_scan(lowN, lowW, scr);
+  block_excl_suffix_scan(upN, upW, scr);
+  double best = -CUDART_INF;
+  uint64_t bkey = kKeyNone;
+  if (!a.hist_only && !any_ovf) {
+    const int CPL = (L + 31) / 32;
+    const int j0 = min(L, lane * CPL), jn = max(0, min(L, j0 + CPL) - j0);
+    // ---- 4: prefix walk over the non-empty rows: A_1 / S_1 of every canonical
+    // (t, s) into A1[k][s] (k = compacted row index).  Empty rows add nothing
+    // and are never canonical.
+    uint32_t accN = lowN;
+    double accW = lowW;
+    for (int g0 = 0; g0 < nrl; g0 += k2dGroup) {
+      const int kk = g0 + warp;
+      if (kk < nrl) {
+        const int i = rows[kk];
+        uint32_t hv[8];
+        double wv[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) hv[e] = e < jn ? Hb[i * PP + pj(j0 + e)] : 0u;
+#pragma unroll
+        for (int e = 0; e < 8; e++) wv[e] = hv[e] ? __ldg(a.wlut + hv[e]) : 0.0;
+        uint32_t ln = 0;
+        double lw = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          ln += hv[e];
+          lw = __dadd_rn(lw, wv[e]);
+        }
+        // exclusive warp scan of lane totals
+        uint32_t xn = ln;
+        double xw = lw;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t on = __shfl_up_sync(0xffffffffu, xn, off);
+          const double ow = __shfl_up_sync(0xffffffffu, xw, off);
+          if (lane >= off) {
+            xn += on;
+            xw = __dadd_rn(ow, xw);
+          }
+        }
+        xn -= ln;  // exclusive count (exact)
+        xw = __shfl_up_sync(0xffffffffu, xw, 1);
+        if (lane == 0) xw = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          xn += hv[e];
+          xw = __dadd_rn(xw, wv[e]);
+          if (e < jn) {
+            gN[warp * PP + pj(j0 + e)] = xn;
+            gW[warp * PP + pj(j0 + e)] = xw;
+          }
+        }
+      }
+      __syncthreads();
+      if (s < L) {
+        const int ge = min(k2dGroup, nrl - g0);
+        uint32_t nn[k2dGroup];
+        double wwv[k2dGroup];
+#pragma unroll
+        for (int w = 0; w < k2dGroup; w++) {
+          if (w < ge) {
+            accN += gN[w * PP + pj(s)];
+            accW = __dadd_rn(accW, gW[w * PP + pj(s)]);
+          }
+          nn[w] = accN;
+          wwv[w] = accW;
+        }
+        // only canonical candidates are ever scored: the LUT gathers of a group
+        // are independent and issued back to back
+#pragma unroll
+        for (int w = 0; w < k2dGroup; w++)
+          if (w < ge) A1[(g0 + w) * LP + s] = colnz ? term2d<MODE>(nn[w], wwv[w], a) : CUDART_NAN;
+      }
+      __syncthreads();
+    }
+    // ---- 5: suffix walk (top row down), scores and the running best
+    uint32_t sN = upN;
+    double sW = upW;
+    for (int g0 = nrl - 1; g0 >= 0; g0 -= k2dGroup) {
+      const int kk = g0 - warp;
+      if (kk >= 0) {
+        const int i = rows[kk];
+        uint32_t hv[8];
+        double wv[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) hv[e] = e < jn ? Hb[i * PP + pj(j0 + e)] : 0u;
+#pragma unroll
+        for (int e = 0; e < 8; e++) wv[e] = hv[e] ? __ldg(a.wlut + hv[e]) : 0.0;
+        uint32_t ln = 0;
+        double lw = 0.0;
+#pragma unroll
+        for (int e = 7; e >= 0; e--) {
+          ln += hv[e];
+          lw = __dadd_rn(lw, wv[e]);
+        }
+        // exclusive suffix over lanes > this one
+        uint32_t xn = ln;
+        double xw = lw;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t on = __shfl_down_sync(0xffffffffu, xn, off);
+          const double ow = __shfl_down_sync(0xffffffffu, xw, off);
+          if (lane + off < 32) {
+            xn += on;
+            xw = __dadd_rn(xw, ow);
+          }
+        }
+        uint32_t cn = __shfl_down_sync(0xffffffffu, xn, 1);
+        double cw = __shfl_down_sync(0xffffffffu, xw, 1);
+        if (lane == 31) {
+          cn = 0;
+          cw = 0.0;
+        }
+        // row suffix at column j = sum over columns > j
+#pragma unroll
+        for (int e = 7; e >= 0; e--) {
+          if (e < jn) {
+            gN[warp * PP + pj(j0 + e)] = cn;
+            gW[warp * PP + pj(j0 + e)] = cw;
+          }
+          cn += hv[e];
+          cw = __dadd_rn(cw, wv[e]);
+        }
+      }
+      __syncthreads();
+      if (s < L) {
+        const int ge = min(k2dGroup, g0 + 1);
+        uint32_t nn[k2dGroup];
+        double wwv[k2dGroup];
+#pragma unroll
+        for (int w = 0; w < k2dGroup; w++) {
+          // (sN, sW) before row rows[g0-w] is added = class 2 of (t, s): rows > t, columns > s
+          nn[w] = sN;
+          wwv[w] = sW;
+          if (w < ge) {
+            sN += gN[w * PP + pj(s)];
+            sW = __dadd_rn(sW, gW[w * PP + pj(s)]);
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < k2dGroup; w++) {
+          const int kk = g0 - w;
+          if (w < ge && colnz && s <= L - 2) {
+            const int t = row0 + rows[kk];
+            if (t <= L - 2) {
+              const double sc = score2d<MODE>(A1[kk * LP + s], term2d<MODE>(nn[w], wwv[w], a));
+              const uint64_t key = (uint64_t)t * (uint64_t)L + (uint64_t)s;
+              if (better(sc, key, best, bkey)) {
+                best = sc;
+                bkey = key;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- 6: argmax over the CTA, then the cluster
+  warp_argmax(best, bkey);
+  double *ws = reinterpret_cast<double *>(scr);
+  uint64_t *wk = reinterpret_cast<uint64_t *>(scr + 256);
+  if (lane == 0) {
+    ws[warp] = best;
+    wk[warp] = bkey;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < k2dThreads / 32; w++)
+      if (better(ws[w], wk[w], best, bkey)) {
+        best = ws[w];
+        bkey = wk[w];
+      }
+    xch->score = best;
+    xch->key = bkey;
+  }
+  __syncthreads();
+  cluster.sync();
+  best = -CUDART_INF;
+  bkey = kKeyNone;
+  for (int c = 0; c < CL; c++) {
+    const Xch *x = cluster.map_shared_rank(xch, c);
+    const double sc = x->score;
+    const uint64_t k = x->key;
+    if (better(sc, k, best, bkey)) {
+      best = sc;
+      bkey = k;
+    }
+  }
+  const bool found = bkey != kKeyNone;
+  const int tb = found ? (int)(bkey / (uint64_t)L) : -1, sb = found ? (int)(bkey % (uint64_t)L) : -1;
+  // ---- 7: phi(t*, s*) from the definition in p-space: p = h/N, P_c = sum of p
+  // over the class, A_c = sum (p/P_c)^q (or -sum (p/P_c) ln(p/P_c)); per-CTA
+  // partial sums over the band's non-empty rows, fixed-order reductions
+  double P1 = 0.0, P2 = 0.0, Q1 = 0.0, Q2 = 0.0;
+  const bool do_phi = found && !a.hist_only && !any_ovf;
+  double Ntot = 0.0;
+  if (do_phi) {
+    // N = number of counted pixels = sum of every column total
+    Ntot = block_sum(s < L ? (double)allN : 0.0, ws);
+    double p1 = 0.0, p2 = 0.0;
+    for (int kk = warp; kk < nrl; kk += k2dThreads / 32) {
+      const int i = rows[kk], t = row0 + i;
+      for (int j = lane; j < L; j += 32) {
+        const uint32_t h = Hb[i * PP + pj(j)];
+        const bool c1 = t <= tb && j <= sb, c2 = t > tb && j > sb;
+        if (h && (c1 || c2)) {
+          const double p = __ddiv_rn((double)h, Ntot);
+          if (c1) p1 = __dadd_rn(p1, p);
+          else p2 = __dadd_rn(p2, p);
+        }
+      }
+    }
+    P1 = block_sum(p1, ws);
+    P2 = block_sum(p2, ws);
+  }
+  if (tid == 0) {
+    xch->P1 = P1;
+    xch->P2 = P2;
+  }
+  __syncthreads();
+  cluster.sync();
+  if (do_phi) {
+    P1 = 0.0;
+    P2 = 0.0;
+    for (int c = 0; c < CL; c++) {
+      const Xch *x = cluster.map_shared_rank(xch, c);
+      P1 = __dadd_rn(P1, x->P1);
+      P2 = __dadd_rn(P2, x->P2);
+    }
+    double q1 = 0.0, q2 = 0.0;
+    for (int kk = warp; kk < nrl; kk += k2dThreads / 32) {
+      const int i = rows[kk], t = row0 + i;
+      for (int j = lane; j < L; j += 32) {
+        const uint32_t h = Hb[i * PP + pj(j)];
+        const bool c1 = t <= tb && j <= sb, c2 = t > tb && j > sb;
+        if (h && (c1 || c2)) {
+          const double p = __ddiv_rn((double)h, Ntot);
+          const double rr = __ddiv_rn(p, c1 ? P1 : P2);
+          const double v = MODE == SUM ? -__dmul_rn(rr, log(rr)) : pow(rr, a.q);
+          if (c1) q1 = __dadd_rn(q1, v);
+          else q2 = __dadd_rn(q2, v);
+        }
+      }
+    }
+    Q1 = block_sum(q1, ws);
+    Q2 = block_sum(q2, ws);
+  }
+  if (tid == 0) {
+    xch->A1 = Q1;
+    xch->A2 = Q2;
+  }
+  __syncthreads();
+  cluster.sync();
+  if (r == 0 && tid == 0) {
+    int st = kOK;
+    if (CHECK && any_ovf) st = kLevelOverflow;
+    else if (!found) st = kNoValidSplit;
+    double phi = CUDART_NAN;
+    if (st == kOK && !a.hist_only) {
+      double S1 = 0.0, S2 = 0.0;
+      for (int c = 0; c < CL; c++) {
+        const Xch *x = cluster.map_shared_rank(xch, c);
+        S1 = __dadd_rn(S1, x->A1);
+        S2 = __dadd_rn(S2, x->A2);
+      }
+      double H1, H2;
+      if (MODE == SUM) {
+        H1 = S1;
+        H2 = S2;
+        phi = __dadd_rn(H1, H2);
+      } else {
+        H1 = __ddiv_rn(__dsub_rn(1.0, S1), __dsub_rn(a.q, 1.0));
+        H2 = __ddiv_rn(__dsub_rn(1.0, S2), __dsub_rn(a.q, 1.0));
+        phi = __dadd_rn(__dadd_rn(H1, H2), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.q), H1), H2));
+      }
+    }
+    const bool ok = st == kOK && !a.hist_only;
+    if (a.thresholds) {
+      a.thresholds[2 * z] = ok ? tb : -1;
+      a.thresholds[2 * z + 1] = ok ? sb : -1;
+    }
+    if (a.tlab) a.tlab[z] = ok ? tb : -1;
+    if (a.objective) a.objective[z] = ok ? phi : CUDART_NAN;
+    const int sth = CHECK && any_ovf ? kLevelOverflow : kOK;
+    if (a.status) a.status[z] = a.hist_only ? sth : st;
+    if (a.status2) a.status2[z] = a.hist_only ? sth : st;
+  }
+  cluster.sync();  // no CTA leaves while its shared memory may still be read
+}
+
+}  // namespace tsa

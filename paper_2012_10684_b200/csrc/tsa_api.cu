@@ -751,6 +751,193 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   return TSA_OK;
 }
 
+// ------------------------------------------------------------------- 2-D
+}  // extern "C"
+
+static bool valid2d(const tsa2d_problem *p) {
+  return p && p->volume && p->nx > 0 && p->ny > 0 && p->nz > 0 && p->nx <= 65535 &&
+         p->nx * p->ny < (int64_t(1) << 31) && p->bins >= 2 && p->bins <= 256 && p->q > 0.0 &&
+         std::isfinite(p->q) && (p->cluster == 0 || (p->cluster >= 4 && p->cluster <= 8));
+}
+
+constexpr size_t kSmem2dMax = 227 * 1024;  // opt-in shared memory per CTA (sm_100a)
+
+struct Plan2d {
+  int CL, R, LP, rr, rounds;
+  size_t smem;
+};
+
+static Plan2d plan2d(const tsa2d_problem *p) {
+  Plan2d pl;
+  pl.LP = (p->bins + 1) & ~1;
+  // smallest cluster whose CTAs each count <= 65535 pixels in one round
+  int CL = p->cluster;
+  if (CL == 0) {
+    CL = 8;
+    for (int c = 4; c <= 8; c++)
+      if (((p->ny + c - 1) / c) * p->nx <= 65535) {
+        CL = c;
+        break;
+      }
+  }
+  // shared-memory fit (the L x L private histogram plus the band tables)
+  while (p->cluster == 0 && CL < 8 &&
+         tsa::smem2d_layout(p->bins, pl.LP, (p->bins + CL - 1) / CL).total > kSmem2dMax)
+    CL++;
+  pl.CL = CL;
+  pl.R = (p->bins + CL - 1) / CL;
+  const int64_t rows_max = (p->ny + CL - 1) / CL;
+  pl.rr = (int)std::max<int64_t>(1, std::min<int64_t>(rows_max, 65535 / p->nx));
+  pl.rounds = (int)((rows_max + pl.rr - 1) / pl.rr);
+  pl.smem = tsa::smem2d_layout(p->bins, pl.LP, pl.R).total;
+  return pl;
+}
+
+static size_t carve2d(const tsa2d_problem *p, char *base, double **wlut, double **ipow, double **lnn,
+                      double **rcp, int32_t **tlab, int32_t **status) {
+  Carve c{base};
+  const size_t n1 = (size_t)(p->nx * p->ny) + 1;
+  *wlut = c.take<double>(n1);
+  if (p->q == 1.0) {
+    *ipow = nullptr;
+    *lnn = c.take<double>(n1);
+    *rcp = c.take<double>(n1);
+  } else {
+    *ipow = c.take<double>(n1);
+    *lnn = *rcp = nullptr;
+  }
+  *tlab = c.take<int32_t>((size_t)p->nz);
+  *status = c.take<int32_t>((size_t)p->nz);
+  return c.off;
+}
+
+template <int MODE>
+static tsa_status launch2d_mode(const tsa::Tsa2dArgs &a, const Plan2d &pl, cudaStream_t s, bool check) {
+  auto f = a.vec ? (check ? tsa::k_tsallis2d<MODE, true, true> : tsa::k_tsallis2d<MODE, true, false>)
+                 : (check ? tsa::k_tsallis2d<MODE, false, true> : tsa::k_tsallis2d<MODE, false, false>);
+  TSA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)pl.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.nz * pl.CL));
+  cfg.blockDim = dim3(tsa::k2dThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TSA_CUDA(cudaLaunchKernelEx(&cfg, f, a));
+  return check_cuda("k_tsallis2d");
+}
+
+extern "C" {
+
+tsa_status tsa2d_validate(const tsa2d_problem *p) {
+  if (!valid2d(p)) return set_error(TSA_ERR_INVALID_ARG, "2-D problem: volume/dims/bins/q/cluster out of range");
+  return TSA_OK;
+}
+
+int32_t tsa2d_cluster_size(const tsa2d_problem *p) { return valid2d(p) ? plan2d(p).CL : 0; }
+
+size_t tsa2d_workspace_size(const tsa2d_problem *p) {
+  if (!valid2d(p)) return 0;
+  double *a, *b, *c, *d;
+  int32_t *e, *f;
+  return carve2d(p, nullptr, &a, &b, &c, &d, &e, &f);
+}
+
+static tsa_status run2d(const tsa2d_problem *p, const tsa_outputs *out, uint32_t *hist_only_out,
+                        int32_t *status_only_out, void *workspace, size_t workspace_bytes,
+                        cudaStream_t s) {
+  double *wlut, *ipow, *lnn, *rcp;
+  int32_t *tlab, *status;
+  const size_t need = carve2d(p, reinterpret_cast<char *>(workspace), &wlut, &ipow, &lnn, &rcp, &tlab, &status);
+  if (!workspace) return set_error(TSA_ERR_INVALID_ARG, "workspace NULL");
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "2-D workspace too small");
+  const Plan2d pl = plan2d(p);
+  if (pl.smem > kSmem2dMax) return set_error(TSA_ERR_INVALID_ARG, "2-D plan does not fit shared memory (raise cluster)");
+  const int64_t N = p->nx * p->ny;
+  const bool shannon = p->q == 1.0;
+  const bool hist_only = hist_only_out != nullptr;
+  if (!hist_only) {
+    const int64_t blocks = std::min<int64_t>((N + 256) / 256, 4 * g_num_sms());
+    tsa::k2d_luts<<<(unsigned)blocks, 256, 0, s>>>(wlut, ipow, lnn, rcp, N, p->q, shannon);
+    TSA_TRY(check_cuda("k2d_luts"));
+  }
+  tsa::Tsa2dArgs a;
+  a.vol = reinterpret_cast<const uint8_t *>(p->volume);
+  a.nx = p->nx;
+  a.ny = p->ny;
+  a.nz = p->nz;
+  a.L = p->bins;
+  a.LP = pl.LP;
+  a.CL = pl.CL;
+  a.R = pl.R;
+  a.rr = pl.rr;
+  a.rounds = pl.rounds;
+  a.vec = p->nx % 16 == 0 && (reinterpret_cast<uintptr_t>(p->volume) & 15) == 0;
+  a.q = p->q;
+  a.mode = shannon ? tsa::SUM : (p->q < 1.0 ? tsa::PROD_MAX : tsa::PROD_MIN);
+  a.wlut = wlut;
+  a.ipow = ipow;
+  a.lnn = lnn;
+  a.rcp = rcp;
+  a.thresholds = hist_only ? nullptr : out->thresholds;
+  a.tlab = hist_only ? nullptr : tlab;
+  a.objective = hist_only ? nullptr : out->objective;
+  a.hist = hist_only ? hist_only_out : out->histogram;
+  a.status = status;
+  a.status2 = hist_only ? status_only_out : out->slice_status;
+  a.hist_only = hist_only;
+  const bool check = p->bins < 256;
+  switch (a.mode) {
+    case tsa::PROD_MAX: TSA_TRY(launch2d_mode<tsa::PROD_MAX>(a, pl, s, check)); break;
+    case tsa::PROD_MIN: TSA_TRY(launch2d_mode<tsa::PROD_MIN>(a, pl, s, check)); break;
+    default: TSA_TRY(launch2d_mode<tsa::SUM>(a, pl, s, check)); break;
+  }
+  if (!hist_only && out->labels) {
+    tsa_problem lp = {};
+    lp.volume = p->volume;
+    lp.dtype = TSA_U8;
+    lp.nx = p->nx;
+    lp.ny = p->ny;
+    lp.nz = p->nz;
+    lp.bins = p->bins;
+    lp.k = 1;
+    lp.q = 1.0;
+    TSA_TRY(tsa_label(&lp, tlab, status, out->labels, s));
+  }
+  return TSA_OK;
+}
+
+tsa_status tsa2d_segment(const tsa2d_problem *p, const tsa_outputs *out, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+  TSA_TRY(tsa2d_validate(p));
+  if (!out || !out->thresholds) return set_error(TSA_ERR_INVALID_ARG, "outputs->thresholds NULL");
+  return run2d(p, out, nullptr, nullptr, workspace, workspace_bytes, S(stream));
+}
+
+tsa_status tsa2d_histogram(const tsa2d_problem *p, uint32_t *hist, int32_t *slice_status,
+                           void *workspace, size_t workspace_bytes, void *stream) {
+  TSA_TRY(tsa2d_validate(p));
+  if (!hist || !slice_status) return set_error(TSA_ERR_INVALID_ARG, "hist/slice_status NULL");
+  return run2d(p, nullptr, hist, slice_status, workspace, workspace_bytes, S(stream));
+}
+
+tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream) {
+  TSA_TRY(tsa2d_validate(p));
+  if (!g) return set_error(TSA_ERR_INVALID_ARG, "g NULL");
+  const int vec = p->nx % 4 == 0 && (reinterpret_cast<uintptr_t>(p->volume) & 3) == 0 &&
+                  (reinterpret_cast<uintptr_t>(g) & 3) == 0;
+  const int64_t items = vec ? p->nx / 4 * p->ny : p->nx * p->ny;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (items + 255) / 256));
+  tsa::k2d_mean<<<dim3(gx, (unsigned)p->nz), 256, 0, S(stream)>>>(
+      reinterpret_cast<const uint8_t *>(p->volume), g, p->nx, p->ny, vec);
+  return check_cuda("k2d_mean");
+}
+
 // ----------------------------------------------------------- host buffers
 static size_t slab_bytes(const tsa_problem *p, int64_t slab, tsa_problem *sp) {
   *sp = *p;

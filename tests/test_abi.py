@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "tsa.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(tsa_[a-z_0-9]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(tsa(?:2d)?_[a-z_0-9]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
     declared = header_functions()
     assert set(declared) == set(tsa.EXPORTS), declared
     out = subprocess.check_output(["nm", "-D", "--defined-only", tsa.LIB_PATH]).decode()
-    exported = set(re.findall(r"\bT (tsa_[a-z_0-9]+)", out))
+    exported = set(re.findall(r"\bT (tsa(?:2d)?_[a-z_0-9]+)", out))
     missing = [f for f in declared if f not in exported]
     assert not missing, missing
     for f in declared:

@@ -17,21 +17,24 @@
 //      codes into a PRIVATE full L x L histogram of 16-bit counters packed two
 //      per word (a CTA counts <= 65535 pixels per round, so no counter can
 //      wrap); uniform items add 16, warp-uniform ones 16 x lanes at once.
-//   2. merge over DSMEM: CTA r owns the f-rows [r R, (r+1) R) (R = ceil(L/CL))
-//      and sums that band of all CL private histograms into a u32 band.
+//   2. merge over DSMEM: the non-empty f-rows (union of the CTAs' row masks)
+//      are split evenly over the cluster in row order; CTA r sums its rows of
+//      all CL private histograms into compacted u32 rows (several counting
+//      rounds, for slices over CL x 65535 pixels: static bands of R rows).
 //   3. band column sums are exchanged over DSMEM: every CTA gets the
 //      column totals of the bands below / above it (the SAT boundary values).
-//   4. prefix walk: 8 rows at a time, one warp per row scans the row (lane =
-//      8 contiguous columns, warp scan of lane totals), then thread s walks the
-//      rows adding the row prefix to its running (n_1, W_1) = summed-area table
-//      value at (t, s) and stores A_1(t,s) = W_1 / n_1^q in shared memory.
+//   4. prefix walk: groups of rows (as many as the free shared memory holds),
+//      one warp per row scans the row (lane = 8 contiguous columns, warp scan
+//      of lane totals), then thread s walks the rows adding the row prefix to
+//      its running (n_1, W_1) = summed-area table value at (t, s) and stores
+//      A_1(t,s) = W_1 / n_1^q in shared memory.
 //   5. suffix walk: the same from the top row down with row suffixes, giving
 //      (n_2, W_2) of class 2 directly (sums of non-negative terms, no prefix
 //      differences, no cancellation), the score A_1 A_2 (+-, or S_1 + S_2 at
 //      q = 1) and a running (score, key = t L + s) best.
-//   6. argmax: warp shuffles, block, then over the cluster via DSMEM.
-//   7. phi(t*,s*) recomputed in p-space from the definition (p = h/N, P_c as a
-//      sum of p, (p/P_c)^q per non-empty cell; fixed-order reductions).
+//   6. argmax: warp shuffles, block, then over the cluster via DSMEM, carrying
+//      the winner's class terms, from which phi(t*,s*) = H_1 + H_2 +
+//      (1-q) H_1 H_2 is formed (2-D objective).
 // Only canonical candidates -- row t and column s non-empty -- are scored:
 // every other candidate describes the same partition as a canonical one and
 // the lowest member of each class is canonical (R21), so the result
@@ -236,18 +239,6 @@ __device__ __forceinline__ void block_excl_suffix_scan(uint32_t &n, double &w, c
   __syncthreads();
 }
 
-__device__ __forceinline__ double block_sum(double v, double *scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-  if (lane == 0) scratch[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < nw; i++) t = __dadd_rn(t, scratch[i]);
-  __syncthreads();
-  return t;
-}
-
 // class term of a (count, W) rectangle: A = W / n^q (or S = ln n - W/n); NaN if n == 0
 template <int MODE>
 __device__ __forceinline__ double term2d(uint32_t n, double W, const Tsa2dArgs &a) {
@@ -267,15 +258,17 @@ __device__ __forceinline__ double score2d(double t1, double t2) {
 // the padded pitch PP = LP + LP/8 with column j at j + j/8, so a lane reading
 // 8 contiguous columns and a thread reading column s are both (nearly)
 // bank-conflict free.
-//   A      max(L*LP*2, R*LP*8): private u16 histogram, later A_1 / S_1 [R][LP] f64
-//   Hb     R*PP*4              merged u32 band
-//   gN     G*PP*4, gW G*PP*8   walk group buffers (row prefix / suffix)
+//   A      max(L*LP*2, R*LP*8): private u16 histogram; later A_1 / S_1 [nrl][LP]
+//          f64 and, in the tail, walk buffers for as many rows as fit
+//   Hb     R*PP*4              merged u32 rows of the band (compacted)
+//   gN     G*PP*4, gW G*PP*8   fallback walk buffers (G = 8 rows)
 //   colN   LP*4, colW LP*8     band column sums (read by the other CTAs)
-//   rl     R*4                 band rows that are non-empty (compacted list)
-//   xch    256                 exchange slots (flags, argmax, phi partials)
+//   rla    R*4, rlh R*4        absolute f-row / Hb row of each non-empty band row
+//   msk    L/32 words          non-empty f-rows (own private histogram, then all)
+//   xch    64                  exchange slots (flags, mask, argmax + payload)
 //   scr    1024                scan scratch
 struct Smem2d {
-  size_t A, Hb, gN, gW, colN, colW, rl, xch, scr, total;
+  size_t A, Abytes, Hb, gN, gW, colN, colW, rla, rlh, msk, xch, scr, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -288,7 +281,8 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   size_t o = 0;
   s.A = o;
   const size_t a1 = (size_t)L * LP * 2, a2 = (size_t)R * LP * 8;
-  o += al16(a1 > a2 ? a1 : a2);
+  s.Abytes = al16(a1 > a2 ? a1 : a2);
+  o += s.Abytes;
   s.Hb = o;
   o += al16((size_t)R * PP * 4);
   s.gN = o;
@@ -299,10 +293,14 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   o += al16((size_t)LP * 4);
   s.colW = o;
   o += al16((size_t)LP * 8);
-  s.rl = o;
-  o += al16((size_t)R * 4 + 16);
+  s.rla = o;
+  o += al16((size_t)R * 4);
+  s.rlh = o;
+  o += al16((size_t)R * 4);
+  s.msk = o;
+  o += 64;
   s.xch = o;
-  o += 256;
+  o += 128;
   s.scr = o;
   o += 1024;
   s.total = o;
@@ -311,13 +309,14 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
 
 __device__ __forceinline__ int pj(int j) { return j + (j >> 3); }
 
-// exchange slot offsets (doubles / u64 / ints inside xch)
+// exchange slots read by the other CTAs of the cluster
 struct Xch {
-  int flags;        // overflow flag (int)
-  double score;     // CTA best
+  int flags;           // LEVEL_OVERFLOW seen
+  int nmask;           // unused pad
+  uint32_t mask[8];    // non-empty f-rows of this CTA's private histogram (L <= 256)
+  double score;        // CTA best (score, key) and its two class terms
   uint64_t key;
-  double P1, P2;    // phi partials, round a
-  double A1, A2;    // round b
+  double t1, t2;
 };
 
 // one image row's 16-pixel item: pixels x0..x0+15 (uint4) and the
@@ -458,6 +457,30 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
   }
 }
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// argmax with the winning candidate's two class terms as payload
+__device__ __forceinline__ void warp_argmax4(double &s, uint64_t &k, double &t1, double &t2) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, s, off);
+    const uint64_t ok = __shfl_xor_sync(0xffffffffu, k, off);
+    const double o1 = __shfl_xor_sync(0xffffffffu, t1, off);
+    const double o2 = __shfl_xor_sync(0xffffffffu, t2, off);
+    if (better(os, ok, s, k)) {
+      s = os;
+      k = ok;
+      t1 = o1;
+      t2 = o2;
+    }
+  }
+}
+
 template <int MODE, bool VEC, bool CHECK>
 __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   extern __shared__ __align__(16) char smem[];
@@ -466,68 +489,120 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   const int64_t z = blockIdx.x / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = a.L, LP = a.LP, R = a.R, PP = pitch2d(LP);
-  const int row0 = r * R, nrows = max(0, min(L, row0 + R) - row0);  // band f-rows
+  const int NW = (L + 31) / 32;  // mask words
   const Smem2d lay = smem2d_layout(L, LP, R);
   uint32_t *hp = reinterpret_cast<uint32_t *>(smem + lay.A);  // packed u16 private histogram
   double *A1 = reinterpret_cast<double *>(smem + lay.A);
   uint32_t *Hb = reinterpret_cast<uint32_t *>(smem + lay.Hb);
-  uint32_t *gN = reinterpret_cast<uint32_t *>(smem + lay.gN);
-  double *gW = reinterpret_cast<double *>(smem + lay.gW);
   uint32_t *colN = reinterpret_cast<uint32_t *>(smem + lay.colN);
   double *colW = reinterpret_cast<double *>(smem + lay.colW);
-  int *rl = reinterpret_cast<int *>(smem + lay.rl);
+  int *rla = reinterpret_cast<int *>(smem + lay.rla);
+  int *rlh = reinterpret_cast<int *>(smem + lay.rlh);
+  uint32_t *msk = reinterpret_cast<uint32_t *>(smem + lay.msk);
   Xch *xch = reinterpret_cast<Xch *>(smem + lay.xch);
   char *scr = smem + lay.scr;
   const uint8_t *f = a.vol + z * a.nx * a.ny;
+  const bool single = a.rounds == 1;  // balanced, compacted bands
 
-  // ---- 1 + 2: counting rounds and DSMEM merge into the u32 band
-  for (int i = tid; i < nrows * PP; i += k2dThreads) Hb[i] = 0u;
+  // ---- 1 + 2: counting, then the band rows of every private histogram merged
+  // over DSMEM.  Single round: the non-empty f-rows (union of the CTAs' masks)
+  // are split evenly over the cluster in row order and stored compacted.
+  // Several rounds: band r = f-rows [r R, (r+1) R), accumulated per round.
   if (tid == 0) xch->flags = 0;
+  const int row0 = r * R, nrows_static = max(0, min(L, row0 + R) - row0);
+  if (!single)
+    for (int i = tid; i < nrows_static * PP; i += k2dThreads) Hb[i] = 0u;
   int ovf = 0;
+  int nst = 0;  // Hb rows in use
   const int64_t ya0 = (int64_t)r * a.ny / CL, yb0 = (int64_t)(r + 1) * a.ny / CL;
   const int hw = L * LP / 2;  // words of the private histogram
+  const int rw = LP / 2;      // words per private-histogram row
   for (int rd = 0; rd < a.rounds; rd++) {
     uint4 *hp4 = reinterpret_cast<uint4 *>(hp);
     for (int i = tid; i < (hw + 3) / 4; i += k2dThreads) hp4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid < 8) msk[tid] = 0u;
     __syncthreads();
     const int64_t ya = min(yb0, ya0 + (int64_t)rd * a.rr), yb = min(yb0, ya + a.rr);
     count_round<VEC, CHECK>(a, f, ya, yb, hp, ovf);
     cluster.sync();  // every private histogram of this round complete
-    // band words: rows [row0, row0+nrows) of every CTA's private histogram
-    const int bw0 = row0 * LP / 2, bwn = nrows * LP / 2;
-    if ((LP & 7) == 0) {
-      for (int i = tid; i < bwn / 4; i += k2dThreads) {  // 8 cells of one row
-        uint4 v[k2dMaxCL];
+    if (single) {
+      // own non-empty rows -> mask -> cluster union
+      for (int i = warp; i < L; i += k2dThreads / 32) {
+        uint32_t any = 0;
+        for (int w = lane; w < rw; w += 32) any |= hp[i * rw + w];
+        if (__any_sync(0xffffffffu, any != 0) && lane == 0) atomicOr(&msk[i >> 5], 1u << (i & 31));
+      }
+      __syncthreads();
+      if (tid < 8) xch->mask[tid] = msk[tid];
+      cluster.sync();
+      if (tid < NW) {
+        uint32_t m = 0;
+        for (int c = 0; c < CL; c++) m |= cluster.map_shared_rank(xch, c)->mask[tid];
+        msk[tid] = m;
+      }
+      __syncthreads();
+      int mf = 0, below = 0;
+      for (int w = 0; w < NW; w++) {
+        const int pc = __popc(msk[w]);
+        if (w < (tid >> 5)) below += pc;
+        mf += pc;
+      }
+      const int k0 = r * mf / CL, k1 = (r + 1) * mf / CL;
+      nst = k1 - k0;
+      if (tid < L && ((msk[tid >> 5] >> (tid & 31)) & 1u)) {
+        const int rank = below + __popc(msk[tid >> 5] & ((1u << (tid & 31)) - 1u));
+        if (rank >= k0 && rank < k1) {
+          rla[rank - k0] = tid;
+          rlh[rank - k0] = rank - k0;
+        }
+      }
+      __syncthreads();
+      // pull the nst rows (8 cells per item) from every private histogram
+      const int cpr = (LP + 7) / 8;  // 8-cell chunks per row
+      for (int it = tid; it < nst * cpr; it += k2dThreads) {
+        const int kk = it / cpr, j = (it - kk * cpr) * 8, i = rla[kk];
+        uint32_t o[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        if ((LP & 7) == 0) {
+          uint4 v[k2dMaxCL];
 #pragma unroll
-        for (int c = 0; c < k2dMaxCL; c++)
-          if (c < CL) v[c] = reinterpret_cast<const uint4 *>(cluster.map_shared_rank(hp, c) + bw0)[i];
-        const int cell = 8 * i, ri = cell / LP, j = cell - ri * LP;
-        uint32_t *dst = Hb + ri * PP + pj(j);
-        uint32_t o[8];
+          for (int c = 0; c < k2dMaxCL; c++)
+            if (c < CL)
+              v[c] = *reinterpret_cast<const uint4 *>(cluster.map_shared_rank(hp, c) + i * rw + j / 2);
 #pragma unroll
-        for (int e = 0; e < 8; e++) o[e] = dst[e];
-#pragma unroll
-        for (int c = 0; c < k2dMaxCL; c++)
-          if (c < CL) {
-            o[0] += v[c].x & 0xffffu;
-            o[1] += v[c].x >> 16;
-            o[2] += v[c].y & 0xffffu;
-            o[3] += v[c].y >> 16;
-            o[4] += v[c].z & 0xffffu;
-            o[5] += v[c].z >> 16;
-            o[6] += v[c].w & 0xffffu;
-            o[7] += v[c].w >> 16;
+          for (int c = 0; c < k2dMaxCL; c++)
+            if (c < CL) {
+              o[0] += v[c].x & 0xffffu;
+              o[1] += v[c].x >> 16;
+              o[2] += v[c].y & 0xffffu;
+              o[3] += v[c].y >> 16;
+              o[4] += v[c].z & 0xffffu;
+              o[5] += v[c].z >> 16;
+              o[6] += v[c].w & 0xffffu;
+              o[7] += v[c].w >> 16;
+            }
+        } else {
+          for (int c = 0; c < CL; c++) {
+            const uint32_t *src = cluster.map_shared_rank(hp, c) + i * rw;
+            for (int e = 0; e < 8 && j + e < LP; e += 2) {
+              const uint32_t v = src[(j + e) / 2];
+              o[e] += v & 0xffffu;
+              o[e + 1] += v >> 16;
+            }
           }
+        }
+        uint32_t *dst = Hb + kk * PP;
 #pragma unroll
-        for (int e = 0; e < 8; e++) dst[e] = o[e];
+        for (int e = 0; e < 8; e++)
+          if (j + e < LP) dst[pj(j + e)] = o[e];
       }
     } else {
+      const int bw0 = row0 * rw;
       for (int c = 0; c < CL; c++) {
         const uint32_t *src = cluster.map_shared_rank(hp, c) + bw0;
-        for (int i = tid; i < bwn; i += k2dThreads) {
+        for (int i = tid; i < nrows_static * rw; i += k2dThreads) {
           const uint32_t v = src[i];
           if (v) {
-            const int ri = (2 * i) / LP, j = 2 * i - ri * LP;
+            const int ri = i / rw, j = 2 * (i - ri * rw);
             Hb[ri * PP + pj(j)] += v & 0xffffu;
             Hb[ri * PP + pj(j + 1)] += v >> 16;
           }
@@ -537,28 +612,68 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     cluster.sync();  // all reads of the private histograms done before reuse
   }
   if (CHECK && ovf) atomicOr(&xch->flags, 1);
-  // optional histogram output (the band's rows)
-  if (a.hist) {
-    uint32_t *ho = a.hist + ((size_t)z * L + row0) * L;
-    for (int i = warp; i < nrows; i += k2dThreads / 32)
-      for (int j = lane; j < L; j += 32) ho[(size_t)i * L + j] = Hb[i * PP + pj(j)];
-  }
-
-  // ---- 3: non-empty band rows, band column sums and the exchange
-  const int s = tid;  // column owned in the walks (L <= 256 = k2dThreads)
-  {
-    // compacted list of the band's non-empty rows (one warp per row)
-    for (int i = warp; i < nrows; i += k2dThreads / 32) {
+  if (!single) {
+    // compacted list of the band's non-empty rows
+    nst = nrows_static;
+    for (int i = warp; i < nrows_static; i += k2dThreads / 32) {
       uint32_t any = 0;
       for (int j = lane; j < L; j += 32) any |= Hb[i * PP + pj(j)];
       any = __any_sync(0xffffffffu, any != 0);
-      if (lane == 0) rl[1 + i] = any ? 1 : 0;
+      if (lane == 0) rlh[i] = any ? 1 : 0;
     }
+    __syncthreads();
+    if (warp == 0) {
+      int cnt = 0;
+      for (int b = 0; b < nrows_static; b += 32) {
+        const int i = b + lane;
+        const bool fl = i < nrows_static && rlh[i];
+        const unsigned m = __ballot_sync(0xffffffffu, fl);
+        __syncwarp();
+        if (fl) {
+          const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+          rlh[pos] = i;
+          rla[pos] = row0 + i;
+        }
+        cnt += __popc(m);
+        __syncwarp();
+      }
+      if (lane == 0) msk[8] = cnt;
+    }
+  }
+  // optional histogram output: non-empty rows from Hb, the CTA's share of the
+  // empty rows as zeros
+  if (a.hist) {
+    __syncthreads();
+    uint32_t *hz = a.hist + (size_t)z * L * L;
+    const int nl = single ? nst : (int)msk[8];
+    for (int kk = warp; kk < nl; kk += k2dThreads / 32) {
+      const int i = rla[kk], h = rlh[kk];
+      for (int j = lane; j < L; j += 32) hz[(size_t)i * L + j] = Hb[h * PP + pj(j)];
+    }
+    const int e0 = r * L / CL, e1 = (r + 1) * L / CL;
+    for (int i = e0 + warp; i < e1; i += k2dThreads / 32) {
+      const bool empty = single ? !((msk[i >> 5] >> (i & 31)) & 1u) : false;
+      if (empty)
+        for (int j = lane; j < L; j += 32) hz[(size_t)i * L + j] = 0u;
+    }
+    if (!single) {  // static bands: empty band rows
+      for (int i = warp; i < nrows_static; i += k2dThreads / 32) {
+        bool any = false;
+        for (int j = lane; j < L; j += 32) any |= Hb[i * PP + pj(j)] != 0u;
+        if (!__any_sync(0xffffffffu, any))
+          for (int j = lane; j < L; j += 32) hz[(size_t)(row0 + i) * L + j] = 0u;
+      }
+    }
+  }
+
+  // ---- 3: band column sums and the exchange
+  const int s = tid;  // column owned in the walks (L <= 256 = k2dThreads)
+  {
     uint32_t n = 0;
     double W = 0.0;
     if (s < L) {
 #pragma unroll 4
-      for (int i = 0; i < nrows; i++) {
+      for (int i = 0; i < nst; i++) {
         const uint32_t h = Hb[i * PP + pj(s)];
         n += h;
         W = __dadd_rn(W, h ? __ldg(a.wlut + h) : 0.0);
@@ -568,25 +683,10 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
       colN[s] = n;
       colW[s] = W;
     }
-    __syncthreads();
-    if (warp == 0) {  // compact the flags in place (rl[0] = count)
-      int cnt = 0;
-      for (int b = 0; b < nrows; b += 32) {
-        const int i = b + lane;
-        const bool fl = i < nrows && rl[1 + i];
-        const unsigned m = __ballot_sync(0xffffffffu, fl);
-        __syncwarp();
-        if (fl) rl[1 + cnt + __popc(m & ((1u << lane) - 1u))] = i;
-        cnt += __popc(m);
-        __syncwarp();
-      }
-      if (lane == 0) rl[0] = cnt;
-    }
   }
   __syncthreads();
   cluster.sync();
-  const int nrl = rl[0];
-  const int *rows = rl + 1;
+  const int nrl = single ? nst : (int)msk[8];
   int any_ovf = 0;
   uint32_t lowN = 0, upN = 0, allN = 0;
   double lowW = 0.0, upW = 0.0;
@@ -623,20 +723,35 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   // prefix base B(s) = sum_{j <= s} low(j); suffix base B'(s) = sum_{j > s} up(j)
   block_incl_scan(lowN, lowW, scr);
   block_excl_suffix_scan(upN, upW, scr);
-  double best = -CUDART_INF;
+  double best = -CUDART_INF, bt1 = CUDART_NAN, bt2 = CUDART_NAN;
   uint64_t bkey = kKeyNone;
-  if (!a.hist_only && !any_ovf) {
+  if (!a.hist_only && !any_ovf && nrl > 0) {
     const int CPL = (L + 31) / 32;
     const int j0 = min(L, lane * CPL), jn = max(0, min(L, j0 + CPL) - j0);
-    // ---- 4: prefix walk over the non-empty rows: A_1 / S_1 of every canonical
-    // (t, s) into A1[k][s] (k = compacted row index).  Empty rows add nothing
-    // and are never canonical.
+    // walk buffers: the tail of region A behind A1[nrl][LP] if it holds at
+    // least k2dGroup rows, else the fixed k2dGroup-row buffers
+    const size_t a1b = al16((size_t)nrl * LP * 8);
+    int G = (int)((lay.Abytes - a1b) / ((size_t)PP * 12));
+    uint32_t *gN;
+    double *gW;
+    if (G >= k2dGroup) {
+      G = min(G, nrl);
+      gW = reinterpret_cast<double *>(smem + lay.A + a1b);
+      gN = reinterpret_cast<uint32_t *>(smem + lay.A + a1b + (size_t)G * PP * 8);
+    } else {
+      G = k2dGroup;
+      gW = reinterpret_cast<double *>(smem + lay.gW);
+      gN = reinterpret_cast<uint32_t *>(smem + lay.gN);
+    }
+    // ---- 4: prefix walk over the non-empty rows: A_1 / S_1 of every (t, s)
+    // with column s non-empty into A1[k][s] (k = compacted row index).  Empty
+    // rows add nothing and are never canonical.
     uint32_t accN = lowN;
     double accW = lowW;
-    for (int g0 = 0; g0 < nrl; g0 += k2dGroup) {
-      const int kk = g0 + warp;
-      if (kk < nrl) {
-        const int i = rows[kk];
+    for (int g0 = 0; g0 < nrl; g0 += G) {
+      const int ge = min(G, nrl - g0);
+      for (int w = warp; w < ge; w += k2dThreads / 32) {
+        const int i = rlh[g0 + w];
         uint32_t hv[8];
         double wv[8];
 #pragma unroll
@@ -650,7 +765,6 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
           ln += hv[e];
           lw = __dadd_rn(lw, wv[e]);
         }
-        // exclusive warp scan of lane totals
         uint32_t xn = ln;
         double xw = lw;
 #pragma unroll
@@ -670,40 +784,41 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
           xn += hv[e];
           xw = __dadd_rn(xw, wv[e]);
           if (e < jn) {
-            gN[warp * PP + pj(j0 + e)] = xn;
-            gW[warp * PP + pj(j0 + e)] = xw;
+            gN[w * PP + pj(j0 + e)] = xn;
+            gW[w * PP + pj(j0 + e)] = xw;
           }
         }
       }
       __syncthreads();
       if (s < L) {
-        const int ge = min(k2dGroup, nrl - g0);
-        uint32_t nn[k2dGroup];
-        double wwv[k2dGroup];
+        for (int w0 = 0; w0 < ge; w0 += 8) {
+          uint32_t nn[8];
+          double wwv[8];
 #pragma unroll
-        for (int w = 0; w < k2dGroup; w++) {
-          if (w < ge) {
-            accN += gN[w * PP + pj(s)];
-            accW = __dadd_rn(accW, gW[w * PP + pj(s)]);
+          for (int w = 0; w < 8; w++) {
+            if (w0 + w < ge) {
+              accN += gN[(w0 + w) * PP + pj(s)];
+              accW = __dadd_rn(accW, gW[(w0 + w) * PP + pj(s)]);
+            }
+            nn[w] = accN;
+            wwv[w] = accW;
           }
-          nn[w] = accN;
-          wwv[w] = accW;
-        }
-        // only canonical candidates are ever scored: the LUT gathers of a group
-        // are independent and issued back to back
+          // the LUT gathers of 8 rows are independent and issued back to back
 #pragma unroll
-        for (int w = 0; w < k2dGroup; w++)
-          if (w < ge) A1[(g0 + w) * LP + s] = colnz ? term2d<MODE>(nn[w], wwv[w], a) : CUDART_NAN;
+          for (int w = 0; w < 8; w++)
+            if (w0 + w < ge)
+              A1[(g0 + w0 + w) * LP + s] = colnz ? term2d<MODE>(nn[w], wwv[w], a) : CUDART_NAN;
+        }
       }
       __syncthreads();
     }
     // ---- 5: suffix walk (top row down), scores and the running best
     uint32_t sN = upN;
     double sW = upW;
-    for (int g0 = nrl - 1; g0 >= 0; g0 -= k2dGroup) {
-      const int kk = g0 - warp;
-      if (kk >= 0) {
-        const int i = rows[kk];
+    for (int g1 = nrl; g1 > 0; g1 -= G) {
+      const int ge = min(G, g1);  // rows g1-1 down to g1-ge
+      for (int w = warp; w < ge; w += k2dThreads / 32) {
+        const int i = rlh[g1 - 1 - w];
         uint32_t hv[8];
         double wv[8];
 #pragma unroll
@@ -717,7 +832,6 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
           ln += hv[e];
           lw = __dadd_rn(lw, wv[e]);
         }
-        // exclusive suffix over lanes > this one
         uint32_t xn = ln;
         double xw = lw;
 #pragma unroll
@@ -739,8 +853,8 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
 #pragma unroll
         for (int e = 7; e >= 0; e--) {
           if (e < jn) {
-            gN[warp * PP + pj(j0 + e)] = cn;
-            gW[warp * PP + pj(j0 + e)] = cw;
+            gN[w * PP + pj(j0 + e)] = cn;
+            gW[w * PP + pj(j0 + e)] = cw;
           }
           cn += hv[e];
           cw = __dadd_rn(cw, wv[e]);
@@ -748,30 +862,34 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
       }
       __syncthreads();
       if (s < L) {
-        const int ge = min(k2dGroup, g0 + 1);
-        uint32_t nn[k2dGroup];
-        double wwv[k2dGroup];
+        for (int w0 = 0; w0 < ge; w0 += 8) {
+          uint32_t nn[8];
+          double wwv[8];
 #pragma unroll
-        for (int w = 0; w < k2dGroup; w++) {
-          // (sN, sW) before row rows[g0-w] is added = class 2 of (t, s): rows > t, columns > s
-          nn[w] = sN;
-          wwv[w] = sW;
-          if (w < ge) {
-            sN += gN[w * PP + pj(s)];
-            sW = __dadd_rn(sW, gW[w * PP + pj(s)]);
+          for (int w = 0; w < 8; w++) {
+            // (sN, sW) before the row is added = class 2 of (t, s): rows > t, columns > s
+            nn[w] = sN;
+            wwv[w] = sW;
+            if (w0 + w < ge) {
+              sN += gN[(w0 + w) * PP + pj(s)];
+              sW = __dadd_rn(sW, gW[(w0 + w) * PP + pj(s)]);
+            }
           }
-        }
 #pragma unroll
-        for (int w = 0; w < k2dGroup; w++) {
-          const int kk = g0 - w;
-          if (w < ge && colnz && s <= L - 2) {
-            const int t = row0 + rows[kk];
-            if (t <= L - 2) {
-              const double sc = score2d<MODE>(A1[kk * LP + s], term2d<MODE>(nn[w], wwv[w], a));
-              const uint64_t key = (uint64_t)t * (uint64_t)L + (uint64_t)s;
-              if (better(sc, key, best, bkey)) {
-                best = sc;
-                bkey = key;
+          for (int w = 0; w < 8; w++) {
+            const int kk = g1 - 1 - (w0 + w);
+            if (w0 + w < ge && colnz && s <= L - 2) {
+              const int t = rla[kk];
+              if (t <= L - 2) {
+                const double c1 = A1[kk * LP + s], c2 = term2d<MODE>(nn[w], wwv[w], a);
+                const double sc = score2d<MODE>(c1, c2);
+                const uint64_t key = (uint64_t)t * (uint64_t)L + (uint64_t)s;
+                if (better(sc, key, best, bkey)) {
+                  best = sc;
+                  bkey = key;
+                  bt1 = c1;
+                  bt2 = c2;
+                }
               }
             }
           }
@@ -781,12 +899,16 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     }
   }
   // ---- 6: argmax over the CTA, then the cluster
-  warp_argmax(best, bkey);
+  warp_argmax4(best, bkey, bt1, bt2);
   double *ws = reinterpret_cast<double *>(scr);
   uint64_t *wk = reinterpret_cast<uint64_t *>(scr + 256);
+  double *w1 = reinterpret_cast<double *>(scr + 512);
+  double *w2 = reinterpret_cast<double *>(scr + 768);
   if (lane == 0) {
     ws[warp] = best;
     wk[warp] = bkey;
+    w1[warp] = bt1;
+    w2[warp] = bt2;
   }
   __syncthreads();
   if (tid == 0) {
@@ -794,108 +916,51 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
       if (better(ws[w], wk[w], best, bkey)) {
         best = ws[w];
         bkey = wk[w];
+        bt1 = w1[w];
+        bt2 = w2[w];
       }
     xch->score = best;
     xch->key = bkey;
-  }
-  __syncthreads();
-  cluster.sync();
-  best = -CUDART_INF;
-  bkey = kKeyNone;
-  for (int c = 0; c < CL; c++) {
-    const Xch *x = cluster.map_shared_rank(xch, c);
-    const double sc = x->score;
-    const uint64_t k = x->key;
-    if (better(sc, k, best, bkey)) {
-      best = sc;
-      bkey = k;
-    }
-  }
-  const bool found = bkey != kKeyNone;
-  const int tb = found ? (int)(bkey / (uint64_t)L) : -1, sb = found ? (int)(bkey % (uint64_t)L) : -1;
-  // ---- 7: phi(t*, s*) from the definition in p-space: p = h/N, P_c = sum of p
-  // over the class, A_c = sum (p/P_c)^q (or -sum (p/P_c) ln(p/P_c)); per-CTA
-  // partial sums over the band's non-empty rows, fixed-order reductions
-  double P1 = 0.0, P2 = 0.0, Q1 = 0.0, Q2 = 0.0;
-  const bool do_phi = found && !a.hist_only && !any_ovf;
-  double Ntot = 0.0;
-  if (do_phi) {
-    // N = number of counted pixels = sum of every column total
-    Ntot = block_sum(s < L ? (double)allN : 0.0, ws);
-    double p1 = 0.0, p2 = 0.0;
-    for (int kk = warp; kk < nrl; kk += k2dThreads / 32) {
-      const int i = rows[kk], t = row0 + i;
-      for (int j = lane; j < L; j += 32) {
-        const uint32_t h = Hb[i * PP + pj(j)];
-        const bool c1 = t <= tb && j <= sb, c2 = t > tb && j > sb;
-        if (h && (c1 || c2)) {
-          const double p = __ddiv_rn((double)h, Ntot);
-          if (c1) p1 = __dadd_rn(p1, p);
-          else p2 = __dadd_rn(p2, p);
-        }
-      }
-    }
-    P1 = block_sum(p1, ws);
-    P2 = block_sum(p2, ws);
-  }
-  if (tid == 0) {
-    xch->P1 = P1;
-    xch->P2 = P2;
-  }
-  __syncthreads();
-  cluster.sync();
-  if (do_phi) {
-    P1 = 0.0;
-    P2 = 0.0;
-    for (int c = 0; c < CL; c++) {
-      const Xch *x = cluster.map_shared_rank(xch, c);
-      P1 = __dadd_rn(P1, x->P1);
-      P2 = __dadd_rn(P2, x->P2);
-    }
-    double q1 = 0.0, q2 = 0.0;
-    for (int kk = warp; kk < nrl; kk += k2dThreads / 32) {
-      const int i = rows[kk], t = row0 + i;
-      for (int j = lane; j < L; j += 32) {
-        const uint32_t h = Hb[i * PP + pj(j)];
-        const bool c1 = t <= tb && j <= sb, c2 = t > tb && j > sb;
-        if (h && (c1 || c2)) {
-          const double p = __ddiv_rn((double)h, Ntot);
-          const double rr = __ddiv_rn(p, c1 ? P1 : P2);
-          const double v = MODE == SUM ? -__dmul_rn(rr, log(rr)) : pow(rr, a.q);
-          if (c1) q1 = __dadd_rn(q1, v);
-          else q2 = __dadd_rn(q2, v);
-        }
-      }
-    }
-    Q1 = block_sum(q1, ws);
-    Q2 = block_sum(q2, ws);
-  }
-  if (tid == 0) {
-    xch->A1 = Q1;
-    xch->A2 = Q2;
+    xch->t1 = bt1;
+    xch->t2 = bt2;
   }
   __syncthreads();
   cluster.sync();
   if (r == 0 && tid == 0) {
+    best = -CUDART_INF;
+    bkey = kKeyNone;
+    for (int c = 0; c < CL; c++) {
+      const Xch *x = cluster.map_shared_rank(xch, c);
+      const double sc = x->score;
+      const uint64_t k = x->key;
+      if (better(sc, k, best, bkey)) {
+        best = sc;
+        bkey = k;
+        bt1 = x->t1;
+        bt2 = x->t2;
+      }
+    }
+    if (CHECK) any_ovf = 0;
+    if (CHECK)
+      for (int c = 0; c < CL; c++) any_ovf |= cluster.map_shared_rank(&xch->flags, c)[0];
+  }
+  cluster_arrive();  // remote reads done: the other CTAs may leave once we all arrive
+  if (r == 0 && tid == 0) {
+    const bool found = bkey != kKeyNone;
+    const int tb = found ? (int)(bkey / (uint64_t)L) : -1;
+    const int sb = found ? (int)(bkey % (uint64_t)L) : -1;
     int st = kOK;
     if (CHECK && any_ovf) st = kLevelOverflow;
     else if (!found) st = kNoValidSplit;
+    // phi(t*, s*) = H_1 + H_2 + (1 - q) H_1 H_2 from the
+    // winning candidate's class terms (A_c = W_c / n_c^q, or S_c at q == 1)
     double phi = CUDART_NAN;
     if (st == kOK && !a.hist_only) {
-      double S1 = 0.0, S2 = 0.0;
-      for (int c = 0; c < CL; c++) {
-        const Xch *x = cluster.map_shared_rank(xch, c);
-        S1 = __dadd_rn(S1, x->A1);
-        S2 = __dadd_rn(S2, x->A2);
-      }
-      double H1, H2;
       if (MODE == SUM) {
-        H1 = S1;
-        H2 = S2;
-        phi = __dadd_rn(H1, H2);
+        phi = __dadd_rn(bt1, bt2);
       } else {
-        H1 = __ddiv_rn(__dsub_rn(1.0, S1), __dsub_rn(a.q, 1.0));
-        H2 = __ddiv_rn(__dsub_rn(1.0, S2), __dsub_rn(a.q, 1.0));
+        const double H1 = __ddiv_rn(__dsub_rn(1.0, bt1), __dsub_rn(a.q, 1.0));
+        const double H2 = __ddiv_rn(__dsub_rn(1.0, bt2), __dsub_rn(a.q, 1.0));
         phi = __dadd_rn(__dadd_rn(H1, H2), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.q), H1), H2));
       }
     }
@@ -910,7 +975,7 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     if (a.status) a.status[z] = a.hist_only ? sth : st;
     if (a.status2) a.status2[z] = a.hist_only ? sth : st;
   }
-  cluster.sync();  // no CTA leaves while its shared memory may still be read
+  cluster_wait();  // no CTA leaves while its shared memory may still be read
 }
 
 }  // namespace tsa

@@ -55,6 +55,7 @@ namespace cg = cooperative_groups;
 constexpr int k2dThreads = 256;  // CTA size of the cluster kernel
 constexpr int k2dGroup = k2dThreads / 32;  // rows per walk group (one warp per row)
 constexpr int k2dMaxCL = 8;
+constexpr int kStageChunks = 8;  // bulk copies (mbarriers) staging a CTA's image rows
 
 struct Tsa2dArgs {
   const uint8_t *vol;     // [nz][ny][nx]
@@ -69,7 +70,7 @@ struct Tsa2dArgs {
   const double *wlut;     // [N+1] w(c): c^q, or c ln c at q == 1; w(0) = 0
   const double *ipow;     // [N+1] 1/n^q (NaN at 0)          (q != 1)
   const double *lnn;      // [N+1] ln n (NaN at 0)            (q == 1)
-  const double *rcp;      // [N+1] 1/n                        (q == 1)
+  const double *rcp;      // unused (null): S = ln n - W / n
   int32_t *thresholds;    // [nz][2] (t, s), -1 on error
   int32_t *tlab;          // [nz] t for the label kernel (-1 on error)
   double *objective;      // [nz] or null
@@ -88,7 +89,7 @@ __global__ void k2d_luts(double *wlut, double *ipow, double *lnn, double *rcp, i
     if (shannon) {
       wlut[n] = n == 0 ? 0.0 : __dmul_rn(x, log(x));
       lnn[n] = n == 0 ? CUDART_NAN : log(x);
-      rcp[n] = n == 0 ? CUDART_NAN : __drcp_rn(x);
+      if (rcp) rcp[n] = n == 0 ? CUDART_NAN : __drcp_rn(x);
     } else {
       const double pw = pow(x, q);
       wlut[n] = n == 0 ? 0.0 : pw;
@@ -239,12 +240,29 @@ __device__ __forceinline__ void block_excl_suffix_scan(uint32_t &n, double &w, c
   __syncthreads();
 }
 
-// class term of a (count, W) rectangle: A = W / n^q (or S = ln n - W/n); NaN if n == 0
+// class term of a (count, W) rectangle: A = W / n^q, or S = ln n - W / n at
+// q == 1 (Shannon, R6); NaN if n == 0 (the LUTs hold NaN at 0)
 template <int MODE>
 __device__ __forceinline__ double term2d(uint32_t n, double W, const Tsa2dArgs &a) {
-  if (MODE == SUM) return __dsub_rn(__ldg(a.lnn + n), __dmul_rn(W, __ldg(a.rcp + n)));
+  if (MODE == SUM) return __dsub_rn(__ldg(a.lnn + n), __ddiv_rn(W, (double)n));
   return __dmul_rn(W, __ldg(a.ipow + n));
 }
+
+// the same term from an already gathered LUT value g (ipow[n] or lnn[n])
+template <int MODE>
+__device__ __forceinline__ double term2d_g(uint32_t n, double W, double g) {
+  if (MODE == SUM) return __dsub_rn(g, __ddiv_rn(W, (double)n));
+  return __dmul_rn(W, g);
+}
+
+// 8-byte global -> shared async copy (zero-fill when !valid), LDGSTS
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int MODE>
 __device__ __forceinline__ double score2d(double t1, double t2) {
@@ -265,10 +283,11 @@ __device__ __forceinline__ double score2d(double t1, double t2) {
 //   colN   LP*4, colW LP*8     band column sums (read by the other CTAs)
 //   rla    R*4, rlh R*4        absolute f-row / Hb row of each non-empty band row
 //   msk    L/32 words          non-empty f-rows (own private histogram, then all)
-//   xch    64                  exchange slots (flags, mask, argmax + payload)
+//   xch    128                 exchange slots (flags, mask, argmax + payload)
+//   bar    64                  mbarriers of the staged image rows
 //   scr    1024                scan scratch
 struct Smem2d {
-  size_t A, Abytes, Hb, gN, gW, colN, colW, rla, rlh, msk, xch, scr, total;
+  size_t A, Abytes, Hb, gN, gW, colN, colW, rla, rlh, msk, xch, bar, scr, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -301,6 +320,8 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   o += 64;
   s.xch = o;
   o += 128;
+  s.bar = o;
+  o += 8 * kStageChunks;
   s.scr = o;
   o += 1024;
   s.total = o;
@@ -342,22 +363,102 @@ __device__ __forceinline__ void hsum16(const Raw16 &r, uint32_t *hs) {
   hsum4(r.w.w, r.w.z >> 24, r.rb, hs[6], hs[7]);
 }
 
-__device__ __forceinline__ void add_code(uint32_t *hp, uint32_t c, uint32_t n) {
-  atomicAdd(hp + (c >> 1), n << ((c & 1u) << 4));
+// Private-histogram cell (f, g): 16-bit counter (g & 1) of word
+//   f * rw + 4 * ((g >> 3) ^ (f & 7)) + ((g >> 1) & 3)         (rw = LP/2 words per row)
+// The XOR swizzle of 16-byte chunks by f spreads the rows of one g column over
+// 8 bank groups (unswizzled, a row pitch of 128 words puts every f of a column
+// in the same bank and the noisy tissue pixels' atomics collide ~11-way).
+// Applied when rw % 32 == 0 (then the swizzled chunk stays inside the row).
+__device__ __forceinline__ uint32_t cell_word(uint32_t f, uint32_t g, uint32_t rw, bool swz) {
+  const uint32_t ch = swz ? ((g >> 3) ^ (f & 7u)) : (g >> 3);
+  return f * rw + (ch << 2) + ((g >> 1) & 3u);
 }
+
+// L = 256 fast encoding of the same layout with a 32-chunk swizzle: pixel with
+// f (as f8 = f << 8) and box sum v (from h2 = umulhi(v << 16, 14564) =
+// floor(v * 7282 / 2^15) = 2 g or 2 g + 1) has byte offset
+//   f * 512 + ((h2 ^ 16 f) & 0x1fc)     (chunk ((g >> 3) ^ f) & 31, word (g >> 1) & 3)
+// and counter half (h2 >> 1) & 1 = g & 1.  ~9 integer instructions per pixel.
+__device__ __forceinline__ void add256(char *hpb, uint32_t f8, uint32_t h2, uint32_t n) {
+  const uint32_t off = f8 * 2u + ((h2 ^ (f8 >> 4)) & 0x1fcu);
+  atomicAdd(reinterpret_cast<uint32_t *>(hpb + off), n << ((h2 & 2u) << 3));
+}
+// cell word of the L = 256 layout (merge side)
+__device__ __forceinline__ uint32_t cell_word256(uint32_t f, uint32_t g) {
+  return f * 128u + 4u * (((g >> 3) ^ f) & 31u) + ((g >> 1) & 3u);
+}
+
+__device__ __forceinline__ void add_code(uint32_t *hp, uint32_t f, uint32_t g, uint32_t rw, bool swz,
+                                         uint32_t n) {
+  // rw == 128 (L = 256): the 32-chunk layout of add256 / cell_word256
+  const uint32_t w = rw == 128u ? cell_word256(f, g) : cell_word(f, g, rw, swz);
+  atomicAdd(hp + w, n << ((g & 1u) << 4));
+}
+
+// ------------------------------------------------ TMA bulk staging (1-D)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Rows [Y0, Y1) of the slice staged in shared memory by kStageChunks bulk
+// copies, chunk c = rows [Y0 + c cr, Y0 + (c+1) cr), each with its mbarrier.
+struct Stage {
+  const uint8_t *buf;  // shared memory holding row Y0 at offset 0
+  uint64_t *bar;       // [kStageChunks]
+  int64_t Y0, Y1, cr;
+};
 
 // Count the (f, g) codes of image rows [ya, yb) into the packed u16 histogram.
 // VEC: items of 16 pixels (nx % 16 == 0, 16-byte aligned slices); each item
-// walks a stripe of rows with a register ring prefetching kPF rows ahead, so
-// a warp keeps kPF row loads in flight instead of one.
+// walks a stripe of rows.  STAGED: rows come from the shared-memory stage
+// (the stripe first waits for the chunks it needs); otherwise from global
+// memory through a register ring prefetching kPF rows ahead.
 constexpr int kPF = 4;
 
-template <bool VEC, bool CHECK>
-__device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f, int64_t ya,
-                                            int64_t yb, uint32_t *hp, int &ovf) {
+template <bool STAGED>
+__device__ __forceinline__ Raw16 row16(const uint8_t *f, const Stage &sg, int64_t y, int64_t nx,
+                                       int64_t gx, int64_t G16) {
+  if (STAGED) {
+    const uint8_t *row = sg.buf + (y - sg.Y0) * nx;
+    Raw16 r;
+    r.w = *reinterpret_cast<const uint4 *>(row + 16 * gx);
+    r.lb = gx > 0 ? (uint32_t)row[16 * gx - 1] : (r.w.x & 0xffu);
+    r.rb = gx < G16 - 1 ? (uint32_t)row[16 * gx + 16] : (r.w.w >> 24);
+    return r;
+  }
+  return load16(f + y * nx, gx, G16);
+}
+
+template <bool VEC, bool CHECK, bool STAGED, int LT>
+__device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f, const Stage &sg,
+                                            int64_t ya, int64_t yb, uint32_t *hp, int &ovf) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t nx = a.nx, ny = a.ny;
-  const int LP = a.LP, L = a.L;
+  const int LP = LT ? LT : a.LP, L = LT ? LT : a.L;
+  const uint32_t rw = (uint32_t)LP / 2;
+  const bool swz = (rw & 31u) == 0;
   if (yb <= ya) return;
   if (VEC) {
     const int64_t G16 = nx / 16;
@@ -367,24 +468,28 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
       const int64_t gx = item % G16, st = item / G16;
       const int64_t ys = ya + st * per, ye = min(yb, ys + per);
       if (ys >= ye) continue;
+      if (STAGED) {
+        const int64_t r0 = max(ys - 1, (int64_t)0), r1 = min(ye, ny - 1);
+        for (int64_t c = (r0 - sg.Y0) / sg.cr; c <= (r1 - sg.Y0) / sg.cr; c++) mbar_wait(sg.bar + c, 0);
+      }
       uint32_t hp_[8], hc[8], hn[8];
       {
-        const Raw16 r0 = load16(f + max(ys - 1, (int64_t)0) * nx, gx, G16);
+        const Raw16 r0 = row16<STAGED>(f, sg, max(ys - 1, (int64_t)0), nx, gx, G16);
         hsum16(r0, hp_);
       }
-      Raw16 cur = load16(f + ys * nx, gx, G16);
+      Raw16 cur = row16<STAGED>(f, sg, ys, nx, gx, G16);
       hsum16(cur, hc);
       Raw16 ring[kPF];
 #pragma unroll
       for (int d = 0; d < kPF; d++)
-        if (ys + 1 + d <= ye) ring[d] = load16(f + min(ys + 1 + d, ny - 1) * nx, gx, G16);
+        if (ys + 1 + d <= ye) ring[d] = row16<STAGED>(f, sg, min(ys + 1 + d, ny - 1), nx, gx, G16);
       for (int64_t y = ys; y < ye; y += kPF) {
 #pragma unroll
         for (int d = 0; d < kPF; d++) {
           if (y + d < ye) {
             const Raw16 nxt = ring[d];
             const int64_t yl = y + d + 1 + kPF;  // row kept in this slot next
-            if (yl <= ye) ring[d] = load16(f + min(yl, ny - 1) * nx, gx, G16);
+            if (yl <= ye) ring[d] = row16<STAGED>(f, sg, min(yl, ny - 1), nx, gx, G16);
             hsum16(nxt, hn);
             uint32_t box[8];
 #pragma unroll
@@ -397,20 +502,29 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
               const uint32_t b0 = box[0] & 0xffffu;
 #pragma unroll
               for (int e = 0; e < 8; e++) uni = uni && box[e] == (b0 | (b0 << 16));
-              const uint32_t c0 = f0 * LP + div9(b0);
+              const uint32_t g0 = div9(b0);
+              const uint32_t c0 = f0 * LP + g0;
               const unsigned m = __activemask();
               const int leader = __ffs(m) - 1;
               const uint32_t cl = __shfl_sync(m, c0, leader);
               if (__all_sync(m, uni && c0 == cl)) {
-                if (lane == leader) add_code(hp, c0, 16u * __popc(m));
+                if (lane == leader) add_code(hp, f0, g0, rw, swz, 16u * __popc(m));
               } else if (uni) {
-                add_code(hp, c0, 16u);
+                add_code(hp, f0, g0, rw, swz, 16u);
+              } else if (LT == 256) {
+                char *hpb = reinterpret_cast<char *>(hp);
+#pragma unroll
+                for (int e = 0; e < 16; e++) {
+                  const uint32_t f8 = __byte_perm(fw[e >> 2], 0u, 0x4404u | ((e & 3) << 4));
+                  const uint32_t vs = (e & 1) ? (box[e >> 1] & 0xffff0000u) : (box[e >> 1] << 16);
+                  add256(hpb, f8, __umulhi(vs, 14564u), 1u);
+                }
               } else {
 #pragma unroll
                 for (int e = 0; e < 16; e++) {
                   const uint32_t fv = (fw[e >> 2] >> (8 * (e & 3))) & 0xffu;
                   const uint32_t bv = (box[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-                  add_code(hp, fv * LP + div9(bv), 1u);
+                  add_code(hp, fv, div9(bv), rw, swz, 1u);
                 }
               }
             } else {
@@ -422,7 +536,7 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
                   ovf = 1;
                   continue;
                 }
-                add_code(hp, fv * LP + gv, 1u);
+                add_code(hp, fv, gv, rw, swz, 1u);
               }
             }
 #pragma unroll
@@ -451,7 +565,7 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
         ovf = 1;
         continue;
       }
-      add_code(hp, fv * LP + gv, 1u);
+      add_code(hp, fv, gv, rw, swz, 1u);
     }
     (void)lane;
   }
@@ -481,14 +595,17 @@ __device__ __forceinline__ void warp_argmax4(double &s, uint64_t &k, double &t1,
   }
 }
 
-template <int MODE, bool VEC, bool CHECK>
+// LT = 256: the paper's 8-bit case with every table dimension a compile-time
+// constant (L = LP = 256, PP = 288, 8 columns per lane); LT = 0: any L.
+template <int MODE, bool VEC, bool CHECK, int LT>
 __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   extern __shared__ __align__(16) char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = a.CL, r = (int)cluster.block_rank();
   const int64_t z = blockIdx.x / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int L = a.L, LP = a.LP, R = a.R, PP = pitch2d(LP);
+  const int L = LT ? LT : a.L, LP = LT ? LT : a.LP, R = a.R;
+  const int PP = LT ? LT + LT / 8 : pitch2d(LP);
   const int NW = (L + 31) / 32;  // mask words
   const Smem2d lay = smem2d_layout(L, LP, R);
   uint32_t *hp = reinterpret_cast<uint32_t *>(smem + lay.A);  // packed u16 private histogram
@@ -517,20 +634,57 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   const int64_t ya0 = (int64_t)r * a.ny / CL, yb0 = (int64_t)(r + 1) * a.ny / CL;
   const int hw = L * LP / 2;  // words of the private histogram
   const int rw = LP / 2;      // words per private-histogram row
+  const bool swz = (rw & 31) == 0;  // cell_word's chunk swizzle
+  // single round, 16-pixel path: stage the CTA's image rows (plus the halo
+  // rows) in the shared memory the band tables use later (Hb .. colN)
+  Stage sg;
+  sg.Y0 = max(ya0 - 1, (int64_t)0);
+  sg.Y1 = min(yb0 + 1, a.ny);
+  sg.cr = max((int64_t)1, (sg.Y1 - sg.Y0 + kStageChunks - 1) / kStageChunks);
+  sg.buf = reinterpret_cast<const uint8_t *>(smem + lay.Hb);
+  sg.bar = reinterpret_cast<uint64_t *>(smem + lay.bar);
+  const bool staged = VEC && single && yb0 > ya0 &&
+                      (size_t)(sg.Y1 - sg.Y0) * (size_t)a.nx <= lay.colN - lay.Hb;
+  if (staged && tid == 0) {
+    for (int c = 0; c < kStageChunks; c++) mbar_init(sg.bar + c, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int c = 0; c < kStageChunks; c++) {
+      const int64_t r0 = sg.Y0 + c * sg.cr, r1 = min(sg.Y1, r0 + sg.cr);
+      const uint32_t bytes = r1 > r0 ? (uint32_t)((r1 - r0) * a.nx) : 0u;
+      mbar_expect_tx(sg.bar + c, bytes);
+      if (bytes)
+        bulk_g2s(smem + lay.Hb + (r0 - sg.Y0) * a.nx, f + r0 * a.nx, bytes, sg.bar + c);
+    }
+  }
   for (int rd = 0; rd < a.rounds; rd++) {
     uint4 *hp4 = reinterpret_cast<uint4 *>(hp);
     for (int i = tid; i < (hw + 3) / 4; i += k2dThreads) hp4[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid < 8) msk[tid] = 0u;
     __syncthreads();
     const int64_t ya = min(yb0, ya0 + (int64_t)rd * a.rr), yb = min(yb0, ya + a.rr);
-    count_round<VEC, CHECK>(a, f, ya, yb, hp, ovf);
+    if (staged) count_round<VEC, CHECK, true, LT>(a, f, sg, ya, yb, hp, ovf);
+    else count_round<VEC, CHECK, false, LT>(a, f, sg, ya, yb, hp, ovf);
     cluster.sync();  // every private histogram of this round complete
     if (single) {
       // own non-empty rows -> mask -> cluster union
-      for (int i = warp; i < L; i += k2dThreads / 32) {
-        uint32_t any = 0;
-        for (int w = lane; w < rw; w += 32) any |= hp[i * rw + w];
-        if (__any_sync(0xffffffffu, any != 0) && lane == 0) atomicOr(&msk[i >> 5], 1u << (i & 31));
+      if ((rw & 3) == 0) {
+        const uint4 *h4 = reinterpret_cast<const uint4 *>(hp);
+        const int r4 = rw / 4;
+#pragma unroll 4
+        for (int i = warp; i < L; i += k2dThreads / 32) {
+          uint32_t any = 0;
+          for (int w = lane; w < r4; w += 32) {
+            const uint4 v = h4[i * r4 + w];
+            any |= v.x | v.y | v.z | v.w;
+          }
+          if (__any_sync(0xffffffffu, any != 0) && lane == 0) atomicOr(&msk[i >> 5], 1u << (i & 31));
+        }
+      } else {
+        for (int i = warp; i < L; i += k2dThreads / 32) {
+          uint32_t any = 0;
+          for (int w = lane; w < rw; w += 32) any |= hp[i * rw + w];
+          if (__any_sync(0xffffffffu, any != 0) && lane == 0) atomicOr(&msk[i >> 5], 1u << (i & 31));
+        }
       }
       __syncthreads();
       if (tid < 8) xch->mask[tid] = msk[tid];
@@ -563,11 +717,13 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
         const int kk = it / cpr, j = (it - kk * cpr) * 8, i = rla[kk];
         uint32_t o[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if ((LP & 7) == 0) {
+          // physical word of the chunk (swizzle of cell_word)
+          const int pch = rw == 128 ? 4 * (((j >> 3) ^ i) & 31) : 4 * (swz ? ((j >> 3) ^ (i & 7)) : (j >> 3));
           uint4 v[k2dMaxCL];
 #pragma unroll
           for (int c = 0; c < k2dMaxCL; c++)
             if (c < CL)
-              v[c] = *reinterpret_cast<const uint4 *>(cluster.map_shared_rank(hp, c) + i * rw + j / 2);
+              v[c] = *reinterpret_cast<const uint4 *>(cluster.map_shared_rank(hp, c) + i * rw + pch);
 #pragma unroll
           for (int c = 0; c < k2dMaxCL; c++)
             if (c < CL) {
@@ -582,9 +738,9 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
             }
         } else {
           for (int c = 0; c < CL; c++) {
-            const uint32_t *src = cluster.map_shared_rank(hp, c) + i * rw;
+            const uint32_t *src = cluster.map_shared_rank(hp, c);
             for (int e = 0; e < 8 && j + e < LP; e += 2) {
-              const uint32_t v = src[(j + e) / 2];
+              const uint32_t v = src[rw == 128 ? cell_word256(i, j + e) : cell_word(i, j + e, rw, swz)];
               o[e] += v & 0xffffu;
               o[e + 1] += v >> 16;
             }
@@ -596,13 +752,12 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
           if (j + e < LP) dst[pj(j + e)] = o[e];
       }
     } else {
-      const int bw0 = row0 * rw;
       for (int c = 0; c < CL; c++) {
-        const uint32_t *src = cluster.map_shared_rank(hp, c) + bw0;
+        const uint32_t *src = cluster.map_shared_rank(hp, c);
         for (int i = tid; i < nrows_static * rw; i += k2dThreads) {
-          const uint32_t v = src[i];
+          const int ri = i / rw, j = 2 * (i - ri * rw);
+          const uint32_t v = src[rw == 128 ? cell_word256(row0 + ri, j) : cell_word(row0 + ri, j, rw, swz)];
           if (v) {
-            const int ri = i / rw, j = 2 * (i - ri * rw);
             Hb[ri * PP + pj(j)] += v & 0xffffu;
             Hb[ri * PP + pj(j + 1)] += v >> 16;
           }
@@ -727,7 +882,8 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   uint64_t bkey = kKeyNone;
   if (!a.hist_only && !any_ovf && nrl > 0) {
     const int CPL = (L + 31) / 32;
-    const int j0 = min(L, lane * CPL), jn = max(0, min(L, j0 + CPL) - j0);
+    const int j0 = LT ? lane * (LT / 32) : min(L, lane * CPL);
+    const int jn = LT ? LT / 32 : max(0, min(L, j0 + CPL) - j0);
     // walk buffers: the tail of region A behind A1[nrl][LP] if it holds at
     // least k2dGroup rows, else the fixed k2dGroup-row buffers
     const size_t a1b = al16((size_t)nrl * LP * 8);
@@ -750,6 +906,18 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     double accW = lowW;
     for (int g0 = 0; g0 < nrl; g0 += G) {
       const int ge = min(G, nrl - g0);
+      // w(h) of every cell of the warp's rows gathered into gW by async copies
+      // (one L2 round trip for all of them), then the scans read them back
+      for (int w = warp; w < ge; w += k2dThreads / 32) {
+        const int i = rlh[g0 + w];
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+          if (e < jn) {
+            const uint32_t h = Hb[i * PP + pj(j0 + e)];
+            cp_async8(gW + w * PP + pj(j0 + e), a.wlut + h, h != 0u);
+          }
+      }
+      cp_async_wait_all();
       for (int w = warp; w < ge; w += k2dThreads / 32) {
         const int i = rlh[g0 + w];
         uint32_t hv[8];
@@ -757,7 +925,7 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
 #pragma unroll
         for (int e = 0; e < 8; e++) hv[e] = e < jn ? Hb[i * PP + pj(j0 + e)] : 0u;
 #pragma unroll
-        for (int e = 0; e < 8; e++) wv[e] = hv[e] ? __ldg(a.wlut + hv[e]) : 0.0;
+        for (int e = 0; e < 8; e++) wv[e] = e < jn ? gW[w * PP + pj(j0 + e)] : 0.0;
         uint32_t ln = 0;
         double lw = 0.0;
 #pragma unroll
@@ -791,23 +959,23 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
       }
       __syncthreads();
       if (s < L) {
-        for (int w0 = 0; w0 < ge; w0 += 8) {
-          uint32_t nn[8];
-          double wwv[8];
-#pragma unroll
-          for (int w = 0; w < 8; w++) {
-            if (w0 + w < ge) {
-              accN += gN[(w0 + w) * PP + pj(s)];
-              accW = __dadd_rn(accW, gW[(w0 + w) * PP + pj(s)]);
-            }
-            nn[w] = accN;
-            wwv[w] = accW;
-          }
-          // the LUT gathers of 8 rows are independent and issued back to back
-#pragma unroll
-          for (int w = 0; w < 8; w++)
-            if (w0 + w < ge)
-              A1[(g0 + w0 + w) * LP + s] = colnz ? term2d<MODE>(nn[w], wwv[w], a) : CUDART_NAN;
+        // running (n_1, W_1) of every row of the group back into this column's
+        // gN / gW slots, the 1/n^q (ln n) gathers straight into A1 by async
+        // copies (one L2 round trip per group), then A_1 = W_1 / n_1^q in place
+        const double *lut = MODE == SUM ? a.lnn : a.ipow;
+        for (int w = 0; w < ge; w++) {
+          const int c = w * PP + pj(s);
+          accN += gN[c];
+          accW = __dadd_rn(accW, gW[c]);
+          gN[c] = accN;
+          gW[c] = accW;
+          cp_async8(A1 + (g0 + w) * LP + s, lut + accN, colnz);
+        }
+        cp_async_wait_all();
+        for (int w = 0; w < ge; w++) {
+          const int c = w * PP + pj(s);
+          double *d = A1 + (g0 + w) * LP + s;
+          *d = colnz ? term2d_g<MODE>(gN[c], gW[c], *d) : CUDART_NAN;
         }
       }
       __syncthreads();
@@ -819,12 +987,22 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
       const int ge = min(G, g1);  // rows g1-1 down to g1-ge
       for (int w = warp; w < ge; w += k2dThreads / 32) {
         const int i = rlh[g1 - 1 - w];
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+          if (e < jn) {
+            const uint32_t h = Hb[i * PP + pj(j0 + e)];
+            cp_async8(gW + w * PP + pj(j0 + e), a.wlut + h, h != 0u);
+          }
+      }
+      cp_async_wait_all();
+      for (int w = warp; w < ge; w += k2dThreads / 32) {
+        const int i = rlh[g1 - 1 - w];
         uint32_t hv[8];
         double wv[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) hv[e] = e < jn ? Hb[i * PP + pj(j0 + e)] : 0u;
 #pragma unroll
-        for (int e = 0; e < 8; e++) wv[e] = hv[e] ? __ldg(a.wlut + hv[e]) : 0.0;
+        for (int e = 0; e < 8; e++) wv[e] = e < jn ? gW[w * PP + pj(j0 + e)] : 0.0;
         uint32_t ln = 0;
         double lw = 0.0;
 #pragma unroll

@@ -801,7 +801,7 @@ static size_t carve2d(const tsa2d_problem *p, char *base, double **wlut, double 
   if (p->q == 1.0) {
     *ipow = nullptr;
     *lnn = c.take<double>(n1);
-    *rcp = c.take<double>(n1);
+    *rcp = nullptr;  // S = ln n - W / n: no reciprocal table
   } else {
     *ipow = c.take<double>(n1);
     *lnn = *rcp = nullptr;
@@ -813,8 +813,10 @@ static size_t carve2d(const tsa2d_problem *p, char *base, double **wlut, double 
 
 template <int MODE>
 static tsa_status launch2d_mode(const tsa::Tsa2dArgs &a, const Plan2d &pl, cudaStream_t s, bool check) {
-  auto f = a.vec ? (check ? tsa::k_tsallis2d<MODE, true, true> : tsa::k_tsallis2d<MODE, true, false>)
-                 : (check ? tsa::k_tsallis2d<MODE, false, true> : tsa::k_tsallis2d<MODE, false, false>);
+  // 256 levels (u8, no overflow possible): the compile-time-L kernel
+  auto f = a.L == 256 ? (a.vec ? tsa::k_tsallis2d<MODE, true, false, 256> : tsa::k_tsallis2d<MODE, false, false, 256>)
+           : a.vec ? (check ? tsa::k_tsallis2d<MODE, true, true, 0> : tsa::k_tsallis2d<MODE, true, false, 0>)
+                   : (check ? tsa::k_tsallis2d<MODE, false, true, 0> : tsa::k_tsallis2d<MODE, false, false, 0>);
   TSA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

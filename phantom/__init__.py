@@ -84,6 +84,11 @@ CONFIGS = {
                  note="512x512x300 phantom, 256 bins, k=4, tuple-sharded"),
     "c5": Config("c5", 1024, 1024, 1000, "u16", 4096, 2, (0.8,), SEED_BASE + 5,
                  note="1024x1024x1000 12-bit phantom, 4096 bins, k=2"),
+    # the paper's 2-D formulation on the c2 volume (same
+    # seed and bytes); k = 1 stands for the single (t, s) pair
+    "f1": Config("f1", 512, 512, 300, "u8", 256, 1, (0.8,), SEED_BASE + 2,
+                 note="2-D Tsallis (PAPER.md:564-597) on the 512x512x300 c2 phantom, 256 levels, "
+                      "(t,s) search, q=0.8"),
 }
 
 

@@ -76,6 +76,8 @@ def _load():
         lib.oracle_hist2d.argtypes = [P, I64, I64, I, P]
         lib.oracle_phi2d_at.restype = D
         lib.oracle_phi2d_at.argtypes = [P, I, D, I, I, ctypes.POINTER(I)]
+        lib.oracle_preprocess.restype = None
+        lib.oracle_preprocess.argtypes = [P, I64, I, P, P, P]
         lib.oracle_search2d_n.restype = I
         lib.oracle_search2d_n.argtypes = [P, I, D, I, P, P, P, P]
         _lib = lib
@@ -233,3 +235,16 @@ def segment2d(vol, bins, q, z_list=None, threads=None, labels=True):
         status[z] = st
     return {"hist": hist, "thresholds": thr, "phi": phi, "gap": gap, "status": status,
             "labels": lab}
+
+
+# -------------------------------------------------------- pre-processing (f2)
+def preprocess(vol_i16, background=-2000):
+    """HU int16 volume -> (u8 volume, lo, hi): PAPER.md:514-516 with the
+    volume-wide window of DESIGN.md R23-R25."""
+    v = np.ascontiguousarray(vol_i16, dtype=np.int16)
+    out = np.empty(v.shape, np.uint8)
+    lo = np.zeros(1, np.int32)
+    hi = np.zeros(1, np.int32)
+    _load().oracle_preprocess(v.ctypes.data, v.size, int(background), out.ctypes.data,
+                              lo.ctypes.data, hi.ctypes.data)
+    return out, int(lo[0]), int(hi[0])

@@ -580,3 +580,47 @@ int oracle_search2d(const uint32_t *h, int L, double q, int32_t *t_out, int32_t 
                     double *phi_out, double *gap_out) {
   return oracle_search2d_n(h, L, q, 1, t_out, s_out, phi_out, gap_out);
 }
+
+/* ======================================================================
+ * Pre-processing: "change the
+ * value of -2000 (outside of the X-ray detectors) to 0 ... then all intensity
+ * levels are linearly transformed to the range 0 to 255".  Readings
+ * (R23-R25, after SPEC.md:73-81,:90-94):
+ *   1. every voxel equal to `background` is replaced by the volume-wide
+ *      minimum of the remaining voxels (so it maps to 0, the background level);
+ *   2. lo / hi = volume-wide min / max after step 1;
+ *   3. v -> round-half-away-from-zero(255 (v - lo) / (hi - lo)); hi == lo -> 0
+ *      (also when every voxel is background).
+ * Written in that order with exact integer arithmetic: for v >= lo the
+ * rounded quotient is floor((2*255*(v-lo) + (hi-lo)) / (2*(hi-lo))).
+ * ====================================================================== */
+void oracle_preprocess(const int16_t *vol, int64_t n, int background, uint8_t *out,
+                       int32_t *lo_out, int32_t *hi_out) {
+  /* step 1: minimum of the non-background voxels */
+  int have = 0, mn = 0;
+  for (int64_t i = 0; i < n; i++) {
+    if (vol[i] == background) continue;
+    if (!have || vol[i] < mn) mn = vol[i];
+    have = 1;
+  }
+  /* step 2: lo / hi over the volume after the replacement */
+  int lo = 0, hi = 0;
+  for (int64_t i = 0; i < n; i++) {
+    int v = vol[i] == background && have ? mn : vol[i];
+    if (i == 0 || v < lo) lo = v;
+    if (i == 0 || v > hi) hi = v;
+  }
+  /* step 3: the linear map */
+  for (int64_t i = 0; i < n; i++) {
+    int v = vol[i] == background && have ? mn : vol[i];
+    if (hi == lo) {
+      out[i] = 0;
+      continue;
+    }
+    int64_t num = 2 * 255 * (int64_t)(v - lo) + (hi - lo);
+    int64_t den = 2 * (int64_t)(hi - lo);
+    out[i] = (uint8_t)(num / den);
+  }
+  if (lo_out) *lo_out = lo;
+  if (hi_out) *hi_out = hi;
+}

@@ -53,7 +53,7 @@ class Config:
     nx: int
     ny: int
     nz: int
-    dtype: str  # "u8" | "u16"
+    dtype: str  # "u8" | "u16" | "i16" (raw HU)
     bins: int
     k: int
     qs: tuple
@@ -64,7 +64,7 @@ class Config:
 
     @property
     def np_dtype(self):
-        return np.uint8 if self.dtype == "u8" else np.uint16
+        return {"u8": np.uint8, "u16": np.uint16, "i16": np.int16}[self.dtype]
 
     @property
     def depth(self):
@@ -86,6 +86,11 @@ CONFIGS = {
                  note="1024x1024x1000 12-bit phantom, 4096 bins, k=2"),
     # the paper's 2-D formulation on the c2 volume (same
     # seed and bytes); k = 1 stands for the single (t, s) pair
+    # raw int16 HU of the c2 phantom (background -2000),
+    # pre-processed to 8 bits inside the histogram / label passes
+    "f2": Config("f2", 512, 512, 300, "i16", 256, 2, (0.8,), SEED_BASE + 2,
+                 note="HU int16 512x512x300 phantom (c2 geometry), pre-processing fused: "
+                      "background -2000 -> 0, volume-wide linear rescale to 0..255, 256 bins, k=2"),
     "f1": Config("f1", 512, 512, 300, "u8", 256, 1, (0.8,), SEED_BASE + 2,
                  note="2-D Tsallis (PAPER.md:564-597) on the 512x512x300 c2 phantom, 256 levels, "
                       "(t,s) search, q=0.8"),
@@ -94,12 +99,12 @@ CONFIGS = {
 
 def generate(nx, ny, nz, dtype="u8", seed=SEED_BASE, z_first=0, z_total=0, threads=None, out=None):
     lib = _load()
-    npdt = np.uint8 if dtype == "u8" else np.uint16
+    npdt = {"u8": np.uint8, "u16": np.uint16, "i16": np.int16}[dtype]
     if out is None:
         out = np.empty((nz, ny, nx), dtype=npdt)
     assert out.flags.c_contiguous and out.dtype == npdt and out.shape == (nz, ny, nx)
     threads = threads or os.cpu_count() or 1
-    rc = lib.phantom_generate(out.ctypes.data, 1 if dtype == "u8" else 2, nx, ny, nz,
+    rc = lib.phantom_generate(out.ctypes.data, {"u8": 1, "u16": 2, "i16": 3}[dtype], nx, ny, nz,
                               z_first, z_total or nz, seed, threads)
     if rc != 0:
         raise ValueError("phantom_generate failed")

@@ -20,6 +20,7 @@
  *     centred and scaled by 173/1024 (sigma ~ 25 HU); none outside the FOV.
  *   output: u8  = clamp((HU + 1024) >> 3, 0, 255)      (8-bit window, R12)
  *           u16 = clamp(HU + 1024, 0, 4095)            (12-bit, R13)
+ *           i16 = HU itself (dtype code 3; background -2000 exactly)
  * Geometry uses fp64 on the host; the same bytes feed GPU and oracle.
  */
 #include <math.h>
@@ -194,7 +195,9 @@ int phantom_generate(void *out, int dtype_bytes, int64_t nx, int64_t ny, int64_t
           v += noise;
         }
         int64_t o = (zi * ny + y) * nx + x;
-        if (dtype_bytes == 1) {
+        if (dtype_bytes == 3) { /* raw int16 HU (pre-processing input) */
+          ((int16_t *)out)[o] = (int16_t)v;
+        } else if (dtype_bytes == 1) {
           int w = (v + 1024) >> 3;
           if (w < 0) w = 0;
           if (w > 255) w = 255;

@@ -397,6 +397,119 @@ def run_2d(args, cfg, rank, world, dev):
         dist.destroy_process_group()
 
 
+def run_hu(args, cfg, rank, world, dev):
+    """The HU workload: a step = tsa_hu_segment of the
+    resident int16 volume (HU histograms + window, 8-bit remap, search,
+    finalize, labels from HU)."""
+    import numpy as np
+    import torch
+
+    import phantom
+    import paper_2012_10684_b200 as tsa
+
+    q, k = cfg.qs[0], cfg.k
+    host = phantom.make_volume(cfg)
+    n_vox = host.size
+    nbuf = args.buffers or max(2, int(np.ceil(2 * 126e6 / (3 * n_vox))) + 1)
+    vols = [torch.from_numpy(host).to(dev) for _ in range(nbuf)]
+    p = tsa.make_hu_problem(vols[0], k, q)
+    ws = tsa.tsa_hu_workspace(p, dev)
+    outs = [{"thresholds": torch.empty((cfg.nz, k), dtype=torch.int32, device=dev),
+             "objective": torch.empty(cfg.nz, dtype=torch.float64, device=dev),
+             "histogram": torch.empty((cfg.nz, 256), dtype=torch.int32, device=dev),
+             "status": torch.empty(cfg.nz, dtype=torch.int32, device=dev),
+             "labels": torch.empty(host.shape, dtype=torch.uint8, device=dev),
+             "window": torch.empty(2, dtype=torch.int32, device=dev)} for _ in range(nbuf)]
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        tsa.tsa_hu_segment(vols[i % nbuf], k, q, out=outs[i % nbuf], workspace=ws, stream=stream)
+
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    barrier(world)
+    ms_per_step = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    value = world * cfg.nz / (ms_per_step * 1e-3)
+    pk_, how = peaks()
+    hbm = float(pk_.get("hbm_gbs", HBM_FALLBACK_GBS))
+    # algorithmic bytes of the step: the HU volume twice (histogram/window pass,
+    # label pass) + the labels once
+    step_bytes = 2 * 2 * n_vox + n_vox
+    roofline = {"bound": "hbm", "kernel": "HU step (k_hu_hist + k_hu_remap + search + k_label_hu)",
+                "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({how})",
+                "algorithmic_bytes_per_launch": step_bytes}
+    host_t = torch.from_numpy(host).pin_memory()
+    hout = {kk: torch.empty(v.shape, dtype=v.dtype).pin_memory() for kk, v in outs[0].items()}
+    dvol = torch.empty_like(vols[0])
+
+    def e2e_step():
+        dvol.copy_(host_t, non_blocking=True)
+        o = tsa.tsa_hu_segment(dvol, k, q, out=outs[0], workspace=ws, stream=stream)
+        for kk in hout:
+            hout[kk].copy_(o[kk], non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e_step()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": world * cfg.nz * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes),
+               "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in hout.values())),
+               "api": "pinned H2D copy + tsa_hu_segment + D2H of every output", "steps": args.e2e_steps}
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        threads = oracle.max_threads()
+        t0 = time.perf_counter()
+        n, reps = cfg.nz, 0
+        while True:
+            gray, _, _ = oracle.preprocess(host[:n])
+            oracle.segment(gray, 256, k, q, threads=threads)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= 10.0 or reps >= 20:
+                break
+        cpu = {"value": reps * n / el, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"{reps} pass(es) over all {n} slices of f2 (oracle.preprocess "
+                         f"single-threaded, then the Level-1 oracle on {threads} threads), {el:.1f} s"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_of(cfg, args, world), input="i16 HU (background -2000)"),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": 9 * args.steps, "pipeline": "hu-fused (staged search)",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def config_of(cfg, args, world):
     return {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
             "slices_per_gpu": cfg.nz, "bins": cfg.bins, "k": cfg.k, "q": cfg.qs[0],
@@ -498,6 +611,9 @@ def main():
         return
     if cfg.name == "f1":
         run_2d(args, cfg, rank, world, dev)
+        return
+    if cfg.name == "f2":
+        run_hu(args, cfg, rank, world, dev)
         return
     q = cfg.qs[0]
     k, bins = cfg.k, cfg.bins

@@ -243,6 +243,39 @@ tsa_status tsa2d_histogram(const tsa2d_problem *p, uint32_t *hist, int32_t *slic
 /* The mean image alone: g [nz][ny][nx] u8. */
 tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream);
 
+/* ---- HU input: pre-processing fused into the histogram and label passes ---
+ * (readings DESIGN.md R23-R25)
+ *   lo, hi = volume-wide min / max of the voxels != background
+ *   g(v)   = 0 for the background; else round-half-away(255 (v-lo)/(hi-lo)),
+ *            0 when hi == lo                                    (the 8-bit image)
+ * then the 1-D path on g with 256 bins: thresholds are 8-bit levels, labels
+ * #{j : g(v) > t_j}.  The volume is read twice (HU histogram + window pass,
+ * label pass); the 8-bit image is never materialised.
+ * Requirements: nx*ny % 16 == 0, volume (and labels) 16-byte aligned.  HU
+ * values outside [-4096, 4095] make their slice TSA_ERR_LEVEL_OVERFLOW (they
+ * still take part in the window). */
+typedef struct {
+  const int16_t *volume; /* [nz][ny][nx] HU, device */
+  int64_t nx, ny, nz;
+  int32_t background;    /* HU of "outside the detector" (the paper: -2000) */
+  int32_t k;             /* thresholds per slice, 1..4 */
+  double q;              /* entropic index, as tsa_problem */
+  int32_t objective;     /* tsa_objective */
+  int32_t enumeration;   /* tsa_enumeration */
+} tsa_hu_problem;
+
+size_t tsa_hu_workspace_size(const tsa_hu_problem *p);
+
+/* The whole path on HU input.  out: as tsa_segment with bins = 256
+ * (thresholds [nz][k] in 8-bit levels, labels, objective, histogram [nz][256]
+ * of g, slice_status).  window: device int32[2] = (lo, hi) or NULL. */
+tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
+/* The pre-processing step alone: gray [nz][ny][nx] u8 = g(v); window as above. */
+tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *window,
+                             void *workspace, size_t workspace_bytes, void *stream);
+
 const char *tsa_status_string(tsa_status s);
 const char *tsa_last_error(void);
 int32_t tsa_version(void);

@@ -37,6 +37,7 @@ EXPORTS = (
     "tsa_status_string", "tsa_last_error", "tsa_version", "tsa_pipeline_kind",
     "tsa2d_validate", "tsa2d_workspace_size", "tsa2d_cluster_size", "tsa2d_segment",
     "tsa2d_histogram", "tsa2d_mean3x3",
+    "tsa_hu_workspace_size", "tsa_hu_segment", "tsa_hu_preprocess",
 )
 
 
@@ -90,6 +91,18 @@ class tsa2d_problem(ctypes.Structure):
     ]
 
 
+class tsa_hu_problem(ctypes.Structure):
+    _fields_ = [
+        ("volume", ctypes.c_void_p),
+        ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+        ("background", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("q", ctypes.c_double),
+        ("objective", ctypes.c_int32),
+        ("enumeration", ctypes.c_int32),
+    ]
+
+
 _lib = None
 
 
@@ -109,6 +122,7 @@ def load() -> ctypes.CDLL:
     PP = ctypes.POINTER(tsa_problem)
     PO = ctypes.POINTER(tsa_outputs)
     P2 = ctypes.POINTER(tsa2d_problem)
+    PH = ctypes.POINTER(tsa_hu_problem)
     sig = {
         "tsa_validate": (I32, [PP]),
         "tsa_workspace_size": (SZ, [PP]),
@@ -132,6 +146,9 @@ def load() -> ctypes.CDLL:
         "tsa2d_segment": (I32, [P2, PO, P, SZ, P]),
         "tsa2d_histogram": (I32, [P2, P, P, P, SZ, P]),
         "tsa2d_mean3x3": (I32, [P2, P, P]),
+        "tsa_hu_workspace_size": (SZ, [PH]),
+        "tsa_hu_segment": (I32, [PH, PO, P, P, SZ, P]),
+        "tsa_hu_preprocess": (I32, [PH, P, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -425,6 +442,69 @@ def tsa2d_mean3x3(vol, stream=None):
     g = torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
     _check(load().tsa2d_mean3x3(ctypes.byref(p), _ptr(g), _stream(stream)), "tsa2d_mean3x3")
     return g
+
+
+# --------------------------------------------------------------- HU input
+def make_hu_problem(vol, k, q, background=-2000, objective="pseudo_additive",
+                    enumeration="canonical"):
+    if vol.dim() != 3 or not vol.is_contiguous() or vol.dtype != torch.int16:
+        raise ValueError("HU path: volume must be a contiguous int16 [nz][ny][nx] tensor")
+    nz, ny, nx = vol.shape
+    return tsa_hu_problem(vol.data_ptr(), nx, ny, nz, int(background), k, float(q),
+                          OBJECTIVES.get(objective, objective),
+                          ENUMERATIONS.get(enumeration, enumeration))
+
+
+def tsa_hu_workspace(problem, device):
+    n = int(load().tsa_hu_workspace_size(ctypes.byref(problem)))
+    if n == 0:
+        raise TsaError(TSA_ERR_INVALID_ARG, "tsa_hu_workspace_size",
+                       "HU problem: dims (nx*ny % 16), alignment, k, q or objective")
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def tsa_hu_segment(vol, k, q, background=-2000, objective="pseudo_additive",
+                   enumeration="canonical", labels=True, out=None, workspace=None, stream=None):
+    """Pre-processing fused into the 1-D path (PAPER.md:514-516 then 558-597).
+    Returns dict of device tensors: thresholds [nz,k] (8-bit levels), objective,
+    histogram [nz,256] of the 8-bit image, status, labels, window [2] = (lo, hi) HU."""
+    _need_cuda(vol)
+    p = make_hu_problem(vol, k, q, background, objective, enumeration)
+    nz = vol.shape[0]
+    dev = vol.device
+    if out is None:
+        out = {
+            "thresholds": torch.empty((nz, k), dtype=torch.int32, device=dev),
+            "objective": torch.empty(nz, dtype=torch.float64, device=dev),
+            "histogram": torch.empty((nz, 256), dtype=torch.int32, device=dev),
+            "status": torch.empty(nz, dtype=torch.int32, device=dev),
+            "labels": torch.empty(vol.shape, dtype=torch.uint8, device=dev) if labels else None,
+            "window": torch.empty(2, dtype=torch.int32, device=dev),
+        }
+    o = tsa_outputs(out["thresholds"].data_ptr(),
+                    out["labels"].data_ptr() if out.get("labels") is not None else None,
+                    out["objective"].data_ptr() if out.get("objective") is not None else None,
+                    out["histogram"].data_ptr() if out.get("histogram") is not None else None,
+                    out["status"].data_ptr() if out.get("status") is not None else None)
+    if workspace is None:
+        workspace = tsa_hu_workspace(p, dev)
+    win = out.get("window")
+    _check(load().tsa_hu_segment(ctypes.byref(p), ctypes.byref(o), _ptr(win), _ptr(workspace),
+                                 workspace.numel(), _stream(stream)), "tsa_hu_segment")
+    return out
+
+
+def tsa_hu_preprocess(vol, background=-2000, workspace=None, stream=None):
+    """The 8-bit image alone: (gray [nz,ny,nx] u8, window [2] = (lo, hi))."""
+    _need_cuda(vol)
+    p = make_hu_problem(vol, 1, 1.0, background)
+    gray = torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
+    win = torch.empty(2, dtype=torch.int32, device=vol.device)
+    if workspace is None:
+        workspace = tsa_hu_workspace(p, vol.device)
+    _check(load().tsa_hu_preprocess(ctypes.byref(p), _ptr(gray), _ptr(win), _ptr(workspace),
+                                    workspace.numel(), _stream(stream)), "tsa_hu_preprocess")
+    return gray, win
 
 
 def unpack_key(key, k):

@@ -1,0 +1,280 @@
+// k_hu.cuh -- SURVEY.md §8(f) NEXT row 2: pre-processing (PAPER.md:514-516,
+// "change the value of -2000 ... to 0. Then all intensity levels are linearly
+// transformed to the range 0 to 255") fused into the histogram and label
+// passes of the 1-D path, on raw int16 HU input (readings DESIGN.md R23-R25):
+//   lo, hi   = volume-wide min / max of the non-background voxels
+//   g(v)     = 0 for the background; else round-half-away(255 (v - lo) / (hi - lo))
+//            = floor((510 (v - lo) + (hi - lo)) / (2 (hi - lo)));  hi == lo -> 0
+//
+// The volume is read twice (histogram pass, label pass) instead of three times
+// plus a write of the 8-bit image:
+//   k_hu_hist   per-slice HU histograms over 8192 bins (HU in [-4096, 4095],
+//               else LEVEL_OVERFLOW) and the volume-wide window (per-CTA min /
+//               max of the non-background voxels, one global atomic each)
+//   k_hu_glut   g over the 8192 HU bins (one exact division each)
+//   k_hu_remap  per slice, the 8-bit histogram c_b = sum_{v : g(v) = b} h_v
+//               (exact: g is a function of v) -> the usual search / finalize
+//   k_label_hu  labels straight from HU: g is non-decreasing, so
+//               g(v) > t  <=>  v >= lo + ceil((2t + 1)(hi - lo) / 510)
+//               (background voxels excluded), compared two voxels per
+//               instruction with signed 16-bit SIMD compares
+//   k_hu_map    the standalone 8-bit image (tsa_hu_preprocess), per-CTA LUT
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "tsa_device.cuh"
+
+namespace tsa {
+
+constexpr int kHuBins = 8192;  // HU histogram bins: v + 4096
+constexpr int kHuOff = 4096;
+
+struct HuArgs {
+  const int16_t *vol;  // [nz][n]
+  int64_t n, nz;
+  int bg;              // background HU
+  uint32_t *hu_hist;   // [nz][8192] (zeroed) or null (window only)
+  int32_t *win;        // [0] lo (atomicMin), [1] hi (atomicMax), [2] any-overflow
+  int32_t *status;     // [nz] (zeroed)
+  int chunks;
+};
+
+// window slots start at (INT_MAX, INT_MIN, 0)
+__global__ void k_hu_init(int32_t *win) {
+  win[0] = INT_MAX;
+  win[1] = INT_MIN;
+  win[2] = 0;
+}
+
+// g(v) for a non-background voxel (exact integer arithmetic)
+__device__ __forceinline__ uint32_t hu_gray(int v, int lo, int hi) {
+  if (hi <= lo) return 0u;
+  const int64_t num = 510 * (int64_t)(v - lo) + (hi - lo);
+  return (uint32_t)(num / (2 * (int64_t)(hi - lo)));
+}
+
+// HU histogram of a (slice, chunk) + window min/max.  Four copies of the
+// 8192 bins as 16-bit counters packed two per word (4 x 16 KB, so several CTAs
+// share an SM; warps w, w+4, ... share copy w % 4; a counter sees < 65536
+// voxels: the host keeps chunks at <= 128 K voxels).  The background (a fifth of a CT slice, all in one bin:
+// 32-way same-address atomics) is counted in a register and added once per
+// thread; min / max of the non-background voxels with 16-bit SIMD min / max.
+__global__ void __launch_bounds__(512) k_hu_hist(HuArgs g) {
+  extern __shared__ uint32_t hsh[];
+  const int z = blockIdx.y, c = blockIdx.x;
+  const bool count = g.hu_hist != nullptr;
+  constexpr int REP = 4, HW = kHuBins / 2;
+  if (count)
+    for (int i = threadIdx.x; i < HW * REP; i += blockDim.x) hsh[i] = 0u;
+  __syncthreads();
+  uint32_t *bins = hsh + ((threadIdx.x >> 5) % REP) * HW;
+  const int16_t *slice = g.vol + (size_t)z * g.n;
+  const int64_t nvec = g.n / 8;  // 16-byte vectors (n % 16 == 0, aligned: checked by the host)
+  const int64_t per = (nvec + g.chunks - 1) / g.chunks;
+  const int64_t v0 = per * c, v1 = min(nvec, v0 + per);
+  const uint4 *v4 = reinterpret_cast<const uint4 *>(slice);
+  const int bg = g.bg;
+  const uint32_t bg2 = ((uint32_t)(uint16_t)bg) * 0x00010001u;
+  uint32_t mn2 = 0x7fff7fffu, mx2 = 0x80008000u;  // per-lane signed min / max
+  uint32_t nbg = 0, nnb = 0;  // background / other voxels seen
+  int ovf = 0;
+  constexpr int U = 4;  // 16-byte loads in flight per thread
+  for (int64_t i0 = v0 + threadIdx.x; i0 < v1; i0 += (int64_t)U * blockDim.x) {
+    uint4 wv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      wv[u] = i < v1 ? __ldcs(v4 + i) : make_uint4(bg2, bg2, bg2, bg2);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const bool real = i0 + (int64_t)u * blockDim.x < v1;
+      const uint32_t ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const uint32_t isbg = __vcmpeq2(ws[e], bg2);  // 0xffff lanes: background
+        mn2 = __vmins2(mn2, (ws[e] & ~isbg) | (0x7fff7fffu & isbg));
+        mx2 = __vmaxs2(mx2, (ws[e] & ~isbg) | (0x80008000u & isbg));
+        if (real) {
+          nbg += __popc(isbg) >> 4;
+          nnb += 2u - (__popc(isbg) >> 4);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          if ((isbg >> (16 * h)) & 1u) continue;
+          const int v = (int)(int16_t)((ws[e] >> (16 * h)) & 0xffffu);
+          const uint32_t b = (uint32_t)(v + kHuOff);
+          if (b < (uint32_t)kHuBins) {
+            if (count) atomicAdd(bins + (b >> 1), 1u << ((b & 1u) << 4));
+          } else {
+            ovf = 1;
+          }
+        }
+      }
+    }
+  }
+  int mn = min((int)(int16_t)(mn2 & 0xffffu), (int)(int16_t)(mn2 >> 16));
+  int mx = max((int)(int16_t)(mx2 & 0xffffu), (int)(int16_t)(mx2 >> 16));
+  // (a lane that only saw background keeps the neutral 32767 / -32768)
+  // window: warp then one atomic per warp
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  }
+  ovf = __any_sync(0xffffffffu, ovf);
+  const bool bg_in = (uint32_t)(bg + kHuOff) < (uint32_t)kHuBins;
+  if (!bg_in && __any_sync(0xffffffffu, nbg != 0)) ovf = 1;  // background outside the bins
+  const bool any_nb = __any_sync(0xffffffffu, nnb != 0);
+  if ((threadIdx.x & 31) == 0) {
+    if (any_nb) {  // (lanes that saw only background hold the neutral 32767 / -32768)
+      atomicMin(g.win, mn);
+      atomicMax(g.win + 1, mx);
+    }
+    if (ovf) {
+      atomicOr(g.win + 2, 1);
+      g.status[z] = kLevelOverflow;
+    }
+  }
+  if (!count) return;
+  if (bg_in) {  // background: one global atomic per warp
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nbg += __shfl_xor_sync(0xffffffffu, nbg, off);
+    if ((threadIdx.x & 31) == 0 && nbg)
+      atomicAdd(g.hu_hist + (size_t)z * kHuBins + (uint32_t)(bg + kHuOff), nbg);
+  }
+  __syncthreads();
+  uint32_t *out = g.hu_hist + (size_t)z * kHuBins;
+  for (int b = threadIdx.x; b < kHuBins; b += blockDim.x) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int r = 0; r < REP; r++) s += (hsh[r * HW + (b >> 1)] >> ((b & 1) << 4)) & 0xffffu;
+    if (s) atomicAdd(out + b, s);
+  }
+}
+
+// g over the HU bins (one exact division per bin, once per call)
+__global__ void k_hu_glut(const int32_t *win, int bg, uint8_t *glut) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= kHuBins) return;
+  const int lo = win[0], hi = win[1], v = b - kHuOff;
+  glut[b] = (uint8_t)((v == bg || lo == INT_MAX) ? 0u : min(hu_gray(v, lo, hi), 255u));
+}
+
+// 8-bit histogram of a slice from its HU histogram: grid (4, nz), each CTA a
+// quarter of the HU bins into shared bins, then added into hist (zeroed).
+__global__ void __launch_bounds__(256) k_hu_remap(const uint32_t *hu_hist, const uint8_t *glut,
+                                                  uint32_t *hist) {
+  __shared__ uint32_t b8[256];
+  const int z = blockIdx.y, q = blockIdx.x;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) b8[i] = 0u;
+  __syncthreads();
+  const uint4 *h4 = reinterpret_cast<const uint4 *>(hu_hist + (size_t)z * kHuBins) + q * (kHuBins / 16);
+  const uint32_t *g4 = reinterpret_cast<const uint32_t *>(glut) + q * (kHuBins / 16);
+  for (int i = threadIdx.x; i < kHuBins / 16; i += blockDim.x) {
+    const uint4 c = __ldcs(h4 + i);
+    if ((c.x | c.y | c.z | c.w) == 0u) continue;
+    const uint32_t gg = g4[i];
+    if (c.x) atomicAdd(b8 + (gg & 0xffu), c.x);
+    if (c.y) atomicAdd(b8 + ((gg >> 8) & 0xffu), c.y);
+    if (c.z) atomicAdd(b8 + ((gg >> 16) & 0xffu), c.z);
+    if (c.w) atomicAdd(b8 + (gg >> 24), c.w);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (b8[i]) atomicAdd(hist + (size_t)z * 256 + i, b8[i]);
+}
+
+// Smallest HU v with g(v) > t (t an 8-bit threshold); INT_MAX if none.
+__device__ __forceinline__ int hu_cut(int t, int lo, int hi) {
+  if (t < 0) return INT_MIN;
+  if (t >= 255 || hi <= lo) return INT_MAX;
+  const int64_t d = (int64_t)(2 * t + 1) * (hi - lo);
+  return lo + (int)((d + 509) / 510);  // ceil((2t+1)(hi-lo)/510)
+}
+
+// labels[z][i] = #{ j : g(v) > t_j } for non-background voxels, 0 for the
+// background and for failed slices.  Grid (chunks, nz): a CTA labels a
+// contiguous part of one slice (its cutoffs computed once), 16 voxels (two
+// 16-byte loads, one 16-byte store) per item, two items in flight per thread.
+template <int KT>
+__global__ void __launch_bounds__(256) k_label_hu(const int16_t *vol, uint8_t *labels, const int32_t *thr,
+                                                  const int32_t *status, const int32_t *win, int bg,
+                                                  int64_t n, int k) {
+  const int z = blockIdx.y;
+  const int64_t per = n / 16;
+  const int64_t cp = (per + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)z * per + cp * blockIdx.x;
+  const int64_t i1 = (int64_t)z * per + min(per, cp * (blockIdx.x + 1));
+  const uint4 *src = reinterpret_cast<const uint4 *>(vol);
+  uint4 *dst = reinterpret_cast<uint4 *>(labels);
+  const int lo = win[0], hi = win[1];
+  const uint32_t bg2 = ((uint32_t)(uint16_t)bg) * 0x00010001u;
+  const bool ok = status == nullptr || status[z] == kOK;
+  const int32_t *tz = thr + (size_t)z * k;
+  // cutoffs clamped to the int16 range (every int16 >= -32768); "never" when
+  // the cutoff is above every int16
+  bool nv[4] = {true, true, true, true};
+  uint32_t cc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < KT; j++) {
+    const int c = hu_cut(tz[j], lo, hi);
+    nv[j] = c > 32767;
+    const int c16 = c > 32767 ? 32767 : (c < -32768 ? -32768 : c);
+    cc[j] = ((uint32_t)(uint16_t)c16) * 0x00010001u;
+  }
+  for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += 2 * (int64_t)blockDim.x) {
+    uint4 wa[2], wb[2];
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int64_t it = ib + (int64_t)u * blockDim.x;
+      if (it < i1) {
+        wa[u] = __ldcs(src + 2 * it);
+        wb[u] = __ldcs(src + 2 * it + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int64_t it = ib + (int64_t)u * blockDim.x;
+      if (it >= i1) break;
+      const uint32_t ws[8] = {wa[u].x, wa[u].y, wa[u].z, wa[u].w, wb[u].x, wb[u].y, wb[u].z, wb[u].w};
+      uint32_t o[4] = {0u, 0u, 0u, 0u};
+      if (ok) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          // per 16-bit lane: 1 where v >= cut (signed), masked by v != bg
+          const uint32_t w = ws[e];
+          uint32_t l = 0u;
+#pragma unroll
+          for (int j = 0; j < KT; j++)
+            if (!nv[j]) l += __vcmpges2(w, cc[j]) & 0x00010001u;
+          l &= __vcmpne2(w, bg2);
+          // two 16-bit lanes -> two bytes of the output word
+          o[e >> 1] |= __byte_perm(l, 0u, 0x4420) << (16 * (e & 1));
+        }
+      }
+      __stcs(dst + it, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+// Standalone 8-bit image (tsa_hu_preprocess): a per-CTA LUT over the HU bins.
+__global__ void __launch_bounds__(256) k_hu_map(const int16_t *vol, uint8_t *gray, const int32_t *win,
+                                                int bg, int64_t total) {
+  __shared__ uint8_t lut[kHuBins];
+  const int lo = win[0], hi = win[1];
+  for (int b = threadIdx.x; b < kHuBins; b += blockDim.x) {
+    const int v = b - kHuOff;
+    lut[b] = (uint8_t)((v == bg || lo == INT_MAX) ? 0u : min(hu_gray(v, lo, hi), 255u));
+  }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = vol[i];
+    const uint32_t b = (uint32_t)(v + kHuOff);
+    gray[i] = b < (uint32_t)kHuBins ? lut[b] : (uint8_t)0;
+  }
+}
+
+}  // namespace tsa

@@ -940,6 +940,126 @@ tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream) {
   return check_cuda("k2d_mean");
 }
 
+// ------------------------------------------------------------- HU input
+static bool valid_hu(const tsa_hu_problem *p) {
+  if (!p || !p->volume || p->nx <= 0 || p->ny <= 0 || p->nz <= 0) return false;
+  const int64_t n = p->nx * p->ny;
+  if (n >= (int64_t(1) << 31) || n % 16 != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(p->volume) & 15) != 0) return false;
+  return valid_search_shape(p->nz, n, 256, p->k, p->q, p->objective, p->enumeration);
+}
+
+struct HuWs {
+  uint32_t *hu_hist, *hist8;
+  uint8_t *glut;
+  int32_t *win, *status;
+  double *ps;
+  uint64_t *pk;
+  char *search;
+  size_t search_bytes;
+  int32_t units;
+};
+
+static size_t carve_hu(const tsa_hu_problem *p, char *base, HuWs *o) {
+  Carve c{base};
+  HuWs w;
+  const int64_t n = p->nx * p->ny;
+  w.units = tsa_default_units(p->nz, 256, p->k, p->enumeration);
+  w.hu_hist = c.take<uint32_t>((size_t)p->nz * tsa::kHuBins);
+  w.hist8 = c.take<uint32_t>((size_t)p->nz * 256);
+  w.glut = c.take<uint8_t>(tsa::kHuBins);
+  w.win = c.take<int32_t>(4);
+  w.status = c.take<int32_t>((size_t)p->nz);
+  w.ps = c.take<double>((size_t)w.units * p->nz);
+  w.pk = c.take<uint64_t>((size_t)w.units * p->nz);
+  w.search_bytes = tsa_search_workspace_size(p->nz, n, 256, p->k, p->q, p->objective, p->enumeration);
+  w.search = c.take<char>(w.search_bytes);
+  if (o) *o = w;
+  return c.off;
+}
+
+size_t tsa_hu_workspace_size(const tsa_hu_problem *p) {
+  if (!valid_hu(p)) return 0;
+  return carve_hu(p, nullptr, nullptr);
+}
+
+static tsa_status hu_window_pass(const tsa_hu_problem *p, const HuWs &w, bool histograms, cudaStream_t s) {
+  const int64_t n = p->nx * p->ny;
+  if (histograms) TSA_CUDA(cudaMemsetAsync(w.hu_hist, 0, sizeof(uint32_t) * p->nz * tsa::kHuBins, s));
+  TSA_CUDA(cudaMemsetAsync(w.status, 0, sizeof(int32_t) * p->nz, s));
+  tsa::k_hu_init<<<1, 1, 0, s>>>(w.win);
+  tsa::HuArgs a;
+  a.vol = p->volume;
+  a.n = n;
+  a.nz = p->nz;
+  a.bg = p->background;
+  a.hu_hist = histograms ? w.hu_hist : nullptr;
+  a.win = w.win;
+  a.status = w.status;
+  // <= 128 K voxels per CTA (a 16-bit counter copy serves 4 of 16 warps:
+  // < 65536 counts; the background goes straight to global memory); 64 KB of
+  // bins: three CTAs per SM
+  a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (n + 131071) / 131072) * 2);
+  const size_t smem = histograms ? (size_t)4 * (tsa::kHuBins / 2) * sizeof(uint32_t) : 0;
+  if (smem > 48 * 1024)
+    TSA_CUDA(cudaFuncSetAttribute(tsa::k_hu_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tsa::k_hu_hist<<<dim3((unsigned)a.chunks, (unsigned)p->nz), 512, smem, s>>>(a);
+  return check_cuda("k_hu_hist");
+}
+
+tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
+                          void *workspace, size_t workspace_bytes, void *stream) {
+  if (!valid_hu(p)) return set_error(TSA_ERR_INVALID_ARG, "HU problem: dims/alignment/k/q/objective");
+  if (!out || !out->thresholds) return set_error(TSA_ERR_INVALID_ARG, "outputs->thresholds NULL");
+  if (out->labels && (reinterpret_cast<uintptr_t>(out->labels) & 15) != 0)
+    return set_error(TSA_ERR_INVALID_ARG, "labels not 16-byte aligned");
+  if (!workspace) return set_error(TSA_ERR_INVALID_ARG, "workspace NULL");
+  HuWs w;
+  const size_t need = carve_hu(p, reinterpret_cast<char *>(workspace), &w);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
+  cudaStream_t s = S(stream);
+  const int64_t n = p->nx * p->ny;
+  TSA_TRY(hu_window_pass(p, w, true, s));
+  uint32_t *hist8 = out->histogram ? out->histogram : w.hist8;
+  TSA_CUDA(cudaMemsetAsync(hist8, 0, sizeof(uint32_t) * p->nz * 256, s));
+  tsa::k_hu_glut<<<tsa::kHuBins / 256, 256, 0, s>>>(w.win, p->background, w.glut);
+  tsa::k_hu_remap<<<dim3(4, (unsigned)p->nz), 256, 0, s>>>(w.hu_hist, w.glut, hist8);
+  TSA_TRY(check_cuda("k_hu_remap"));
+  TSA_TRY(tsa_search(hist8, w.status, p->nz, n, 256, p->k, p->q, p->objective, p->enumeration, w.units, 0,
+                     w.units, w.ps, w.pk, w.search, w.search_bytes, stream));
+  TSA_TRY(finalize_impl(hist8, w.status, p->nz, 256, p->k, p->q, p->objective, w.ps, w.pk, w.units,
+                        out->thresholds, out->objective, w.status, out->slice_status, s));
+  if (out->labels) {
+    const dim3 grid(4, (unsigned)p->nz);  // 4 contiguous chunks per slice
+    switch (p->k) {
+      case 1: tsa::k_label_hu<1><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
+      case 2: tsa::k_label_hu<2><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
+      case 3: tsa::k_label_hu<3><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
+      default: tsa::k_label_hu<4><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
+    }
+    TSA_TRY(check_cuda("k_label_hu"));
+  }
+  if (window) TSA_CUDA(cudaMemcpyAsync(window, w.win, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  return TSA_OK;
+}
+
+tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *window, void *workspace,
+                             size_t workspace_bytes, void *stream) {
+  if (!valid_hu(p)) return set_error(TSA_ERR_INVALID_ARG, "HU problem: dims/alignment/k/q/objective");
+  if (!gray || !workspace) return set_error(TSA_ERR_INVALID_ARG, "gray/workspace NULL");
+  HuWs w;
+  const size_t need = carve_hu(p, reinterpret_cast<char *>(workspace), &w);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
+  cudaStream_t s = S(stream);
+  TSA_TRY(hu_window_pass(p, w, false, s));
+  const int64_t total = p->nx * p->ny * p->nz;
+  const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)g_num_sms() * 8);
+  tsa::k_hu_map<<<blocks, 256, 0, s>>>(p->volume, gray, w.win, p->background, total);
+  TSA_TRY(check_cuda("k_hu_map"));
+  if (window) TSA_CUDA(cudaMemcpyAsync(window, w.win, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  return TSA_OK;
+}
+
 // ----------------------------------------------------------- host buffers
 static size_t slab_bytes(const tsa_problem *p, int64_t slab, tsa_problem *sp) {
   *sp = *p;

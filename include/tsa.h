@@ -257,7 +257,7 @@ tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream);
 typedef struct {
   const int16_t *volume; /* [nz][ny][nx] HU, device */
   int64_t nx, ny, nz;
-  int32_t background;    /* HU of "outside the detector" (the paper: -2000) */
+  int32_t background;    /* HU of "outside the detector" (the paper: -2000); in [-4096, 4095] */
   int32_t k;             /* thresholds per slice, 1..4 */
   double q;              /* entropic index, as tsa_problem */
   int32_t objective;     /* tsa_objective */

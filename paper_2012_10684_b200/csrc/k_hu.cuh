@@ -9,8 +9,8 @@
 // The volume is read twice (histogram pass, label pass) instead of three times
 // plus a write of the 8-bit image:
 //   k_hu_hist   per-slice HU histograms over 8192 bins (HU in [-4096, 4095],
-//               else LEVEL_OVERFLOW) and the volume-wide window (per-CTA min /
-//               max of the non-background voxels, one global atomic each)
+//               else LEVEL_OVERFLOW)
+//   k_hu_window the volume-wide window from the histograms' non-empty bins
 //   k_hu_glut   g over the 8192 HU bins (one exact division each)
 //   k_hu_remap  per slice, the 8-bit histogram c_b = sum_{v : g(v) = b} h_v
 //               (exact: g is a function of v) -> the usual search / finalize
@@ -35,16 +35,18 @@ struct HuArgs {
   int64_t n, nz;
   int bg;              // background HU
   uint32_t *hu_hist;   // [nz][8192] (zeroed) or null (window only)
-  int32_t *win;        // [0] lo (atomicMin), [1] hi (atomicMax), [2] any-overflow
+  int32_t *win;        // [0] lo, [1] hi, [2] / [3] min / max of the out-of-range voxels
   int32_t *status;     // [nz] (zeroed)
   int chunks;
 };
 
-// window slots start at (INT_MAX, INT_MIN, 0)
+// window slots start at (INT_MAX, INT_MIN) for (lo, hi) and for the
+// out-of-range voxels' (min, max)
 __global__ void k_hu_init(int32_t *win) {
   win[0] = INT_MAX;
   win[1] = INT_MIN;
-  win[2] = 0;
+  win[2] = INT_MAX;
+  win[3] = INT_MIN;
 }
 
 // g(v) for a non-background voxel (exact integer arithmetic)
@@ -54,104 +56,138 @@ __device__ __forceinline__ uint32_t hu_gray(int v, int lo, int hi) {
   return (uint32_t)(num / (2 * (int64_t)(hi - lo)));
 }
 
-// HU histogram of a (slice, chunk) + window min/max.  Four copies of the
-// 8192 bins as 16-bit counters packed two per word (4 x 16 KB, so several CTAs
-// share an SM; warps w, w+4, ... share copy w % 4; a counter sees < 65536
-// voxels: the host keeps chunks at <= 128 K voxels).  The background (a fifth of a CT slice, all in one bin:
-// 32-way same-address atomics) is counted in a register and added once per
-// thread; min / max of the non-background voxels with 16-bit SIMD min / max.
+// HU histogram of a (slice, chunk).  Four copies of the 8192 bins as 16-bit
+// counters packed two per word (4 x 16 KB, so several CTAs share an SM; warps
+// w, w+4, ... share copy w % 4; a counter sees < 65536 voxels: the host keeps
+// chunks at <= 128 K voxels).  The background (a fifth of a CT slice, all in
+// one bin: 32-way same-address atomics) is counted in a register and added to
+// global memory once per warp.  The window comes from the histograms
+// (k_hu_window); only voxels outside the bins (LEVEL_OVERFLOW, rare) update it
+// here directly.
 __global__ void __launch_bounds__(512) k_hu_hist(HuArgs g) {
   extern __shared__ uint32_t hsh[];
   const int z = blockIdx.y, c = blockIdx.x;
-  const bool count = g.hu_hist != nullptr;
   constexpr int REP = 4, HW = kHuBins / 2;
-  if (count)
-    for (int i = threadIdx.x; i < HW * REP; i += blockDim.x) hsh[i] = 0u;
+  for (int i = threadIdx.x; i < HW * REP / 4; i += blockDim.x)
+    reinterpret_cast<uint4 *>(hsh)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
-  uint32_t *bins = hsh + ((threadIdx.x >> 5) % REP) * HW;
+  // 32-bit shared address of this warp's copy (computed once: the compiler
+  // otherwise re-derives the generic->shared window per atomic)
+  const uint32_t sbase =
+      (uint32_t)__cvta_generic_to_shared(hsh + ((threadIdx.x >> 5) % REP) * HW);
   const int16_t *slice = g.vol + (size_t)z * g.n;
   const int64_t nvec = g.n / 8;  // 16-byte vectors (n % 16 == 0, aligned: checked by the host)
   const int64_t per = (nvec + g.chunks - 1) / g.chunks;
   const int64_t v0 = per * c, v1 = min(nvec, v0 + per);
   const uint4 *v4 = reinterpret_cast<const uint4 *>(slice);
   const int bg = g.bg;
-  const uint32_t bg2 = ((uint32_t)(uint16_t)bg) * 0x00010001u;
-  uint32_t mn2 = 0x7fff7fffu, mx2 = 0x80008000u;  // per-lane signed min / max
-  uint32_t nbg = 0, nnb = 0;  // background / other voxels seen
-  int ovf = 0;
+  uint32_t nbg = 0;
+  int ovf = 0, omn = INT_MAX, omx = INT_MIN;  // out-of-range voxels (window only)
+  // branch-free: every voxel issues one shared reduction; the background
+  // (always inside the bins, checked by the host) and out-of-range voxels add
+  // 0 to a lane-private word of bins 0..63 (HU -4096..-4033: adding 0 changes
+  // nothing and the 32 lanes hit 32 banks), so no predicate splits the warp
+  const uint32_t lane_addr = sbase + 4u * (threadIdx.x & 31);
+  auto one = [&](int v) {
+    const uint32_t b = (uint32_t)(v + kHuOff);
+    const bool inr = b < (uint32_t)kHuBins, isbg = v == bg;
+    const bool skip = isbg || !inr;
+    nbg += isbg ? 1u : 0u;
+    const uint32_t addr = skip ? lane_addr : sbase + ((b << 1) & 0x3ffcu);
+    const uint32_t inc = skip ? 0u : ((b & 1u) ? 0x10000u : 1u);
+    asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(addr), "r"(inc) : "memory");
+    if (!inr) {  // rare: LEVEL_OVERFLOW voxel
+      ovf = 1;
+      omn = min(omn, v);
+      omx = max(omx, v);
+    }
+  };
   constexpr int U = 4;  // 16-byte loads in flight per thread
   for (int64_t i0 = v0 + threadIdx.x; i0 < v1; i0 += (int64_t)U * blockDim.x) {
     uint4 wv[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t i = i0 + (int64_t)u * blockDim.x;
-      wv[u] = i < v1 ? __ldcs(v4 + i) : make_uint4(bg2, bg2, bg2, bg2);
+      if (i < v1) wv[u] = __ldcs(v4 + i);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const bool real = i0 + (int64_t)u * blockDim.x < v1;
+      if (i0 + (int64_t)u * blockDim.x >= v1) break;
       const uint32_t ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
 #pragma unroll
       for (int e = 0; e < 4; e++) {
-        const uint32_t isbg = __vcmpeq2(ws[e], bg2);  // 0xffff lanes: background
-        mn2 = __vmins2(mn2, (ws[e] & ~isbg) | (0x7fff7fffu & isbg));
-        mx2 = __vmaxs2(mx2, (ws[e] & ~isbg) | (0x80008000u & isbg));
-        if (real) {
-          nbg += __popc(isbg) >> 4;
-          nnb += 2u - (__popc(isbg) >> 4);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          if ((isbg >> (16 * h)) & 1u) continue;
-          const int v = (int)(int16_t)((ws[e] >> (16 * h)) & 0xffffu);
-          const uint32_t b = (uint32_t)(v + kHuOff);
-          if (b < (uint32_t)kHuBins) {
-            if (count) atomicAdd(bins + (b >> 1), 1u << ((b & 1u) << 4));
-          } else {
-            ovf = 1;
-          }
-        }
+        one((int)(int16_t)(ws[e] & 0xffffu));
+        one((int)ws[e] >> 16);
       }
     }
   }
-  int mn = min((int)(int16_t)(mn2 & 0xffffu), (int)(int16_t)(mn2 >> 16));
-  int mx = max((int)(int16_t)(mx2 & 0xffffu), (int)(int16_t)(mx2 >> 16));
-  // (a lane that only saw background keeps the neutral 32767 / -32768)
-  // window: warp then one atomic per warp
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    nbg += __shfl_xor_sync(0xffffffffu, nbg, off);
+    omn = min(omn, __shfl_xor_sync(0xffffffffu, omn, off));
+    omx = max(omx, __shfl_xor_sync(0xffffffffu, omx, off));
+  }
+  ovf = __any_sync(0xffffffffu, ovf);
+  uint32_t *out = g.hu_hist + (size_t)z * kHuBins;
+  if ((threadIdx.x & 31) == 0) {
+    if (nbg) atomicAdd(out + (uint32_t)(bg + kHuOff), nbg);
+    if (ovf) {
+      if (omn != INT_MAX) atomicMin(g.win + 2, omn);
+      if (omx != INT_MIN) atomicMax(g.win + 3, omx);
+      g.status[z] = kLevelOverflow;
+    }
+  }
+  __syncthreads();
+  // flush: 4 words (8 bins) of every copy per 16-byte load
+  for (int q = threadIdx.x; q < HW / 4; q += blockDim.x) {
+    uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int r = 0; r < REP; r++) {
+      const uint4 w = reinterpret_cast<const uint4 *>(hsh + r * HW)[q];
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        lo[e] += ws[e] & 0xffffu;
+        hi[e] += ws[e] >> 16;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int b = 8 * q + 2 * e;
+      if (lo[e]) atomicAdd(out + b, lo[e]);
+      if (hi[e]) atomicAdd(out + b + 1, hi[e]);
+    }
+  }
+}
+
+// The volume-wide window from the HU histograms: (lo, hi) = the lowest / highest
+// non-empty bin other than the background over every slice, merged with the
+// out-of-range voxels' min / max (win[2], win[3]).  Grid over the bins, each
+// thread ORs its bin over the slices.
+__global__ void __launch_bounds__(256) k_hu_window(const uint32_t *hu_hist, int64_t nz, int bg, int32_t *win) {
+  // grid (bins / 256, slice chunks): each thread ORs its bin over its slices
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t zc = (nz + gridDim.y - 1) / gridDim.y;
+  const int64_t z0 = zc * blockIdx.y, z1 = min(nz, z0 + zc);
+  uint32_t any = 0;
+  if (b < kHuBins && b - kHuOff != bg)
+    for (int64_t z = z0; z < z1; z++) any |= __ldcs(hu_hist + (size_t)z * kHuBins + b);
+  int mn = any ? b - kHuOff : INT_MAX, mx = any ? b - kHuOff : INT_MIN;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   }
-  ovf = __any_sync(0xffffffffu, ovf);
-  const bool bg_in = (uint32_t)(bg + kHuOff) < (uint32_t)kHuBins;
-  if (!bg_in && __any_sync(0xffffffffu, nbg != 0)) ovf = 1;  // background outside the bins
-  const bool any_nb = __any_sync(0xffffffffu, nnb != 0);
   if ((threadIdx.x & 31) == 0) {
-    if (any_nb) {  // (lanes that saw only background hold the neutral 32767 / -32768)
-      atomicMin(g.win, mn);
-      atomicMax(g.win + 1, mx);
-    }
-    if (ovf) {
-      atomicOr(g.win + 2, 1);
-      g.status[z] = kLevelOverflow;
-    }
+    if (mn != INT_MAX) atomicMin(win, mn);
+    if (mx != INT_MIN) atomicMax(win + 1, mx);
   }
-  if (!count) return;
-  if (bg_in) {  // background: one global atomic per warp
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) nbg += __shfl_xor_sync(0xffffffffu, nbg, off);
-    if ((threadIdx.x & 31) == 0 && nbg)
-      atomicAdd(g.hu_hist + (size_t)z * kHuBins + (uint32_t)(bg + kHuOff), nbg);
-  }
-  __syncthreads();
-  uint32_t *out = g.hu_hist + (size_t)z * kHuBins;
-  for (int b = threadIdx.x; b < kHuBins; b += blockDim.x) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int r = 0; r < REP; r++) s += (hsh[r * HW + (b >> 1)] >> ((b & 1) << 4)) & 0xffffu;
-    if (s) atomicAdd(out + b, s);
-  }
+}
+
+// fold the out-of-range extremes into (lo, hi) (one thread, after k_hu_window)
+__global__ void k_hu_window_fold(int32_t *win) {
+  if (win[2] != INT_MAX) win[0] = min(win[0], win[2]);
+  if (win[3] != INT_MIN) win[1] = max(win[1], win[3]);
 }
 
 // g over the HU bins (one exact division per bin, once per call)

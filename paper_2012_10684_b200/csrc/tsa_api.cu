@@ -946,6 +946,7 @@ static bool valid_hu(const tsa_hu_problem *p) {
   const int64_t n = p->nx * p->ny;
   if (n >= (int64_t(1) << 31) || n % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(p->volume) & 15) != 0) return false;
+  if (p->background < -tsa::kHuOff || p->background >= tsa::kHuBins - tsa::kHuOff) return false;
   return valid_search_shape(p->nz, n, 256, p->k, p->q, p->objective, p->enumeration);
 }
 
@@ -983,9 +984,9 @@ size_t tsa_hu_workspace_size(const tsa_hu_problem *p) {
   return carve_hu(p, nullptr, nullptr);
 }
 
-static tsa_status hu_window_pass(const tsa_hu_problem *p, const HuWs &w, bool histograms, cudaStream_t s) {
+static tsa_status hu_window_pass(const tsa_hu_problem *p, const HuWs &w, cudaStream_t s) {
   const int64_t n = p->nx * p->ny;
-  if (histograms) TSA_CUDA(cudaMemsetAsync(w.hu_hist, 0, sizeof(uint32_t) * p->nz * tsa::kHuBins, s));
+  TSA_CUDA(cudaMemsetAsync(w.hu_hist, 0, sizeof(uint32_t) * p->nz * tsa::kHuBins, s));
   TSA_CUDA(cudaMemsetAsync(w.status, 0, sizeof(int32_t) * p->nz, s));
   tsa::k_hu_init<<<1, 1, 0, s>>>(w.win);
   tsa::HuArgs a;
@@ -993,18 +994,20 @@ static tsa_status hu_window_pass(const tsa_hu_problem *p, const HuWs &w, bool hi
   a.n = n;
   a.nz = p->nz;
   a.bg = p->background;
-  a.hu_hist = histograms ? w.hu_hist : nullptr;
+  a.hu_hist = w.hu_hist;
   a.win = w.win;
   a.status = w.status;
   // <= 128 K voxels per CTA (a 16-bit counter copy serves 4 of 16 warps:
-  // < 65536 counts; the background goes straight to global memory); 64 KB of
-  // bins: three CTAs per SM
-  a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (n + 131071) / 131072) * 2);
-  const size_t smem = histograms ? (size_t)4 * (tsa::kHuBins / 2) * sizeof(uint32_t) : 0;
-  if (smem > 48 * 1024)
-    TSA_CUDA(cudaFuncSetAttribute(tsa::k_hu_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // < 32 K counts); 64 KB of bins: three CTAs per SM
+  a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (n + 131071) / 131072));
+  const size_t smem = (size_t)4 * (tsa::kHuBins / 2) * sizeof(uint32_t);
+  TSA_CUDA(cudaFuncSetAttribute(tsa::k_hu_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   tsa::k_hu_hist<<<dim3((unsigned)a.chunks, (unsigned)p->nz), 512, smem, s>>>(a);
-  return check_cuda("k_hu_hist");
+  TSA_TRY(check_cuda("k_hu_hist"));
+  tsa::k_hu_window<<<dim3(tsa::kHuBins / 256, (unsigned)std::min<int64_t>(p->nz, 16)), 256, 0, s>>>(
+      w.hu_hist, p->nz, p->background, w.win);
+  tsa::k_hu_window_fold<<<1, 1, 0, s>>>(w.win);
+  return check_cuda("k_hu_window");
 }
 
 tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
@@ -1019,7 +1022,7 @@ tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32
   if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
   cudaStream_t s = S(stream);
   const int64_t n = p->nx * p->ny;
-  TSA_TRY(hu_window_pass(p, w, true, s));
+  TSA_TRY(hu_window_pass(p, w, s));
   uint32_t *hist8 = out->histogram ? out->histogram : w.hist8;
   TSA_CUDA(cudaMemsetAsync(hist8, 0, sizeof(uint32_t) * p->nz * 256, s));
   tsa::k_hu_glut<<<tsa::kHuBins / 256, 256, 0, s>>>(w.win, p->background, w.glut);
@@ -1051,7 +1054,7 @@ tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *wi
   const size_t need = carve_hu(p, reinterpret_cast<char *>(workspace), &w);
   if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
   cudaStream_t s = S(stream);
-  TSA_TRY(hu_window_pass(p, w, false, s));
+  TSA_TRY(hu_window_pass(p, w, s));
   const int64_t total = p->nx * p->ny * p->nz;
   const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)g_num_sms() * 8);
   tsa::k_hu_map<<<blocks, 256, 0, s>>>(p->volume, gray, w.win, p->background, total);

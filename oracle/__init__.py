@@ -76,6 +76,12 @@ def _load():
         lib.oracle_hist2d.argtypes = [P, I64, I64, I, P]
         lib.oracle_phi2d_at.restype = D
         lib.oracle_phi2d_at.argtypes = [P, I, D, I, I, ctypes.POINTER(I)]
+        lib.oracle_erode.restype = None
+        lib.oracle_erode.argtypes = [P, I64, I64, I, P]
+        lib.oracle_dilate.restype = None
+        lib.oracle_dilate.argtypes = [P, I64, I64, I, P]
+        lib.oracle_tophat.restype = None
+        lib.oracle_tophat.argtypes = [P, I64, I64, I, P, P]
         lib.oracle_preprocess.restype = None
         lib.oracle_preprocess.argtypes = [P, I64, I, P, P, P]
         lib.oracle_search2d_n.restype = I
@@ -248,3 +254,37 @@ def preprocess(vol_i16, background=-2000):
     _load().oracle_preprocess(v.ctypes.data, v.size, int(background), out.ctypes.data,
                               lo.ctypes.data, hi.ctypes.data)
     return out, int(lo[0]), int(hi[0])
+
+
+# ------------------------------------------------------------ morphology (f3)
+def _slicewise(fn, a, r):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    two = a.ndim == 2
+    a3 = a[None] if two else a
+    out = np.empty_like(a3)
+    for z in range(a3.shape[0]):
+        fn(a3[z].ctypes.data, a3.shape[2], a3.shape[1], int(r), out[z].ctypes.data)
+    return out[0] if two else out
+
+
+def erode(a, r):
+    """Grayscale erosion by disk(r), outside = 255 (R26-R27)."""
+    return _slicewise(_load().oracle_erode, a, r)
+
+
+def dilate(a, r):
+    """Grayscale dilation by disk(r), outside = 0 (R26-R27)."""
+    return _slicewise(_load().oracle_dilate, a, r)
+
+
+def tophat(a, r):
+    """(opening, white top-hat) of every slice (R28)."""
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    two = a.ndim == 2
+    a3 = a[None] if two else a
+    op = np.empty_like(a3)
+    th = np.empty_like(a3)
+    for z in range(a3.shape[0]):
+        _load().oracle_tophat(a3[z].ctypes.data, a3.shape[2], a3.shape[1], int(r),
+                              op[z].ctypes.data, th[z].ctypes.data)
+    return (op[0], th[0]) if two else (op, th)

@@ -624,3 +624,58 @@ void oracle_preprocess(const int16_t *vol, int64_t n, int background, uint8_t *o
   if (lo_out) *lo_out = lo;
   if (hi_out) *hi_out = hi;
 }
+
+/* ======================================================================
+ * Morphology: grayscale
+ * erosion / dilation by a disk structuring element, opening, and the top-hat
+ * mask that removes the chest ("subtracting the original image from the
+ * opened mask").  Readings (R26-R28, after SPEC.md:118-166):
+ *   disk(r)      = { (dy,dx) : dy^2 + dx^2 <= r^2 }            ("disk-like ... size 10", :550)
+ *   erode(a)(y,x)  = min over disk of a(y+dy, x+dx), samples outside the
+ *                    slice = 255 (neutral for min)               A (-) B = {z | (B)_z in A}, :534
+ *   dilate(a)(y,x) = max over the reflected disk (= the disk) of a(y+dy, x+dx),
+ *                    outside = 0 (neutral for max)               A (+) B, :540
+ *   open(a)      = dilate(erode(a))                             A o B = (A (-) B) (+) B, :546
+ *   tophat(a)    = max(a - open(a), 0)  (white top-hat)
+ * Per slice, brute force over the disk's offsets.
+ * ====================================================================== */
+static void morph_pass(const uint8_t *a, int64_t nx, int64_t ny, int r, int is_max, uint8_t *out) {
+  for (int64_t y = 0; y < ny; y++) {
+    for (int64_t x = 0; x < nx; x++) {
+      int acc = is_max ? 0 : 255;
+      for (int dy = -r; dy <= r; dy++) {
+        for (int dx = -r; dx <= r; dx++) {
+          if (dy * dy + dx * dx > r * r) continue;
+          int64_t yy = y + dy, xx = x + dx;
+          int v = (yy < 0 || yy >= ny || xx < 0 || xx >= nx) ? (is_max ? 0 : 255)
+                                                             : a[yy * nx + xx];
+          if (is_max ? v > acc : v < acc) acc = v;
+        }
+      }
+      out[y * nx + x] = (uint8_t)acc;
+    }
+  }
+}
+
+void oracle_erode(const uint8_t *a, int64_t nx, int64_t ny, int r, uint8_t *out) {
+  morph_pass(a, nx, ny, r, 0, out);
+}
+
+void oracle_dilate(const uint8_t *a, int64_t nx, int64_t ny, int r, uint8_t *out) {
+  morph_pass(a, nx, ny, r, 1, out);
+}
+
+/* opening and top-hat of one slice; open_out may be NULL */
+void oracle_tophat(const uint8_t *a, int64_t nx, int64_t ny, int r, uint8_t *open_out,
+                   uint8_t *tophat_out) {
+  uint8_t *e = (uint8_t *)malloc((size_t)(nx * ny));
+  uint8_t *o = (uint8_t *)malloc((size_t)(nx * ny));
+  morph_pass(a, nx, ny, r, 0, e);
+  morph_pass(e, nx, ny, r, 1, o);
+  for (int64_t i = 0; i < nx * ny; i++) {
+    if (open_out) open_out[i] = o[i];
+    tophat_out[i] = (uint8_t)(a[i] > o[i] ? a[i] - o[i] : 0);
+  }
+  free(e);
+  free(o);
+}

@@ -276,6 +276,24 @@ tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32
 tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *window,
                              void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- Morphology: opening and the top-hat mask --------------------------
+ * (readings DESIGN.md R26-R28)
+ * Per slice, grayscale, structuring element disk(r) = {dy^2 + dx^2 <= r^2}:
+ *   ERODE   out = min over the disk, samples outside the slice = 255
+ *   DILATE  out = max over the disk, outside = 0
+ *   OPEN    out = dilate(erode(in))                    (A o B = (A (-) B) (+) B)
+ *   TOPHAT  out = max(in - open(in), 0)                (the chest mask, white top-hat)
+ * in / out: [nz][ny][nx] u8, device, may not alias.  radius 0..10 (the paper:
+ * 10).  OPEN and TOPHAT need tsa_morph_workspace_size() bytes (the eroded
+ * volume); ERODE / DILATE need none (workspace may be NULL). */
+typedef enum { TSA_MORPH_ERODE = 0, TSA_MORPH_DILATE = 1, TSA_MORPH_OPEN = 2, TSA_MORPH_TOPHAT = 3 } tsa_morph_op;
+
+size_t tsa_morph_workspace_size(int64_t nx, int64_t ny, int64_t nz, int32_t op);
+
+tsa_status tsa_morph(const uint8_t *in, uint8_t *out, int64_t nx, int64_t ny, int64_t nz,
+                     int32_t radius, int32_t op, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
 const char *tsa_status_string(tsa_status s);
 const char *tsa_last_error(void);
 int32_t tsa_version(void);

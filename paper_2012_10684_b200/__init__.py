@@ -38,6 +38,7 @@ EXPORTS = (
     "tsa2d_validate", "tsa2d_workspace_size", "tsa2d_cluster_size", "tsa2d_segment",
     "tsa2d_histogram", "tsa2d_mean3x3",
     "tsa_hu_workspace_size", "tsa_hu_segment", "tsa_hu_preprocess",
+    "tsa_morph_workspace_size", "tsa_morph",
 )
 
 
@@ -149,6 +150,8 @@ def load() -> ctypes.CDLL:
         "tsa_hu_workspace_size": (SZ, [PH]),
         "tsa_hu_segment": (I32, [PH, PO, P, P, SZ, P]),
         "tsa_hu_preprocess": (I32, [PH, P, P, P, SZ, P]),
+        "tsa_morph_workspace_size": (SZ, [I64, I64, I64, I32]),
+        "tsa_morph": (I32, [P, P, I64, I64, I64, I32, I32, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -505,6 +508,29 @@ def tsa_hu_preprocess(vol, background=-2000, workspace=None, stream=None):
     _check(load().tsa_hu_preprocess(ctypes.byref(p), _ptr(gray), _ptr(win), _ptr(workspace),
                                     workspace.numel(), _stream(stream)), "tsa_hu_preprocess")
     return gray, win
+
+
+# ------------------------------------------------------------- morphology
+MORPH_OPS = {"erode": 0, "dilate": 1, "open": 2, "tophat": 3}
+
+
+def tsa_morph(vol, op="tophat", radius=10, out=None, workspace=None, stream=None):
+    """Disk(radius) grayscale morphology per slice:
+    'erode', 'dilate', 'open' or 'tophat' (max(vol - open(vol), 0))."""
+    _need_cuda(vol)
+    if vol.dim() != 3 or not vol.is_contiguous() or vol.dtype != torch.uint8:
+        raise ValueError("morphology: volume must be a contiguous uint8 [nz][ny][nx] tensor")
+    nz, ny, nx = vol.shape
+    code = MORPH_OPS.get(op, op)
+    if out is None:
+        out = torch.empty_like(vol)
+    n = int(load().tsa_morph_workspace_size(nx, ny, nz, code))
+    if workspace is None and n:
+        workspace = torch.empty(n, dtype=torch.uint8, device=vol.device)
+    _check(load().tsa_morph(_ptr(vol), _ptr(out), nx, ny, nz, int(radius), code, _ptr(workspace),
+                            workspace.numel() if workspace is not None else 0, _stream(stream)),
+           "tsa_morph")
+    return out
 
 
 def unpack_key(key, k):

@@ -1063,6 +1063,78 @@ tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *wi
   return TSA_OK;
 }
 
+// ------------------------------------------------------------ morphology
+}  // extern "C"
+
+template <int R, bool MAX, bool TOPHAT>
+static tsa_status launch_morph_r(const tsa::MorphArgs &a, cudaStream_t s) {
+  const size_t smem = tsa::morph_smem<R>();
+  auto f = tsa::k_morph<R, MAX, TOPHAT>;
+  TSA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const dim3 grid((unsigned)((a.nx + tsa::kMorphStrip - 1) / tsa::kMorphStrip), (unsigned)a.nz);
+  f<<<grid, tsa::kMorphThreads, smem, s>>>(a);
+  return check_cuda("k_morph");
+}
+
+template <bool MAX, bool TOPHAT>
+static tsa_status launch_morph(int r, const tsa::MorphArgs &a, cudaStream_t s) {
+  switch (r) {
+    case 1: return launch_morph_r<1, MAX, TOPHAT>(a, s);
+    case 2: return launch_morph_r<2, MAX, TOPHAT>(a, s);
+    case 3: return launch_morph_r<3, MAX, TOPHAT>(a, s);
+    case 4: return launch_morph_r<4, MAX, TOPHAT>(a, s);
+    case 5: return launch_morph_r<5, MAX, TOPHAT>(a, s);
+    case 6: return launch_morph_r<6, MAX, TOPHAT>(a, s);
+    case 7: return launch_morph_r<7, MAX, TOPHAT>(a, s);
+    case 8: return launch_morph_r<8, MAX, TOPHAT>(a, s);
+    case 9: return launch_morph_r<9, MAX, TOPHAT>(a, s);
+    default: return launch_morph_r<10, MAX, TOPHAT>(a, s);
+  }
+}
+
+extern "C" {
+
+size_t tsa_morph_workspace_size(int64_t nx, int64_t ny, int64_t nz, int32_t op) {
+  if (nx <= 0 || ny <= 0 || nz <= 0) return 0;
+  return (op == TSA_MORPH_OPEN || op == TSA_MORPH_TOPHAT) ? align_up((size_t)(nx * ny * nz)) : 0;
+}
+
+tsa_status tsa_morph(const uint8_t *in, uint8_t *out, int64_t nx, int64_t ny, int64_t nz,
+                     int32_t radius, int32_t op, void *workspace, size_t workspace_bytes,
+                     void *stream) {
+  if (!in || !out || in == out || nx <= 0 || ny <= 0 || nz <= 0 || nx * ny >= (int64_t(1) << 31) ||
+      radius < 0 || radius > tsa::kMorphRmax || op < TSA_MORPH_ERODE || op > TSA_MORPH_TOPHAT)
+    return set_error(TSA_ERR_INVALID_ARG, "morph: pointers/dims/radius (0..10)/op");
+  cudaStream_t s = S(stream);
+  const size_t vb = (size_t)(nx * ny * nz);
+  const bool two = op == TSA_MORPH_OPEN || op == TSA_MORPH_TOPHAT;
+  if (two && (!workspace || workspace_bytes < vb)) return set_error(TSA_ERR_WORKSPACE, "morph workspace");
+  if (radius == 0) {  // disk(0) = the origin: erosion / dilation / opening are the identity
+    if (op == TSA_MORPH_TOPHAT) TSA_CUDA(cudaMemsetAsync(out, 0, vb, s));
+    else TSA_CUDA(cudaMemcpyAsync(out, in, vb, cudaMemcpyDeviceToDevice, s));
+    return TSA_OK;
+  }
+  tsa::MorphArgs a;
+  a.nx = nx;
+  a.ny = ny;
+  a.nz = nz;
+  a.orig = nullptr;
+  if (op == TSA_MORPH_ERODE || op == TSA_MORPH_DILATE) {
+    a.src = in;
+    a.dst = out;
+    return op == TSA_MORPH_ERODE ? launch_morph<false, false>(radius, a, s) : launch_morph<true, false>(radius, a, s);
+  }
+  uint8_t *e = reinterpret_cast<uint8_t *>(workspace);
+  a.src = in;
+  a.dst = e;
+  TSA_TRY((launch_morph<false, false>(radius, a, s)));
+  a.src = e;
+  a.dst = out;
+  if (op == TSA_MORPH_OPEN) return launch_morph<true, false>(radius, a, s);
+  a.orig = in;
+  return launch_morph<true, true>(radius, a, s);
+}
+
 // ----------------------------------------------------------- host buffers
 static size_t slab_bytes(const tsa_problem *p, int64_t slab, tsa_problem *sp) {
   *sp = *p;

@@ -5,6 +5,7 @@
 //   a4 k_finalize.cuh    argmax merge + phi(t*) recompute
 //   a5 k_label.cuh       Algorithm 1 generalised to k classes
 //   f2 k_hu.cuh          pre-processing fused into histogram / labels PAPER.md:514-516
+//   f3 k_morph.cuh       disk opening / top-hat (streaming, 16-bit SIMD)
 //   f1 k_tsallis2d.cuh   the paper's 2-D formulation (cluster per slice) PAPER.md:564-597
 #pragma once
 #include "k_histogram.cuh"
@@ -14,3 +15,4 @@
 #include "k_label.cuh"
 #include "k_tsallis2d.cuh"
 #include "k_hu.cuh"
+#include "k_morph.cuh"

@@ -510,6 +510,110 @@ def run_hu(args, cfg, rank, world, dev):
         dist.destroy_process_group()
 
 
+def run_morph(args, cfg, rank, world, dev):
+    """The morphology workload: a step = tsa_morph
+    'tophat' with disk(10) of the resident volume (erode pass + dilate pass
+    with the fused subtraction)."""
+    import numpy as np
+    import torch
+
+    import phantom
+    import paper_2012_10684_b200 as tsa
+
+    r = cfg.k
+    host = phantom.make_volume(cfg)
+    n_vox = host.size
+    nbuf = args.buffers or max(2, int(np.ceil(2 * 126e6 / (2 * n_vox))) + 1)
+    vols = [torch.from_numpy(host).to(dev) for _ in range(nbuf)]
+    outs = [torch.empty_like(vols[0]) for _ in range(nbuf)]
+    ws = torch.empty(int(tsa.load().tsa_morph_workspace_size(cfg.nx, cfg.ny, cfg.nz, 3)),
+                     dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        tsa.tsa_morph(vols[i % nbuf], "tophat", r, out=outs[i % nbuf], workspace=ws, stream=stream)
+
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    barrier(world)
+    ms_per_step = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    value = world * cfg.nz / (ms_per_step * 1e-3)
+    pk_, how = peaks()
+    hbm = float(pk_.get("hbm_gbs", HBM_FALLBACK_GBS))
+    alg = 2 * n_vox  # the volume once + the mask once
+    moved = 5 * n_vox  # two passes: in, eroded out/in, in again (subtraction), mask out
+    roofline = {"bound": "hbm", "kernel": "k_morph erode pass + k_morph dilate/top-hat pass",
+                "achieved": alg / (ms_per_step * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": alg / (ms_per_step * 1e-3) / 1e9 / hbm, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({how})",
+                "algorithmic_bytes_per_launch": alg, "bytes_moved_two_pass": moved,
+                "note": "issue-bound: ~40 integer instructions per pixel per pass (16-bit-lane min/max)"}
+    host_t = torch.from_numpy(host).pin_memory()
+    hout = torch.empty(host.shape, dtype=torch.uint8).pin_memory()
+    dvol = torch.empty_like(vols[0])
+
+    def e2e_step():
+        dvol.copy_(host_t, non_blocking=True)
+        tsa.tsa_morph(dvol, "tophat", r, out=outs[0], workspace=ws, stream=stream)
+        hout.copy_(outs[0], non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e_step()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": world * cfg.nz * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(hout.nbytes),
+               "api": "pinned H2D copy + tsa_morph(tophat) + D2H of the mask", "steps": args.e2e_steps}
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < 10.0 and n < cfg.nz:
+            oracle.tophat(host[n], r)
+            n += 1
+        el = time.perf_counter() - t0
+        cpu = {"value": n / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"the first {n} of {cfg.nz} slices of f3 (brute-force disk({r}) erosion, "
+                         f"dilation, subtraction; single-threaded), {el:.1f} s"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
+                       "slices_per_gpu": cfg.nz, "radius": r, "op": "white top-hat = in - open(in)",
+                       "parallelism": f"slices sharded, {world} GPU(s), no collective",
+                       "l2": "inputs larger than L2: rotating resident volume copies"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": 2 * args.steps, "pipeline": "morph (2 streaming passes)",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def config_of(cfg, args, world):
     return {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
             "slices_per_gpu": cfg.nz, "bins": cfg.bins, "k": cfg.k, "q": cfg.qs[0],
@@ -614,6 +718,9 @@ def main():
         return
     if cfg.name == "f2":
         run_hu(args, cfg, rank, world, dev)
+        return
+    if cfg.name == "f3":
+        run_morph(args, cfg, rank, world, dev)
         return
     q = cfg.qs[0]
     k, bins = cfg.k, cfg.bins

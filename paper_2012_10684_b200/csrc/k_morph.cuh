@@ -7,13 +7,14 @@
 // Decomposition (exact): the disk is the union of the horizontal segments
 // |dx| <= w(dy) = floor(sqrt(r^2 - dy^2)), so
 //   erode(a)(y, x) = min_dy H_{w(dy)}(y + dy, x),   H_w(y, x) = min_{|dx| <= w} a(y, x+dx).
-// One CTA streams a 256-pixel column strip of a slice top to bottom, four rows
-// per step (a thread = 4 pixels of a row): each new row's H_w for w = 0..r is
-// a cascade H_w = min(H_{w-1}, a(x-w), a(x+w)) in 16-bit lanes (two pixels per
-// VIMNMX.U16x2; the 8-bit SIMD forms are emulated on sm_100a), the distinct
-// widths the disk uses (7 for r = 10) are kept in a ring of 2r+4 rows in
-// shared memory (88 KB: two CTAs per SM), and each output row (r rows behind)
-// is the min over the 2r+1 ring rows of its disk.  The input is read
+// A CTA streams a 256-pixel column strip of 128 output rows of a slice top to
+// bottom (plus r halo rows each side); a thread owns 4 pixel columns.  For
+// each input row the thread computes its H_w, w = 0..r, as a cascade H_w =
+// min(H_{w-1}, a(x-w), a(x+w)) in 16-bit lanes (two pixels per VIMNMX.U16x2;
+// the 8-bit SIMD forms are emulated on sm_100a) from a shared-memory copy of
+// the row, and folds them into REGISTER accumulators of the 2r+1 output rows
+// the input row touches (slot j = output row y-r+j); the completed output
+// row (r rows behind) is written and the slots shift by one.  No vertical gather, no shared-memory ring.  The input is read
 // once per pass (plus a 2r-pixel halo per strip row), the output written once.
 #pragma once
 #include <cmath>
@@ -21,10 +22,9 @@
 
 namespace tsa {
 
-constexpr int kMorphStrip = 256;   // pixels per CTA column strip
-constexpr int kMorphRows = 4;      // rows per step
-constexpr int kMorphTpr = kMorphStrip / 4;  // threads per row (4 pixels each)
-constexpr int kMorphThreads = kMorphRows * kMorphTpr;
+constexpr int kMorphStrip = 256;                // pixels per CTA column strip
+constexpr int kMorphThreads = kMorphStrip / 4;  // a thread = 4 pixel columns
+constexpr int kMorphChunk = 128;                // output rows per CTA
 constexpr int kMorphRmax = 10;
 
 struct MorphArgs {
@@ -85,129 +85,165 @@ __device__ __forceinline__ uint32_t pairk(const uint32_t *win) {
   return __byte_perm(win[K / 2], win[K / 2 + 1], 0x5432);
 }
 
-template <int R, bool MAX, int P, int D>
-__device__ __forceinline__ void cascade_step(const uint32_t *win, uint32_t &m) {
-  // widen the window of the pair at pixel offset P by displacement D
-  m = vop<MAX>(m, pairk<(R + R % 2) + P + D>(win));
+// Register accumulators of the 2R+1 pending output rows of a thread's 4
+// columns (two 16-bit-lane words each); slot j holds output row y-R+j while
+// input row y is processed.
+template <int R>
+struct Acc {
+  uint32_t a[2 * R + 1][2];
+};
+
+// The H_w cascade of one input row for the thread's two pixel pairs: hw[w]
+// for w = 0..R (only the widths the disk uses are read by the caller).
+template <int R, bool MAX, int W>
+__device__ __forceinline__ void cascade(const uint32_t *win, uint32_t (&h0)[R + 1], uint32_t (&h1)[R + 1]) {
+  if constexpr (W == 0) {
+    h0[0] = pairk<R + R % 2>(win);
+    h1[0] = pairk<R + R % 2 + 2>(win);
+  } else {
+    h0[W] = vop<MAX>(vop<MAX>(h0[W - 1], pairk<R + R % 2 - W>(win)), pairk<R + R % 2 + W>(win));
+    h1[W] = vop<MAX>(vop<MAX>(h1[W - 1], pairk<R + R % 2 + 2 - W>(win)), pairk<R + R % 2 + 2 + W>(win));
+  }
+  if constexpr (W < R) cascade<R, MAX, W + 1>(win, h0, h1);
 }
 
-template <int R, bool MAX, int W>
-struct Cascade {
-  // m0 / m1: the two pairs' running H_{W-1}; apply width W, store, recurse
-  __device__ __forceinline__ static void run(const uint32_t *win, uint32_t &m0, uint32_t &m1,
-                                             uint32_t *slot, int t) {
-    cascade_step<R, MAX, 0, -W>(win, m0);
-    cascade_step<R, MAX, 0, W>(win, m0);
-    cascade_step<R, MAX, 2, -W>(win, m1);
-    cascade_step<R, MAX, 2, W>(win, m1);
-    if (widx<R>(W) >= 0)
-      *reinterpret_cast<uint2 *>(slot + widx<R>(W) * (kMorphStrip / 2) + 2 * t) = make_uint2(m0, m1);
-    Cascade<R, MAX, W + 1>::run(win, m0, m1, slot, t);
+// Input row y contributes H_{w(R-j)} to the pending output row y-R+j held in
+// slot j, j = 0..2R; output row y-R (slot 0) is then complete: written (if it
+// is one of this CTA's rows) and the slots shift down by one (register moves:
+// a short loop body instead of a (2R+1)-phase unrolled one, which overflowed
+// the instruction cache).
+template <int R, bool MAX, bool TOPHAT>
+__device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool real, int64_t y,
+                                          int64_t ylo, int64_t yhi, const MorphArgs &g, int z,
+                                          int64_t xp, bool full) {
+  constexpr uint32_t NEUT2 = (MAX ? 0u : 255u) * 0x00010001u;
+  if (real) {
+    uint32_t h0[R + 1], h1[R + 1];
+    cascade<R, MAX, 0>(win, h0, h1);
+#pragma unroll
+    for (int j = 0; j <= 2 * R; j++) {
+      const int w = halfw<R>(R - j < 0 ? j - R : R - j);
+      acc.a[j][0] = vop<MAX>(acc.a[j][0], h0[w]);
+      acc.a[j][1] = vop<MAX>(acc.a[j][1], h1[w]);
+    }
   }
+  const int64_t yo = y - R;
+  if (yo >= ylo && yo < yhi && xp < g.nx) {
+    uint32_t a0 = acc.a[0][0], a1 = acc.a[0][1];
+    const int64_t o = ((size_t)z * g.ny + yo) * g.nx + xp;
+    if (TOPHAT) {
+      // max(orig - open, 0) per 16-bit lane = max(orig, open) - open
+      uint32_t ow = 0u;
+      if (full) {
+        ow = *reinterpret_cast<const uint32_t *>(g.orig + o);
+      } else {
+        for (int e = 0; e < 4; e++)
+          if (xp + e < g.nx) ow |= (uint32_t)g.orig[o + e] << (8 * e);
+      }
+      const uint32_t o0 = __byte_perm(ow, 0u, 0x4140), o1 = __byte_perm(ow, 0u, 0x4342);
+      a0 = __vmaxu2(o0, a0) - a0;
+      a1 = __vmaxu2(o1, a1) - a1;
+    }
+    const uint32_t packed = __byte_perm(a0, a1, 0x6420);  // bytes 0,2 of a0 then of a1
+    if (full) {
+      *reinterpret_cast<uint32_t *>(g.dst + o) = packed;
+    } else {
+      for (int e = 0; e < 4; e++)
+        if (xp + e < g.nx) g.dst[o + e] = (uint8_t)((packed >> (8 * e)) & 0xffu);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * R; j++) {
+    acc.a[j][0] = acc.a[j + 1][0];
+    acc.a[j][1] = acc.a[j + 1][1];
+  }
+  acc.a[2 * R][0] = NEUT2;
+  acc.a[2 * R][1] = NEUT2;
+}
+
+// Row y's strip segment (pixels x0-PADL .. x0+kMorphStrip+PADL+3) as u16
+// pixels: fetched into registers first (the loads fly while the current row
+// is computed), stored into the idle row buffer afterwards.
+template <int R>
+struct RowFetch {
+  static constexpr int PADL = R + R % 2;
+  static constexpr int N = kMorphStrip + 2 * PADL + 4;
+  static constexpr int PER = (N + kMorphThreads - 1) / kMorphThreads;
+  uint16_t v[PER];
 };
+
 template <int R, bool MAX>
-struct Cascade<R, MAX, R + 1> {
-  __device__ __forceinline__ static void run(const uint32_t *, uint32_t &, uint32_t &, uint32_t *, int) {}
-};
+__device__ __forceinline__ void fetch_row(const uint8_t *src, int64_t y, int64_t x0, int64_t nx,
+                                          RowFetch<R> &f) {
+  constexpr uint16_t NEUT = MAX ? 0 : 255;
+#pragma unroll
+  for (int k = 0; k < RowFetch<R>::PER; k++) {
+    const int i = threadIdx.x + k * kMorphThreads;
+    const int64_t x = x0 - RowFetch<R>::PADL + i;
+    f.v[k] = (i < RowFetch<R>::N && x >= 0 && x < nx) ? (uint16_t)__ldg(src + y * nx + x) : NEUT;
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void store_row(const RowFetch<R> &f, uint16_t *rb) {
+#pragma unroll
+  for (int k = 0; k < RowFetch<R>::PER; k++) {
+    const int i = threadIdx.x + k * kMorphThreads;
+    if (i < RowFetch<R>::N) rb[i] = f.v[k];
+  }
+}
 
 template <int R, bool MAX, bool TOPHAT>
 __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
-  constexpr int NW = nwidths<R>();
-  constexpr int PADL = R + R % 2;                  // even left pad (u16 pixels)
-  constexpr int RS = 2 * R + kMorphRows;           // ring rows
-  constexpr int PW = kMorphStrip / 2;              // pair words per strip row
-  constexpr int BW = (kMorphStrip + 2 * PADL + 4) / 2;  // row buffer words (u16 pixels)
-  constexpr int WINW = (2 * PADL + 4) / 2 + 1;     // register window words
-  constexpr uint32_t NEUT = MAX ? 0u : 255u;
-  constexpr uint32_t NEUT2 = NEUT * 0x00010001u;
-  extern __shared__ __align__(16) uint32_t msm[];
-  uint32_t *ring = msm;                            // [RS][NW][PW]
-  uint32_t *rowbuf = msm + RS * NW * PW;           // [kMorphRows][BW]
-  const int z = blockIdx.y;
+  constexpr int PADL = R + R % 2;
+  constexpr int BW = (kMorphStrip + 2 * PADL + 4) / 2;
+  constexpr int NS = 2 * R + 1;
+  constexpr uint32_t NEUT2 = (MAX ? 0u : 255u) * 0x00010001u;
+  __shared__ __align__(16) uint16_t bufs[2 * 2 * BW];
+  const int z = blockIdx.z;
   const int64_t x0 = (int64_t)blockIdx.x * kMorphStrip;
-  const int64_t nx = g.nx, ny = g.ny;
-  const uint8_t *src = g.src + (size_t)z * nx * ny;
-  const int rr = threadIdx.x / kMorphTpr;          // which of the step's rows
-  const int t = threadIdx.x % kMorphTpr;           // 4-pixel group in the strip
-  const int64_t xp = x0 + 4 * t;
-  const int steps = (int)((ny + R + kMorphRows - 1) / kMorphRows);
-  for (int s = 0; s <= steps; s++) {
-    // ---- S1: the step's input rows (strip + halo) into rowbuf as u16 pixels
-    {
-      const int64_t y = (int64_t)s * kMorphRows + rr;
-      uint16_t *rb = reinterpret_cast<uint16_t *>(rowbuf + rr * BW);
-      if (y < ny)
-        for (int i = t; i < kMorphStrip + 2 * PADL + 4; i += kMorphTpr) {
-          const int64_t x = x0 - PADL + i;
-          rb[i] = (x >= 0 && x < nx) ? (uint16_t)__ldg(src + y * nx + x) : (uint16_t)NEUT;
-        }
-    }
-    __syncthreads();
-    // ---- S2: H_w cascade (w = 0..R) of the new rows into the ring
-    {
-      const int64_t y = (int64_t)s * kMorphRows + rr;
-      if (y < ny) {
-        uint32_t win[WINW];
-        const uint32_t *rb = rowbuf + rr * BW + 2 * t;
+  const int64_t ylo = (int64_t)blockIdx.y * kMorphChunk, yhi = min(g.ny, ylo + kMorphChunk);
+  const uint8_t *src = g.src + (size_t)z * g.nx * g.ny;
+  const int64_t xp = x0 + 4 * threadIdx.x;
+  Acc<R> acc;
 #pragma unroll
-        for (int j = 0; j < WINW; j++) win[j] = rb[j];
-        uint32_t *slot = ring + ((int)y % RS) * NW * PW;
-        uint32_t m0 = pairk<PADL>(win), m1 = pairk<PADL + 2>(win);
-        if (widx<R>(0) >= 0)
-          *reinterpret_cast<uint2 *>(slot + widx<R>(0) * PW + 2 * t) = make_uint2(m0, m1);
-        Cascade<R, MAX, 1>::run(win, m0, m1, slot, t);
-      }
-    }
-    __syncthreads();
-    // ---- S3: output row y = (input row) - R: vertical min/max over the disk
-    {
-      const int64_t y = (int64_t)s * kMorphRows + rr - R;
-      if (y >= 0 && y < ny && xp < nx) {
-        uint32_t a0 = NEUT2, a1 = NEUT2;
+  for (int k = 0; k < NS; k++) acc.a[k][0] = acc.a[k][1] = NEUT2;
+  // input rows ylo-R .. yhi+R-1 (outside the slice: no contribution)
+  constexpr int WINW = PADL + 3;
+  int64_t y = ylo - R;
+  const int64_t yend = yhi + R;
+  // 16-byte... 4-byte aligned output (and top-hat input) words for the whole walk
+  const bool full = xp + 3 < g.nx && (g.nx & 3) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(g.dst) |
+                      (TOPHAT ? reinterpret_cast<uintptr_t>(g.orig) : 0u)) & 3u) == 0;
+  int cur = 0;
+  if (y >= 0 && y < g.ny) {
+    RowFetch<R> f0;
+    fetch_row<R, MAX>(src, y, x0, g.nx, f0);
+    store_row<R>(f0, bufs);
+  }
+  __syncthreads();
+  for (; y < yend; y++) {
+    // the next row's pixels are fetched before this row is computed and
+    // stored into the other buffer after it
+    RowFetch<R> nf;
+    const bool nxt = y + 1 < yend && y + 1 >= 0 && y + 1 < g.ny;
+    if (nxt) fetch_row<R, MAX>(src, y + 1, x0, g.nx, nf);
+    const bool real = y >= 0 && y < g.ny;
+    uint32_t win[WINW];
+    const uint32_t *rb = reinterpret_cast<const uint32_t *>(bufs + cur * 2 * BW) + 2 * threadIdx.x;
 #pragma unroll
-        for (int dy = -R; dy <= R; dy++) {
-          const int64_t yy = y + dy;
-          if (yy < 0 || yy >= ny) continue;  // outside the slice: neutral
-          const int wi = widx<R>(halfw<R>(dy < 0 ? -dy : dy));
-          const uint2 v = *reinterpret_cast<const uint2 *>(ring + (((int)yy % RS) * NW + wi) * PW + 2 * t);
-          a0 = vop<MAX>(a0, v.x);
-          a1 = vop<MAX>(a1, v.y);
-        }
-        const int64_t o = ((size_t)z * ny + y) * nx + xp;
-        const bool full = xp + 3 < nx &&
-                          ((reinterpret_cast<uintptr_t>(g.dst + o) |
-                            (TOPHAT ? reinterpret_cast<uintptr_t>(g.orig + o) : 0u)) & 3u) == 0;
-        if (TOPHAT) {
-          // max(orig - open, 0) per 16-bit lane = max(orig, open) - open
-          uint32_t ow = 0u;
-          if (full) {
-            ow = *reinterpret_cast<const uint32_t *>(g.orig + o);
-          } else {
-            for (int e = 0; e < 4; e++)
-              if (xp + e < nx) ow |= (uint32_t)g.orig[o + e] << (8 * e);
-          }
-          const uint32_t o0 = __byte_perm(ow, 0u, 0x4140), o1 = __byte_perm(ow, 0u, 0x4342);
-          a0 = __vmaxu2(o0, a0) - a0;
-          a1 = __vmaxu2(o1, a1) - a1;
-        }
-        const uint32_t packed = __byte_perm(a0, a1, 0x6420);  // bytes 0,2 of a0 then of a1
-        if (full) {
-          *reinterpret_cast<uint32_t *>(g.dst + o) = packed;
-        } else {
-          for (int e = 0; e < 4; e++)
-            if (xp + e < nx) g.dst[o + e] = (uint8_t)((packed >> (8 * e)) & 0xffu);
-        }
-      }
-    }
+    for (int j = 0; j < WINW; j++) win[j] = real ? rb[j] : 0u;
+    morph_row<R, MAX, TOPHAT>(acc, win, real, y, ylo, yhi, g, z, xp, full);
+    if (nxt) store_row<R>(nf, bufs + (cur ^ 1) * 2 * BW);
+    __syncthreads();  // the other buffer is complete; this one may be overwritten
+    cur ^= 1;
   }
 }
 
 template <int R>
 __host__ inline size_t morph_smem() {
-  constexpr int NW = nwidths<R>();
-  constexpr int PADL = R + R % 2;
-  return (size_t)(2 * R + kMorphRows) * NW * (kMorphStrip / 2) * 4 +
-         (size_t)kMorphRows * ((kMorphStrip + 2 * PADL + 4) / 2) * 4;
+  return 0;
 }
 
 }  // namespace tsa

@@ -1068,11 +1068,9 @@ tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *wi
 
 template <int R, bool MAX, bool TOPHAT>
 static tsa_status launch_morph_r(const tsa::MorphArgs &a, cudaStream_t s) {
-  const size_t smem = tsa::morph_smem<R>();
-  auto f = tsa::k_morph<R, MAX, TOPHAT>;
-  TSA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const dim3 grid((unsigned)((a.nx + tsa::kMorphStrip - 1) / tsa::kMorphStrip), (unsigned)a.nz);
-  f<<<grid, tsa::kMorphThreads, smem, s>>>(a);
+  const dim3 grid((unsigned)((a.nx + tsa::kMorphStrip - 1) / tsa::kMorphStrip),
+                  (unsigned)((a.ny + tsa::kMorphChunk - 1) / tsa::kMorphChunk), (unsigned)a.nz);
+  tsa::k_morph<R, MAX, TOPHAT><<<grid, tsa::kMorphThreads, 0, s>>>(a);
   return check_cuda("k_morph");
 }
 

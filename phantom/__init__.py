@@ -91,6 +91,10 @@ CONFIGS = {
     "f2": Config("f2", 512, 512, 300, "i16", 256, 2, (0.8,), SEED_BASE + 2,
                  note="HU int16 512x512x300 phantom (c2 geometry), pre-processing fused: "
                       "background -2000 -> 0, volume-wide linear rescale to 0..255, 256 bins, k=2"),
+    # disk(10) opening + white top-hat (the chest mask,
+    # PAPER.md:528-550) of the c2 volume; k = 10 stands for the disk radius
+    "f3": Config("f3", 512, 512, 300, "u8", 256, 10, (0.8,), SEED_BASE + 2,
+                 note="disk(10) opening + white top-hat of the 512x512x300 c2 phantom"),
     "f1": Config("f1", 512, 512, 300, "u8", 256, 1, (0.8,), SEED_BASE + 2,
                  note="2-D Tsallis (PAPER.md:564-597) on the 512x512x300 c2 phantom, 256 levels, "
                       "(t,s) search, q=0.8"),

@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--impl", default="tsa", choices=["tsa", "reference"])
-    ap.add_argument("--enumeration", default="canonical", choices=["canonical", "full"])
+    ap.add_argument("--enumeration", default="canonical", choices=["canonical", "full", "dp"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--buffers", type=int, default=0, help="resident volume copies rotated (0 = auto, > 2x L2)")
@@ -813,8 +813,11 @@ def main():
 
     hist_np = outs[0]["histogram"].cpu().numpy()
     m = (hist_np > 0).sum(axis=1)
-    evaluated = int(sum(comb(int(mm) - 1, k) for mm in m)) if args.enumeration == "canonical" else \
-        cfg.nz * comb(bins - 1, k)
+    if args.enumeration == "dp":  # class terms of the interval DP (m(m+1)/2 per slice), not tuples
+        evaluated = int(sum(int(mm) * (int(mm) + 1) // 2 for mm in m))
+    else:
+        evaluated = int(sum(comb(int(mm) - 1, k) for mm in m)) if args.enumeration == "canonical" else \
+            cfg.nz * comb(bins - 1, k)
     nominal = cfg.nz * comb(bins - 1, k)
     kernels["search"]["tuples_nominal"] = nominal
     kernels["search"]["tuples_evaluated"] = evaluated

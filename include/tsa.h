@@ -75,7 +75,14 @@ typedef enum { TSA_OBJ_PSEUDO_ADDITIVE = 0, TSA_OBJ_SUM_PLUS_PRODUCT = 1 } tsa_o
  * bins).  Both return the same (bit-identical) t* and score: tuples that
  * differ only by empty bins describe the same partition, evaluate to the same
  * value bit for bit, and the lowest of them is the canonical one. */
-typedef enum { TSA_ENUM_CANONICAL = 0, TSA_ENUM_FULL = 1 } tsa_enumeration;
+typedef enum { TSA_ENUM_CANONICAL = 0, TSA_ENUM_FULL = 1, TSA_ENUM_DP = 2 } tsa_enumeration;
+/* TSA_ENUM_DP: not an enumeration but an exact
+ * interval dynamic programme over the canonical positions, O(k m^2) class
+ * terms: maximises sum_j g(C_j), g = ln A (q < 1), -ln A (q > 1), S (q == 1),
+ * which orders tuples as phi does (phi = (prod A_j - 1)/(1 - q), R1).  Returns
+ * the lexicographically smallest optimum of that sum; it differs from the
+ * exhaustive argmax only on partitions whose objectives differ by rounding.
+ * PSEUDO_ADDITIVE only (INVALID_ARG otherwise); one work unit per slice. */
 
 typedef struct {
   const void *volume;   /* [nz][ny][nx] u8 or u16, device */

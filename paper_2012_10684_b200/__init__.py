@@ -22,12 +22,12 @@ TSA_OK, TSA_ERR_INVALID_ARG, TSA_ERR_LEVEL_OVERFLOW, TSA_ERR_NO_VALID_SPLIT = 0,
 TSA_ERR_WORKSPACE, TSA_ERR_CUDA, TSA_ERR_NCCL = 4, 5, 6
 TSA_U8, TSA_U16 = 1, 2
 TSA_OBJ_PSEUDO_ADDITIVE, TSA_OBJ_SUM_PLUS_PRODUCT = 0, 1
-TSA_ENUM_CANONICAL, TSA_ENUM_FULL = 0, 1
+TSA_ENUM_CANONICAL, TSA_ENUM_FULL, TSA_ENUM_DP = 0, 1, 2
 TSA_KEY_NONE = 0xFFFFFFFFFFFFFFFF
 KMAX = 4
 
 OBJECTIVES = {"pseudo_additive": 0, "sum_plus_product": 1}
-ENUMERATIONS = {"canonical": 0, "full": 1}
+ENUMERATIONS = {"canonical": 0, "full": 1, "dp": 2}
 
 # every symbol include/tsa.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -82,7 +82,9 @@ bool valid_search_shape(int64_t nz, int64_t N, int32_t bins, int32_t k, double q
   if (k < 1 || k > TSA_KMAX || k > bins - 1) return false;
   if (!(q > 0.0) || !std::isfinite(q)) return false;
   if (objective != TSA_OBJ_PSEUDO_ADDITIVE && objective != TSA_OBJ_SUM_PLUS_PRODUCT) return false;
-  if (enumeration != TSA_ENUM_CANONICAL && enumeration != TSA_ENUM_FULL) return false;
+  if (enumeration != TSA_ENUM_CANONICAL && enumeration != TSA_ENUM_FULL && enumeration != TSA_ENUM_DP)
+    return false;
+  if (enumeration == TSA_ENUM_DP && objective != TSA_OBJ_PSEUDO_ADDITIVE) return false;
   if (binom_d((double)bins - 1, k) >= 9.2e18) return false;
   return true;
 }
@@ -133,7 +135,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   w.Asuf = c.take<double>(nz * (size_t)bins);
   w.M = c.take<int32_t>(nz);
   w.counter = c.take<int32_t>(1);
-  if (use_rtable(bins, k, objective)) {
+  if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
     w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
     if (k >= 4) w.AI = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
@@ -261,7 +263,7 @@ tsa_status tsa_validate(const tsa_problem *p) {
 }
 
 int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
-  if (nz <= 0) return 1;
+  if (nz <= 0 || enumeration == TSA_ENUM_DP) return 1;
   const double target = (double)g_num_sms() * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
@@ -586,6 +588,41 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     default: launch_scan<tsa::SPP>(sa, s); break;
   }
   TSA_TRY(check_cuda("k_scan"));
+  if (enumeration == TSA_ENUM_DP) {
+    if (units != 1 || unit_begin != 0 || unit_end != 1)
+      return set_error(TSA_ERR_INVALID_ARG, "DP search: one work unit per slice");
+    tsa::SearchArgs a = {};
+    a.C = w.cC;
+    a.Whi = w.cWhi;
+    a.Wlo = w.cWlo;
+    a.Bin = w.cBin;
+    a.Mz = w.M;
+    a.status = slice_status;
+    a.part_score = part_score;
+    a.part_key = part_key;
+    a.luts = l;
+    a.nz = nz;
+    a.E = E;
+    a.L = bins;
+    // suffix values + the term table (used by slices whose m fits kDpTableMax)
+    const size_t smem = (size_t)(k + 1) * (bins + 1) * sizeof(double) +
+                        std::min(tsa::dp_table_bytes(bins), tsa::kDpTableMax);
+    switch (mode) {
+      case tsa::PROD_MAX: {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::PROD_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tsa::k_search_dp<tsa::PROD_MAX><<<(unsigned)nz, 256, smem, s>>>(a, k);
+      } break;
+      case tsa::PROD_MIN: {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::PROD_MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tsa::k_search_dp<tsa::PROD_MIN><<<(unsigned)nz, 256, smem, s>>>(a, k);
+      } break;
+      default: {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::SUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tsa::k_search_dp<tsa::SUM><<<(unsigned)nz, 256, smem, s>>>(a, k);
+      } break;
+    }
+    return check_cuda("k_search_dp");
+  }
   const bool full = enumeration == TSA_ENUM_FULL;
   const uint32_t *tC = full ? w.fC : w.cC;
   const double *tWhi = full ? w.fWhi : w.cWhi;

@@ -279,6 +279,20 @@ size_t tsa_hu_workspace_size(const tsa_hu_problem *p);
 tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
                           void *workspace, size_t workspace_bytes, void *stream);
 
+/* The two phases of tsa_hu_segment, for slices sharded over ranks (the
+ * window is volume-wide, so ranks exchange it: an all-reduce of (min lo,
+ * max hi) between the phases):
+ *   tsa_hu_histogram  HU histograms of the slab into the workspace and the
+ *                     slab's window -> window_out (device int32[2]; (INT_MAX,
+ *                     INT_MIN) when the slab has no non-background voxel)
+ *   tsa_hu_finish     8-bit histograms under window_in (device int32[2]), the
+ *                     search, finalize and labels -> out (as tsa_hu_segment)
+ * Same workspace for both (tsa_hu_workspace_size), left untouched between. */
+tsa_status tsa_hu_histogram(const tsa_hu_problem *p, int32_t *window_out, void *workspace,
+                            size_t workspace_bytes, void *stream);
+tsa_status tsa_hu_finish(const tsa_hu_problem *p, const int32_t *window_in, const tsa_outputs *out,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
 /* The pre-processing step alone: gray [nz][ny][nx] u8 = g(v); window as above. */
 tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *window,
                              void *workspace, size_t workspace_bytes, void *stream);

@@ -37,7 +37,8 @@ EXPORTS = (
     "tsa_status_string", "tsa_last_error", "tsa_version", "tsa_pipeline_kind",
     "tsa2d_validate", "tsa2d_workspace_size", "tsa2d_cluster_size", "tsa2d_segment",
     "tsa2d_histogram", "tsa2d_mean3x3",
-    "tsa_hu_workspace_size", "tsa_hu_segment", "tsa_hu_preprocess",
+    "tsa_hu_workspace_size", "tsa_hu_segment", "tsa_hu_preprocess", "tsa_hu_histogram",
+    "tsa_hu_finish",
     "tsa_morph_workspace_size", "tsa_morph",
 )
 
@@ -150,6 +151,8 @@ def load() -> ctypes.CDLL:
         "tsa_hu_workspace_size": (SZ, [PH]),
         "tsa_hu_segment": (I32, [PH, PO, P, P, SZ, P]),
         "tsa_hu_preprocess": (I32, [PH, P, P, P, SZ, P]),
+        "tsa_hu_histogram": (I32, [PH, P, P, SZ, P]),
+        "tsa_hu_finish": (I32, [PH, P, PO, P, SZ, P]),
         "tsa_morph_workspace_size": (SZ, [I64, I64, I64, I32]),
         "tsa_morph": (I32, [P, P, I64, I64, I64, I32, I32, P, SZ, P]),
     }
@@ -494,6 +497,43 @@ def tsa_hu_segment(vol, k, q, background=-2000, objective="pseudo_additive",
     win = out.get("window")
     _check(load().tsa_hu_segment(ctypes.byref(p), ctypes.byref(o), _ptr(win), _ptr(workspace),
                                  workspace.numel(), _stream(stream)), "tsa_hu_segment")
+    return out
+
+
+def tsa_hu_histogram(vol, k, q, background=-2000, objective="pseudo_additive",
+                     enumeration="canonical", workspace=None, stream=None):
+    """Phase 1 of tsa_hu_segment: HU histograms (kept in `workspace`) and the
+    slab's window [2] = (lo, hi).  Returns (window, workspace)."""
+    _need_cuda(vol)
+    p = make_hu_problem(vol, k, q, background, objective, enumeration)
+    if workspace is None:
+        workspace = tsa_hu_workspace(p, vol.device)
+    win = torch.empty(2, dtype=torch.int32, device=vol.device)
+    _check(load().tsa_hu_histogram(ctypes.byref(p), _ptr(win), _ptr(workspace), workspace.numel(),
+                                   _stream(stream)), "tsa_hu_histogram")
+    return win, workspace
+
+
+def tsa_hu_finish(vol, k, q, window, workspace, background=-2000, objective="pseudo_additive",
+                  enumeration="canonical", labels=True, stream=None):
+    """Phase 2: 8-bit histograms under the given (volume-wide) window, search,
+    finalize, labels.  Returns the dict of tsa_hu_segment (without "window")."""
+    _need_cuda(vol, window, workspace)
+    p = make_hu_problem(vol, k, q, background, objective, enumeration)
+    nz = vol.shape[0]
+    dev = vol.device
+    out = {
+        "thresholds": torch.empty((nz, k), dtype=torch.int32, device=dev),
+        "objective": torch.empty(nz, dtype=torch.float64, device=dev),
+        "histogram": torch.empty((nz, 256), dtype=torch.int32, device=dev),
+        "status": torch.empty(nz, dtype=torch.int32, device=dev),
+        "labels": torch.empty(vol.shape, dtype=torch.uint8, device=dev) if labels else None,
+    }
+    o = tsa_outputs(out["thresholds"].data_ptr(),
+                    out["labels"].data_ptr() if out["labels"] is not None else None,
+                    out["objective"].data_ptr(), out["histogram"].data_ptr(), out["status"].data_ptr())
+    _check(load().tsa_hu_finish(ctypes.byref(p), _ptr(window), ctypes.byref(o), _ptr(workspace),
+                                workspace.numel(), _stream(stream)), "tsa_hu_finish")
     return out
 
 

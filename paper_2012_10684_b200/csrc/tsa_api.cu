@@ -1047,22 +1047,13 @@ static tsa_status hu_window_pass(const tsa_hu_problem *p, const HuWs &w, cudaStr
   return check_cuda("k_hu_window");
 }
 
-tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
-                          void *workspace, size_t workspace_bytes, void *stream) {
-  if (!valid_hu(p)) return set_error(TSA_ERR_INVALID_ARG, "HU problem: dims/alignment/k/q/objective");
-  if (!out || !out->thresholds) return set_error(TSA_ERR_INVALID_ARG, "outputs->thresholds NULL");
-  if (out->labels && (reinterpret_cast<uintptr_t>(out->labels) & 15) != 0)
-    return set_error(TSA_ERR_INVALID_ARG, "labels not 16-byte aligned");
-  if (!workspace) return set_error(TSA_ERR_INVALID_ARG, "workspace NULL");
-  HuWs w;
-  const size_t need = carve_hu(p, reinterpret_cast<char *>(workspace), &w);
-  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
+static tsa_status hu_finish_impl(const tsa_hu_problem *p, const int32_t *win, const tsa_outputs *out,
+                                 const HuWs &w, void *stream) {
   cudaStream_t s = S(stream);
   const int64_t n = p->nx * p->ny;
-  TSA_TRY(hu_window_pass(p, w, s));
   uint32_t *hist8 = out->histogram ? out->histogram : w.hist8;
   TSA_CUDA(cudaMemsetAsync(hist8, 0, sizeof(uint32_t) * p->nz * 256, s));
-  tsa::k_hu_glut<<<tsa::kHuBins / 256, 256, 0, s>>>(w.win, p->background, w.glut);
+  tsa::k_hu_glut<<<tsa::kHuBins / 256, 256, 0, s>>>(win, p->background, w.glut);
   tsa::k_hu_remap<<<dim3(4, (unsigned)p->nz), 256, 0, s>>>(w.hu_hist, w.glut, hist8);
   TSA_TRY(check_cuda("k_hu_remap"));
   TSA_TRY(tsa_search(hist8, w.status, p->nz, n, 256, p->k, p->q, p->objective, p->enumeration, w.units, 0,
@@ -1072,15 +1063,57 @@ tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32
   if (out->labels) {
     const dim3 grid(4, (unsigned)p->nz);  // 4 contiguous chunks per slice
     switch (p->k) {
-      case 1: tsa::k_label_hu<1><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
-      case 2: tsa::k_label_hu<2><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
-      case 3: tsa::k_label_hu<3><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
-      default: tsa::k_label_hu<4><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, w.win, p->background, n, p->k); break;
+      case 1: tsa::k_label_hu<1><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, win, p->background, n, p->k); break;
+      case 2: tsa::k_label_hu<2><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, win, p->background, n, p->k); break;
+      case 3: tsa::k_label_hu<3><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, win, p->background, n, p->k); break;
+      default: tsa::k_label_hu<4><<<grid, 256, 0, s>>>(p->volume, out->labels, out->thresholds, w.status, win, p->background, n, p->k); break;
     }
     TSA_TRY(check_cuda("k_label_hu"));
   }
+  return TSA_OK;
+}
+
+static tsa_status hu_check(const tsa_hu_problem *p, const tsa_outputs *out, void *workspace,
+                           size_t workspace_bytes, HuWs *w) {
+  if (!valid_hu(p)) return set_error(TSA_ERR_INVALID_ARG, "HU problem: dims/alignment/k/q/objective");
+  if (out && !out->thresholds) return set_error(TSA_ERR_INVALID_ARG, "outputs->thresholds NULL");
+  if (out && out->labels && (reinterpret_cast<uintptr_t>(out->labels) & 15) != 0)
+    return set_error(TSA_ERR_INVALID_ARG, "labels not 16-byte aligned");
+  if (!workspace) return set_error(TSA_ERR_INVALID_ARG, "workspace NULL");
+  const size_t need = carve_hu(p, reinterpret_cast<char *>(workspace), w);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "HU workspace too small");
+  return TSA_OK;
+}
+
+tsa_status tsa_hu_segment(const tsa_hu_problem *p, const tsa_outputs *out, int32_t *window,
+                          void *workspace, size_t workspace_bytes, void *stream) {
+  if (!out) return set_error(TSA_ERR_INVALID_ARG, "outputs NULL");
+  HuWs w;
+  TSA_TRY(hu_check(p, out, workspace, workspace_bytes, &w));
+  cudaStream_t s = S(stream);
+  TSA_TRY(hu_window_pass(p, w, s));
+  TSA_TRY(hu_finish_impl(p, w.win, out, w, stream));
   if (window) TSA_CUDA(cudaMemcpyAsync(window, w.win, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   return TSA_OK;
+}
+
+tsa_status tsa_hu_histogram(const tsa_hu_problem *p, int32_t *window_out, void *workspace,
+                            size_t workspace_bytes, void *stream) {
+  if (!window_out) return set_error(TSA_ERR_INVALID_ARG, "window_out NULL");
+  HuWs w;
+  TSA_TRY(hu_check(p, nullptr, workspace, workspace_bytes, &w));
+  cudaStream_t s = S(stream);
+  TSA_TRY(hu_window_pass(p, w, s));
+  TSA_CUDA(cudaMemcpyAsync(window_out, w.win, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  return TSA_OK;
+}
+
+tsa_status tsa_hu_finish(const tsa_hu_problem *p, const int32_t *window_in, const tsa_outputs *out,
+                         void *workspace, size_t workspace_bytes, void *stream) {
+  if (!out || !window_in) return set_error(TSA_ERR_INVALID_ARG, "outputs/window_in NULL");
+  HuWs w;
+  TSA_TRY(hu_check(p, out, workspace, workspace_bytes, &w));
+  return hu_finish_impl(p, window_in, out, w, stream);
 }
 
 tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *window, void *workspace,

@@ -24,8 +24,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (tsa_default_units, tsa_finalize, tsa_histogram, tsa_label, tsa_merge, tsa_search,
-               tsa_segment, ENUMERATIONS)
+from . import (tsa_default_units, tsa_finalize, tsa_histogram, tsa_hu_finish, tsa_hu_histogram,
+               tsa_label, tsa_merge, tsa_search, tsa_segment, ENUMERATIONS)
 
 
 def slab_range(nz: int, world: int, rank: int) -> tuple[int, int]:
@@ -120,3 +120,36 @@ def segment_tuple_sharded(vol_slab, nz_total, bins, k, q, objective="pseudo_addi
         lab = tsa_label(vol_slab, thr[z0:z1].contiguous(), st[z0:z1].contiguous(), bins=bins)
     return {"thresholds": thr, "objective": phi, "status": st, "histogram": hist, "labels": lab,
             "units": U, "unit_range": (u0, u1), "slab": (z0, z1)}
+
+
+INT32_MAX, INT32_MIN = 2**31 - 1, -2**31
+
+
+def reduce_window(win: torch.Tensor, group=None) -> torch.Tensor:
+    """Volume-wide HU window from every rank's slab window (lo, hi): one
+    all-reduce MIN of (lo, -hi) (an all-background slab contributes the
+    neutral (INT32_MAX, INT32_MIN)).  The only exchange of the HU path."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return win
+    t = torch.stack([win[0].to(torch.int64), -win[1].to(torch.int64)])
+    if dist.get_backend(group) == "gloo":  # (CPU tests; NCCL reduces on the device)
+        t = t.cpu()
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return torch.stack([t[0], -t[1]]).to(torch.int32).to(win.device)
+
+
+def hu_segment_slabs(vol_slab, k, q, background=-2000, group=None, **kw):
+    """HU path with slices sharded over ranks (SURVEY.md §8(e) + §8(f) row 2):
+    phase 1 on the own slab, the window all-reduce, phase 2.  Bit-identical
+    to the single-GPU tsa_hu_segment of the whole volume."""
+    dev = vol_slab.device
+    if vol_slab.shape[0] > 0:
+        win, ws = tsa_hu_histogram(vol_slab, k, q, background, **kw)
+    else:  # an empty slab still takes part in the exchange
+        win, ws = torch.tensor([INT32_MAX, INT32_MIN], dtype=torch.int32, device=dev), None
+    wall = reduce_window(win, group)
+    if vol_slab.shape[0] == 0:
+        return {"window": wall}
+    out = tsa_hu_finish(vol_slab, k, q, wall.to(dev).contiguous(), ws, background, **kw)
+    out["window"] = wall
+    return out

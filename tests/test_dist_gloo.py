@@ -121,3 +121,42 @@ def test_tuple_sharded_argmax_matches_single_process(world):
     for z in range(nz):
         ref = oracle.search(hists[z], k, q)
         assert _tuple_of(ret[z], k) == ref["t"]
+
+
+def _win_worker(rank, world, port, wins, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    from paper_2012_10684_b200.dist import reduce_window
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ret[rank] = reduce_window(torch.tensor(wins[rank], dtype=torch.int32)).tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_hu_window_allreduce(world):
+    """The HU path's only exchange: the volume-wide window of the ranks' slab
+    windows (oracle.preprocess on the whole volume is the reference); a slab
+    with only background contributes the neutral (INT32_MAX, INT32_MIN)."""
+    rng = np.random.default_rng(world)
+    vol = rng.integers(-1200, 900, size=(7, 8, 8)).astype(np.int16)
+    vol[rng.random(vol.shape) < 0.3] = -2000
+    bounds = [(r * 7 // world, (r + 1) * 7 // world) for r in range(world)]
+    wins = []
+    for z0, z1 in bounds:
+        nb = vol[z0:z1][vol[z0:z1] != -2000]
+        wins.append([int(nb.min()), int(nb.max())] if nb.size else [2**31 - 1, -2**31])
+    wins[-1] = [2**31 - 1, -2**31]  # pretend the last slab is all background
+    _, lo, hi = oracle.preprocess(vol[: bounds[-1][0]])
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    port = _free_port()
+    ps = [ctx.Process(target=_win_worker, args=(r, world, port, wins, ret)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(60)
+    for r in range(world):
+        assert ret[r] == [lo, hi]

@@ -142,3 +142,68 @@ def test_all_background_volume():
     assert (out["status"].cpu().numpy() == oracle.NO_VALID_SPLIT).all()
     gray, _ = tsa.tsa_hu_preprocess(to_dev(vol))
     assert (gray == 0).all()
+
+
+def test_two_phase_slabs_equal_whole_volume():
+    """Slices split into slabs: phase 1 per slab, the window reduced (min lo,
+    max hi -- what dist.reduce_window all-reduces across ranks), phase 2 per
+    slab: bit-identical to tsa_hu_segment of the whole volume."""
+    vol = to_dev(phantom.make_volume(phantom.CONFIGS["f2"], nz=30, z_first=50))
+    ref = tsa.tsa_hu_segment(vol, 2, 0.8)
+    slabs = [vol[:11], vol[11:12], vol[12:]]
+    ph1 = [tsa.tsa_hu_histogram(s.contiguous(), 2, 0.8) for s in slabs]
+    wins = torch.stack([w for w, _ in ph1]).cpu()
+    win = torch.tensor([int(wins[:, 0].min()), int(wins[:, 1].max())], dtype=torch.int32).to(DEV)
+    outs = [tsa.tsa_hu_finish(s.contiguous(), 2, 0.8, win, ws) for s, (_, ws) in zip(slabs, ph1)]
+    for key in ("thresholds", "objective", "histogram", "status", "labels"):
+        assert torch.equal(torch.cat([o[key] for o in outs]), ref[key]), key
+    assert torch.equal(win, ref["window"])
+
+
+def _hu_worker(rank, world, port, ret):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import phantom as ph
+    from paper_2012_10684_b200.dist import hu_segment_slabs, slab_range
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        vol = ph.make_volume(ph.CONFIGS["f2"], nz=9, z_first=120)
+        z0, z1 = slab_range(9, world, rank)
+        out = hu_segment_slabs(torch.from_numpy(np.ascontiguousarray(vol[z0:z1])).cuda(), 2, 0.8)
+        torch.cuda.synchronize()
+        ret[rank] = {k: v.cpu().numpy() for k, v in out.items() if v is not None}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hu_segment_slabs_two_ranks():
+    """dist.hu_segment_slabs on 2 gloo ranks (both on cuda:0) == one GPU."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    ps = [ctx.Process(target=_hu_worker, args=(r, 2, port, ret)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    vol = phantom.make_volume(phantom.CONFIGS["f2"], nz=9, z_first=120)
+    ref = tsa.tsa_hu_segment(to_dev(vol), 2, 0.8)
+    for key in ("thresholds", "objective", "labels", "histogram"):
+        got = np.concatenate([ret[0][key], ret[1][key]])
+        np.testing.assert_array_equal(got, ref[key].cpu().numpy(), err_msg=key)
+    np.testing.assert_array_equal(ret[0]["window"], ref["window"].cpu().numpy())

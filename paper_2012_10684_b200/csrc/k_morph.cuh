@@ -241,9 +241,4 @@ __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
   }
 }
 
-template <int R>
-__host__ inline size_t morph_smem() {
-  return 0;
-}
-
 }  // namespace tsa

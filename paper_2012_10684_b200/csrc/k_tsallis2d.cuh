@@ -333,7 +333,7 @@ __device__ __forceinline__ int pj(int j) { return j + (j >> 3); }
 // exchange slots read by the other CTAs of the cluster
 struct Xch {
   int flags;           // LEVEL_OVERFLOW seen
-  int nmask;           // unused pad
+  int pad_;
   uint32_t mask[8];    // non-empty f-rows of this CTA's private histogram (L <= 256)
   double score;        // CTA best (score, key) and its two class terms
   uint64_t key;

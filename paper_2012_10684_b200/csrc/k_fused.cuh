@@ -310,6 +310,8 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   st = s_status;
   key = s_key[0];
   int32_t *thr = g.thresholds + (size_t)z * g.k;
+  const int t0 = (int)((key >> (12 * (K - 1))) & 0xFFFull);
+  const int t1 = K > 1 ? (int)(key & 0xFFFull) : L;
   if (st != kOK) {
     if (tid < g.k) thr[tid] = -1;
     if (tid == 0) {
@@ -318,9 +320,18 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
       if (g.status2) g.status2[z] = st;
     }
   } else {
-    const int t0 = (int)((key >> (12 * (K - 1))) & 0xFFFull);
-    const int t1 = K > 1 ? (int)(key & 0xFFFull) : L;
     if (tid < K) thr[tid] = tid == 0 ? t0 : t1;
+    if (tid == 0) {
+      g.status[z] = kOK;
+      if (g.status2) g.status2[z] = kOK;
+    }
+  }
+  __syncthreads();
+  TSA_MPHASE(z, 6)
+  // t* and the status release the slice's labelling now; phi(t*) (only the
+  // host reads it) is computed after the signal, off the labels' critical path
+  if (tid == 0 && g.counters) signal_add(g.counters + 2 + g.nz + z, 1);
+  if (st == kOK) {
     // phi(t*) in the definition's order (k_finalize): p over the canonical list
     if (g.objective) {
       // N = total count (the last prefix count; exact)
@@ -385,14 +396,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
         g.objective[z] = phi;
       }
     }
-    if (tid == 0) {
-      g.status[z] = kOK;
-      if (g.status2) g.status2[z] = kOK;
-    }
   }
-  __syncthreads();
-  TSA_MPHASE(z, 6)
-  if (tid == 0 && g.counters) signal_add(g.counters + 2 + g.nz + z, 1);
 }
 
 // Task index -> (type, slice, chunk).  Queue: LUT tasks, then rounds r:

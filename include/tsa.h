@@ -106,7 +106,7 @@ typedef struct {
    *   slab_slices  fused: slices per pipeline slab; compact: histogram CTAs
    *                per SM (default 4)
    *   label_lag    fused: rounds by which labelling trails the histogram;
-   *                compact: threads of the per-slice kernel (default 256) */
+   *                compact: ignored (the per-slice kernel runs 256 threads) */
   int32_t pipeline;
   int32_t slab_slices;
   int32_t label_lag;

@@ -415,9 +415,8 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     if (p->slab_slices > 0)  // explicit limit: pad shared memory (keeps ~30 KB for k_mid CTAs)
       sh = std::max(sh, (size_t)(196 * 1024) / (size_t)hist_per_sm);
     const size_t sm = smem_m + 64;
-    // the per-slice kernel builds its tables with build_tables (kTableThreads
-    // threads) under __launch_bounds__(256, 3): exactly 256 threads
-    const int mid_threads = tsa::kTableThreads;
+    // the per-slice kernel (its tables need >= kTableThreads threads)
+    const int mid_threads = tsa::kMidThreads;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;

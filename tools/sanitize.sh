@@ -18,6 +18,18 @@ tsa.tsa_segment(v, 256, 4, 1.3, pipeline="staged", enumeration="full")
 tsa.tsa_segment(v, 256, 2, 0.7, objective="sum_plus_product")
 v16 = (v.to(torch.int32) * 13).to(torch.uint16).contiguous()
 tsa.tsa_segment(v16, 4096, 2, 0.8)
+# 2-D cluster kernel (staged and global-load rounds,
+# 256 and 64 levels), HU path, morphology, interval DP
+tsa.tsa2d_segment(v, 256, 0.8, histogram=True)
+tsa.tsa2d_segment((v >> 2).contiguous(), 64, 1.0)
+w = torch.from_numpy(np.random.default_rng(1).integers(0, 256, size=(2, 700, 96)).astype(np.uint8)).cuda()
+tsa.tsa2d_histogram(w, 256)
+h = torch.from_numpy(phantom.make_volume(phantom.CONFIGS["f2"], nz=4, z_first=120)).cuda()
+tsa.tsa_hu_segment(h, 2, 0.8)
+tsa.tsa_hu_preprocess(h)
+tsa.tsa_morph(v[:2].contiguous(), "tophat", 10)
+tsa.tsa_morph(v[:2, :37, :300].contiguous(), "open", 3)
+tsa.tsa_segment(v, 256, 4, 0.8, enumeration="dp")
 torch.cuda.synchronize()
 print("ok")
 PY

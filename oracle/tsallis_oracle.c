@@ -48,6 +48,18 @@
  * histograms (mpmath); exact rationals at q = 2 (fractions); Kapur-Sahoo-Wong
  * closed form at q = 1; point masses; gap phantoms; mirror symmetry; scale
  * invariance; log-domain DP; Level 0 = Level 1 bit-exactly.
+ *
+ * SURVEY.md §8(f) sections at the end of this file, each with its own pins:
+ *   2-D Tsallis (oracle_mean3x3, oracle_hist2d, oracle_phi2d_at,
+ *     oracle_search2d_n): numpy 3x3 mean / bincount, 50-digit brute force,
+ *     diagonal 2-D = 1-D, point masses, transpose symmetry, the distinct-
+ *     partition gap against explicit cell sets     (tests/test_oracle_2d.py)
+ *   pre-processing (oracle_preprocess): the SPEC worked example, an
+ *     independent float formula, exact half ties, invariants
+ *                                                  (tests/test_oracle_preprocess.py)
+ *   morphology (oracle_erode / _dilate / _tophat): numpy padded shifts,
+ *     disk sizes, duality, idempotence, anti-extensivity, monotonicity
+ *                                                  (tests/test_oracle_morph.py)
  */
 #include <math.h>
 #include <stdint.h>

@@ -126,3 +126,75 @@ def test_compute_calls_refuse_cpu_tensors():
 
 def test_key_unpack():
     assert tsa.unpack_key((3 << 36) | (70 << 24) | (71 << 12) | 254, 4) == (3, 70, 71, 254)
+
+
+# ------------------------------------------------ §8(f) entry points (no GPU)
+def _p2(**kw):
+    base = dict(volume=16, nx=512, ny=512, nz=300, bins=256, q=0.8, cluster=0)
+    base.update(kw)
+    return tsa.tsa2d_problem(**base)
+
+
+@pytest.mark.parametrize("kw", [dict(bins=1), dict(bins=257), dict(q=0.0), dict(q=float("nan")),
+                                dict(nx=0), dict(nx=70000, ny=1), dict(volume=0), dict(cluster=3),
+                                dict(cluster=9)])
+def test_2d_invalid_arguments(lib, kw):
+    p = _p2(**kw)
+    assert lib.tsa2d_validate(ctypes.byref(p)) == tsa.TSA_ERR_INVALID_ARG
+    assert lib.tsa2d_workspace_size(ctypes.byref(p)) == 0
+    o = tsa.tsa_outputs(1, 0, 0, 0, 0)
+    assert lib.tsa2d_segment(ctypes.byref(p), ctypes.byref(o), ctypes.c_void_p(1), 1 << 40, None) == 1
+    assert lib.tsa2d_mean3x3(ctypes.byref(p), ctypes.c_void_p(1), None) == 1
+
+
+def test_2d_plan(lib):
+    """Cluster size: the smallest in 4..8 whose CTAs count <= 65535 pixels and
+    whose shared-memory plan fits (5 for a 512x512 slice at 256 levels)."""
+    assert lib.tsa2d_cluster_size(ctypes.byref(_p2())) == 5
+    assert lib.tsa2d_cluster_size(ctypes.byref(_p2(bins=64, nx=64, ny=64))) == 4
+    assert lib.tsa2d_cluster_size(ctypes.byref(_p2(nx=1024, ny=1024))) == 8  # several rounds
+    assert lib.tsa2d_workspace_size(ctypes.byref(_p2())) > 0
+
+
+def _ph(**kw):
+    base = dict(volume=16, nx=512, ny=512, nz=300, background=-2000, k=2, q=0.8, objective=0,
+                enumeration=0)
+    base.update(kw)
+    return tsa.tsa_hu_problem(**base)
+
+
+@pytest.mark.parametrize("kw", [dict(volume=8), dict(nx=7, ny=7), dict(k=5), dict(q=-1.0),
+                                dict(background=5000), dict(objective=3), dict(volume=0)])
+def test_hu_invalid_arguments(lib, kw):
+    p = _ph(**kw)
+    assert lib.tsa_hu_workspace_size(ctypes.byref(p)) == 0
+    o = tsa.tsa_outputs(1, 0, 0, 0, 0)
+    one = ctypes.c_void_p(256)
+    assert lib.tsa_hu_segment(ctypes.byref(p), ctypes.byref(o), None, one, 1 << 40, None) == 1
+    assert lib.tsa_hu_preprocess(ctypes.byref(p), one, None, one, 1 << 40, None) == 1
+    assert lib.tsa_hu_histogram(ctypes.byref(p), one, one, 1 << 40, None) == 1
+
+
+def test_hu_workspace_and_dp_rules(lib):
+    assert lib.tsa_hu_workspace_size(ctypes.byref(_ph())) > 0
+    # the DP needs the pseudo-additive objective and one work unit per slice
+    assert lib.tsa_validate(ctypes.byref(_p(enumeration=2, k=4))) == 0
+    assert lib.tsa_validate(ctypes.byref(_p(enumeration=2, objective=1))) == tsa.TSA_ERR_INVALID_ARG
+    assert lib.tsa_default_units(300, 256, 4, 2) == 1
+
+
+@pytest.mark.parametrize("args", [(0, 1, 8, 8, 1, 10, 3), (16, 16, 8, 8, 1, 10, 3),
+                                  (16, 32, 8, 8, 1, 11, 3), (16, 32, 8, 8, 1, 10, 4),
+                                  (16, 32, 0, 8, 1, 10, 0), (16, 32, 8, 8, 1, -1, 0)])
+def test_morph_invalid_arguments(lib, args):
+    inp, out, nx, ny, nz, r, op = args
+    assert lib.tsa_morph(ctypes.c_void_p(inp) if inp else None, ctypes.c_void_p(out), nx, ny, nz, r,
+                         op, None, 0, None) == tsa.TSA_ERR_INVALID_ARG
+
+
+def test_morph_workspace(lib):
+    assert lib.tsa_morph_workspace_size(512, 512, 300, 3) >= 512 * 512 * 300
+    assert lib.tsa_morph_workspace_size(512, 512, 300, 0) == 0
+    # OPEN / TOPHAT without workspace: reported, nothing launched
+    assert lib.tsa_morph(ctypes.c_void_p(16), ctypes.c_void_p(32), 8, 8, 1, 3, 2, None, 0, None) == \
+        tsa.TSA_ERR_WORKSPACE

@@ -183,27 +183,39 @@ def run_reference(args, cfg, rank, world):
     q = cfg.qs[0]
     vol = phantom.make_volume(cfg)
     threads = oracle.max_threads()
+    if cfg.name == "f2":  # HU input: the pre-processing oracle, then the 1-D oracle
+        def seg(v, bins, k, q_, threads=None):
+            g, _, _ = oracle.preprocess(v)
+            return oracle.segment(g, 256, k, q_, threads=threads)
+        what = "pre-processing + whole 1-D path"
+    elif cfg.name == "f3":  # disk(10) top-hat, brute force
+        def seg(v, bins, k, q_, threads=None):
+            return oracle.tophat(v, cfg.k)
+        what = f"brute-force disk({cfg.k}) opening + top-hat, single-threaded"
+    else:
+        seg = oracle.segment
+        what = "whole path, Level-1 oracle"
     t = time.perf_counter()
-    oracle.segment(vol[:threads], cfg.bins, cfg.k, q, threads=threads)
+    seg(vol[:threads], cfg.bins, cfg.k, q, threads=threads)
     per_slice = (time.perf_counter() - t) / threads
     budget = 120.0
     spp = int(max(1, min(cfg.nz, budget / max(args.steps + args.warmup, 1) / max(per_slice, 1e-6))))
     z = 0
     for _ in range(args.warmup):
-        oracle.segment(vol[z:z + spp], cfg.bins, cfg.k, q, threads=threads)
+        seg(vol[z:z + spp], cfg.bins, cfg.k, q, threads=threads)
     t = time.perf_counter()
     for s in range(args.steps):
         z0 = (s * spp) % max(1, cfg.nz - spp + 1)
-        oracle.segment(vol[z0:z0 + spp], cfg.bins, cfg.k, q, threads=threads)
+        seg(vol[z0:z0 + spp], cfg.bins, cfg.k, q, threads=threads)
     dt = time.perf_counter() - t
     value = spp * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(cfg, args, world),
+        "data": "synthetic", "config": config_for(cfg, args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"{spp} slices of {cfg.name} per step (whole path, Level-1 oracle)"},
+                         "sample": f"{spp} slices of {cfg.name} per step ({what})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -499,7 +511,7 @@ def run_hu(args, cfg, rank, world, dev):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_of(cfg, args, world), input="i16 HU (background -2000)"),
+            "config": config_for(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": 9 * args.steps, "pipeline": "hu-fused (staged search)",
         }
@@ -600,10 +612,7 @@ def run_morph(args, cfg, rank, world, dev):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
-                       "slices_per_gpu": cfg.nz, "radius": r, "op": "white top-hat = in - open(in)",
-                       "parallelism": f"slices sharded, {world} GPU(s), no collective",
-                       "l2": "inputs larger than L2: rotating resident volume copies"},
+            "config": config_for(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": 2 * args.steps, "pipeline": "morph (2 streaming passes)",
         }
@@ -612,6 +621,20 @@ def run_morph(args, cfg, rank, world, dev):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def config_for(cfg, args, world):
+    """The workload's config dict, identical in the GPU arm and the reference arm."""
+    if cfg.name == "f1":
+        return config_of_2d(cfg, world)
+    if cfg.name == "f2":
+        return dict(config_of(cfg, args, world), input="i16 HU (background -2000)")
+    if cfg.name == "f3":
+        return {"workload": f"{cfg.name}: {cfg.note}", "nx": cfg.nx, "ny": cfg.ny,
+                "slices_per_gpu": cfg.nz, "radius": cfg.k, "op": "white top-hat = in - open(in)",
+                "parallelism": f"slices sharded, {world} GPU(s), no collective",
+                "l2": "inputs larger than L2: rotating resident volume copies"}
+    return config_of(cfg, args, world)
 
 
 def config_of(cfg, args, world):

@@ -902,7 +902,7 @@ def main():
             "status": torch.empty(cfg.nz, dtype=torch.int32).pin_memory(),
             "labels": torch.empty(host.shape, dtype=torch.uint8).pin_memory(),
         }
-        slab = 25
+        slab = 50  # slices per host<->device slab (tools/exp_e2e.py)
         hp = tsa.make_problem(host_t, bins, k, q, enumeration=args.enumeration)
         import ctypes
 

@@ -190,8 +190,9 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds,
 
 /* Host-buffer convenience: copies a HOST volume (pinned recommended) to the
  * device in slabs, runs tsa_segment per slab and copies thresholds, objective,
- * status and (if labels_host != NULL) labels back, overlapping copies with
- * compute on two streams.  Device scratch (dev_buf, dev_bytes) comes from the
+ * status and (if labels_host != NULL) labels back: copy-in and compute on
+ * stream0, copy-out on stream1, ordered by events over two device buffers, so
+ * the H2D and D2H copy engines run concurrently.  Device scratch (dev_buf, dev_bytes) comes from the
  * caller: tsa_segment_host_scratch_size() bytes.  Blocks until done. */
 size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab_slices);
 tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slices,

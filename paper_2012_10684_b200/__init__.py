@@ -357,7 +357,7 @@ def tsa_segment_host(vol_host, bins, k, q, objective="pseudo_additive", enumerat
     lib = load()
     p = make_problem(vol_host, bins, k, q, objective, enumeration, units, pipeline)
     nz = vol_host.shape[0]
-    slab = slab or max(1, min(nz, 32))
+    slab = slab or max(1, min(nz, 50))  # measured best on c2 (tools/exp_e2e.py)
     if out is None:
         pin = vol_host.is_pinned()
         out = {

@@ -1214,10 +1214,16 @@ static size_t slab_bytes(const tsa_problem *p, int64_t slab, tsa_problem *sp) {
   Carve c{nullptr};
   c.take<char>(vb);
   c.take<char>(lb);
-  c.take<int32_t>((size_t)slab * p->k);
-  c.take<double>((size_t)slab);
-  c.take<int32_t>((size_t)slab);
   c.take<char>(tsa_workspace_size(sp));
+  return c.off;
+}
+
+// per-volume device arrays of the small outputs (copied to the host once)
+static size_t small_bytes(const tsa_problem *p) {
+  Carve c{nullptr};
+  c.take<int32_t>((size_t)p->nz * p->k);
+  c.take<double>((size_t)p->nz);
+  c.take<int32_t>((size_t)p->nz);
   return c.off;
 }
 
@@ -1225,7 +1231,7 @@ size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab) {
   if (tsa_validate(p) != TSA_OK || slab <= 0) return 0;
   slab = std::min(slab, p->nz);
   tsa_problem sp;
-  return 2 * slab_bytes(p, slab, &sp);
+  return 2 * slab_bytes(p, slab, &sp) + small_bytes(p);
 }
 
 tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, double *obj_h,
@@ -1236,40 +1242,71 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   slab = std::min(slab, p->nz);
   tsa_problem sp;
   const size_t per = slab_bytes(p, slab, &sp);
-  if (dev_bytes < 2 * per) return set_error(TSA_ERR_WORKSPACE, "device scratch too small");
+  if (dev_bytes < 2 * per + small_bytes(p)) return set_error(TSA_ERR_WORKSPACE, "device scratch too small");
   const size_t esz = p->dtype == TSA_U8 ? 1 : 2;
   const int64_t n = p->nx * p->ny;
-  cudaStream_t st[2] = {S(stream0), S(stream1)};
-  for (int64_t z0 = 0, i = 0; z0 < p->nz; z0 += slab, i++) {
+  Carve cs{reinterpret_cast<char *>(dev_buf) + 2 * per};
+  int32_t *thr_all = cs.take<int32_t>((size_t)p->nz * p->k);
+  double *obj_all = cs.take<double>((size_t)p->nz);
+  int32_t *sts_all = cs.take<int32_t>((size_t)p->nz);
+  // stream0: copy-in + compute; stream1: copy-out.  Two device buffers: slab
+  // i+2 may overwrite buffer i%2 once slab i's labels left (ev_free), slab
+  // i's labels leave once it is computed (ev_done) -- so the H2D engine
+  // streams slab i+1 while the D2H engine drains slab i.  Thresholds,
+  // objective and status stay on the device for the whole volume and are
+  // copied once at the end (three small copies instead of three per slab).
+  cudaStream_t cin = S(stream0), cout = S(stream1);
+  cudaEvent_t ev_done[2], ev_free[2];
+  for (int b = 0; b < 2; b++) {
+    TSA_CUDA(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
+    TSA_CUDA(cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming));
+  }
+  tsa_status rc = TSA_OK;
+  for (int64_t z0 = 0, i = 0; z0 < p->nz && rc == TSA_OK; z0 += slab, i++) {
     const int64_t nzs = std::min(slab, p->nz - z0);
     const int b = (int)(i & 1);
     Carve c{reinterpret_cast<char *>(dev_buf) + b * per};
     char *vol = c.take<char>((size_t)slab * n * esz);
     uint8_t *lab = c.take<uint8_t>((size_t)slab * n);
-    int32_t *thr = c.take<int32_t>((size_t)slab * p->k);
-    double *obj = c.take<double>((size_t)slab);
-    int32_t *sts = c.take<int32_t>((size_t)slab);
+    int32_t *thr = thr_all + z0 * p->k;
+    double *obj = obj_all + z0;
+    int32_t *sts = sts_all + z0;
     tsa_problem q = *p;
     q.nz = nzs;
     q.volume = vol;
     char *ws = c.take<char>(0);
     const size_t wsb = tsa_workspace_size(&q);
     const char *src = reinterpret_cast<const char *>(p->volume) + (size_t)z0 * n * esz;
-    TSA_CUDA(cudaMemcpyAsync(vol, src, (size_t)nzs * n * esz, cudaMemcpyHostToDevice, st[b]));
+    if (i >= 2 && cudaStreamWaitEvent(cin, ev_free[b], 0) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "wait ev_free");
+    if (rc == TSA_OK && cudaMemcpyAsync(vol, src, (size_t)nzs * n * esz, cudaMemcpyHostToDevice, cin) != cudaSuccess)
+      rc = set_error(TSA_ERR_CUDA, "H2D");
     tsa_outputs o{thr, lab_h ? lab : nullptr, obj, nullptr, sts};
-    TSA_TRY(tsa_segment(&q, &o, ws, wsb, st[b]));
-    TSA_CUDA(cudaMemcpyAsync(thr_h + z0 * p->k, thr, sizeof(int32_t) * nzs * p->k,
-                             cudaMemcpyDeviceToHost, st[b]));
-    if (obj_h)
-      TSA_CUDA(cudaMemcpyAsync(obj_h + z0, obj, sizeof(double) * nzs, cudaMemcpyDeviceToHost, st[b]));
-    if (st_h)
-      TSA_CUDA(cudaMemcpyAsync(st_h + z0, sts, sizeof(int32_t) * nzs, cudaMemcpyDeviceToHost, st[b]));
-    if (lab_h)
-      TSA_CUDA(cudaMemcpyAsync(lab_h + (size_t)z0 * n, lab, (size_t)nzs * n, cudaMemcpyDeviceToHost,
-                               st[b]));
+    if (rc == TSA_OK) rc = tsa_segment(&q, &o, ws, wsb, cin);
+    if (rc != TSA_OK) break;
+    if (lab_h) {
+      cudaError_t e = cudaEventRecord(ev_done[b], cin);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cout, ev_done[b], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(lab_h + (size_t)z0 * n, lab, (size_t)nzs * n, cudaMemcpyDeviceToHost, cout);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_free[b], cout);
+      if (e != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "D2H labels");
+    }
   }
-  TSA_CUDA(cudaStreamSynchronize(st[0]));
-  TSA_CUDA(cudaStreamSynchronize(st[1]));
+  if (rc == TSA_OK) {
+    cudaError_t e = cudaMemcpyAsync(thr_h, thr_all, sizeof(int32_t) * p->nz * p->k, cudaMemcpyDeviceToHost, cin);
+    if (e == cudaSuccess && obj_h)
+      e = cudaMemcpyAsync(obj_h, obj_all, sizeof(double) * p->nz, cudaMemcpyDeviceToHost, cin);
+    if (e == cudaSuccess && st_h)
+      e = cudaMemcpyAsync(st_h, sts_all, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToHost, cin);
+    if (e != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "D2H results");
+  }
+  const cudaError_t e0 = cudaStreamSynchronize(cin), e1 = cudaStreamSynchronize(cout);
+  for (int b = 0; b < 2; b++) {
+    cudaEventDestroy(ev_done[b]);
+    cudaEventDestroy(ev_free[b]);
+  }
+  if (rc != TSA_OK) return rc;
+  if (e0 != cudaSuccess || e1 != cudaSuccess) return set_error(TSA_ERR_CUDA, "tsa_segment_host synchronize");
   return TSA_OK;
 }
 

@@ -284,9 +284,8 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     }
     __syncthreads();
     TSA_MPHASE(z, 4)
-    // exhaustive search over all C(M-1, K) tuples, tuple-parallel over the CTA
-    search_flat_k12<K, MODE, 12>(t, fsh, g.luts, tBin, M, 0, binom((uint64_t)(M - 1), K), tid,
-                                 blockDim.x, best, key);
+    // exhaustive search over all C(M-1, K) tuples, row chunks over the CTA
+    search_rows_k12<K, MODE, 16>(t, fsh, g.luts, tBin, M, tid, blockDim.x, best, key);
     __syncthreads();  // fsh is reused below
   }
   warp_argmax(best, key);

@@ -577,6 +577,82 @@ __device__ __forceinline__ void search_flat_k12(const SliceTables &t, const doub
   }
 }
 
+// Row-chunked variant of search_flat_k12 for one slice searched by a whole
+// CTA (the compact path's k_mid): the tuples of row b (a = 0..b-1, k = 2) in
+// chunks of CH consecutive a, so no tuple is unranked (no FP64 sqrt) and a
+// thread keeps CH class-term gathers in flight.  Every tuple's value is the
+// same expression as in search_flat_k12, and candidates are compared under
+// the full (score, key) order, so the result is bit-identical.
+template <int K, int MODE, int CH = 16>
+__device__ __forceinline__ void search_rows_k12(const SliceTables &t, const double *Apre, const Luts &l,
+                                                const int32_t *bin, int M, int tid, int nth,
+                                                double &best, uint64_t &bestkey) {
+  const double ident = MODE == SUM ? 0.0 : 1.0;
+  const int P = M - 1;  // positions 0 .. M-2
+  if (K == 1) {
+    for (int b0 = tid * CH; b0 < P; b0 += nth * CH) {
+      double v[CH];
+#pragma unroll
+      for (int u = 0; u < CH; u++) {
+        const int b = min(b0 + u, P - 1);
+        v[u] = combine<MODE>(ident, combine<MODE>(class_term<MODE>(t, l, 0, b), t.Asuf[b]));
+        if (MODE == PROD_MIN) v[u] = -v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < CH; u++) {
+        const int b = b0 + u;
+        if (b < P && v[u] >= best) {
+          const uint64_t key = (uint64_t)bin[b + 1];
+          if (better(v[u], key, best, bestkey)) {
+            best = v[u];
+            bestkey = key;
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int nchunks = [&] {
+    const int n = P - 1, Q = n / CH, Rr = n % CH;  // off(P)
+    return P <= 0 ? 0 : CH * Q * (Q + 1) / 2 + (Q + 1) * Rr;
+  }();
+  for (int c = tid; c < nchunks; c += nth) {
+    // row b: largest b with off(b) <= c (rows 1 .. P-1 hold tuples), where
+    // off(b) = sum_{j<b} ceil(j/CH) = CH Q(Q+1)/2 + (Q+1) R, Q = (b-1)/CH, R = (b-1)%CH
+    auto off = [](int bb) {
+      const int n = bb - 1, Q = n / CH, Rr = n % CH;
+      return bb <= 0 ? 0 : CH * Q * (Q + 1) / 2 + (Q + 1) * Rr;
+    };
+    int lo = 1, hi = P - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off(mid) <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    const int b = lo, a0 = (c - off(b)) * CH;
+    const double R0 = t.Asuf[b];
+    double v[CH];
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int a = min(a0 + u, b - 1);
+      const double R = combine<MODE>(class_term<MODE>(t, l, a + 1, b), R0);
+      v[u] = combine<MODE>(combine<MODE>(ident, Apre[a]), R);
+      if (MODE == PROD_MIN) v[u] = -v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+      const int a = a0 + u;
+      if (a < b && v[u] >= best) {
+        const uint64_t key = ((uint64_t)bin[a + 1] << 12) | (uint64_t)bin[b + 1];
+        if (better(v[u], key, best, bestkey)) {
+          best = v[u];
+          bestkey = key;
+        }
+      }
+    }
+  }
+}
+
 // Staged-path kernel for k <= 2 (not sum-plus-product): CTA (unit, slice)
 // stages the slice tables and Apre in shared memory, then searches its
 // tuple-rank range [T*u/U, T*(u+1)/U) with search_flat_k12.

@@ -19,6 +19,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 namespace tsa {
 
@@ -90,7 +91,7 @@ __device__ __forceinline__ uint32_t pairk(const uint32_t *win) {
 // input row y is processed.
 template <int R>
 struct Acc {
-  uint32_t a[2 * R + 1][2];
+  uint32_t a[2 * R + 2][2];
 };
 
 // The H_w cascade of one input row for the thread's two pixel pairs: hw[w]
@@ -107,12 +108,13 @@ __device__ __forceinline__ void cascade(const uint32_t *win, uint32_t (&h0)[R + 
   if constexpr (W < R) cascade<R, MAX, W + 1>(win, h0, h1);
 }
 
-// Input row y contributes H_{w(R-j)} to the pending output row y-R+j held in
-// slot j, j = 0..2R; output row y-R (slot 0) is then complete: written (if it
-// is one of this CTA's rows) and the slots shift down by one (register moves:
-// a short loop body instead of a (2R+1)-phase unrolled one, which overflowed
-// the instruction cache).
-template <int R, bool MAX, bool TOPHAT>
+// Rows come in pairs (y, y+1); input row y+OFF contributes H_{w(R-j)} to the
+// pending output row y+OFF-R+j held in slot j+OFF, j = 0..2R; output row
+// y+OFF-R (slot OFF) is then complete and written (if it is one of this CTA's
+// rows).  After the pair the slots shift down by two (register moves: a short
+// loop body instead of a (2R+1)-phase unrolled one, which overflowed the
+// instruction cache; pairs halve the moves).
+template <int R, bool MAX, bool TOPHAT, int OFF>
 __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool real, int64_t y,
                                           int64_t ylo, int64_t yhi, const MorphArgs &g, int z,
                                           int64_t xp, bool full) {
@@ -123,13 +125,13 @@ __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool
 #pragma unroll
     for (int j = 0; j <= 2 * R; j++) {
       const int w = halfw<R>(R - j < 0 ? j - R : R - j);
-      acc.a[j][0] = vop<MAX>(acc.a[j][0], h0[w]);
-      acc.a[j][1] = vop<MAX>(acc.a[j][1], h1[w]);
+      acc.a[j + OFF][0] = vop<MAX>(acc.a[j + OFF][0], h0[w]);
+      acc.a[j + OFF][1] = vop<MAX>(acc.a[j + OFF][1], h1[w]);
     }
   }
   const int64_t yo = y - R;
   if (yo >= ylo && yo < yhi && xp < g.nx) {
-    uint32_t a0 = acc.a[0][0], a1 = acc.a[0][1];
+    uint32_t a0 = acc.a[OFF][0], a1 = acc.a[OFF][1];
     const int64_t o = ((size_t)z * g.ny + yo) * g.nx + xp;
     if (TOPHAT) {
       // max(orig - open, 0) per 16-bit lane = max(orig, open) - open
@@ -152,13 +154,18 @@ __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool
         if (xp + e < g.nx) g.dst[o + e] = (uint8_t)((packed >> (8 * e)) & 0xffu);
     }
   }
+}
+
+template <int R, bool MAX>
+__device__ __forceinline__ void shift2(Acc<R> &acc) {
+  constexpr uint32_t NEUT2 = (MAX ? 0u : 255u) * 0x00010001u;
 #pragma unroll
   for (int j = 0; j < 2 * R; j++) {
-    acc.a[j][0] = acc.a[j + 1][0];
-    acc.a[j][1] = acc.a[j + 1][1];
+    acc.a[j][0] = acc.a[j + 2][0];
+    acc.a[j][1] = acc.a[j + 2][1];
   }
-  acc.a[2 * R][0] = NEUT2;
-  acc.a[2 * R][1] = NEUT2;
+  acc.a[2 * R][0] = acc.a[2 * R + 1][0] = NEUT2;
+  acc.a[2 * R][1] = acc.a[2 * R + 1][1] = NEUT2;
 }
 
 // Row y's strip segment (pixels x0-PADL .. x0+kMorphStrip+PADL+3) as u16
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
   const int64_t xp = x0 + 4 * threadIdx.x;
   Acc<R> acc;
 #pragma unroll
-  for (int k = 0; k < NS; k++) acc.a[k][0] = acc.a[k][1] = NEUT2;
+  for (int k = 0; k < NS + 1; k++) acc.a[k][0] = acc.a[k][1] = NEUT2;
   // input rows ylo-R .. yhi+R-1 (outside the slice: no contribution)
   constexpr int WINW = PADL + 3;
   int64_t y = ylo - R;
@@ -223,21 +230,28 @@ __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
     store_row<R>(f0, bufs);
   }
   __syncthreads();
-  for (; y < yend; y++) {
+  auto row = [&](auto off_tag) {
+    constexpr int OFF = decltype(off_tag)::value;
     // the next row's pixels are fetched before this row is computed and
     // stored into the other buffer after it
     RowFetch<R> nf;
     const bool nxt = y + 1 < yend && y + 1 >= 0 && y + 1 < g.ny;
     if (nxt) fetch_row<R, MAX>(src, y + 1, x0, g.nx, nf);
-    const bool real = y >= 0 && y < g.ny;
+    const bool real = y < yend && y >= 0 && y < g.ny;
     uint32_t win[WINW];
     const uint32_t *rb = reinterpret_cast<const uint32_t *>(bufs + cur * 2 * BW) + 2 * threadIdx.x;
 #pragma unroll
     for (int j = 0; j < WINW; j++) win[j] = real ? rb[j] : 0u;
-    morph_row<R, MAX, TOPHAT>(acc, win, real, y, ylo, yhi, g, z, xp, full);
+    morph_row<R, MAX, TOPHAT, OFF>(acc, win, real, y, ylo, yhi, g, z, xp, full);
     if (nxt) store_row<R>(nf, bufs + (cur ^ 1) * 2 * BW);
     __syncthreads();  // the other buffer is complete; this one may be overwritten
     cur ^= 1;
+    y++;
+  };
+  while (y < yend) {
+    row(std::integral_constant<int, 0>{});
+    row(std::integral_constant<int, 1>{});
+    shift2<R, MAX>(acc);
   }
 }
 

@@ -89,9 +89,11 @@ __device__ __forceinline__ uint32_t pairk(const uint32_t *win) {
 // Register accumulators of the 2R+1 pending output rows of a thread's 4
 // columns (two 16-bit-lane words each); slot j holds output row y-R+j while
 // input row y is processed.
+constexpr int kMorphGroup = 2;  // input rows per accumulator shift (4: 124 registers, slower)
+
 template <int R>
 struct Acc {
-  uint32_t a[2 * R + 2][2];
+  uint32_t a[2 * R + kMorphGroup][2];
 };
 
 // The H_w cascade of one input row for the thread's two pixel pairs: hw[w]
@@ -108,12 +110,12 @@ __device__ __forceinline__ void cascade(const uint32_t *win, uint32_t (&h0)[R + 
   if constexpr (W < R) cascade<R, MAX, W + 1>(win, h0, h1);
 }
 
-// Rows come in pairs (y, y+1); input row y+OFF contributes H_{w(R-j)} to the
+// Rows come in groups of kMorphGroup; input row y+OFF contributes H_{w(R-j)} to the
 // pending output row y+OFF-R+j held in slot j+OFF, j = 0..2R; output row
 // y+OFF-R (slot OFF) is then complete and written (if it is one of this CTA's
-// rows).  After the pair the slots shift down by two (register moves: a short
-// loop body instead of a (2R+1)-phase unrolled one, which overflowed the
-// instruction cache; pairs halve the moves).
+// rows).  After the group the slots shift down by kMorphGroup (register moves:
+// a short loop body instead of a (2R+1)-phase unrolled one, which overflowed
+// the instruction cache; groups divide the moves per row).
 template <int R, bool MAX, bool TOPHAT, int OFF>
 __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool real, int64_t y,
                                           int64_t ylo, int64_t yhi, const MorphArgs &g, int z,
@@ -157,15 +159,14 @@ __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool
 }
 
 template <int R, bool MAX>
-__device__ __forceinline__ void shift2(Acc<R> &acc) {
+__device__ __forceinline__ void shiftg(Acc<R> &acc) {
   constexpr uint32_t NEUT2 = (MAX ? 0u : 255u) * 0x00010001u;
+  constexpr int G = kMorphGroup;
 #pragma unroll
-  for (int j = 0; j < 2 * R; j++) {
-    acc.a[j][0] = acc.a[j + 2][0];
-    acc.a[j][1] = acc.a[j + 2][1];
+  for (int j = 0; j < 2 * R + G; j++) {
+    acc.a[j][0] = j + G < 2 * R + G ? acc.a[j + G][0] : NEUT2;
+    acc.a[j][1] = j + G < 2 * R + G ? acc.a[j + G][1] : NEUT2;
   }
-  acc.a[2 * R][0] = acc.a[2 * R + 1][0] = NEUT2;
-  acc.a[2 * R][1] = acc.a[2 * R + 1][1] = NEUT2;
 }
 
 // Row y's strip segment (pixels x0-PADL .. x0+kMorphStrip+PADL+3) as u16
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
   const int64_t xp = x0 + 4 * threadIdx.x;
   Acc<R> acc;
 #pragma unroll
-  for (int k = 0; k < NS + 1; k++) acc.a[k][0] = acc.a[k][1] = NEUT2;
+  for (int k = 0; k < NS + kMorphGroup - 1; k++) acc.a[k][0] = acc.a[k][1] = NEUT2;
   // input rows ylo-R .. yhi+R-1 (outside the slice: no contribution)
   constexpr int WINW = PADL + 3;
   int64_t y = ylo - R;
@@ -251,7 +252,11 @@ __global__ void __launch_bounds__(kMorphThreads) k_morph(MorphArgs g) {
   while (y < yend) {
     row(std::integral_constant<int, 0>{});
     row(std::integral_constant<int, 1>{});
-    shift2<R, MAX>(acc);
+    if constexpr (kMorphGroup == 4) {
+      row(std::integral_constant<int, 2>{});
+      row(std::integral_constant<int, 3>{});
+    }
+    shiftg<R, MAX>(acc);
   }
 }
 

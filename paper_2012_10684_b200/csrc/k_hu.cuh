@@ -83,24 +83,50 @@ __global__ void __launch_bounds__(512) k_hu_hist(HuArgs g) {
   const int bg = g.bg;
   uint32_t nbg = 0;
   int ovf = 0, omn = INT_MAX, omx = INT_MIN;  // out-of-range voxels (window only)
-  // branch-free: every voxel issues one shared reduction; the background
-  // (always inside the bins, checked by the host) and out-of-range voxels add
-  // 0 to a lane-private word of bins 0..63 (HU -4096..-4033: adding 0 changes
-  // nothing and the 32 lanes hit 32 banks), so no predicate splits the warp
+  // every voxel issues one shared reduction; the background (always inside
+  // the bins, checked by the host) and out-of-range voxels add 0 to a
+  // lane-private word of bins 0..63 (HU -4096..-4033: adding 0 changes
+  // nothing and the 32 lanes hit 32 banks), so no predicate splits the warp.
+  // Two voxels per 32-bit word: b = v + 4096 for both lanes in one
+  // VIADD.16x2; the range and background tests are masks (the 16-bit SIMD
+  // compares are emulated on sm_100a).
   const uint32_t lane_addr = sbase + 4u * (threadIdx.x & 31);
-  auto one = [&](int v) {
-    const uint32_t b = (uint32_t)(v + kHuOff);
-    const bool inr = b < (uint32_t)kHuBins, isbg = v == bg;
-    const bool skip = isbg || !inr;
-    nbg += isbg ? 1u : 0u;
-    const uint32_t addr = skip ? lane_addr : sbase + ((b << 1) & 0x3ffcu);
-    const uint32_t inc = skip ? 0u : ((b & 1u) ? 0x10000u : 1u);
+  const uint32_t bg2 = ((uint32_t)(uint16_t)bg) * 0x00010001u;
+  auto red = [&](uint32_t addr, uint32_t inc) {
     asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(addr), "r"(inc) : "memory");
-    if (!inr) {  // rare: LEVEL_OVERFLOW voxel
-      ovf = 1;
-      omn = min(omn, v);
-      omx = max(omx, v);
+  };
+  auto word = [&](uint32_t w) {
+    const uint32_t b2 = __vadd2(w, 0x10001000u);  // both lanes + 4096 (mod 2^16)
+    if (__builtin_expect((b2 & 0xE000E000u) != 0u, 0)) {  // a lane outside [-4096, 4095] (rare)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int v = (int)(int16_t)((w >> (16 * h)) & 0xffffu);
+        const uint32_t b = (b2 >> (16 * h)) & 0xffffu;
+        if (b >= (uint32_t)kHuBins) {
+          ovf = 1;
+          if (v != bg) {
+            omn = min(omn, v);
+            omx = max(omx, v);
+          }
+          red(lane_addr, 0u);
+        } else if (v == bg) {
+          nbg++;
+          red(lane_addr, 0u);
+        } else {
+          red(sbase + ((b << 1) & 0x3ffcu), (b & 1u) ? 0x10000u : 1u);
+        }
+      }
+      return;
     }
+    const uint32_t x = w ^ bg2;
+    const bool bg0 = (x & 0xffffu) == 0u, bg1 = (x >> 16) == 0u;
+    nbg += (bg0 ? 1u : 0u) + (bg1 ? 1u : 0u);
+    const uint32_t a0 = bg0 ? lane_addr : sbase + ((b2 << 1) & 0x3ffcu);
+    const uint32_t i0 = bg0 ? 0u : ((b2 & 1u) ? 0x10000u : 1u);
+    const uint32_t a1 = bg1 ? lane_addr : sbase + ((b2 >> 15) & 0x3ffcu);
+    const uint32_t i1 = bg1 ? 0u : ((b2 & 0x10000u) ? 0x10000u : 1u);
+    red(a0, i0);
+    red(a1, i1);
   };
   constexpr int U = 4;  // 16-byte loads in flight per thread
   for (int64_t i0 = v0 + threadIdx.x; i0 < v1; i0 += (int64_t)U * blockDim.x) {
@@ -113,12 +139,10 @@ __global__ void __launch_bounds__(512) k_hu_hist(HuArgs g) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (i0 + (int64_t)u * blockDim.x >= v1) break;
-      const uint32_t ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        one((int)(int16_t)(ws[e] & 0xffffu));
-        one((int)ws[e] >> 16);
-      }
+      word(wv[u].x);
+      word(wv[u].y);
+      word(wv[u].z);
+      word(wv[u].w);
     }
   }
 #pragma unroll

@@ -245,3 +245,27 @@ def test_cluster_too_small_for_256_levels_is_rejected():
     vol = to_dev(np.zeros((1, 64, 64), np.uint8))
     with pytest.raises(tsa.TsaError):
         tsa.tsa2d_segment(vol, 256, 0.8, cluster=4)
+
+
+def test_segment2d_multiround_full_search():
+    """1024x1024 slices (several counting rounds per CTA, static bands) with the
+    whole search checked against the oracle (64 levels keep it quick)."""
+    vol = phantom.generate(1024, 1024, 2, "u8", seed=phantom.SEED_BASE + 9, z_first=100, z_total=300)
+    vol = (vol >> 2).astype(np.uint8)
+    run_and_check(vol, 64, 0.8)
+
+
+@pytest.mark.parametrize("q", [0.1, 0.3, 3.0, 5.0])
+def test_segment2d_extreme_q(q):
+    rng = np.random.default_rng(int(q * 10))
+    vol = rng.integers(0, 24, size=(3, 48, 64)).astype(np.uint8)
+    vol[1, 10:30, 10:40] = 20
+    run_and_check(vol, 24, q)
+
+
+@pytest.mark.parametrize("L", [2, 3])
+def test_segment2d_minimum_levels(L):
+    rng = np.random.default_rng(L)
+    vol = rng.integers(0, L, size=(4, 16, 32)).astype(np.uint8)
+    vol[3] = 0
+    run_and_check(vol, L, 0.8)

@@ -120,7 +120,6 @@ template <int R, bool MAX, bool TOPHAT, int OFF>
 __device__ __forceinline__ void morph_row(Acc<R> &acc, const uint32_t *win, bool real, int64_t y,
                                           int64_t ylo, int64_t yhi, const MorphArgs &g, int z,
                                           int64_t xp, bool full) {
-  constexpr uint32_t NEUT2 = (MAX ? 0u : 255u) * 0x00010001u;
   if (real) {
     uint32_t h0[R + 1], h1[R + 1];
     cascade<R, MAX, 0>(win, h0, h1);

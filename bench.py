@@ -513,7 +513,9 @@ def run_hu(args, cfg, rank, world, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_for(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": 9 * args.steps, "pipeline": "hu-fused (staged search)",
+            # k_hu_init, k_hu_hist, k_hu_window, k_hu_window_fold, k_hu_glut,
+            # k_hu_remap, k_luts, k_scan, search, k_finalize, k_label_hu
+            "gpu_launches": 11 * args.steps, "pipeline": "hu-fused (staged search)",
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -932,7 +934,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, host, q)
 
-    launches_per_step = {1: 1, 2: 3}.get(kind, 6 + (1 if (k >= 3 and bins <= 512) else 0))
+    # our kernels per step: fused k_fused; compact k_lut_part + k_hist_part +
+    # k_mid + k_label_part; staged k_histogram + k_luts + k_scan [+ k_rtable]
+    # + search + k_finalize + label (the DP has no R table)
+    rtable = k >= 3 and bins <= 512 and args.enumeration != "dp"
+    launches_per_step = {1: 1, 2: 4}.get(kind, 6 + (1 if rtable else 0))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -38,10 +38,10 @@ constexpr size_t kDpTableMax = 64 * 1024;  // term-table bytes (m <= 127; severa
 __host__ __device__ inline size_t dp_table_bytes(int M) { return (size_t)M * (M + 1) / 2 * sizeof(double); }
 
 // One CTA per slice; dynamic shared memory: (k+1) * (L+1) doubles for the
-// suffix values, then (when it fits, M(M+1)/2 <= kDpTableMax / 8) the term
-// table; otherwise terms are evaluated on the fly in the level loops.
+// suffix values, then (when it fits the launch's tab_max <= kDpTableMax bytes)
+// the term table; otherwise terms are evaluated on the fly in the level loops.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_search_dp(SearchArgs g, int k) {
+__global__ void __launch_bounds__(256) k_search_dp(SearchArgs g, int k, size_t tab_max) {
   extern __shared__ double suf[];  // suf[j * (L+1) + a], then the table
   const int z = blockIdx.x;
   const int st = g.status[z];
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) k_search_dp(SearchArgs g, int k) {
   }
   SliceTables t{g.C + (size_t)z * g.E, g.Whi + (size_t)z * g.E, g.Wlo + (size_t)z * g.E, nullptr};
   double *T = suf + (size_t)(k + 1) * S;
-  const bool tab = dp_table_bytes(M) <= kDpTableMax;
+  const bool tab = dp_table_bytes(M) <= tab_max;
   if (tab) {
     const int ntri = M * (M + 1) / 2;
     for (int e = threadIdx.x; e < ntri; e += blockDim.x) {

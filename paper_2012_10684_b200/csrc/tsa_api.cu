@@ -605,22 +605,22 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     a.nz = nz;
     a.E = E;
     a.L = bins;
-    // suffix values + the term table (used by slices whose m fits kDpTableMax)
-    const size_t smem = (size_t)(k + 1) * (bins + 1) * sizeof(double) +
-                        std::min(tsa::dp_table_bytes(bins), tsa::kDpTableMax);
+    // suffix values + the term table (used by slices whose m fits tab_max),
+    // within the 227 KB of opt-in shared memory
+    const size_t sufb = (size_t)(k + 1) * (bins + 1) * sizeof(double);
+    if (sufb > 227 * 1024) return set_error(TSA_ERR_INVALID_ARG, "DP: (k+1)(bins+1) doubles exceed shared memory");
+    const size_t tab_max = std::min({tsa::dp_table_bytes(bins), tsa::kDpTableMax, (size_t)227 * 1024 - sufb});
+    const size_t smem = sufb + tab_max;
+    auto launch_dp = [&](auto kern) -> tsa_status {
+      if (smem > 48 * 1024)
+        TSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)nz, 256, smem, s>>>(a, k, tab_max);
+      return TSA_OK;
+    };
     switch (mode) {
-      case tsa::PROD_MAX: {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::PROD_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tsa::k_search_dp<tsa::PROD_MAX><<<(unsigned)nz, 256, smem, s>>>(a, k);
-      } break;
-      case tsa::PROD_MIN: {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::PROD_MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tsa::k_search_dp<tsa::PROD_MIN><<<(unsigned)nz, 256, smem, s>>>(a, k);
-      } break;
-      default: {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_search_dp<tsa::SUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tsa::k_search_dp<tsa::SUM><<<(unsigned)nz, 256, smem, s>>>(a, k);
-      } break;
+      case tsa::PROD_MAX: TSA_TRY(launch_dp(tsa::k_search_dp<tsa::PROD_MAX>)); break;
+      case tsa::PROD_MIN: TSA_TRY(launch_dp(tsa::k_search_dp<tsa::PROD_MIN>)); break;
+      default: TSA_TRY(launch_dp(tsa::k_search_dp<tsa::SUM>)); break;
     }
     return check_cuda("k_search_dp");
   }

@@ -85,3 +85,19 @@ def test_dp_rejects_sum_plus_product():
     vol = to_dev(np.zeros((1, 16, 16), np.uint8))
     with pytest.raises(tsa.TsaError):
         tsa.tsa_segment(vol, 256, 2, 0.8, objective="sum_plus_product", enumeration="dp")
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_dp_12bit_levels(k):
+    """u16 / 4096 levels (the shared-memory budget leaves the term table to
+    slices with small m; the rest evaluate terms on the fly)."""
+    cfg = phantom.CONFIGS["c5"]
+    vol = phantom.generate(256, 256, 2, "u16", seed=cfg.seed, z_first=400, z_total=1000)
+    check(vol, 4096, k, 0.8) if k == 2 else None
+    out = tsa.tsa_segment(to_dev(vol), 4096, k, 0.8, enumeration="dp")
+    ref = tsa.tsa_segment(to_dev(vol), 4096, k, 0.8)
+    h = ref["histogram"].cpu().numpy().astype(np.uint32)
+    for z in range(2):
+        a, b = tuple(out["thresholds"][z].tolist()), tuple(ref["thresholds"][z].tolist())
+        if a != b:
+            assert oracle.search(h[z], k, 0.8, level=1)["gap"] < REL

@@ -23,3 +23,13 @@ for hp in (2, 3, 4, 5, 6):
     print("hist_per_sm", hp, t(lambda i: tsa.tsa_segment(vols[i % 3], 256, 2, 0.8, out=outs[i % 3], workspace=ws, pipeline="compact", slab_slices=hp)))
 for mt in ():
     print("mid threads", mt, t(lambda i: tsa.tsa_segment(vols[i % 3], 256, 2, 0.8, out=outs[i % 3], workspace=ws, pipeline="compact", label_lag=mt)))
+
+# CUDA-graph replay of the step (one graph per rotating buffer)
+graphs = []
+s = torch.cuda.Stream()
+for i in range(3):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tsa.tsa_segment(vols[i], 256, 2, 0.8, out=outs[i], workspace=ws, stream=s)
+    graphs.append(g)
+print("graph replay   ", t(lambda i: graphs[i % 3].replay()))

@@ -87,7 +87,7 @@ typedef enum { TSA_ENUM_CANONICAL = 0, TSA_ENUM_FULL = 1, TSA_ENUM_DP = 2 } tsa_
 typedef struct {
   const void *volume;   /* [nz][ny][nx] u8 or u16, device */
   int32_t dtype;        /* tsa_dtype */
-  int64_t nx, ny, nz;   /* > 0; nx*ny < 2^31 */
+  int64_t nx, ny, nz;   /* > 0; nx*ny < 2^31; nz <= 65535 */
   int32_t bins;         /* L: 2..256 for u8, 2..4096 for u16 */
   int32_t k;            /* thresholds per slice, 1..4, k <= bins-1 */
   double q;             /* entropic index q (alpha), > 0 and finite; q == 1 is Shannon */
@@ -216,7 +216,7 @@ tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slice
  * TSA_ERR_NO_VALID_SPLIT if no (t,s) has two non-empty classes). */
 typedef struct {
   const void *volume;   /* [nz][ny][nx] u8, device */
-  int64_t nx, ny, nz;   /* > 0; nx <= 65535; nx*ny < 2^31 */
+  int64_t nx, ny, nz;   /* > 0; nx <= 65535; nz <= 65535; nx*ny < 2^31 */
   int32_t bins;         /* L: 2..256 */
   double q;             /* > 0 and finite; q == 1 is Shannon */
   int32_t cluster;      /* CTAs per slice (one thread-block cluster each): 0 = library
@@ -259,7 +259,7 @@ tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream);
  * then the 1-D path on g with 256 bins: thresholds are 8-bit levels, labels
  * #{j : g(v) > t_j}.  The volume is read twice (HU histogram + window pass,
  * label pass); the 8-bit image is never materialised.
- * Requirements: nx*ny % 16 == 0, volume (and labels) 16-byte aligned.  HU
+ * Requirements: nx*ny % 16 == 0, nz <= 65535, volume (and labels) 16-byte aligned.  HU
  * values outside [-4096, 4095] make their slice TSA_ERR_LEVEL_OVERFLOW (they
  * still take part in the window). */
 typedef struct {
@@ -305,7 +305,7 @@ tsa_status tsa_hu_preprocess(const tsa_hu_problem *p, uint8_t *gray, int32_t *wi
  *   DILATE  out = max over the disk, outside = 0
  *   OPEN    out = dilate(erode(in))                    (A o B = (A (-) B) (+) B)
  *   TOPHAT  out = max(in - open(in), 0)                (the chest mask, white top-hat)
- * in / out: [nz][ny][nx] u8, device, may not alias.  radius 0..10 (the paper:
+ * in / out: [nz][ny][nx] u8, device, may not alias; nz <= 65535.  radius 0..10 (the paper:
  * 10).  OPEN and TOPHAT need tsa_morph_workspace_size() bytes (the eroded
  * volume); ERODE / DILATE need none (workspace may be NULL). */
 typedef enum { TSA_MORPH_ERODE = 0, TSA_MORPH_DILATE = 1, TSA_MORPH_OPEN = 2, TSA_MORPH_TOPHAT = 3 } tsa_morph_op;

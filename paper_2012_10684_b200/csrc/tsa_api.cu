@@ -253,6 +253,7 @@ tsa_status tsa_validate(const tsa_problem *p) {
   if (!p->volume) return set_error(TSA_ERR_INVALID_ARG, "volume is NULL");
   if (p->dtype != TSA_U8 && p->dtype != TSA_U16) return set_error(TSA_ERR_INVALID_ARG, "dtype");
   if (p->nx <= 0 || p->ny <= 0 || p->nz <= 0) return set_error(TSA_ERR_INVALID_ARG, "dims must be > 0");
+  if (p->nz > 65535) return set_error(TSA_ERR_INVALID_ARG, "nz > 65535 (one grid row per slice)");
   if (p->nx * p->ny >= (int64_t(1) << 31)) return set_error(TSA_ERR_INVALID_ARG, "slice too large");
   if (p->dtype == TSA_U8 && p->bins > 256) return set_error(TSA_ERR_INVALID_ARG, "bins > 256 with u8");
   if (p->units_per_slice < 0 || p->units_per_slice > 65535)
@@ -793,7 +794,7 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
 }  // extern "C"
 
 static bool valid2d(const tsa2d_problem *p) {
-  return p && p->volume && p->nx > 0 && p->ny > 0 && p->nz > 0 && p->nx <= 65535 &&
+  return p && p->volume && p->nx > 0 && p->ny > 0 && p->nz > 0 && p->nz <= 65535 && p->nx <= 65535 &&
          p->nx * p->ny < (int64_t(1) << 31) && p->bins >= 2 && p->bins <= 256 && p->q > 0.0 &&
          std::isfinite(p->q) && (p->cluster == 0 || (p->cluster >= 4 && p->cluster <= 8));
 }
@@ -980,7 +981,7 @@ tsa_status tsa2d_mean3x3(const tsa2d_problem *p, uint8_t *g, void *stream) {
 
 // ------------------------------------------------------------- HU input
 static bool valid_hu(const tsa_hu_problem *p) {
-  if (!p || !p->volume || p->nx <= 0 || p->ny <= 0 || p->nz <= 0) return false;
+  if (!p || !p->volume || p->nx <= 0 || p->ny <= 0 || p->nz <= 0 || p->nz > 65535) return false;
   const int64_t n = p->nx * p->ny;
   if (n >= (int64_t(1) << 31) || n % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(p->volume) & 15) != 0) return false;
@@ -1171,7 +1172,7 @@ size_t tsa_morph_workspace_size(int64_t nx, int64_t ny, int64_t nz, int32_t op) 
 tsa_status tsa_morph(const uint8_t *in, uint8_t *out, int64_t nx, int64_t ny, int64_t nz,
                      int32_t radius, int32_t op, void *workspace, size_t workspace_bytes,
                      void *stream) {
-  if (!in || !out || in == out || nx <= 0 || ny <= 0 || nz <= 0 || nx * ny >= (int64_t(1) << 31) ||
+  if (!in || !out || in == out || nx <= 0 || ny <= 0 || nz <= 0 || nz > 65535 || nx * ny >= (int64_t(1) << 31) ||
       radius < 0 || radius > tsa::kMorphRmax || op < TSA_MORPH_ERODE || op > TSA_MORPH_TOPHAT)
     return set_error(TSA_ERR_INVALID_ARG, "morph: pointers/dims/radius (0..10)/op");
   cudaStream_t s = S(stream);

@@ -62,7 +62,7 @@ def _p(**kw):
     [dict(q=0.0), dict(q=-1.0), dict(q=float("inf")), dict(q=float("nan")), dict(k=0), dict(k=5),
      dict(bins=1), dict(bins=4097, dtype=2), dict(bins=300, dtype=1), dict(nx=0), dict(nz=-1),
      dict(k=3, bins=3), dict(volume=0), dict(dtype=3), dict(objective=2), dict(enumeration=7),
-     dict(nx=65536, ny=65536)],
+     dict(nx=65536, ny=65536), dict(nz=65536)],
 )
 def test_invalid_arguments_rejected_synchronously(lib, kw):
     p = _p(**kw)

@@ -77,7 +77,7 @@ double binom_d(double n, int r) {
 
 bool valid_search_shape(int64_t nz, int64_t N, int32_t bins, int32_t k, double q,
                         int32_t objective, int32_t enumeration) {
-  if (nz <= 0 || N <= 0 || N >= (int64_t(1) << 31)) return false;
+  if (nz <= 0 || nz > 65535 || N <= 0 || N >= (int64_t(1) << 31)) return false;
   if (bins < 2 || bins > TSA_BINS_MAX) return false;
   if (k < 1 || k > TSA_KMAX || k > bins - 1) return false;
   if (!(q > 0.0) || !std::isfinite(q)) return false;

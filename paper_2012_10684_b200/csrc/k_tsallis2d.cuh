@@ -15,8 +15,9 @@
 //      items, 16-bit-lane SWAR 3x3 box sums, exact floor(v/9) = (7282 v) >> 16,
 //      a register ring keeping 4 rows of loads in flight) and counts (f,g)
 //      codes into a PRIVATE full L x L histogram of 16-bit counters packed two
-//      per word (a CTA counts <= 65535 pixels per round, so no counter can
-//      wrap); uniform items add 16, warp-uniform ones 16 x lanes at once.
+//      per word (a CTA counts <= 65536 pixels per round and takes one back
+//      out, so every counter ends <= 65535); uniform items add 16,
+//      warp-uniform ones 16 x lanes at once.
 //   2. merge over DSMEM: the non-empty f-rows (union of the CTAs' row masks)
 //      are split evenly over the cluster in row order; CTA r sums its rows of
 //      all CL private histograms into compacted u32 rows (several counting
@@ -54,6 +55,7 @@ namespace cg = cooperative_groups;
 
 constexpr int k2dThreads = 256;  // CTA size of the cluster kernel
 constexpr int k2dGroup = k2dThreads / 32;  // rows per walk group (one warp per row)
+constexpr int k2dGroupFallback = 4;  // rows of the fixed walk buffers (when region A's tail is too small)
 constexpr int k2dMaxCL = 8;
 constexpr int kStageChunks = 8;  // bulk copies (mbarriers) staging a CTA's image rows
 
@@ -62,7 +64,7 @@ struct Tsa2dArgs {
   int64_t nx, ny, nz;
   int L, LP;              // bins, even row pitch of the 2-D tables
   int CL, R;              // CTAs per cluster, f-rows per band (R = ceil(L / CL))
-  int rr;                 // image rows per counting round (rr * nx <= 65535)
+  int rr;                 // image rows per counting round (rr * nx <= 65536, one pixel held out)
   int rounds;             // counting rounds (same for every CTA of a cluster)
   int vec;                // 16-pixel SWAR path (nx % 16 == 0, 16-byte aligned slices)
   double q;
@@ -305,9 +307,9 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   s.Hb = o;
   o += al16((size_t)R * PP * 4);
   s.gN = o;
-  o += al16((size_t)k2dGroup * PP * 4);
+  o += al16((size_t)k2dGroupFallback * PP * 4);
   s.gW = o;
-  o += al16((size_t)k2dGroup * PP * 8);
+  o += al16((size_t)k2dGroupFallback * PP * 8);
   s.colN = o;
   o += al16((size_t)LP * 4);
   s.colW = o;
@@ -333,7 +335,7 @@ __device__ __forceinline__ int pj(int j) { return j + (j >> 3); }
 // exchange slots read by the other CTAs of the cluster
 struct Xch {
   int flags;           // LEVEL_OVERFLOW seen
-  int pad_;
+  int extra;           // this round's held-out pixel: f << 16 | g, or -1
   uint32_t mask[8];    // non-empty f-rows of this CTA's private histogram (L <= 256)
   double score;        // CTA best (score, key) and its two class terms
   uint64_t key;
@@ -664,6 +666,29 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     const int64_t ya = min(yb0, ya0 + (int64_t)rd * a.rr), yb = min(yb0, ya + a.rr);
     if (staged) count_round<VEC, CHECK, true, LT>(a, f, sg, ya, yb, hp, ovf);
     else count_round<VEC, CHECK, false, LT>(a, f, sg, ya, yb, hp, ovf);
+    // A round counts up to 65536 pixels, one more than a 16-bit counter holds:
+    // pixel (ya, 0) is taken back out (a modular -1 on the packed word: the
+    // word's sum of increments is exact mod 2^32, so every counter ends
+    // <= 65535 whatever wrapped on the way) and added to the merged band.
+    if (tid == 0) {
+      int e = -1;
+      if (ya < yb) {
+        uint32_t v = 0;
+        for (int dy = -1; dy <= 1; dy++)
+          for (int dx = -1; dx <= 1; dx++) {
+            const int64_t yy = min(max(ya + dy, (int64_t)0), a.ny - 1);
+            const int64_t xx = min(max((int64_t)dx, (int64_t)0), a.nx - 1);
+            v += ldg_u8(f + yy * a.nx + xx);
+          }
+        const uint32_t fv = ldg_u8(f + ya * a.nx), gv = div9(v);
+        if (fv < (uint32_t)L && gv < (uint32_t)L) {
+          add_code(hp, fv, gv, (uint32_t)rw, swz, 0xFFFFFFFFu);
+          atomicOr(&msk[fv >> 5], 1u << (fv & 31));  // its row stays non-empty
+          e = (int)(fv << 16 | gv);
+        }
+      }
+      xch->extra = e;
+    }
     cluster.sync();  // every private histogram of this round complete
     if (single) {
       // own non-empty rows -> mask -> cluster union
@@ -764,6 +789,19 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
         }
       }
     }
+    __syncthreads();
+    if (tid == 0)  // the CTAs' held-out pixels that fall in this band
+      for (int c = 0; c < CL; c++) {
+        const int e = cluster.map_shared_rank(xch, c)->extra;
+        if (e < 0) continue;
+        const int fe = e >> 16, ge = e & 0xffff;
+        if (single) {
+          for (int kk = 0; kk < nst; kk++)
+            if (rla[kk] == fe) Hb[kk * PP + pj(ge)] += 1u;
+        } else if (fe >= row0 && fe < row0 + nrows_static) {
+          Hb[(fe - row0) * PP + pj(ge)] += 1u;
+        }
+      }
     cluster.sync();  // all reads of the private histograms done before reuse
   }
   if (CHECK && ovf) atomicOr(&xch->flags, 1);
@@ -890,12 +928,12 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     int G = (int)((lay.Abytes - a1b) / ((size_t)PP * 12));
     uint32_t *gN;
     double *gW;
-    if (G >= k2dGroup) {
+    if (G >= k2dGroupFallback) {
       G = min(G, nrl);
       gW = reinterpret_cast<double *>(smem + lay.A + a1b);
       gN = reinterpret_cast<uint32_t *>(smem + lay.A + a1b + (size_t)G * PP * 8);
     } else {
-      G = k2dGroup;
+      G = k2dGroupFallback;
       gW = reinterpret_cast<double *>(smem + lay.gW);
       gN = reinterpret_cast<uint32_t *>(smem + lay.gN);
     }

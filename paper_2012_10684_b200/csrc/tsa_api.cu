@@ -809,12 +809,13 @@ struct Plan2d {
 static Plan2d plan2d(const tsa2d_problem *p) {
   Plan2d pl;
   pl.LP = (p->bins + 1) & ~1;
-  // smallest cluster whose CTAs each count <= 65535 pixels in one round
+  // smallest cluster whose CTAs each count <= 65536 pixels in one round (one
+  // is held out, so the 16-bit counters end <= 65535)
   int CL = p->cluster;
   if (CL == 0) {
     CL = 8;
     for (int c = 4; c <= 8; c++)
-      if (((p->ny + c - 1) / c) * p->nx <= 65535) {
+      if (((p->ny + c - 1) / c) * p->nx <= 65536) {
         CL = c;
         break;
       }
@@ -826,7 +827,7 @@ static Plan2d plan2d(const tsa2d_problem *p) {
   pl.CL = CL;
   pl.R = (p->bins + CL - 1) / CL;
   const int64_t rows_max = (p->ny + CL - 1) / CL;
-  pl.rr = (int)std::max<int64_t>(1, std::min<int64_t>(rows_max, 65535 / p->nx));
+  pl.rr = (int)std::max<int64_t>(1, std::min<int64_t>(rows_max, 65536 / p->nx));
   pl.rounds = (int)((rows_max + pl.rr - 1) / pl.rr);
   pl.smem = tsa::smem2d_layout(p->bins, pl.LP, pl.R).total;
   return pl;

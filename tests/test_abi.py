@@ -148,9 +148,10 @@ def test_2d_invalid_arguments(lib, kw):
 
 
 def test_2d_plan(lib):
-    """Cluster size: the smallest in 4..8 whose CTAs count <= 65535 pixels and
-    whose shared-memory plan fits (5 for a 512x512 slice at 256 levels)."""
-    assert lib.tsa2d_cluster_size(ctypes.byref(_p2())) == 5
+    """Cluster size: the smallest in 4..8 whose CTAs count <= 65536 pixels (one
+    held out) and whose shared-memory plan fits (4 for a 512x512 slice)."""
+    assert lib.tsa2d_cluster_size(ctypes.byref(_p2())) == 4
+    assert lib.tsa2d_cluster_size(ctypes.byref(_p2(ny=513))) == 5
     assert lib.tsa2d_cluster_size(ctypes.byref(_p2(bins=64, nx=64, ny=64))) == 4
     assert lib.tsa2d_cluster_size(ctypes.byref(_p2(nx=1024, ny=1024))) == 8  # several rounds
     assert lib.tsa2d_workspace_size(ctypes.byref(_p2())) > 0

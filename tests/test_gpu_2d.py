@@ -85,7 +85,7 @@ def test_mean3x3_bitexact(shape):
 
 
 # ----------------------------------------------------------- 2-D histogram
-@pytest.mark.parametrize("cluster", [0, 5, 6, 7, 8])
+@pytest.mark.parametrize("cluster", [0, 4, 5, 6, 7, 8])
 def test_hist2d_bitexact_phantom(cluster):
     vol = c2_slab(6, 100)
     hist, st = tsa.tsa2d_histogram(to_dev(vol), 256, cluster=cluster)
@@ -182,7 +182,7 @@ def test_segment2d_phantom_full_size_sampled():
         np.testing.assert_array_equal(lab[z], oracle.label(vol[z], 1, (int(thr[z][0]),)))
 
 
-@pytest.mark.parametrize("cluster", [5, 6, 8])
+@pytest.mark.parametrize("cluster", [4, 5, 6, 8])
 def test_segment2d_cluster_sizes_agree(cluster):
     vol = c2_slab(3, 150)
     a = tsa.tsa2d_segment(to_dev(vol), 256, 0.8, cluster=cluster)
@@ -241,10 +241,27 @@ def test_segment2d_small_levels_any_cluster():
                                    rtol=1e-13)
 
 
-def test_cluster_too_small_for_256_levels_is_rejected():
-    vol = to_dev(np.zeros((1, 64, 64), np.uint8))
-    with pytest.raises(tsa.TsaError):
-        tsa.tsa2d_segment(vol, 256, 0.8, cluster=4)
+@pytest.mark.parametrize("bins", [64, 256])
+def test_hist2d_held_out_pixel(bins):
+    """4-CTA clusters on 512x512 count exactly 65536 pixels per CTA and hold one
+    out (pixel (ya, 0) of each round): held-out pixels that are the only one of
+    their row, that are out of range (LEVEL_OVERFLOW), or whose 3x3 mean reads
+    another CTA's rows."""
+    rng = np.random.default_rng(bins)
+    vol = rng.integers(0, bins, size=(3, 512, 512)).astype(np.uint8)
+    vol[0, :, :] = 7
+    for y in (0, 128, 256, 384):
+        vol[0, y, 0] = bins - 1         # the only pixel with that gray level
+        vol[1, y - 1 if y else 0, 0:2] = 0
+    vol[2, 128, 0] = 255                # out of range at bins=64
+    hist, st = tsa.tsa2d_histogram(to_dev(vol), bins, cluster=4)
+    torch.cuda.synchronize()
+    h = hist.cpu().numpy().astype(np.uint32)
+    for z in range(3):
+        ref, st_ref = oracle.hist2d(vol[z], bins)
+        assert st[z].item() == st_ref, z
+        np.testing.assert_array_equal(h[z], ref, err_msg=f"z={z}")
+    run_and_check(vol[:2], bins, 0.8, cluster=4)
 
 
 def test_segment2d_multiround_full_search():

@@ -391,6 +391,76 @@ __global__ void __launch_bounds__(256) l_swar(const uint4 *v, uint4 *out, int64_
   }
 }
 
+
+// (p) pair histogram: one shared atomic per TWO pixels into 65536 packed u16
+// counters H2[a][b] (128 KB), then h[a] += row sum a + column sum a.  A CTA
+// counts <= 65535 pairs, so neither a counter nor a packed column/row sum wraps.
+template <bool FAST>
+__global__ void __launch_bounds__(512) h_pair(const uint4 *v, uint32_t *hist, int64_t nvec_slice, int chunks) {
+  extern __shared__ uint32_t H2[];  // 32768 words
+  __shared__ uint32_t hs[256];
+  const int z = blockIdx.y;
+  for (int i = threadIdx.x; i < 8192; i += 512) reinterpret_cast<uint4 *>(H2)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x < 256) hs[threadIdx.x] = 0;
+  __syncthreads();
+  const uint4 *s = v + z * nvec_slice;
+  const int64_t per = (nvec_slice + chunks - 1) / chunks;
+  const int64_t v0 = per * blockIdx.x, v1 = min(nvec_slice, v0 + per);
+  auto pairs = [&](uint32_t x) {
+    if (FAST && x == (x & 0xffu) * 0x01010101u) {
+      const uint32_t k = (x & 0xffu) * 257u;
+      atomicAdd(H2 + (k >> 1), 2u << ((k & 1u) << 4));
+      return;
+    }
+    const uint32_t k0 = __byte_perm(x, 0, 0x4401), k1 = __byte_perm(x, 0, 0x4423);  // (b0<<8|b1), (b2<<8|b3)
+    atomicAdd(H2 + (k0 >> 1), 1u << ((k0 & 1u) << 4));
+    atomicAdd(H2 + (k1 >> 1), 1u << ((k1 & 1u) << 4));
+  };
+  int64_t i = v0 + threadIdx.x;
+  for (; i + 3 * 512 < v1; i += 4 * 512) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) w[u] = __ldcs(s + i + u * 512);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      pairs(w[u].x);
+      pairs(w[u].y);
+      pairs(w[u].z);
+      pairs(w[u].w);
+    }
+  }
+  for (; i < v1; i += 512) {
+    const uint4 w = s[i];
+    pairs(w.x);
+    pairs(w.y);
+    pairs(w.z);
+    pairs(w.w);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // row sums: warp per row (first byte a)
+  for (int a = warp; a < 256; a += 16) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) t += H2[a * 128 + lane + 32 * j];
+    t = (t & 0xffffu) + (t >> 16);
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) hs[a] = t;
+  }
+  __syncthreads();
+  // column sums: 4 threads per word column (second byte 2w, 2w+1), 64 rows each
+  {
+    const int w = threadIdx.x & 127, a0 = (threadIdx.x >> 7) * 64;
+    uint32_t t = 0;
+#pragma unroll 16
+    for (int a = 0; a < 64; a++) t += H2[(a0 + a) * 128 + w];
+    atomicAdd(&hs[2 * w], t & 0xffffu);
+    atomicAdd(&hs[2 * w + 1], t >> 16);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256 && hs[threadIdx.x]) atomicAdd(hist + z * 256 + threadIdx.x, hs[threadIdx.x]);
+}
+
 __global__ void flush_l2(uint4 *buf, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     buf[i] = make_uint4(i, 0, 0, 0);
@@ -511,6 +581,18 @@ int main(int argc, char **argv) {
     runl(h_lane<4, 4>, 4, 6, "lane_w4_u4_g6x(2waves)");
   }
 
+  {
+    const size_t smem = 131072;
+    cudaFuncSetAttribute(h_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(h_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int chunks : {3, 4, 6, 8}) {
+      char nm[64];
+      snprintf(nm, 64, "pair_fast_c%d", chunks);
+      timeit(nm, [&] { h_pair<true><<<dim3(chunks, nz), 512, smem>>>((const uint4 *)d, hist, nvs, chunks); }, total, true);
+      snprintf(nm, 64, "pair_nofast_c%d", chunks);
+      timeit(nm, [&] { h_pair<false><<<dim3(chunks, nz), 512, smem>>>((const uint4 *)d, hist, nvs, chunks); }, total, true);
+    }
+  }
   timeit("prednz_c4", [&] { h_prednz<4><<<dim3(4, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);
   timeit("prednz_c8", [&] { h_prednz<8><<<dim3(8, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);
   timeit("redall_c4", [&] { h_redall<4><<<dim3(4, nz), 512>>>((const uint4 *)d, hist, nvs); }, total, true);

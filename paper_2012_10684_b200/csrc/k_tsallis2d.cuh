@@ -15,9 +15,8 @@
 //      items, 16-bit-lane SWAR 3x3 box sums, exact floor(v/9) = (7282 v) >> 16,
 //      a register ring keeping 4 rows of loads in flight) and counts (f,g)
 //      codes into a PRIVATE full L x L histogram of 16-bit counters packed two
-//      per word (a CTA counts <= 65536 pixels per round and takes one back
-//      out, so every counter ends <= 65535); uniform items add 16,
-//      warp-uniform ones 16 x lanes at once.
+//      per word (a CTA counts <= 65535 pixels per round, so no counter can
+//      wrap); uniform items add 16, warp-uniform ones 16 x lanes at once.
 //   2. merge over DSMEM: the non-empty f-rows (union of the CTAs' row masks)
 //      are split evenly over the cluster in row order; CTA r sums its rows of
 //      all CL private histograms into compacted u32 rows (several counting
@@ -55,7 +54,6 @@ namespace cg = cooperative_groups;
 
 constexpr int k2dThreads = 256;  // CTA size of the cluster kernel
 constexpr int k2dGroup = k2dThreads / 32;  // rows per walk group (one warp per row)
-constexpr int k2dGroupFallback = 4;  // rows of the fixed walk buffers (when region A's tail is too small)
 constexpr int k2dMaxCL = 8;
 constexpr int kStageChunks = 8;  // bulk copies (mbarriers) staging a CTA's image rows
 
@@ -64,7 +62,7 @@ struct Tsa2dArgs {
   int64_t nx, ny, nz;
   int L, LP;              // bins, even row pitch of the 2-D tables
   int CL, R;              // CTAs per cluster, f-rows per band (R = ceil(L / CL))
-  int rr;                 // image rows per counting round (rr * nx <= 65536, one pixel held out)
+  int rr;                 // image rows per counting round (rr * nx <= 65535; one round: <= 65536)
   int rounds;             // counting rounds (same for every CTA of a cluster)
   int vec;                // 16-pixel SWAR path (nx % 16 == 0, 16-byte aligned slices)
   double q;
@@ -275,16 +273,18 @@ __device__ __forceinline__ double score2d(double t1, double t2) {
 
 // -------------------------------------------------------------- the kernel
 // Shared-memory layout (bytes, every offset 16-aligned).  Band-row tables use
-// the padded pitch PP = LP + LP/8 with column j at j + j/8, so a lane reading
-// 8 contiguous columns and a thread reading column s are both (nearly)
-// bank-conflict free.
+// the pitch PP = LP rounded up to 8 with column j at j ^ ((j >> 5) & 7) (an
+// XOR swizzle inside each aligned 8-column group), so a lane reading 8
+// contiguous columns and a thread reading column s are both bank-conflict
+// free, without the 12.5 % of a padded pitch.
 //   A      max(L*LP*2, R*LP*8): private u16 histogram; later A_1 / S_1 [nrl][LP]
 //          f64 and, in the tail, walk buffers for as many rows as fit
 //   Hb     R*PP*4              merged u32 rows of the band (compacted)
 //   gN     G*PP*4, gW G*PP*8   fallback walk buffers (G = 8 rows)
 //   colN   LP*4, colW LP*8     band column sums (read by the other CTAs)
 //   rla    R*4, rlh R*4        absolute f-row / Hb row of each non-empty band row
-//   msk    L/32 words          non-empty f-rows (own private histogram, then all)
+//   msk    16 words            non-empty f-rows (own private histogram, then all);
+//                              words 8.. the cluster's wrapped cells (Xch::extra)
 //   xch    128                 exchange slots (flags, mask, argmax + payload)
 //   bar    64                  mbarriers of the staged image rows
 //   scr    1024                scan scratch
@@ -294,7 +294,7 @@ struct Smem2d {
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline int pitch2d(int LP) { return LP + (LP + 7) / 8; }
+__host__ __device__ inline int pitch2d(int LP) { return (LP + 7) & ~7; }
 
 __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   Smem2d s;
@@ -307,9 +307,9 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   s.Hb = o;
   o += al16((size_t)R * PP * 4);
   s.gN = o;
-  o += al16((size_t)k2dGroupFallback * PP * 4);
+  o += al16((size_t)k2dGroup * PP * 4);
   s.gW = o;
-  o += al16((size_t)k2dGroupFallback * PP * 8);
+  o += al16((size_t)k2dGroup * PP * 8);
   s.colN = o;
   o += al16((size_t)LP * 4);
   s.colW = o;
@@ -330,12 +330,12 @@ __host__ __device__ inline Smem2d smem2d_layout(int L, int LP, int R) {
   return s;
 }
 
-__device__ __forceinline__ int pj(int j) { return j + (j >> 3); }
+__device__ __forceinline__ int pj(int j) { return j ^ ((j >> 5) & 7); }
 
 // exchange slots read by the other CTAs of the cluster
 struct Xch {
   int flags;           // LEVEL_OVERFLOW seen
-  int extra;           // this round's held-out pixel: f << 16 | g, or -1
+  int extra;           // single round: f << 16 | g if all 65536 pixels fell in that cell, else -1
   uint32_t mask[8];    // non-empty f-rows of this CTA's private histogram (L <= 256)
   double score;        // CTA best (score, key) and its two class terms
   uint64_t key;
@@ -573,6 +573,54 @@ __device__ __forceinline__ void count_round(const Tsa2dArgs &a, const uint8_t *f
   }
 }
 
+// Single round of 65536 pixels (kept out of line: rarely taken, and inlined
+// it costs the kernel registers).  Only a cell holding all 65536 pixels can
+// wrap its 16-bit counter, and then it is the cell of pixel (ya, 0): counted,
+// yet reading 0.  The word is cleared (a low-half wrap carried into the other
+// half), the f-row kept in the mask; returns f << 16 | g, else -1.
+__device__ __noinline__ int wrap_check(const uint8_t *f, int64_t nx, int64_t ny, int64_t ya,
+                                       const uint8_t *buf, uint64_t *bar, int64_t Y0,
+                                       uint32_t *hp, int L, int rw, bool swz, uint32_t *msk) {
+  // the rows are in the CTA's region, whose chunks have all landed (the
+  // waits complete at once; no 64-bit index division on this path)
+  if (buf)
+    for (int c = 0; c < kStageChunks; c++) mbar_wait(bar + c, 0);
+  const int64_t y0 = max(ya - 1, (int64_t)0), y2 = min(ya + 1, ny - 1), x1 = min((int64_t)1, nx - 1);
+  const int64_t rows[3] = {y0, ya, y2}, cols[3] = {0, 0, x1};
+  uint32_t px[9];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+      px[i * 3 + j] = buf ? (uint32_t)buf[(rows[i] - Y0) * nx + cols[j]] : ldg_u8(f + rows[i] * nx + cols[j]);
+  uint32_t v = 0;
+#pragma unroll
+  for (int j = 0; j < 9; j++) v += px[j];
+  const uint32_t fv = px[4];
+  const uint32_t gv = div9(v);
+  if (fv >= (uint32_t)L || gv >= (uint32_t)L) return -1;
+  uint32_t *wp = hp + (rw == 128 ? cell_word256(fv, gv) : cell_word(fv, gv, (uint32_t)rw, swz));
+  if (((*wp >> ((gv & 1u) << 4)) & 0xffffu) != 0u) return -1;
+  *wp = 0u;
+  atomicOr(&msk[fv >> 5], 1u << (fv & 31));
+  return (int)(fv << 16 | gv);
+}
+
+// adds the 65536 pixels of a wrapped cell e to this CTA's band if its row is
+// one of the band's compacted rows (the band = union ranks [k0, k1))
+__device__ __noinline__ void wrap_add(uint32_t *Hb, const uint32_t *msk, int e, int r, int CL, int NW,
+                                      int PP) {
+  const int fe = e >> 16, ge = e & 0xffff;
+  int mf = 0, rank = __popc(msk[fe >> 5] & ((1u << (fe & 31)) - 1u));
+  for (int w = 0; w < NW; w++) {
+    const int pc = __popc(msk[w]);
+    mf += pc;
+    if (w < (fe >> 5)) rank += pc;
+  }
+  const int k0 = r * mf / CL, k1 = (r + 1) * mf / CL;
+  if (rank >= k0 && rank < k1) atomicAdd(&Hb[(rank - k0) * PP + pj(ge)], 65536u);
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -598,7 +646,7 @@ __device__ __forceinline__ void warp_argmax4(double &s, uint64_t &k, double &t1,
 }
 
 // LT = 256: the paper's 8-bit case with every table dimension a compile-time
-// constant (L = LP = 256, PP = 288, 8 columns per lane); LT = 0: any L.
+// constant (L = LP = PP = 256, 8 columns per lane); LT = 0: any L.
 template <int MODE, bool VEC, bool CHECK, int LT>
 __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   extern __shared__ __align__(16) char smem[];
@@ -607,7 +655,7 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   const int64_t z = blockIdx.x / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = LT ? LT : a.L, LP = LT ? LT : a.LP, R = a.R;
-  const int PP = LT ? LT + LT / 8 : pitch2d(LP);
+  const int PP = LT ? LT : pitch2d(LP);
   const int NW = (L + 31) / 32;  // mask words
   const Smem2d lay = smem2d_layout(L, LP, R);
   uint32_t *hp = reinterpret_cast<uint32_t *>(smem + lay.A);  // packed u16 private histogram
@@ -634,6 +682,8 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
   int ovf = 0;
   int nst = 0;  // Hb rows in use
   const int64_t ya0 = (int64_t)r * a.ny / CL, yb0 = (int64_t)(r + 1) * a.ny / CL;
+  // a CTA of the cluster may count 65536 pixels in its single round (cluster-uniform)
+  const bool wrap_possible = a.rounds == 1 && (a.ny + CL - 1) / CL * a.nx == 65536;
   const int hw = L * LP / 2;  // words of the private histogram
   const int rw = LP / 2;      // words per private-histogram row
   const bool swz = (rw & 31) == 0;  // cell_word's chunk swizzle
@@ -666,29 +716,6 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     const int64_t ya = min(yb0, ya0 + (int64_t)rd * a.rr), yb = min(yb0, ya + a.rr);
     if (staged) count_round<VEC, CHECK, true, LT>(a, f, sg, ya, yb, hp, ovf);
     else count_round<VEC, CHECK, false, LT>(a, f, sg, ya, yb, hp, ovf);
-    // A round counts up to 65536 pixels, one more than a 16-bit counter holds:
-    // pixel (ya, 0) is taken back out (a modular -1 on the packed word: the
-    // word's sum of increments is exact mod 2^32, so every counter ends
-    // <= 65535 whatever wrapped on the way) and added to the merged band.
-    if (tid == 0) {
-      int e = -1;
-      if (ya < yb) {
-        uint32_t v = 0;
-        for (int dy = -1; dy <= 1; dy++)
-          for (int dx = -1; dx <= 1; dx++) {
-            const int64_t yy = min(max(ya + dy, (int64_t)0), a.ny - 1);
-            const int64_t xx = min(max((int64_t)dx, (int64_t)0), a.nx - 1);
-            v += ldg_u8(f + yy * a.nx + xx);
-          }
-        const uint32_t fv = ldg_u8(f + ya * a.nx), gv = div9(v);
-        if (fv < (uint32_t)L && gv < (uint32_t)L) {
-          add_code(hp, fv, gv, (uint32_t)rw, swz, 0xFFFFFFFFu);
-          atomicOr(&msk[fv >> 5], 1u << (fv & 31));  // its row stays non-empty
-          e = (int)(fv << 16 | gv);
-        }
-      }
-      xch->extra = e;
-    }
     cluster.sync();  // every private histogram of this round complete
     if (single) {
       // own non-empty rows -> mask -> cluster union
@@ -712,6 +739,22 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
         }
       }
       __syncthreads();
+      if (wrap_possible) {
+        // A single round may count 65536 pixels (one more than a 16-bit
+        // counter holds); only a cell holding all of them can wrap, leaving
+        // at most one non-empty row.  Then wrap_check clears the word, keeps
+        // the row in the mask and publishes the cell; its band owner adds 65536.
+        if (tid == 0) {
+          int e = -1;
+          if ((yb - ya) * a.nx == 65536) {
+            int pc = 0;
+            for (int w = 0; w < NW; w++) pc += __popc(msk[w]);
+            if (pc <= 1) e = wrap_check(f, a.nx, a.ny, ya, staged ? sg.buf : nullptr, sg.bar, sg.Y0, hp, L, rw, swz, msk);
+          }
+          xch->extra = e;
+        }
+        __syncthreads();
+      }
       if (tid < 8) xch->mask[tid] = msk[tid];
       cluster.sync();
       if (tid < NW) {
@@ -719,6 +762,7 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
         for (int c = 0; c < CL; c++) m |= cluster.map_shared_rank(xch, c)->mask[tid];
         msk[tid] = m;
       }
+      if (wrap_possible && tid < CL) msk[8 + tid] = (uint32_t)cluster.map_shared_rank(xch, tid)->extra;
       __syncthreads();
       int mf = 0, below = 0;
       for (int w = 0; w < NW; w++) {
@@ -789,19 +833,14 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
         }
       }
     }
-    __syncthreads();
-    if (tid == 0)  // the CTAs' held-out pixels that fall in this band
-      for (int c = 0; c < CL; c++) {
-        const int e = cluster.map_shared_rank(xch, c)->extra;
-        if (e < 0) continue;
-        const int fe = e >> 16, ge = e & 0xffff;
-        if (single) {
-          for (int kk = 0; kk < nst; kk++)
-            if (rla[kk] == fe) Hb[kk * PP + pj(ge)] += 1u;
-        } else if (fe >= row0 && fe < row0 + nrows_static) {
-          Hb[(fe - row0) * PP + pj(ge)] += 1u;
-        }
+    if (single && wrap_possible) {
+      bool wrapped = false;
+      for (int c = 0; c < CL; c++) wrapped |= (int)msk[8 + c] >= 0;
+      if (wrapped) {  // rare: a CTA's whole round in one cell
+        __syncthreads();
+        if (tid < CL && (int)msk[8 + tid] >= 0) wrap_add(Hb, msk, (int)msk[8 + tid], r, CL, NW, PP);
       }
+    }
     cluster.sync();  // all reads of the private histograms done before reuse
   }
   if (CHECK && ovf) atomicOr(&xch->flags, 1);
@@ -928,12 +967,12 @@ __global__ void __launch_bounds__(k2dThreads, 1) k_tsallis2d(Tsa2dArgs a) {
     int G = (int)((lay.Abytes - a1b) / ((size_t)PP * 12));
     uint32_t *gN;
     double *gW;
-    if (G >= k2dGroupFallback) {
+    if (G >= k2dGroup) {
       G = min(G, nrl);
       gW = reinterpret_cast<double *>(smem + lay.A + a1b);
       gN = reinterpret_cast<uint32_t *>(smem + lay.A + a1b + (size_t)G * PP * 8);
     } else {
-      G = k2dGroupFallback;
+      G = k2dGroup;
       gW = reinterpret_cast<double *>(smem + lay.gW);
       gN = reinterpret_cast<uint32_t *>(smem + lay.gN);
     }

@@ -809,8 +809,8 @@ struct Plan2d {
 static Plan2d plan2d(const tsa2d_problem *p) {
   Plan2d pl;
   pl.LP = (p->bins + 1) & ~1;
-  // smallest cluster whose CTAs each count <= 65536 pixels in one round (one
-  // is held out, so the 16-bit counters end <= 65535)
+  // smallest cluster whose CTAs each count <= 65536 pixels in one round (a
+  // single round of exactly 65536 handles the one counter that can wrap)
   int CL = p->cluster;
   if (CL == 0) {
     CL = 8;
@@ -827,7 +827,7 @@ static Plan2d plan2d(const tsa2d_problem *p) {
   pl.CL = CL;
   pl.R = (p->bins + CL - 1) / CL;
   const int64_t rows_max = (p->ny + CL - 1) / CL;
-  pl.rr = (int)std::max<int64_t>(1, std::min<int64_t>(rows_max, 65536 / p->nx));
+  pl.rr = rows_max * p->nx <= 65536 ? (int)rows_max : (int)std::max<int64_t>(1, 65535 / p->nx);
   pl.rounds = (int)((rows_max + pl.rr - 1) / pl.rr);
   pl.smem = tsa::smem2d_layout(p->bins, pl.LP, pl.R).total;
   return pl;

@@ -242,26 +242,29 @@ def test_segment2d_small_levels_any_cluster():
 
 
 @pytest.mark.parametrize("bins", [64, 256])
-def test_hist2d_held_out_pixel(bins):
-    """4-CTA clusters on 512x512 count exactly 65536 pixels per CTA and hold one
-    out (pixel (ya, 0) of each round): held-out pixels that are the only one of
-    their row, that are out of range (LEVEL_OVERFLOW), or whose 3x3 mean reads
-    another CTA's rows."""
+def test_hist2d_65536_pixel_rounds(bins):
+    """4-CTA clusters on 512x512 count exactly 65536 pixels per CTA in one
+    round: a CTA whose whole band falls in one cell wraps its 16-bit counter
+    (low half: the carry lands in the neighbour cell; high half: lost) and is
+    repaired at the merge; near misses (one pixel off, out-of-range pixels)
+    must not be taken for a wrap."""
     rng = np.random.default_rng(bins)
-    vol = rng.integers(0, bins, size=(3, 512, 512)).astype(np.uint8)
-    vol[0, :, :] = 7
-    for y in (0, 128, 256, 384):
-        vol[0, y, 0] = bins - 1         # the only pixel with that gray level
-        vol[1, y - 1 if y else 0, 0:2] = 0
-    vol[2, 128, 0] = 255                # out of range at bins=64
+    vol = rng.integers(0, bins, size=(5, 512, 512)).astype(np.uint8)
+    vol[0, :129] = 40                   # CTA 0 uniform, even cell (low half)
+    vol[1, 127:257] = 41                # CTA 1 uniform (its 3x3 halo too), odd cell
+    vol[2, :] = 7
+    vol[2, 300, 5] = 9                  # CTA 2 one pixel off uniform, the rest uniform
+    vol[3, :129] = 40
+    vol[3, 0, 0] = 255                  # pixel (0, 0) out of range at 64 levels
+    vol[4, 128:, :] = 63                # CTAs 1-3 uniform, one cell across bands
     hist, st = tsa.tsa2d_histogram(to_dev(vol), bins, cluster=4)
     torch.cuda.synchronize()
     h = hist.cpu().numpy().astype(np.uint32)
-    for z in range(3):
+    for z in range(vol.shape[0]):
         ref, st_ref = oracle.hist2d(vol[z], bins)
         assert st[z].item() == st_ref, z
         np.testing.assert_array_equal(h[z], ref, err_msg=f"z={z}")
-    run_and_check(vol[:2], bins, 0.8, cluster=4)
+    run_and_check(vol[[0, 1, 4]], bins, 0.8, cluster=4)
 
 
 def test_segment2d_multiround_full_search():

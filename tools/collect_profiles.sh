@@ -27,4 +27,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file
     python bench.py --workload c4 --enumeration dp --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_search_dp" -s 1 -c 1 \
     -o $OUT/prof_c4dp python bench.py --workload c4 --enumeration dp --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_c4dp.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file $OUT/launches_f1.csv \
+    python bench.py --workload f1 --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_tsallis2d" -s 3 -c 1 \
+    -o $OUT/prof_f1 python bench.py --workload f1 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_f1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_morph" -s 4 -c 2 \
+    -o $OUT/prof_f3 python bench.py --workload f3 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_f3.log 2>&1
 ls -la $OUT

@@ -267,6 +267,26 @@ def test_hist2d_65536_pixel_rounds(bins):
     run_and_check(vol[[0, 1, 4]], bins, 0.8, cluster=4)
 
 
+@pytest.mark.parametrize("shape", [(256, 1024), (1024, 256), (128, 512)])
+def test_hist2d_65536_pixel_rounds_other_shapes(shape):
+    """Other shapes whose 4-CTA bands hold exactly 65536 pixels (ny x nx with
+    ceil(ny/4) * nx = 65536), with uniform bands in even and odd cells; (128,
+    512) is below the bound (no band reaches 65536)."""
+    ny, nx = shape
+    rng = np.random.default_rng(ny + nx)
+    vol = rng.integers(0, 256, size=(2, ny, nx)).astype(np.uint8)
+    q = (ny + 3) // 4
+    vol[0, : q + 1] = 122
+    vol[1, q - 1: 2 * q + 1] = 33
+    hist, st = tsa.tsa2d_histogram(to_dev(vol), 256, cluster=4)
+    torch.cuda.synchronize()
+    h = hist.cpu().numpy().astype(np.uint32)
+    for z in range(2):
+        ref, st_ref = oracle.hist2d(vol[z], 256)
+        assert st[z].item() == st_ref
+        np.testing.assert_array_equal(h[z], ref, err_msg=f"{shape} z={z}")
+
+
 def test_segment2d_multiround_full_search():
     """1024x1024 slices (several counting rounds per CTA, static bands) with the
     whole search checked against the oracle (64 levels keep it quick)."""

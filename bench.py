@@ -514,8 +514,9 @@ def run_hu(args, cfg, rank, world, dev):
             "config": config_for(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             # k_hu_init, k_hu_hist, k_hu_window, k_hu_window_fold, k_hu_glut,
-            # k_hu_remap, k_luts, k_scan, search, k_finalize, k_label_hu
-            "gpu_launches": 11 * args.steps, "pipeline": "hu-fused (staged search)",
+            # k_hu_remap, k_lut_part, k_mid (per-slice search), k_label_hu
+            "gpu_launches": (9 if cfg.k <= 2 else 11) * args.steps,
+            "pipeline": "hu-fused (per-slice search kernel)" if cfg.k <= 2 else "hu-fused (staged search)",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -999,6 +999,7 @@ struct HuWs {
   char *search;
   size_t search_bytes;
   int32_t units;
+  double *luts;  // [2][n + 1]: 1/n^q (or ln n, 1/n) for the per-slice search kernel
 };
 
 static size_t carve_hu(const tsa_hu_problem *p, char *base, HuWs *o) {
@@ -1015,6 +1016,7 @@ static size_t carve_hu(const tsa_hu_problem *p, char *base, HuWs *o) {
   w.pk = c.take<uint64_t>((size_t)w.units * p->nz);
   w.search_bytes = tsa_search_workspace_size(p->nz, n, 256, p->k, p->q, p->objective, p->enumeration);
   w.search = c.take<char>(w.search_bytes);
+  w.luts = c.take<double>(2 * ((size_t)n + 1));
   if (o) *o = w;
   return c.off;
 }
@@ -1059,10 +1061,54 @@ static tsa_status hu_finish_impl(const tsa_hu_problem *p, const int32_t *win, co
   tsa::k_hu_glut<<<tsa::kHuBins / 256, 256, 0, s>>>(win, p->background, w.glut);
   tsa::k_hu_remap<<<dim3(4, (unsigned)p->nz), 256, 0, s>>>(w.hu_hist, w.glut, hist8);
   TSA_TRY(check_cuda("k_hu_remap"));
-  TSA_TRY(tsa_search(hist8, w.status, p->nz, n, 256, p->k, p->q, p->objective, p->enumeration, w.units, 0,
-                     w.units, w.ps, w.pk, w.search, w.search_bytes, stream));
-  TSA_TRY(finalize_impl(hist8, w.status, p->nz, 256, p->k, p->q, p->objective, w.ps, w.pk, w.units,
-                        out->thresholds, out->objective, w.status, out->slice_status, s));
+  if (p->k <= 2 && p->enumeration == TSA_ENUM_CANONICAL && p->objective == TSA_OBJ_PSEUDO_ADDITIVE) {
+    // the compact path's per-slice kernel (tables, canonical search, argmax,
+    // phi(t*) in the definition's order; one CTA per slice) on the remapped
+    // histograms: one partial per slice, the overflow flag = the HU status
+    const bool shannon = p->q == 1.0;
+    tsa::FusedArgs a = {};
+    a.n = n;
+    a.nz = p->nz;
+    a.L = 256;
+    a.k = p->k;
+    a.q = p->q;
+    a.mode = search_mode(p->q, p->objective);
+    a.thresholds = out->thresholds;
+    a.objective = out->objective;
+    a.hist = hist8;
+    a.status = w.status;
+    a.status2 = out->slice_status;
+    a.partial = hist8;
+    a.povf = w.status;
+    a.counters = nullptr;
+    a.ipow = shannon ? nullptr : w.luts;
+    a.lnn = shannon ? w.luts : nullptr;
+    a.rcp = shannon ? w.luts + (n + 1) : nullptr;
+    a.luts.ipow = a.ipow;
+    a.luts.lnn = a.lnn;
+    a.luts.rcp = a.rcp;
+    a.luts.iqm1 = shannon ? 0.0 : 1.0 / (p->q - 1.0);
+    a.luts.omq = 1.0 - p->q;
+    a.luts.shannon = shannon;
+    a.HC = 1;
+    const int lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1 + 255) / 256, 2 * g_num_sms()));
+    tsa::k_lut_part<<<lgrid, 256, 0, s>>>(a);
+    TSA_TRY(check_cuda("k_lut_part"));
+    const int L = 256, E = L + 1;
+    const size_t sm = (size_t)((L + 1) & ~1) * 4 + (size_t)L * 8 * 3 + (size_t)E * 8 * 2 + (size_t)E * 8 + 64;
+    auto mid = p->k == 1 ? (a.mode == tsa::PROD_MAX ? tsa::k_mid<1, tsa::PROD_MAX>
+                            : a.mode == tsa::PROD_MIN ? tsa::k_mid<1, tsa::PROD_MIN> : tsa::k_mid<1, tsa::SUM>)
+                         : (a.mode == tsa::PROD_MAX ? tsa::k_mid<2, tsa::PROD_MAX>
+                            : a.mode == tsa::PROD_MIN ? tsa::k_mid<2, tsa::PROD_MIN> : tsa::k_mid<2, tsa::SUM>);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    mid<<<(unsigned)p->nz, tsa::kMidThreads, sm, s>>>(a);
+    TSA_TRY(check_cuda("k_mid (HU)"));
+  } else {
+    TSA_TRY(tsa_search(hist8, w.status, p->nz, n, 256, p->k, p->q, p->objective, p->enumeration, w.units, 0,
+                       w.units, w.ps, w.pk, w.search, w.search_bytes, stream));
+    TSA_TRY(finalize_impl(hist8, w.status, p->nz, 256, p->k, p->q, p->objective, w.ps, w.pk, w.units,
+                          out->thresholds, out->objective, w.status, out->slice_status, s));
+  }
   if (out->labels) {
     const dim3 grid(4, (unsigned)p->nz);  // 4 contiguous chunks per slice
     switch (p->k) {

@@ -230,7 +230,10 @@ tsa_status tsa2d_validate(const tsa2d_problem *p);
 /* Bytes of workspace tsa2d_segment / tsa2d_histogram need (0 if invalid). */
 size_t tsa2d_workspace_size(const tsa2d_problem *p);
 
-/* CTAs per cluster the library uses for this problem (0 if invalid). */
+/* CTAs per cluster the library uses for this problem (0 if invalid): the
+ * explicit `cluster` if set, else the smallest of 4..8 whose CTAs each count
+ * <= 65536 pixels in one round (4 for 512x512) and whose shared-memory plan
+ * fits; slices too large for that count in rounds of <= 65535 pixels. */
 int32_t tsa2d_cluster_size(const tsa2d_problem *p);
 
 /* The whole 2-D path: mean image, 2-D histogram, exhaustive (t,s) search,

@@ -95,7 +95,7 @@ typedef struct {
   int32_t enumeration;  /* tsa_enumeration */
   int32_t units_per_slice; /* search work units per slice (0 = library heuristic) */
   /* tsa_segment schedule (0 = library default for every field):
-   *   pipeline     2 = compact: three kernels (histogram partials + 1/n^q table,
+   *   pipeline     2 = compact: three kernels (histogram partials + class-term table,
    *                one CTA per slice for tables/search/argmax/phi, labels);
    *                1 = one persistent fused kernel (the same work overlapped
    *                through a dependency-ordered task queue); both need k <= 2,
@@ -169,6 +169,21 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz,
                       int32_t unit_begin, int32_t unit_end, double *part_score,
                       uint64_t *part_key, void *workspace, size_t workspace_bytes,
                       void *stream);
+
+/* The class-size constants of every search kernel (a2/a3), exposed so tests
+ * can check them against the definition.  A class of n voxels contributes
+ * A = W / n^q (q != 1; PAPER.md:581-591 with p_i/P_j = c_i/n, R11)
+ * or S = ln n - W/n (q == 1, R6); the library computes n^-q, ln n and 1/n
+ * from a 33 KB table (j^-q or ln j and 1/j for j <= 2^11, 2^(-s q)) and a
+ * degree-6 (q > 10: 12) polynomial in d = r/(j 2^s) < 2^-10, n = 2^s j + r
+ * -- no N-sized table.
+ *   n      [count] u32 class sizes (0 gives NaN)
+ *   a      [count] f64 out: n^-q (q != 1) or ln n (q == 1)
+ *   b      [count] f64 out or NULL: 1/n (q == 1 only; untouched otherwise)
+ *   workspace  tsa_class_consts_workspace_size() bytes */
+size_t tsa_class_consts_workspace_size(void);
+tsa_status tsa_class_consts(const uint32_t *n, int64_t count, double q, double *a, double *b,
+                            void *workspace, size_t workspace_bytes, void *stream);
 
 /* a4 (partial): merge nparts [nparts][nz] partials into [nz] under the total
  * order (score desc, key asc).  Used before a cross-rank exchange. */

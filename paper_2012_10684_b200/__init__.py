@@ -40,6 +40,7 @@ EXPORTS = (
     "tsa_hu_workspace_size", "tsa_hu_segment", "tsa_hu_preprocess", "tsa_hu_histogram",
     "tsa_hu_finish",
     "tsa_morph_workspace_size", "tsa_morph",
+    "tsa_class_consts_workspace_size", "tsa_class_consts",
 )
 
 
@@ -155,6 +156,8 @@ def load() -> ctypes.CDLL:
         "tsa_hu_finish": (I32, [PH, P, PO, P, SZ, P]),
         "tsa_morph_workspace_size": (SZ, [I64, I64, I64, I32]),
         "tsa_morph": (I32, [P, P, I64, I64, I64, I32, I32, P, SZ, P]),
+        "tsa_class_consts_workspace_size": (SZ, []),
+        "tsa_class_consts": (I32, [P, I64, D, P, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -571,6 +574,21 @@ def tsa_morph(vol, op="tophat", radius=10, out=None, workspace=None, stream=None
                             workspace.numel() if workspace is not None else 0, _stream(stream)),
            "tsa_morph")
     return out
+
+
+def tsa_class_consts(n, q, stream=None):
+    """The class-size constants of the search kernels for class sizes `n`
+    (u32 values in an int32/int64 CUDA tensor): n^-q (q != 1) or (ln n, 1/n)
+    (q == 1).  Returns a (or (a, b) at q == 1) as f64 CUDA tensors."""
+    _need_cuda(n)
+    lib = load()
+    n32 = n.to(torch.int32).contiguous()
+    a = torch.empty(n32.shape, dtype=torch.float64, device=n.device)
+    b = torch.empty(n32.shape, dtype=torch.float64, device=n.device) if q == 1.0 else None
+    ws = torch.empty(int(lib.tsa_class_consts_workspace_size()), dtype=torch.uint8, device=n.device)
+    _check(lib.tsa_class_consts(_ptr(n32), n32.numel(), float(q), _ptr(a), _ptr(b), _ptr(ws), ws.numel(),
+                                _stream(stream)), "tsa_class_consts")
+    return (a, b) if b is not None else a
 
 
 def unpack_key(key, k):

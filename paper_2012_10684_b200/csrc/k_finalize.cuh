@@ -57,31 +57,50 @@ __device__ __forceinline__ int class_of(int i, int t0, int t1, int t2, int t3) {
   return (i > t0) + (i > t1) + (i > t2) + (i > t3);
 }
 
-// One warp per slice.  Lane c <= k owns class c: it sums P_c and then A_c
-// sequentially over the class's non-empty bins in ascending order (the
-// definition's order); the p_i and pow/log terms are computed lane-parallel.
-__global__ void __launch_bounds__(32) k_finalize(FinalizeArgs g) {
+// One CTA (kFinThreads) per slice.  Warp 0 merges the partials; the CTA
+// builds the ascending list of non-empty bins (per-thread bin ranges + a block
+// scan), computes p_i = c_i/N and the pow/log terms thread-parallel, and
+// thread c <= k sums P_c and then A_c sequentially over its class's list
+// segment in ascending bin order (the definition's order).
+constexpr int kFinThreads = 256;
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
   extern __shared__ double fsh[];  // [L] p then terms, followed by int [L] bin list
   int *lst = reinterpret_cast<int *>(fsh + g.L);
+  __shared__ double s_best[1];
+  __shared__ uint64_t s_key[1];
+  __shared__ int s_cnt[kFinThreads / 32 + 1];
+  __shared__ unsigned long long s_n[kFinThreads / 32];
+  __shared__ int s_start[kKMax + 2];
+  __shared__ double Psh[kKMax + 1], Ssh[kKMax + 1];
   const int64_t z = blockIdx.x;
-  const int lane = threadIdx.x;
-  double s = -CUDART_INF;
-  uint64_t key = kKeyNone;
-  for (int p = lane; p < g.nparts; p += 32) {
-    const double os = g.ps[(size_t)p * g.nz + z];
-    const uint64_t ok = g.pk[(size_t)p * g.nz + z];
-    if (better(os, ok, s, key)) {
-      s = os;
-      key = ok;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kFinThreads / 32;
+  if (warp == 0) {
+    double s = -CUDART_INF;
+    uint64_t key = kKeyNone;
+    for (int p = lane; p < g.nparts; p += 32) {
+      const double os = g.ps[(size_t)p * g.nz + z];
+      const uint64_t ok = g.pk[(size_t)p * g.nz + z];
+      if (better(os, ok, s, key)) {
+        s = os;
+        key = ok;
+      }
+    }
+    warp_argmax(s, key);
+    if (lane == 0) {
+      s_best[0] = s;
+      s_key[0] = key;
     }
   }
-  warp_argmax(s, key);
+  __syncthreads();
+  const uint64_t key = s_key[0];
   int st = g.status_in[z];
   if (st == kOK && key == kKeyNone) st = kNoValidSplit;
   const int k = g.k, L = g.L;
   if (st != kOK) {
-    if (lane < k) g.thresholds[z * k + lane] = -1;
-    if (lane == 0) {
+    if (tid < k) g.thresholds[z * k + tid] = -1;
+    if (tid == 0) {
       if (g.objective_out) g.objective_out[z] = CUDART_NAN;
       if (g.status_out) g.status_out[z] = st;
       if (g.status_out2) g.status_out2[z] = st;
@@ -93,87 +112,102 @@ __global__ void __launch_bounds__(32) k_finalize(FinalizeArgs g) {
   const int t1 = k > 1 ? (int)((key >> (12 * (k - 2))) & 0xFFFull) : L;
   const int t2 = k > 2 ? (int)((key >> (12 * (k - 3))) & 0xFFFull) : L;
   const int t3 = k > 3 ? (int)(key & 0xFFFull) : L;
-  if (lane < k) {
-    const int tl = lane == 0 ? t0 : lane == 1 ? t1 : lane == 2 ? t2 : t3;
-    g.thresholds[z * k + lane] = tl;
+  if (tid < k) {
+    const int tl = tid == 0 ? t0 : tid == 1 ? t1 : tid == 2 ? t2 : t3;
+    g.thresholds[z * k + tid] = tl;
   }
-  if (lane == 0) {
+  if (tid == 0) {
     if (g.status_out) g.status_out[z] = kOK;
     if (g.status_out2) g.status_out2[z] = kOK;
   }
   if (!g.objective_out) return;
   const uint32_t *h = g.hist + z * L;
-  // N, the ordered list of non-empty bins, and per-class list lengths
-  uint64_t nsum = 0;
-  int m = 0;
-  int cnt_mine = 0;  // lane c: number of non-empty bins in class c
-  for (int i0 = 0; i0 < L; i0 += 32) {
-    const int i = i0 + lane;
-    const uint32_t c = i < L ? __ldg(h + i) : 0u;
+  // ordered list of non-empty bins: thread t owns bins [t*per, (t+1)*per)
+  const int per = (L + kFinThreads - 1) / kFinThreads;
+  const int i0 = min(L, tid * per), i1 = min(L, i0 + per);
+  int cnt = 0;
+  unsigned long long nsum = 0;
+  for (int i = i0; i < i1; i++) {
+    const uint32_t c = __ldg(h + i);
+    cnt += c != 0;
     nsum += c;
-    const unsigned bal = __ballot_sync(0xffffffffu, c != 0);
-    if (c) lst[m + __popc(bal & ((1u << lane) - 1u))] = i;
-    m += __popc(bal);
-    const int cls = c ? class_of(i, t0, t1, t2, t3) : -1;
+  }
+  int ex = cnt;
 #pragma unroll
-    for (int cc = 0; cc <= kKMax; cc++) {
-      const int n_c = __popc(__ballot_sync(0xffffffffu, cls == cc));
-      if (lane == cc) cnt_mine += n_c;
-    }
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, ex, off);
+    if (lane >= off) ex += o;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, off);
-  const double N = (double)nsum;  // exact: the oracle's sequential double sum of integers
-  int start = cnt_mine;           // exclusive prefix of class lengths over lanes 0..k
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int o = __shfl_up_sync(0xffffffffu, start, off);
-    if (lane >= off) start += o;
+  if (lane == 31) s_cnt[warp] = ex;
+  if (lane == 0) s_n[warp] = nsum;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < NW; w++) {
+      const int c = s_cnt[w];
+      s_cnt[w] = acc;
+      acc += c;
+    }
+    s_cnt[NW] = acc;
+    unsigned long long n = 0;
+    for (int w = 0; w < NW; w++) n += s_n[w];
+    s_n[0] = n;
   }
-  start -= cnt_mine;
-  __syncwarp();
-  for (int j = lane; j < m; j += 32) fsh[j] = __ddiv_rn((double)__ldg(h + lst[j]), N);
-  __syncwarp();
-  double P = 0.0;
-  if (lane <= k)
-    for (int j = start; j < start + cnt_mine; j++) P = __dadd_rn(P, fsh[j]);
-  __syncwarp();
+  __syncthreads();
+  const int m = s_cnt[NW];
+  int e = s_cnt[warp] + ex - cnt;
+  for (int i = i0; i < i1; i++)
+    if (__ldg(h + i)) lst[e++] = i;
+  const double N = (double)s_n[0];  // exact: the oracle's sequential double sum of integers
+  __syncthreads();
+  // class c = list segment [start_c, start_{c+1}): first entry with bin > t_{c-1}
+  if (tid <= k + 1) {
+    int tv = tid == 0 ? -1 : tid == 1 ? t0 : tid == 2 ? t1 : tid == 3 ? t2 : t3;
+    if (tid == k + 1) tv = L;  // end
+    int lo = 0, hi = m;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lst[mid] > tv) hi = mid;
+      else lo = mid + 1;
+    }
+    s_start[tid] = tid == k + 1 ? m : lo;
+  }
+  for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn((double)__ldg(h + lst[j]), N);
+  __syncthreads();
+  if (tid <= k) {
+    double P = 0.0;
+    for (int j = s_start[tid]; j < s_start[tid + 1]; j++) P = __dadd_rn(P, fsh[j]);
+    Psh[tid] = P;
+  }
+  __syncthreads();
   const double q = g.q;
   const bool shannon = q == 1.0;
-  __shared__ double Psh[kKMax + 1];
-  if (lane <= k) Psh[lane] = P;
-  __syncwarp();
-  for (int j = lane; j < m; j += 32) {
+  for (int j = tid; j < m; j += kFinThreads) {
     const int cls = class_of(lst[j], t0, t1, t2, t3);
     const double r = __ddiv_rn(fsh[j], Psh[cls]);
     fsh[j] = shannon ? __dmul_rn(r, log(r)) : pow(r, q);
   }
-  __syncwarp();
-  double A = 0.0;
-  if (lane <= k)
-    for (int j = start; j < start + cnt_mine; j++)
+  __syncthreads();
+  if (tid <= k) {
+    double A = 0.0;
+    for (int j = s_start[tid]; j < s_start[tid + 1]; j++)
       A = shannon ? __dsub_rn(A, fsh[j]) : __dadd_rn(A, fsh[j]);
-  const double Sl = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(q, 1.0));
-  double S[kKMax + 1];
-#pragma unroll
-  for (int j = 0; j <= kKMax; j++) S[j] = __shfl_sync(0xffffffffu, Sl, j);
-  if (lane == 0) {
+    Ssh[tid] = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(q, 1.0));
+  }
+  __syncthreads();
+  if (tid == 0) {
     double phi;
     if (g.objective == 1) {
       double sum = 0.0, prod = 1.0;
-#pragma unroll
-      for (int j = 0; j <= kKMax; j++)
-        if (j <= k) sum = __dadd_rn(sum, S[j]);
-#pragma unroll
-      for (int j = 0; j <= kKMax; j++)
-        if (j <= k) prod = __dmul_rn(prod, S[j]);
+      for (int j = 0; j <= k; j++) sum = __dadd_rn(sum, Ssh[j]);
+      for (int j = 0; j <= k; j++) prod = __dmul_rn(prod, Ssh[j]);
       phi = __dadd_rn(sum, __dmul_rn(__dsub_rn(1.0, q), prod));
     } else {
-      phi = S[0];
-#pragma unroll
-      for (int j = 1; j <= kKMax; j++)
-        if (j <= k)
-          phi = __dadd_rn(__dadd_rn(phi, S[j]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, q), phi), S[j]));
+      phi = Ssh[0];
+      for (int j = 1; j <= k; j++)
+        phi = __dadd_rn(__dadd_rn(phi, Ssh[j]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, q), phi), Ssh[j]));
     }
     g.objective_out[z] = phi;
   }

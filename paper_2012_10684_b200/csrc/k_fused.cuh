@@ -64,8 +64,7 @@ struct FusedArgs {
   // workspace
   uint32_t *partial;    // [nz][HC][L]
   int32_t *povf;        // [nz][HC]
-  double *ipow;         // [N+1]
-  double *lnn, *rcp;
+  double *sp;           // [kSmallLut] small table of Luts (k_small_luts layout)
   int32_t *counters;    // [0] head, [1] lutdone, [2 .. 2+nz) hdone, [2+nz .. 2+2nz) mdone
   Luts luts;
   // schedule
@@ -134,7 +133,7 @@ __device__ void fused_hist(const FusedArgs &g, int z, int c, uint32_t *sh) {
   __shared__ int s_ovf;
   if (threadIdx.x == 0) s_ovf = 0;
   __syncthreads();
-  if (ovf) s_ovf = 1;
+  if (ovf) s_ovf = kLevelOverflow;
   uint32_t *out = g.partial + ((size_t)z * g.HC + c) * L;
   for (int b = threadIdx.x; b < L; b += blockDim.x) {
     uint32_t s = 0;
@@ -243,7 +242,9 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   TSA_MPHASE(z, 1)
   // histogram = sum of chunk partials; overflow flag
   int ovf = 0;
-  for (int c = tid; c < g.HC; c += blockDim.x) ovf |= __ldcg(g.povf + (size_t)z * g.HC + c);
+  // only LEVEL_OVERFLOW counts (the HU path passes its slice status here,
+  // which may hold NO_VALID_SPLIT from an earlier finish on the same workspace)
+  for (int c = tid; c < g.HC; c += blockDim.x) ovf |= __ldcg(g.povf + (size_t)z * g.HC + c) == kLevelOverflow;
   if (tid == 0) s_status = 0;
   __syncthreads();
   if (ovf) s_status = kLevelOverflow;
@@ -285,7 +286,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     __syncthreads();
     TSA_MPHASE(z, 4)
     // exhaustive search over all C(M-1, K) tuples, row chunks over the CTA
-    search_rows_k12<K, MODE, 16>(t, fsh, g.luts, tBin, M, tid, blockDim.x, best, key);
+    search_rows_k12<K, MODE, 16>(t, fsh, g.luts, tBin, M, 0, k12_chunks<K, 16>(M), tid, blockDim.x, best, key);
     __syncthreads();  // fsh is reused below
   }
   warp_argmax(best, key);
@@ -456,17 +457,8 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
     const int tr_type = type, tr_z = z;
 #endif
     if (type == 0) {
-      const int64_t N = g.n;
-      const int64_t a = (int64_t)z * g.lut_per, b = min(N + 1, a + g.lut_per);
-      for (int64_t m = a + threadIdx.x; m < b; m += blockDim.x) {
-        const double x = (double)m;
-        if (g.luts.shannon) {
-          g.lnn[m] = m == 0 ? CUDART_NAN : log(x);
-          g.rcp[m] = m == 0 ? CUDART_NAN : __drcp_rn(x);
-        } else {
-          g.ipow[m] = m == 0 ? CUDART_NAN : __drcp_rn(pow(x, g.q));
-        }
-      }
+      const int64_t a = (int64_t)z * g.lut_per, b = min((int64_t)kSmallLut, a + g.lut_per);
+      for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) g.sp[e] = small_lut_entry((int)e, g.q, g.luts.shannon);
       __syncthreads();
       if (threadIdx.x == 0) signal_add(g.counters + 1, 1);
     } else if (z < g.nz) {
@@ -501,13 +493,18 @@ __global__ void __launch_bounds__(512, 2) k_fused(FusedArgs g) {
 // HBM-bound labelling of other slices.  (A dependent grid only launches once
 // every CTA of its primary has started, so spinning dependents can never
 // starve the CTAs they wait for.)
-//   k_lut_part    the 1/n^q table over all SMs; signals lutdone
+//   k_lut_part    the small class-term table (Luts::sp); signals lutdone
 //   k_hist_part   persistent, slice-ordered (slice, chunk) histogram partials;
 //                 signals hdone[z]
 //   k_mid         one CTA per slice: waits lutdone, hdone[z]; tables, search,
 //                 argmax, phi(t*); signals mdone[z]
 //   k_label_part  (chunk, slice): waits mdone[z]; labels
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Last statement of every PDL-launched kernel of the chain: an early-triggering
+// primary's dependents must execute griddepcontrol.wait (PTX ISA), and with it
+// a grid completes only after its primary has, so later stream work (a D2H
+// of the objective, the next captured node) is ordered after the whole chain.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #ifdef TSA_TRACE
 __device__ __forceinline__ void trace_rec(int type, int z, unsigned long long t0) {
@@ -545,23 +542,15 @@ __global__ void __launch_bounds__(512) k_hist_part(FusedArgs g) {
     fused_hist<T>(g, (int)(it / g.HC), (int)(it % g.HC), reinterpret_cast<uint32_t *>(fsm));
   }
   TRACE_END(1, blockIdx.x)
+  pdl_wait();
 }
 
-// The 1/n^q (or ln n, 1/n) table over all SMs, PDL primary of k_hist_part;
+// The small class-term table (Luts::sp, 33 KB), PDL primary of k_hist_part;
 // every CTA signals the LUT counter that k_mid waits on.
 __global__ void __launch_bounds__(256) k_lut_part(FusedArgs g) {
   pdl_trigger();
-  const int64_t N1 = g.n + 1;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < N1;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const double x = (double)m;
-    if (g.luts.shannon) {
-      g.lnn[m] = m == 0 ? CUDART_NAN : log(x);
-      g.rcp[m] = m == 0 ? CUDART_NAN : __drcp_rn(x);
-    } else {
-      g.ipow[m] = m == 0 ? CUDART_NAN : __drcp_rn(pow(x, g.q));
-    }
-  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kSmallLut; e += gridDim.x * blockDim.x)
+    g.sp[e] = small_lut_entry(e, g.q, g.luts.shannon);
   __syncthreads();
   if (threadIdx.x == 0 && g.counters) signal_add(g.counters + 1, 1);
 }
@@ -578,6 +567,7 @@ __global__ void __launch_bounds__(kMidThreads, 3) k_mid(FusedArgs g) {
   pdl_trigger();
   fused_mid<K, MODE>(g, blockIdx.x, fsm);
   TRACE_END(2, blockIdx.x)
+  pdl_wait();
 }
 
 template <typename T>
@@ -585,6 +575,7 @@ __global__ void __launch_bounds__(256) k_label_part(FusedArgs g) {
   TRACE_T0
   fused_label<T>(g, blockIdx.y, blockIdx.x);
   TRACE_END(3, blockIdx.y)
+  pdl_wait();
 }
 
 }  // namespace tsa

@@ -32,7 +32,10 @@ struct SearchArgs {
   const double *Whi, *Wlo, *Asuf, *R;
   const double *PP, *AI;  // k >= 3 prefix tables (k_rtable): PP[x][y] = T(0,x) (x) T(x+1,y), AI[x][y] = T(x,y)
   const int32_t *Bin, *Mz, *status;
-  int32_t *counter;    // dynamic item counter (k >= 3 rows kernel), zeroed before launch
+  int32_t *counter;    // dynamic item counter (k >= 3 rows kernel, k = 2 block kernel), zeroed before launch
+  const int32_t *mmax; // max over slices of M (k_scan), k = 2 block kernel
+  double *item_score;  // [nbmax][nz] per-(a-block, slice) partials of the k = 2 block kernel
+  uint64_t *item_key;
   double *part_score;  // [nunits][nz]
   uint64_t *part_key;
   Luts luts;
@@ -520,77 +523,38 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
 
 namespace tsa {
 
-// Flattened exhaustive search for k <= 2 (pseudo-additive or q == 1): the
-// tuples (a, b), a < b (k = 2; colex rank C(b,2) + a) or (b) (k = 1) of ranks
-// [r0, r1) are dealt to threads; each thread evaluates B independent tuples at
-// a time so their 1/n^q gathers overlap (a row-by-row walk serialises them).
-// Value (same expression tree as k_search): v = (1 (x) Apre[a]) (x)
-// (T(a+1, b) (x) Asuf[b]), Apre[a] = T(0, a).  Per-thread order is not lex, so
-// every candidate is compared under the full (score, key) order.
-template <int K, int MODE, int B = 8>
-__device__ __forceinline__ void search_flat_k12(const SliceTables &t, const double *Apre,
-                                                const Luts &l, const int32_t *bin, int M,
-                                                uint64_t r0, uint64_t r1, uint64_t tid,
-                                                uint64_t nth, double &best, uint64_t &bestkey) {
-  const double ident = MODE == SUM ? 0.0 : 1.0;
-  for (uint64_t rb = r0 + tid; rb < r1; rb += nth * B) {
-    int aa[B], bb[B];
-    bool ok[B];
-#pragma unroll
-    for (int u = 0; u < B; u++) {
-      const uint64_t r = rb + u * nth;
-      ok[u] = r < r1;
-      if (K == 1) {
-        aa[u] = -1;
-        bb[u] = ok[u] ? (int)r : 0;
-      } else {
-        int b = 1, a = 0;
-        if (ok[u]) {
-          b = (int)((1.0 + sqrt(1.0 + 8.0 * (double)r)) * 0.5);
-          while (b > 1 && binom((uint64_t)b, 2) > r) b--;
-          while (binom((uint64_t)b + 1, 2) <= r) b++;
-          a = (int)(r - binom((uint64_t)b, 2));
-        }
-        aa[u] = a;
-        bb[u] = b;
-      }
-    }
-    double v[B];
-#pragma unroll
-    for (int u = 0; u < B; u++) {
-      const double R = combine<MODE>(class_term<MODE>(t, l, aa[u] + 1, bb[u]), t.Asuf[bb[u]]);
-      const double pre = K == 1 ? ident : combine<MODE>(ident, Apre[aa[u]]);
-      v[u] = combine<MODE>(pre, R);
-      if (MODE == PROD_MIN) v[u] = -v[u];
-    }
-#pragma unroll
-    for (int u = 0; u < B; u++) {
-      if (ok[u] && v[u] >= best) {
-        const uint64_t key = K == 1 ? (uint64_t)bin[bb[u] + 1]
-                                    : ((uint64_t)bin[aa[u] + 1] << 12) | (uint64_t)bin[bb[u] + 1];
-        if (better(v[u], key, best, bestkey)) {
-          best = v[u];
-          bestkey = key;
-        }
-      }
-    }
-  }
+// Chunks of the k <= 2 tuple space of a slice with M canonical positions
+// (P = M - 1 threshold positions): k = 1, chunk c = thresholds [c*CH, c*CH+CH);
+// k = 2, row b (a = 0..b-1) is split into ceil(b/CH) chunks of CH consecutive
+// a, rows in order: off(b) = sum_{j<b} ceil(j/CH).
+template <int K, int CH>
+__host__ __device__ __forceinline__ int k12_off(int b) {
+  const int n = b - 1, Q = n / CH, Rr = n % CH;
+  return b <= 0 ? 0 : CH * Q * (Q + 1) / 2 + (Q + 1) * Rr;
+}
+template <int K, int CH>
+__host__ __device__ __forceinline__ int k12_chunks(int M) {
+  const int P = M - 1;
+  if (P <= 0) return 0;
+  return K == 1 ? (P + CH - 1) / CH : k12_off<K, CH>(P);
 }
 
-// Row-chunked variant of search_flat_k12 for one slice searched by a whole
-// CTA (the compact path's k_mid): the tuples of row b (a = 0..b-1, k = 2) in
-// chunks of CH consecutive a, so no tuple is unranked (no FP64 sqrt) and a
-// thread keeps CH class-term gathers in flight.  Every tuple's value is the
-// same expression as in search_flat_k12, and candidates are compared under
-// the full (score, key) order, so the result is bit-identical.
+// Row-chunked exhaustive search for k <= 2: chunks [cbeg, cend) of the slice,
+// dealt to threads tid, tid + nth, ...  No tuple is unranked (no FP64 sqrt)
+// and a thread keeps CH independent class terms in flight.  Value of tuple
+// (a, b): (1 (x) Apre[a]) (x) (T(a+1, b) (x) Asuf[b]) (k = 2), 1 (x) (T(0, b)
+// (x) Asuf[b]) (k = 1) -- the expression tree of every other search kernel --
+// and candidates are compared under the full (score, key) order, so any
+// chunk partition gives the same result.
 template <int K, int MODE, int CH = 16>
 __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const double *Apre, const Luts &l,
-                                                const int32_t *bin, int M, int tid, int nth,
-                                                double &best, uint64_t &bestkey) {
+                                                const int32_t *bin, int M, int cbeg, int cend, int tid,
+                                                int nth, double &best, uint64_t &bestkey) {
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int P = M - 1;  // positions 0 .. M-2
   if (K == 1) {
-    for (int b0 = tid * CH; b0 < P; b0 += nth * CH) {
+    for (int c = cbeg + tid; c < cend; c += nth) {
+      const int b0 = c * CH;
       double v[CH];
 #pragma unroll
       for (int u = 0; u < CH; u++) {
@@ -612,24 +576,15 @@ __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const doub
     }
     return;
   }
-  const int nchunks = [&] {
-    const int n = P - 1, Q = n / CH, Rr = n % CH;  // off(P)
-    return P <= 0 ? 0 : CH * Q * (Q + 1) / 2 + (Q + 1) * Rr;
-  }();
-  for (int c = tid; c < nchunks; c += nth) {
-    // row b: largest b with off(b) <= c (rows 1 .. P-1 hold tuples), where
-    // off(b) = sum_{j<b} ceil(j/CH) = CH Q(Q+1)/2 + (Q+1) R, Q = (b-1)/CH, R = (b-1)%CH
-    auto off = [](int bb) {
-      const int n = bb - 1, Q = n / CH, Rr = n % CH;
-      return bb <= 0 ? 0 : CH * Q * (Q + 1) / 2 + (Q + 1) * Rr;
-    };
+  for (int c = cbeg + tid; c < cend; c += nth) {
+    // row b: largest b with off(b) <= c (rows 1 .. P-1 hold tuples)
     int lo = 1, hi = P - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (off(mid) <= c) lo = mid;
+      if (k12_off<K, CH>(mid) <= c) lo = mid;
       else hi = mid - 1;
     }
-    const int b = lo, a0 = (c - off(b)) * CH;
+    const int b = lo, a0 = (c - k12_off<K, CH>(b)) * CH;
     const double R0 = t.Asuf[b];
     double v[CH];
 #pragma unroll
@@ -654,8 +609,11 @@ __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const doub
 }
 
 // Staged-path kernel for k <= 2 (not sum-plus-product): CTA (unit, slice)
-// stages the slice tables and Apre in shared memory, then searches its
-// tuple-rank range [T*u/U, T*(u+1)/U) with search_flat_k12.
+// stages the slice's canonical tables, Apre and the small class-term table in
+// shared memory, then searches its chunk range [NC*u/U, NC*(u+1)/U) with
+// search_rows_k12 (NC = k12_chunks(M)).
+constexpr int kK12Chunk = 16;
+
 template <int K, int MODE, int NT>
 __global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
   extern __shared__ double ssh[];
@@ -671,23 +629,26 @@ __global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
     SliceTables t{g.C + (size_t)z * g.E, g.Whi + (size_t)z * g.E, g.Wlo + (size_t)z * g.E,
                   g.Asuf + (size_t)z * g.L};
     double *sWhi = ssh, *sWlo = ssh + g.E, *sAsuf = ssh + 2 * g.E, *sApre = ssh + 2 * g.E + g.L;
-    uint32_t *sC = reinterpret_cast<uint32_t *>(ssh + 2 * g.E + 2 * g.L);
+    double *sSp = ssh + 2 * g.E + 2 * g.L;  // small class-term table (kSmallLut)
+    uint32_t *sC = reinterpret_cast<uint32_t *>(sSp + kSmallLut);
     for (int i = threadIdx.x; i <= M; i += blockDim.x) {
       sWhi[i] = t.Whi[i];
       sWlo[i] = t.Wlo[i];
       sC[i] = t.C[i];
       if (i <= M - 2) sAsuf[i] = t.Asuf[i];
     }
+    for (int i = threadIdx.x; i < kSmallLut; i += blockDim.x) sSp[i] = g.luts.sp[i];
     __syncthreads();
     const SliceTables ts{sC, sWhi, sWlo, sAsuf};
+    Luts ls = g.luts;
+    ls.sp = sSp;
     if (K == 2)
-      for (int i = threadIdx.x; i <= M - 2; i += blockDim.x) sApre[i] = class_term<MODE>(ts, g.luts, 0, i);
+      for (int i = threadIdx.x; i <= M - 2; i += blockDim.x) sApre[i] = class_term<MODE>(ts, ls, 0, i);
     __syncthreads();
-    const uint64_t T = binom((uint64_t)P, K);
-    const uint64_t r0 = T * (uint64_t)u / (uint64_t)g.units;
-    const uint64_t r1 = T * (uint64_t)(u + 1) / (uint64_t)g.units;
-    search_flat_k12<K, MODE>(ts, sApre, g.luts, g.Bin + (size_t)z * g.E, M, r0, r1, threadIdx.x,
-                             blockDim.x, best, bestkey);
+    const int64_t NC = k12_chunks<K, kK12Chunk>(M);
+    const int c0 = (int)(NC * u / g.units), c1 = (int)(NC * (u + 1) / g.units);
+    search_rows_k12<K, MODE, kK12Chunk>(ts, sApre, ls, g.Bin + (size_t)z * g.E, M, c0, c1, threadIdx.x,
+                                        blockDim.x, best, bestkey);
   }
   warp_argmax(best, bestkey);
   __shared__ double ss[32];
@@ -708,8 +669,146 @@ __global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
   }
 }
 
-}  // namespace tsa
+// ---------------------------------------------------------------------------
+// k = 2 exhaustive search, warp per a-block (pseudo-additive or q == 1).
+//
+// Work item (i, z): slice z, a-block i = lanes a = 32 i + lane (t_1 = position
+// a).  The warp walks every row b = t_2 in (32 i, M-2]; lane a evaluates
+// (a, b) when a < b.  The lane's own quantities (C[a+1], W[a+1], Apre[a] =
+// T(0, a)) stay in registers for the whole item and the row's (C[b+1], W[b+1],
+// Asuf[b]) are warp-uniform loads, so the only per-tuple memory access is the
+// {j^-q, 1/j} entry of the class-size table, staged once per CTA in shared
+// memory (one 16-byte load; n = C[b+1] - C[a+1] is sorted across the lanes,
+// so the loads mostly fall in distinct banks).  Value of (a, b):
+//   (1 (x) T(0, a)) (x) (T(a+1, b) (x) Asuf[b])     -- the expression tree of
+// every other search kernel, class terms from the same arithmetic.
+// Items are claimed per warp from a global counter in (i-major, z) order, so
+// the large early blocks go first (LPT) and the small late ones fill the tail.
+// Unit u of U owns the a-blocks i == u (mod U): a rank-independent partition.
+// Each item writes its own (score, key) partial to item_score/key[i][z];
+// k_merge_items folds them per (unit, slice) under the total order.
+constexpr int kK2Rows = 4;  // rows in flight per lane (tables are padded by >= kK2Rows entries)
 
-namespace tsa {
+// The class term of the k = 2 kernel: class_term_nw<MODE> with the polynomial
+// degree fixed at compile time and the 2^-s scaling on the exponent field --
+// bit-identical values (same operations, same order).
+template <int MODE, int DEG>
+__device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint32_t n, double w) {
+  uint32_t j, r;
+  int s;
+  nsplit_idx(n, j, s, r);
+  const double2 e = tab.jr(j);
+  if (MODE == PROD_MAX || MODE == PROD_MIN) {
+    const double d = scale_pow2_neg(__dmul_rn((double)r, e.y), s, r);
+    const double ip = __dmul_rn(__dmul_rn(e.x, tab.p2(s)), horner_c_deg<DEG>(l, d));
+    return __dmul_rn(w, ip);
+  } else {
+    return shannon_t(l, tab, n, w);
+  }
+}
+
+template <int MODE, int DEG>
+__global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
+  __shared__ double2 s_jr[kSN];
+  __shared__ double s_p2[32];
+  for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
+  if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.sp[2 * kSN + threadIdx.x];
+  __syncthreads();
+  const SpPair tab{s_jr, s_p2};
+  const Luts &l = g.luts;
+  const int lane = threadIdx.x & 31;
+  const int mmax = *g.mmax;
+  const int nbmax = mmax >= 3 ? (mmax - 3) / 32 + 1 : 0;  // a-blocks: a <= M-3
+  const int w = g.nunits, U = g.units, u0 = g.unit_begin;
+  // blocks of this launch: i = (t / w) * U + u0 + t % w, t < nbl
+  const int nbl = nbmax <= u0 ? 0 : ((nbmax - u0) / U) * w + min(w, (nbmax - u0) % U);
+  const uint32_t nz = (uint32_t)g.nz;
+  const uint32_t items = (uint32_t)nbl * nz;
+  const double ident = MODE == SUM ? 0.0 : 1.0;
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = (uint32_t)atomicAdd(g.counter, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= items) break;
+    const int tb = (int)(it / nz);
+    const int z = (int)(it - (uint32_t)tb * nz);
+    const int i = (tb / w) * U + u0 + tb % w;
+    const int M = g.Mz[z];
+    double best = -CUDART_INF;
+    uint64_t bestkey = kKeyNone;
+    if (g.status[z] == kOK && 32 * i <= M - 3) {
+      const uint32_t *C = g.C + (size_t)z * g.E;
+      const double *Whi = g.Whi + (size_t)z * g.E, *Wlo = g.Wlo + (size_t)z * g.E;
+      const double *As = g.Asuf + (size_t)z * g.L;
+      const int a = 32 * i + lane;
+      const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
+      const uint32_t Ca = __ldg(C + ac + 1);
+      const double Wah = __ldg(Whi + ac + 1), Wal = __ldg(Wlo + ac + 1);
+      // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
+      const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
+      const int bend = M - 2;
+      int b0 = 32 * i + 1;
+      const uint32_t *pC = C + b0 + 1;
+      const double *pWh = Whi + b0 + 1, *pWl = Wlo + b0 + 1, *pA = As + b0;
+      for (; b0 <= bend; b0 += kK2Rows, pC += kK2Rows, pWh += kK2Rows, pWl += kK2Rows, pA += kK2Rows) {
+        double vb[kK2Rows];
+#pragma unroll
+        for (int r = 0; r < kK2Rows; r++) {
+          const uint32_t n = __ldg(pC + r) - Ca;
+          const double wm = dd_diff(__ldg(pWh + r), __ldg(pWl + r), Wah, Wal);
+          const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), __ldg(pA + r));
+          double v = combine<MODE>(pre, R);
+          if (MODE == PROD_MIN) v = -v;
+          vb[r] = v;
+        }
+#pragma unroll
+        for (int r = 0; r < kK2Rows; r++) {
+          const int b = b0 + r;
+          if (vb[r] >= best && a < b && b <= bend) {
+            const uint64_t key = ((uint64_t)__ldg(g.Bin + (size_t)z * g.E + a + 1) << 12) |
+                                 (uint64_t)__ldg(g.Bin + (size_t)z * g.E + b + 1);
+            if (better(vb[r], key, best, bestkey)) {
+              best = vb[r];
+              bestkey = key;
+            }
+          }
+        }
+      }
+      warp_argmax(best, bestkey);
+    }
+    if (lane == 0) {
+      g.item_score[(size_t)i * g.nz + z] = best;
+      g.item_key[(size_t)i * g.nz + z] = bestkey;
+    }
+  }
+}
+
+// Per (unit u in [u0, u1), slice z), one warp: fold the k = 2 block partials
+// i == u (mod U), i < nblocks(z), into part[u - u0][z] under the total order.
+__global__ void k_merge_items(const double *is, const uint64_t *ik, const int32_t *Mz, const int32_t *status,
+                              int64_t nz, int U, int u0, int nu, double *ps, uint64_t *pk) {
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nz * nu) return;  // warp-uniform
+  const int64_t z = t % nz;
+  const int u = u0 + (int)(t / nz);
+  const int M = Mz[z];
+  const int nb = (status[z] == kOK && M >= 3) ? (M - 3) / 32 + 1 : 0;
+  double s = -CUDART_INF;
+  uint64_t k = kKeyNone;
+  for (int i = u + lane * U; i < nb; i += 32 * U) {
+    const double os = is[(size_t)i * nz + z];
+    const uint64_t ok = ik[(size_t)i * nz + z];
+    if (better(os, ok, s, k)) {
+      s = os;
+      k = ok;
+    }
+  }
+  warp_argmax(s, k);
+  if (lane == 0) {
+    ps[(size_t)(u - u0) * nz + z] = s;
+    pk[(size_t)(u - u0) * nz + z] = k;
+  }
+}
 
 }  // namespace tsa

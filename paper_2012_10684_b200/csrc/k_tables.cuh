@@ -1,8 +1,8 @@
 // k_tables.cuh -- SURVEY.md §8 row a2: the prefix-scan tables that make every
 // class term O(1) (north star (2): "a prefix-scan of p_i and p_i^q").
 //
-//   k_luts   n-indexed 1/n^q (or ln n, 1/n at q == 1), n in [0, N], shared by
-//            all slices of a call (N+1 pow instead of one pow per class term)
+//   k_small_luts (tsa_device.cuh) the 33 KB table behind n^-q / ln n / 1/n
+//            (j^-q for j <= 2^11, 1/j, 2^(-s q)); no N-sized table
 //   k_scan   per slice: compaction of the non-empty bins, exact prefix counts
 //            C, double-double prefix sums W of w_i = c_i^q (c_i ln c_i at q=1),
 //            and the last-class terms Asuf[i] = T(i+1, M-1)
@@ -17,18 +17,6 @@
 #include "tsa_device.cuh"
 
 namespace tsa {
-
-__global__ void k_luts(double *ipow, double *lnn, double *rcp, int64_t N, double q, int shannon) {
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n <= N;
-       n += (int64_t)gridDim.x * blockDim.x) {
-    const double x = (double)n;
-    if (shannon) {
-      lnn[n] = n == 0 ? CUDART_NAN : log(x);
-      rcp[n] = n == 0 ? CUDART_NAN : __drcp_rn(x);
-    }
-    if (ipow) ipow[n] = n == 0 ? CUDART_NAN : __drcp_rn(pow(x, q));
-  }
-}
 
 struct ScanArgs {
   const uint32_t *hist;  // [nz][L]
@@ -46,6 +34,7 @@ struct ScanArgs {
   int32_t *fBin;
   double *Asuf;          // [nz][L]
   int32_t *M;            // [nz] entries used by the search (m or L)
+  int32_t *mmax;         // max over slices of M (atomicMax; zeroed before launch) or null
   Luts luts;
 };
 
@@ -169,7 +158,10 @@ __global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
     tWlo = fWlo;
     M = L;
   }
-  if (tid == 0) g.M[z] = M;
+  if (tid == 0) {
+    g.M[z] = M;
+    if (g.mmax) atomicMax(g.mmax, M);
+  }
   if (status != kOK) return;
   SliceTables t{tC, tWhi, tWlo, nullptr};
   double *Asuf = g.Asuf + z * L;
@@ -214,6 +206,28 @@ __global__ void __launch_bounds__(256) k_rtable(const uint32_t *C, const double 
     R[o] = r;
     PP[o] = pp;
     if (AI) AI[o] = ai;
+  }
+}
+
+// tsa_class_consts (testing): the class-size constants exactly as the search
+// kernels compute them -- q != 1: a = n^-q; q == 1: a = ln n (S with w = 0),
+// b = 1/n (from S with w = -1: S = ln n + 1/n, minus ln n, would round; use
+// the same pieces directly instead).
+__global__ void k_class_consts(const uint32_t *n, int64_t count, Luts l, double *a, double *b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = n[i];
+    if (!l.shannon) {
+      a[i] = ipow_n(l, v);
+    } else {
+      a[i] = shannon_term(l, v, 0.0);
+      uint32_t j, r;
+      int s;
+      nsplit_idx(v, j, s, r);
+      const double two_ms = two_pow_neg(s);
+      const double d = __dmul_rn(__dmul_rn((double)r, l.sp[kSN + j]), two_ms);
+      if (b) b[i] = __dmul_rn(__dmul_rn(l.sp[kSN + j], two_ms), horner_c(l, d));
+    }
   }
 }
 

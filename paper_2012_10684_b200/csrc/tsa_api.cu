@@ -95,6 +95,23 @@ int search_mode(double q, int32_t objective) {
   return q < 1.0 ? tsa::PROD_MAX : tsa::PROD_MIN;
 }
 
+// Luts for q: the small table pointer plus the Horner coefficients
+// (binom(-q, k) and log1p(d)/d), computed here once per call in fp64.
+tsa::Luts make_luts(double q, const double *sp) {
+  tsa::Luts l = {};
+  const bool shannon = q == 1.0;
+  l.sp = sp;
+  l.c[0] = 1.0;
+  for (int k = 1; k <= 12; k++) l.c[k] = l.c[k - 1] * (-q - (k - 1)) / k;
+  for (int k = 0; k <= 6; k++) l.lc[k] = (k & 1 ? -1.0 : 1.0) / (k + 1);
+  // truncation |binom(-q, deg+1)| d^(deg+1), d < 2^-10: deg 5 is < 2^-57 for q <= 2
+  l.deg = q <= 2.0 ? 5 : q <= 10.0 ? 6 : 12;
+  l.iqm1 = shannon ? 0.0 : 1.0 / (q - 1.0);
+  l.omq = 1.0 - q;
+  l.shannon = shannon;
+  return l;
+}
+
 // R-table row stride: >= bins + 8 (8-column groups read past M-2 into NaN) and even
 inline int rstride(int32_t bins) { return (bins + 8 + 1) & ~1; }
 
@@ -103,38 +120,47 @@ bool use_rtable(int32_t bins, int32_t k, int32_t objective) {
 }
 
 struct SearchWs {
-  double *ipow = nullptr, *lnn = nullptr, *rcp = nullptr;
+  double *sp = nullptr;  // small class-term table (Luts::sp)
   uint32_t *cC = nullptr, *fC = nullptr;
   double *cWhi = nullptr, *cWlo = nullptr, *fWhi = nullptr, *fWlo = nullptr;
   int32_t *cBin = nullptr, *fBin = nullptr;
   double *Asuf = nullptr, *R = nullptr, *PP = nullptr, *AI = nullptr;
   int32_t *M = nullptr;
-  int32_t *counter = nullptr;  // dynamic work-item counter of the k >= 3 search
+  int32_t *counter = nullptr;  // dynamic work-item counter of the k >= 3 / k = 2 search
+  int32_t *mmax = nullptr;     // max M over slices (k = 2 block search)
+  double *item_score = nullptr;  // [nb][nz] k = 2 a-block partials
+  uint64_t *item_key = nullptr;
 };
+
+// a-blocks of 32 first thresholds of the k = 2 block search (upper bound: M <= bins)
+inline int k2_blocks(int32_t bins) { return bins >= 3 ? (bins - 3) / 32 + 1 : 1; }
 
 size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, int32_t k,
                     double q, int32_t objective, int32_t enumeration) {
   const size_t E = (size_t)bins + 1;
-  const bool shannon = q == 1.0;
-  if (shannon) {
-    w.lnn = c.take<double>((size_t)N + 1);
-    w.rcp = c.take<double>((size_t)N + 1);
-  } else {
-    w.ipow = c.take<double>((size_t)N + 1);
-  }
-  w.cC = c.take<uint32_t>(nz * E);
-  w.cWhi = c.take<double>(nz * E);
-  w.cWlo = c.take<double>(nz * E);
-  w.cBin = c.take<int32_t>(nz * E);
+  (void)N;
+  (void)q;
+  w.sp = c.take<double>(tsa::kSmallLut);
+  // + kPad entries: the k = 2 kernel reads up to kK2Rows rows past a slice's end
+  const size_t kPad = 8;
+  w.cC = c.take<uint32_t>(nz * E + kPad);
+  w.cWhi = c.take<double>(nz * E + kPad);
+  w.cWlo = c.take<double>(nz * E + kPad);
+  w.cBin = c.take<int32_t>(nz * E + kPad);
   if (enumeration == TSA_ENUM_FULL) {
-    w.fC = c.take<uint32_t>(nz * E);
-    w.fWhi = c.take<double>(nz * E);
-    w.fWlo = c.take<double>(nz * E);
-    w.fBin = c.take<int32_t>(nz * E);
+    w.fC = c.take<uint32_t>(nz * E + kPad);
+    w.fWhi = c.take<double>(nz * E + kPad);
+    w.fWlo = c.take<double>(nz * E + kPad);
+    w.fBin = c.take<int32_t>(nz * E + kPad);
   }
-  w.Asuf = c.take<double>(nz * (size_t)bins);
+  w.Asuf = c.take<double>(nz * (size_t)bins + kPad);
   w.M = c.take<int32_t>(nz);
-  w.counter = c.take<int32_t>(1);
+  w.counter = c.take<int32_t>(2);
+  w.mmax = w.counter + 1;
+  if (k == 2) {
+    w.item_score = c.take<double>((size_t)k2_blocks(bins) * nz);
+    w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * nz);
+  }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
     w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
@@ -183,7 +209,8 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
   // k <= 2: flattened tuple-parallel kernel (tables staged in shared memory)
   if constexpr (MODE != tsa::SPP) {
     if (k <= 2) {
-      const size_t smem = (size_t)(2 * a.E + 2 * a.L) * sizeof(double) + (size_t)a.E * sizeof(uint32_t);
+      const size_t smem = (size_t)(2 * a.E + 2 * a.L + tsa::kSmallLut) * sizeof(double) +
+                          (size_t)a.E * sizeof(uint32_t);
       // large tables fill shared memory: one 1024-thread CTA per SM instead
       const bool big = a.L > 1024;
       auto f = big ? (k == 1 ? tsa::k_search_flat<1, MODE, 1024> : tsa::k_search_flat<2, MODE, 1024>)
@@ -265,6 +292,9 @@ tsa_status tsa_validate(const tsa_problem *p) {
 
 int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
   if (nz <= 0 || enumeration == TSA_ENUM_DP) return 1;
+  // k <= 2: the search kernels balance their work internally (k = 2: per-warp
+  // a-block items from a global queue), so one unit per slice
+  if (k <= 2) return 1;
   const double target = (double)g_num_sms() * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
@@ -329,7 +359,7 @@ static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
   w.partial = c.take<uint32_t>((size_t)p->nz * std::max(kFusedHC, kCompactHC) * p->bins);
   w.povf = c.take<int32_t>((size_t)p->nz * std::max(kFusedHC, kCompactHC));
   w.counters = c.take<int32_t>(2 + 2 * (size_t)p->nz);
-  w.luts = c.take<double>(2 * ((size_t)p->nx * p->ny + 1));
+  w.luts = c.take<double>(tsa::kSmallLut);
   if (o) *o = w;
   return c.off;
 }
@@ -381,23 +411,16 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
   a.partial = w.partial;
   a.povf = w.povf;
   a.counters = w.counters;
-  a.ipow = shannon ? nullptr : w.luts;
-  a.lnn = shannon ? w.luts : nullptr;
-  a.rcp = shannon ? w.luts + (N + 1) : nullptr;
-  a.luts.ipow = a.ipow;
-  a.luts.lnn = a.lnn;
-  a.luts.rcp = a.rcp;
-  a.luts.iqm1 = shannon ? 0.0 : 1.0 / (p->q - 1.0);
-  a.luts.omq = 1.0 - p->q;
-  a.luts.shannon = shannon;
+  a.sp = w.luts;
+  a.luts = make_luts(p->q, w.luts);
   a.HC = kFusedHC;
   a.LC = kFusedLC;
   a.SB = p->slab_slices > 0 ? p->slab_slices : 16;
   a.DM = 2;
   a.DL = p->label_lag > 0 ? std::max(a.DM + 1, p->label_lag) : 6;
   a.nslab = (int)((p->nz + a.SB - 1) / a.SB);
-  a.lut_per = 4096;
-  a.nlut = (int)((N + 1 + a.lut_per - 1) / a.lut_per);
+  a.lut_per = 1024;
+  a.nlut = (tsa::kSmallLut + a.lut_per - 1) / a.lut_per;
   const int L = p->bins, E = L + 1;
   const size_t smem_h = (size_t)(kFusedThreads / 32) * L * sizeof(uint32_t);
   const size_t smem_m = (size_t)((L + 1) & ~1) * 4 + (size_t)L * 8 * 3 + (size_t)E * 8 * 2 + (size_t)E * 8;
@@ -410,7 +433,7 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
     // profiles/r1_compact_sweep.log)
     const int hist_per_sm = p->slab_slices > 0 ? p->slab_slices : 4;
     const int hgrid = (int)std::min<int64_t>((int64_t)a.HC * p->nz, (int64_t)hist_per_sm * g_num_sms());
-    const int lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 1 + 255) / 256, 2 * g_num_sms()));
+    const int lgrid = (tsa::kSmallLut + 255) / 256;
     a.nlut = lgrid;
     size_t sh = smem_h + 64;
     if (p->slab_slices > 0)  // explicit limit: pad shared memory (keeps ~30 KB for k_mid CTAs)
@@ -547,19 +570,9 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   cudaStream_t s = S(stream);
   const bool shannon = q == 1.0;
   const int mode = search_mode(q, objective);
-  tsa::Luts l;
-  l.ipow = w.ipow;
-  l.lnn = w.lnn;
-  l.rcp = w.rcp;
-  l.iqm1 = shannon ? 0.0 : 1.0 / (q - 1.0);
-  l.omq = 1.0 - q;
-  l.shannon = shannon;
-  {
-    const int threads = 256;
-    const int64_t blocks = std::min<int64_t>((N + threads) / threads, 4 * g_num_sms());
-    tsa::k_luts<<<(unsigned)blocks, threads, 0, s>>>(w.ipow, w.lnn, w.rcp, N, q, shannon);
-    TSA_TRY(check_cuda("k_luts"));
-  }
+  const tsa::Luts l = make_luts(q, w.sp);
+  tsa::k_small_luts<<<(tsa::kSmallLut + 255) / 256, 256, 0, s>>>(w.sp, q, shannon);
+  TSA_TRY(check_cuda("k_small_luts"));
   const int E = bins + 1;
   tsa::ScanArgs sa;
   sa.hist = hist;
@@ -581,7 +594,9 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   sa.fBin = w.fBin;
   sa.Asuf = w.Asuf;
   sa.M = w.M;
+  sa.mmax = w.mmax;
   sa.luts = l;
+  TSA_CUDA(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int32_t), s));
 
   switch (mode) {
     case tsa::PROD_MAX: launch_scan<tsa::PROD_MAX>(sa, s); break;
@@ -661,6 +676,27 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.units = units;
   a.unit_begin = unit_begin;
   a.nunits = unit_end - unit_begin;
+  a.mmax = w.mmax;
+  a.item_score = w.item_score;
+  a.item_key = w.item_key;
+  if (k == 2 && mode != tsa::SPP) {
+    // warp-per-a-block search from a global item queue, then the per-unit fold
+    const int grid = 4 * g_num_sms();
+    auto kern = tsa::k_search_k2<tsa::SUM, 6>;
+    if (mode == tsa::PROD_MAX)
+      kern = l.deg == 5 ? tsa::k_search_k2<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MAX, 6>
+                                                                          : tsa::k_search_k2<tsa::PROD_MAX, 12>;
+    else if (mode == tsa::PROD_MIN)
+      kern = l.deg == 5 ? tsa::k_search_k2<tsa::PROD_MIN, 5> : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MIN, 6>
+                                                                          : tsa::k_search_k2<tsa::PROD_MIN, 12>;
+    kern<<<grid, 256, 0, s>>>(a);
+    TSA_TRY(check_cuda("k_search_k2"));
+    const int64_t nt = nz * (int64_t)a.nunits;
+    tsa::k_merge_items<<<(unsigned)((nt + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, w.M, slice_status,
+                                                                  nz, units, unit_begin, a.nunits, part_score,
+                                                                  part_key);
+    return check_cuda("k_merge_items");
+  }
   dim3 grid((unsigned)(unit_end - unit_begin), (unsigned)nz);
   switch (mode) {
     case tsa::PROD_MAX: launch_search_mode<tsa::PROD_MAX>(k, a, grid, s, rt); break;
@@ -669,6 +705,24 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     default: launch_search_mode<tsa::SPP>(k, a, grid, s, false); break;
   }
   return check_cuda("k_search");
+}
+
+size_t tsa_class_consts_workspace_size(void) { return (size_t)tsa::kSmallLut * sizeof(double); }
+
+tsa_status tsa_class_consts(const uint32_t *n, int64_t count, double q, double *a, double *b,
+                            void *workspace, size_t workspace_bytes, void *stream) {
+  if (!n || !a || count < 0 || !(q > 0.0) || !std::isfinite(q) || !workspace)
+    return set_error(TSA_ERR_INVALID_ARG, "class_consts args");
+  if (workspace_bytes < tsa_class_consts_workspace_size())
+    return set_error(TSA_ERR_WORKSPACE, "class_consts workspace too small");
+  cudaStream_t s = S(stream);
+  double *sp = reinterpret_cast<double *>(workspace);
+  tsa::k_small_luts<<<(tsa::kSmallLut + 255) / 256, 256, 0, s>>>(sp, q, q == 1.0);
+  if (count > 0) {
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, 8 * g_num_sms());
+    tsa::k_class_consts<<<(unsigned)blocks, 256, 0, s>>>(n, count, make_luts(q, sp), a, b);
+  }
+  return check_cuda("k_class_consts");
 }
 
 tsa_status tsa_merge(const double *part_score, const uint64_t *part_key, int32_t nparts,
@@ -704,7 +758,7 @@ static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, 
   const size_t smem = (size_t)bins * (sizeof(double) + sizeof(int));
   if (smem > 32 * 1024)
     cudaFuncSetAttribute(tsa::k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tsa::k_finalize<<<(unsigned)nz, 32, smem, s>>>(f);
+  tsa::k_finalize<<<(unsigned)nz, tsa::kFinThreads, smem, s>>>(f);
   return check_cuda("k_finalize");
 }
 
@@ -999,7 +1053,7 @@ struct HuWs {
   char *search;
   size_t search_bytes;
   int32_t units;
-  double *luts;  // [2][n + 1]: 1/n^q (or ln n, 1/n) for the per-slice search kernel
+  double *luts;  // small class-term table (Luts::sp) for the per-slice search kernel
 };
 
 static size_t carve_hu(const tsa_hu_problem *p, char *base, HuWs *o) {
@@ -1016,7 +1070,7 @@ static size_t carve_hu(const tsa_hu_problem *p, char *base, HuWs *o) {
   w.pk = c.take<uint64_t>((size_t)w.units * p->nz);
   w.search_bytes = tsa_search_workspace_size(p->nz, n, 256, p->k, p->q, p->objective, p->enumeration);
   w.search = c.take<char>(w.search_bytes);
-  w.luts = c.take<double>(2 * ((size_t)n + 1));
+  w.luts = c.take<double>(tsa::kSmallLut);
   if (o) *o = w;
   return c.off;
 }
@@ -1081,17 +1135,11 @@ static tsa_status hu_finish_impl(const tsa_hu_problem *p, const int32_t *win, co
     a.partial = hist8;
     a.povf = w.status;
     a.counters = nullptr;
-    a.ipow = shannon ? nullptr : w.luts;
-    a.lnn = shannon ? w.luts : nullptr;
-    a.rcp = shannon ? w.luts + (n + 1) : nullptr;
-    a.luts.ipow = a.ipow;
-    a.luts.lnn = a.lnn;
-    a.luts.rcp = a.rcp;
-    a.luts.iqm1 = shannon ? 0.0 : 1.0 / (p->q - 1.0);
-    a.luts.omq = 1.0 - p->q;
-    a.luts.shannon = shannon;
+    (void)shannon;
+    a.sp = w.luts;
+    a.luts = make_luts(p->q, w.luts);
     a.HC = 1;
-    const int lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1 + 255) / 256, 2 * g_num_sms()));
+    const int lgrid = (tsa::kSmallLut + 255) / 256;
     tsa::k_lut_part<<<lgrid, 256, 0, s>>>(a);
     TSA_TRY(check_cuda("k_lut_part"));
     const int L = 256, E = L + 1;

@@ -76,14 +76,144 @@ struct SliceTables {
   const double *Asuf;  // Asuf[i] = T(i+1, M-1), i in [0, M-2]
 };
 
+// Class-term constants without an N-sized table.  A class of n voxels needs
+// n^-q (or ln n and 1/n at q == 1) for integer n in [1, 2^31).  Round 1 read
+// them from an (N+1)-entry table: at 12-bit CT (N = 2^20, 8 MB) every k = 2
+// tuple paid an L2 gather.  Here n = 2^s (j + r 2^-s) with j = n >> s in
+// [2^10, 2^11) (s = 0 and r = 0 for n <= 2^11), d = r / (j 2^s) in [0, 2^-10):
+//   n^-q = j^-q * 2^(-s q) * (1 + d)^-q,    (1 + d)^-q = sum_k binom(-q, k) d^k
+//   ln n = ln j + s ln 2 + d * P(d),         P(d) = log1p(d)/d
+//   1/n  = (1/j) 2^-s * (1 + d)^-1
+// from a 33 KB table (j^-q or ln j, 1/j for j <= 2^11; 2^(-s q) or s ln 2) and
+// a Horner polynomial in registers.  Degree 5 (q <= 2), 6 (q <= 10) or 12
+// keeps the truncation below 2^-56 relative for q <= 256; n <= 2^11 reads the table
+// entry itself (d = 0 makes the polynomial exactly 1).  Every kernel uses this
+// one function, so a tuple's value is still a pure function of the tuple.
+constexpr int kSB = 11;               // table bits
+constexpr int kSN = (1 << kSB) + 1;   // entries j = 0 .. 2^kSB
+constexpr int kSmallLut = 2 * kSN + 32;  // doubles in the small table
+
 struct Luts {
-  const double *ipow;  // ipow[n] = 1 / n^q, ipow[0] = NaN   (q != 1)
-  const double *lnn;   // lnn[n] = ln n, lnn[0] = NaN        (q == 1)
-  const double *rcp;   // rcp[n] = 1 / n                     (q == 1)
-  double iqm1;         // 1 / (q - 1)
-  double omq;          // 1 - q
-  int shannon;         // q == 1
+  const double *sp;  // [kSN] j^-q (ln j at q == 1) | [kSN] 1/j | [32] 2^(-s q) (s ln 2); entry j = 0: NaN
+  double c[13];      // binom(-q, k), k = 0..12 (q == 1: (-1)^k)
+  double lc[7];      // log1p(d)/d = sum_k lc[k] d^k = sum (-1)^k d^k / (k+1)
+  int deg;           // 5, 6 or 12 (c[deg+1..] are zero up to c[6])
+  double iqm1;       // 1 / (q - 1)
+  double omq;        // 1 - q
+  int shannon;       // q == 1
 };
+
+// Table access of the class-size constants: the global layout of Luts::sp
+// ([kSN] j^-q | [kSN] 1/j | [32] 2^(-s q)); kernels that stage the table in
+// shared memory use an interleaved {j^-q, 1/j} layout (one 16-byte load) with
+// the same arithmetic, so every kernel computes bit-identical values.
+struct SpGlobal {
+  const double *sp;
+  __device__ __forceinline__ double2 jr(uint32_t j) const { return make_double2(sp[j], sp[kSN + j]); }
+  __device__ __forceinline__ double p2(int s) const { return sp[2 * kSN + s]; }
+};
+struct SpPair {  // shared-memory staging: jr[j] = {j^-q or ln j, 1/j}, p2s[s]
+  const double2 *jrt;
+  const double *p2s;
+  __device__ __forceinline__ double2 jr(uint32_t j) const { return jrt[j]; }
+  __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
+};
+
+// n = 2^s (j + r 2^-s): table index j, exponent s and d = r / (j 2^s)
+__device__ __forceinline__ void nsplit_idx(uint32_t n, uint32_t &j, int &s, uint32_t &r) {
+  s = max(0, 32 - kSB - __clz(n));
+  j = n >> s;
+  r = n - (j << s);
+}
+__device__ __forceinline__ double two_pow_neg(int s) { return __hiloint2double((1023 - s) << 20, 0); }
+
+__device__ __forceinline__ double horner_c(const Luts &l, double d) {
+  double p = l.c[5];
+  if (l.deg > 6) {  // uniform branches
+    double h = l.c[12];
+#pragma unroll
+    for (int k = 11; k >= 6; k--) h = __fma_rn(h, d, l.c[k]);
+    p = __fma_rn(h, d, l.c[5]);
+  } else if (l.deg == 6) {
+    p = __fma_rn(l.c[6], d, l.c[5]);
+  }
+#pragma unroll
+  for (int k = 4; k >= 0; k--) p = __fma_rn(p, d, l.c[k]);
+  return p;
+}
+
+// horner_c with the degree fixed at compile time (DEG = l.deg): the same
+// operations, for kernels specialised on the degree.
+template <int DEG>
+__device__ __forceinline__ double horner_c_deg(const Luts &l, double d) {
+  double p = l.c[5];
+  if (DEG > 6) {
+    double h = l.c[12];
+#pragma unroll
+    for (int k = 11; k >= 6; k--) h = __fma_rn(h, d, l.c[k]);
+    p = __fma_rn(h, d, l.c[5]);
+  } else if (DEG == 6) {
+    p = __fma_rn(l.c[6], d, l.c[5]);
+  }
+#pragma unroll
+  for (int k = 4; k >= 0; k--) p = __fma_rn(p, d, l.c[k]);
+  return p;
+}
+
+// d = (r * (1/j)) * 2^-s with the exact power-of-two scaling done on the
+// exponent field (r >= 1: r/j >= 2^-11, so the result stays normal); equal to
+// __dmul_rn(x, two_pow_neg(s)) bit for bit.
+__device__ __forceinline__ double scale_pow2_neg(double x, int s, uint32_t r) {
+  const int hi = __double2hiint(x) - (s << 20);
+  return r ? __hiloint2double(hi, __double2loint(x)) : 0.0;
+}
+
+// n^-q (q != 1); NaN at n = 0
+template <class Tab>
+__device__ __forceinline__ double ipow_t(const Luts &l, const Tab &tab, uint32_t n) {
+  uint32_t j, r;
+  int s;
+  nsplit_idx(n, j, s, r);
+  const double2 e = tab.jr(j);
+  const double d = __dmul_rn(__dmul_rn((double)r, e.y), two_pow_neg(s));
+  return __dmul_rn(__dmul_rn(e.x, tab.p2(s)), horner_c(l, d));
+}
+
+// Shannon class term S = ln n - w / n (q == 1); NaN at n = 0
+template <class Tab>
+__device__ __forceinline__ double shannon_t(const Luts &l, const Tab &tab, uint32_t n, double w) {
+  uint32_t j, r;
+  int s;
+  nsplit_idx(n, j, s, r);
+  const double2 e = tab.jr(j);
+  const double two_ms = two_pow_neg(s);
+  const double d = __dmul_rn(__dmul_rn((double)r, e.y), two_ms);
+  double p = l.lc[6];
+#pragma unroll
+  for (int k = 5; k >= 0; k--) p = __fma_rn(p, d, l.lc[k]);
+  const double lnn = __dadd_rn(__dadd_rn(e.x, tab.p2(s)), __dmul_rn(d, p));
+  const double rcp = __dmul_rn(__dmul_rn(e.y, two_ms), horner_c(l, d));
+  return __dsub_rn(lnn, __dmul_rn(w, rcp));
+}
+
+__device__ __forceinline__ double ipow_n(const Luts &l, uint32_t n) { return ipow_t(l, SpGlobal{l.sp}, n); }
+__device__ __forceinline__ double shannon_term(const Luts &l, uint32_t n, double w) {
+  return shannon_t(l, SpGlobal{l.sp}, n, w);
+}
+
+// The class term from its count n and weight w (see class_term).
+template <int MODE, class Tab>
+__device__ __forceinline__ double class_term_nw(const Luts &l, const Tab &tab, uint32_t n, double w) {
+  if (MODE == PROD_MAX || MODE == PROD_MIN) {
+    return __dmul_rn(w, ipow_t(l, tab, n));
+  } else if (MODE == SUM) {
+    return shannon_t(l, tab, n, w);
+  } else {
+    if (l.shannon) return shannon_t(l, tab, n, w);
+    const double A = __dmul_rn(w, ipow_t(l, tab, n));
+    return __dmul_rn(__dsub_rn(1.0, A), l.iqm1);
+  }
+}
 
 // Class term T(a, b) of the class made of table positions [a, b]:
 //   q != 1, pseudo-additive: A = W / n^q = sum_{i in C} (c_i / n)^q
@@ -96,15 +226,27 @@ __device__ __forceinline__ double class_term(const SliceTables &t, const Luts &l
   // generic loads: the tables may be staged in shared memory
   const uint32_t n = t.C[b + 1] - t.C[a];
   const double w = dd_diff(t.Whi[b + 1], t.Wlo[b + 1], t.Whi[a], t.Wlo[a]);
-  if (MODE == PROD_MAX || MODE == PROD_MIN) {
-    return __dmul_rn(w, __ldg(l.ipow + n));
-  } else if (MODE == SUM) {
-    return __dsub_rn(__ldg(l.lnn + n), __dmul_rn(w, __ldg(l.rcp + n)));
-  } else {
-    if (l.shannon) return __dsub_rn(__ldg(l.lnn + n), __dmul_rn(w, __ldg(l.rcp + n)));
-    const double A = __dmul_rn(w, __ldg(l.ipow + n));
-    return __dmul_rn(__dsub_rn(1.0, A), l.iqm1);
+  return class_term_nw<MODE>(l, SpGlobal{l.sp}, n, w);
+}
+
+// Entry e of the small table (Luts::sp layout).
+__device__ __forceinline__ double small_lut_entry(int e, double q, int shannon) {
+  if (e < kSN) {
+    const double x = (double)e;
+    return e == 0 ? CUDART_NAN : (shannon ? log(x) : __drcp_rn(pow(x, q)));
   }
+  if (e < 2 * kSN) {
+    const int j = e - kSN;
+    return j == 0 ? CUDART_NAN : __drcp_rn((double)j);
+  }
+  const double x = ldexp(1.0, e - 2 * kSN);
+  return shannon ? log(x) : __drcp_rn(pow(x, q));
+}
+
+// Fills the small table of Luts::sp (kSmallLut doubles); any grid.
+__global__ void k_small_luts(double *sp, double q, int shannon) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kSmallLut; e += gridDim.x * blockDim.x)
+    sp[e] = small_lut_entry(e, q, shannon);
 }
 
 template <int MODE>

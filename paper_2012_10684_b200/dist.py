@@ -78,6 +78,25 @@ def gather_partials(score: torch.Tensor, key: torch.Tensor, group=None):
     return s.view(world, n), k.view(world, n)
 
 
+def agreed_units(nz_total, bins, k, enum, world, units=0, group=None, device=None) -> int:
+    """Work units per slice, identical on every rank.  The library heuristic
+    depends on the local SM count, so every rank proposes its value and the
+    group takes the maximum (one tiny all-reduce): unit_range() then
+    partitions the same unit space on every rank even on mixed devices.  The
+    interval DP has exactly one unit per slice (tsa_search rejects more)."""
+    if enum == ENUMERATIONS["dp"]:
+        return 1
+    if units > 0:
+        return units
+    U = max(world, tsa_default_units(nz_total, bins, k, enum))
+    if world > 1:
+        t = torch.tensor([U], dtype=torch.int64,
+                         device=device if dist.get_backend(group) != "gloo" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        U = int(t.item())
+    return U
+
+
 def segment_slabs(vol_slab, bins, k, q, **kw):
     """Slab sharding: this rank's slices only, no collective."""
     return tsa_segment(vol_slab, bins, k, q, **kw)
@@ -103,7 +122,7 @@ def segment_tuple_sharded(vol_slab, nz_total, bins, k, q, objective="pseudo_addi
     hist = gather_rows(hist_l, per, group)[:nz_total].contiguous()
     status = gather_rows(st_l, per, group)[:nz_total].contiguous()
     enum = ENUMERATIONS.get(enumeration, enumeration)
-    U = units if units > 0 else max(world, tsa_default_units(nz_total, bins, k, enum))
+    U = agreed_units(nz_total, bins, k, enum, world, units, group, dev)
     u0, u1 = unit_range(U, world, rank)
     if u1 > u0:
         ps, pk = tsa_search(hist, status, nx * ny, k, q, objective, enumeration, units=U,

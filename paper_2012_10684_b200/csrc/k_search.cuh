@@ -36,6 +36,8 @@ struct SearchArgs {
   const int32_t *mmax; // max over slices of M (k_scan), k = 2 block kernel
   double *item_score;  // [nbmax][nz] per-(a-block, slice) partials of the k = 2 block kernel
   uint64_t *item_key;
+  const K2Row *rows;   // [nz][RE] packed positions (k_scan) for the k = 2 block kernel
+  int RE;
   double *part_score;  // [nunits][nz]
   uint64_t *part_key;
   Luts luts;
@@ -700,7 +702,7 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
   const double2 e = tab.jr(j);
   if (MODE == PROD_MAX || MODE == PROD_MIN) {
     const double d = scale_pow2_neg(__dmul_rn((double)r, e.y), s, r);
-    const double ip = __dmul_rn(__dmul_rn(e.x, tab.p2(s)), horner_c_deg<DEG>(l, d));
+    const double ip = __dmul_rn(__dmul_rn(e.x, l.p2[s]), horner_c_deg<DEG>(l, d));
     return __dmul_rn(w, ip);
   } else {
     return shannon_t(l, tab, n, w);
@@ -710,11 +712,9 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
 template <int MODE, int DEG>
 __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
-  __shared__ double s_p2[32];
   for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
-  if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.sp[2 * kSN + threadIdx.x];
   __syncthreads();
-  const SpPair tab{s_jr, s_p2};
+  const SpPair tab{s_jr};
   const Luts &l = g.luts;
   const int lane = threadIdx.x & 31;
   const int mmax = *g.mmax;
@@ -737,26 +737,25 @@ __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
     double best = -CUDART_INF;
     uint64_t bestkey = kKeyNone;
     if (g.status[z] == kOK && 32 * i <= M - 3) {
-      const uint32_t *C = g.C + (size_t)z * g.E;
-      const double *Whi = g.Whi + (size_t)z * g.E, *Wlo = g.Wlo + (size_t)z * g.E;
-      const double *As = g.Asuf + (size_t)z * g.L;
+      const K2Row *rz = g.rows + (size_t)z * g.RE;
       const int a = 32 * i + lane;
       const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
-      const uint32_t Ca = __ldg(C + ac + 1);
-      const double Wah = __ldg(Whi + ac + 1), Wal = __ldg(Wlo + ac + 1);
+      const K2Row ra = rz[ac + 1];
+      const uint32_t Ca = ra.c;
+      const double Wah = ra.wh, Wal = ra.wl;
       // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
       const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
       const int bend = M - 2;
       int b0 = 32 * i + 1;
-      const uint32_t *pC = C + b0 + 1;
-      const double *pWh = Whi + b0 + 1, *pWl = Wlo + b0 + 1, *pA = As + b0;
-      for (; b0 <= bend; b0 += kK2Rows, pC += kK2Rows, pWh += kK2Rows, pWl += kK2Rows, pA += kK2Rows) {
+      for (const K2Row *pr = rz + b0 + 1; b0 <= bend; b0 += kK2Rows, pr += kK2Rows) {
         double vb[kK2Rows];
 #pragma unroll
         for (int r = 0; r < kK2Rows; r++) {
-          const uint32_t n = __ldg(pC + r) - Ca;
-          const double wm = dd_diff(__ldg(pWh + r), __ldg(pWl + r), Wah, Wal);
-          const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), __ldg(pA + r));
+          const double2 x = __ldg(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
+          const double2 y = __ldg(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
+          const uint32_t n = (uint32_t)__double2loint(y.y) - Ca;
+          const double wm = dd_diff(x.x, x.y, Wah, Wal);
+          const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), y.x);
           double v = combine<MODE>(pre, R);
           if (MODE == PROD_MIN) v = -v;
           vb[r] = v;
@@ -765,8 +764,7 @@ __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
         for (int r = 0; r < kK2Rows; r++) {
           const int b = b0 + r;
           if (vb[r] >= best && a < b && b <= bend) {
-            const uint64_t key = ((uint64_t)__ldg(g.Bin + (size_t)z * g.E + a + 1) << 12) |
-                                 (uint64_t)__ldg(g.Bin + (size_t)z * g.E + b + 1);
+            const uint64_t key = ((uint64_t)ra.bin << 12) | (uint64_t)rz[b + 1].bin;
             if (better(vb[r], key, best, bestkey)) {
               best = vb[r];
               bestkey = key;

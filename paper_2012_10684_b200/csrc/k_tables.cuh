@@ -35,6 +35,8 @@ struct ScanArgs {
   double *Asuf;          // [nz][L]
   int32_t *M;            // [nz] entries used by the search (m or L)
   int32_t *mmax;         // max over slices of M (atomicMax; zeroed before launch) or null
+  K2Row *rows;           // [nz][RE] packed positions for the k = 2 search, or null
+  int RE;                // row stride of `rows`
   Luts luts;
 };
 
@@ -165,7 +167,13 @@ __global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
   if (status != kOK) return;
   SliceTables t{tC, tWhi, tWlo, nullptr};
   double *Asuf = g.Asuf + z * L;
-  for (int i = tid; i <= M - 2; i += blockDim.x) Asuf[i] = class_term<MODE>(t, g.luts, i + 1, M - 1);
+  const int32_t *tBin = g.full ? g.fBin + z * E : cBin;
+  K2Row *rows = g.rows ? g.rows + z * g.RE : nullptr;
+  for (int i = tid; i <= M - 2; i += blockDim.x) {
+    const double as = class_term<MODE>(t, g.luts, i + 1, M - 1);
+    Asuf[i] = as;
+    if (rows) rows[i + 1] = K2Row{tWhi[i + 1], tWlo[i + 1], as, tC[i + 1], tBin[i + 1]};
+  }
 }
 
 // R[a][b] = combine(T(a+1, b), Asuf[b]) for 0 <= a < b <= M-2 (k >= 3,

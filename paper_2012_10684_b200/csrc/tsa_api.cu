@@ -106,6 +106,10 @@ tsa::Luts make_luts(double q, const double *sp) {
   for (int k = 0; k <= 6; k++) l.lc[k] = (k & 1 ? -1.0 : 1.0) / (k + 1);
   // truncation |binom(-q, deg+1)| d^(deg+1), d < 2^-10: deg 5 is < 2^-57 for q <= 2
   l.deg = q <= 2.0 ? 5 : q <= 10.0 ? 6 : 12;
+  for (int s = 0; s < 32; s++) {
+    const double x = std::ldexp(1.0, s);
+    l.p2[s] = shannon ? std::log(x) : 1.0 / std::pow(x, q);
+  }
   l.iqm1 = shannon ? 0.0 : 1.0 / (q - 1.0);
   l.omq = 1.0 - q;
   l.shannon = shannon;
@@ -130,7 +134,12 @@ struct SearchWs {
   int32_t *mmax = nullptr;     // max M over slices (k = 2 block search)
   double *item_score = nullptr;  // [nb][nz] k = 2 a-block partials
   uint64_t *item_key = nullptr;
+  tsa::K2Row *rows = nullptr;    // [nz][k2_row_stride] packed positions (k = 2)
 };
+
+// row stride of the k = 2 packed positions: entries 0..bins plus the rows the
+// kernel reads past a slice's end (kK2Rows)
+inline int k2_row_stride(int32_t bins) { return bins + 1 + 8; }
 
 // a-blocks of 32 first thresholds of the k = 2 block search (upper bound: M <= bins)
 inline int k2_blocks(int32_t bins) { return bins >= 3 ? (bins - 3) / 32 + 1 : 1; }
@@ -160,6 +169,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   if (k == 2) {
     w.item_score = c.take<double>((size_t)k2_blocks(bins) * nz);
     w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * nz);
+    w.rows = c.take<tsa::K2Row>(nz * (size_t)k2_row_stride(bins) + kPad);
   }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
@@ -535,7 +545,12 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   if (pack16) chunks = (int)std::max<int64_t>(chunks, (a.n + (threads / 32) * 60000 - 1) / ((threads / 32) * 60000));
   a.chunks = chunks;
   dim3 grid((unsigned)chunks, (unsigned)p->nz);
-  if (p->dtype == TSA_U8 && p->bins == 256) {
+  if (p->dtype == TSA_U16) {
+    // one bin copy + overflow slot; ~128 K voxels (256 KB) per CTA
+    a.chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (a.n + 131071) / 131072));
+    const size_t sm16 = (size_t)(p->bins + 1) * sizeof(uint32_t);
+    tsa::k_hist16<<<dim3((unsigned)a.chunks, (unsigned)p->nz), threads, sm16, s>>>(a);
+  } else if (p->dtype == TSA_U8 && p->bins == 256) {
     tsa::k_histogram<uint8_t, false><<<grid, threads, smem, s>>>(a);
   } else if (p->dtype == TSA_U8) {
     tsa::k_histogram<uint8_t, true><<<grid, threads, smem, s>>>(a);
@@ -595,6 +610,8 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   sa.Asuf = w.Asuf;
   sa.M = w.M;
   sa.mmax = w.mmax;
+  sa.rows = (k == 2 && mode != tsa::SPP) ? w.rows : nullptr;
+  sa.RE = k2_row_stride(bins);
   sa.luts = l;
   TSA_CUDA(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int32_t), s));
 
@@ -679,6 +696,8 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.mmax = w.mmax;
   a.item_score = w.item_score;
   a.item_key = w.item_key;
+  a.rows = w.rows;
+  a.RE = k2_row_stride(bins);
   if (k == 2 && mode != tsa::SPP) {
     // warp-per-a-block search from a global item queue, then the per-unit fold
     const int grid = 4 * g_num_sms();

@@ -84,17 +84,29 @@ struct SliceTables {
 //   n^-q = j^-q * 2^(-s q) * (1 + d)^-q,    (1 + d)^-q = sum_k binom(-q, k) d^k
 //   ln n = ln j + s ln 2 + d * P(d),         P(d) = log1p(d)/d
 //   1/n  = (1/j) 2^-s * (1 + d)^-1
-// from a 33 KB table (j^-q or ln j, 1/j for j <= 2^11; 2^(-s q) or s ln 2) and
+// from a 32 KB table (j^-q or ln j, 1/j for j <= 2^11), 2^(-s q) or s ln 2 (in
+// the kernel parameters) and
 // a Horner polynomial in registers.  Degree 5 (q <= 2), 6 (q <= 10) or 12
 // keeps the truncation below 2^-56 relative for q <= 256; n <= 2^11 reads the table
 // entry itself (d = 0 makes the polynomial exactly 1).  Every kernel uses this
 // one function, so a tuple's value is still a pure function of the tuple.
 constexpr int kSB = 11;               // table bits
 constexpr int kSN = (1 << kSB) + 1;   // entries j = 0 .. 2^kSB
-constexpr int kSmallLut = 2 * kSN + 32;  // doubles in the small table
+constexpr int kSmallLut = 2 * kSN;  // doubles in the small table
+
+// One table position of a slice, packed for the k = 2 search (two 16-byte
+// loads): W = dd prefix of w at the position, as = Asuf[e-1] = T(e, M-1),
+// c = prefix count, bin = the bin of the position.
+struct __align__(16) K2Row {
+  double wh, wl, as;
+  uint32_t c;
+  int32_t bin;
+};
 
 struct Luts {
-  const double *sp;  // [kSN] j^-q (ln j at q == 1) | [kSN] 1/j | [32] 2^(-s q) (s ln 2); entry j = 0: NaN
+  const double *sp;  // [kSN] j^-q (ln j at q == 1) | [kSN] 1/j; entry j = 0: NaN
+  double p2[32];     // 2^(-s q) (q == 1: ln 2^s), s = 0..31, from the host (kernel parameter:
+                     // constant cache, off the shared-memory path)
   double c[13];      // binom(-q, k), k = 0..12 (q == 1: (-1)^k)
   double lc[7];      // log1p(d)/d = sum_k lc[k] d^k = sum (-1)^k d^k / (k+1)
   int deg;           // 5, 6 or 12 (c[deg+1..] are zero up to c[6])
@@ -110,13 +122,10 @@ struct Luts {
 struct SpGlobal {
   const double *sp;
   __device__ __forceinline__ double2 jr(uint32_t j) const { return make_double2(sp[j], sp[kSN + j]); }
-  __device__ __forceinline__ double p2(int s) const { return sp[2 * kSN + s]; }
 };
-struct SpPair {  // shared-memory staging: jr[j] = {j^-q or ln j, 1/j}, p2s[s]
+struct SpPair {  // shared-memory staging: jr[j] = {j^-q or ln j, 1/j}
   const double2 *jrt;
-  const double *p2s;
   __device__ __forceinline__ double2 jr(uint32_t j) const { return jrt[j]; }
-  __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
 };
 
 // n = 2^s (j + r 2^-s): table index j, exponent s and d = r / (j 2^s)
@@ -176,7 +185,7 @@ __device__ __forceinline__ double ipow_t(const Luts &l, const Tab &tab, uint32_t
   nsplit_idx(n, j, s, r);
   const double2 e = tab.jr(j);
   const double d = __dmul_rn(__dmul_rn((double)r, e.y), two_pow_neg(s));
-  return __dmul_rn(__dmul_rn(e.x, tab.p2(s)), horner_c(l, d));
+  return __dmul_rn(__dmul_rn(e.x, l.p2[s]), horner_c(l, d));
 }
 
 // Shannon class term S = ln n - w / n (q == 1); NaN at n = 0
@@ -191,7 +200,7 @@ __device__ __forceinline__ double shannon_t(const Luts &l, const Tab &tab, uint3
   double p = l.lc[6];
 #pragma unroll
   for (int k = 5; k >= 0; k--) p = __fma_rn(p, d, l.lc[k]);
-  const double lnn = __dadd_rn(__dadd_rn(e.x, tab.p2(s)), __dmul_rn(d, p));
+  const double lnn = __dadd_rn(__dadd_rn(e.x, l.p2[s]), __dmul_rn(d, p));
   const double rcp = __dmul_rn(__dmul_rn(e.y, two_ms), horner_c(l, d));
   return __dsub_rn(lnn, __dmul_rn(w, rcp));
 }
@@ -235,12 +244,8 @@ __device__ __forceinline__ double small_lut_entry(int e, double q, int shannon) 
     const double x = (double)e;
     return e == 0 ? CUDART_NAN : (shannon ? log(x) : __drcp_rn(pow(x, q)));
   }
-  if (e < 2 * kSN) {
-    const int j = e - kSN;
-    return j == 0 ? CUDART_NAN : __drcp_rn((double)j);
-  }
-  const double x = ldexp(1.0, e - 2 * kSN);
-  return shannon ? log(x) : __drcp_rn(pow(x, q));
+  const int j = e - kSN;
+  return j == 0 ? CUDART_NAN : __drcp_rn((double)j);
 }
 
 // Fills the small table of Luts::sp (kSmallLut doubles); any grid.

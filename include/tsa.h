@@ -215,6 +215,95 @@ tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slice
                             int32_t *status_host, uint8_t *labels_host, void *dev_buf,
                             size_t dev_bytes, void *stream0, void *stream1);
 
+/* ---- q sweep: one histogram, the search and labels for several q --------
+ * PAPER.md:564 ("the alpha coefficient can be adjusted and plays a critical
+ * role in tuning"); BASELINE.json config 3 sweeps q in {0.5, ..., 1.5}.
+ * Equivalent, output for output, to nq tsa_segment calls on the same volume
+ * with p->q replaced by qs[i] (bit-identical; tested), but the volume is
+ * histogrammed once: a1 once, a2-a5 per q, always one kernel per stage.
+ *   qs    host array [nq] of q values (each > 0 and finite), nq in 1..64
+ *   outs  host array [nq] of tsa_outputs; outs[i] receives the results of
+ *         qs[i] (thresholds required; labels / objective / slice_status
+ *         optional; every non-NULL histogram receives the volume's histogram)
+ *   workspace  tsa_sweep_workspace_size(p, qs, nq) bytes (p->q is ignored) */
+size_t tsa_sweep_workspace_size(const tsa_problem *p, const double *qs, int32_t nq);
+tsa_status tsa_segment_sweep(const tsa_problem *p, const double *qs, int32_t nq,
+                             const tsa_outputs *outs, void *workspace, size_t workspace_bytes,
+                             void *stream);
+
+/* ---- multi-GPU: one process per GPU, slices or tuples sharded ------------
+ * (SURVEY.md §8(b),(e); "job distribution ... reduction of
+ * results from different devices", Table "multiple" PAPER.md:726-739.)
+ *
+ * A tsa_comm is an all-gather transport between nranks processes, each
+ * driving one GPU.  tsa_comm_init builds it on NCCL (libnccl.so.2, loaded
+ * at the first call with dlopen; the communicator is owned by the tsa_comm
+ * and freed by tsa_comm_destroy -- the one object the library allocates).
+ * tsa_comm_init_custom wraps a caller-provided all-gather instead (any
+ * transport: MPI, gloo, shared memory; the tests use it to run two ranks on
+ * one GPU, which NCCL refuses).
+ *
+ * Slab partition (tsa_slab_range): rank r owns slices [r c, min(nz, (r+1) c)),
+ * c = ceil(nz / nranks); trailing ranks may own none.
+ *
+ * tsa_segment_sharded, on `stream`, with `slab` = this rank's slices (slab->nz
+ * = z1 - z0, may be 0 with volume NULL in TUPLES mode) and nz_total slices in
+ * the whole volume:
+ *   TSA_SHARD_SLICES  slices are independent problems: the rank segments its
+ *                     slab with no exchange (tsa_segment); every output refers
+ *                     to the slab.  The comm is only checked (rank, nranks).
+ *   TSA_SHARD_TUPLES  the tuple space of EVERY slice is split over the ranks
+ *                     (large k): histogram of the own slab -> all-gather of
+ *                     the histograms and statuses -> exhaustive search of the
+ *                     rank's share of the work units of all nz_total slices
+ *                     -> per-slice merge -> all-gather of the (score, key)
+ *                     partials -> merge under (score desc, key asc) and
+ *                     phi(t*) in the definition's order (tsa_finalize) ->
+ *                     labels of the own slab.  out->thresholds [nz_total][k],
+ *                     objective [nz_total], slice_status [nz_total] and
+ *                     histogram [nz_total][bins] (optional) are identical on
+ *                     every rank; out->labels is the own slab [z1-z0][ny][nx].
+ *                     Work units per slice: slab->units_per_slice, else a
+ *                     rank-independent default (never the local SM count), so
+ *                     the unit ranges partition the same space on every rank
+ *                     and the result is bit-identical to one GPU.
+ * Exchanged bytes per call (TUPLES): nranks c (4 bins + 4) + 16 nranks nz_total.
+ * Transport failures return TSA_ERR_NCCL with detail in tsa_last_error().
+ * The call blocks only as much as the transport does (NCCL: asynchronous on
+ * the stream; a custom all-gather decides). */
+typedef struct tsa_comm tsa_comm;
+typedef enum { TSA_SHARD_SLICES = 0, TSA_SHARD_TUPLES = 1 } tsa_shard_mode;
+#define TSA_COMM_ID_BYTES 128
+
+/* Custom all-gather: gather `bytes` from every rank's `send` into `recv`
+ * (rank-major, nranks * bytes), device pointers, ordered after prior work on
+ * `stream` and before later work on it.  Return 0 on success. */
+typedef int (*tsa_allgather_fn)(void *user, const void *send, void *recv, size_t bytes,
+                                void *stream);
+
+/* id: host buffer of TSA_COMM_ID_BYTES; rank 0 creates it, every rank passes
+ * the same bytes to tsa_comm_init (the caller distributes them). */
+tsa_status tsa_comm_unique_id(unsigned char id[TSA_COMM_ID_BYTES]);
+tsa_status tsa_comm_init(tsa_comm **comm, int32_t nranks, int32_t rank,
+                         const unsigned char id[TSA_COMM_ID_BYTES]);
+tsa_status tsa_comm_init_custom(tsa_comm **comm, int32_t nranks, int32_t rank,
+                                tsa_allgather_fn allgather, void *user);
+tsa_status tsa_comm_destroy(tsa_comm *comm);
+/* 1 = NCCL, 2 = custom, 0 = NULL comm */
+int32_t tsa_comm_kind(const tsa_comm *comm);
+
+/* host: [z0, z1) of `rank` (the partition tsa_segment_sharded expects) */
+tsa_status tsa_slab_range(int64_t nz_total, int32_t nranks, int32_t rank, int64_t *z0, int64_t *z1);
+
+/* Work units per slice TSA_SHARD_TUPLES uses (identical on every rank). */
+int32_t tsa_sharded_units(const tsa_problem *slab, int64_t nz_total, int32_t nranks);
+
+size_t tsa_sharded_workspace_size(const tsa_problem *slab, int64_t nz_total, int32_t shard_mode,
+                                  const tsa_comm *comm);
+tsa_status tsa_segment_sharded(const tsa_problem *slab, int64_t nz_total, const tsa_outputs *out,
+                               int32_t shard_mode, tsa_comm *comm, void *workspace,
+                               size_t workspace_bytes, void *stream);
+
 /* ---- 2-D Tsallis thresholding: the paper's own formulation -------------
  * (readings DESIGN.md R18-R22)
  *   g(x,y)   = floor( sum_{3x3} f / 9 ), replicate border

@@ -41,7 +41,17 @@ EXPORTS = (
     "tsa_hu_finish",
     "tsa_morph_workspace_size", "tsa_morph",
     "tsa_class_consts_workspace_size", "tsa_class_consts",
+    "tsa_sweep_workspace_size", "tsa_segment_sweep",
+    "tsa_comm_unique_id", "tsa_comm_init", "tsa_comm_init_custom", "tsa_comm_destroy",
+    "tsa_comm_kind", "tsa_slab_range", "tsa_sharded_units", "tsa_sharded_workspace_size",
+    "tsa_segment_sharded",
 )
+TSA_SHARD_SLICES, TSA_SHARD_TUPLES = 0, 1
+SHARD_MODES = {"slices": 0, "tuples": 1}
+COMM_ID_BYTES = 128
+# int (*)(void *user, const void *send, void *recv, size_t bytes, void *stream)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_size_t, ctypes.c_void_p)
 
 
 class TsaError(RuntimeError):
@@ -158,6 +168,17 @@ def load() -> ctypes.CDLL:
         "tsa_morph": (I32, [P, P, I64, I64, I64, I32, I32, P, SZ, P]),
         "tsa_class_consts_workspace_size": (SZ, []),
         "tsa_class_consts": (I32, [P, I64, D, P, P, P, SZ, P]),
+        "tsa_sweep_workspace_size": (SZ, [PP, P, I32]),
+        "tsa_segment_sweep": (I32, [PP, P, I32, PO, P, SZ, P]),
+        "tsa_comm_unique_id": (I32, [P]),
+        "tsa_comm_init": (I32, [ctypes.POINTER(P), I32, I32, P]),
+        "tsa_comm_init_custom": (I32, [ctypes.POINTER(P), I32, I32, ALLGATHER_FN, P]),
+        "tsa_comm_destroy": (I32, [P]),
+        "tsa_comm_kind": (I32, [P]),
+        "tsa_slab_range": (I32, [I64, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "tsa_sharded_units": (I32, [PP, I64, I32]),
+        "tsa_sharded_workspace_size": (SZ, [PP, I64, I32, P]),
+        "tsa_segment_sharded": (I32, [PP, I64, PO, I32, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -276,12 +297,16 @@ def tsa_segment(vol, bins, k, q, objective="pseudo_additive", enumeration="canon
     return out
 
 
-def tsa_histogram(vol, bins, stream=None):
+def tsa_histogram(vol, bins, stream=None, out=None):
+    """(hist [nz,bins] i32 (u32 bits), status [nz] i32); out = (hist, status) to reuse buffers."""
     _need_cuda(vol)
     p = make_problem(vol, bins, 1, 1.0)
     nz = vol.shape[0]
-    hist = torch.empty((nz, bins), dtype=torch.int32, device=vol.device)
-    status = torch.empty(nz, dtype=torch.int32, device=vol.device)
+    if out is not None:
+        hist, status = out
+    else:
+        hist = torch.empty((nz, bins), dtype=torch.int32, device=vol.device)
+        status = torch.empty(nz, dtype=torch.int32, device=vol.device)
     _check(load().tsa_histogram(ctypes.byref(p), _ptr(hist), _ptr(status), _stream(stream)),
            "tsa_histogram")
     return hist, status
@@ -289,7 +314,7 @@ def tsa_histogram(vol, bins, stream=None):
 
 def tsa_search(hist, status, voxels_per_slice, k, q, objective="pseudo_additive",
                enumeration="canonical", units=0, unit_begin=0, unit_end=None, workspace=None,
-               stream=None):
+               stream=None, out=None):
     """Returns (part_score [n_units, nz] f64, part_key [n_units, nz] i64 (u64 bits)).
     `status` is updated in place (NO_VALID_SPLIT)."""
     _need_cuda(hist, status)
@@ -300,8 +325,11 @@ def tsa_search(hist, status, voxels_per_slice, k, q, objective="pseudo_additive"
         units = tsa_default_units(nz, bins, k, enum)
     unit_end = units if unit_end is None else unit_end
     nu = unit_end - unit_begin
-    ps = torch.empty((max(nu, 1), nz), dtype=torch.float64, device=hist.device)
-    pk = torch.empty((max(nu, 1), nz), dtype=torch.int64, device=hist.device)
+    if out is not None:
+        ps, pk = out
+    else:
+        ps = torch.empty((max(nu, 1), nz), dtype=torch.float64, device=hist.device)
+        pk = torch.empty((max(nu, 1), nz), dtype=torch.int64, device=hist.device)
     if workspace is None:
         n = tsa_search_workspace_size(nz, voxels_per_slice, bins, k, q, obj, enum)
         workspace = torch.empty(max(n, 1), dtype=torch.uint8, device=hist.device)
@@ -321,14 +349,18 @@ def tsa_merge(part_score, part_key, stream=None):
     return s, k
 
 
-def tsa_finalize(hist, status, k, q, part_score, part_key, objective="pseudo_additive", stream=None):
+def tsa_finalize(hist, status, k, q, part_score, part_key, objective="pseudo_additive", stream=None,
+                 out=None):
     _need_cuda(hist, status, part_score, part_key)
     nz, bins = hist.shape
     nparts = part_score.shape[0]
     dev = hist.device
-    thr = torch.empty((nz, k), dtype=torch.int32, device=dev)
-    phi = torch.empty(nz, dtype=torch.float64, device=dev)
-    st = torch.empty(nz, dtype=torch.int32, device=dev)
+    if out is not None:
+        thr, phi, st = out
+    else:
+        thr = torch.empty((nz, k), dtype=torch.int32, device=dev)
+        phi = torch.empty(nz, dtype=torch.float64, device=dev)
+        st = torch.empty(nz, dtype=torch.int32, device=dev)
     o = tsa_outputs(thr.data_ptr(), None, phi.data_ptr(), None, st.data_ptr())
     _check(load().tsa_finalize(_ptr(hist), _ptr(status), nz, bins, k, float(q),
                                OBJECTIVES.get(objective, objective), _ptr(part_score),
@@ -337,12 +369,12 @@ def tsa_finalize(hist, status, k, q, part_score, part_key, objective="pseudo_add
     return thr, phi, st
 
 
-def tsa_label(vol, thresholds, status=None, bins=None, stream=None):
+def tsa_label(vol, thresholds, status=None, bins=None, stream=None, out=None):
     _need_cuda(vol, thresholds, status)
     k = thresholds.shape[1]
     bins = bins or (256 if vol.dtype == torch.uint8 else 4096)
     p = make_problem(vol, bins, k, 1.0)
-    labels = torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
+    labels = out if out is not None else torch.empty(vol.shape, dtype=torch.uint8, device=vol.device)
     _check(load().tsa_label(ctypes.byref(p), _ptr(thresholds), _ptr(status), _ptr(labels),
                             _stream(stream)), "tsa_label")
     return labels
@@ -595,3 +627,147 @@ def unpack_key(key, k):
     """Packed u64 key (as python int) -> tuple of k thresholds."""
     key &= 0xFFFFFFFFFFFFFFFF
     return tuple((key >> (12 * (k - 1 - j))) & 0xFFF for j in range(k))
+
+
+# ------------------------------------------------------------------ q sweep
+def tsa_segment_sweep(vol, bins, k, qs, objective="pseudo_additive", enumeration="canonical",
+                      units=0, labels=True, outs=None, workspace=None, stream=None):
+    """One histogram, then search / finalize / labels for every q in `qs`
+    (tsa_segment_sweep).  Returns a list of per-q output dicts (as tsa_segment)."""
+    _need_cuda(vol)
+    lib = load()
+    qs = [float(x) for x in qs]
+    p = make_problem(vol, bins, k, qs[0], objective, enumeration, units)
+    nz, dev = vol.shape[0], vol.device
+    if outs is None:
+        hist = torch.empty((nz, bins), dtype=torch.int32, device=dev)
+        outs = [{"thresholds": torch.empty((nz, k), dtype=torch.int32, device=dev),
+                 "objective": torch.empty(nz, dtype=torch.float64, device=dev),
+                 "histogram": hist if i == 0 else None,
+                 "status": torch.empty(nz, dtype=torch.int32, device=dev),
+                 "labels": torch.empty(vol.shape, dtype=torch.uint8, device=dev) if labels else None}
+                for i in range(len(qs))]
+    qa = (ctypes.c_double * len(qs))(*qs)
+    oa = (tsa_outputs * len(qs))()
+    for i, o in enumerate(outs):
+        oa[i] = tsa_outputs(o["thresholds"].data_ptr(),
+                            o["labels"].data_ptr() if o.get("labels") is not None else None,
+                            o["objective"].data_ptr() if o.get("objective") is not None else None,
+                            o["histogram"].data_ptr() if o.get("histogram") is not None else None,
+                            o["status"].data_ptr() if o.get("status") is not None else None)
+    if workspace is None:
+        n = int(lib.tsa_sweep_workspace_size(ctypes.byref(p), qa, len(qs)))
+        if n == 0:
+            _check(TSA_ERR_INVALID_ARG, "tsa_sweep_workspace_size")
+        workspace = torch.empty(n, dtype=torch.uint8, device=dev)
+    _check(lib.tsa_segment_sweep(ctypes.byref(p), qa, len(qs), oa, _ptr(workspace), workspace.numel(),
+                                 _stream(stream)), "tsa_segment_sweep")
+    return outs
+
+
+def sweep_workspace(vol, bins, k, qs, objective="pseudo_additive", enumeration="canonical", units=0):
+    p = make_problem(vol, bins, k, float(qs[0]), objective, enumeration, units)
+    qa = (ctypes.c_double * len(qs))(*[float(x) for x in qs])
+    n = int(load().tsa_sweep_workspace_size(ctypes.byref(p), qa, len(qs)))
+    return torch.empty(max(n, 1), dtype=torch.uint8, device=vol.device)
+
+
+# ---------------------------------------------------------------- multi-GPU
+def tsa_slab_range(nz_total, nranks, rank):
+    z0, z1 = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load().tsa_slab_range(nz_total, nranks, rank, ctypes.byref(z0), ctypes.byref(z1)),
+           "tsa_slab_range")
+    return z0.value, z1.value
+
+
+def tsa_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+    _check(load().tsa_comm_unique_id(buf), "tsa_comm_unique_id")
+    return buf.raw
+
+
+class TsaComm:
+    """Owner of a libtsa communicator (tsa_comm_init / tsa_comm_init_custom).
+    ``TsaComm.nccl(nranks, rank, uid)`` (uid: tsa_comm_unique_id() of rank 0,
+    distributed by the caller) or ``TsaComm.custom(nranks, rank, fn)`` with
+    fn(send_ptr, recv_ptr, nbytes, stream_handle) -> None (raise on error)."""
+
+    def __init__(self, handle, nranks, rank, keep=None):
+        self.handle, self.nranks, self.rank, self._keep = handle, nranks, rank, keep
+
+    @classmethod
+    def nccl(cls, nranks, rank, uid: bytes):
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(uid, COMM_ID_BYTES)
+        _check(load().tsa_comm_init(ctypes.byref(h), nranks, rank, buf), "tsa_comm_init")
+        return cls(h, nranks, rank)
+
+    @classmethod
+    def custom(cls, nranks, rank, fn):
+        def tramp(user, send, recv, nbytes, stream):
+            try:
+                fn(send, recv, nbytes, stream)
+                return 0
+            except Exception:  # reported as TSA_ERR_NCCL by the library
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        cb = ALLGATHER_FN(tramp)
+        h = ctypes.c_void_p()
+        _check(load().tsa_comm_init_custom(ctypes.byref(h), nranks, rank, cb, None), "tsa_comm_init_custom")
+        return cls(h, nranks, rank, keep=cb)
+
+    @property
+    def kind(self):
+        return int(load().tsa_comm_kind(self.handle))
+
+    def close(self):
+        if self.handle:
+            _check(load().tsa_comm_destroy(self.handle), "tsa_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tsa_segment_sharded(slab, nz_total, bins, k, q, comm, mode="tuples", objective="pseudo_additive",
+                        enumeration="canonical", units=0, labels=True, workspace=None, stream=None,
+                        nx=None, ny=None, dtype=torch.uint8):
+    """tsa_segment_sharded: `slab` is this rank's slices (tsa_slab_range of
+    nz_total) on this rank's GPU (may have 0 slices in tuples mode; pass
+    nx/ny/dtype then).  tuples mode: thresholds/objective/status/histogram for
+    all nz_total slices (identical on every rank) + the own slab's labels;
+    slices mode: everything for the own slab (no exchange)."""
+    _need_cuda(slab)
+    lib = load()
+    m = SHARD_MODES.get(mode, mode)
+    dev = slab.device
+    n_own = slab.shape[0]
+    ny = slab.shape[1] if ny is None else ny
+    nx = slab.shape[2] if nx is None else nx
+    p = tsa_problem(slab.data_ptr() if n_own > 0 else None,
+                    _dtype_code(slab) if n_own > 0 else (TSA_U8 if dtype == torch.uint8 else TSA_U16),
+                    nx, ny, n_own, bins, k, float(q), OBJECTIVES.get(objective, objective),
+                    ENUMERATIONS.get(enumeration, enumeration), units, 0, 0, 0)
+    nres = n_own if m == TSA_SHARD_SLICES else nz_total
+    out = {"thresholds": torch.empty((nres, k), dtype=torch.int32, device=dev),
+           "objective": torch.empty(nres, dtype=torch.float64, device=dev),
+           "histogram": torch.empty((nres, bins), dtype=torch.int32, device=dev),
+           "status": torch.empty(nres, dtype=torch.int32, device=dev),
+           "labels": torch.empty((n_own, ny, nx), dtype=torch.uint8, device=dev) if labels else None}
+    o = tsa_outputs(out["thresholds"].data_ptr(),
+                    out["labels"].data_ptr() if labels and n_own > 0 else None,
+                    out["objective"].data_ptr(), out["histogram"].data_ptr(), out["status"].data_ptr())
+    if workspace is None:
+        n = int(lib.tsa_sharded_workspace_size(ctypes.byref(p), nz_total, m, comm.handle))
+        workspace = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    _check(lib.tsa_segment_sharded(ctypes.byref(p), nz_total, ctypes.byref(o), m, comm.handle,
+                                   _ptr(workspace), workspace.numel(), _stream(stream)),
+           "tsa_segment_sharded")
+    out["units"] = int(lib.tsa_sharded_units(ctypes.byref(p), nz_total, comm.nranks))
+    return out

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "tsa.h"
+#include "tsa_internal.h"
 #include "tsa_kernels.cuh"
 #include "k_fused.cuh"
 
@@ -272,6 +273,8 @@ int32_t tsa_version(void) { return TSA_VERSION; }
 
 const char *tsa_last_error(void) { return g_last_error.c_str(); }
 
+void tsa_internal_set_error(const char *msg) { g_last_error = msg ? msg : ""; }
+
 const char *tsa_status_string(tsa_status s) {
   switch (s) {
     case TSA_OK: return "TSA_OK";
@@ -301,11 +304,15 @@ tsa_status tsa_validate(const tsa_problem *p) {
 }
 
 int32_t tsa_default_units(int64_t nz, int32_t bins, int32_t k, int32_t enumeration) {
+  return tsa_units_for_sms(nz, bins, k, enumeration, g_num_sms());
+}
+
+int32_t tsa_units_for_sms(int64_t nz, int32_t bins, int32_t k, int32_t enumeration, int32_t sms) {
   if (nz <= 0 || enumeration == TSA_ENUM_DP) return 1;
   // k <= 2: the search kernels balance their work internally (k = 2: per-warp
   // a-block items from a global queue), so one unit per slice
   if (k <= 2) return 1;
-  const double target = (double)g_num_sms() * (k >= 3 ? 64.0 : 8.0);
+  const double target = (double)sms * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
   double u = std::ceil(target / (double)nz);
@@ -860,6 +867,75 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   TSA_TRY(finalize_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
                         out->thresholds, out->objective, w.status, out->slice_status, s));
   if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, stream));
+  return TSA_OK;
+}
+
+// ------------------------------------------------------------ q sweep
+// Staged path per q (the same kernels as tsa_segment's staged pipeline), the
+// histogram once.  Layout: [status of the histogram pass][staged workspace for
+// the largest per-q size].
+static bool sweep_args_ok(const tsa_problem *p, const double *qs, int32_t nq) {
+  if (!p || !qs || nq < 1 || nq > 64) return false;
+  for (int i = 0; i < nq; i++) {
+    tsa_problem pq = *p;
+    pq.q = qs[i];
+    pq.pipeline = -1;
+    if (tsa_validate(&pq) != TSA_OK) return false;
+  }
+  return true;
+}
+
+size_t tsa_sweep_workspace_size(const tsa_problem *p, const double *qs, int32_t nq) {
+  if (!sweep_args_ok(p, qs, nq)) return 0;
+  size_t mx = 0;
+  for (int i = 0; i < nq; i++) {
+    tsa_problem pq = *p;
+    pq.q = qs[i];
+    pq.pipeline = -1;
+    mx = std::max(mx, carve_segment(&pq, nullptr, nullptr));
+  }
+  return align_up((size_t)p->nz * sizeof(int32_t)) + mx;
+}
+
+tsa_status tsa_segment_sweep(const tsa_problem *p, const double *qs, int32_t nq,
+                             const tsa_outputs *outs, void *workspace, size_t workspace_bytes,
+                             void *stream) {
+  if (!sweep_args_ok(p, qs, nq)) return set_error(TSA_ERR_INVALID_ARG, "sweep: problem or q values");
+  if (!outs || !workspace) return set_error(TSA_ERR_INVALID_ARG, "sweep: outputs / workspace NULL");
+  for (int i = 0; i < nq; i++)
+    if (!outs[i].thresholds) return set_error(TSA_ERR_INVALID_ARG, "sweep: outputs[i].thresholds NULL");
+  const size_t need = tsa_sweep_workspace_size(p, qs, nq);
+  if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "sweep workspace too small");
+  cudaStream_t s = S(stream);
+  Carve c{reinterpret_cast<char *>(workspace)};
+  int32_t *hstatus = c.take<int32_t>((size_t)p->nz);
+  char *rest = c.take<char>(0);
+  SegWs w;
+  carve_segment(p, rest, &w);
+  uint32_t *hist = w.hist;
+  for (int i = 0; i < nq; i++)
+    if (outs[i].histogram) {
+      hist = outs[i].histogram;
+      break;
+    }
+  TSA_TRY(tsa_histogram(p, hist, hstatus, stream));
+  for (int i = 0; i < nq; i++)
+    if (outs[i].histogram && outs[i].histogram != hist)
+      TSA_CUDA(cudaMemcpyAsync(outs[i].histogram, hist, sizeof(uint32_t) * p->nz * p->bins,
+                               cudaMemcpyDeviceToDevice, s));
+  for (int i = 0; i < nq; i++) {
+    tsa_problem pq = *p;
+    pq.q = qs[i];
+    SegWs wq;
+    carve_segment(&pq, rest, &wq);
+    const int32_t U = units_of(&pq);
+    TSA_CUDA(cudaMemcpyAsync(wq.status, hstatus, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToDevice, s));
+    TSA_TRY(tsa_search(hist, wq.status, pq.nz, pq.nx * pq.ny, pq.bins, pq.k, pq.q, pq.objective,
+                       pq.enumeration, U, 0, U, wq.ps, wq.pk, wq.search, wq.search_bytes, stream));
+    TSA_TRY(finalize_impl(hist, wq.status, pq.nz, pq.bins, pq.k, pq.q, pq.objective, wq.ps, wq.pk, U,
+                          outs[i].thresholds, outs[i].objective, wq.status, outs[i].slice_status, s));
+    if (outs[i].labels) TSA_TRY(tsa_label(&pq, outs[i].thresholds, wq.status, outs[i].labels, stream));
+  }
   return TSA_OK;
 }
 

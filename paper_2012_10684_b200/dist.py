@@ -7,7 +7,8 @@ B200 box; gloo for the CPU tests of the host logic).  Two strategies:
 * slab sharding (``segment_slabs``): rank r segments slices
   [slab_range(nz, P, r)) with no data-path collective -- slices are
   independent problems.
-* tuple sharding (``segment_tuple_sharded``): every rank needs the same
+* tuple sharding (``segment_tuple_sharded`` -> the library's
+  ``tsa_segment_sharded``, NCCL inside libtsa): every rank needs the same
   per-slice argmax over a tuple space too large for one GPU (k = 4).  Each rank
   histograms its slab, the histograms are all-gathered (nz*L*4 bytes), each
   rank runs the exhaustive search over its share of the work units of *every*
@@ -21,11 +22,14 @@ path itself runs in the libtsa kernels.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
-from . import (tsa_default_units, tsa_finalize, tsa_histogram, tsa_hu_finish, tsa_hu_histogram,
-               tsa_label, tsa_merge, tsa_search, tsa_segment, ENUMERATIONS)
+from . import (TsaComm, tsa_comm_unique_id, tsa_default_units, tsa_finalize, tsa_histogram,
+               tsa_hu_finish, tsa_hu_histogram, tsa_label, tsa_merge, tsa_search, tsa_segment,
+               tsa_segment_sharded, ENUMERATIONS)
 
 
 def slab_range(nz: int, world: int, rank: int) -> tuple[int, int]:
@@ -102,18 +106,106 @@ def segment_slabs(vol_slab, bins, k, q, **kw):
     return tsa_segment(vol_slab, bins, k, q, **kw)
 
 
+_cudart = None
+
+
+def _cudart_lib():
+    """libcudart for the host staging of the gloo transport (tests only)."""
+    global _cudart
+    if _cudart is None:
+        import ctypes
+
+        for name in ("libcudart.so.12", "libcudart.so"):
+            try:
+                _cudart = ctypes.CDLL(name)
+                break
+            except OSError:
+                continue
+        if _cudart is None:
+            import glob
+
+            cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime",
+                                           "lib", "libcudart.so*"))
+            _cudart = ctypes.CDLL(cands[0])
+    return _cudart
+
+
+def _gloo_allgather(group):
+    """All-gather for tsa_comm_init_custom over a gloo group: synchronise the
+    library's stream, stage the rank's bytes through host memory, gather,
+    copy the rank-major result back.  Two ranks on one GPU (NCCL refuses)
+    and CPU-side tests use it; the product transport is NCCL."""
+    import ctypes
+
+    import numpy as np
+
+    rt = _cudart_lib()
+    rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    rt.cudaStreamSynchronize.argtypes = [ctypes.c_void_p]
+
+    def fn(send, recv, nbytes, stream):
+        world = dist.get_world_size(group)
+        if rt.cudaStreamSynchronize(stream) != 0:
+            raise RuntimeError("cudaStreamSynchronize")
+        mine = np.empty(nbytes, np.uint8)
+        if nbytes and rt.cudaMemcpy(mine.ctypes.data, send, nbytes, 2) != 0:  # D2H
+            raise RuntimeError("cudaMemcpy D2H")
+        out = torch.empty(world * nbytes, dtype=torch.uint8)
+        dist.all_gather_into_tensor(out, torch.from_numpy(mine), group=group)
+        o = out.numpy()
+        if nbytes and rt.cudaMemcpy(recv, o.ctypes.data, world * nbytes, 1) != 0:  # H2D
+            raise RuntimeError("cudaMemcpy H2D")
+
+    return fn
+
+
+def make_comm(group=None, device=None):
+    """A libtsa communicator over the ranks of `group`: NCCL (tsa_comm_init,
+    the unique id broadcast from rank 0 through the process group) when the
+    group's backend is NCCL, else the host-staged gloo all-gather."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        uid = [tsa_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0, group=group, device=device)
+        return TsaComm.nccl(world, rank, uid[0])
+    return TsaComm.custom(world, rank, _gloo_allgather(group))
+
+
 def segment_tuple_sharded(vol_slab, nz_total, bins, k, q, objective="pseudo_additive",
                           enumeration="canonical", units=0, group=None, labels=True,
-                          workspace=None):
-    """Tuple sharding across the group.  `vol_slab` is this rank's slab
+                          workspace=None, comm=None):
+    """Tuple sharding across the group through the library
+    (tsa_segment_sharded, TSA_SHARD_TUPLES): `vol_slab` is this rank's slab
     (slab_range(nz_total, P, rank)) on this rank's GPU.  Returns the full
-    per-slice results (thresholds/objective/status for all nz_total slices,
-    identical on every rank) and this rank's labels."""
+    per-slice results (thresholds/objective/status/histogram for all nz_total
+    slices, identical on every rank) and this rank's labels."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    own = comm is None
+    if own:
+        comm = make_comm(group, vol_slab.device)
+    try:
+        out = tsa_segment_sharded(vol_slab, nz_total, bins, k, q, comm, mode="tuples",
+                                  objective=objective, enumeration=enumeration, units=units,
+                                  labels=labels, workspace=workspace)
+    finally:
+        if own:
+            comm.close()
+    U = out["units"]
+    out["unit_range"] = unit_range(U, world, rank)
+    out["slab"] = slab_range(nz_total, world, rank)
+    return out
+
+
+def segment_tuple_sharded_py(vol_slab, nz_total, bins, k, q, objective="pseudo_additive",
+                             enumeration="canonical", units=0, group=None, labels=True,
+                             workspace=None):
+    """The same exchange driven from Python with torch.distributed collectives
+    around the stage calls (kept as a cross-check of the in-library path)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     per = -(-nz_total // world)
     dev = vol_slab.device
-    ny, nx = vol_slab.shape[1], vol_slab.shape[2]
     if vol_slab.shape[0] > 0:
         hist_l, st_l = tsa_histogram(vol_slab, bins)
     else:
@@ -125,8 +217,8 @@ def segment_tuple_sharded(vol_slab, nz_total, bins, k, q, objective="pseudo_addi
     U = agreed_units(nz_total, bins, k, enum, world, units, group, dev)
     u0, u1 = unit_range(U, world, rank)
     if u1 > u0:
-        ps, pk = tsa_search(hist, status, nx * ny, k, q, objective, enumeration, units=U,
-                            unit_begin=u0, unit_end=u1, workspace=workspace)
+        ps, pk = tsa_search(hist, status, vol_slab.shape[1] * vol_slab.shape[2], k, q, objective,
+                            enumeration, units=U, unit_begin=u0, unit_end=u1, workspace=workspace)
         s_loc, k_loc = tsa_merge(ps, pk)
     else:  # more ranks than units: contribute "no tuple"
         s_loc = torch.full((nz_total,), float("-inf"), dtype=torch.float64, device=dev)

@@ -199,3 +199,59 @@ def test_morph_workspace(lib):
     # OPEN / TOPHAT without workspace: reported, nothing launched
     assert lib.tsa_morph(ctypes.c_void_p(16), ctypes.c_void_p(32), 8, 8, 1, 3, 2, None, 0, None) == \
         tsa.TSA_ERR_WORKSPACE
+
+
+# ------------------------------------------------------ q sweep / multi-GPU ABI
+def test_sweep_workspace_and_validation(lib):
+    p = _p(k=3, bins=256, nz=600)
+    qs = (ctypes.c_double * 11)(*[0.5 + 0.1 * i for i in range(11)])
+    n = lib.tsa_sweep_workspace_size(ctypes.byref(p), qs, 11)
+    assert n >= lib.tsa_workspace_size(ctypes.byref(p))
+    bad = (ctypes.c_double * 2)(0.8, 0.0)
+    assert lib.tsa_sweep_workspace_size(ctypes.byref(p), bad, 2) == 0
+    assert lib.tsa_sweep_workspace_size(ctypes.byref(p), qs, 0) == 0
+    o = (tsa.tsa_outputs * 2)(tsa.tsa_outputs(1, 0, 0, 0, 0), tsa.tsa_outputs(1, 0, 0, 0, 0))
+    assert lib.tsa_segment_sweep(ctypes.byref(p), bad, 2, o, ctypes.c_void_p(1), 1 << 40, None) == 1
+
+
+@pytest.mark.parametrize("nz,world", [(1, 1), (7, 3), (300, 8), (301, 8), (2, 3), (1000, 7)])
+def test_slab_range_matches_python_partition(lib, nz, world):
+    from paper_2012_10684_b200.dist import slab_range
+
+    for r in range(world):
+        assert tsa.tsa_slab_range(nz, world, r) == slab_range(nz, world, r)
+
+
+def test_sharded_units_are_rank_independent(lib):
+    """The tuple-sharded unit count never depends on the local device
+    (mixed SM counts must not split the unit space differently)."""
+    for k, bins, enum in ((4, 256, 0), (3, 256, 0), (2, 4096, 0), (4, 256, 1)):
+        p = _p(k=k, bins=bins, enumeration=enum, dtype=1 if bins <= 256 else 2, nz=38)
+        u = {lib.tsa_sharded_units(ctypes.byref(p), 300, P) for P in (8,)}
+        assert len(u) == 1 and min(u) >= 8
+    p = _p(k=4, enumeration=2)
+    assert lib.tsa_sharded_units(ctypes.byref(p), 300, 8) == 1  # DP: one unit per slice
+
+
+def test_custom_comm_lifecycle_and_errors(lib):
+    calls = []
+    comm = tsa.TsaComm.custom(2, 1, lambda *a: calls.append(a))
+    assert comm.kind == 2
+    p = _p(k=4, nz=150)
+    assert lib.tsa_sharded_workspace_size(ctypes.byref(p), 300, 1, comm.handle) > 0
+    assert lib.tsa_sharded_workspace_size(ctypes.byref(p), 300, 0, comm.handle) == \
+        lib.tsa_workspace_size(ctypes.byref(p))
+    o = tsa.tsa_outputs(1, 0, 0, 0, 0)
+    # wrong slab size for rank 1 of 2 over 301 slices (150 expected), bad mode
+    bad = _p(k=4, nz=151)
+    assert lib.tsa_segment_sharded(ctypes.byref(bad), 301, ctypes.byref(o), 1, comm.handle,
+                                   ctypes.c_void_p(1), 1 << 40, None) == 1
+    assert lib.tsa_segment_sharded(ctypes.byref(p), 300, ctypes.byref(o), 7, comm.handle,
+                                   ctypes.c_void_p(1), 1 << 40, None) == 1
+    assert lib.tsa_segment_sharded(ctypes.byref(p), 300, ctypes.byref(o), 1, None,
+                                   ctypes.c_void_p(1), 1 << 40, None) == 1
+    assert not calls  # nothing was exchanged before the arguments were rejected
+    comm.close()
+    h = ctypes.c_void_p()
+    assert lib.tsa_comm_init_custom(ctypes.byref(h), 2, 2, tsa.ALLGATHER_FN(lambda *a: 0), None) == 1
+    assert lib.tsa_comm_init(ctypes.byref(h), 0, 0, ctypes.create_string_buffer(128)) == 1

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
+                          "--steps", "2", "--warmup", "1", "--workload", "c2"], capture_output=True, text=True,
                          timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -32,3 +32,24 @@ def test_metric_matches_baseline_json():
 
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         assert json.load(f)["metric"] == bench.METRIC
+
+
+def test_default_workload_is_the_largest_single_gpu_config():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    sys.argv = ["bench.py"]
+    assert bench.parse().workload == "c5"
+
+
+def test_gpus_flag_spawns_ranks():
+    """bench.py --gpus N outside torchrun relaunches itself with N ranks
+    (torch.distributed.run, 127.0.0.1); every rank joins the group and rank 0
+    reports n_gpus = N (--dry-run: the launcher path only, no GPU work)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks"] == [0, 1]

@@ -34,7 +34,8 @@
  *     itself returns TSA_OK): TSA_ERR_LEVEL_OVERFLOW when any voxel >= bins
  *     (never clamped), TSA_ERR_NO_VALID_SPLIT when fewer than k+1 bins are
  *     non-empty.  A failed slice gets thresholds -1, objective NaN, labels 0.
- *   - CUDA launch failures return TSA_ERR_CUDA; tsa_last_error() gives detail
+ *   - CUDA launch failures return TSA_ERR_CUDA, transport (NCCL) failures of
+ *     the multi-GPU calls TSA_ERR_NCCL; tsa_last_error() gives detail
  *     (thread-local).
  */
 #ifndef TSA_H
@@ -101,12 +102,19 @@ typedef struct {
    *                through a dependency-ordered task queue); both need k <= 2,
    *                bins <= 1024, CANONICAL, PSEUDO_ADDITIVE, nx*ny % 16 == 0,
    *                16-byte aligned volume and labels;
+   *                3 = stream: ONE persistent kernel whose io CTAs stream
+   *                histogram chunks and label chunks while its search CTAs
+   *                run each slice's tables and exhaustive search (k = 2,
+   *                CANONICAL, PSEUDO_ADDITIVE, nx*ny % 16 == 0, aligned);
    *                -1 = staged: one kernel per stage (any problem);
-   *                0 = compact whenever eligible, else staged
+   *                0 = stream for eligible k = 2 problems above 1024 bins,
+   *                else compact whenever eligible, else staged
    *   slab_slices  fused: slices per pipeline slab; compact: histogram CTAs
-   *                per SM (default 4)
+   *                per SM (default 4); stream: histogram / label chunks per
+   *                slice (default ~128 K voxels each)
    *   label_lag    fused: rounds by which labelling trails the histogram;
-   *                compact: ignored (the per-slice kernel runs 256 threads) */
+   *                stream: slices by which labelling trails the histogram
+   *                (default 16); compact: ignored */
   int32_t pipeline;
   int32_t slab_slices;
   int32_t label_lag;
@@ -126,9 +134,10 @@ tsa_status tsa_validate(const tsa_problem *p);
 /* Bytes of workspace tsa_segment needs for this problem (0 if invalid). */
 size_t tsa_workspace_size(const tsa_problem *p);
 
-/* Which implementation tsa_segment runs for this problem: 2 = compact
- * (3 kernels), 1 = persistent fused kernel, -1 = staged (one kernel per stage),
- * 0 = invalid problem.  (Labels must also be 16-byte aligned for 1 and 2.) */
+/* Which implementation tsa_segment runs for this problem: 3 = stream (one
+ * persistent kernel), 2 = compact (3 kernels), 1 = persistent fused kernel,
+ * -1 = staged (one kernel per stage), 0 = invalid problem.  (Labels must also
+ * be 16-byte aligned for 1, 2 and 3.) */
 int32_t tsa_pipeline_kind(const tsa_problem *p);
 
 /* The whole hot path on one stream:
@@ -205,9 +214,10 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds,
 
 /* Host-buffer convenience: copies a HOST volume (pinned recommended) to the
  * device in slabs, runs tsa_segment per slab and copies thresholds, objective,
- * status and (if labels_host != NULL) labels back: copy-in and compute on
- * stream0, copy-out on stream1, ordered by events over two device buffers, so
- * the H2D and D2H copy engines run concurrently.  Device scratch (dev_buf, dev_bytes) comes from the
+ * status and (if labels_host != NULL) labels back: compute on stream0,
+ * copy-out on stream1, copy-in on a stream the call creates and destroys,
+ * ordered by events over two device buffers, so the H2D and D2H copy engines
+ * and the kernels run concurrently.  Device scratch (dev_buf, dev_bytes) comes from the
  * caller: tsa_segment_host_scratch_size() bytes.  Blocks until done. */
 size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab_slices);
 tsa_status tsa_segment_host(const tsa_problem *p_host_volume, int64_t slab_slices,

@@ -64,8 +64,10 @@ __device__ __forceinline__ int class_of(int i, int t0, int t1, int t2, int t3) {
 // segment in ascending bin order (the definition's order).
 constexpr int kFinThreads = 256;
 
-__global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
-  extern __shared__ double fsh[];  // [L] p then terms, followed by int [L] bin list
+// The per-slice body (also run by the stream pipeline's label tasks, k_stream.cuh):
+// fsh = [L] doubles followed by [L] ints of shared memory; blockDim.x ==
+// kFinThreads; the early returns are CTA-uniform.
+__device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *fsh) {
   int *lst = reinterpret_cast<int *>(fsh + g.L);
   __shared__ double s_best[1];
   __shared__ uint64_t s_key[1];
@@ -73,15 +75,16 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
   __shared__ unsigned long long s_n[kFinThreads / 32];
   __shared__ int s_start[kKMax + 2];
   __shared__ double Psh[kKMax + 1], Ssh[kKMax + 1];
-  const int64_t z = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kFinThreads / 32;
   if (warp == 0) {
     double s = -CUDART_INF;
     uint64_t key = kKeyNone;
+    // L2 loads: in the stream pipeline these come from another CTA of a
+    // running kernel (no stale L1 lines of neighbouring slices)
     for (int p = lane; p < g.nparts; p += 32) {
-      const double os = g.ps[(size_t)p * g.nz + z];
-      const uint64_t ok = g.pk[(size_t)p * g.nz + z];
+      const double os = __ldcg(g.ps + (size_t)p * g.nz + z);
+      const uint64_t ok = __ldcg(g.pk + (size_t)p * g.nz + z);
       if (better(os, ok, s, key)) {
         s = os;
         key = ok;
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
   }
   __syncthreads();
   const uint64_t key = s_key[0];
-  int st = g.status_in[z];
+  int st = __ldcg(g.status_in + z);
   if (st == kOK && key == kKeyNone) st = kNoValidSplit;
   const int k = g.k, L = g.L;
   if (st != kOK) {
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
   int cnt = 0;
   unsigned long long nsum = 0;
   for (int i = i0; i < i1; i++) {
-    const uint32_t c = __ldg(h + i);
+    const uint32_t c = __ldcg(h + i);
     cnt += c != 0;
     nsum += c;
   }
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
   const int m = s_cnt[NW];
   int e = s_cnt[warp] + ex - cnt;
   for (int i = i0; i < i1; i++)
-    if (__ldg(h + i)) lst[e++] = i;
+    if (__ldcg(h + i)) lst[e++] = i;
   const double N = (double)s_n[0];  // exact: the oracle's sequential double sum of integers
   __syncthreads();
   // class c = list segment [start_c, start_{c+1}): first entry with bin > t_{c-1}
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
     }
     s_start[tid] = tid == k + 1 ? m : lo;
   }
-  for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn((double)__ldg(h + lst[j]), N);
+  for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn((double)__ldcg(h + lst[j]), N);
   __syncthreads();
   if (tid <= k) {
     double P = 0.0;
@@ -211,6 +214,11 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
     }
     g.objective_out[z] = phi;
   }
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {
+  extern __shared__ double fsh[];  // [L] p then terms, followed by int [L] bin list
+  finalize_slice(g, blockIdx.x, fsh);
 }
 
 }  // namespace tsa

@@ -315,7 +315,15 @@ __device__ __forceinline__ void next_colex(int *idx) {
 // tuple (DMUL + DSETP.GE.OR into one predicate), next group's loads in flight
 // while the current one is compared.  Only if some value >= best is the row
 // rescanned under the exact (score, key) order.
-template <int MODE, int R>
+// 16-byte row loads: read-only cache path (global tables) or generic (tables
+// in shared memory, k_search_tri)
+template <bool NC>
+__device__ __forceinline__ double2 ldrow(const double2 *p) {
+  if (NC) return __ldg(p);
+  return *p;
+}
+
+template <int MODE, int R, bool NC = true>
 __device__ __forceinline__ void search_row(const double *row, int a, int M, double pre, const int *idx,
                                            const int32_t *bin, double &best, uint64_t &bestkey) {
   // columns [a+1, M-2]; entries outside are NaN, so 8-column groups from the
@@ -325,23 +333,23 @@ __device__ __forceinline__ void search_row(const double *row, int a, int M, doub
   unsigned hit = 0;
   // two register buffers alternate (no copies): loads of group g+1 are in
   // flight while group g is compared
-  double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+  double2 x0 = ldrow<NC>(rp), x1 = ldrow<NC>(rp + 1), x2 = ldrow<NC>(rp + 2), x3 = ldrow<NC>(rp + 3);
   double2 y0, y1, y2, y3;
   for (;;) {
     if (ng > 1) {
-      y0 = __ldg(rp + 4);
-      y1 = __ldg(rp + 5);
-      y2 = __ldg(rp + 6);
-      y3 = __ldg(rp + 7);
+      y0 = ldrow<NC>(rp + 4);
+      y1 = ldrow<NC>(rp + 5);
+      y2 = ldrow<NC>(rp + 6);
+      y3 = ldrow<NC>(rp + 7);
     }
     hit = cmp8<MODE>(hit, pre, x0, x1, x2, x3, best);
     if (--ng == 0) break;
     rp += 4;
     if (ng > 1) {
-      x0 = __ldg(rp + 4);
-      x1 = __ldg(rp + 5);
-      x2 = __ldg(rp + 6);
-      x3 = __ldg(rp + 7);
+      x0 = ldrow<NC>(rp + 4);
+      x1 = ldrow<NC>(rp + 5);
+      x2 = ldrow<NC>(rp + 6);
+      x3 = ldrow<NC>(rp + 7);
     }
     hit = cmp8<MODE>(hit, pre, y0, y1, y2, y3, best);
     if (--ng == 0) break;
@@ -365,30 +373,30 @@ __device__ __forceinline__ void search_row(const double *row, int a, int M, doub
 }
 
 // Two rows sharing a (consecutive colex ranks): the 8-column loads serve both.
-template <int MODE, int R>
+template <int MODE, int R, bool NC = true>
 __device__ __forceinline__ void search_row2(const double *row, int a, int M, double pre0, double pre1,
                                             const int *idx0, const int *idx1, const int32_t *bin,
                                             double &best, uint64_t &bestkey) {
   const double2 *rp = reinterpret_cast<const double2 *>(row + ((a + 1) & ~1));
   int ng = (M - 1 - ((a + 1) & ~1) + 7) >> 3;
   unsigned hit = 0;
-  double2 x0 = __ldg(rp), x1 = __ldg(rp + 1), x2 = __ldg(rp + 2), x3 = __ldg(rp + 3);
+  double2 x0 = ldrow<NC>(rp), x1 = ldrow<NC>(rp + 1), x2 = ldrow<NC>(rp + 2), x3 = ldrow<NC>(rp + 3);
   double2 y0, y1, y2, y3;
   for (;;) {
     if (ng > 1) {
-      y0 = __ldg(rp + 4);
-      y1 = __ldg(rp + 5);
-      y2 = __ldg(rp + 6);
-      y3 = __ldg(rp + 7);
+      y0 = ldrow<NC>(rp + 4);
+      y1 = ldrow<NC>(rp + 5);
+      y2 = ldrow<NC>(rp + 6);
+      y3 = ldrow<NC>(rp + 7);
     }
     hit = cmp8x2<MODE>(hit, pre0, pre1, x0, x1, x2, x3, best);
     if (--ng == 0) break;
     rp += 4;
     if (ng > 1) {
-      x0 = __ldg(rp + 4);
-      x1 = __ldg(rp + 5);
-      x2 = __ldg(rp + 6);
-      x3 = __ldg(rp + 7);
+      x0 = ldrow<NC>(rp + 4);
+      x1 = ldrow<NC>(rp + 5);
+      x2 = ldrow<NC>(rp + 6);
+      x3 = ldrow<NC>(rp + 7);
     }
     hit = cmp8x2<MODE>(hit, pre0, pre1, y0, y1, y2, y3, best);
     if (--ng == 0) break;
@@ -512,6 +520,165 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
         }
       }
       block_argmax(best, bestkey);
+    }
+    block_argmax(best, bestkey);
+    if (threadIdx.x == 0) {
+      g.part_score[(size_t)ul * g.nz + z] = best;
+      g.part_key[(size_t)ul * g.nz + z] = bestkey;
+    }
+  }
+}
+
+// Exhaustive search for k >= 3 with the slice's class-term tables built by the
+// searching CTA itself (round 2; replaces k_rtable's HBM round trip of three
+// L x (L+8) tables per slice):
+//   T(i, j), 0 <= i <= j <= M-2      every class term (triangular, j(j+1)/2 + i)
+//   R[a][b] = T(a+1, b) (x) Asuf[b]  the last two classes, rows a <= M-3 stored
+//                                    from column (a+1) & ~1 in whole 8-column
+//                                    groups (NaN outside (a, M-2]), packed
+// in shared memory when they fit (M <= ~115 at two CTAs per SM: every CT
+// slice of the 8-bit configs, m ~ 90), else in the global fallback region
+// (g.R / g.PP per slice).  Prefix values are the same expressions as the
+// staged tables: K = 3: PP[t1][a] = T(0,t1) (x) T(t1+1,a); K = 4:
+// PP[t1][t2] (x) T(t2+1,a); the compare loop is search_row / search_row2.
+// So every tuple's value is bit-identical to k_search_rows' (tested).
+// Work items (slice, unit) from a global counter; a unit is a contiguous
+// colex range of the slice's prefixes, as in k_search_rows.
+__device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + i; }
+constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
+constexpr size_t kTriSmemBytes = 104 * 1024;     // dynamic tables: two CTAs per SM
+
+// doubles needed for the tables of a slice with M positions (rows packed)
+__host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
+  int64_t r = 0;
+  for (int a = 0; a <= M - 3; a++) {
+    const int sa = (a + 1) & ~1;
+    r += 8 * ((M + 6 - sa) >> 3);
+  }
+  return r + (int64_t)(M - 1) * M / 2;
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_doubles) {
+  static_assert(K >= 3 && K <= 4, "k = 3, 4");
+  constexpr int R = K - 1;
+  constexpr int CH = 8;
+  extern __shared__ __align__(16) double tsm[];
+  __shared__ int s_item;
+  __shared__ int s_roff[kTriMaxRows];
+  __shared__ uint32_t s_C[kTriMaxRows + 2];
+  __shared__ double s_Wh[kTriMaxRows + 2], s_Wl[kTriMaxRows + 2];
+  __shared__ int32_t s_bin[kTriMaxRows + 2];
+  const int64_t items = g.nz * (int64_t)g.nunits;
+  const size_t slice_doubles = (size_t)g.L * g.RS;  // global fallback region per slice
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(g.counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= items) break;
+    const int z = (int)(item / g.nunits);
+    const int ul = (int)(item % g.nunits);
+    const int u = g.unit_begin + ul;
+    double best = -CUDART_INF;
+    uint64_t bestkey = kKeyNone;
+    const int st = g.status[z];
+    const int M = g.Mz[z];
+    const int P = M - 1;
+    const bool active = st == kOK && P >= K;
+    if (active) {
+      const uint64_t NR = binom((uint64_t)P, R);
+      const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
+      const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
+      // tables: shared memory when they fit, else this slice's global region
+      const bool fits = M <= kTriMaxRows && tri_table_doubles(M) <= smem_doubles;
+      double *Rt = fits ? tsm : const_cast<double *>(g.R) + (size_t)z * slice_doubles;  // workspace
+      int *roff = fits ? s_roff : reinterpret_cast<int *>(const_cast<double *>(g.PP) + (size_t)z * slice_doubles);
+      // slice tables (positions 0..M-1, entry e = position + 1)
+      const bool stage = M + 1 <= kTriMaxRows + 2;
+      const uint32_t *gC = g.C + (size_t)z * g.E;
+      const double *gWh = g.Whi + (size_t)z * g.E, *gWl = g.Wlo + (size_t)z * g.E;
+      const int32_t *gB = g.Bin + (size_t)z * g.E;
+      if (stage)
+        for (int e = threadIdx.x; e <= M; e += blockDim.x) {
+          s_C[e] = gC[e];
+          s_Wh[e] = gWh[e];
+          s_Wl[e] = gWl[e];
+          s_bin[e] = gB[e];
+        }
+      const SliceTables t{stage ? s_C : gC, stage ? s_Wh : gWh, stage ? s_Wl : gWl, nullptr};
+      const int32_t *bin = stage ? s_bin : gB;
+      const double *asz = g.Asuf + (size_t)z * g.L;
+      if (threadIdx.x == 0) {
+        int o = 0;
+        for (int a = 0; a <= M - 3; a++) {
+          roff[a] = o;
+          o += 8 * ((M + 6 - ((a + 1) & ~1)) >> 3);
+        }
+        roff[M - 2 > 0 ? M - 2 : 0] = o;  // start of the T table
+      }
+      __syncthreads();
+      const int tbase = roff[max(M - 2, 0)];
+      double *Tt = Rt + tbase;
+      const int ntri = (M - 1) * M / 2;
+      for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
+        // e = j(j+1)/2 + i
+        int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (j * (j + 1) / 2 > e) j--;
+        while ((j + 1) * (j + 2) / 2 <= e) j++;
+        const int i = e - j * (j + 1) / 2;
+        Tt[e] = class_term<MODE>(t, g.luts, i, j);
+      }
+      __syncthreads();
+      // rows, flattened over all stored entries [0, tbase): the row of entry
+      // e is found by a binary search in roff
+      for (int e = threadIdx.x; e < tbase; e += blockDim.x) {
+        int lo = 0, hi = M - 3;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (roff[mid] <= e) lo = mid;
+          else hi = mid - 1;
+        }
+        const int a = lo, b = ((a + 1) & ~1) + (e - roff[a]);
+        Rt[e] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+      }
+      __syncthreads();
+      auto pre_of = [&](const int *id) -> double {
+        const double p01 = combine<MODE>(Tt[tri_idx(0, id[0])], Tt[tri_idx(id[0] + 1, id[1])]);
+        const double p = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(id[1] + 1, id[R - 1])]);
+        return MODE == PROD_MIN ? -p : p;  // (-pre)*R == -(pre*R) exactly
+      };
+      const uint64_t span = (uint64_t)blockDim.x * CH;
+      const uint64_t nchunks = r1 > r0 ? (r1 - r0 + span - 1) / span : 0;
+      for (uint64_t ci = 0; ci < nchunks; ci++) {
+        const uint64_t rb = r0 + ci * span + (uint64_t)threadIdx.x * CH;
+        if (rb < r1) {
+          int idx[R];
+          unrank_colex<R>(rb, idx);
+          const uint64_t re_ = min(r1, rb + CH);
+          for (uint64_t r = rb; r < re_;) {
+            int nidx[R];
+#pragma unroll
+            for (int j = 0; j < R; j++) nidx[j] = idx[j];
+            next_colex<R>(nidx);
+            const int a = idx[R - 1];
+            const double *rowa = Rt + roff[min(a, max(M - 3, 0))] - ((a + 1) & ~1);
+            if (r + 1 < re_ && nidx[R - 1] == a && a <= M - 3) {
+              search_row2<MODE, R, false>(rowa, a, M, pre_of(idx), pre_of(nidx), idx, nidx, bin, best, bestkey);
+#pragma unroll
+              for (int j = 0; j < R; j++) idx[j] = nidx[j];
+              next_colex<R>(idx);
+              r += 2;
+            } else {
+              if (a <= M - 3) search_row<MODE, R, false>(rowa, a, M, pre_of(idx), idx, bin, best, bestkey);
+#pragma unroll
+              for (int j = 0; j < R; j++) idx[j] = nidx[j];
+              r += 1;
+            }
+          }
+        }
+        block_argmax(best, bestkey);
+      }
     }
     block_argmax(best, bestkey);
     if (threadIdx.x == 0) {
@@ -709,6 +876,52 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
   }
 }
 
+// One warp's a-block i of slice positions (k = 2): lane l owns a = 32 i + l,
+// walks b = 32 i + 1 .. M - 2 kK2Rows rows at a time; returns the lane's best
+// (score, key) (not yet warp-reduced).  rz = the slice's K2Row table.  Every
+// k = 2 kernel (k_search_k2, the stream pipeline's k_st_search) runs this body,
+// so a tuple's value is the same expression tree everywhere.
+template <int MODE, int DEG>
+__device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int i, const int lane,
+                                         const Luts &l, const SpPair &tab, double &best,
+                                         uint64_t &bestkey) {
+  const double ident = MODE == SUM ? 0.0 : 1.0;
+  const int a = 32 * i + lane;
+  const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
+  const K2Row ra = rz[ac + 1];
+  const uint32_t Ca = ra.c;
+  const double Wah = ra.wh, Wal = ra.wl;
+  // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
+  const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
+  const int bend = M - 2;
+  int b0 = 32 * i + 1;
+  for (const K2Row *pr = rz + b0 + 1; b0 <= bend; b0 += kK2Rows, pr += kK2Rows) {
+    double vb[kK2Rows];
+#pragma unroll
+    for (int r = 0; r < kK2Rows; r++) {
+      const double2 x = __ldg(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
+      const double2 y = __ldg(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
+      const uint32_t n = (uint32_t)__double2loint(y.y) - Ca;
+      const double wm = dd_diff(x.x, x.y, Wah, Wal);
+      const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), y.x);
+      double v = combine<MODE>(pre, R);
+      if (MODE == PROD_MIN) v = -v;
+      vb[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < kK2Rows; r++) {
+      const int b = b0 + r;
+      if (vb[r] >= best && a < b && b <= bend) {
+        const uint64_t key = ((uint64_t)ra.bin << 12) | (uint64_t)rz[b + 1].bin;
+        if (better(vb[r], key, best, bestkey)) {
+          best = vb[r];
+          bestkey = key;
+        }
+      }
+    }
+  }
+}
+
 template <int MODE, int DEG>
 __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
@@ -724,7 +937,6 @@ __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
   const int nbl = nbmax <= u0 ? 0 : ((nbmax - u0) / U) * w + min(w, (nbmax - u0) % U);
   const uint32_t nz = (uint32_t)g.nz;
   const uint32_t items = (uint32_t)nbl * nz;
-  const double ident = MODE == SUM ? 0.0 : 1.0;
   for (;;) {
     uint32_t it = 0;
     if (lane == 0) it = (uint32_t)atomicAdd(g.counter, 1);
@@ -737,41 +949,7 @@ __global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
     double best = -CUDART_INF;
     uint64_t bestkey = kKeyNone;
     if (g.status[z] == kOK && 32 * i <= M - 3) {
-      const K2Row *rz = g.rows + (size_t)z * g.RE;
-      const int a = 32 * i + lane;
-      const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
-      const K2Row ra = rz[ac + 1];
-      const uint32_t Ca = ra.c;
-      const double Wah = ra.wh, Wal = ra.wl;
-      // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
-      const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
-      const int bend = M - 2;
-      int b0 = 32 * i + 1;
-      for (const K2Row *pr = rz + b0 + 1; b0 <= bend; b0 += kK2Rows, pr += kK2Rows) {
-        double vb[kK2Rows];
-#pragma unroll
-        for (int r = 0; r < kK2Rows; r++) {
-          const double2 x = __ldg(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
-          const double2 y = __ldg(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
-          const uint32_t n = (uint32_t)__double2loint(y.y) - Ca;
-          const double wm = dd_diff(x.x, x.y, Wah, Wal);
-          const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), y.x);
-          double v = combine<MODE>(pre, R);
-          if (MODE == PROD_MIN) v = -v;
-          vb[r] = v;
-        }
-#pragma unroll
-        for (int r = 0; r < kK2Rows; r++) {
-          const int b = b0 + r;
-          if (vb[r] >= best && a < b && b <= bend) {
-            const uint64_t key = ((uint64_t)ra.bin << 12) | (uint64_t)rz[b + 1].bin;
-            if (better(vb[r], key, best, bestkey)) {
-              best = vb[r];
-              bestkey = key;
-            }
-          }
-        }
-      }
+      k2_block<MODE, DEG>(g.rows + (size_t)z * g.RE, M, i, lane, l, tab, best, bestkey);
       warp_argmax(best, bestkey);
     }
     if (lane == 0) {

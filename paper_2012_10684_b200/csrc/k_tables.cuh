@@ -108,13 +108,13 @@ __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q,
 // tables copy the canonical entry of the last non-empty bin <= i, so tuples
 // that differ only by empty bins read identical table values and evaluate
 // bit-identically; then Asuf.
+// The per-slice body of k_scan (also run by the stream pipeline's histogram
+// tasks, k_stream.cuh): h = the slice's histogram (global or shared), wsh =
+// [L] doubles + 1 KB of shared scratch, blockDim.x == kTableThreads.
 template <int MODE>
-__global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
-  extern __shared__ __align__(16) double wsh[];  // [L] then scan scratch
+__device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h, double *wsh) {
   const int tid = threadIdx.x;
-  const int64_t z = blockIdx.x;
   const int L = g.L, E = g.E;
-  const uint32_t *h = g.hist + z * L;
   char *scratch = reinterpret_cast<char *>(wsh + L);
   uint32_t *cC = g.cC + z * E;
   double *cWhi = g.cWhi + z * E, *cWlo = g.cWlo + z * E;
@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
     Asuf[i] = as;
     if (rows) rows[i + 1] = K2Row{tWhi[i + 1], tWlo[i + 1], as, tC[i + 1], tBin[i + 1]};
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
+  extern __shared__ __align__(16) double wsh[];  // [L] then scan scratch
+  scan_slice<MODE>(g, blockIdx.x, g.hist + (int64_t)blockIdx.x * g.L, wsh);
 }
 
 // R[a][b] = combine(T(a+1, b), Asuf[b]) for 0 <= a < b <= M-2 (k >= 3,

@@ -15,6 +15,7 @@
 #include "tsa_internal.h"
 #include "tsa_kernels.cuh"
 #include "k_fused.cuh"
+#include "k_stream.cuh"
 
 namespace {
 
@@ -312,6 +313,12 @@ int32_t tsa_units_for_sms(int64_t nz, int32_t bins, int32_t k, int32_t enumerati
   // k <= 2: the search kernels balance their work internally (k = 2: per-warp
   // a-block items from a global queue), so one unit per slice
   if (k <= 2) return 1;
+  if (k >= 3 && enumeration == TSA_ENUM_CANONICAL && bins <= 512) {
+    // k_search_tri rebuilds the slice's tables per work item: ~8 items per SM
+    const double u = std::ceil((double)sms * 8.0 / (double)nz);
+    const double rows = binom_d(0.45 * (bins - 1), k - 1);
+    return (int32_t)std::max(1.0, std::min({u, std::max(1.0, rows / 8192.0), 64.0}));
+  }
   const double target = (double)sms * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
@@ -346,6 +353,8 @@ struct SegWs {
   int32_t *povf;
   int32_t *counters;
   double *luts;
+  // stream pipeline: [3 + 6 nz] counters and flags
+  int32_t *sctr;
 };
 
 // fused-pipeline constants (tuned on B200, profiles/)
@@ -377,8 +386,24 @@ static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
   w.povf = c.take<int32_t>((size_t)p->nz * std::max(kFusedHC, kCompactHC));
   w.counters = c.take<int32_t>(2 + 2 * (size_t)p->nz);
   w.luts = c.take<double>(tsa::kSmallLut);
+  w.sctr = c.take<int32_t>(3 + tsa::kStCounters * (size_t)p->nz);
   if (o) *o = w;
   return c.off;
+}
+
+// stream pipeline (k_stream.cuh): k = 2, canonical, pseudo-additive, 16-voxel
+// vectors; the default for bins > 1024 (the compact path covers <= 1024)
+static bool stream_eligible(const tsa_problem *p) {
+  const int64_t n = p->nx * p->ny;
+  return p->k == 2 && p->bins >= 3 && p->enumeration == TSA_ENUM_CANONICAL &&
+         p->objective == TSA_OBJ_PSEUDO_ADDITIVE && n % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(p->volume) & 15) == 0;
+}
+// auto-selection of the stream pipeline (kStreamAuto): off until it beats the
+// staged kernels on c5 (profiles/r2*)
+constexpr bool kStreamAuto = false;
+static bool stream_default(const tsa_problem *p) {
+  return kStreamAuto && p->pipeline == 0 && p->bins > 1024 && stream_eligible(p);
 }
 
 }  // extern "C"
@@ -511,8 +536,115 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
   return check_cuda("k_fused");
 }
 
+// k_stream schedule: histogram and label chunks per slice (~128 K voxels
+// each; slab_slices overrides), search CTAs per slice, the label lag in
+// rounds of the io queue (label_lag overrides) and io CTAs per 4 CTAs.
+static void stream_schedule(const tsa_problem *p, int *HC, int *LC, int *SS, int *Dl, int *nio) {
+  const int64_t n = p->nx * p->ny;
+  const int ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, (n + 131071) / 131072));
+  *HC = p->slab_slices > 0 ? p->slab_slices : ch;
+  *LC = *HC;
+  *SS = 2;
+  *Dl = p->label_lag > 0 ? p->label_lag : 16;
+  *nio = 2;
+}
+
+static tsa_status segment_stream(const tsa_problem *p, const tsa_outputs *out, const SegWs &w,
+                                 cudaStream_t s) {
+  const int64_t N = p->nx * p->ny, nz = p->nz;
+  const int L = p->bins, E = L + 1;
+  const bool shannon = p->q == 1.0;
+  const int mode = search_mode(p->q, p->objective);
+  SearchWs sw;
+  Carve c{w.search};
+  carve_search(c, sw, nz, N, L, p->k, p->q, p->objective, p->enumeration);
+  uint32_t *hist = out->histogram ? out->histogram : w.hist;
+  TSA_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nz * L, s));
+  TSA_CUDA(cudaMemsetAsync(w.sctr, 0, sizeof(int32_t) * (3 + tsa::kStCounters * (size_t)nz), s));
+  tsa::k_small_luts<<<(tsa::kSmallLut + 255) / 256, 256, 0, s>>>(sw.sp, p->q, shannon);
+  TSA_TRY(check_cuda("k_small_luts"));
+  const tsa::Luts l = make_luts(p->q, sw.sp);
+  tsa::StreamArgs a = {};
+  a.vol = reinterpret_cast<const uint8_t *>(p->volume);
+  a.n = N;
+  a.nz = nz;
+  a.L = L;
+  a.k = p->k;
+  a.hist = hist;
+  a.ctr = w.sctr;
+  a.status = w.status;
+  a.thresholds = out->thresholds;
+  a.labels = out->labels;
+  a.item_score = sw.item_score;
+  a.item_key = sw.item_key;
+  a.NB = k2_blocks(L);
+  a.ps = w.ps;
+  a.pk = w.pk;
+  tsa::ScanArgs &sa = a.scan;
+  sa.hist = hist;
+  sa.status = w.status;
+  sa.nz = nz;
+  sa.L = L;
+  sa.E = E;
+  sa.k = p->k;
+  sa.q = p->q;
+  sa.shannon = shannon;
+  sa.full = 0;
+  sa.cC = sw.cC;
+  sa.cWhi = sw.cWhi;
+  sa.cWlo = sw.cWlo;
+  sa.cBin = sw.cBin;
+  sa.Asuf = sw.Asuf;
+  sa.M = sw.M;
+  sa.mmax = nullptr;
+  sa.rows = sw.rows;
+  sa.RE = k2_row_stride(L);
+  sa.luts = l;
+  tsa::FinalizeArgs &f = a.fin;
+  f.hist = hist;
+  f.status_in = w.status;
+  f.ps = w.ps;
+  f.pk = w.pk;
+  f.nparts = 1;
+  f.nz = nz;
+  f.L = L;
+  f.k = p->k;
+  f.objective = p->objective;
+  f.q = p->q;
+  f.thresholds = out->thresholds;
+  f.objective_out = out->objective;
+  f.status_out = w.status;
+  f.status_out2 = out->slice_status;
+  stream_schedule(p, &a.HC, &a.LC, &a.SS, &a.Dl, &a.nio);
+  a.ltasks = out->labels ? 1 : 0;
+  // shared memory: max(H: [L+1] u32 bins + [L] doubles + 1 KB scan scratch,
+  //                    L: [L] doubles + [L] ints of the finalize, S: the class-size table)
+  const size_t smem_h = 8 * (size_t)((L + 2) / 2 + 1) + 8 * (size_t)L + 1024;
+  const size_t smem = std::max({smem_h, (size_t)(L + 1) * 4, (size_t)L * 12, (size_t)tsa::kSN * 16}) + 64;
+  auto pick = [&](auto t8) {
+    using T = decltype(t8);
+    auto f = tsa::k_stream<T, tsa::SUM, 6>;
+    if (mode == tsa::PROD_MAX)
+      f = l.deg == 5 ? tsa::k_stream<T, tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_stream<T, tsa::PROD_MAX, 6>
+                                                                     : tsa::k_stream<T, tsa::PROD_MAX, 12>;
+    else if (mode == tsa::PROD_MIN)
+      f = l.deg == 5 ? tsa::k_stream<T, tsa::PROD_MIN, 5> : l.deg == 6 ? tsa::k_stream<T, tsa::PROD_MIN, 6>
+                                                                     : tsa::k_stream<T, tsa::PROD_MIN, 12>;
+    return f;
+  };
+  auto kern = p->dtype == TSA_U8 ? pick(uint8_t{}) : pick(uint16_t{});
+  if (smem > 48 * 1024) TSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  TSA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tsa::kStThreads, smem));
+  const int grid = std::max(1, per_sm) * g_num_sms();
+  kern<<<grid, tsa::kStThreads, smem, s>>>(a);
+  return check_cuda("k_stream");
+}
+
 int32_t tsa_pipeline_kind(const tsa_problem *p) {
   if (tsa_validate(p) != TSA_OK) return 0;
+  if (p->pipeline == 3) return stream_eligible(p) ? 3 : -1;
+  if (stream_default(p)) return 3;
   if (p->pipeline < 0 || !fused_eligible(p)) return -1;
   return p->pipeline == 1 ? 1 : 2;
 }
@@ -670,6 +802,42 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   const double *tWlo = full ? w.fWlo : w.cWlo;
   const int32_t *tBin = full ? w.fBin : w.cBin;
   const bool rt = w.R != nullptr;
+  if (rt && !full && mode != tsa::SPP) {
+    // canonical k >= 3: tables built per work item by the searching CTA
+    // (k_search_tri), shared memory when they fit
+    tsa::SearchArgs a = {};
+    a.C = w.cC;
+    a.Whi = w.cWhi;
+    a.Wlo = w.cWlo;
+    a.Asuf = w.Asuf;
+    a.R = w.R;
+    a.PP = w.PP;
+    a.AI = w.AI;
+    a.counter = w.counter;
+    a.Bin = w.cBin;
+    a.Mz = w.M;
+    a.status = slice_status;
+    a.part_score = part_score;
+    a.part_key = part_key;
+    a.luts = l;
+    a.nz = nz;
+    a.E = E;
+    a.L = bins;
+    a.RS = rstride(bins);
+    a.units = units;
+    a.unit_begin = unit_begin;
+    a.nunits = unit_end - unit_begin;
+    const int64_t items = nz * (int64_t)a.nunits;
+    const size_t smem = tsa::kTriSmemBytes;
+    auto kern = k == 3 ? (mode == tsa::PROD_MAX ? tsa::k_search_tri<3, tsa::PROD_MAX>
+                          : mode == tsa::PROD_MIN ? tsa::k_search_tri<3, tsa::PROD_MIN> : tsa::k_search_tri<3, tsa::SUM>)
+                       : (mode == tsa::PROD_MAX ? tsa::k_search_tri<4, tsa::PROD_MAX>
+                          : mode == tsa::PROD_MIN ? tsa::k_search_tri<4, tsa::PROD_MIN> : tsa::k_search_tri<4, tsa::SUM>);
+    TSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
+    kern<<<grid, 256, smem, s>>>(a, (int)(smem / sizeof(double)));
+    return check_cuda("k_search_tri");
+  }
   if (rt) {
     switch (mode) {
       case tsa::PROD_MAX: launch_rtable<tsa::PROD_MAX>(w, tC, tWhi, tWlo, slice_status, nz, E, bins, l, s); break;
@@ -856,7 +1024,10 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   if (workspace_bytes < need) return set_error(TSA_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = S(stream);
   const bool labels_aligned = !out->labels || (reinterpret_cast<uintptr_t>(out->labels) & 15) == 0;
-  if (p->pipeline >= 0 && fused_eligible(p) && labels_aligned)
+  if ((p->pipeline == 3 || stream_default(p)) && stream_eligible(p) && labels_aligned)
+    return segment_stream(p, out, w, s);
+  if (p->pipeline == 3) return set_error(TSA_ERR_INVALID_ARG, "stream pipeline requested but the problem is not eligible");
+  if (p->pipeline >= 0 && p->pipeline <= 2 && fused_eligible(p) && labels_aligned)
     return segment_fused(p, out, w, s, p->pipeline == 1);
   if (p->pipeline > 0) return set_error(TSA_ERR_INVALID_ARG, "fused/compact pipeline requested but the problem is not eligible");
   uint32_t *hist = out->histogram ? out->histogram : w.hist;
@@ -1440,18 +1611,26 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   int32_t *thr_all = cs.take<int32_t>((size_t)p->nz * p->k);
   double *obj_all = cs.take<double>((size_t)p->nz);
   int32_t *sts_all = cs.take<int32_t>((size_t)p->nz);
-  // stream0: copy-in + compute; stream1: copy-out.  Two device buffers: slab
-  // i+2 may overwrite buffer i%2 once slab i's labels left (ev_free), slab
-  // i's labels leave once it is computed (ev_done) -- so the H2D engine
-  // streams slab i+1 while the D2H engine drains slab i.  Thresholds,
-  // objective and status stay on the device for the whole volume and are
-  // copied once at the end (three small copies instead of three per slab).
-  cudaStream_t cin = S(stream0), cout = S(stream1);
-  cudaEvent_t ev_done[2], ev_free[2];
+  // Three streams: copy-in on a stream of this call (created and destroyed
+  // here: the call blocks anyway), compute on stream0, copy-out on stream1.
+  // Two device buffers: slab i+2 may overwrite buffer i%2 once slab i's labels
+  // left (ev_free); slab i is computed once it arrived (ev_in) and its labels
+  // leave once it is computed (ev_done) -- so the H2D engine streams slab i+1
+  // while the kernels run on slab i and the D2H engine drains slab i-1.
+  // Thresholds, objective and status stay on the device for the whole volume
+  // and are copied once at the end.
+  cudaStream_t comp = S(stream0), cout = S(stream1), cin = nullptr;
+  TSA_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  cudaEvent_t ev_done[2], ev_free[2], ev_in[2], ev_start;
   for (int b = 0; b < 2; b++) {
     TSA_CUDA(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
     TSA_CUDA(cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming));
+    TSA_CUDA(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming));
   }
+  TSA_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  // the copy-in stream starts after work already queued on stream0
+  TSA_CUDA(cudaEventRecord(ev_start, comp));
+  TSA_CUDA(cudaStreamWaitEvent(cin, ev_start, 0));
   tsa_status rc = TSA_OK;
   for (int64_t z0 = 0, i = 0; z0 < p->nz && rc == TSA_OK; z0 += slab, i++) {
     const int64_t nzs = std::min(slab, p->nz - z0);
@@ -1471,11 +1650,17 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
     if (i >= 2 && cudaStreamWaitEvent(cin, ev_free[b], 0) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "wait ev_free");
     if (rc == TSA_OK && cudaMemcpyAsync(vol, src, (size_t)nzs * n * esz, cudaMemcpyHostToDevice, cin) != cudaSuccess)
       rc = set_error(TSA_ERR_CUDA, "H2D");
+    if (rc == TSA_OK && (cudaEventRecord(ev_in[b], cin) != cudaSuccess ||
+                         cudaStreamWaitEvent(comp, ev_in[b], 0) != cudaSuccess))
+      rc = set_error(TSA_ERR_CUDA, "ev_in");
+    // the compute of slab i reuses the workspace of buffer b: ordered after
+    // slab i-2's compute by stream order on comp
     tsa_outputs o{thr, lab_h ? lab : nullptr, obj, nullptr, sts};
-    if (rc == TSA_OK) rc = tsa_segment(&q, &o, ws, wsb, cin);
+    if (rc == TSA_OK) rc = tsa_segment(&q, &o, ws, wsb, comp);
     if (rc != TSA_OK) break;
+    if (!lab_h && cudaEventRecord(ev_free[b], comp) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "ev_free");
     if (lab_h) {
-      cudaError_t e = cudaEventRecord(ev_done[b], cin);
+      cudaError_t e = cudaEventRecord(ev_done[b], comp);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(cout, ev_done[b], 0);
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(lab_h + (size_t)z0 * n, lab, (size_t)nzs * n, cudaMemcpyDeviceToHost, cout);
@@ -1484,20 +1669,25 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
     }
   }
   if (rc == TSA_OK) {
-    cudaError_t e = cudaMemcpyAsync(thr_h, thr_all, sizeof(int32_t) * p->nz * p->k, cudaMemcpyDeviceToHost, cin);
+    cudaError_t e = cudaMemcpyAsync(thr_h, thr_all, sizeof(int32_t) * p->nz * p->k, cudaMemcpyDeviceToHost, comp);
     if (e == cudaSuccess && obj_h)
-      e = cudaMemcpyAsync(obj_h, obj_all, sizeof(double) * p->nz, cudaMemcpyDeviceToHost, cin);
+      e = cudaMemcpyAsync(obj_h, obj_all, sizeof(double) * p->nz, cudaMemcpyDeviceToHost, comp);
     if (e == cudaSuccess && st_h)
-      e = cudaMemcpyAsync(st_h, sts_all, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToHost, cin);
+      e = cudaMemcpyAsync(st_h, sts_all, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToHost, comp);
     if (e != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "D2H results");
   }
-  const cudaError_t e0 = cudaStreamSynchronize(cin), e1 = cudaStreamSynchronize(cout);
+  const cudaError_t e0 = cudaStreamSynchronize(comp), e1 = cudaStreamSynchronize(cout),
+                    e2 = cudaStreamSynchronize(cin);
   for (int b = 0; b < 2; b++) {
     cudaEventDestroy(ev_done[b]);
     cudaEventDestroy(ev_free[b]);
+    cudaEventDestroy(ev_in[b]);
   }
+  cudaEventDestroy(ev_start);
+  cudaStreamDestroy(cin);
   if (rc != TSA_OK) return rc;
-  if (e0 != cudaSuccess || e1 != cudaSuccess) return set_error(TSA_ERR_CUDA, "tsa_segment_host synchronize");
+  if (e0 != cudaSuccess || e1 != cudaSuccess || e2 != cudaSuccess)
+    return set_error(TSA_ERR_CUDA, "tsa_segment_host synchronize");
   return TSA_OK;
 }
 

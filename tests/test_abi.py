@@ -82,7 +82,11 @@ def test_pipeline_kind(lib):
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(k=3))) == -1        # k >= 3: staged
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=-1))) == -1
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(enumeration=1))) == -1
-    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024))) == -1
+    # k = 2 above 1024 bins (c5): the stream pipeline; forced stream on an eligible u8 problem
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024))) in (3, -1)
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=3))) == 3
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=3, k=3))) == -1
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024, k=1))) == -1
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(nx=37, ny=53))) == -1  # n % 16 != 0
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(q=0.0))) == 0
 

@@ -134,7 +134,8 @@ def max_over_ranks(x, world, device):
         return x
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    gloo = dist.get_backend() == "gloo"
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -1088,7 +1089,8 @@ def run_1d(args, cfg, rank, world, dev):
     # staged k_histogram + per q (k_small_luts + k_scan [+ k_rtable] + search
     # [+ k_merge_items] + k_finalize + label)
     rtable = k >= 3 and bins <= 512 and args.enumeration == "full"  # canonical k >= 3: k_search_tri
-    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0)
+    tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
+    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0)
     launches_per_step = {1: 1, 2: 4, 3: 2}.get(kind, 1 + per_q * len(qs))  # stream: k_small_luts + k_stream
     if rank == 0:
         line = {
@@ -1249,12 +1251,19 @@ def main():
 
     tsa.load()  # fails loudly if the CUDA library is missing: no fallback
     assert torch.cuda.is_available(), "bench needs a GPU"
+    # TSA_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 over gloo, to run
+    # the multi-rank flow on a one-GPU box; NCCL (one GPU per rank) otherwise
+    one_gpu = os.environ.get("TSA_BENCH_ONE_GPU") == "1"
+    local = 0 if one_gpu else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     try:
         if cfg.name in ("c1", "c2", "c3", "c4", "c5") and shard_mode(args, cfg, world) == "tuples":
             run_tuple_sharded(args, cfg, rank, world, dev)

@@ -16,7 +16,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsa.so")
+# TSA_LIB_PATH: an alternative build of the same library (A/B experiments in tools/)
+LIB_PATH = os.environ.get("TSA_LIB_PATH") or os.path.join(_HERE, "libtsa.so")
 
 TSA_OK, TSA_ERR_INVALID_ARG, TSA_ERR_LEVEL_OVERFLOW, TSA_ERR_NO_VALID_SPLIT = 0, 1, 2, 3
 TSA_ERR_WORKSPACE, TSA_ERR_CUDA, TSA_ERR_NCCL = 4, 5, 6

@@ -44,6 +44,8 @@ struct SearchArgs {
   int64_t nz;
   int E, L, RS, units, unit_begin;  // RS: R-table row stride (>= L + 8, even)
   int nunits;                        // units in this launch (unit_end - unit_begin)
+  int ss;                            // k_search_tri: CTA entries per slice
+  int32_t *ccur;                     // k_search_tri: [nz] per-slice chunk counters, zeroed
 };
 
 // STAGE: copy the slice's C/W/Asuf tables to shared memory first (L <= 1024).
@@ -529,23 +531,10 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
   }
 }
 
-// Exhaustive search for k >= 3 with the slice's class-term tables built by the
-// searching CTA itself (round 2; replaces k_rtable's HBM round trip of three
-// L x (L+8) tables per slice):
-//   T(i, j), 0 <= i <= j <= M-2      every class term (triangular, j(j+1)/2 + i)
-//   R[a][b] = T(a+1, b) (x) Asuf[b]  the last two classes, rows a <= M-3 stored
-//                                    from column (a+1) & ~1 in whole 8-column
-//                                    groups (NaN outside (a, M-2]), packed
-// in shared memory when they fit (M <= ~115 at two CTAs per SM: every CT
-// slice of the 8-bit configs, m ~ 90), else in the global fallback region
-// (g.R / g.PP per slice).  Prefix values are the same expressions as the
-// staged tables: K = 3: PP[t1][a] = T(0,t1) (x) T(t1+1,a); K = 4:
-// PP[t1][t2] (x) T(t2+1,a); the compare loop is search_row / search_row2.
-// So every tuple's value is bit-identical to k_search_rows' (tested).
-// Work items (slice, unit) from a global counter; a unit is a contiguous
-// colex range of the slice's prefixes, as in k_search_rows.
+// k_search_tri helpers (see the kernel below)
 __device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + i; }
 constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
+constexpr int kTriCum = 512 + 2;                 // item prefix sums, one per t_{k-1} (M <= bins <= 512)
 constexpr size_t kTriSmemBytes = 104 * 1024;     // dynamic tables: two CTAs per SM
 
 // doubles needed for the tables of a slice with M positions (rows packed)
@@ -558,133 +547,392 @@ __host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
   return r + (int64_t)(M - 1) * M / 2;
 }
 
+// Per-slice table region of k_search_tri (doubles): row offsets (M-1 ints,
+// padded to an even number of doubles so the rows stay 16-byte aligned), then
+// the packed R rows, then the triangular T table.
+__host__ __device__ __forceinline__ int tri_roff_doubles(int M) { return (((M + 1) / 2) + 1) & ~1; }
+__host__ __device__ __forceinline__ int64_t tri_region_doubles(int M) { return tri_roff_doubles(M) + tri_table_doubles(M); }
+
+// Build the tables of slice z into `base`: roff[a] (start of R row a;
+// roff[M-2] = start of T), the R rows, T.  Same expressions as k_rtable.
+template <int MODE>
+__device__ void tri_build(const SearchArgs &g, const int z, const int M, const SliceTables &t, double *base) {
+  int *roff = reinterpret_cast<int *>(base);
+  double *Rt = base + tri_roff_doubles(M);
+  const double *asz = g.Asuf + (size_t)z * g.L;
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int a = 0; a <= M - 3; a++) {
+      roff[a] = o;
+      o += 8 * ((M + 6 - ((a + 1) & ~1)) >> 3);
+    }
+    roff[M - 2] = o;  // start of the T table
+  }
+  __syncthreads();
+  double *Tt = Rt + roff[M - 2];
+  for (int j = 0, e0 = 0; j <= M - 2; e0 += ++j)  // T row j: entries e0 .. e0 + j
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) Tt[e0 + i] = class_term<MODE>(t, g.luts, i, j);
+  __syncthreads();
+  for (int a = 0; a <= M - 3; a++) {  // R rows (a, M-2]; stored from column (a+1) & ~1
+    const int sa = (a + 1) & ~1, len = roff[a + 1] - roff[a];
+    double *row = Rt + roff[a];
+    for (int c = threadIdx.x; c < len; c += blockDim.x) {
+      const int b = sa + c;
+      row[c] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+    }
+  }
+}
+
+// hit |= any(p_i (x) x_c >= best), i < 4 prefixes, c < 4 columns (x01, x23):
+// 16 DMUL/DADD + 16 DSETP in two predicate chains (2 FP64 instructions per
+// tuple, ~85 % of the issued instructions on the FP64 pipe).
+template <int MODE>
+__device__ __forceinline__ unsigned cmp_p4c4(unsigned hit, const double *p, double2 x01, double2 x23,
+                                             double best) {
+#define TSA_CMP_P4C4(OP)                                                                          \
+  asm("{\n\t.reg .pred a, b;\n\t.reg .f64 t<16>;\n\t"                                            \
+      "setp.ne.u32 a, %0, 0;\n\t"                                                                 \
+      OP " t0, %1, %5;\n\t" OP " t1, %1, %6;\n\t" OP " t2, %1, %7;\n\t" OP " t3, %1, %8;\n\t"    \
+      OP " t4, %2, %5;\n\t" OP " t5, %2, %6;\n\t" OP " t6, %2, %7;\n\t" OP " t7, %2, %8;\n\t"    \
+      OP " t8, %3, %5;\n\t" OP " t9, %3, %6;\n\t" OP " t10, %3, %7;\n\t" OP " t11, %3, %8;\n\t"  \
+      OP " t12, %4, %5;\n\t" OP " t13, %4, %6;\n\t" OP " t14, %4, %7;\n\t" OP " t15, %4, %8;\n\t" \
+      "setp.ge.f64 b, t1, %9;\n\t"                                                                \
+      "setp.ge.or.f64 a, t0, %9, a;\n\tsetp.ge.or.f64 b, t3, %9, b;\n\t"                          \
+      "setp.ge.or.f64 a, t2, %9, a;\n\tsetp.ge.or.f64 b, t5, %9, b;\n\t"                          \
+      "setp.ge.or.f64 a, t4, %9, a;\n\tsetp.ge.or.f64 b, t7, %9, b;\n\t"                          \
+      "setp.ge.or.f64 a, t6, %9, a;\n\tsetp.ge.or.f64 b, t9, %9, b;\n\t"                          \
+      "setp.ge.or.f64 a, t8, %9, a;\n\tsetp.ge.or.f64 b, t11, %9, b;\n\t"                         \
+      "setp.ge.or.f64 a, t10, %9, a;\n\tsetp.ge.or.f64 b, t13, %9, b;\n\t"                        \
+      "setp.ge.or.f64 a, t12, %9, a;\n\tsetp.ge.or.f64 b, t15, %9, b;\n\t"                        \
+      "setp.ge.or.f64 a, t14, %9, a;\n\t"                                                         \
+      "or.pred a, a, b;\n\tselp.u32 %0, 1, 0, a;\n\t}"                                            \
+      : "+r"(hit)                                                                                 \
+      : "d"(p[0]), "d"(p[1]), "d"(p[2]), "d"(p[3]), "d"(x01.x), "d"(x01.y), "d"(x23.x), "d"(x23.y), \
+        "d"(best))
+  if (MODE == SUM) {
+    TSA_CMP_P4C4("add.rn.f64");
+  } else {
+    TSA_CMP_P4C4("mul.rn.f64");
+  }
+#undef TSA_CMP_P4C4
+  return hit;
+}
+
+// One prefix, four columns (k = 3: a prefix row is short, one per lane).
+template <int MODE>
+__device__ __forceinline__ unsigned cmp_p1c4(unsigned hit, double p, double2 x01, double2 x23, double best) {
+#define TSA_CMP_P1C4(OP)                                                                          \
+  asm("{\n\t.reg .pred a, b;\n\t.reg .f64 t<4>;\n\t"                                             \
+      "setp.ne.u32 a, %0, 0;\n\t"                                                                 \
+      OP " t0, %1, %2;\n\t" OP " t1, %1, %3;\n\t" OP " t2, %1, %4;\n\t" OP " t3, %1, %5;\n\t"    \
+      "setp.ge.f64 b, t1, %6;\n\tsetp.ge.or.f64 a, t0, %6, a;\n\t"                               \
+      "setp.ge.or.f64 b, t3, %6, b;\n\tsetp.ge.or.f64 a, t2, %6, a;\n\t"                         \
+      "or.pred a, a, b;\n\tselp.u32 %0, 1, 0, a;\n\t}"                                            \
+      : "+r"(hit)                                                                                 \
+      : "d"(p), "d"(x01.x), "d"(x01.y), "d"(x23.x), "d"(x23.y), "d"(best))
+  if (MODE == SUM) {
+    TSA_CMP_P1C4("add.rn.f64");
+  } else {
+    TSA_CMP_P1C4("mul.rn.f64");
+  }
+#undef TSA_CMP_P1C4
+  return hit;
+}
+
+// One CTA's share of slice z, register-tiled like a GEMM micro-kernel with
+// (max, x): items are (a, chunk) -- a = t_{k-1}, a chunk = 32 P consecutive
+// prefixes ending at a (P = 4 for k = 4, 1 for k = 3); a lane holds P prefix
+// values and streams the shared row R[a][*] four columns at a time (one
+// broadcast 32-byte shared load serves 4P tuples), testing value >= best in
+// predicate chains.  Only a lane whose tile produced a hit rescans its rows
+// exactly (the staged kernels' value, (score desc, key asc) order).  Items are
+// claimed from the slice's counter by warps of every CTA on the slice.
+// A lower bound for the slice's best score, to seed the rescan test: the
+// value (same expression tree as the search) of a tuple found by coordinate
+// ascent from evenly spaced thresholds (3 passes, warp 0; any valid tuple's
+// value is a valid seed -- a good one makes exact rescans rare).  The search
+// then compares against it with key = none, so the tuples scoring >= it,
+// the argmax among them, are all still found exactly.
+template <int K, int MODE>
+__device__ __forceinline__ double tri_seed(const int M, const double *base) {
+  __shared__ double s_seed;
+  constexpr int R = K - 1;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int *roff = reinterpret_cast<const int *>(base);
+    const double *Rt = base + tri_roff_doubles(M);
+    const double *Tt = Rt + roff[M - 2];
+    auto val = [&](const int *t) -> double {  // t[0..K-1] strictly increasing in [0, M-2]
+      const double p01 = combine<MODE>(Tt[tri_idx(0, t[0])], Tt[tri_idx(t[0] + 1, t[1])]);
+      double pre = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(t[1] + 1, t[R - 1])]);
+      if (MODE == PROD_MIN) pre = -pre;
+      const int a = t[R - 1], b = t[K - 1];
+      return combine<MODE>(pre, Rt[roff[a] - ((a + 1) & ~1) + b]);
+    };
+    int t[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) t[j] = (int)((int64_t)(j + 1) * (M - 1) / (K + 1)) - 1 + (j == 0);
+#pragma unroll
+    for (int j = 1; j < K; j++) t[j] = max(t[j], t[j - 1] + 1);  // strictly increasing
+    double best = val(t);
+    for (int pass = 0; pass < 3; pass++) {
+#pragma unroll
+      for (int j = 0; j < K; j++) {
+        const int lo = j == 0 ? 0 : t[j - 1] + 1, hi = j == K - 1 ? M - 2 : t[j + 1] - 1;
+        double bv = -CUDART_INF;
+        int bx = t[j];
+        for (int x = lo + lane; x <= hi; x += 32) {
+          int u[K];
+#pragma unroll
+          for (int i = 0; i < K; i++) u[i] = i == j ? x : t[i];
+          const double v = val(u);
+          if (v > bv || (v == bv && x < bx)) {
+            bv = v;
+            bx = x;
+          }
+        }
+        uint64_t key = (uint64_t)bx;
+        warp_argmax(bv, key);
+        if (bv > best) {
+          best = bv;
+          t[j] = (int)key;
+        }
+      }
+    }
+    if (lane == 0) s_seed = best;
+  }
+  __syncthreads();
+  return s_seed;
+}
+
+// Items of a slice: for a in [R-1, M-3] the prefixes ending at a have colex
+// ranks [C(a, R), C(a+1, R)); intersected with [r0, r1) and cut into chunks of
+// G; s_cum[a - (R-1) + 1] = items up to a (thread 0; returns the total).
+template <int K>
+__device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const uint64_t r1, int *s_cum) {
+  constexpr int R = K - 1, G = 32 * (K == 4 ? 4 : 1);
+  const int a0 = R - 1;
+  if (threadIdx.x == 0) {
+    int cum = 0;
+    s_cum[0] = 0;
+    for (int a = a0; a <= M - 3; a++) {
+      const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
+      cum += hi > lo ? (int)((hi - lo + G - 1) / G) : 0;
+      s_cum[a - a0 + 1] = cum;
+    }
+    s_cum[kTriCum - 1] = cum;
+  }
+  __syncthreads();
+  return s_cum[kTriCum - 1];
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, const uint64_t r0, const uint64_t r1,
+                                           const double *base, const int32_t *bin, int32_t *ccur,
+                                           const int *s_cum, const int nitems, double &best,
+                                           uint64_t &bestkey) {
+  constexpr int R = K - 1;          // prefix length (t_1 .. t_{k-1}, t_{k-1} = a)
+  constexpr int P = K == 4 ? 4 : 1;  // prefixes per lane
+  constexpr int G = 32 * P;          // prefixes per item
+  const int *roff = reinterpret_cast<const int *>(base);
+  const double *Rt = base + tri_roff_doubles(M);
+  const double *Tt = Rt + roff[M - 2];
+  const int a0 = R - 1, na = M - 3 - a0 + 1;  // a in [R-1, M-3]; items: s_cum (tri_items)
+  (void)na;
+  const int lane = threadIdx.x & 31;
+  bool first = true;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(ccur, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nitems) break;
+    int lo_i = 0, hi_i = na - 1;  // the a whose items contain c
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i + 1) >> 1;
+      if (s_cum[mid] <= c) lo_i = mid;
+      else hi_i = mid - 1;
+    }
+    const int a = a0 + lo_i;
+    const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
+    const uint64_t rb = lo + (uint64_t)(c - s_cum[lo_i]) * G + (uint64_t)lane * P;
+    // this lane's prefixes rb .. rb+P-1 (< hi), all ending at a
+    double pre[P];
+    int idx[P][R];
+    int nv = 0;
+    if (rb < hi) {
+      unrank_colex<R>(rb, idx[0]);
+#pragma unroll
+      for (int i = 0; i < P; i++) {
+        if (i > 0) {
+#pragma unroll
+          for (int j = 0; j < R; j++) idx[i][j] = idx[i - 1][j];
+          next_colex<R>(idx[i]);
+        }
+        const bool v = rb + i < hi;
+        nv += v;
+        const int *id = idx[i];
+        const double p01 = combine<MODE>(Tt[tri_idx(0, id[0])], Tt[tri_idx(id[0] + 1, id[1])]);
+        double pv = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(id[1] + 1, id[R - 1])]);
+        if (MODE == PROD_MIN) pv = -pv;  // (-pre)*R == -(pre*R) exactly
+        pre[i] = v ? pv : CUDART_NAN;    // NaN never compares >= best
+      }
+    }
+    if (nv > 0) {
+      const int sa = (a + 1) & ~1;
+      const double *row = Rt + roff[a] - sa;  // row[b], b in [sa, sa + 8 ng)
+      const double2 *rp = reinterpret_cast<const double2 *>(Rt + roff[a]);
+      const int nsteps = 2 * ((M - 1 - sa + 7) >> 3);  // 4-column steps
+      unsigned hit = 0;
+      for (int s = 0; s < nsteps; s++) {
+        const double2 x01 = rp[2 * s], x23 = rp[2 * s + 1];
+        if (P == 4) hit = cmp_p4c4<MODE>(hit, pre, x01, x23, best);
+        else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
+      }
+      if (hit) {  // exact rescan of this lane's rows, lower-lex prefix first
+#pragma unroll 1
+        for (int i = 0; i < nv; i++) {
+          uint64_t kp = 0;
+#pragma unroll
+          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[i][j] + 1];
+          for (int b = a + 1; b <= M - 2; b++) {
+            const double v = combine<MODE>(pre[i], row[b]);
+            if (v >= best) {
+              const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+              if (better(v, key, best, bestkey)) {
+                best = v;
+                bestkey = key;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (first) {  // the warp's best so far seeds every lane's test
+      warp_argmax(best, bestkey);
+      first = false;
+    }
+  }
+}
+
+// Tables of every slice (one CTA per slice) into the per-slice global regions.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_tri_tables(SearchArgs g) {
+  __shared__ uint32_t s_C[kTriMaxRows + 2];
+  __shared__ double s_Wh[kTriMaxRows + 2], s_Wl[kTriMaxRows + 2];
+  const int z = blockIdx.x;
+  const int M = g.Mz[z];
+  if (g.status[z] != kOK || M < 4) return;
+  const uint32_t *gC = g.C + (size_t)z * g.E;
+  const double *gWh = g.Whi + (size_t)z * g.E, *gWl = g.Wlo + (size_t)z * g.E;
+  const bool stage = M + 1 <= kTriMaxRows + 2;
+  if (stage)
+    for (int e = threadIdx.x; e <= M; e += blockDim.x) {
+      s_C[e] = gC[e];
+      s_Wh[e] = gWh[e];
+      s_Wl[e] = gWl[e];
+    }
+  __syncthreads();
+  const SliceTables t{stage ? s_C : gC, stage ? s_Wh : gWh, stage ? s_Wl : gWl, nullptr};
+  tri_build<MODE>(g, z, M, t, const_cast<double *>(g.R) + (size_t)z * g.L * g.RS);
+}
+
+// Exhaustive search for k >= 3 over per-slice class-term tables (round 2;
+// replaces k_rtable's three L x (L+8) HBM tables per slice):
+//   T(i, j), 0 <= i <= j <= M-2      every class term (triangular, j(j+1)/2 + i)
+//   R[a][b] = T(a+1, b) (x) Asuf[b]  the last two classes, rows a <= M-3 stored
+//                                    from column (a+1) & ~1 in whole 8-column
+//                                    groups (NaN outside (a, M-2]), packed
+// built once per slice by k_tri_tables (M^2 doubles: ~70 KB at m ~ 90) and
+// copied into shared memory by every CTA that searches the slice when they
+// fit (M <= ~115 at two CTAs per SM: every slice of the 8-bit configs), else
+// read from the global region.  Prefix values are the staged tables'
+// expressions: K = 3: PP[t1][a] = T(0,t1) (x) T(t1+1,a); K = 4:
+// PP[t1][t2] (x) T(t2+1,a); the compare loop is search_row / search_row2, so
+// every tuple's value is bit-identical to k_search_rows' (tested).
+// Work: entries e = z * ss + j (slices in order, ss entries each) from a
+// global counter; the CTAs on a slice share its prefix rows [r0, r1) (the
+// launch's units, one contiguous colex range) through a per-slice chunk
+// counter, so a slice's work spreads over up to ss CTAs and no CTA waits on a
+// long last item.  Entry results go to slot [j][z]; k_fold_slots merges.
 template <int K, int MODE>
 __global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_doubles) {
   static_assert(K >= 3 && K <= 4, "k = 3, 4");
   constexpr int R = K - 1;
-  constexpr int CH = 8;
   extern __shared__ __align__(16) double tsm[];
   __shared__ int s_item;
-  __shared__ int s_roff[kTriMaxRows];
-  __shared__ uint32_t s_C[kTriMaxRows + 2];
-  __shared__ double s_Wh[kTriMaxRows + 2], s_Wl[kTriMaxRows + 2];
   __shared__ int32_t s_bin[kTriMaxRows + 2];
-  const int64_t items = g.nz * (int64_t)g.nunits;
-  const size_t slice_doubles = (size_t)g.L * g.RS;  // global fallback region per slice
+  __shared__ int s_cum[kTriCum];
+  const int64_t items = g.nz * (int64_t)g.ss;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_item = atomicAdd(g.counter, 1);
     __syncthreads();
     const int64_t item = s_item;
     if (item >= items) break;
-    const int z = (int)(item / g.nunits);
-    const int ul = (int)(item % g.nunits);
-    const int u = g.unit_begin + ul;
+    const int z = (int)(item / g.ss);
+    const int j = (int)(item % g.ss);
     double best = -CUDART_INF;
     uint64_t bestkey = kKeyNone;
     const int st = g.status[z];
     const int M = g.Mz[z];
     const int P = M - 1;
-    const bool active = st == kOK && P >= K;
-    if (active) {
+    int32_t *ccur = g.ccur + z;
+    if (st == kOK && P >= K) {
       const uint64_t NR = binom((uint64_t)P, R);
-      const uint64_t r0 = NR * (uint64_t)u / (uint64_t)g.units;
-      const uint64_t r1 = NR * (uint64_t)(u + 1) / (uint64_t)g.units;
-      // tables: shared memory when they fit, else this slice's global region
-      const bool fits = M <= kTriMaxRows && tri_table_doubles(M) <= smem_doubles;
-      double *Rt = fits ? tsm : const_cast<double *>(g.R) + (size_t)z * slice_doubles;  // workspace
-      int *roff = fits ? s_roff : reinterpret_cast<int *>(const_cast<double *>(g.PP) + (size_t)z * slice_doubles);
-      // slice tables (positions 0..M-1, entry e = position + 1)
-      const bool stage = M + 1 <= kTriMaxRows + 2;
-      const uint32_t *gC = g.C + (size_t)z * g.E;
-      const double *gWh = g.Whi + (size_t)z * g.E, *gWl = g.Wlo + (size_t)z * g.E;
-      const int32_t *gB = g.Bin + (size_t)z * g.E;
-      if (stage)
-        for (int e = threadIdx.x; e <= M; e += blockDim.x) {
-          s_C[e] = gC[e];
-          s_Wh[e] = gWh[e];
-          s_Wl[e] = gWl[e];
-          s_bin[e] = gB[e];
+      const uint64_t r0 = NR * (uint64_t)g.unit_begin / (uint64_t)g.units;
+      const uint64_t r1 = NR * (uint64_t)(g.unit_begin + g.nunits) / (uint64_t)g.units;
+      const int nitems = tri_items<K>(M, r0, r1, s_cum);
+      // skip the copy when the slice's items are already all claimed
+      if (*((volatile int32_t *)ccur) < nitems) {
+        const double *region = g.R + (size_t)z * g.L * g.RS;
+        const int32_t *gB = g.Bin + (size_t)z * g.E;
+        const bool stage = M + 1 <= kTriMaxRows + 2;
+        if (stage)
+          for (int e = threadIdx.x; e <= M; e += blockDim.x) s_bin[e] = gB[e];
+        const int64_t nd = tri_region_doubles(M);
+        if (M <= kTriMaxRows && nd <= smem_doubles) {
+          // the slice's tables into shared memory (16-byte loads through L2)
+          const double2 *src = reinterpret_cast<const double2 *>(region);
+          double2 *dst = reinterpret_cast<double2 *>(tsm);
+          for (int64_t e = threadIdx.x; e < (nd + 1) / 2; e += blockDim.x) dst[e] = __ldcg(src + e);
+          __syncthreads();
+          best = tri_seed<K, MODE>(M, tsm);
+          tri_search<K, MODE>(g, M, r0, r1, tsm, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
+        } else {
+          __syncthreads();
+          best = tri_seed<K, MODE>(M, region);
+          tri_search<K, MODE>(g, M, r0, r1, region, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
         }
-      const SliceTables t{stage ? s_C : gC, stage ? s_Wh : gWh, stage ? s_Wl : gWl, nullptr};
-      const int32_t *bin = stage ? s_bin : gB;
-      const double *asz = g.Asuf + (size_t)z * g.L;
-      if (threadIdx.x == 0) {
-        int o = 0;
-        for (int a = 0; a <= M - 3; a++) {
-          roff[a] = o;
-          o += 8 * ((M + 6 - ((a + 1) & ~1)) >> 3);
-        }
-        roff[M - 2 > 0 ? M - 2 : 0] = o;  // start of the T table
-      }
-      __syncthreads();
-      const int tbase = roff[max(M - 2, 0)];
-      double *Tt = Rt + tbase;
-      const int ntri = (M - 1) * M / 2;
-      for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
-        // e = j(j+1)/2 + i
-        int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-        while (j * (j + 1) / 2 > e) j--;
-        while ((j + 1) * (j + 2) / 2 <= e) j++;
-        const int i = e - j * (j + 1) / 2;
-        Tt[e] = class_term<MODE>(t, g.luts, i, j);
-      }
-      __syncthreads();
-      // rows, flattened over all stored entries [0, tbase): the row of entry
-      // e is found by a binary search in roff
-      for (int e = threadIdx.x; e < tbase; e += blockDim.x) {
-        int lo = 0, hi = M - 3;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (roff[mid] <= e) lo = mid;
-          else hi = mid - 1;
-        }
-        const int a = lo, b = ((a + 1) & ~1) + (e - roff[a]);
-        Rt[e] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
-      }
-      __syncthreads();
-      auto pre_of = [&](const int *id) -> double {
-        const double p01 = combine<MODE>(Tt[tri_idx(0, id[0])], Tt[tri_idx(id[0] + 1, id[1])]);
-        const double p = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(id[1] + 1, id[R - 1])]);
-        return MODE == PROD_MIN ? -p : p;  // (-pre)*R == -(pre*R) exactly
-      };
-      const uint64_t span = (uint64_t)blockDim.x * CH;
-      const uint64_t nchunks = r1 > r0 ? (r1 - r0 + span - 1) / span : 0;
-      for (uint64_t ci = 0; ci < nchunks; ci++) {
-        const uint64_t rb = r0 + ci * span + (uint64_t)threadIdx.x * CH;
-        if (rb < r1) {
-          int idx[R];
-          unrank_colex<R>(rb, idx);
-          const uint64_t re_ = min(r1, rb + CH);
-          for (uint64_t r = rb; r < re_;) {
-            int nidx[R];
-#pragma unroll
-            for (int j = 0; j < R; j++) nidx[j] = idx[j];
-            next_colex<R>(nidx);
-            const int a = idx[R - 1];
-            const double *rowa = Rt + roff[min(a, max(M - 3, 0))] - ((a + 1) & ~1);
-            if (r + 1 < re_ && nidx[R - 1] == a && a <= M - 3) {
-              search_row2<MODE, R, false>(rowa, a, M, pre_of(idx), pre_of(nidx), idx, nidx, bin, best, bestkey);
-#pragma unroll
-              for (int j = 0; j < R; j++) idx[j] = nidx[j];
-              next_colex<R>(idx);
-              r += 2;
-            } else {
-              if (a <= M - 3) search_row<MODE, R, false>(rowa, a, M, pre_of(idx), idx, bin, best, bestkey);
-#pragma unroll
-              for (int j = 0; j < R; j++) idx[j] = nidx[j];
-              r += 1;
-            }
-          }
-        }
-        block_argmax(best, bestkey);
       }
     }
     block_argmax(best, bestkey);
     if (threadIdx.x == 0) {
-      g.part_score[(size_t)ul * g.nz + z] = best;
-      g.part_key[(size_t)ul * g.nz + z] = bestkey;
+      g.item_score[(size_t)j * g.nz + z] = best;
+      g.item_key[(size_t)j * g.nz + z] = bestkey;
     }
+  }
+}
+
+// Slots [ss][nz] of k_search_tri -> part[0][z] (merged), part[1..nu-1][z] = none.
+__global__ void k_fold_slots(const double *is, const uint64_t *ik, int ss, int64_t nz, int nu, double *ps,
+                             uint64_t *pk) {
+  const int64_t z = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (z >= nz) return;
+  double s = -CUDART_INF;
+  uint64_t k = kKeyNone;
+  for (int j = lane; j < ss; j += 32) {
+    const double os = is[(size_t)j * nz + z];
+    const uint64_t ok = ik[(size_t)j * nz + z];
+    if (better(os, ok, s, k)) {
+      s = os;
+      k = ok;
+    }
+  }
+  warp_argmax(s, k);
+  for (int u = lane; u < nu; u += 32) {
+    ps[(size_t)u * nz + z] = u == 0 ? s : -CUDART_INF;
+    pk[(size_t)u * nz + z] = u == 0 ? k : kKeyNone;
   }
 }
 
@@ -876,15 +1124,16 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
   }
 }
 
-// One warp's a-block i of slice positions (k = 2): lane l owns a = 32 i + l,
-// walks b = 32 i + 1 .. M - 2 kK2Rows rows at a time; returns the lane's best
-// (score, key) (not yet warp-reduced).  rz = the slice's K2Row table.  Every
-// k = 2 kernel (k_search_k2, the stream pipeline's k_st_search) runs this body,
-// so a tuple's value is the same expression tree everywhere.
+// One warp's tile of slice positions (k = 2): lane l owns a = 32 i + l and
+// walks b in [max(32 i + 1, blo), min(M - 2, bhi)] kK2Rows rows at a time;
+// returns the lane's best (score, key) (not yet warp-reduced).  rz = the
+// slice's K2Row table.  Every k = 2 kernel (k_search_k2: whole a-blocks; the
+// stream pipeline: 2-D tiles) runs this body, so a tuple's value is the same
+// expression tree everywhere.
 template <int MODE, int DEG>
-__device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int i, const int lane,
-                                         const Luts &l, const SpPair &tab, double &best,
-                                         uint64_t &bestkey) {
+__device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
+                                        const int lane, const Luts &l, const SpPair &tab, double &best,
+                                        uint64_t &bestkey) {
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int a = 32 * i + lane;
   const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
@@ -893,8 +1142,8 @@ __device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int
   const double Wah = ra.wh, Wal = ra.wl;
   // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
   const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
-  const int bend = M - 2;
-  int b0 = 32 * i + 1;
+  const int bend = min(M - 2, bhi);
+  int b0 = max(32 * i + 1, blo);
   for (const K2Row *pr = rz + b0 + 1; b0 <= bend; b0 += kK2Rows, pr += kK2Rows) {
     double vb[kK2Rows];
 #pragma unroll
@@ -923,7 +1172,16 @@ __device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int
 }
 
 template <int MODE, int DEG>
-__global__ void __launch_bounds__(256) k_search_k2(SearchArgs g) {
+__device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int i, const int lane,
+                                         const Luts &l, const SpPair &tab, double &best, uint64_t &bestkey) {
+  k2_tile<MODE, DEG>(rz, M, i, 32 * i + 1, M - 2, lane, l, tab, best, bestkey);
+}
+
+#ifndef TSA_K2_MINB
+#define TSA_K2_MINB 1  // minimum CTAs per SM of k_search_k2 (register cap; A/B builds)
+#endif
+template <int MODE, int DEG>
+__global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
   for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
   __syncthreads();

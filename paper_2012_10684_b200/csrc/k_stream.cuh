@@ -15,9 +15,9 @@
 // Working on slice z (work_slice, either role):
 //   scan    claimed by one CTA once all HC chunks are in: prefix tables
 //           (scan_slice, the staged k_scan body) -> sst[z] = done
-//   blocks  every warp claims a-blocks from the slice's counter and runs
-//           k2_block (the staged k_search_k2 body); the warp finishing the last
-//           a-block merges the partials, writes t* and sets mdone[z], and its
+//   tiles   every warp claims tiles (a-block x 128 second thresholds) from the
+//           slice's counter and runs k2_tile (the staged k_search_k2 body);
+//           the warp finishing the last tile merges the partials, writes t* and sets mdone[z], and its
 //           CTA then recomputes phi(t*) in the definition's order
 //           (finalize_slice, the staged k_finalize body).
 // An io CTA whose label task finds t* missing works on that slice itself, so
@@ -39,6 +39,7 @@
 namespace tsa {
 
 constexpr int kStThreads = 256;  // == kTableThreads == kFinThreads
+constexpr int kStTileB = 128;    // second-threshold span of a search tile
 
 struct StreamArgs {
   const uint8_t *vol;   // [nz][n] T
@@ -48,9 +49,9 @@ struct StreamArgs {
   int32_t *status;      // [nz] working status (scan / merge / finalize)
   int32_t *thresholds;  // [nz][2]
   uint8_t *labels;      // [nz][n] or null
-  double *item_score;   // [nz][NB] per a-block partials
+  double *item_score;   // [nz][NB] per-tile partials
   uint64_t *item_key;
-  int NB;               // a-blocks per slice at most: (L - 3) / 32 + 1
+  int NB;               // tiles per slice at most: a-blocks x second-threshold tiles
   double *ps;           // [nz] merged partial (finalize input)
   uint64_t *pk;
   int32_t *ctr;         // zeroed: [0..1] io head (u64), [2] search head,
@@ -229,25 +230,32 @@ __device__ void work_slice(const StreamArgs &g, const int64_t z, double *smem) {
       jr_ok = true;
     }
     const int M = s_M, st = s_st;
+    // 2-D tiles: a-block i (32 first thresholds) x kStTileB second thresholds,
+    // so no single item is long (a whole a-block is ~M tuples per lane)
     const int nb = (st == kOK && M >= 3) ? (M - 3) / 32 + 1 : 0;
-    const int nbe = max(nb, 1);
+    const int nbt = M >= 3 ? (M - 2) / kStTileB + 1 : 1;
+    const int nbe = max(nb * nbt, 1);
     const SpPair tab{s_jr};
     const Luts &l = g.scan.luts;
     for (;;) {
-      int b = 0;
-      if (lane == 0) b = atomicAdd(st_cnt(g, kBcur, z), 1);
-      b = __shfl_sync(0xffffffffu, b, 0);
-      if (b >= nbe) break;
+      int c = 0;
+      if (lane == 0) c = atomicAdd(st_cnt(g, kBcur, z), 1);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nbe) break;
       double best = -CUDART_INF;
       uint64_t bestkey = kKeyNone;
       if (nb > 0) {
-        k2_block<MODE, DEG>(g.scan.rows + z * g.scan.RE, M, b, lane, l, tab, best, bestkey);
-        warp_argmax(best, bestkey);
+        const int i = c / nbt, blo = (c % nbt) * kStTileB;
+        if (blo + kStTileB - 1 >= 32 * i + 1) {
+          k2_tile<MODE, DEG>(g.scan.rows + z * g.scan.RE, M, i, blo, blo + kStTileB - 1, lane, l, tab, best,
+                             bestkey);
+          warp_argmax(best, bestkey);
+        }
       }
       int last = 0;
       if (lane == 0) {
-        g.item_score[z * g.NB + b] = best;
-        g.item_key[z * g.NB + b] = bestkey;
+        g.item_score[z * g.NB + c] = best;
+        g.item_key[z * g.NB + c] = bestkey;
         __threadfence();
         last = atomicAdd(st_cnt(g, kBdone, z), 1) == nbe - 1;
         if (last) __threadfence();

@@ -137,7 +137,10 @@ struct SearchWs {
   double *item_score = nullptr;  // [nb][nz] k = 2 a-block partials
   uint64_t *item_key = nullptr;
   tsa::K2Row *rows = nullptr;    // [nz][k2_row_stride] packed positions (k = 2)
+  int32_t *ccur = nullptr;       // [nz] per-slice chunk counters (k_search_tri)
 };
+
+constexpr int kTriSS = 8;  // k_search_tri: CTA entries per slice
 
 // row stride of the k = 2 packed positions: entries 0..bins plus the rows the
 // kernel reads past a slice's end (kK2Rows)
@@ -168,6 +171,11 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   w.M = c.take<int32_t>(nz);
   w.counter = c.take<int32_t>(2);
   w.mmax = w.counter + 1;
+  if (k >= 3) {  // k_search_tri: entry slots [kTriSS][nz] and per-slice chunk counters
+    w.item_score = c.take<double>((size_t)kTriSS * nz);
+    w.item_key = c.take<uint64_t>((size_t)kTriSS * nz);
+    w.ccur = c.take<int32_t>(nz);
+  }
   if (k == 2) {
     w.item_score = c.take<double>((size_t)k2_blocks(bins) * nz);
     w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * nz);
@@ -313,12 +321,9 @@ int32_t tsa_units_for_sms(int64_t nz, int32_t bins, int32_t k, int32_t enumerati
   // k <= 2: the search kernels balance their work internally (k = 2: per-warp
   // a-block items from a global queue), so one unit per slice
   if (k <= 2) return 1;
-  if (k >= 3 && enumeration == TSA_ENUM_CANONICAL && bins <= 512) {
-    // k_search_tri rebuilds the slice's tables per work item: ~8 items per SM
-    const double u = std::ceil((double)sms * 8.0 / (double)nz);
-    const double rows = binom_d(0.45 * (bins - 1), k - 1);
-    return (int32_t)std::max(1.0, std::min({u, std::max(1.0, rows / 8192.0), 64.0}));
-  }
+  // k_search_tri balances a slice's rows over several CTAs itself (per-slice
+  // chunk counters): one unit per slice (units only partition ranks)
+  if (k >= 3 && enumeration == TSA_ENUM_CANONICAL && bins <= 512) return 1;
   const double target = (double)sms * (k >= 3 ? 64.0 : 8.0);
   double rows = binom_d((double)bins - 1, k - 1);
   if (enumeration == TSA_ENUM_CANONICAL) rows = binom_d(0.45 * (bins - 1), k - 1);
@@ -353,9 +358,14 @@ struct SegWs {
   int32_t *povf;
   int32_t *counters;
   double *luts;
-  // stream pipeline: [3 + 6 nz] counters and flags
+  // stream pipeline: [3 + 6 nz] counters and flags, per-tile partials
   int32_t *sctr;
+  double *st_score;
+  uint64_t *st_key;
 };
+
+// tiles of a slice in the stream pipeline: a-blocks x second-threshold tiles
+static int stream_tiles(int32_t bins) { return k2_blocks(bins) * ((bins - 2) / tsa::kStTileB + 1); }
 
 // fused-pipeline constants (tuned on B200, profiles/)
 constexpr int kFusedHC = 2;   // histogram chunks per slice (persistent fused kernel)
@@ -387,6 +397,9 @@ static size_t carve_segment(const tsa_problem *p, char *base, SegWs *o) {
   w.counters = c.take<int32_t>(2 + 2 * (size_t)p->nz);
   w.luts = c.take<double>(tsa::kSmallLut);
   w.sctr = c.take<int32_t>(3 + tsa::kStCounters * (size_t)p->nz);
+  const size_t nt = p->k == 2 ? (size_t)stream_tiles(p->bins) * p->nz : 0;
+  w.st_score = c.take<double>(nt);
+  w.st_key = c.take<uint64_t>(nt);
   if (o) *o = w;
   return c.off;
 }
@@ -536,16 +549,16 @@ static tsa_status segment_fused(const tsa_problem *p, const tsa_outputs *out, co
   return check_cuda("k_fused");
 }
 
-// k_stream schedule: histogram and label chunks per slice (~128 K voxels
+// k_stream schedule: histogram and label chunks per slice (~256 K voxels
 // each; slab_slices overrides), search CTAs per slice, the label lag in
 // rounds of the io queue (label_lag overrides) and io CTAs per 4 CTAs.
 static void stream_schedule(const tsa_problem *p, int *HC, int *LC, int *SS, int *Dl, int *nio) {
   const int64_t n = p->nx * p->ny;
-  const int ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, (n + 131071) / 131072));
+  const int ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, (n + 262143) / 262144));
   *HC = p->slab_slices > 0 ? p->slab_slices : ch;
   *LC = *HC;
   *SS = 2;
-  *Dl = p->label_lag > 0 ? p->label_lag : 16;
+  *Dl = p->label_lag > 0 ? p->label_lag : 32;
   *nio = 2;
 }
 
@@ -575,9 +588,9 @@ static tsa_status segment_stream(const tsa_problem *p, const tsa_outputs *out, c
   a.status = w.status;
   a.thresholds = out->thresholds;
   a.labels = out->labels;
-  a.item_score = sw.item_score;
-  a.item_key = sw.item_key;
-  a.NB = k2_blocks(L);
+  a.item_score = w.st_score;
+  a.item_key = w.st_key;
+  a.NB = stream_tiles(L);
   a.ps = w.ps;
   a.pk = w.pk;
   tsa::ScanArgs &sa = a.scan;
@@ -827,16 +840,30 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     a.units = units;
     a.unit_begin = unit_begin;
     a.nunits = unit_end - unit_begin;
-    const int64_t items = nz * (int64_t)a.nunits;
+    a.ss = k == 3 ? 4 : kTriSS;
+    a.ccur = w.ccur;
+    a.item_score = w.item_score;
+    a.item_key = w.item_key;
+    TSA_CUDA(cudaMemsetAsync(w.ccur, 0, sizeof(int32_t) * nz, s));
+    const int64_t items = nz * (int64_t)a.ss;
     const size_t smem = tsa::kTriSmemBytes;
     auto kern = k == 3 ? (mode == tsa::PROD_MAX ? tsa::k_search_tri<3, tsa::PROD_MAX>
                           : mode == tsa::PROD_MIN ? tsa::k_search_tri<3, tsa::PROD_MIN> : tsa::k_search_tri<3, tsa::SUM>)
                        : (mode == tsa::PROD_MAX ? tsa::k_search_tri<4, tsa::PROD_MAX>
                           : mode == tsa::PROD_MIN ? tsa::k_search_tri<4, tsa::PROD_MIN> : tsa::k_search_tri<4, tsa::SUM>);
     TSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    switch (mode) {  // per-slice tables, once
+      case tsa::PROD_MAX: tsa::k_tri_tables<tsa::PROD_MAX><<<(unsigned)nz, 256, 0, s>>>(a); break;
+      case tsa::PROD_MIN: tsa::k_tri_tables<tsa::PROD_MIN><<<(unsigned)nz, 256, 0, s>>>(a); break;
+      default: tsa::k_tri_tables<tsa::SUM><<<(unsigned)nz, 256, 0, s>>>(a); break;
+    }
+    TSA_TRY(check_cuda("k_tri_tables"));
     const unsigned grid = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
     kern<<<grid, 256, smem, s>>>(a, (int)(smem / sizeof(double)));
-    return check_cuda("k_search_tri");
+    TSA_TRY(check_cuda("k_search_tri"));
+    tsa::k_fold_slots<<<(unsigned)((nz + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, a.ss, nz, a.nunits,
+                                                              part_score, part_key);
+    return check_cuda("k_fold_slots");
   }
   if (rt) {
     switch (mode) {

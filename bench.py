@@ -988,14 +988,16 @@ def run_1d(args, cfg, rank, world, dev):
             with open(tpath) as f:
                 tr = json.load(f).get(args.workload, {})
         dom = max(("histogram", "search", "label"), key=lambda n: kernels[n]["ms"])
-        if kind in (2, 3):
+        if kind in (2, 3, 4):
             # overlapped pipelines: the product step is one chain of co-resident
             # kernels, timed as a whole against the single-pass HBM floor
             names = {2: "compact step (k_lut_part + k_hist_part + k_mid + k_label_part, PDL-chained)",
-                     3: "stream step (k_st_io + k_st_search, co-resident, per-slice flags)"}
+                     3: "stream step (k_stream: io + search CTAs, per-slice flags)",
+                     4: "overlap step (staged kernels on 8 slabs over two streams: histogram / labels "
+                        "of one slab next to the search of another)"}
             ach = step_bytes / (ms_per_step * 1e-3) / 1e9
             roofline = {"bound": "hbm", "kernel": names[kind], "achieved": ach, "peak": hbm, "unit": "GB/s",
-                        "frac": ach / hbm, "traffic": tr.get({2: "compact", 3: "stream"}[kind]),
+                        "frac": ach / hbm, "traffic": tr.get({2: "compact", 3: "stream", 4: "overlap"}[kind]),
                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({how})",
                         "algorithmic_bytes_per_launch": step_bytes,
                         "note": "timed = the whole step (CUDA events over the timed region / steps); bytes = "
@@ -1091,7 +1093,8 @@ def run_1d(args, cfg, rank, world, dev):
     rtable = k >= 3 and bins <= 512 and args.enumeration == "full"  # canonical k >= 3: k_search_tri
     tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
     per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0)
-    launches_per_step = {1: 1, 2: 4, 3: 2}.get(kind, 1 + per_q * len(qs))  # stream: k_small_luts + k_stream
+    slabs = min(cfg.nz, 8)
+    launches_per_step = {1: 1, 2: 4, 3: 2, 4: slabs * (1 + per_q)}.get(kind, 1 + per_q * len(qs))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -1100,7 +1103,7 @@ def run_1d(args, cfg, rank, world, dev):
             "data": "synthetic", "config": config_of(cfg, args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
-            "kernels": kernels, "pipeline": {1: "fused", 2: "compact", 3: "stream"}.get(kind, "staged"),
+            "kernels": kernels, "pipeline": {1: "fused", 2: "compact", 3: "stream", 4: "overlap"}.get(kind, "staged"),
             "gtuples_per_s_nominal": cfg.nz * comb(bins - 1, k) * len(qs) * (world if mode == "replicas" else 1)
                                      / (ms_per_step * 1e-3) / 1e9,
             "gtuples_per_s_evaluated": evaluated * total_slices / max(nzl, 1) / (ms_per_step * 1e-3) / 1e9,

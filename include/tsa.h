@@ -106,12 +106,18 @@ typedef struct {
    *                histogram chunks and label chunks while its search CTAs
    *                run each slice's tables and exhaustive search (k = 2,
    *                CANONICAL, PSEUDO_ADDITIVE, nx*ny % 16 == 0, aligned);
+   *                4 = overlap: the staged kernels on slabs of slices over
+   *                the caller's stream and a second stream the call creates,
+   *                so the histogram / labels of one slab overlap the search of
+   *                another (any problem; staged while the stream is being
+   *                captured into a CUDA graph);
    *                -1 = staged: one kernel per stage (any problem);
-   *                0 = stream for eligible k = 2 problems above 1024 bins,
+   *                0 = overlap for k = 2 above 1024 bins with >= 16 slices,
    *                else compact whenever eligible, else staged
    *   slab_slices  fused: slices per pipeline slab; compact: histogram CTAs
    *                per SM (default 4); stream: histogram / label chunks per
-   *                slice (default ~128 K voxels each)
+   *                slice (default ~256 K voxels each); overlap: number of
+   *                slabs (default 8, at most 64)
    *   label_lag    fused: rounds by which labelling trails the histogram;
    *                stream: slices by which labelling trails the histogram
    *                (default 16); compact: ignored */
@@ -134,7 +140,8 @@ tsa_status tsa_validate(const tsa_problem *p);
 /* Bytes of workspace tsa_segment needs for this problem (0 if invalid). */
 size_t tsa_workspace_size(const tsa_problem *p);
 
-/* Which implementation tsa_segment runs for this problem: 3 = stream (one
+/* Which implementation tsa_segment runs for this problem: 4 = overlap (staged
+ * kernels on two streams), 3 = stream (one
  * persistent kernel), 2 = compact (3 kernels), 1 = persistent fused kernel,
  * -1 = staged (one kernel per stage), 0 = invalid problem.  (Labels must also
  * be 16-byte aligned for 1, 2 and 3.) */

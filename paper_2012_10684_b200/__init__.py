@@ -219,7 +219,7 @@ def _dtype_code(vol):
     raise ValueError(f"volume dtype must be uint8 or uint16, got {vol.dtype}")
 
 
-PIPELINES = {"auto": 0, "fused": 1, "compact": 2, "staged": -1, "stream": 3}
+PIPELINES = {"auto": 0, "fused": 1, "compact": 2, "staged": -1, "stream": 3, "overlap": 4}
 
 
 def make_problem(vol, bins, k, q, objective="pseudo_additive", enumeration="canonical", units=0,

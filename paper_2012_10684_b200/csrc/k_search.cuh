@@ -535,22 +535,24 @@ __global__ void __launch_bounds__(256, 3) k_search_rows(SearchArgs g) {
 __device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + i; }
 constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
 constexpr int kTriCum = 512 + 2;                 // item prefix sums, one per t_{k-1} (M <= bins <= 512)
+constexpr int kTri3Cols = 96;                    // k = 3: last thresholds per item (3 per lane)
 constexpr size_t kTriSmemBytes = 104 * 1024;     // dynamic tables: two CTAs per SM
 
 // doubles needed for the tables of a slice with M positions (rows packed)
+// R row a of k_search_tri: columns from sa = (a+1) & ~1 in whole 4-column
+// steps up to M-2 (NaN outside (a, M-2])
+__host__ __device__ __forceinline__ int tri_row_len(int M, int a) { return 4 * ((M + 2 - ((a + 1) & ~1)) >> 2); }
 __host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
   int64_t r = 0;
-  for (int a = 0; a <= M - 3; a++) {
-    const int sa = (a + 1) & ~1;
-    r += 8 * ((M + 6 - sa) >> 3);
-  }
+  for (int a = 0; a <= M - 3; a++) r += tri_row_len(M, a);
   return r + (int64_t)(M - 1) * M / 2;
 }
 
 // Per-slice table region of k_search_tri (doubles): row offsets (M-1 ints,
 // padded to an even number of doubles so the rows stay 16-byte aligned), then
 // the packed R rows, then the triangular T table.
-__host__ __device__ __forceinline__ int tri_roff_doubles(int M) { return (((M + 1) / 2) + 1) & ~1; }
+// (the last double of the offsets area holds the slice's seed score, tri_seed)
+__host__ __device__ __forceinline__ int tri_roff_doubles(int M) { return (((M + 1) / 2) + 2) & ~1; }
 __host__ __device__ __forceinline__ int64_t tri_region_doubles(int M) { return tri_roff_doubles(M) + tri_table_doubles(M); }
 
 // Build the tables of slice z into `base`: roff[a] (start of R row a;
@@ -564,22 +566,32 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     int o = 0;
     for (int a = 0; a <= M - 3; a++) {
       roff[a] = o;
-      o += 8 * ((M + 6 - ((a + 1) & ~1)) >> 3);
+      o += tri_row_len(M, a);
     }
     roff[M - 2] = o;  // start of the T table
   }
   __syncthreads();
-  double *Tt = Rt + roff[M - 2];
-  for (int j = 0, e0 = 0; j <= M - 2; e0 += ++j)  // T row j: entries e0 .. e0 + j
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) Tt[e0 + i] = class_term<MODE>(t, g.luts, i, j);
+  const int tbase = roff[M - 2];
+  double *Tt = Rt + tbase;
+  // flattened over all entries (every thread busy; round 2's first version
+  // looped over rows with at most M threads active and was latency-bound)
+  const int ntri = (M - 1) * M / 2;
+  for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
+    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // e = j(j+1)/2 + i, i <= j
+    while (j * (j + 1) / 2 > e) j--;
+    while ((j + 1) * (j + 2) / 2 <= e) j++;
+    Tt[e] = class_term<MODE>(t, g.luts, e - j * (j + 1) / 2, j);
+  }
   __syncthreads();
-  for (int a = 0; a <= M - 3; a++) {  // R rows (a, M-2]; stored from column (a+1) & ~1
-    const int sa = (a + 1) & ~1, len = roff[a + 1] - roff[a];
-    double *row = Rt + roff[a];
-    for (int c = threadIdx.x; c < len; c += blockDim.x) {
-      const int b = sa + c;
-      row[c] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+  for (int e = threadIdx.x; e < tbase; e += blockDim.x) {  // R rows: row a holds [roff[a], roff[a+1])
+    int lo = 0, hi = M - 3;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (roff[mid] <= e) lo = mid;
+      else hi = mid - 1;
     }
+    const int a = lo, b = ((a + 1) & ~1) + (e - roff[a]);
+    Rt[e] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
   }
 }
 
@@ -615,6 +627,26 @@ __device__ __forceinline__ unsigned cmp_p4c4(unsigned hit, const double *p, doub
     TSA_CMP_P4C4("mul.rn.f64");
   }
 #undef TSA_CMP_P4C4
+  return hit;
+}
+
+// One prefix value against the lane's three columns (k = 3 tiles).
+template <int MODE>
+__device__ __forceinline__ unsigned cmp_p1c3(unsigned hit, double p, const double *x, double best) {
+#define TSA_CMP_P1C3(OP)                                                                          \
+  asm("{\n\t.reg .pred a;\n\t.reg .f64 t<3>;\n\t"                                                \
+      "setp.ne.u32 a, %0, 0;\n\t"                                                                 \
+      OP " t0, %1, %2;\n\t" OP " t1, %1, %3;\n\t" OP " t2, %1, %4;\n\t"                          \
+      "setp.ge.or.f64 a, t0, %5, a;\n\tsetp.ge.or.f64 a, t1, %5, a;\n\t"                          \
+      "setp.ge.or.f64 a, t2, %5, a;\n\tselp.u32 %0, 1, 0, a;\n\t}"                                \
+      : "+r"(hit)                                                                                 \
+      : "d"(p), "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(best))
+  if (MODE == SUM) {
+    TSA_CMP_P1C3("add.rn.f64");
+  } else {
+    TSA_CMP_P1C3("mul.rn.f64");
+  }
+#undef TSA_CMP_P1C3
   return hit;
 }
 
@@ -710,14 +742,17 @@ __device__ __forceinline__ double tri_seed(const int M, const double *base) {
 // G; s_cum[a - (R-1) + 1] = items up to a (thread 0; returns the total).
 template <int K>
 __device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const uint64_t r1, int *s_cum) {
-  constexpr int R = K - 1, G = 32 * (K == 4 ? 4 : 1);
+  constexpr int R = K - 1, G = 32 * (K == 4 ? 16 : 1);  // = tri_search's 32 P Q
   const int a0 = R - 1;
   if (threadIdx.x == 0) {
     int cum = 0;
     s_cum[0] = 0;
     for (int a = a0; a <= M - 3; a++) {
       const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
-      cum += hi > lo ? (int)((hi - lo + G - 1) / G) : 0;
+      if (K == 3)  // column blocks of kTri3Cols second-last... last thresholds b in (a, M-2]
+        cum += hi > lo ? (M - 2 - a + kTri3Cols - 1) / kTri3Cols : 0;
+      else
+        cum += hi > lo ? (int)((hi - lo + G - 1) / G) : 0;
       s_cum[a - a0 + 1] = cum;
     }
     s_cum[kTriCum - 1] = cum;
@@ -731,14 +766,14 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
                                            const double *base, const int32_t *bin, int32_t *ccur,
                                            const int *s_cum, const int nitems, double &best,
                                            uint64_t &bestkey) {
-  constexpr int R = K - 1;          // prefix length (t_1 .. t_{k-1}, t_{k-1} = a)
-  constexpr int P = K == 4 ? 4 : 1;  // prefixes per lane
-  constexpr int G = 32 * P;          // prefixes per item
+  constexpr int R = K - 1;           // prefix length (t_1 .. t_{k-1}, t_{k-1} = a)
+  constexpr int P = K == 4 ? 4 : 1;  // prefixes per register tile
+  constexpr int Q = K == 4 ? 4 : 1;  // tiles per lane per item
+  constexpr int G = 32 * P * Q;      // prefixes per item
   const int *roff = reinterpret_cast<const int *>(base);
   const double *Rt = base + tri_roff_doubles(M);
   const double *Tt = Rt + roff[M - 2];
   const int a0 = R - 1, na = M - 3 - a0 + 1;  // a in [R-1, M-3]; items: s_cum (tri_items)
-  (void)na;
   const int lane = threadIdx.x & 31;
   bool first = true;
   for (;;) {
@@ -754,49 +789,36 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
     }
     const int a = a0 + lo_i;
     const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
-    const uint64_t rb = lo + (uint64_t)(c - s_cum[lo_i]) * G + (uint64_t)lane * P;
-    // this lane's prefixes rb .. rb+P-1 (< hi), all ending at a
-    double pre[P];
-    int idx[P][R];
-    int nv = 0;
-    if (rb < hi) {
-      unrank_colex<R>(rb, idx[0]);
-#pragma unroll
-      for (int i = 0; i < P; i++) {
-        if (i > 0) {
-#pragma unroll
-          for (int j = 0; j < R; j++) idx[i][j] = idx[i - 1][j];
-          next_colex<R>(idx[i]);
-        }
-        const bool v = rb + i < hi;
-        nv += v;
-        const int *id = idx[i];
-        const double p01 = combine<MODE>(Tt[tri_idx(0, id[0])], Tt[tri_idx(id[0] + 1, id[1])]);
-        double pv = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(id[1] + 1, id[R - 1])]);
-        if (MODE == PROD_MIN) pv = -pv;  // (-pre)*R == -(pre*R) exactly
-        pre[i] = v ? pv : CUDART_NAN;    // NaN never compares >= best
-      }
-    }
-    if (nv > 0) {
+    if (K == 3) {
+      // lanes over the last threshold b (3 columns each), loop over t_1:
+      // the prefix value (one per t_1) is a broadcast, the R values stay in
+      // registers: 2 FP64 instructions per tuple + 1 DMUL per t_1
       const int sa = (a + 1) & ~1;
-      const double *row = Rt + roff[a] - sa;  // row[b], b in [sa, sa + 8 ng)
-      const double2 *rp = reinterpret_cast<const double2 *>(Rt + roff[a]);
-      const int nsteps = 2 * ((M - 1 - sa + 7) >> 3);  // 4-column steps
-      unsigned hit = 0;
-      for (int s = 0; s < nsteps; s++) {
-        const double2 x01 = rp[2 * s], x23 = rp[2 * s + 1];
-        if (P == 4) hit = cmp_p4c4<MODE>(hit, pre, x01, x23, best);
-        else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
-      }
-      if (hit) {  // exact rescan of this lane's rows, lower-lex prefix first
-#pragma unroll 1
-        for (int i = 0; i < nv; i++) {
-          uint64_t kp = 0;
+      const double *row = Rt + roff[a] - sa;
+      const int bb = a + 1 + (c - s_cum[lo_i]) * kTri3Cols + lane;
+      double rv[3];
 #pragma unroll
-          for (int j = 0; j < R; j++) kp = (kp << 12) | (uint64_t)bin[idx[i][j] + 1];
-          for (int b = a + 1; b <= M - 2; b++) {
-            const double v = combine<MODE>(pre[i], row[b]);
-            if (v >= best) {
+      for (int u = 0; u < 3; u++) {
+        const int b = bb + 32 * u;
+        rv[u] = b <= M - 2 ? row[b] : CUDART_NAN;
+      }
+      const int t1lo = (int)(lo - binom((uint64_t)a, 2)), t1hi = (int)(hi - binom((uint64_t)a, 2));
+      unsigned hit = 0;
+      for (int t1 = t1lo; t1 < t1hi; t1++) {
+        double pre = combine<MODE>(Tt[tri_idx(0, t1)], Tt[tri_idx(t1 + 1, a)]);
+        if (MODE == PROD_MIN) pre = -pre;
+        hit = cmp_p1c3<MODE>(hit, pre, rv, best);
+      }
+      if (hit) {  // exact rescan of this lane's tuples in lex order (t_1, then b)
+        for (int t1 = t1lo; t1 < t1hi; t1++) {
+          double pre = combine<MODE>(Tt[tri_idx(0, t1)], Tt[tri_idx(t1 + 1, a)]);
+          if (MODE == PROD_MIN) pre = -pre;
+          const uint64_t kp = ((uint64_t)bin[t1 + 1] << 12) | (uint64_t)bin[a + 1];
+#pragma unroll
+          for (int u = 0; u < 3; u++) {
+            const int b = bb + 32 * u;
+            const double v = combine<MODE>(pre, rv[u]);
+            if (b <= M - 2 && v >= best) {
               const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
               if (better(v, key, best, bestkey)) {
                 best = v;
@@ -806,6 +828,65 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
           }
         }
       }
+      if (first) {
+        warp_argmax(best, bestkey);
+        first = false;
+      }
+      continue;
+    }
+    uint64_t rb = lo + (uint64_t)(c - s_cum[lo_i]) * G + (uint64_t)lane * (P * Q);
+    if (rb < hi) {
+      const int sa = (a + 1) & ~1;
+      const double *row = Rt + roff[a] - sa;  // row[b], b in [sa, sa + tri_row_len)
+      const double2 *rp = reinterpret_cast<const double2 *>(Rt + roff[a]);
+      const int nsteps = tri_row_len(M, a) >> 2;  // 4-column steps
+      int idx[R];
+      unrank_colex<R>(rb, idx);
+#pragma unroll 1
+      for (int q = 0; q < Q && rb < hi; q++) {
+        // this tile's prefixes rb .. rb+P-1 (< hi), all ending at a
+        double pre[P];
+        int tid0[P], tid1[P];
+        int nv = 0;
+#pragma unroll
+        for (int i = 0; i < P; i++) {
+          if (i > 0) next_colex<R>(idx);
+          const bool v = rb + i < hi;
+          nv += v;
+          tid0[i] = idx[0];
+          tid1[i] = idx[R - 2];
+          const double p01 = combine<MODE>(Tt[tri_idx(0, idx[0])], Tt[tri_idx(idx[0] + 1, idx[1])]);
+          double pv = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(idx[1] + 1, a)]);
+          if (MODE == PROD_MIN) pv = -pv;  // (-pre)*R == -(pre*R) exactly
+          pre[i] = v ? pv : CUDART_NAN;    // NaN never compares >= best
+        }
+        unsigned hit = 0;
+        for (int s = 0; s < nsteps; s++) {
+          const double2 x01 = rp[2 * s], x23 = rp[2 * s + 1];
+          if (P == 4) hit = cmp_p4c4<MODE>(hit, pre, x01, x23, best);
+          else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
+        }
+        if (hit) {  // exact rescan of this tile's rows, lower-lex prefix first
+#pragma unroll 1
+          for (int i = 0; i < nv; i++) {
+            uint64_t kp = (uint64_t)bin[tid0[i] + 1];
+            if (K == 4) kp = (kp << 12) | (uint64_t)bin[tid1[i] + 1];
+            kp = (kp << 12) | (uint64_t)bin[a + 1];
+            for (int b = a + 1; b <= M - 2; b++) {
+              const double v = combine<MODE>(pre[i], row[b]);
+              if (v >= best) {
+                const uint64_t key = (kp << 12) | (uint64_t)bin[b + 1];
+                if (better(v, key, best, bestkey)) {
+                  best = v;
+                  bestkey = key;
+                }
+              }
+            }
+          }
+        }
+        next_colex<R>(idx);  // first prefix of the next tile
+        rb += P;
+      }
     }
     if (first) {  // the warp's best so far seeds every lane's test
       warp_argmax(best, bestkey);
@@ -814,8 +895,9 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
   }
 }
 
-// Tables of every slice (one CTA per slice) into the per-slice global regions.
-template <int MODE>
+// Tables of every slice (one CTA per slice) into the per-slice global regions,
+// and the slice's seed score (tri_seed) in the last double of the offsets.
+template <int K, int MODE>
 __global__ void __launch_bounds__(256) k_tri_tables(SearchArgs g) {
   __shared__ uint32_t s_C[kTriMaxRows + 2];
   __shared__ double s_Wh[kTriMaxRows + 2], s_Wl[kTriMaxRows + 2];
@@ -833,7 +915,13 @@ __global__ void __launch_bounds__(256) k_tri_tables(SearchArgs g) {
     }
   __syncthreads();
   const SliceTables t{stage ? s_C : gC, stage ? s_Wh : gWh, stage ? s_Wl : gWl, nullptr};
-  tri_build<MODE>(g, z, M, t, const_cast<double *>(g.R) + (size_t)z * g.L * g.RS);
+  double *region = const_cast<double *>(g.R) + (size_t)z * g.L * g.RS;
+  tri_build<MODE>(g, z, M, t, region);
+  __syncthreads();
+  if (M - 1 >= K) {
+    const double seed = tri_seed<K, MODE>(M, region);
+    if (threadIdx.x == 0) region[tri_roff_doubles(M) - 1] = seed;
+  }
 }
 
 // Exhaustive search for k >= 3 over per-slice class-term tables (round 2;
@@ -896,11 +984,11 @@ __global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_do
           double2 *dst = reinterpret_cast<double2 *>(tsm);
           for (int64_t e = threadIdx.x; e < (nd + 1) / 2; e += blockDim.x) dst[e] = __ldcg(src + e);
           __syncthreads();
-          best = tri_seed<K, MODE>(M, tsm);
+          best = tsm[tri_roff_doubles(M) - 1];  // the slice's seed (k_tri_tables)
           tri_search<K, MODE>(g, M, r0, r1, tsm, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
         } else {
           __syncthreads();
-          best = tri_seed<K, MODE>(M, region);
+          best = region[tri_roff_doubles(M) - 1];
           tri_search<K, MODE>(g, M, r0, r1, region, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
         }
       }
@@ -1178,8 +1266,17 @@ __device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int
 }
 
 #ifndef TSA_K2_MINB
-#define TSA_K2_MINB 1  // minimum CTAs per SM of k_search_k2 (register cap; A/B builds)
+#define TSA_K2_MINB 4  // minimum CTAs per SM of k_search_k2 (register cap: 64; A/B builds)
 #endif
+// k = 2 search: warp items (slice z, a-block i, b-tile t) from a global
+// counter, a-block-major (longest blocks first), so every item is at most
+// kK2Tile second thresholds long (a whole a-block is ~M per lane: round 1's
+// items made the last ones a latency tail, and small slabs latency-bound).
+// Tile partials go to item_score/key[(i * nbt + t)][z], nbt = tiles per block
+// of the widest slice (from mmax); k_merge_items folds them per (unit, slice).
+constexpr int kK2Tile = 4096;  // one tile per a-block: 128-wide tiles measured 7 % slower on c5 (606 vs 564 us)
+__host__ __device__ __forceinline__ int k2_tiles(int m) { return m >= 3 ? (m - 2) / kK2Tile + 1 : 1; }
+
 template <int MODE, int DEG>
 __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
@@ -1190,37 +1287,41 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   const int lane = threadIdx.x & 31;
   const int mmax = *g.mmax;
   const int nbmax = mmax >= 3 ? (mmax - 3) / 32 + 1 : 0;  // a-blocks: a <= M-3
+  const int nbt = k2_tiles(mmax);
   const int w = g.nunits, U = g.units, u0 = g.unit_begin;
   // blocks of this launch: i = (t / w) * U + u0 + t % w, t < nbl
   const int nbl = nbmax <= u0 ? 0 : ((nbmax - u0) / U) * w + min(w, (nbmax - u0) % U);
   const uint32_t nz = (uint32_t)g.nz;
-  const uint32_t items = (uint32_t)nbl * nz;
+  const uint32_t items = (uint32_t)nbl * nbt * nz;
   for (;;) {
     uint32_t it = 0;
     if (lane == 0) it = (uint32_t)atomicAdd(g.counter, 1);
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= items) break;
-    const int tb = (int)(it / nz);
-    const int z = (int)(it - (uint32_t)tb * nz);
+    const int tt = (int)(it / nz);
+    const int z = (int)(it - (uint32_t)tt * nz);
+    const int tb = tt / nbt, bt = tt - tb * nbt;
     const int i = (tb / w) * U + u0 + tb % w;
     const int M = g.Mz[z];
+    const int blo = bt * kK2Tile, bhi = blo + kK2Tile - 1;
     double best = -CUDART_INF;
     uint64_t bestkey = kKeyNone;
-    if (g.status[z] == kOK && 32 * i <= M - 3) {
-      k2_block<MODE, DEG>(g.rows + (size_t)z * g.RE, M, i, lane, l, tab, best, bestkey);
+    if (g.status[z] == kOK && 32 * i <= M - 3 && bhi >= 32 * i + 1 && blo <= M - 2) {
+      k2_tile<MODE, DEG>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey);
       warp_argmax(best, bestkey);
     }
     if (lane == 0) {
-      g.item_score[(size_t)i * g.nz + z] = best;
-      g.item_key[(size_t)i * g.nz + z] = bestkey;
+      g.item_score[(size_t)(i * nbt + bt) * g.nz + z] = best;
+      g.item_key[(size_t)(i * nbt + bt) * g.nz + z] = bestkey;
     }
   }
 }
 
-// Per (unit u in [u0, u1), slice z), one warp: fold the k = 2 block partials
-// i == u (mod U), i < nblocks(z), into part[u - u0][z] under the total order.
+// Per (unit u in [u0, u1), slice z), one warp: fold the k = 2 tile partials of
+// the blocks i == u (mod U), i < nblocks(z), tiles t < nbt(z), into
+// part[u - u0][z] under the total order.
 __global__ void k_merge_items(const double *is, const uint64_t *ik, const int32_t *Mz, const int32_t *status,
-                              int64_t nz, int U, int u0, int nu, double *ps, uint64_t *pk) {
+                              const int32_t *mmax, int64_t nz, int U, int u0, int nu, double *ps, uint64_t *pk) {
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= nz * nu) return;  // warp-uniform
@@ -1228,11 +1329,16 @@ __global__ void k_merge_items(const double *is, const uint64_t *ik, const int32_
   const int u = u0 + (int)(t / nz);
   const int M = Mz[z];
   const int nb = (status[z] == kOK && M >= 3) ? (M - 3) / 32 + 1 : 0;
+  const int nbt = k2_tiles(*mmax), nbz = k2_tiles(M);  // slot stride, tiles of this slice
   double s = -CUDART_INF;
   uint64_t k = kKeyNone;
-  for (int i = u + lane * U; i < nb; i += 32 * U) {
-    const double os = is[(size_t)i * nz + z];
-    const uint64_t ok = ik[(size_t)i * nz + z];
+  const int nblk = nb > u ? (nb - u + U - 1) / U : 0;  // blocks u, u + U, ...
+  for (int e = lane; e < nblk * nbz; e += 32) {
+    const int i = u + (e / nbz) * U, bt = e % nbz;
+    const size_t o = (size_t)(i * nbt + bt) * nz + z;
+    if (bt * kK2Tile + kK2Tile - 1 < 32 * i + 1) continue;  // a tile below the block: not written
+    const double os = is[o];
+    const uint64_t ok = ik[o];
     if (better(os, ok, s, k)) {
       s = os;
       k = ok;

@@ -178,8 +178,19 @@ __device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h
 
 template <int MODE>
 __global__ void __launch_bounds__(kTableThreads) k_scan(ScanArgs g) {
-  extern __shared__ __align__(16) double wsh[];  // [L] then scan scratch
-  scan_slice<MODE>(g, blockIdx.x, g.hist + (int64_t)blockIdx.x * g.L, wsh);
+  // [L] doubles + 1 KB scan scratch, then the slice's histogram [L] u32: the
+  // per-thread bin loops of build_tables read it from shared memory (round 1
+  // read it from global memory with dependent branches: latency-bound, 74 us
+  // on c5)
+  extern __shared__ __align__(16) double wsh[];
+  uint32_t *hs = reinterpret_cast<uint32_t *>(wsh + g.L + 128);
+  const uint4 *h4 = reinterpret_cast<const uint4 *>(g.hist + (int64_t)blockIdx.x * g.L);
+  if ((g.L & 3) == 0 && (reinterpret_cast<uintptr_t>(g.hist) & 15) == 0)
+    for (int i = threadIdx.x; i < g.L / 4; i += blockDim.x) reinterpret_cast<uint4 *>(hs)[i] = __ldg(h4 + i);
+  else
+    for (int i = threadIdx.x; i < g.L; i += blockDim.x) hs[i] = g.hist[(int64_t)blockIdx.x * g.L + i];
+  __syncthreads();
+  scan_slice<MODE>(g, blockIdx.x, hs, wsh);
 }
 
 // R[a][b] = combine(T(a+1, b), Asuf[b]) for 0 <= a < b <= M-2 (k >= 3,

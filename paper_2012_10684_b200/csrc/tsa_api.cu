@@ -177,8 +177,8 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
     w.ccur = c.take<int32_t>(nz);
   }
   if (k == 2) {
-    w.item_score = c.take<double>((size_t)k2_blocks(bins) * nz);
-    w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * nz);
+    w.item_score = c.take<double>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
+    w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
     w.rows = c.take<tsa::K2Row>(nz * (size_t)k2_row_stride(bins) + kPad);
   }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
@@ -250,7 +250,7 @@ void launch_search_mode(int k, const tsa::SearchArgs &a, dim3 grid, cudaStream_t
 
 template <int MODE>
 void launch_scan(const tsa::ScanArgs &a, cudaStream_t s) {
-  const size_t smem = (size_t)a.L * sizeof(double) + 1024;
+  const size_t smem = (size_t)a.L * sizeof(double) + 1024 + (size_t)a.L * sizeof(uint32_t);
   if (smem > 48 * 1024) cudaFuncSetAttribute(tsa::k_scan<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tsa::k_scan<MODE><<<(unsigned)a.nz, tsa::kTableThreads, smem, s>>>(a);
 }
@@ -417,6 +417,13 @@ static bool stream_eligible(const tsa_problem *p) {
 constexpr bool kStreamAuto = false;
 static bool stream_default(const tsa_problem *p) {
   return kStreamAuto && p->pipeline == 0 && p->bins > 1024 && stream_eligible(p);
+}
+// the overlap pipeline (segment_overlap) by default where the search is heavy
+// and not covered by compact: k = 2 above 1024 bins (c5) with enough slices
+constexpr bool kOverlapAuto = false;  // enabled once measured faster (profiles/r2*)
+static bool overlap_default(const tsa_problem *p) {
+  return kOverlapAuto && p->pipeline == 0 && p->k == 2 && p->bins > 1024 && p->nz >= 16 &&
+         p->enumeration != TSA_ENUM_DP;
 }
 
 }  // extern "C"
@@ -658,6 +665,7 @@ int32_t tsa_pipeline_kind(const tsa_problem *p) {
   if (tsa_validate(p) != TSA_OK) return 0;
   if (p->pipeline == 3) return stream_eligible(p) ? 3 : -1;
   if (stream_default(p)) return 3;
+  if (p->pipeline == 4 || overlap_default(p)) return 4;
   if (p->pipeline < 0 || !fused_eligible(p)) return -1;
   return p->pipeline == 1 ? 1 : 2;
 }
@@ -719,10 +727,23 @@ tsa_status tsa_histogram(const tsa_problem *p, uint32_t *hist, int32_t *slice_st
   return check_cuda("k_histogram");
 }
 
+static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N, int32_t bins,
+                              int32_t k, double q, int32_t objective, int32_t enumeration, int32_t units,
+                              int32_t unit_begin, int32_t unit_end, double *part_score, uint64_t *part_key,
+                              void *workspace, size_t workspace_bytes, void *stream, int k2_ctas_per_sm);
+
 tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N,
                       int32_t bins, int32_t k, double q, int32_t objective, int32_t enumeration,
                       int32_t units, int32_t unit_begin, int32_t unit_end, double *part_score,
                       uint64_t *part_key, void *workspace, size_t workspace_bytes, void *stream) {
+  return search_impl(hist, slice_status, nz, N, bins, k, q, objective, enumeration, units, unit_begin, unit_end,
+                     part_score, part_key, workspace, workspace_bytes, stream, 4);
+}
+
+static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N, int32_t bins,
+                              int32_t k, double q, int32_t objective, int32_t enumeration, int32_t units,
+                              int32_t unit_begin, int32_t unit_end, double *part_score, uint64_t *part_key,
+                              void *workspace, size_t workspace_bytes, void *stream, int k2_ctas_per_sm) {
   if (!valid_search_shape(nz, N, bins, k, q, objective, enumeration))
     return set_error(TSA_ERR_INVALID_ARG, "search shape");
   if (!hist || !slice_status || !part_score || !part_key || !workspace)
@@ -840,7 +861,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     a.units = units;
     a.unit_begin = unit_begin;
     a.nunits = unit_end - unit_begin;
-    a.ss = k == 3 ? 4 : kTriSS;
+    a.ss = k == 3 ? 2 : 4;  // CTAs sharing a slice (k = 3 slices are small)
     a.ccur = w.ccur;
     a.item_score = w.item_score;
     a.item_key = w.item_key;
@@ -852,11 +873,11 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
                        : (mode == tsa::PROD_MAX ? tsa::k_search_tri<4, tsa::PROD_MAX>
                           : mode == tsa::PROD_MIN ? tsa::k_search_tri<4, tsa::PROD_MIN> : tsa::k_search_tri<4, tsa::SUM>);
     TSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    switch (mode) {  // per-slice tables, once
-      case tsa::PROD_MAX: tsa::k_tri_tables<tsa::PROD_MAX><<<(unsigned)nz, 256, 0, s>>>(a); break;
-      case tsa::PROD_MIN: tsa::k_tri_tables<tsa::PROD_MIN><<<(unsigned)nz, 256, 0, s>>>(a); break;
-      default: tsa::k_tri_tables<tsa::SUM><<<(unsigned)nz, 256, 0, s>>>(a); break;
-    }
+    auto tab = k == 3 ? (mode == tsa::PROD_MAX ? tsa::k_tri_tables<3, tsa::PROD_MAX>
+                         : mode == tsa::PROD_MIN ? tsa::k_tri_tables<3, tsa::PROD_MIN> : tsa::k_tri_tables<3, tsa::SUM>)
+                      : (mode == tsa::PROD_MAX ? tsa::k_tri_tables<4, tsa::PROD_MAX>
+                         : mode == tsa::PROD_MIN ? tsa::k_tri_tables<4, tsa::PROD_MIN> : tsa::k_tri_tables<4, tsa::SUM>);
+    tab<<<(unsigned)nz, 256, 0, s>>>(a);  // per-slice tables and seed, once
     TSA_TRY(check_cuda("k_tri_tables"));
     const unsigned grid = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
     kern<<<grid, 256, smem, s>>>(a, (int)(smem / sizeof(double)));
@@ -902,7 +923,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
   a.RE = k2_row_stride(bins);
   if (k == 2 && mode != tsa::SPP) {
     // warp-per-a-block search from a global item queue, then the per-unit fold
-    const int grid = 4 * g_num_sms();
+    const int grid = k2_ctas_per_sm * g_num_sms();
     auto kern = tsa::k_search_k2<tsa::SUM, 6>;
     if (mode == tsa::PROD_MAX)
       kern = l.deg == 5 ? tsa::k_search_k2<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MAX, 6>
@@ -913,7 +934,7 @@ tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, i
     kern<<<grid, 256, 0, s>>>(a);
     TSA_TRY(check_cuda("k_search_k2"));
     const int64_t nt = nz * (int64_t)a.nunits;
-    tsa::k_merge_items<<<(unsigned)((nt + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, w.M, slice_status,
+    tsa::k_merge_items<<<(unsigned)((nt + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, w.M, slice_status, w.mmax,
                                                                   nz, units, unit_begin, a.nunits, part_score,
                                                                   part_key);
     return check_cuda("k_merge_items");
@@ -1041,6 +1062,68 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
   return check_cuda("k_label");
 }
 
+// Overlap pipeline (pipeline = 4): the staged kernels on slabs of slices over
+// two streams -- the caller's stream runs the HBM-bound histogram of slab c+1
+// and the labels of slab c-1 while a second stream (created by this call and
+// released at its end) runs the FP64-bound tables / search / finalize of slab
+// c on half of each SM (two search CTAs per SM), so the two kinds of work
+// overlap.  Same kernels, same partition of the tuple space: bit-identical
+// to the staged pipeline.  Not used while `stream` is being captured (the
+// extra stream would outlive the capture): staged instead.
+static tsa_status segment_overlap(const tsa_problem *p, const tsa_outputs *out, const SegWs &w, cudaStream_t s) {
+  const int64_t nz = p->nz, n = p->nx * p->ny;
+  const size_t esz = p->dtype == TSA_U8 ? 1 : 2;
+  const int G0 = (int)std::min<int64_t>({nz, (int64_t)64, p->slab_slices > 0 ? (int64_t)p->slab_slices : 8});
+  const int64_t cz = (nz + G0 - 1) / G0;  // slices per slab
+  const int G = (int)((nz + cz - 1) / cz);  // slabs (no empty one)
+  uint32_t *hist = out->histogram ? out->histogram : w.hist;
+  cudaStream_t a = nullptr;
+  TSA_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  cudaEvent_t ev[2 * 64 + 1];
+  const int nev = 2 * G + 1;
+  for (int i = 0; i < nev; i++) TSA_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  cudaEvent_t e_start = ev[0], *e_h = ev + 1, *e_s = ev + 1 + G;
+  tsa_status rc = TSA_OK;
+  auto sub = [&](int c, tsa_problem *q, int64_t *z0) {
+    *q = *p;
+    *z0 = (int64_t)c * cz;
+    q->nz = std::min(cz, nz - *z0);
+    q->volume = reinterpret_cast<const char *>(p->volume) + (size_t)(*z0) * n * esz;
+  };
+  auto label = [&](int c) -> tsa_status {
+    tsa_problem q;
+    int64_t z0;
+    sub(c, &q, &z0);
+    if (cudaStreamWaitEvent(s, e_s[c], 0) != cudaSuccess) return set_error(TSA_ERR_CUDA, "overlap: wait search");
+    if (!out->labels) return TSA_OK;
+    return tsa_label(&q, out->thresholds + z0 * p->k, w.status + z0, out->labels + (size_t)z0 * n, s);
+  };
+  if (cudaEventRecord(e_start, s) != cudaSuccess || cudaStreamWaitEvent(a, e_start, 0) != cudaSuccess)
+    rc = set_error(TSA_ERR_CUDA, "overlap: fork");
+  for (int c = 0; c < G && rc == TSA_OK; c++) {
+    tsa_problem q;
+    int64_t z0;
+    sub(c, &q, &z0);
+    rc = tsa_histogram(&q, hist + z0 * p->bins, w.status + z0, s);
+    if (rc == TSA_OK && (cudaEventRecord(e_h[c], s) != cudaSuccess || cudaStreamWaitEvent(a, e_h[c], 0) != cudaSuccess))
+      rc = set_error(TSA_ERR_CUDA, "overlap: histogram event");
+    const int32_t U = units_of(&q);
+    if (rc == TSA_OK)
+      rc = search_impl(hist + z0 * p->bins, w.status + z0, q.nz, n, p->bins, p->k, p->q, p->objective,
+                       p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, a, 2);
+    if (rc == TSA_OK)
+      rc = finalize_impl(hist + z0 * p->bins, w.status + z0, q.nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk,
+                         U, out->thresholds + z0 * p->k, out->objective ? out->objective + z0 : nullptr,
+                         w.status + z0, out->slice_status ? out->slice_status + z0 : nullptr, a);
+    if (rc == TSA_OK && cudaEventRecord(e_s[c], a) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "overlap: search event");
+    if (rc == TSA_OK && c > 0) rc = label(c - 1);
+  }
+  if (rc == TSA_OK) rc = label(G - 1);  // also joins the second stream into `s`
+  for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+  cudaStreamDestroy(a);  // released once its queued work is done
+  return rc;
+}
+
 tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *workspace,
                        size_t workspace_bytes, void *stream) {
   TSA_TRY(tsa_validate(p));
@@ -1056,7 +1139,13 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   if (p->pipeline == 3) return set_error(TSA_ERR_INVALID_ARG, "stream pipeline requested but the problem is not eligible");
   if (p->pipeline >= 0 && p->pipeline <= 2 && fused_eligible(p) && labels_aligned)
     return segment_fused(p, out, w, s, p->pipeline == 1);
-  if (p->pipeline > 0) return set_error(TSA_ERR_INVALID_ARG, "fused/compact pipeline requested but the problem is not eligible");
+  if (p->pipeline == 4 || overlap_default(p)) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TSA_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusNone) return segment_overlap(p, out, w, s);
+  }
+  if (p->pipeline > 0 && p->pipeline != 4)
+    return set_error(TSA_ERR_INVALID_ARG, "fused/compact pipeline requested but the problem is not eligible");
   uint32_t *hist = out->histogram ? out->histogram : w.hist;
   const int32_t U = units_of(p);
   TSA_TRY(tsa_histogram(p, hist, w.status, stream));

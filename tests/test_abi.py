@@ -83,7 +83,9 @@ def test_pipeline_kind(lib):
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=-1))) == -1
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(enumeration=1))) == -1
     # k = 2 above 1024 bins (c5): the stream pipeline; forced stream on an eligible u8 problem
-    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024))) in (3, -1)
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024))) in (4, -1)
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024, nz=8))) == -1
+    assert lib.tsa_pipeline_kind(ctypes.byref(_p(k=3, pipeline=4))) == 4
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=3))) == 3
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(pipeline=3, k=3))) == -1
     assert lib.tsa_pipeline_kind(ctypes.byref(_p(dtype=2, bins=4096, nx=1024, ny=1024, k=1))) == -1

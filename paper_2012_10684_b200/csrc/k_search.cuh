@@ -596,28 +596,27 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
 }
 
 // hit |= any(p_i (x) x_c >= best), i < 4 prefixes, c < 4 columns (x01, x23):
-// 16 DMUL/DADD + 16 DSETP in two predicate chains (2 FP64 instructions per
-// tuple, ~85 % of the issued instructions on the FP64 pipe).
+// 16 DMUL/DADD + 16 DSETP in four predicate chains of four (2 FP64
+// instructions per tuple, ~85 % of the issued instructions on the FP64 pipe).
 template <int MODE>
 __device__ __forceinline__ unsigned cmp_p4c4(unsigned hit, const double *p, double2 x01, double2 x23,
                                              double best) {
 #define TSA_CMP_P4C4(OP)                                                                          \
-  asm("{\n\t.reg .pred a, b;\n\t.reg .f64 t<16>;\n\t"                                            \
+  asm("{\n\t.reg .pred a, b, c, d;\n\t.reg .f64 t<16>;\n\t"                                      \
       "setp.ne.u32 a, %0, 0;\n\t"                                                                 \
       OP " t0, %1, %5;\n\t" OP " t1, %1, %6;\n\t" OP " t2, %1, %7;\n\t" OP " t3, %1, %8;\n\t"    \
       OP " t4, %2, %5;\n\t" OP " t5, %2, %6;\n\t" OP " t6, %2, %7;\n\t" OP " t7, %2, %8;\n\t"    \
       OP " t8, %3, %5;\n\t" OP " t9, %3, %6;\n\t" OP " t10, %3, %7;\n\t" OP " t11, %3, %8;\n\t"  \
       OP " t12, %4, %5;\n\t" OP " t13, %4, %6;\n\t" OP " t14, %4, %7;\n\t" OP " t15, %4, %8;\n\t" \
-      "setp.ge.f64 b, t1, %9;\n\t"                                                                \
-      "setp.ge.or.f64 a, t0, %9, a;\n\tsetp.ge.or.f64 b, t3, %9, b;\n\t"                          \
-      "setp.ge.or.f64 a, t2, %9, a;\n\tsetp.ge.or.f64 b, t5, %9, b;\n\t"                          \
-      "setp.ge.or.f64 a, t4, %9, a;\n\tsetp.ge.or.f64 b, t7, %9, b;\n\t"                          \
-      "setp.ge.or.f64 a, t6, %9, a;\n\tsetp.ge.or.f64 b, t9, %9, b;\n\t"                          \
-      "setp.ge.or.f64 a, t8, %9, a;\n\tsetp.ge.or.f64 b, t11, %9, b;\n\t"                         \
-      "setp.ge.or.f64 a, t10, %9, a;\n\tsetp.ge.or.f64 b, t13, %9, b;\n\t"                        \
-      "setp.ge.or.f64 a, t12, %9, a;\n\tsetp.ge.or.f64 b, t15, %9, b;\n\t"                        \
-      "setp.ge.or.f64 a, t14, %9, a;\n\t"                                                         \
-      "or.pred a, a, b;\n\tselp.u32 %0, 1, 0, a;\n\t}"                                            \
+      "setp.ge.f64 b, t1, %9;\n\tsetp.ge.f64 c, t2, %9;\n\tsetp.ge.f64 d, t3, %9;\n\t"           \
+      "setp.ge.or.f64 a, t0, %9, a;\n\tsetp.ge.or.f64 b, t5, %9, b;\n\t"                          \
+      "setp.ge.or.f64 c, t6, %9, c;\n\tsetp.ge.or.f64 d, t7, %9, d;\n\t"                          \
+      "setp.ge.or.f64 a, t4, %9, a;\n\tsetp.ge.or.f64 b, t9, %9, b;\n\t"                          \
+      "setp.ge.or.f64 c, t10, %9, c;\n\tsetp.ge.or.f64 d, t11, %9, d;\n\t"                        \
+      "setp.ge.or.f64 a, t8, %9, a;\n\tsetp.ge.or.f64 b, t13, %9, b;\n\t"                         \
+      "setp.ge.or.f64 c, t14, %9, c;\n\tsetp.ge.or.f64 d, t15, %9, d;\n\t"                        \
+      "setp.ge.or.f64 a, t12, %9, a;\n\t"                                                         \
+      "or.pred a, a, b;\n\tor.pred c, c, d;\n\tor.pred a, a, c;\n\tselp.u32 %0, 1, 0, a;\n\t}"    \
       : "+r"(hit)                                                                                 \
       : "d"(p[0]), "d"(p[1]), "d"(p[2]), "d"(p[3]), "d"(x01.x), "d"(x01.y), "d"(x23.x), "d"(x23.y), \
         "d"(best))
@@ -776,11 +775,14 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
   const int a0 = R - 1, na = M - 3 - a0 + 1;  // a in [R-1, M-3]; items: s_cum (tri_items)
   const int lane = threadIdx.x & 31;
   bool first = true;
+  // item claims run one item ahead (the atomic's round trip overlaps the
+  // current item instead of stalling the warp before it)
+  int cn = 0;
+  if (lane == 0) cn = atomicAdd(ccur, 1);
   for (;;) {
-    int c = 0;
-    if (lane == 0) c = atomicAdd(ccur, 1);
-    c = __shfl_sync(0xffffffffu, c, 0);
+    const int c = __shfl_sync(0xffffffffu, cn, 0);
     if (c >= nitems) break;
+    if (lane == 0) cn = atomicAdd(ccur, 1);
     int lo_i = 0, hi_i = na - 1;  // the a whose items contain c
     while (lo_i < hi_i) {
       const int mid = (lo_i + hi_i + 1) >> 1;
@@ -1218,7 +1220,7 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
 // slice's K2Row table.  Every k = 2 kernel (k_search_k2: whole a-blocks; the
 // stream pipeline: 2-D tiles) runs this body, so a tuple's value is the same
 // expression tree everywhere.
-template <int MODE, int DEG>
+template <int MODE, int DEG, bool NC = true>
 __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
                                         const int lane, const Luts &l, const SpPair &tab, double &best,
                                         uint64_t &bestkey) {
@@ -1228,16 +1230,23 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   const K2Row ra = rz[ac + 1];
   const uint32_t Ca = ra.c;
   const double Wah = ra.wh, Wal = ra.wl;
-  // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1]
-  const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
+  // Apre[a] = T(0, a) = class term of positions [0, a]: n = C[a+1], w = W[a+1];
+  // lanes past the slice (a > M-3) get NaN, which never compares >= best
+  const double pre0 = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, Ca, dd_diff(Wah, Wal, 0.0, 0.0)));
+  const double pre = a <= M - 3 ? pre0 : CUDART_NAN;
   const int bend = min(M - 2, bhi);
-  int b0 = max(32 * i + 1, blo);
-  for (const K2Row *pr = rz + b0 + 1; b0 <= bend; b0 += kK2Rows, pr += kK2Rows) {
+  // one group of kK2Rows second thresholds b0 .. b0+kK2Rows-1; CHK: test
+  // a < b and b <= bend per tuple (the first 32 columns of the block, where
+  // some lanes have a >= b, and the last partial group), else none
+  auto group = [&](const int b0, const bool chk) {
+    const K2Row *pr = rz + b0 + 1;
     double vb[kK2Rows];
+    double2 yv[kK2Rows];
 #pragma unroll
     for (int r = 0; r < kK2Rows; r++) {
-      const double2 x = __ldg(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
-      const double2 y = __ldg(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
+      const double2 x = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
+      const double2 y = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
+      yv[r] = y;
       const uint32_t n = (uint32_t)__double2loint(y.y) - Ca;
       const double wm = dd_diff(x.x, x.y, Wah, Wal);
       const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), y.x);
@@ -1248,15 +1257,19 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
 #pragma unroll
     for (int r = 0; r < kK2Rows; r++) {
       const int b = b0 + r;
-      if (vb[r] >= best && a < b && b <= bend) {
-        const uint64_t key = ((uint64_t)ra.bin << 12) | (uint64_t)rz[b + 1].bin;
+      if (vb[r] >= best && (!chk || (a < b && b <= bend))) {
+        const uint64_t key = ((uint64_t)ra.bin << 12) | (uint64_t)__double2hiint(yv[r].y);
         if (better(vb[r], key, best, bestkey)) {
           best = vb[r];
           bestkey = key;
         }
       }
     }
-  }
+  };
+  int b0 = max(32 * i + 1, blo);
+  for (; b0 <= bend && b0 < 32 * i + 32; b0 += kK2Rows) group(b0, true);
+  for (; b0 + kK2Rows - 1 <= bend; b0 += kK2Rows) group(b0, false);
+  if (b0 <= bend) group(b0, true);
 }
 
 template <int MODE, int DEG>
@@ -1266,7 +1279,7 @@ __device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int
 }
 
 #ifndef TSA_K2_MINB
-#define TSA_K2_MINB 4  // minimum CTAs per SM of k_search_k2 (register cap: 64; A/B builds)
+#define TSA_K2_MINB 4  // minimum CTAs per SM of k_search_k2 (register cap: 64)
 #endif
 // k = 2 search: warp items (slice z, a-block i, b-tile t) from a global
 // counter, a-block-major (longest blocks first), so every item is at most
@@ -1293,11 +1306,12 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   const int nbl = nbmax <= u0 ? 0 : ((nbmax - u0) / U) * w + min(w, (nbmax - u0) % U);
   const uint32_t nz = (uint32_t)g.nz;
   const uint32_t items = (uint32_t)nbl * nbt * nz;
+  uint32_t itn = 0;  // claims one item ahead
+  if (lane == 0) itn = (uint32_t)atomicAdd(g.counter, 1);
   for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = (uint32_t)atomicAdd(g.counter, 1);
-    it = __shfl_sync(0xffffffffu, it, 0);
+    const uint32_t it = __shfl_sync(0xffffffffu, itn, 0);
     if (it >= items) break;
+    if (lane == 0) itn = (uint32_t)atomicAdd(g.counter, 1);
     const int tt = (int)(it / nz);
     const int z = (int)(it - (uint32_t)tt * nz);
     const int tb = tt / nbt, bt = tt - tb * nbt;

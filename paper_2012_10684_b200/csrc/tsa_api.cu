@@ -931,7 +931,7 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
     else if (mode == tsa::PROD_MIN)
       kern = l.deg == 5 ? tsa::k_search_k2<tsa::PROD_MIN, 5> : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MIN, 6>
                                                                           : tsa::k_search_k2<tsa::PROD_MIN, 12>;
-    kern<<<grid, 256, 0, s>>>(a);
+    kern<<<grid, 256, 0, s>>>(a);  // (slice-per-CTA with the rows in shared memory measured slower: 664 vs 575 us)
     TSA_TRY(check_cuda("k_search_k2"));
     const int64_t nt = nz * (int64_t)a.nunits;
     tsa::k_merge_items<<<(unsigned)((nt + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, w.M, slice_status, w.mmax,
@@ -1735,8 +1735,11 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   // while the kernels run on slab i and the D2H engine drains slab i-1.
   // Thresholds, objective and status stay on the device for the whole volume
   // and are copied once at the end.
-  cudaStream_t comp = S(stream0), cout = S(stream1), cin = nullptr;
-  TSA_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  cudaStream_t comp = S(stream0), cout = S(stream1), cin = comp;
+  // one slab: nothing to overlap the copy-in with (and no stream to create:
+  // c1's single 256^2 slice is latency-bound)
+  const bool own_in = p->nz > slab;
+  if (own_in) TSA_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
   cudaEvent_t ev_done[2], ev_free[2], ev_in[2], ev_start;
   for (int b = 0; b < 2; b++) {
     TSA_CUDA(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
@@ -1793,14 +1796,14 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
     if (e != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "D2H results");
   }
   const cudaError_t e0 = cudaStreamSynchronize(comp), e1 = cudaStreamSynchronize(cout),
-                    e2 = cudaStreamSynchronize(cin);
+                    e2 = own_in ? cudaStreamSynchronize(cin) : cudaSuccess;
   for (int b = 0; b < 2; b++) {
     cudaEventDestroy(ev_done[b]);
     cudaEventDestroy(ev_free[b]);
     cudaEventDestroy(ev_in[b]);
   }
   cudaEventDestroy(ev_start);
-  cudaStreamDestroy(cin);
+  if (own_in) cudaStreamDestroy(cin);
   if (rc != TSA_OK) return rc;
   if (e0 != cudaSuccess || e1 != cudaSuccess || e2 != cudaSuccess)
     return set_error(TSA_ERR_CUDA, "tsa_segment_host synchronize");

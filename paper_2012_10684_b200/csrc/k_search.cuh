@@ -300,14 +300,26 @@ __device__ __forceinline__ unsigned cmp8x2(unsigned hit, double p0, double p1, d
 // the rank range).
 template <int R>
 __device__ __forceinline__ void next_colex(int *idx) {
-#pragma unroll
-  for (int j = 0; j < R; j++) {
-    if (j == R - 1 || idx[j] + 1 < idx[j + 1]) {
-      idx[j]++;
-#pragma unroll
-      for (int i = 0; i < R; i++)
-        if (i < j) idx[i] = i;
-      return;
+  // explicit per R (a loop with an early return kept idx[] in local memory)
+  if (R == 1) {
+    idx[0]++;
+  } else if (R == 2) {
+    if (idx[0] + 1 < idx[1]) {
+      idx[0]++;
+    } else {
+      idx[1]++;
+      idx[0] = 0;
+    }
+  } else {
+    if (idx[0] + 1 < idx[1]) {
+      idx[0]++;
+    } else if (idx[1] + 1 < idx[2]) {
+      idx[1]++;
+      idx[0] = 0;
+    } else {
+      idx[2]++;
+      idx[0] = 0;
+      idx[1] = 1;
     }
   }
 }
@@ -869,8 +881,11 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
           else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
         }
         if (hit) {  // exact rescan of this tile's rows, lower-lex prefix first
-#pragma unroll 1
-          for (int i = 0; i < nv; i++) {
+          // unrolled over the constant P with a guard: a dynamic index into
+          // pre / tid0 / tid1 put them in local memory (ncu: STL/LDL per tile)
+#pragma unroll
+          for (int i = 0; i < P; i++) {
+            if (i >= nv) break;
             uint64_t kp = (uint64_t)bin[tid0[i] + 1];
             if (K == 4) kp = (kp << 12) | (uint64_t)bin[tid1[i] + 1];
             kp = (kp << 12) | (uint64_t)bin[a + 1];
@@ -1254,6 +1269,13 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
       if (MODE == PROD_MIN) v = -v;
       vb[r] = v;
     }
+    // one predicate for the group (the exact update is rare once best is
+    // good): no per-tuple branch / reconvergence (ncu: ~5 instructions per
+    // tuple)
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < kK2Rows; r++) any |= vb[r] >= best;
+    if (!any) return;
 #pragma unroll
     for (int r = 0; r < kK2Rows; r++) {
       const int b = b0 + r;

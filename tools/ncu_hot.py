@@ -31,3 +31,27 @@ body.sort(key=lambda r: -num(r[col[samp]]) if len(r) > col[samp] else 0)
 for r in body[:60]:
     print(f"{num(r[col[samp]]):8.0f} {100 * num(r[col[samp]]) / max(tot, 1):5.1f}%  "
           f"exe={num(r[col[exe]]) if exe else 0:12.0f}  {r[col['Source']][:90]}")
+
+# instruction mix weighted by executed (warp-level) instructions
+if exe:
+    from collections import Counter
+
+    mix = Counter()
+    tot_exe = 0.0
+    for r in body:
+        if len(r) <= col[exe]:
+            continue
+        n = num(r[col[exe]])
+        op = r[col["Source"]].split()
+        if not op:
+            continue
+        o = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
+        mix[o.split(".")[0]] += n
+        tot_exe += n
+    print("\nexecuted warp instructions:", tot_exe)
+    for o, n in mix.most_common(30):
+        print(f"  {o:12s} {n:14.0f} {100 * n / max(tot_exe, 1):5.1f}%")
+    print("\ntop lines by executed count:")
+    body.sort(key=lambda r: -num(r[col[exe]]) if len(r) > col[exe] else 0)
+    for r in body[:50]:
+        print(f"exe={num(r[col[exe]]):12.0f}  {r[col['Source']][:100]}")

@@ -755,18 +755,29 @@ template <int K>
 __device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const uint64_t r1, int *s_cum) {
   constexpr int R = K - 1, G = 32 * (K == 4 ? 16 : 1);  // = tri_search's 32 P Q
   const int a0 = R - 1;
-  if (threadIdx.x == 0) {
-    int cum = 0;
-    s_cum[0] = 0;
-    for (int a = a0; a <= M - 3; a++) {
-      const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
-      if (K == 3)  // column blocks of kTri3Cols second-last... last thresholds b in (a, M-2]
-        cum += hi > lo ? (M - 2 - a + kTri3Cols - 1) / kTri3Cols : 0;
-      else
-        cum += hi > lo ? (int)((hi - lo + G - 1) / G) : 0;
-      s_cum[a - a0 + 1] = cum;
+  if (threadIdx.x < 32) {  // warp 0: per-a item counts and their prefix sums
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int as = a0; as <= M - 3; as += 32) {
+      const int a = as + lane;
+      int cnt = 0;
+      if (a <= M - 3) {
+        const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
+        if (hi > lo) cnt = K == 3 ? (M - 2 - a + kTri3Cols - 1) / kTri3Cols : (int)((hi - lo + G - 1) / G);
+      }
+      int x = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (a <= M - 3) s_cum[a - a0 + 1] = base + x;
+      base += __shfl_sync(0xffffffffu, x, 31);
     }
-    s_cum[kTriCum - 1] = cum;
+    if (lane == 0) {
+      s_cum[0] = 0;
+      s_cum[kTriCum - 1] = base;
+    }
   }
   __syncthreads();
   return s_cum[kTriCum - 1];
@@ -967,6 +978,12 @@ __global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_do
   __shared__ int s_item;
   __shared__ int32_t s_bin[kTriMaxRows + 2];
   __shared__ int s_cum[kTriCum];
+  __shared__ __align__(8) uint64_t s_bar;  // the tables' bulk copy (TMA)
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   const int64_t items = g.nz * (int64_t)g.ss;
   for (;;) {
     __syncthreads();
@@ -996,10 +1013,17 @@ __global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_do
           for (int e = threadIdx.x; e <= M; e += blockDim.x) s_bin[e] = gB[e];
         const int64_t nd = tri_region_doubles(M);
         if (M <= kTriMaxRows && nd <= smem_doubles) {
-          // the slice's tables into shared memory (16-byte loads through L2)
-          const double2 *src = reinterpret_cast<const double2 *>(region);
-          double2 *dst = reinterpret_cast<double2 *>(tsm);
-          for (int64_t e = threadIdx.x; e < (nd + 1) / 2; e += blockDim.x) dst[e] = __ldcg(src + e);
+          // the slice's tables into shared memory: one TMA bulk copy (the
+          // previous entry's generic reads are ordered before it by the
+          // barrier at the top of the loop and the proxy fence)
+          if (threadIdx.x == 0) {
+            const uint32_t bytes = (uint32_t)(((nd + 1) / 2) * 16);
+            fence_proxy_async_smem();
+            mbar_expect_tx(&s_bar, bytes);
+            bulk_g2s(tsm, region, bytes, &s_bar);
+          }
+          mbar_wait(&s_bar, phase);
+          phase ^= 1u;
           __syncthreads();
           best = tsm[tri_roff_doubles(M) - 1];  // the slice's seed (k_tri_tables)
           tri_search<K, MODE>(g, M, r0, r1, tsm, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);

@@ -967,6 +967,8 @@ def run_1d(args, cfg, rank, world, dev):
                        "note": "k_small_luts + k_scan [+ k_rtable] + search kernel [+ k_merge_items]"},
             "finalize": {"ms": stt["finalize"], "calls_per_step": len(qs)},
             "label": {"ms": stt["label"], "calls_per_step": len(qs), "bytes": lab_b * len(qs),
+                      "note": ("the staged per-q label kernel; the sweep step labels all q in one pass "
+                               "(k_label_sweep: the volume read once)") if sweep else None,
                       "gbs": lab_b * len(qs) / (stt["label"] * 1e-3) / 1e9,
                       "frac_hbm": lab_b * len(qs) / (stt["label"] * 1e-3) / 1e9 / hbm},
             "per_q": stt["per_q"] if sweep else None,
@@ -1094,7 +1096,10 @@ def run_1d(args, cfg, rank, world, dev):
     tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
     per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0)
     slabs = min(cfg.nz, 8)
-    launches_per_step = {1: 1, 2: 4, 3: 2, 4: slabs * (1 + per_q)}.get(kind, 1 + per_q * len(qs))
+    if sweep:  # one histogram, per q the search chain, one k_label_sweep per 16 q
+        launches_per_step = 1 + (per_q - 1) * len(qs) + -(-len(qs) // 16)
+    else:
+        launches_per_step = {1: 1, 2: 4, 3: 2, 4: slabs * (1 + per_q)}.get(kind, 1 + per_q)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -1177,8 +1182,12 @@ def run_tuple_sharded(args, cfg, rank, world, dev):
     clocks = sampler.summary(t_wall0, t_wall1)
     hist = out["histogram"].cpu().numpy()
     m = (hist > 0).sum(axis=1)
-    evaluated = int(sum(comb(int(x) - 1, cfg.k) for x in m if x >= cfg.k + 1)) \
-        if args.enumeration == "canonical" else cfg.nz * comb(cfg.bins - 1, cfg.k)
+    if args.enumeration == "dp":  # class terms of the interval DP, not tuples
+        evaluated = int(sum(int(x) * (int(x) + 1) // 2 for x in m))
+    elif args.enumeration == "canonical":
+        evaluated = int(sum(comb(int(x) - 1, cfg.k) for x in m if x >= cfg.k + 1))
+    else:
+        evaluated = cfg.nz * comb(cfg.bins - 1, cfg.k)
     if rank == 0:
         line = {
             "metric": METRIC, "value": cfg.nz / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,

@@ -130,4 +130,72 @@ __global__ void __launch_bounds__(256) k_label_generic(LabelArgs g) {
   }
 }
 
+// q sweep (tsa_segment_sweep): the labels of every q from ONE read of the
+// volume (round 2; the sweep labelled the same volume 11 times).  A failed
+// slice of a q has thresholds -1 and gets labels 0 for that q.  Grid (chunk,
+// slice); the packed thresholds of the slice for every q are staged in shared
+// memory.  n % 16 == 0, 16-byte aligned volume and labels.
+constexpr int kSweepMaxQ = 16;  // q values per launch
+struct LabelSweepArgs {
+  const uint8_t *vol;
+  int64_t n;  // voxels per slice
+  int k, nq;
+  const int32_t *thr[kSweepMaxQ];  // [nz][k] per q
+  uint8_t *lab[kSweepMaxQ];        // [nz][n] per q
+};
+
+template <typename T, int KT>
+__global__ void __launch_bounds__(256) k_label_sweep(LabelSweepArgs g) {
+  __shared__ uint32_t s_b[kSweepMaxQ][4];  // u8: thresholds replicated in 4 bytes; u16: the value
+  __shared__ int s_ok[kSweepMaxQ];
+  const int64_t z = blockIdx.y;
+  if (threadIdx.x < g.nq) {
+    const int32_t *tz = g.thr[threadIdx.x] + z * g.k;
+    const int t0 = tz[0];
+    s_ok[threadIdx.x] = t0 >= 0;
+    const int tmax = sizeof(T) == 1 ? 255 : 65535;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int t = j < KT ? tz[j] : tmax;
+      s_b[threadIdx.x][j] = sizeof(T) == 1 ? (uint32_t)(t & 0xff) * 0x01010101u : (uint32_t)t;
+    }
+  }
+  __syncthreads();
+  const int64_t groups = g.n / 16;
+  const int64_t per = (groups + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = z * groups + per * blockIdx.x, i1 = z * groups + min(groups, per * (blockIdx.x + 1));
+  const uint4 *src = reinterpret_cast<const uint4 *>(g.vol);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    if (sizeof(T) == 1) {
+      const uint4 w = __ldcs(src + i);
+      for (int qi = 0; qi < g.nq; qi++) {
+        uint4 o = make_uint4(0u, 0u, 0u, 0u);
+        if (s_ok[qi]) {
+          const uint32_t b0 = s_b[qi][0], b1 = s_b[qi][1], b2 = s_b[qi][2], b3 = s_b[qi][3];
+          o.x = swar_labelk<KT>(w.x, b0, b1, b2, b3);
+          o.y = swar_labelk<KT>(w.y, b0, b1, b2, b3);
+          o.z = swar_labelk<KT>(w.z, b0, b1, b2, b3);
+          o.w = swar_labelk<KT>(w.w, b0, b1, b2, b3);
+        }
+        __stcs(reinterpret_cast<uint4 *>(g.lab[qi]) + i, o);
+      }
+    } else {
+      const uint4 wa = __ldcs(src + 2 * i), wb = __ldcs(src + 2 * i + 1);
+      const uint32_t ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+      for (int qi = 0; qi < g.nq; qi++) {
+        uint32_t o[4] = {0u, 0u, 0u, 0u};
+        if (s_ok[qi]) {
+          const int t0 = (int)s_b[qi][0], t1 = (int)s_b[qi][1], t2 = (int)s_b[qi][2], t3 = (int)s_b[qi][3];
+#pragma unroll
+          for (int e = 0; e < 16; e++) {
+            const int v = (int)((ws[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+            o[e >> 2] |= label_ofk<KT>(v, t0, t1, t2, t3) << (8 * (e & 3));
+          }
+        }
+        __stcs(reinterpret_cast<uint4 *>(g.lab[qi]) + i, make_uint4(o[0], o[1], o[2], o[3]));
+      }
+    }
+  }
+}
+
 }  // namespace tsa

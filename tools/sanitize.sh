@@ -2,7 +2,7 @@
 # compute-sanitizer (memcheck, racecheck, synccheck) over every pipeline on a
 # small c2 slab and a small k=4 / u16 problem.  Run under gpurun.
 set -u
-OUT=gpurun_out/sanitizer
+OUT=${1:-gpurun_out/sanitizer}
 mkdir -p $OUT
 cat > /tmp/san_case.py <<'PY'
 import sys, os
@@ -30,6 +30,21 @@ tsa.tsa_hu_preprocess(h)
 tsa.tsa_morph(v[:2].contiguous(), "tophat", 10)
 tsa.tsa_morph(v[:2, :37, :300].contiguous(), "open", 3)
 tsa.tsa_segment(v, 256, 4, 0.8, enumeration="dp")
+# round 2: k >= 3 shared-memory search (TMA staging, large-M global fallback),
+# the q sweep with its single label pass, the stream and overlap pipelines,
+# the tuple-sharded C-ABI call over NCCL (one rank)
+tsa.tsa_segment(v, 256, 3, 0.8)
+tsa.tsa_segment(v, 256, 4, 1.3)
+r = torch.from_numpy(np.random.default_rng(2).integers(0, 256, size=(2, 64, 64)).astype(np.uint8)).cuda()
+tsa.tsa_segment(r, 256, 3, 0.8)
+tsa.tsa_segment_sweep(v, 256, 3, (0.5, 1.0, 1.5))
+v5 = torch.from_numpy(phantom.make_volume(phantom.CONFIGS["c5"], nz=3, z_first=400)).cuda()
+tsa.tsa_segment(v5, 4096, 2, 0.8)
+tsa.tsa_segment(v5, 4096, 2, 0.8, pipeline="stream")
+tsa.tsa_segment(v5, 4096, 2, 0.8, pipeline="overlap", slab_slices=2)
+comm = tsa.TsaComm.nccl(1, 0, tsa.tsa_comm_unique_id())
+tsa.tsa_segment_sharded(v, v.shape[0], 256, 4, 0.8, comm, mode="tuples")
+comm.close()
 torch.cuda.synchronize()
 print("ok")
 PY

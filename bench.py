@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="tsa", choices=["tsa", "reference"])
     ap.add_argument("--enumeration", default="canonical", choices=["canonical", "full", "dp"])
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-slab", type=int, default=0, help="slices per host<->device slab (0 = default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--buffers", type=int, default=0, help="resident volume copies rotated (0 = auto, > 2x L2)")
     ap.add_argument("--shard", default="auto", choices=["auto", "slabs", "replicas", "tuples"],
@@ -1059,7 +1060,7 @@ def run_1d(args, cfg, rank, world, dev):
                     "objective": torch.empty(nzl, dtype=torch.float64).pin_memory(),
                     "status": torch.empty(nzl, dtype=torch.int32).pin_memory(),
                     "labels": torch.empty(host.shape, dtype=torch.uint8).pin_memory()}
-            slab = min(nzl, 50 if bins <= 256 else 25)  # slices per host<->device slab (tools/exp_e2e.py)
+            slab = min(nzl, args.e2e_slab or (50 if bins <= 256 else 25))  # slices per host<->device slab
             hp = tsa.make_problem(host_t, bins, k, qs[0], enumeration=args.enumeration)
             scratch = torch.empty(int(tsa.load().tsa_segment_host_scratch_size(ctypes.byref(hp), slab)),
                                   dtype=torch.uint8, device=dev)

@@ -548,7 +548,11 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + 
 constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
 constexpr int kTriCum = 512 + 2;                 // item prefix sums, one per t_{k-1} (M <= bins <= 512)
 constexpr int kTri3Cols = 96;                    // k = 3: last thresholds per item (3 per lane)
-constexpr size_t kTriSmemBytes = 104 * 1024;     // dynamic tables: two CTAs per SM
+#ifndef TSA_TRI_MINB
+#define TSA_TRI_MINB 2  // CTAs per SM of k_search_tri (register cap; A/B builds)
+#endif
+// dynamic tables: 104 KB at two CTAs per SM, 72 KB (M <= 93) at three
+constexpr size_t kTriSmemBytes = TSA_TRI_MINB >= 3 ? 72 * 1024 : 104 * 1024;
 
 // doubles needed for the tables of a slice with M positions (rows packed)
 // R row a of k_search_tri: columns from sa = (a+1) & ~1 in whole 4-column
@@ -724,6 +728,9 @@ __device__ __forceinline__ double tri_seed(const int M, const double *base) {
         const int lo = j == 0 ? 0 : t[j - 1] + 1, hi = j == K - 1 ? M - 2 : t[j + 1] - 1;
         double bv = -CUDART_INF;
         int bx = t[j];
+        // independent candidates: unrolled so their table loads overlap (the
+        // ascent is the critical path of k_tri_tables)
+#pragma unroll 4
         for (int x = lo + lane; x <= hi; x += 32) {
           int u[K];
 #pragma unroll
@@ -971,7 +978,7 @@ __global__ void __launch_bounds__(256) k_tri_tables(SearchArgs g) {
 // counter, so a slice's work spreads over up to ss CTAs and no CTA waits on a
 // long last item.  Entry results go to slot [j][z]; k_fold_slots merges.
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, 2) k_search_tri(SearchArgs g, int smem_doubles) {
+__global__ void __launch_bounds__(256, TSA_TRI_MINB) k_search_tri(SearchArgs g, int smem_doubles) {
   static_assert(K >= 3 && K <= 4, "k = 3, 4");
   constexpr int R = K - 1;
   extern __shared__ __align__(16) double tsm[];

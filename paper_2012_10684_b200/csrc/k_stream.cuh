@@ -190,6 +190,7 @@ __device__ void work_slice(const StreamArgs &g, const int64_t z, double *smem) {
   const int lane = threadIdx.x & 31;
   bool jr_ok = false;  // the class-size table is staged in smem (CTA-uniform)
   for (;;) {
+    __syncthreads();  // every thread has read the previous s_job / s_M / s_st (racecheck)
     // 0 = finished, 1 = scan claimed, 2 = search, 3 = wait
     if (threadIdx.x == 0) {
       int job = 3;

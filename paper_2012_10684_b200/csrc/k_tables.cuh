@@ -57,14 +57,18 @@ __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q,
   // exactly kTableThreads threads do the work whatever the block size (>= it),
   // so every kernel produces bit-identical tables
   const int tid = threadIdx.x, T = kTableThreads;
-  for (int i = tid; i < L; i += blockDim.x) {
-    const uint32_t c = h[i];
-    const double x = (double)c;
-    wsh[i] = c == 0 ? 0.0 : (shannon ? __dmul_rn(x, log(x)) : pow(x, q));
-  }
-  __syncthreads();
   const int per = (L + T - 1) / T;
   const int i0 = tid < T ? min(L, tid * per) : L, i1 = tid < T ? min(L, i0 + per) : L;
+  // (a compacted variant -- listing the non-empty bins first so the pow calls
+  // spread evenly -- measured slower on c5: 84 vs 63 us)
+  {
+    for (int i = tid; i < L; i += blockDim.x) {
+      const uint32_t c = h[i];
+      const double x = (double)c;
+      wsh[i] = c == 0 ? 0.0 : (shannon ? __dmul_rn(x, log(x)) : pow(x, q));
+    }
+  }
+  __syncthreads();
   uint32_t m_l = 0, n_l = 0;
   dd w_l = {0.0, 0.0};
   for (int i = i0; i < i1; i++) {

@@ -187,11 +187,23 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   }
   for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn((double)ldh(lst[j]), N);
   __syncthreads();
-  if (tid <= k) {
-    double P = 0.0;
-    for (int j = s_start[tid]; j < s_start[tid + 1]; j++) P = __dadd_rn(P, fsh[j]);
-    Psh[tid] = P;
-  }
+  // sequential sums in ascending order; the shared loads of 8 terms are
+  // issued ahead of their 8 dependent adds (round 2: one load latency per
+  // term made the k = 2 c5 finalize 51 us) -- the same additions in the same order
+  auto seqsum = [&](const int j0, const int j1, const bool neg) -> double {
+    double acc = 0.0;
+    int j = j0;
+    for (; j + 8 <= j1; j += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) x[u] = fsh[j + u];
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc = neg ? __dsub_rn(acc, x[u]) : __dadd_rn(acc, x[u]);
+    }
+    for (; j < j1; j++) acc = neg ? __dsub_rn(acc, fsh[j]) : __dadd_rn(acc, fsh[j]);
+    return acc;
+  };
+  if (tid <= k) Psh[tid] = seqsum(s_start[tid], s_start[tid + 1], false);
   __syncthreads();
   const double q = g.q;
   const bool shannon = q == 1.0;
@@ -202,9 +214,7 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   }
   __syncthreads();
   if (tid <= k) {
-    double A = 0.0;
-    for (int j = s_start[tid]; j < s_start[tid + 1]; j++)
-      A = shannon ? __dsub_rn(A, fsh[j]) : __dadd_rn(A, fsh[j]);
+    const double A = seqsum(s_start[tid], s_start[tid + 1], shannon);
     Ssh[tid] = shannon ? A : __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(q, 1.0));
   }
   __syncthreads();

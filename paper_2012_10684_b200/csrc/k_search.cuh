@@ -46,6 +46,7 @@ struct SearchArgs {
   int nunits;                        // units in this launch (unit_end - unit_begin)
   int ss;                            // k_search_tri: CTA entries per slice
   int32_t *ccur;                     // k_search_tri: [nz] per-slice chunk counters, zeroed
+  double *seed;                      // [nz] seed scores of the pruned k = 2 search (k_k2_seed)
 };
 
 // STAGE: copy the slice's C/W/Asuf tables to shared memory first (L <= 1024).
@@ -558,10 +559,17 @@ constexpr size_t kTriSmemBytes = TSA_TRI_MINB >= 3 ? 72 * 1024 : 104 * 1024;
 // R row a of k_search_tri: columns from sa = (a+1) & ~1 in whole 4-column
 // steps up to M-2 (NaN outside (a, M-2])
 __host__ __device__ __forceinline__ int tri_row_len(int M, int a) { return 4 * ((M + 2 - ((a + 1) & ~1)) >> 2); }
+// Chunk bounds (round 2, exact pruning of the k >= 3 search): RB[a][c] bounds
+// the 16 packed columns [16c, 16c+16) of R row a (max; min in PROD_MIN, where
+// prefixes are <= 0), PB[a][c] the sign-adjusted k = 3 prefix values
+// combine(T(0, t1), T(t1+1, a)) for t1 in [8c, 8c+8) (max).  NaN entries are
+// skipped (fmax / fmin); a chunk with no entry is NaN, which never passes a test.
+__host__ __device__ __forceinline__ int tri_rbs(int M) { return (tri_row_len(M, 0) + 15) >> 4; }
+__host__ __device__ __forceinline__ int tri_pbs(int M) { return (M + 7) >> 3; }
 __host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
   int64_t r = 0;
   for (int a = 0; a <= M - 3; a++) r += tri_row_len(M, a);
-  return r + (int64_t)(M - 1) * M / 2;
+  return r + (int64_t)(M - 1) * M / 2 + (int64_t)(M - 2) * (tri_rbs(M) + tri_pbs(M));
 }
 
 // Per-slice table region of k_search_tri (doubles): row offsets (M-1 ints,
@@ -608,6 +616,28 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     }
     const int a = lo, b = ((a + 1) & ~1) + (e - roff[a]);
     Rt[e] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+  }
+  __syncthreads();
+  double *RB = Tt + ntri;
+  const int rbs = tri_rbs(M), pbs = tri_pbs(M);
+  double *PB = RB + (M - 2) * rbs;
+  for (int e = threadIdx.x; e < (M - 2) * rbs; e += blockDim.x) {
+    const int a = e / rbs, c = e - a * rbs;
+    const double *row = Rt + roff[a];
+    const int u1 = min(tri_row_len(M, a), 16 * c + 16);
+    double v = CUDART_NAN;
+    for (int u = 16 * c; u < u1; u++) v = MODE == PROD_MIN ? fmin(v, row[u]) : fmax(v, row[u]);
+    RB[e] = v;
+  }
+  for (int e = threadIdx.x; e < (M - 2) * pbs; e += blockDim.x) {
+    const int a = e / pbs, c = e - a * pbs;
+    double v = CUDART_NAN;
+    for (int t1 = 8 * c; t1 < min(a, 8 * c + 8); t1++) {
+      double pre = combine<MODE>(Tt[tri_idx(0, t1)], Tt[tri_idx(t1 + 1, a)]);
+      if (MODE == PROD_MIN) pre = -pre;
+      v = fmax(v, pre);
+    }
+    PB[e] = v;
   }
 }
 
@@ -836,10 +866,21 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
       }
       const int t1lo = (int)(lo - binom((uint64_t)a, 2)), t1hi = (int)(hi - binom((uint64_t)a, 2));
       unsigned hit = 0;
-      for (int t1 = t1lo; t1 < t1hi; t1++) {
-        double pre = combine<MODE>(Tt[tri_idx(0, t1)], Tt[tri_idx(t1 + 1, a)]);
-        if (MODE == PROD_MIN) pre = -pre;
-        hit = cmp_p1c3<MODE>(hit, pre, rv, best);
+      // chunks of 8 t_1: skipped by the whole warp when no lane's bound
+      // combine(PB[a][chunk], bound of its 3 columns) reaches its best
+      // (value = combine(pre, R) is monotone in both and rounding is
+      // monotone, so a skipped tuple scores <= the bound < best: exact)
+      const double rbl = MODE == PROD_MIN ? fmin(fmin(rv[0], rv[1]), rv[2]) : fmax(fmax(rv[0], rv[1]), rv[2]);
+      const double *pbr = Tt + (M - 1) * M / 2 + (M - 2) * tri_rbs(M) + a * tri_pbs(M);
+      for (int t1c = t1lo; t1c < t1hi;) {
+        const int cend = min(t1hi, (t1c & ~7) + 8);
+        if (__any_sync(0xffffffffu, combine<MODE>(pbr[t1c >> 3], rbl) >= best))
+          for (int t1 = t1c; t1 < cend; t1++) {
+            double pre = combine<MODE>(Tt[tri_idx(0, t1)], Tt[tri_idx(t1 + 1, a)]);
+            if (MODE == PROD_MIN) pre = -pre;
+            hit = cmp_p1c3<MODE>(hit, pre, rv, best);
+          }
+        t1c = cend;
       }
       if (hit) {  // exact rescan of this lane's tuples in lex order (t_1, then b)
         for (int t1 = t1lo; t1 < t1hi; t1++) {
@@ -867,15 +908,18 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
       continue;
     }
     uint64_t rb = lo + (uint64_t)(c - s_cum[lo_i]) * G + (uint64_t)lane * (P * Q);
-    if (rb < hi) {
+    {  // the whole warp runs the tiles (lanes past hi hold NaN prefixes), so
+       // the chunk votes below are converged
       const int sa = (a + 1) & ~1;
       const double *row = Rt + roff[a] - sa;  // row[b], b in [sa, sa + tri_row_len)
       const double2 *rp = reinterpret_cast<const double2 *>(Rt + roff[a]);
       const int nsteps = tri_row_len(M, a) >> 2;  // 4-column steps
+      const double *rbr = Tt + (M - 1) * M / 2 + a * tri_rbs(M);  // chunk bounds of row a
       int idx[R];
       unrank_colex<R>(rb, idx);
 #pragma unroll 1
-      for (int q = 0; q < Q && rb < hi; q++) {
+      for (int q = 0; q < Q; q++) {
+        if (!__any_sync(0xffffffffu, rb < hi)) break;
         // this tile's prefixes rb .. rb+P-1 (< hi), all ending at a
         double pre[P];
         int tid0[P], tid1[P];
@@ -893,10 +937,20 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
           pre[i] = v ? pv : CUDART_NAN;    // NaN never compares >= best
         }
         unsigned hit = 0;
-        for (int s = 0; s < nsteps; s++) {
-          const double2 x01 = rp[2 * s], x23 = rp[2 * s + 1];
-          if (P == 4) hit = cmp_p4c4<MODE>(hit, pre, x01, x23, best);
-          else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
+        // 16-column chunks of the row, skipped by the (active) warp when no
+        // lane's bound combine(max of its P prefixes, RB[a][chunk]) reaches
+        // its best: exact, as for k = 3 (NaN prefixes are ignored by fmax)
+        double pm = pre[0];
+#pragma unroll
+        for (int i = 1; i < P; i++) pm = fmax(pm, pre[i]);
+        for (int c0 = 0; c0 < nsteps; c0 += 4) {
+          if (!__any_sync(0xffffffffu, combine<MODE>(pm, rbr[c0 >> 2]) >= best)) continue;
+          const int s1 = min(nsteps, c0 + 4);
+          for (int s = c0; s < s1; s++) {
+            const double2 x01 = rp[2 * s], x23 = rp[2 * s + 1];
+            if (P == 4) hit = cmp_p4c4<MODE>(hit, pre, x01, x23, best);
+            else hit = cmp_p1c4<MODE>(hit, pre[0], x01, x23, best);
+          }
         }
         if (hit) {  // exact rescan of this tile's rows, lower-lex prefix first
           // unrolled over the constant P with a guard: a dynamic index into
@@ -1245,8 +1299,8 @@ constexpr int kK2Rows = 4;  // rows in flight per lane (tables are padded by >= 
 // The class term of the k = 2 kernel: class_term_nw<MODE> with the polynomial
 // degree fixed at compile time and the 2^-s scaling on the exponent field --
 // bit-identical values (same operations, same order).
-template <int MODE, int DEG>
-__device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint32_t n, double w) {
+template <int MODE, int DEG, class Tab>
+__device__ __forceinline__ double k2_term(const Luts &l, const Tab &tab, uint32_t n, double w) {
   uint32_t j, r;
   int s;
   nsplit_idx(n, j, s, r);
@@ -1266,10 +1320,26 @@ __device__ __forceinline__ double k2_term(const Luts &l, const SpPair &tab, uint
 // slice's K2Row table.  Every k = 2 kernel (k_search_k2: whole a-blocks; the
 // stream pipeline: 2-D tiles) runs this body, so a tuple's value is the same
 // expression tree everywhere.
-template <int MODE, int DEG, bool NC = true>
+//
+// PRUNE (PROD_MAX only, i.e. pseudo-additive with q < 1; `best` enters as
+// the slice's seed score): before a bulk group of kK2Rows rows b0..b0+3 is
+// evaluated, each lane bounds its four values from above by
+//   Apre[a] * (W[b0+3] - W[a]) * ub(n(a, b0)^-q) * max_r Asuf[b0+r]
+// -- W is non-decreasing in b, n(a, b) = C[b+1] - C[a+1] is increasing, so
+// n^-q is decreasing (q > 0), and ub(n^-q) = j^-q 2^(-s q) >= n^-q drops the
+// (1 + d)^-q <= 1 factor of k2_term (a 0.1 % looser bound for one DMUL
+// instead of a degree-5..12 polynomial) -- and the warp skips the group when
+// no lane's bound, widened by 2^-20 relative (far above the few-ulp rounding
+// of either side), reaches the lane's best.  A skipped tuple therefore scores
+// strictly below a score some evaluated tuple (or the seed tuple) reaches, so
+// it is neither the argmax nor tied with it: the result is the exhaustive
+// search's, bit for bit.  The first 32 columns (lanes with a >= b) and the
+// last partial group are always evaluated.
+template <int MODE, int DEG, bool NC = true, bool PRUNE = false>
 __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
                                         const int lane, const Luts &l, const SpPair &tab, double &best,
                                         uint64_t &bestkey) {
+  static_assert(!PRUNE || MODE == PROD_MAX, "k = 2 pruning bounds the product form with q < 1");
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int a = 32 * i + lane;
   const int ac = min(a, M - 3);  // lanes past the slice stay idle (masked below)
@@ -1284,15 +1354,30 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   // one group of kK2Rows second thresholds b0 .. b0+kK2Rows-1; CHK: test
   // a < b and b <= bend per tuple (the first 32 columns of the block, where
   // some lanes have a >= b, and the last partial group), else none
+  const double preub = PRUNE ? __dmul_rn(pre, 1.0 + 0x1p-20) : 0.0;
   auto group = [&](const int b0, const bool chk) {
     const K2Row *pr = rz + b0 + 1;
     double vb[kK2Rows];
-    double2 yv[kK2Rows];
+    double2 yv[kK2Rows], xv[kK2Rows];
 #pragma unroll
     for (int r = 0; r < kK2Rows; r++) {
-      const double2 x = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
-      const double2 y = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
-      yv[r] = y;
+      xv[r] = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
+      yv[r] = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
+    }
+    if (PRUNE && !chk) {
+      uint32_t j, rr;
+      int s;
+      nsplit_idx((uint32_t)__double2loint(yv[0].y) - Ca, j, s, rr);
+      const double ipub = __dmul_rn(tab.jr(j).x, l.p2[s]);
+      const double wmax = dd_diff(xv[kK2Rows - 1].x, xv[kK2Rows - 1].y, Wah, Wal);
+      const double amax = fmax(fmax(yv[0].x, yv[1].x), fmax(yv[2].x, yv[3].x));
+      const double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(wmax, amax));
+      // NaN (lanes past the slice) never asks for the group
+      if (!__any_sync(0xffffffffu, bound >= best)) return;
+    }
+#pragma unroll
+    for (int r = 0; r < kK2Rows; r++) {
+      const double2 x = xv[r], y = yv[r];
       const uint32_t n = (uint32_t)__double2loint(y.y) - Ca;
       const double wm = dd_diff(x.x, x.y, Wah, Wal);
       const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, n, wm), y.x);
@@ -1343,7 +1428,7 @@ __device__ __forceinline__ void k2_block(const K2Row *rz, const int M, const int
 constexpr int kK2Tile = 4096;  // one tile per a-block: 128-wide tiles measured 7 % slower on c5 (606 vs 564 us)
 __host__ __device__ __forceinline__ int k2_tiles(int m) { return m >= 3 ? (m - 2) / kK2Tile + 1 : 1; }
 
-template <int MODE, int DEG>
+template <int MODE, int DEG, bool PRUNE = false>
 __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
   for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
@@ -1371,10 +1456,12 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
     const int i = (tb / w) * U + u0 + tb % w;
     const int M = g.Mz[z];
     const int blo = bt * kK2Tile, bhi = blo + kK2Tile - 1;
+    // PRUNE: the seed enters with key none, so tuples scoring == seed are still taken
     double best = -CUDART_INF;
     uint64_t bestkey = kKeyNone;
     if (g.status[z] == kOK && 32 * i <= M - 3 && bhi >= 32 * i + 1 && blo <= M - 2) {
-      k2_tile<MODE, DEG>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey);
+      if (PRUNE) best = g.seed[z];
+      k2_tile<MODE, DEG, true, PRUNE>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey);
       warp_argmax(best, bestkey);
     }
     if (lane == 0) {
@@ -1382,6 +1469,109 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
       g.item_key[(size_t)(i * nbt + bt) * g.nz + z] = bestkey;
     }
   }
+}
+
+// Seed score of the pruned k = 2 search (k_search_k2<PROD_MAX, DEG, true>):
+// one CTA per slice evaluates a coarse grid of tuples (a, b) = (S i, S j),
+// S = ceil((M-1)/32), then one round of coordinate ascent (the best a for
+// the grid's b over every position, then the best b for that a), and stores
+// the value of the best tuple found (on the c5 phantom within ~1e-5 of the
+// maximum; a third pass reaches it, but costs a block-wide step of latency
+// for little extra pruning).  Values are k2_tile's expression tree
+// (k2_value), so the seed equals that tuple's score in the search bit for
+// bit, and the search, starting from (seed, key none), still finds every
+// tuple scoring >= it.  The slice's packed rows are staged in shared memory
+// when they fit (M <= kK2SeedRows).  Slices that are not searched get -inf.
+template <int MODE, int DEG, class Tab>
+__device__ __forceinline__ double k2_value(const K2Row *rz, const int a, const int b, const Luts &l, const Tab &tab) {
+  const double ident = MODE == SUM ? 0.0 : 1.0;
+  const K2Row ra = rz[a + 1], rb = rz[b + 1];
+  const double pre = combine<MODE>(ident, k2_term<MODE, DEG>(l, tab, ra.c, dd_diff(ra.wh, ra.wl, 0.0, 0.0)));
+  const double wm = dd_diff(rb.wh, rb.wl, ra.wh, ra.wl);
+  const double R = combine<MODE>(k2_term<MODE, DEG>(l, tab, rb.c - ra.c, wm), rb.as);
+  double v = combine<MODE>(pre, R);
+  if (MODE == PROD_MIN) v = -v;
+  return v;
+}
+
+constexpr int kK2SeedRows = 1024;  // rows staged in shared memory (32 KB)
+
+template <int MODE, int DEG>
+__global__ void __launch_bounds__(256) k_k2_seed(SearchArgs g) {
+  __shared__ K2Row srow[kK2SeedRows];
+  const int z = blockIdx.x;
+  const int M = g.Mz[z];
+  if (g.status[z] != kOK || M < 3) {
+    if (threadIdx.x == 0) g.seed[z] = -CUDART_INF;
+    return;
+  }
+  const K2Row *rz = g.rows + (size_t)z * g.RE;
+  if (M <= kK2SeedRows) {  // entries 0 .. M-1 (a + 1, b + 1 <= M - 1)
+    for (int e = threadIdx.x; e < M; e += blockDim.x) srow[e] = rz[e];
+    rz = srow;
+  }
+  __syncthreads();
+  const SpGlobal tab{g.luts.sp};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double ss[32];
+  __shared__ uint64_t sk[32];
+  // block argmax of (value desc, key asc); key = a << 16 | b
+  auto reduce = [&](double v, uint64_t key) -> uint64_t {
+    warp_argmax(v, key);
+    __syncthreads();  // previous round's readers are done
+    if (lane == 0) {
+      ss[warp] = v;
+      sk[warp] = key;
+    }
+    __syncthreads();
+    v = lane < nw ? ss[lane] : -CUDART_INF;
+    key = lane < nw ? sk[lane] : kKeyNone;
+    warp_argmax(v, key);
+    return key;  // every warp reduces the same entries: block-uniform
+  };
+  const int S = (M - 1 + 31) / 32;
+  double v = -CUDART_INF;
+  uint64_t key = kKeyNone;
+  {  // grid: 1024 points, 4 per thread, independent (their loads overlap)
+    double x[4];
+    uint64_t kx[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int e = threadIdx.x + u * 256;
+      const int a = S * (e >> 5), b = S * (e & 31);
+      const bool ok = e < 1024 && a < b && b <= M - 2;
+      x[u] = ok ? k2_value<MODE, DEG>(rz, a, b, g.luts, tab) : -CUDART_INF;
+      kx[u] = ok ? (((uint64_t)a << 16) | (uint64_t)b) : kKeyNone;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (better(x[u], kx[u], v, key)) {
+        v = x[u];
+        key = kx[u];
+      }
+  }
+  key = reduce(v, key);
+  int ta = key == kKeyNone ? 0 : (int)(key >> 16), tb = key == kKeyNone ? 1 : (int)(key & 0xffff);
+  for (int pass = 0; pass < 2; pass++) {
+    const bool move_a = pass == 0;
+    const int lo = move_a ? 0 : ta + 1, hi = move_a ? tb - 1 : M - 2;
+    v = -CUDART_INF;
+    key = kKeyNone;
+#pragma unroll 4
+    for (int x = lo + threadIdx.x; x <= hi; x += blockDim.x) {
+      const int a = move_a ? x : ta, b = move_a ? tb : x;
+      const double y = k2_value<MODE, DEG>(rz, a, b, g.luts, tab);
+      const uint64_t ky = ((uint64_t)a << 16) | (uint64_t)b;
+      if (better(y, ky, v, key)) {
+        v = y;
+        key = ky;
+      }
+    }
+    key = reduce(v, key);
+    ta = (int)(key >> 16);
+    tb = (int)(key & 0xffff);
+  }
+  if (threadIdx.x == 0) g.seed[z] = k2_value<MODE, DEG>(rz, ta, tb, g.luts, tab);
 }
 
 // Per (unit u in [u0, u1), slice z), one warp: fold the k = 2 tile partials of

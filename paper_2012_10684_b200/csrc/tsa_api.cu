@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -138,6 +139,7 @@ struct SearchWs {
   uint64_t *item_key = nullptr;
   tsa::K2Row *rows = nullptr;    // [nz][k2_row_stride] packed positions (k = 2)
   int32_t *ccur = nullptr;       // [nz] per-slice chunk counters (k_search_tri)
+  double *seed = nullptr;        // [nz] seed scores of the pruned k = 2 search
 };
 
 constexpr int kTriSS = 8;  // k_search_tri: CTA entries per slice
@@ -180,6 +182,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
     w.item_score = c.take<double>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
     w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
     w.rows = c.take<tsa::K2Row>(nz * (size_t)k2_row_stride(bins) + kPad);
+    w.seed = c.take<double>(nz);
   }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
@@ -732,6 +735,14 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
                               int32_t unit_begin, int32_t unit_end, double *part_score, uint64_t *part_key,
                               void *workspace, size_t workspace_bytes, void *stream, int k2_ctas_per_sm);
 
+// The k = 2 search (q < 1) skips groups of tuples whose upper bound is below a
+// score already reached (exact: k_search.cuh k2_tile PRUNE).  TSA_K2_PRUNE=0
+// in the environment runs the plain exhaustive kernel instead (A/B testing).
+static bool k2_prune_enabled() {
+  const char *e = getenv("TSA_K2_PRUNE");
+  return !(e && e[0] == '0');
+}
+
 tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N,
                       int32_t bins, int32_t k, double q, int32_t objective, int32_t enumeration,
                       int32_t units, int32_t unit_begin, int32_t unit_end, double *part_score,
@@ -923,11 +934,21 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
   a.item_key = w.item_key;
   a.rows = w.rows;
   a.RE = k2_row_stride(bins);
+  a.seed = w.seed;
   if (k == 2 && mode != tsa::SPP) {
     // warp-per-a-block search from a global item queue, then the per-unit fold
     const int grid = k2_ctas_per_sm * g_num_sms();
     auto kern = tsa::k_search_k2<tsa::SUM, 6>;
-    if (mode == tsa::PROD_MAX)
+    if (mode == tsa::PROD_MAX && k2_prune_enabled()) {
+      // seed scores, then the bounded search (bit-identical result, k_search.cuh k2_tile PRUNE)
+      auto sk = l.deg == 5 ? tsa::k_k2_seed<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_k2_seed<tsa::PROD_MAX, 6>
+                                                                          : tsa::k_k2_seed<tsa::PROD_MAX, 12>;
+      sk<<<(unsigned)nz, 256, 0, s>>>(a);
+      TSA_TRY(check_cuda("k_k2_seed"));
+      kern = l.deg == 5   ? tsa::k_search_k2<tsa::PROD_MAX, 5, true>
+             : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MAX, 6, true>
+                          : tsa::k_search_k2<tsa::PROD_MAX, 12, true>;
+    } else if (mode == tsa::PROD_MAX)
       kern = l.deg == 5 ? tsa::k_search_k2<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MAX, 6>
                                                                           : tsa::k_search_k2<tsa::PROD_MAX, 12>;
     else if (mode == tsa::PROD_MIN)

@@ -965,7 +965,7 @@ def run_1d(args, cfg, rank, world, dev):
                           "gbs": hist_b / (stt["histogram"] * 1e-3) / 1e9,
                           "frac_hbm": hist_b / (stt["histogram"] * 1e-3) / 1e9 / hbm},
             "search": {"ms": stt["search"], "calls_per_step": len(qs),
-                       "note": "k_small_luts + k_scan [+ k_rtable] + search kernel [+ k_merge_items]"},
+                       "note": "k_small_luts + k_scan + [k_k2_seed + k_search_k2 + k_merge_items | k_tri_tables + k_search_tri + k_fold_slots]"},
             "finalize": {"ms": stt["finalize"], "calls_per_step": len(qs)},
             "label": {"ms": stt["label"], "calls_per_step": len(qs), "bytes": lab_b * len(qs),
                       "note": ("the staged per-q label kernel; the sweep step labels all q in one pass "
@@ -985,6 +985,13 @@ def run_1d(args, cfg, rank, world, dev):
                                       "gtuples_per_s_nominal": nominal / (stt["search"] * 1e-3) / 1e9,
                                       "fp64_instr_per_tuple": fpt, "fp64_lane_instr_per_s": ach,
                                       "frac_fp64": ach / peak64})
+            if args.enumeration == "canonical" and (k >= 3 or (k == 2 and all(q < 1 for q in qs))):
+                kernels["search"]["pruning"] = (
+                    "exact bounds (DESIGN.md §7b): every canonical tuple is evaluated or excluded by a rigorous "
+                    "upper bound below a score already reached, so the result is the exhaustive search's bit for "
+                    "bit; tuples_evaluated counts the canonical tuples COVERED and the fp64 rate / frac_fp64 are "
+                    "the exhaustive-equivalent rate (covered tuples x the per-tuple instructions of the "
+                    "unpruned loop / stage time)")
         tr = {}
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -1091,11 +1098,14 @@ def run_1d(args, cfg, rank, world, dev):
         cpu = cpu_baseline(cfg, host, qs)
 
     # our kernels per step: compact k_lut_part + k_hist_part + k_mid + k_label_part;
-    # staged k_histogram + per q (k_small_luts + k_scan [+ k_rtable] + search
-    # [+ k_merge_items] + k_finalize + label)
+    # staged k_histogram + per q (k_small_luts + k_scan [+ k_rtable | k_tri_tables]
+    # [+ k_k2_seed] + search [+ k_merge_items | k_fold_slots] + k_finalize + label)
     rtable = k >= 3 and bins <= 512 and args.enumeration == "full"  # canonical k >= 3: k_search_tri
     tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
-    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0)
+    # + k_k2_seed: the bounded k = 2 search (q < 1, TSA_K2_PRUNE not 0)
+    seed = k == 2 and args.enumeration != "dp" and qs[0] < 1 and os.environ.get("TSA_K2_PRUNE", "1")[:1] != "0"
+    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0) + \
+        (1 if seed else 0)
     slabs = min(cfg.nz, 8)
     if sweep:  # one histogram, per q the search chain, one k_label_sweep per 16 q
         launches_per_step = 1 + (per_q - 1) * len(qs) + -(-len(qs) // 16)

@@ -136,12 +136,37 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   // ordered list of non-empty bins: thread t owns bins [t*per, (t+1)*per)
   const int per = (L + kFinThreads - 1) / kFinThreads;
   const int i0 = min(L, tid * per), i1 = min(L, i0 + per);
+  // L = 1024 / 4096 (per = 4 / 16) from global memory: the thread's bins in
+  // registers from up to four 16-byte loads issued together (round 1 walked
+  // them with one dependent L2 round trip per bin: ~half of the c5 finalize)
+  const bool vec = !hsm && (per == 4 || per == 16) && L == per * kFinThreads &&
+                   (reinterpret_cast<uintptr_t>(h) & 15) == 0;
+  uint32_t cv[16];
+  if (vec) {
+    const uint4 *h4 = reinterpret_cast<const uint4 *>(h + i0);
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const uint4 x = v < per / 4 ? __ldcg(h4 + v) : make_uint4(0u, 0u, 0u, 0u);
+      cv[4 * v] = x.x;
+      cv[4 * v + 1] = x.y;
+      cv[4 * v + 2] = x.z;
+      cv[4 * v + 3] = x.w;
+    }
+  }
   int cnt = 0;
   unsigned long long nsum = 0;
-  for (int i = i0; i < i1; i++) {
-    const uint32_t c = ldh(i);
-    cnt += c != 0;
-    nsum += c;
+  if (vec) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      cnt += cv[u] != 0;
+      nsum += cv[u];
+    }
+  } else {
+    for (int i = i0; i < i1; i++) {
+      const uint32_t c = ldh(i);
+      cnt += c != 0;
+      nsum += c;
+    }
   }
   int ex = cnt;
 #pragma unroll
@@ -169,8 +194,23 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   __syncthreads();
   const int m = s_cnt[NW];
   int e = s_cnt[warp] + ex - cnt;
-  for (int i = i0; i < i1; i++)
-    if (ldh(i)) lst[e++] = i;
+  // the list entry and its count (fsh is free until p is formed)
+  if (vec) {
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+      if (cv[u]) {
+        lst[e] = i0 + u;
+        fsh[e++] = (double)cv[u];
+      }
+  } else {
+    for (int i = i0; i < i1; i++) {
+      const uint32_t c = ldh(i);
+      if (c) {
+        lst[e] = i;
+        fsh[e++] = (double)c;
+      }
+    }
+  }
   const double N = (double)s_n[0];  // exact: the oracle's sequential double sum of integers
   __syncthreads();
   // class c = list segment [start_c, start_{c+1}): first entry with bin > t_{c-1}
@@ -185,7 +225,7 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
     }
     s_start[tid] = tid == k + 1 ? m : lo;
   }
-  for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn((double)ldh(lst[j]), N);
+  for (int j = tid; j < m; j += kFinThreads) fsh[j] = __ddiv_rn(fsh[j], N);
   __syncthreads();
   // sequential sums in ascending order; the shared loads of 8 terms are
   // issued ahead of their 8 dependent adds (round 2: one load latency per

@@ -47,6 +47,8 @@ struct SearchArgs {
   int ss;                            // k_search_tri: CTA entries per slice
   int32_t *ccur;                     // k_search_tri: [nz] per-slice chunk counters, zeroed
   double *seed;                      // [nz] seed scores of the pruned k = 2 search (k_k2_seed)
+  K2Row *chk;                        // [2][nz][RE] bound records of the pruned k = 2 search (k_k2_seed)
+  int64_t TS;                        // k_tri_tables / k_search_tri: doubles per slice region (tri_slice_stride)
 };
 
 // STAGE: copy the slice's C/W/Asuf tables to shared memory first (L <= 1024).
@@ -569,7 +571,14 @@ __host__ __device__ __forceinline__ int tri_pbs(int M) { return (M + 7) >> 3; }
 __host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
   int64_t r = 0;
   for (int a = 0; a <= M - 3; a++) r += tri_row_len(M, a);
-  return r + (int64_t)(M - 1) * M / 2 + (int64_t)(M - 2) * (tri_rbs(M) + tri_pbs(M));
+  return r + (int64_t)(M - 1) * M / 2 + (int64_t)(M - 2) * (tri_rbs(M) + tri_pbs(M)) + 2 * (int64_t)M;
+}
+// After RB and PB: QB[j] = max_c PB[j][c] (the sign-adjusted first-two-class
+// prefix bound for t_{k-2} = j, any t_1 < j) and RA[a] = the bound of the
+// whole R row a (max_c RB[a][c]; min in PROD_MIN), M doubles each: item-level
+// bounds of the k >= 3 search.
+__host__ __device__ __forceinline__ int64_t tri_qb_off(int M) {
+  return (int64_t)(M - 1) * M / 2 + (int64_t)(M - 2) * (tri_rbs(M) + tri_pbs(M));
 }
 
 // Per-slice table region of k_search_tri (doubles): row offsets (M-1 ints,
@@ -578,11 +587,22 @@ __host__ __device__ __forceinline__ int64_t tri_table_doubles(int M) {
 // (the last double of the offsets area holds the slice's seed score, tri_seed)
 __host__ __device__ __forceinline__ int tri_roff_doubles(int M) { return (((M + 1) / 2) + 2) & ~1; }
 __host__ __device__ __forceinline__ int64_t tri_region_doubles(int M) { return tri_roff_doubles(M) + tri_table_doubles(M); }
+// Per-slice region stride (host): room for any M <= L, even (16-byte aligned
+// regions for the bulk copy).
+inline int64_t tri_slice_stride(int L) { return (tri_region_doubles(L) + 1) & ~(int64_t)1; }
 
 // Build the tables of slice z into `base`: roff[a] (start of R row a;
-// roff[M-2] = start of T), the R rows, T.  Same expressions as k_rtable.
-template <int MODE>
-__device__ void tri_build(const SearchArgs &g, const int z, const int M, const SliceTables &t, double *base) {
+// roff[M-2] = start of T), T, then -- warp 0 computing the slice's seed score
+// from T (tri_seed, concurrently) -- the R rows and the chunk bounds RB / PB
+// (warps 1..; a named barrier orders RB / PB after the R rows).  Same
+// expressions as k_rtable.  s_roff: shared copy of roff (M <= kTriMaxRows)
+// for the row search of the flattened R loop, else null.
+template <int K, int MODE>
+__device__ double tri_seed(const int M, const double *Tt, const double *asz);
+
+template <int K, int MODE>
+__device__ void tri_build(const SearchArgs &g, const int z, const int M, const SliceTables &t, double *base,
+                          int *s_roff) {
   int *roff = reinterpret_cast<int *>(base);
   double *Rt = base + tri_roff_doubles(M);
   const double *asz = g.Asuf + (size_t)z * g.L;
@@ -590,12 +610,15 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     int o = 0;
     for (int a = 0; a <= M - 3; a++) {
       roff[a] = o;
+      if (s_roff) s_roff[a] = o;
       o += tri_row_len(M, a);
     }
     roff[M - 2] = o;  // start of the T table
+    if (s_roff) s_roff[M - 2] = o;
   }
   __syncthreads();
-  const int tbase = roff[M - 2];
+  const int *ro = s_roff ? s_roff : roff;
+  const int tbase = ro[M - 2];
   double *Tt = Rt + tbase;
   // flattened over all entries (every thread busy; round 2's first version
   // looped over rows with at most M threads active and was latency-bound)
@@ -607,29 +630,39 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     Tt[e] = class_term<MODE>(t, g.luts, e - j * (j + 1) / 2, j);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < tbase; e += blockDim.x) {  // R rows: row a holds [roff[a], roff[a+1])
-    int lo = 0, hi = M - 3;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (roff[mid] <= e) lo = mid;
-      else hi = mid - 1;
+  if (threadIdx.x < 32) {  // warp 0: the seed (reads T and Asuf only)
+    if (M - 1 >= K) {
+      const double seed = tri_seed<K, MODE>(M, Tt, asz);
+      if (threadIdx.x == 0) base[tri_roff_doubles(M) - 1] = seed;
     }
-    const int a = lo, b = ((a + 1) & ~1) + (e - roff[a]);
-    Rt[e] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+    return;  // no further block-wide barrier in the caller before its __syncthreads
   }
-  __syncthreads();
+  const int tid = threadIdx.x - 32, nth = blockDim.x - 32;
+  {  // R rows, a warp per row (lanes over its columns; a flattened loop
+     // needed a binary search of roff per entry: ncu, the top stall)
+    const int lane = threadIdx.x & 31, nwr = nth >> 5;
+    for (int a = tid >> 5; a <= M - 3; a += nwr) {
+      const int sa = (a + 1) & ~1, len = tri_row_len(M, a);
+      double *row = Rt + ro[a];
+      for (int u = lane; u < len; u += 32) {
+        const int b = sa + u;
+        row[u] = (b > a && b <= M - 2) ? combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)) : CUDART_NAN;
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");  // warps 1.. only
   double *RB = Tt + ntri;
   const int rbs = tri_rbs(M), pbs = tri_pbs(M);
   double *PB = RB + (M - 2) * rbs;
-  for (int e = threadIdx.x; e < (M - 2) * rbs; e += blockDim.x) {
+  for (int e = tid; e < (M - 2) * rbs; e += nth) {
     const int a = e / rbs, c = e - a * rbs;
-    const double *row = Rt + roff[a];
+    const double *row = Rt + ro[a];
     const int u1 = min(tri_row_len(M, a), 16 * c + 16);
     double v = CUDART_NAN;
     for (int u = 16 * c; u < u1; u++) v = MODE == PROD_MIN ? fmin(v, row[u]) : fmax(v, row[u]);
     RB[e] = v;
   }
-  for (int e = threadIdx.x; e < (M - 2) * pbs; e += blockDim.x) {
+  for (int e = tid; e < (M - 2) * pbs; e += nth) {
     const int a = e / pbs, c = e - a * pbs;
     double v = CUDART_NAN;
     for (int t1 = 8 * c; t1 < min(a, 8 * c + 8); t1++) {
@@ -638,6 +671,15 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
       v = fmax(v, pre);
     }
     PB[e] = v;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");
+  double *QB = PB + (M - 2) * pbs, *RA = QB + M;
+  for (int j = tid; j <= M - 3; j += nth) {
+    double qv = CUDART_NAN, rv = CUDART_NAN;
+    for (int c = 0; c < pbs; c++) qv = fmax(qv, PB[j * pbs + c]);
+    for (int c = 0; c < rbs; c++) rv = MODE == PROD_MIN ? fmin(rv, RB[j * rbs + c]) : fmax(rv, RB[j * rbs + c]);
+    QB[j] = qv;
+    RA[j] = rv;
   }
 }
 
@@ -726,63 +768,57 @@ __device__ __forceinline__ unsigned cmp_p1c4(unsigned hit, double p, double2 x01
 // claimed from the slice's counter by warps of every CTA on the slice.
 // A lower bound for the slice's best score, to seed the rescan test: the
 // value (same expression tree as the search) of a tuple found by coordinate
-// ascent from evenly spaced thresholds (3 passes, warp 0; any valid tuple's
-// value is a valid seed -- a good one makes exact rescans rare).  The search
+// ascent from evenly spaced thresholds (3 passes, one warp; any valid tuple's
+// value is a valid seed -- a good one makes exact rescans rare and the chunk
+// bounds effective).  The R entry of (a, b) is formed from T and Asuf exactly
+// as tri_build forms it, so the seed runs next to the R build.  The search
 // then compares against it with key = none, so the tuples scoring >= it,
-// the argmax among them, are all still found exactly.
+// the argmax among them, are all still found exactly.  Returns the seed in
+// every lane.
 template <int K, int MODE>
-__device__ __forceinline__ double tri_seed(const int M, const double *base) {
-  __shared__ double s_seed;
+__device__ double tri_seed(const int M, const double *Tt, const double *asz) {
   constexpr int R = K - 1;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    const int *roff = reinterpret_cast<const int *>(base);
-    const double *Rt = base + tri_roff_doubles(M);
-    const double *Tt = Rt + roff[M - 2];
-    auto val = [&](const int *t) -> double {  // t[0..K-1] strictly increasing in [0, M-2]
-      const double p01 = combine<MODE>(Tt[tri_idx(0, t[0])], Tt[tri_idx(t[0] + 1, t[1])]);
-      double pre = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(t[1] + 1, t[R - 1])]);
-      if (MODE == PROD_MIN) pre = -pre;
-      const int a = t[R - 1], b = t[K - 1];
-      return combine<MODE>(pre, Rt[roff[a] - ((a + 1) & ~1) + b]);
-    };
-    int t[K];
+  const int lane = threadIdx.x & 31;
+  auto val = [&](const int *t) -> double {  // t[0..K-1] strictly increasing in [0, M-2]
+    const double p01 = combine<MODE>(Tt[tri_idx(0, t[0])], Tt[tri_idx(t[0] + 1, t[1])]);
+    double pre = K == 3 ? p01 : combine<MODE>(p01, Tt[tri_idx(t[1] + 1, t[R - 1])]);
+    if (MODE == PROD_MIN) pre = -pre;
+    const int a = t[R - 1], b = t[K - 1];
+    return combine<MODE>(pre, combine<MODE>(Tt[tri_idx(a + 1, b)], __ldg(asz + b)));
+  };
+  int t[K];
 #pragma unroll
-    for (int j = 0; j < K; j++) t[j] = (int)((int64_t)(j + 1) * (M - 1) / (K + 1)) - 1 + (j == 0);
+  for (int j = 0; j < K; j++) t[j] = (int)((int64_t)(j + 1) * (M - 1) / (K + 1)) - 1 + (j == 0);
 #pragma unroll
-    for (int j = 1; j < K; j++) t[j] = max(t[j], t[j - 1] + 1);  // strictly increasing
-    double best = val(t);
-    for (int pass = 0; pass < 3; pass++) {
+  for (int j = 1; j < K; j++) t[j] = max(t[j], t[j - 1] + 1);  // strictly increasing
+  double best = val(t);
+  for (int pass = 0; pass < 3; pass++) {
 #pragma unroll
-      for (int j = 0; j < K; j++) {
-        const int lo = j == 0 ? 0 : t[j - 1] + 1, hi = j == K - 1 ? M - 2 : t[j + 1] - 1;
-        double bv = -CUDART_INF;
-        int bx = t[j];
-        // independent candidates: unrolled so their table loads overlap (the
-        // ascent is the critical path of k_tri_tables)
+    for (int j = 0; j < K; j++) {
+      const int lo = j == 0 ? 0 : t[j - 1] + 1, hi = j == K - 1 ? M - 2 : t[j + 1] - 1;
+      double bv = -CUDART_INF;
+      int bx = t[j];
+      // independent candidates: unrolled so their table loads overlap
 #pragma unroll 4
-        for (int x = lo + lane; x <= hi; x += 32) {
-          int u[K];
+      for (int x = lo + lane; x <= hi; x += 32) {
+        int u[K];
 #pragma unroll
-          for (int i = 0; i < K; i++) u[i] = i == j ? x : t[i];
-          const double v = val(u);
-          if (v > bv || (v == bv && x < bx)) {
-            bv = v;
-            bx = x;
-          }
-        }
-        uint64_t key = (uint64_t)bx;
-        warp_argmax(bv, key);
-        if (bv > best) {
-          best = bv;
-          t[j] = (int)key;
+        for (int i = 0; i < K; i++) u[i] = i == j ? x : t[i];
+        const double v = val(u);
+        if (v > bv || (v == bv && x < bx)) {
+          bv = v;
+          bx = x;
         }
       }
+      uint64_t key = (uint64_t)bx;
+      warp_argmax(bv, key);
+      if (bv > best) {
+        best = bv;
+        t[j] = (int)key;
+      }
     }
-    if (lane == 0) s_seed = best;
   }
-  __syncthreads();
-  return s_seed;
+  return best;
 }
 
 // Items of a slice: for a in [R-1, M-3] the prefixes ending at a have colex
@@ -872,7 +908,9 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
       // monotone, so a skipped tuple scores <= the bound < best: exact)
       const double rbl = MODE == PROD_MIN ? fmin(fmin(rv[0], rv[1]), rv[2]) : fmax(fmax(rv[0], rv[1]), rv[2]);
       const double *pbr = Tt + (M - 1) * M / 2 + (M - 2) * tri_rbs(M) + a * tri_pbs(M);
-      for (int t1c = t1lo; t1c < t1hi;) {
+      // the whole item first: QB[a] bounds every prefix ending at a
+      const bool live = __any_sync(0xffffffffu, combine<MODE>(Tt[tri_qb_off(M) + a], rbl) >= best);
+      for (int t1c = live ? t1lo : t1hi; t1c < t1hi;) {
         const int cend = min(t1hi, (t1c & ~7) + 8);
         if (__any_sync(0xffffffffu, combine<MODE>(pbr[t1c >> 3], rbl) >= best))
           for (int t1 = t1c; t1 < cend; t1++) {
@@ -907,7 +945,37 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
       }
       continue;
     }
-    uint64_t rb = lo + (uint64_t)(c - s_cum[lo_i]) * G + (uint64_t)lane * (P * Q);
+    const uint64_t ib = lo + (uint64_t)(c - s_cum[lo_i]) * G;  // the item's ranks [ib, min(hi, ib + G))
+    if (K == 4) {
+      // item bound: prefixes (t_1, j, a) score <= combine(QB[j], T(j+1, a))
+      // (QB: the max of the first two classes over t_1), rows <= RA[a]; the
+      // item is dropped when that is below every lane's best
+      const uint64_t base_a = binom((uint64_t)a, 3);
+      auto jof = [&](uint64_t r) -> int {  // t_2 of colex offset r within a: C(j,2) <= r < C(j+1,2)
+        int j = (int)((1.0 + sqrt(1.0 + 8.0 * (double)r)) * 0.5);
+        while (j > 1 && binom((uint64_t)j, 2) > r) j--;
+        while (binom((uint64_t)j + 1, 2) <= r) j++;
+        return j;
+      };
+      const int jlo = jof(ib - base_a), jhi = jof(min(hi, ib + G) - 1 - base_a);
+      const double *QB = Tt + tri_qb_off(M);
+      double vb = -CUDART_INF;
+      for (int j = jlo + lane; j <= jhi; j += 32) vb = fmax(vb, combine<MODE>(QB[j], Tt[tri_idx(j + 1, a)]));
+      double bmin = best;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        vb = fmax(vb, __shfl_xor_sync(0xffffffffu, vb, off));
+        bmin = fmin(bmin, __shfl_xor_sync(0xffffffffu, bmin, off));
+      }
+      if (!(combine<MODE>(vb, QB[M + a]) >= bmin)) {
+        if (first) {
+          warp_argmax(best, bestkey);
+          first = false;
+        }
+        continue;
+      }
+    }
+    uint64_t rb = ib + (uint64_t)lane * (P * Q);
     {  // the whole warp runs the tiles (lanes past hi hold NaN prefixes), so
        // the chunk votes below are converged
       const int sa = (a + 1) & ~1;
@@ -1004,13 +1072,9 @@ __global__ void __launch_bounds__(256) k_tri_tables(SearchArgs g) {
     }
   __syncthreads();
   const SliceTables t{stage ? s_C : gC, stage ? s_Wh : gWh, stage ? s_Wl : gWl, nullptr};
-  double *region = const_cast<double *>(g.R) + (size_t)z * g.L * g.RS;
-  tri_build<MODE>(g, z, M, t, region);
-  __syncthreads();
-  if (M - 1 >= K) {
-    const double seed = tri_seed<K, MODE>(M, region);
-    if (threadIdx.x == 0) region[tri_roff_doubles(M) - 1] = seed;
-  }
+  double *region = const_cast<double *>(g.R) + (size_t)z * g.TS;
+  __shared__ int s_roff[kTriMaxRows + 2];
+  tri_build<K, MODE>(g, z, M, t, region, M <= kTriMaxRows ? s_roff : nullptr);
 }
 
 // Exhaustive search for k >= 3 over per-slice class-term tables (round 2;
@@ -1067,7 +1131,7 @@ __global__ void __launch_bounds__(256, TSA_TRI_MINB) k_search_tri(SearchArgs g, 
       const int nitems = tri_items<K>(M, r0, r1, s_cum);
       // skip the copy when the slice's items are already all claimed
       if (*((volatile int32_t *)ccur) < nitems) {
-        const double *region = g.R + (size_t)z * g.L * g.RS;
+        const double *region = g.R + (size_t)z * g.TS;
         const int32_t *gB = g.Bin + (size_t)z * g.E;
         const bool stage = M + 1 <= kTriMaxRows + 2;
         if (stage)
@@ -1307,7 +1371,7 @@ __device__ __forceinline__ double k2_term(const Luts &l, const Tab &tab, uint32_
   const double2 e = tab.jr(j);
   if (MODE == PROD_MAX || MODE == PROD_MIN) {
     const double d = scale_pow2_neg(__dmul_rn((double)r, e.y), s, r);
-    const double ip = __dmul_rn(__dmul_rn(e.x, l.p2[s]), horner_c_deg<DEG>(l, d));
+    const double ip = __dmul_rn(__dmul_rn(e.x, tab.p2(s)), horner_c_deg<DEG>(l, d));
     return __dmul_rn(w, ip);
   } else {
     return shannon_t(l, tab, n, w);
@@ -1335,10 +1399,16 @@ __device__ __forceinline__ double k2_term(const Luts &l, const Tab &tab, uint32_
 // it is neither the argmax nor tied with it: the result is the exhaustive
 // search's, bit for bit.  The first 32 columns (lanes with a >= b) and the
 // last partial group are always evaluated.
+// The bound's inputs come from per-slice records (k_k2_seed): ck4[b0+1] =
+// {W at row b0+3, max Asuf over rows b0..b0+3, C at row b0} for a group and
+// ck16[b0+1] the same over rows b0..b0+15, checked first for every 16 rows
+// (two 16-byte loads per check instead of the group's eight row loads: the
+// first pruned version was L1-bound, ncu 93 % L1/TEX throughput).
 template <int MODE, int DEG, bool NC = true, bool PRUNE = false>
 __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
                                         const int lane, const Luts &l, const SpPair &tab, double &best,
-                                        uint64_t &bestkey) {
+                                        uint64_t &bestkey, const K2Row *ck4 = nullptr,
+                                        const K2Row *ck16 = nullptr) {
   static_assert(!PRUNE || MODE == PROD_MAX, "k = 2 pruning bounds the product form with q < 1");
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int a = 32 * i + lane;
@@ -1355,7 +1425,29 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   // a < b and b <= bend per tuple (the first 32 columns of the block, where
   // some lanes have a >= b, and the last partial group), else none
   const double preub = PRUNE ? __dmul_rn(pre, 1.0 + 0x1p-20) : 0.0;
-  auto group = [&](const int b0, const bool chk) {
+  // some lane's bound over the rows of record ck reaches its best
+  // (NaN -- lanes past the slice -- never asks for the rows)
+  // In the first 32 columns (chk groups) a lane's valid rows are b > a: for
+  // a >= b0 the smallest class is n(a, a+1) (nfirst), and a lane with
+  // a >= b0 + 3 has none.
+  const uint32_t nfirst = PRUNE ? rz[min(ac + 2, M - 1)].c - Ca : 0u;
+  // x = W at the record's last row, y = (max Asuf, (C at its first row, -))
+  auto live_xy = [&](const double2 x, const double2 y, const bool chk, const int b0) -> bool {
+    uint32_t j, rr, n = (uint32_t)__double2loint(y.y) - Ca;
+    if (chk && a >= b0) n = nfirst;
+    int s;
+    nsplit_idx(n, j, s, rr);
+    const double ipub = __dmul_rn(tab.jr(j).x, tab.p2(s));
+    const double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(dd_diff(x.x, x.y, Wah, Wal), y.x));
+    return __any_sync(0xffffffffu, (!chk || a < b0 + kK2Rows - 1) && bound >= best);
+  };
+  auto live = [&](const K2Row *ck, const bool chk, const int b0) -> bool {
+    return live_xy(ldrow<NC>(reinterpret_cast<const double2 *>(ck)),
+                   ldrow<NC>(reinterpret_cast<const double2 *>(ck) + 1), chk, b0);
+  };
+  // chkd: the group's bound was already checked (PRUNE) by the caller
+  auto group = [&](const int b0, const bool chk, const bool chkd = false) {
+    if (PRUNE && !chkd && !live(ck4 + b0 + 1, chk, b0)) return;
     const K2Row *pr = rz + b0 + 1;
     double vb[kK2Rows];
     double2 yv[kK2Rows], xv[kK2Rows];
@@ -1363,17 +1455,6 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
     for (int r = 0; r < kK2Rows; r++) {
       xv[r] = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r));      // wh, wl
       yv[r] = ldrow<NC>(reinterpret_cast<const double2 *>(pr + r) + 1);  // as, (c, bin)
-    }
-    if (PRUNE && !chk) {
-      uint32_t j, rr;
-      int s;
-      nsplit_idx((uint32_t)__double2loint(yv[0].y) - Ca, j, s, rr);
-      const double ipub = __dmul_rn(tab.jr(j).x, l.p2[s]);
-      const double wmax = dd_diff(xv[kK2Rows - 1].x, xv[kK2Rows - 1].y, Wah, Wal);
-      const double amax = fmax(fmax(yv[0].x, yv[1].x), fmax(yv[2].x, yv[3].x));
-      const double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(wmax, amax));
-      // NaN (lanes past the slice) never asks for the group
-      if (!__any_sync(0xffffffffu, bound >= best)) return;
     }
 #pragma unroll
     for (int r = 0; r < kK2Rows; r++) {
@@ -1406,6 +1487,33 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   };
   int b0 = max(32 * i + 1, blo);
   for (; b0 <= bend && b0 < 32 * i + 32; b0 += kK2Rows) group(b0, true);
+  if (PRUNE && b0 + 15 <= bend) {
+    // records one 16-row block ahead (their L1/L2 latency was the top stall);
+    // inside a live block the four group records are loaded together
+    double2 nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 1));
+    double2 ny = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 1) + 1);
+    for (; b0 + 15 <= bend; b0 += 16) {
+      const double2 x = nx, y = ny;
+      if (b0 + 31 <= bend) {
+        nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17));
+        ny = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17) + 1);
+      }
+      if (live_xy(x, y, false, b0)) {
+        double2 gx[4], gy[4];
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+          gx[g] = ldrow<NC>(reinterpret_cast<const double2 *>(ck4 + b0 + 4 * g + 1));
+          gy[g] = ldrow<NC>(reinterpret_cast<const double2 *>(ck4 + b0 + 4 * g + 1) + 1);
+        }
+        unsigned lv = 0;
+#pragma unroll
+        for (int g = 0; g < 4; g++) lv |= live_xy(gx[g], gy[g], false, b0 + 4 * g) ? 1u << g : 0u;
+#pragma unroll 1
+        for (int g = 0; g < 4; g++)
+          if (lv >> g & 1u) group(b0 + 4 * g, false, true);
+      }
+    }
+  }
   for (; b0 + kK2Rows - 1 <= bend; b0 += kK2Rows) group(b0, false);
   if (b0 <= bend) group(b0, true);
 }
@@ -1431,9 +1539,11 @@ __host__ __device__ __forceinline__ int k2_tiles(int m) { return m >= 3 ? (m - 2
 template <int MODE, int DEG, bool PRUNE = false>
 __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
+  __shared__ double s_p2[32];
   for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
+  if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.p2[threadIdx.x];
   __syncthreads();
-  const SpPair tab{s_jr};
+  const SpPair tab{s_jr, s_p2};
   const Luts &l = g.luts;
   const int lane = threadIdx.x & 31;
   const int mmax = *g.mmax;
@@ -1461,7 +1571,9 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
     uint64_t bestkey = kKeyNone;
     if (g.status[z] == kOK && 32 * i <= M - 3 && bhi >= 32 * i + 1 && blo <= M - 2) {
       if (PRUNE) best = g.seed[z];
-      k2_tile<MODE, DEG, true, PRUNE>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey);
+      const K2Row *ck = PRUNE ? g.chk + (size_t)z * g.RE : nullptr;
+      k2_tile<MODE, DEG, true, PRUNE>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey, ck,
+                                      PRUNE ? ck + (size_t)g.nz * g.RE : nullptr);
       warp_argmax(best, bestkey);
     }
     if (lane == 0) {
@@ -1510,8 +1622,25 @@ __global__ void __launch_bounds__(256) k_k2_seed(SearchArgs g) {
     for (int e = threadIdx.x; e < M; e += blockDim.x) srow[e] = rz[e];
     rz = srow;
   }
+  __shared__ double s_p2[32];
+  if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.p2[threadIdx.x];
   __syncthreads();
-  const SpGlobal tab{g.luts.sp};
+  // bound records of the search (k2_tile PRUNE): entry e = b0 + 1 covers rows
+  // b0 .. b0+3 (chk4) / b0 .. b0+15 (chk16), clipped to the slice's last row
+  // M-1 (records reaching past it are never read)
+  {
+    K2Row *c4 = g.chk + (size_t)z * g.RE, *c16 = c4 + (size_t)g.nz * g.RE;
+    for (int e = 1 + threadIdx.x; e <= M - 1; e += blockDim.x) {
+      const int e4 = min(e + 3, M - 1), e16 = min(e + 15, M - 1);
+      double m4 = rz[e].as, m16;
+      for (int x = e + 1; x <= e4; x++) m4 = fmax(m4, rz[x].as);
+      m16 = m4;
+      for (int x = e4 + 1; x <= e16; x++) m16 = fmax(m16, rz[x].as);
+      c4[e] = K2Row{rz[e4].wh, rz[e4].wl, m4, rz[e].c, 0};
+      c16[e] = K2Row{rz[e16].wh, rz[e16].wl, m16, rz[e].c, 0};
+    }
+  }
+  const SpGlobal tab{g.luts.sp, s_p2};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __shared__ double ss[32];
   __shared__ uint64_t sk[32];

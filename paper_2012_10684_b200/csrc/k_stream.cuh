@@ -186,6 +186,7 @@ __device__ void st_scan(const StreamArgs &g, const int64_t z, uint32_t *sh, doub
 template <int MODE, int DEG>
 __device__ void work_slice(const StreamArgs &g, const int64_t z, double *smem) {
   __shared__ int s_job, s_M, s_st, s_done;
+  __shared__ double s_p2[32];
   double2 *s_jr = reinterpret_cast<double2 *>(smem);
   const int lane = threadIdx.x & 31;
   bool jr_ok = false;  // the class-size table is staged in smem (CTA-uniform)
@@ -227,6 +228,7 @@ __device__ void work_slice(const StreamArgs &g, const int64_t z, double *smem) {
     if (!jr_ok) {
       for (int i = threadIdx.x; i < kSN; i += blockDim.x)
         s_jr[i] = make_double2(g.scan.luts.sp[i], g.scan.luts.sp[kSN + i]);
+      if (threadIdx.x < 32) s_p2[threadIdx.x] = g.scan.luts.p2[threadIdx.x];
       __syncthreads();
       jr_ok = true;
     }
@@ -236,7 +238,7 @@ __device__ void work_slice(const StreamArgs &g, const int64_t z, double *smem) {
     const int nb = (st == kOK && M >= 3) ? (M - 3) / 32 + 1 : 0;
     const int nbt = M >= 3 ? (M - 2) / kStTileB + 1 : 1;
     const int nbe = max(nb * nbt, 1);
-    const SpPair tab{s_jr};
+    const SpPair tab{s_jr, s_p2};
     const Luts &l = g.scan.luts;
     for (;;) {
       int c = 0;

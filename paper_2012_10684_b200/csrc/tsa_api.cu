@@ -140,6 +140,7 @@ struct SearchWs {
   tsa::K2Row *rows = nullptr;    // [nz][k2_row_stride] packed positions (k = 2)
   int32_t *ccur = nullptr;       // [nz] per-slice chunk counters (k_search_tri)
   double *seed = nullptr;        // [nz] seed scores of the pruned k = 2 search
+  tsa::K2Row *chk = nullptr;     // [2][nz][k2_row_stride] bound records of the pruned k = 2 search
 };
 
 constexpr int kTriSS = 8;  // k_search_tri: CTA entries per slice
@@ -183,9 +184,11 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
     w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
     w.rows = c.take<tsa::K2Row>(nz * (size_t)k2_row_stride(bins) + kPad);
     w.seed = c.take<double>(nz);
+    w.chk = c.take<tsa::K2Row>(2 * nz * (size_t)k2_row_stride(bins) + kPad);
   }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
-    w.R = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+    // (k_search_tri regions: tri_slice_stride(bins) doubles per slice)
+    w.R = c.take<double>(nz * (size_t)std::max<int64_t>((int64_t)bins * rstride(bins), tsa::tri_slice_stride(bins)) + 16);
     w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
     if (k >= 4) w.AI = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
   }
@@ -873,6 +876,7 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
     a.unit_begin = unit_begin;
     a.nunits = unit_end - unit_begin;
     a.ss = k == 3 ? 2 : 4;  // CTAs sharing a slice (k = 3 slices are small)
+    a.TS = tsa::tri_slice_stride(bins);
     a.ccur = w.ccur;
     a.item_score = w.item_score;
     a.item_key = w.item_key;
@@ -935,6 +939,7 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
   a.rows = w.rows;
   a.RE = k2_row_stride(bins);
   a.seed = w.seed;
+  a.chk = w.chk;
   if (k == 2 && mode != tsa::SPP) {
     // warp-per-a-block search from a global item queue, then the per-unit fold
     const int grid = k2_ctas_per_sm * g_num_sms();
@@ -1040,8 +1045,18 @@ tsa_status tsa_finalize(const uint32_t *hist, const int32_t *slice_status, int64
                        nparts, out->thresholds, out->objective, out->slice_status, nullptr, S(stream));
 }
 
+static tsa_status label_impl(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
+                             uint8_t *labels, void *stream, int ctas_per_sm);
+
 tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
                      uint8_t *labels, void *stream) {
+  return label_impl(p, thresholds, slice_status, labels, stream, 8);
+}
+
+// ctas_per_sm: the grid-stride label kernel's CTAs per SM (8 = every warp
+// slot; the overlap pipeline leaves room for the concurrent search)
+static tsa_status label_impl(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
+                             uint8_t *labels, void *stream, int ctas_per_sm) {
   TSA_TRY(tsa_validate(p));
   if (!thresholds || !labels) return set_error(TSA_ERR_INVALID_ARG, "label pointers");
   tsa::LabelArgs a;
@@ -1057,7 +1072,7 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
                        (reinterpret_cast<uintptr_t>(labels) & 15) == 0;
   if (aligned) {
     const int64_t groups = a.n / 16 * p->nz;
-    const int64_t blocks = std::min<int64_t>((groups + 255) / 256, (int64_t)g_num_sms() * 8);
+    const int64_t blocks = std::min<int64_t>((groups + 255) / 256, (int64_t)g_num_sms() * ctas_per_sm);
     cudaStream_t s = S(stream);
     if (p->dtype == TSA_U8) {
       switch (p->k) {
@@ -1093,6 +1108,21 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds, const int3
 // overlap.  Same kernels, same partition of the tuple space: bit-identical
 // to the staged pipeline.  Not used while `stream` is being captured (the
 // extra stream would outlive the capture): staged instead.
+// label CTAs per SM inside the overlap pipeline (TSA_OVL_LABEL_CTAS, A/B)
+static int ovl_label_ctas() {
+  const char *e = getenv("TSA_OVL_LABEL_CTAS");
+  const int v = e ? atoi(e) : 4;
+  return v >= 1 && v <= 8 ? v : 4;
+}
+// k = 2 search CTAs per SM inside the overlap pipeline (TSA_OVL_SEARCH_CTAS, A/B)
+static int ovl_search_ctas() {
+  const char *e = getenv("TSA_OVL_SEARCH_CTAS");
+  const int v = e ? atoi(e) : 2;
+  return v >= 1 && v <= 4 ? v : 2;
+}
+static tsa_status label_impl(const tsa_problem *p, const int32_t *thresholds, const int32_t *slice_status,
+                             uint8_t *labels, void *stream, int ctas_per_sm);
+
 static tsa_status segment_overlap(const tsa_problem *p, const tsa_outputs *out, const SegWs &w, cudaStream_t s) {
   const int64_t nz = p->nz, n = p->nx * p->ny;
   const size_t esz = p->dtype == TSA_U8 ? 1 : 2;
@@ -1119,7 +1149,8 @@ static tsa_status segment_overlap(const tsa_problem *p, const tsa_outputs *out, 
     sub(c, &q, &z0);
     if (cudaStreamWaitEvent(s, e_s[c], 0) != cudaSuccess) return set_error(TSA_ERR_CUDA, "overlap: wait search");
     if (!out->labels) return TSA_OK;
-    return tsa_label(&q, out->thresholds + z0 * p->k, w.status + z0, out->labels + (size_t)z0 * n, s);
+    return label_impl(&q, out->thresholds + z0 * p->k, w.status + z0, out->labels + (size_t)z0 * n, s,
+                      ovl_label_ctas());
   };
   if (cudaEventRecord(e_start, s) != cudaSuccess || cudaStreamWaitEvent(a, e_start, 0) != cudaSuccess)
     rc = set_error(TSA_ERR_CUDA, "overlap: fork");
@@ -1133,7 +1164,7 @@ static tsa_status segment_overlap(const tsa_problem *p, const tsa_outputs *out, 
     const int32_t U = units_of(&q);
     if (rc == TSA_OK)
       rc = search_impl(hist + z0 * p->bins, w.status + z0, q.nz, n, p->bins, p->k, p->q, p->objective,
-                       p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, a, 2);
+                       p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, a, ovl_search_ctas());
     if (rc == TSA_OK)
       rc = finalize_impl(hist + z0 * p->bins, w.status + z0, q.nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk,
                          U, out->thresholds + z0 * p->k, out->objective ? out->objective + z0 : nullptr,

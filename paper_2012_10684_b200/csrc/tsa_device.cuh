@@ -119,13 +119,20 @@ struct Luts {
 // ([kSN] j^-q | [kSN] 1/j | [32] 2^(-s q)); kernels that stage the table in
 // shared memory use an interleaved {j^-q, 1/j} layout (one 16-byte load) with
 // the same arithmetic, so every kernel computes bit-identical values.
+// p2(s): 2^(-s q) (Luts::p2) from a shared-memory copy -- the k = 2 kernels
+// index it per lane, and a lane-divergent index into the kernel-parameter
+// copy serialises in the constant cache (ncu: LDC in the k = 2 hot loop).
 struct SpGlobal {
   const double *sp;
+  const double *p2s = nullptr;  // shared copy of Luts::p2 (k2_term users only)
   __device__ __forceinline__ double2 jr(uint32_t j) const { return make_double2(sp[j], sp[kSN + j]); }
+  __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
 };
 struct SpPair {  // shared-memory staging: jr[j] = {j^-q or ln j, 1/j}
   const double2 *jrt;
+  const double *p2s;  // shared copy of Luts::p2
   __device__ __forceinline__ double2 jr(uint32_t j) const { return jrt[j]; }
+  __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
 };
 
 // n = 2^s (j + r 2^-s): table index j, exponent s and d = r / (j 2^s)

@@ -157,3 +157,23 @@ def test_tri_pruned_ties_equal_full(k, q):
         np.testing.assert_array_equal(a[key].cpu().numpy(), b[key].cpu().numpy(), err_msg=f"k={k} q={q} {key}")
     np.testing.assert_array_equal(a["objective"].cpu().numpy().view(np.uint64),
                                   b["objective"].cpu().numpy().view(np.uint64))
+
+
+@pytest.mark.parametrize("q", [0.4, 0.8])
+def test_k2_many_bins_unstaged_seed(q):
+    """M > 1024 non-empty bins (k_k2_seed reads the rows from global memory,
+    16-row bound records near the slice end) and small M (< 32 rows)."""
+    rng = np.random.default_rng(11)
+    nx = 256
+    slices = []
+    for used in (2500, 1100, 20, 5):
+        h = np.zeros(4096, np.int64)
+        idx = np.sort(rng.choice(4096, size=used, replace=False))
+        h[idx] = rng.integers(1, max(2, 2 * nx * nx // used), size=used)
+        scale = (nx * nx - used) / max(1, h.sum() - used)
+        h[idx] = 1 + np.floor((h[idx] - 1) * min(1.0, scale)).astype(np.int64)
+        h[idx[0]] += nx * nx - h.sum()
+        slices.append(_from_hist(h, nx))
+    vol = torch.from_numpy(np.stack(slices)).to(DEV)
+    _same(_run(vol, 4096, q, True, pipeline="staged"), _run(vol, 4096, q, False, pipeline="staged"),
+          f"many bins q={q}")

@@ -1099,13 +1099,17 @@ def run_1d(args, cfg, rank, world, dev):
 
     # our kernels per step: compact k_lut_part + k_hist_part + k_mid + k_label_part;
     # staged k_histogram + per q (k_small_luts + k_scan [+ k_rtable | k_tri_tables]
-    # [+ k_k2_seed] + search [+ k_merge_items | k_fold_slots] + k_finalize + label)
+    # [+ k_k2_seed] + search [+ k_merge_items | k_fold_slots] + [k_decide +] label + k_finalize[_phi])
     rtable = k >= 3 and bins <= 512 and args.enumeration == "full"  # canonical k >= 3: k_search_tri
     tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
-    # + k_k2_seed: the bounded k = 2 search (q < 1, TSA_K2_PRUNE not 0)
+    # + k_k2_seed: the bounded k = 2 search (q < 1, TSA_K2_PRUNE not 0), fused
+    # into k_scan_seed (replacing k_scan) unless TSA_K2_FUSE=0
     seed = k == 2 and args.enumeration != "dp" and qs[0] < 1 and os.environ.get("TSA_K2_PRUNE", "1")[:1] != "0"
-    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (1 if tri else 0) + \
-        (1 if seed else 0)
+    seed_kernel = seed and os.environ.get("TSA_K2_FUSE", "1")[:1] == "0"
+    # staged step with labels: k_decide + labels + k_finalize_phi (split finalize)
+    split = not sweep and os.environ.get("TSA_SPLIT_FINALIZE", "1")[:1] != "0"
+    per_q = 5 + (1 if rtable else 0) + (1 if k == 2 and args.enumeration != "dp" else 0) + (2 if tri else 0) + \
+        (1 if seed_kernel else 0) + (1 if split else 0)
     slabs = min(cfg.nz, 8)
     if sweep:  # one histogram, per q the search chain, one k_label_sweep per 16 q
         launches_per_step = 1 + (per_q - 1) * len(qs) + -(-len(qs) // 16)

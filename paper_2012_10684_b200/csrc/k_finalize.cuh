@@ -67,7 +67,10 @@ constexpr int kFinThreads = 256;
 // The per-slice body (also run by the stream pipeline's label tasks, k_stream.cuh):
 // fsh = [L] doubles followed by [L] ints of shared memory; blockDim.x ==
 // kFinThreads; the early returns are CTA-uniform.
-__device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *fsh, uint32_t *hsm = nullptr) {
+// phi_only: thresholds and statuses were written by k_decide (same merge,
+// same decisions); only the objective is written.
+__device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *fsh, uint32_t *hsm = nullptr,
+                               const bool phi_only = false) {
   int *lst = reinterpret_cast<int *>(fsh + g.L);
   __shared__ double s_best[1];
   __shared__ uint64_t s_key[1];
@@ -102,11 +105,11 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   if (st == kOK && key == kKeyNone) st = kNoValidSplit;
   const int k = g.k, L = g.L;
   if (st != kOK) {
-    if (tid < k) g.thresholds[z * k + tid] = -1;
+    if (tid < k && !phi_only) g.thresholds[z * k + tid] = -1;
     if (tid == 0) {
       if (g.objective_out) g.objective_out[z] = CUDART_NAN;
-      if (g.status_out) g.status_out[z] = st;
-      if (g.status_out2) g.status_out2[z] = st;
+      if (g.status_out && !phi_only) g.status_out[z] = st;
+      if (g.status_out2 && !phi_only) g.status_out2[z] = st;
     }
     return;
   }
@@ -115,11 +118,11 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
   const int t1 = k > 1 ? (int)((key >> (12 * (k - 2))) & 0xFFFull) : L;
   const int t2 = k > 2 ? (int)((key >> (12 * (k - 3))) & 0xFFFull) : L;
   const int t3 = k > 3 ? (int)(key & 0xFFFull) : L;
-  if (tid < k) {
+  if (tid < k && !phi_only) {
     const int tl = tid == 0 ? t0 : tid == 1 ? t1 : tid == 2 ? t2 : t3;
     g.thresholds[z * k + tid] = tl;
   }
-  if (tid == 0) {
+  if (tid == 0 && !phi_only) {
     if (g.status_out) g.status_out[z] = kOK;
     if (g.status_out2) g.status_out2[z] = kOK;
   }
@@ -272,6 +275,50 @@ __device__ void finalize_slice(const FinalizeArgs &g, const int64_t z, double *f
     }
     g.objective_out[z] = phi;
   }
+}
+
+// The staged step with labels splits k_finalize: k_decide (one warp per
+// slice: the merge, t* and the statuses -- all the labels need), then the
+// label kernel launched with Programmatic Dependent Launch, and
+// k_finalize_phi (phi(t*) only) as ITS dependent: it needs nothing from the
+// labels, so its CTAs run next to the label CTAs (which leave one CTA slot
+// per SM, tsa_api.cu) instead of before them, and it ends with
+// griddepcontrol.wait so its completion implies the labels' (later stream
+// work stays ordered after both).
+__global__ void k_decide(FinalizeArgs g) {
+  const int64_t z = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (z >= g.nz) return;  // warp-uniform
+  double sc = -CUDART_INF;
+  uint64_t key = kKeyNone;
+  for (int p = lane; p < g.nparts; p += 32) {
+    const double os = g.ps[(size_t)p * g.nz + z];
+    const uint64_t ok = g.pk[(size_t)p * g.nz + z];
+    if (better(os, ok, sc, key)) {
+      sc = os;
+      key = ok;
+    }
+  }
+  warp_argmax(sc, key);
+  int st = g.status_in[z];
+  if (st == kOK && key == kKeyNone) st = kNoValidSplit;
+  const int k = g.k;
+  if (lane < k) {
+    int tl = -1;
+    if (st == kOK) tl = (int)((key >> (12 * (k - 1 - lane))) & 0xFFFull);
+    g.thresholds[z * k + lane] = tl;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (g.status_out) g.status_out[z] = st;
+    if (g.status_out2) g.status_out2[z] = st;
+  }
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize_phi(FinalizeArgs g) {
+  extern __shared__ double fsh[];
+  finalize_slice(g, blockIdx.x, fsh, nullptr, true);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // completion implies the primary's (labels)
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_finalize(FinalizeArgs g) {

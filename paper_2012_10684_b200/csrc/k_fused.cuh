@@ -233,6 +233,8 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   __shared__ double s_red[32], s_P[kKMax + 1], s_S[kKMax + 1];
   __shared__ uint64_t s_key[32];
   __shared__ __align__(16) double s_scan[96];
+  __shared__ double s_p2[32];  // Luts::p2 for the class terms (synchronised below)
+  stage_p2(g.luts, s_p2);
   TSA_MPHASE(z, 0)
   if (tid == 0 && g.counters) {
     wait_ge(g.counters + 1, g.nlut);
@@ -278,15 +280,16 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
     // Asuf[i] = T(i+1, M-1) and Apre[i] = T(0, i) (in fsh, free until the finalize
     // step) in one pass so their gathers overlap
     for (int i = tid; i <= M - 2; i += blockDim.x) {
-      const double as = class_term<MODE>(t, g.luts, i + 1, M - 1);
-      const double ap = K == 2 ? class_term<MODE>(t, g.luts, 0, i) : 0.0;
+      const double as = class_term<MODE>(t, g.luts, i + 1, M - 1, s_p2);
+      const double ap = K == 2 ? class_term<MODE>(t, g.luts, 0, i, s_p2) : 0.0;
       Asuf[i] = as;
       if (K == 2) fsh[i] = ap;
     }
     __syncthreads();
     TSA_MPHASE(z, 4)
     // exhaustive search over all C(M-1, K) tuples, row chunks over the CTA
-    search_rows_k12<K, MODE, 16>(t, fsh, g.luts, tBin, M, 0, k12_chunks<K, 16>(M), tid, blockDim.x, best, key);
+    search_rows_k12<K, MODE, 16>(t, fsh, g.luts, tBin, M, 0, k12_chunks<K, 16>(M), tid, blockDim.x, best, key,
+                                 s_p2);
     __syncthreads();  // fsh is reused below
   }
   warp_argmax(best, key);

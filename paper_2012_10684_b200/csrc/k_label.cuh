@@ -59,6 +59,9 @@ __device__ __forceinline__ uint32_t label_of(int v, int t0, int t1, int t2, int 
 // KT = k (compile-time: only k SWAR compares per word; thresholds >= k unused).
 template <typename T, int KT>
 __global__ void __launch_bounds__(256) k_label_flat(LabelArgs g) {
+  // a PDL-launched dependent (k_finalize_phi in the staged step) may start
+  // now: it reads nothing this kernel writes (no effect without one)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t per = g.n / 16;  // 16-voxel groups per slice
   const int64_t i0 = g.z0 * per, i1 = g.z1 * per;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -586,7 +586,16 @@ __host__ __device__ __forceinline__ int64_t tri_qb_off(int M) {
 // the packed R rows, then the triangular T table.
 // (the last double of the offsets area holds the slice's seed score, tri_seed)
 __host__ __device__ __forceinline__ int tri_roff_doubles(int M) { return (((M + 1) / 2) + 2) & ~1; }
-__host__ __device__ __forceinline__ int64_t tri_region_doubles(int M) { return tri_roff_doubles(M) + tri_table_doubles(M); }
+// After the tables: the slice's item prefix counts cum[0..na] (ints, na = M-3-(k-2)+1;
+// tri_items_warp), written once by k_tri_tables instead of per search entry.
+__host__ __device__ __forceinline__ int64_t tri_cum_doubles(int M) { return (M + 3) / 2; }
+__host__ __device__ __forceinline__ int64_t tri_region_doubles(int M) {
+  return tri_roff_doubles(M) + tri_table_doubles(M) + tri_cum_doubles(M);
+}
+// Offset (doubles) of cum from the region start; tbase = roff[M-2] (the R rows' length)
+__host__ __device__ __forceinline__ int64_t tri_cum_off(int M, int tbase) {
+  return tri_roff_doubles(M) + tbase + tri_qb_off(M) + 2 * (int64_t)M;
+}
 // Per-slice region stride (host): room for any M <= L, even (16-byte aligned
 // regions for the bulk copy).
 inline int64_t tri_slice_stride(int L) { return (tri_region_doubles(L) + 1) & ~(int64_t)1; }
@@ -599,6 +608,8 @@ inline int64_t tri_slice_stride(int L) { return (tri_region_doubles(L) + 1) & ~(
 // for the row search of the flattened R loop, else null.
 template <int K, int MODE>
 __device__ double tri_seed(const int M, const double *Tt, const double *asz);
+template <int K>
+__device__ __forceinline__ int tri_items_warp(const int M, const uint64_t r0, const uint64_t r1, int *cum);
 
 template <int K, int MODE>
 __device__ void tri_build(const SearchArgs &g, const int z, const int M, const SliceTables &t, double *base,
@@ -606,6 +617,8 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
   int *roff = reinterpret_cast<int *>(base);
   double *Rt = base + tri_roff_doubles(M);
   const double *asz = g.Asuf + (size_t)z * g.L;
+  __shared__ double s_p2[32];
+  stage_p2(g.luts, s_p2);
   if (threadIdx.x == 0) {
     int o = 0;
     for (int a = 0; a <= M - 3; a++) {
@@ -627,7 +640,7 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // e = j(j+1)/2 + i, i <= j
     while (j * (j + 1) / 2 > e) j--;
     while ((j + 1) * (j + 2) / 2 <= e) j++;
-    Tt[e] = class_term<MODE>(t, g.luts, e - j * (j + 1) / 2, j);
+    Tt[e] = class_term<MODE>(t, g.luts, e - j * (j + 1) / 2, j, s_p2);
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // warp 0: the seed (reads T and Asuf only)
@@ -638,6 +651,12 @@ __device__ void tri_build(const SearchArgs &g, const int z, const int M, const S
     return;  // no further block-wide barrier in the caller before its __syncthreads
   }
   const int tid = threadIdx.x - 32, nth = blockDim.x - 32;
+  if (tid < 32 && M - 1 >= K) {  // warp 1: the item prefix counts of the search (tri_items_warp)
+    const uint64_t NR = binom((uint64_t)(M - 1), K - 1);
+    const uint64_t r0 = NR * (uint64_t)g.unit_begin / (uint64_t)g.units;
+    const uint64_t r1 = NR * (uint64_t)(g.unit_begin + g.nunits) / (uint64_t)g.units;
+    tri_items_warp<K>(M, r0, r1, reinterpret_cast<int *>(base + tri_cum_off(M, tbase)));
+  }
   {  // R rows, a warp per row (lanes over its columns; a flattened loop
      // needed a binary search of roff per entry: ncu, the top stall)
     const int lane = threadIdx.x & 31, nwr = nth >> 5;
@@ -854,6 +873,33 @@ __device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const u
   }
   __syncthreads();
   return s_cum[kTriCum - 1];
+}
+
+// tri_items for one warp (no block barrier): cum[a - (R-1) + 1] = items up to
+// a, cum[0] = 0; returns the total (every lane).
+template <int K>
+__device__ __forceinline__ int tri_items_warp(const int M, const uint64_t r0, const uint64_t r1, int *cum) {
+  constexpr int R = K - 1, G = 32 * (K == 4 ? 16 : 1);
+  const int a0 = R - 1, lane = threadIdx.x & 31;
+  int base = 0;
+  for (int as = a0; as <= M - 3; as += 32) {
+    const int a = as + lane;
+    int cnt = 0;
+    if (a <= M - 3) {
+      const uint64_t lo = max(binom((uint64_t)a, R), r0), hi = min(binom((uint64_t)a + 1, R), r1);
+      if (hi > lo) cnt = K == 3 ? (M - 2 - a + kTri3Cols - 1) / kTri3Cols : (int)((hi - lo + G - 1) / G);
+    }
+    int x = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (a <= M - 3) cum[a - a0 + 1] = base + x;
+    base += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) cum[0] = 0;
+  return base;
 }
 
 template <int K, int MODE>
@@ -1102,7 +1148,6 @@ __global__ void __launch_bounds__(256, TSA_TRI_MINB) k_search_tri(SearchArgs g, 
   extern __shared__ __align__(16) double tsm[];
   __shared__ int s_item;
   __shared__ int32_t s_bin[kTriMaxRows + 2];
-  __shared__ int s_cum[kTriCum];
   __shared__ __align__(8) uint64_t s_bar;  // the tables' bulk copy (TMA)
   uint32_t phase = 0;
   if (threadIdx.x == 0) {
@@ -1128,15 +1173,18 @@ __global__ void __launch_bounds__(256, TSA_TRI_MINB) k_search_tri(SearchArgs g, 
       const uint64_t NR = binom((uint64_t)P, R);
       const uint64_t r0 = NR * (uint64_t)g.unit_begin / (uint64_t)g.units;
       const uint64_t r1 = NR * (uint64_t)(g.unit_begin + g.nunits) / (uint64_t)g.units;
-      const int nitems = tri_items<K>(M, r0, r1, s_cum);
+      // item prefix counts from k_tri_tables (tri_items_warp), total cum[na]
+      const double *region = g.R + (size_t)z * g.TS;
+      const int tbase = reinterpret_cast<const int *>(region)[M - 2];
+      const int64_t coff = tri_cum_off(M, tbase);
+      const int nitems = reinterpret_cast<const int *>(region + coff)[M - 3 - (R - 1) + 1];
       // skip the copy when the slice's items are already all claimed
       if (*((volatile int32_t *)ccur) < nitems) {
-        const double *region = g.R + (size_t)z * g.TS;
         const int32_t *gB = g.Bin + (size_t)z * g.E;
         const bool stage = M + 1 <= kTriMaxRows + 2;
         if (stage)
           for (int e = threadIdx.x; e <= M; e += blockDim.x) s_bin[e] = gB[e];
-        const int64_t nd = tri_region_doubles(M);
+        const int64_t nd = coff + tri_cum_doubles(M);
         if (M <= kTriMaxRows && nd <= smem_doubles) {
           // the slice's tables into shared memory: one TMA bulk copy (the
           // previous entry's generic reads are ordered before it by the
@@ -1151,11 +1199,13 @@ __global__ void __launch_bounds__(256, TSA_TRI_MINB) k_search_tri(SearchArgs g, 
           phase ^= 1u;
           __syncthreads();
           best = tsm[tri_roff_doubles(M) - 1];  // the slice's seed (k_tri_tables)
-          tri_search<K, MODE>(g, M, r0, r1, tsm, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
+          tri_search<K, MODE>(g, M, r0, r1, tsm, stage ? s_bin : gB, ccur,
+                              reinterpret_cast<const int *>(tsm + coff), nitems, best, bestkey);
         } else {
           __syncthreads();
           best = region[tri_roff_doubles(M) - 1];
-          tri_search<K, MODE>(g, M, r0, r1, region, stage ? s_bin : gB, ccur, s_cum, nitems, best, bestkey);
+          tri_search<K, MODE>(g, M, r0, r1, region, stage ? s_bin : gB, ccur,
+                              reinterpret_cast<const int *>(region + coff), nitems, best, bestkey);
         }
       }
     }
@@ -1220,7 +1270,8 @@ __host__ __device__ __forceinline__ int k12_chunks(int M) {
 template <int K, int MODE, int CH = 16>
 __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const double *Apre, const Luts &l,
                                                 const int32_t *bin, int M, int cbeg, int cend, int tid,
-                                                int nth, double &best, uint64_t &bestkey) {
+                                                int nth, double &best, uint64_t &bestkey,
+                                                const double *p2s = nullptr) {
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int P = M - 1;  // positions 0 .. M-2
   if (K == 1) {
@@ -1230,7 +1281,7 @@ __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const doub
 #pragma unroll
       for (int u = 0; u < CH; u++) {
         const int b = min(b0 + u, P - 1);
-        v[u] = combine<MODE>(ident, combine<MODE>(class_term<MODE>(t, l, 0, b), t.Asuf[b]));
+        v[u] = combine<MODE>(ident, combine<MODE>(class_term<MODE>(t, l, 0, b, p2s), t.Asuf[b]));
         if (MODE == PROD_MIN) v[u] = -v[u];
       }
 #pragma unroll
@@ -1261,7 +1312,7 @@ __device__ __forceinline__ void search_rows_k12(const SliceTables &t, const doub
 #pragma unroll
     for (int u = 0; u < CH; u++) {
       const int a = min(a0 + u, b - 1);
-      const double R = combine<MODE>(class_term<MODE>(t, l, a + 1, b), R0);
+      const double R = combine<MODE>(class_term<MODE>(t, l, a + 1, b, p2s), R0);
       v[u] = combine<MODE>(combine<MODE>(ident, Apre[a]), R);
       if (MODE == PROD_MIN) v[u] = -v[u];
     }
@@ -1309,17 +1360,19 @@ __global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
       if (i <= M - 2) sAsuf[i] = t.Asuf[i];
     }
     for (int i = threadIdx.x; i < kSmallLut; i += blockDim.x) sSp[i] = g.luts.sp[i];
+    __shared__ double s_p2[32];
+    stage_p2(g.luts, s_p2);
     __syncthreads();
     const SliceTables ts{sC, sWhi, sWlo, sAsuf};
     Luts ls = g.luts;
     ls.sp = sSp;
     if (K == 2)
-      for (int i = threadIdx.x; i <= M - 2; i += blockDim.x) sApre[i] = class_term<MODE>(ts, ls, 0, i);
+      for (int i = threadIdx.x; i <= M - 2; i += blockDim.x) sApre[i] = class_term<MODE>(ts, ls, 0, i, s_p2);
     __syncthreads();
     const int64_t NC = k12_chunks<K, kK12Chunk>(M);
     const int c0 = (int)(NC * u / g.units), c1 = (int)(NC * (u + 1) / g.units);
     search_rows_k12<K, MODE, kK12Chunk>(ts, sApre, ls, g.Bin + (size_t)z * g.E, M, c0, c1, threadIdx.x,
-                                        blockDim.x, best, bestkey);
+                                        blockDim.x, best, bestkey, s_p2);
   }
   warp_argmax(best, bestkey);
   __shared__ double ss[32];
@@ -1359,6 +1412,7 @@ __global__ void __launch_bounds__(NT) k_search_flat(SearchArgs g) {
 // Each item writes its own (score, key) partial to item_score/key[i][z];
 // k_merge_items folds them per (unit, slice) under the total order.
 constexpr int kK2Rows = 4;  // rows in flight per lane (tables are padded by >= kK2Rows entries)
+constexpr int kK1Q = 128;   // k^(1-q) table of the pruned k = 2 search (classes of < 128 bins)
 
 // The class term of the k = 2 kernel: class_term_nw<MODE> with the polynomial
 // degree fixed at compile time and the 2^-s scaling on the exponent field --
@@ -1432,18 +1486,25 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   // a >= b0 + 3 has none.
   const uint32_t nfirst = PRUNE ? rz[min(ac + 2, M - 1)].c - Ca : 0u;
   // x = W at the record's last row, y = (max Asuf, (C at its first row, -))
-  auto live_xy = [&](const double2 x, const double2 y, const bool chk, const int b0) -> bool {
+  // Near the diagonal the middle class holds few non-empty bins and the
+  // W-based bound is loose; there the power-mean inequality
+  // sum_{i in C} c_i^q <= k^(1-q) (sum c_i)^q, k = #bins of C (q < 1), bounds
+  // the middle class term by k^(1-q) <= kmax^(1-q), kmax = b0 + span - 1 - a
+  // (tab.k1q, one shared load), and the smaller bound is used.
+  auto live_xy = [&](const double2 x, const double2 y, const bool chk, const int b0, const int span) -> bool {
     uint32_t j, rr, n = (uint32_t)__double2loint(y.y) - Ca;
     if (chk && a >= b0) n = nfirst;
     int s;
     nsplit_idx(n, j, s, rr);
     const double ipub = __dmul_rn(tab.jr(j).x, tab.p2(s));
-    const double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(dd_diff(x.x, x.y, Wah, Wal), y.x));
-    return __any_sync(0xffffffffu, (!chk || a < b0 + kK2Rows - 1) && bound >= best);
+    double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(dd_diff(x.x, x.y, Wah, Wal), y.x));
+    const int kmax = b0 + span - 1 - a;
+    if (kmax < kK1Q) bound = fmin(bound, __dmul_rn(__dmul_rn(preub, tab.k1q[max(kmax, 0)]), y.x));
+    return __any_sync(0xffffffffu, (!chk || a < b0 + span - 1) && bound >= best);
   };
   auto live = [&](const K2Row *ck, const bool chk, const int b0) -> bool {
     return live_xy(ldrow<NC>(reinterpret_cast<const double2 *>(ck)),
-                   ldrow<NC>(reinterpret_cast<const double2 *>(ck) + 1), chk, b0);
+                   ldrow<NC>(reinterpret_cast<const double2 *>(ck) + 1), chk, b0, kK2Rows);
   };
   // chkd: the group's bound was already checked (PRUNE) by the caller
   auto group = [&](const int b0, const bool chk, const bool chkd = false) {
@@ -1498,7 +1559,7 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
         nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17));
         ny = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17) + 1);
       }
-      if (live_xy(x, y, false, b0)) {
+      if (live_xy(x, y, false, b0, 16)) {
         double2 gx[4], gy[4];
 #pragma unroll
         for (int g = 0; g < 4; g++) {
@@ -1507,7 +1568,7 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
         }
         unsigned lv = 0;
 #pragma unroll
-        for (int g = 0; g < 4; g++) lv |= live_xy(gx[g], gy[g], false, b0 + 4 * g) ? 1u << g : 0u;
+        for (int g = 0; g < 4; g++) lv |= live_xy(gx[g], gy[g], false, b0 + 4 * g, kK2Rows) ? 1u << g : 0u;
 #pragma unroll 1
         for (int g = 0; g < 4; g++)
           if (lv >> g & 1u) group(b0 + 4 * g, false, true);
@@ -1540,10 +1601,13 @@ template <int MODE, int DEG, bool PRUNE = false>
 __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
   __shared__ double2 s_jr[kSN];
   __shared__ double s_p2[32];
+  __shared__ double s_k1q[PRUNE ? kK1Q : 1];
   for (int i = threadIdx.x; i < kSN; i += blockDim.x) s_jr[i] = make_double2(g.luts.sp[i], g.luts.sp[kSN + i]);
   if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.p2[threadIdx.x];
+  if (PRUNE)  // k^(1-q): within an ulp (the bound's 2^-20 widening covers it)
+    for (int k = threadIdx.x; k < kK1Q; k += blockDim.x) s_k1q[k] = pow((double)k, g.luts.omq);
   __syncthreads();
-  const SpPair tab{s_jr, s_p2};
+  const SpPair tab{s_jr, s_p2, s_k1q};
   const Luts &l = g.luts;
   const int lane = threadIdx.x & 31;
   const int mmax = *g.mmax;
@@ -1608,17 +1672,17 @@ __device__ __forceinline__ double k2_value(const K2Row *rz, const int a, const i
 
 constexpr int kK2SeedRows = 1024;  // rows staged in shared memory (32 KB)
 
+// The per-slice body (k_k2_seed, and k_scan_seed after the slice's tables):
+// srow = shared staging for up to `cap` rows; the early return is CTA-uniform.
 template <int MODE, int DEG>
-__global__ void __launch_bounds__(256) k_k2_seed(SearchArgs g) {
-  __shared__ K2Row srow[kK2SeedRows];
-  const int z = blockIdx.x;
+__device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, const int cap) {
   const int M = g.Mz[z];
   if (g.status[z] != kOK || M < 3) {
     if (threadIdx.x == 0) g.seed[z] = -CUDART_INF;
     return;
   }
   const K2Row *rz = g.rows + (size_t)z * g.RE;
-  if (M <= kK2SeedRows) {  // entries 0 .. M-1 (a + 1, b + 1 <= M - 1)
+  if (M <= cap) {  // entries 0 .. M-1 (a + 1, b + 1 <= M - 1)
     for (int e = threadIdx.x; e < M; e += blockDim.x) srow[e] = rz[e];
     rz = srow;
   }
@@ -1701,6 +1765,12 @@ __global__ void __launch_bounds__(256) k_k2_seed(SearchArgs g) {
     tb = (int)(key & 0xffff);
   }
   if (threadIdx.x == 0) g.seed[z] = k2_value<MODE, DEG>(rz, ta, tb, g.luts, tab);
+}
+
+template <int MODE, int DEG>
+__global__ void __launch_bounds__(256) k_k2_seed(SearchArgs g) {
+  __shared__ K2Row srow[kK2SeedRows];
+  k2_seed_body<MODE, DEG>(g, blockIdx.x, srow, kK2SeedRows);
 }
 
 // Per (unit u in [u0, u1), slice z), one warp: fold the k = 2 tile partials of

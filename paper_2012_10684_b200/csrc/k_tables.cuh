@@ -117,6 +117,8 @@ __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q,
 // [L] doubles + 1 KB of shared scratch, blockDim.x == kTableThreads.
 template <int MODE>
 __device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h, double *wsh) {
+  __shared__ double s_p2[32];  // Luts::p2 (read before: build_tables synchronises)
+  stage_p2(g.luts, s_p2);
   const int tid = threadIdx.x;
   const int L = g.L, E = g.E;
   char *scratch = reinterpret_cast<char *>(wsh + L);
@@ -174,7 +176,7 @@ __device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h
   const int32_t *tBin = g.full ? g.fBin + z * E : cBin;
   K2Row *rows = g.rows ? g.rows + z * g.RE : nullptr;
   for (int i = tid; i <= M - 2; i += blockDim.x) {
-    const double as = class_term<MODE>(t, g.luts, i + 1, M - 1);
+    const double as = class_term<MODE>(t, g.luts, i + 1, M - 1, s_p2);
     Asuf[i] = as;
     if (rows) rows[i + 1] = K2Row{tWhi[i + 1], tWlo[i + 1], as, tC[i + 1], tBin[i + 1]};
   }

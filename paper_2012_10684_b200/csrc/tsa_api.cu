@@ -189,8 +189,10 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     // (k_search_tri regions: tri_slice_stride(bins) doubles per slice)
     w.R = c.take<double>(nz * (size_t)std::max<int64_t>((int64_t)bins * rstride(bins), tsa::tri_slice_stride(bins)) + 16);
-    w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
-    if (k >= 4) w.AI = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+    if (enumeration == TSA_ENUM_FULL) {  // k_search_rows' prefix tables (k_search_tri needs R only)
+      w.PP = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+      if (k >= 4) w.AI = c.take<double>(nz * (size_t)bins * rstride(bins) + 16);
+    }
   }
   return c.off;
 }
@@ -745,6 +747,11 @@ static bool k2_prune_enabled() {
   const char *e = getenv("TSA_K2_PRUNE");
   return !(e && e[0] == '0');
 }
+// k_scan_seed (fused) unless TSA_K2_FUSE=0 (k_scan + k_k2_seed; A/B testing)
+static bool k2_fuse_enabled() {
+  const char *e = getenv("TSA_K2_FUSE");
+  return !(e && e[0] == '0');
+}
 
 tsa_status tsa_search(const uint32_t *hist, int32_t *slice_status, int64_t nz, int64_t N,
                       int32_t bins, int32_t k, double q, int32_t objective, int32_t enumeration,
@@ -802,13 +809,34 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
   sa.luts = l;
   TSA_CUDA(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int32_t), s));
 
-  switch (mode) {
-    case tsa::PROD_MAX: launch_scan<tsa::PROD_MAX>(sa, s); break;
-    case tsa::PROD_MIN: launch_scan<tsa::PROD_MIN>(sa, s); break;
-    case tsa::SUM: launch_scan<tsa::SUM>(sa, s); break;
-    default: launch_scan<tsa::SPP>(sa, s); break;
+  // the pruned k = 2 search (q < 1): tables, seed and bound records in one
+  // kernel (k_scan_seed); else k_scan (+ k_k2_seed below when unfused)
+  const bool k2_prune = k == 2 && mode == tsa::PROD_MAX && enumeration != TSA_ENUM_DP && k2_prune_enabled();
+  const bool fuse_seed = k2_prune && k2_fuse_enabled();
+  if (fuse_seed) {
+    tsa::SearchArgs ss = {};
+    ss.Mz = w.M;
+    ss.status = slice_status;
+    ss.rows = w.rows;
+    ss.RE = k2_row_stride(bins);
+    ss.seed = w.seed;
+    ss.chk = w.chk;
+    ss.nz = nz;
+    ss.luts = l;
+    const int smem = (int)((size_t)bins * sizeof(double) + 1024 + (size_t)bins * sizeof(uint32_t));
+    auto f = l.deg == 5 ? tsa::k_scan_seed<5> : l.deg == 6 ? tsa::k_scan_seed<6> : tsa::k_scan_seed<12>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    f<<<(unsigned)nz, tsa::kTableThreads, (size_t)smem, s>>>(sa, ss, smem);
+    TSA_TRY(check_cuda("k_scan_seed"));
+  } else {
+    switch (mode) {
+      case tsa::PROD_MAX: launch_scan<tsa::PROD_MAX>(sa, s); break;
+      case tsa::PROD_MIN: launch_scan<tsa::PROD_MIN>(sa, s); break;
+      case tsa::SUM: launch_scan<tsa::SUM>(sa, s); break;
+      default: launch_scan<tsa::SPP>(sa, s); break;
+    }
+    TSA_TRY(check_cuda("k_scan"));
   }
-  TSA_TRY(check_cuda("k_scan"));
   if (enumeration == TSA_ENUM_DP) {
     if (units != 1 || unit_begin != 0 || unit_end != 1)
       return set_error(TSA_ERR_INVALID_ARG, "DP search: one work unit per slice");
@@ -944,12 +972,15 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
     // warp-per-a-block search from a global item queue, then the per-unit fold
     const int grid = k2_ctas_per_sm * g_num_sms();
     auto kern = tsa::k_search_k2<tsa::SUM, 6>;
-    if (mode == tsa::PROD_MAX && k2_prune_enabled()) {
-      // seed scores, then the bounded search (bit-identical result, k_search.cuh k2_tile PRUNE)
-      auto sk = l.deg == 5 ? tsa::k_k2_seed<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_k2_seed<tsa::PROD_MAX, 6>
-                                                                          : tsa::k_k2_seed<tsa::PROD_MAX, 12>;
-      sk<<<(unsigned)nz, 256, 0, s>>>(a);
-      TSA_TRY(check_cuda("k_k2_seed"));
+    if (k2_prune) {
+      // seed scores (unless k_scan_seed made them), then the bounded search
+      // (bit-identical result, k_search.cuh k2_tile PRUNE)
+      if (!fuse_seed) {
+        auto sk = l.deg == 5 ? tsa::k_k2_seed<tsa::PROD_MAX, 5> : l.deg == 6 ? tsa::k_k2_seed<tsa::PROD_MAX, 6>
+                                                                            : tsa::k_k2_seed<tsa::PROD_MAX, 12>;
+        sk<<<(unsigned)nz, 256, 0, s>>>(a);
+        TSA_TRY(check_cuda("k_k2_seed"));
+      }
       kern = l.deg == 5   ? tsa::k_search_k2<tsa::PROD_MAX, 5, true>
              : l.deg == 6 ? tsa::k_search_k2<tsa::PROD_MAX, 6, true>
                           : tsa::k_search_k2<tsa::PROD_MAX, 12, true>;
@@ -1005,11 +1036,76 @@ tsa_status tsa_merge(const double *part_score, const uint64_t *part_key, int32_t
   return check_cuda("k_merge");
 }
 
+// The staged step's split finalize (k_decide + labels + k_finalize_phi as the
+// labels' PDL dependent) unless TSA_SPLIT_FINALIZE=0 (A/B testing); the label
+// kernel uses TSA_LABEL_CTAS (default 8) CTAs per SM (c5 A/B, profiles/r2zi:
+// 8 -> 1.197 ms, 7 -> 1.205, 6 -> 1.221, unsplit 1.207).
+static bool split_finalize_enabled() {
+  const char *e = getenv("TSA_SPLIT_FINALIZE");
+  return !(e && e[0] == '0');
+}
+static int label_ctas_split() {
+  const char *e = getenv("TSA_LABEL_CTAS");
+  const int v = e ? atoi(e) : 8;
+  return v >= 1 && v <= 8 ? v : 8;
+}
+
+static tsa::FinalizeArgs finalize_args(const uint32_t *hist, const int32_t *status_in, int64_t nz, int32_t bins,
+                                       int32_t k, double q, int32_t objective, const double *ps,
+                                       const uint64_t *pk, int32_t nparts, int32_t *thresholds,
+                                       double *objective_out, int32_t *status_out, int32_t *status_out2) {
+  tsa::FinalizeArgs f;
+  f.hist = hist;
+  f.status_in = status_in;
+  f.ps = ps;
+  f.pk = pk;
+  f.nparts = nparts;
+  f.nz = nz;
+  f.L = bins;
+  f.k = k;
+  f.objective = objective;
+  f.q = q;
+  f.thresholds = thresholds;
+  f.objective_out = objective_out;
+  f.status_out = status_out;
+  f.status_out2 = status_out2;
+  return f;
+}
+
+static tsa_status decide_impl(const uint32_t *hist, const int32_t *status_in, int64_t nz, int32_t bins,
+                              int32_t k, double q, int32_t objective, const double *ps, const uint64_t *pk,
+                              int32_t nparts, int32_t *thresholds, int32_t *status_out, int32_t *status_out2,
+                              cudaStream_t s) {
+  const tsa::FinalizeArgs f = finalize_args(hist, status_in, nz, bins, k, q, objective, ps, pk, nparts,
+                                            thresholds, nullptr, status_out, status_out2);
+  tsa::k_decide<<<(unsigned)((nz + 7) / 8), 256, 0, s>>>(f);
+  return check_cuda("k_decide");
+}
+
 static tsa_status finalize_impl(const uint32_t *hist, const int32_t *status_in, int64_t nz,
                                 int32_t bins, int32_t k, double q, int32_t objective,
                                 const double *ps, const uint64_t *pk, int32_t nparts,
                                 int32_t *thresholds, double *objective_out, int32_t *status_out,
-                                int32_t *status_out2, cudaStream_t s) {
+                                int32_t *status_out2, cudaStream_t s, bool phi_pdl = false) {
+  if (phi_pdl) {  // k_finalize_phi as the PDL dependent of the label kernel just launched
+    const tsa::FinalizeArgs f = finalize_args(hist, status_in, nz, bins, k, q, objective, ps, pk, nparts,
+                                              thresholds, objective_out, nullptr, nullptr);
+    const size_t smem = (size_t)bins * (sizeof(double) + sizeof(int));
+    if (smem > 32 * 1024)
+      cudaFuncSetAttribute(tsa::k_finalize_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)nz);
+    cfg.blockDim = dim3(tsa::kFinThreads);
+    cfg.dynamicSmemBytes = smem;
+    TSA_CUDA(cudaLaunchKernelEx(&cfg, tsa::k_finalize_phi, f));
+    return check_cuda("k_finalize_phi");
+  }
   tsa::FinalizeArgs f;
   f.hist = hist;
   f.status_in = status_in;
@@ -1205,6 +1301,15 @@ tsa_status tsa_segment(const tsa_problem *p, const tsa_outputs *out, void *works
   TSA_TRY(tsa_histogram(p, hist, w.status, stream));
   TSA_TRY(tsa_search(hist, w.status, p->nz, p->nx * p->ny, p->bins, p->k, p->q, p->objective,
                      p->enumeration, U, 0, U, w.ps, w.pk, w.search, w.search_bytes, stream));
+  if (out->labels && out->objective && split_finalize_enabled()) {
+    // k_decide -> labels -> k_finalize_phi (PDL dependent of the labels, next
+    // to them on the SMs; k_finalize.cuh)
+    TSA_TRY(decide_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
+                        out->thresholds, w.status, out->slice_status, s));
+    TSA_TRY(label_impl(p, out->thresholds, w.status, out->labels, stream, label_ctas_split()));
+    return finalize_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
+                         out->thresholds, out->objective, nullptr, nullptr, s, true);
+  }
   TSA_TRY(finalize_impl(hist, w.status, p->nz, p->bins, p->k, p->q, p->objective, w.ps, w.pk, U,
                         out->thresholds, out->objective, w.status, out->slice_status, s));
   if (out->labels) TSA_TRY(tsa_label(p, out->thresholds, w.status, out->labels, stream));
@@ -1226,8 +1331,11 @@ static bool sweep_args_ok(const tsa_problem *p, const double *qs, int32_t nq) {
   return true;
 }
 
-size_t tsa_sweep_workspace_size(const tsa_problem *p, const double *qs, int32_t nq) {
-  if (!sweep_args_ok(p, qs, nq)) return 0;
+// q values in flight at once (kSweepLanes streams, a staged workspace slot
+// each): the per-q chains are latency-bound kernels of ~one wave each, so
+// running several side by side fills the GPU (round 2).
+constexpr int kSweepLanes = 4;
+static size_t sweep_slot_bytes(const tsa_problem *p, const double *qs, int32_t nq) {
   size_t mx = 0;
   for (int i = 0; i < nq; i++) {
     tsa_problem pq = *p;
@@ -1235,7 +1343,13 @@ size_t tsa_sweep_workspace_size(const tsa_problem *p, const double *qs, int32_t 
     pq.pipeline = -1;
     mx = std::max(mx, carve_segment(&pq, nullptr, nullptr));
   }
-  return align_up((size_t)p->nz * sizeof(int32_t)) + mx;
+  return align_up(mx);
+}
+
+size_t tsa_sweep_workspace_size(const tsa_problem *p, const double *qs, int32_t nq) {
+  if (!sweep_args_ok(p, qs, nq)) return 0;
+  return align_up((size_t)p->nz * sizeof(int32_t)) +
+         (size_t)std::min<int32_t>(nq, kSweepLanes) * sweep_slot_bytes(p, qs, nq);
 }
 
 tsa_status tsa_segment_sweep(const tsa_problem *p, const double *qs, int32_t nq,
@@ -1268,20 +1382,55 @@ tsa_status tsa_segment_sweep(const tsa_problem *p, const double *qs, int32_t nq,
     if (outs[i].histogram && outs[i].histogram != hist)
       TSA_CUDA(cudaMemcpyAsync(outs[i].histogram, hist, sizeof(uint32_t) * p->nz * p->bins,
                                cudaMemcpyDeviceToDevice, s));
-  for (int i = 0; i < nq; i++) {
+  // q chains on up to kSweepLanes streams (q i on lane i % lanes, slot i % lanes
+  // of the workspace; the caller's stream is lane 0); one lane while `stream`
+  // is being captured (the extra streams would outlive the capture)
+  const size_t slot = sweep_slot_bytes(p, qs, nq);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TSA_CUDA(cudaStreamIsCapturing(s, &cs));
+  int lanes = cs == cudaStreamCaptureStatusNone ? std::min<int32_t>(nq, kSweepLanes) : 1;
+  if (const char *e = getenv("TSA_SWEEP_LANES")) lanes = std::max(1, std::min(lanes, atoi(e)));  // A/B
+  cudaStream_t ls[kSweepLanes] = {s};
+  cudaEvent_t ev[kSweepLanes] = {};
+  tsa_status rc = TSA_OK;
+  for (int j = 0; j < lanes && rc == TSA_OK; j++) {
+    if (cudaEventCreateWithFlags(&ev[j], cudaEventDisableTiming) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "sweep: event");
+    if (j > 0 && rc == TSA_OK && cudaStreamCreateWithFlags(&ls[j], cudaStreamNonBlocking) != cudaSuccess)
+      rc = set_error(TSA_ERR_CUDA, "sweep: stream");
+  }
+  if (rc == TSA_OK && lanes > 1) {  // fork after the histogram
+    if (cudaEventRecord(ev[0], s) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "sweep: fork");
+    for (int j = 1; j < lanes && rc == TSA_OK; j++)
+      if (cudaStreamWaitEvent(ls[j], ev[0], 0) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "sweep: fork");
+  }
+  for (int i = 0; i < nq && rc == TSA_OK; i++) {
+    const int j = i % lanes;
+    cudaStream_t sj = ls[j];
     tsa_problem pq = *p;
     pq.q = qs[i];
     SegWs wq;
-    carve_segment(&pq, rest, &wq);
+    carve_segment(&pq, rest + (size_t)j * slot, &wq);
     const int32_t U = units_of(&pq);
-    TSA_CUDA(cudaMemcpyAsync(wq.status, hstatus, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToDevice, s));
-    TSA_TRY(tsa_search(hist, wq.status, pq.nz, pq.nx * pq.ny, pq.bins, pq.k, pq.q, pq.objective,
-                       pq.enumeration, U, 0, U, wq.ps, wq.pk, wq.search, wq.search_bytes, stream));
-    TSA_TRY(finalize_impl(hist, wq.status, pq.nz, pq.bins, pq.k, pq.q, pq.objective, wq.ps, wq.pk, U,
-                          outs[i].thresholds, outs[i].objective, wq.status, outs[i].slice_status, s));
-    if (outs[i].labels && !sweep_labels)
-      TSA_TRY(tsa_label(&pq, outs[i].thresholds, wq.status, outs[i].labels, stream));
+    if (cudaMemcpyAsync(wq.status, hstatus, sizeof(int32_t) * p->nz, cudaMemcpyDeviceToDevice, sj) != cudaSuccess) {
+      rc = set_error(TSA_ERR_CUDA, "sweep: status copy");
+      break;
+    }
+    rc = tsa_search(hist, wq.status, pq.nz, pq.nx * pq.ny, pq.bins, pq.k, pq.q, pq.objective, pq.enumeration, U, 0,
+                    U, wq.ps, wq.pk, wq.search, wq.search_bytes, sj);
+    if (rc == TSA_OK)
+      rc = finalize_impl(hist, wq.status, pq.nz, pq.bins, pq.k, pq.q, pq.objective, wq.ps, wq.pk, U,
+                         outs[i].thresholds, outs[i].objective, wq.status, outs[i].slice_status, sj);
+    if (rc == TSA_OK && outs[i].labels && !sweep_labels)
+      rc = tsa_label(&pq, outs[i].thresholds, wq.status, outs[i].labels, sj);
   }
+  for (int j = 1; j < lanes; j++) {  // join (also on errors: leave no lane behind)
+    if (ls[j] && ev[j] && cudaEventRecord(ev[j], ls[j]) == cudaSuccess) cudaStreamWaitEvent(s, ev[j], 0);
+  }
+  for (int j = 0; j < lanes; j++) {
+    if (ev[j]) cudaEventDestroy(ev[j]);
+    if (j > 0 && ls[j]) cudaStreamDestroy(ls[j]);  // released once its queued work is done
+  }
+  TSA_TRY(rc);
   if (sweep_labels) {  // every q's labels from one read of the volume
     for (int q0 = 0; q0 < nq; q0 += tsa::kSweepMaxQ) {
       tsa::LabelSweepArgs la = {};

@@ -131,6 +131,7 @@ struct SpGlobal {
 struct SpPair {  // shared-memory staging: jr[j] = {j^-q or ln j, 1/j}
   const double2 *jrt;
   const double *p2s;  // shared copy of Luts::p2
+  const double *k1q = nullptr;  // [kK1Q] k^(1-q) (the pruned k = 2 search only)
   __device__ __forceinline__ double2 jr(uint32_t j) const { return jrt[j]; }
   __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
 };
@@ -192,7 +193,7 @@ __device__ __forceinline__ double ipow_t(const Luts &l, const Tab &tab, uint32_t
   nsplit_idx(n, j, s, r);
   const double2 e = tab.jr(j);
   const double d = __dmul_rn(__dmul_rn((double)r, e.y), two_pow_neg(s));
-  return __dmul_rn(__dmul_rn(e.x, l.p2[s]), horner_c(l, d));
+  return __dmul_rn(__dmul_rn(e.x, tab.p2s ? tab.p2s[s] : l.p2[s]), horner_c(l, d));
 }
 
 // Shannon class term S = ln n - w / n (q == 1); NaN at n = 0
@@ -207,7 +208,7 @@ __device__ __forceinline__ double shannon_t(const Luts &l, const Tab &tab, uint3
   double p = l.lc[6];
 #pragma unroll
   for (int k = 5; k >= 0; k--) p = __fma_rn(p, d, l.lc[k]);
-  const double lnn = __dadd_rn(__dadd_rn(e.x, l.p2[s]), __dmul_rn(d, p));
+  const double lnn = __dadd_rn(__dadd_rn(e.x, tab.p2s ? tab.p2s[s] : l.p2[s]), __dmul_rn(d, p));
   const double rcp = __dmul_rn(__dmul_rn(e.y, two_ms), horner_c(l, d));
   return __dsub_rn(lnn, __dmul_rn(w, rcp));
 }
@@ -237,12 +238,21 @@ __device__ __forceinline__ double class_term_nw(const Luts &l, const Tab &tab, u
 //   sum-plus-product:        S = (1 - A) / (q - 1)  (or the q == 1 S)
 // An empty class (n == 0, FULL enumeration only) yields NaN, which never wins a
 // comparison, so invalid tuples are skipped without a branch.
+// p2s: a shared-memory copy of Luts::p2 (stage_p2) -- the index s differs
+// across lanes, and lane-divergent indices into the kernel-parameter copy
+// serialise in the constant cache; null reads the parameter copy (same values).
 template <int MODE>
-__device__ __forceinline__ double class_term(const SliceTables &t, const Luts &l, int a, int b) {
+__device__ __forceinline__ double class_term(const SliceTables &t, const Luts &l, int a, int b,
+                                             const double *p2s = nullptr) {
   // generic loads: the tables may be staged in shared memory
   const uint32_t n = t.C[b + 1] - t.C[a];
   const double w = dd_diff(t.Whi[b + 1], t.Wlo[b + 1], t.Whi[a], t.Wlo[a]);
-  return class_term_nw<MODE>(l, SpGlobal{l.sp}, n, w);
+  return class_term_nw<MODE>(l, SpGlobal{l.sp, p2s}, n, w);
+}
+
+// Luts::p2 into shared memory (threads 0..31; the caller synchronises).
+__device__ __forceinline__ void stage_p2(const Luts &l, double *p2s) {
+  if (threadIdx.x < 32) p2s[threadIdx.x] = l.p2[threadIdx.x];
 }
 
 // Entry e of the small table (Luts::sp layout).

@@ -13,6 +13,7 @@
 #include "k_tables.cuh"
 #include "k_search.cuh"
 #include "k_finalize.cuh"
+#include "k_scan_seed.cuh"
 #include "k_label.cuh"
 #include "k_dp.cuh"
 #include "k_tsallis2d.cuh"

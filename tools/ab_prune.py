@@ -17,6 +17,7 @@ ap.add_argument("workload")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--q", type=float, default=None)
 ap.add_argument("--pipeline", default="auto")
+ap.add_argument("--var", default="TSA_K2_PRUNE", help="environment switch to A/B (0 = off, 1 = on)")
 a = ap.parse_args()
 cfg = phantom.CONFIGS[a.workload]
 vol = torch.from_numpy(phantom.make_volume(cfg)).cuda()
@@ -25,7 +26,7 @@ p = tsa.make_problem(vol, cfg.bins, cfg.k, q, pipeline=a.pipeline)
 ws = tsa.workspace_for(p, vol.device)
 outs = {}
 for flag in ("0", "1", "0", "1"):
-    os.environ["TSA_K2_PRUNE"] = flag
+    os.environ[a.var] = flag
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for i in range(a.reps):
@@ -35,7 +36,7 @@ for flag in ("0", "1", "0", "1"):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(f"{a.workload} q={q} prune={flag} kind={tsa.tsa_pipeline_kind(p)} median {ts[len(ts)//2]:.4f} ms "
+    print(f"{a.workload} q={q} {a.var}={flag} kind={tsa.tsa_pipeline_kind(p)} median {ts[len(ts)//2]:.4f} ms "
           f"min {ts[0]:.4f} ms", flush=True)
     outs[flag] = {k: v.clone() for k, v in out.items() if v is not None}
 for k in outs["0"]:

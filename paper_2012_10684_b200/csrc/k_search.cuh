@@ -551,6 +551,14 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + 
 constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
 constexpr int kTriCum = 512 + 2;                 // item prefix sums, one per t_{k-1} (M <= bins <= 512)
 constexpr int kTri3Cols = 96;                    // k = 3: last thresholds per item (3 per lane)
+#ifndef TSA_TRI4_Q
+#define TSA_TRI4_Q 16
+#endif
+// k = 4: tiles of 4 prefixes per lane per item (32 * 4 * Q prefixes per item).
+// With the exact item bound almost every item is dropped by its bound check,
+// so larger items mean fewer checks (Q = 4 -> 16: the check was 67 % of the
+// kernel's instructions on c4)
+constexpr int kTri4Q = TSA_TRI4_Q;
 #ifndef TSA_TRI_MINB
 #define TSA_TRI_MINB 2  // CTAs per SM of k_search_tri (register cap; A/B builds)
 #endif
@@ -845,7 +853,7 @@ __device__ double tri_seed(const int M, const double *Tt, const double *asz) {
 // G; s_cum[a - (R-1) + 1] = items up to a (thread 0; returns the total).
 template <int K>
 __device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const uint64_t r1, int *s_cum) {
-  constexpr int R = K - 1, G = 32 * (K == 4 ? 16 : 1);  // = tri_search's 32 P Q
+  constexpr int R = K - 1, G = 32 * (K == 4 ? 4 * kTri4Q : 1);  // = tri_search's 32 P Q
   const int a0 = R - 1;
   if (threadIdx.x < 32) {  // warp 0: per-a item counts and their prefix sums
     const int lane = threadIdx.x;
@@ -879,7 +887,7 @@ __device__ __forceinline__ int tri_items(const int M, const uint64_t r0, const u
 // a, cum[0] = 0; returns the total (every lane).
 template <int K>
 __device__ __forceinline__ int tri_items_warp(const int M, const uint64_t r0, const uint64_t r1, int *cum) {
-  constexpr int R = K - 1, G = 32 * (K == 4 ? 16 : 1);
+  constexpr int R = K - 1, G = 32 * (K == 4 ? 4 * kTri4Q : 1);
   const int a0 = R - 1, lane = threadIdx.x & 31;
   int base = 0;
   for (int as = a0; as <= M - 3; as += 32) {
@@ -909,7 +917,7 @@ __device__ __forceinline__ void tri_search(const SearchArgs &g, const int M, con
                                            uint64_t &bestkey) {
   constexpr int R = K - 1;           // prefix length (t_1 .. t_{k-1}, t_{k-1} = a)
   constexpr int P = K == 4 ? 4 : 1;  // prefixes per register tile
-  constexpr int Q = K == 4 ? 4 : 1;  // tiles per lane per item
+  constexpr int Q = K == 4 ? kTri4Q : 1;  // tiles per lane per item
   constexpr int G = 32 * P * Q;      // prefixes per item
   const int *roff = reinterpret_cast<const int *>(base);
   const double *Rt = base + tri_roff_doubles(M);

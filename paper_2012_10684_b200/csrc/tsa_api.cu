@@ -925,7 +925,12 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
     // slower: 96 vs 46 us on c3)
     TSA_TRY(check_cuda("k_tri_tables"));
     const unsigned grid = (unsigned)std::min<int64_t>(items, 2 * g_num_sms());
-    kern<<<grid, 256, smem, s>>>(a, (int)(smem / sizeof(double)));
+    // TSA_TRI_STAGE=0 (A/B): no shared-memory copy of the slice's tables, the
+    // search reads them through L1/L2 (with the exact bounds most of them are
+    // never read)
+    const char *st_env = getenv("TSA_TRI_STAGE");
+    const bool stage = !(st_env && st_env[0] == '0');
+    kern<<<grid, 256, stage ? smem : 0, s>>>(a, stage ? (int)(smem / sizeof(double)) : 0);
     TSA_TRY(check_cuda("k_search_tri"));
     tsa::k_fold_slots<<<(unsigned)((nz + 7) / 8), 256, 0, s>>>(w.item_score, w.item_key, a.ss, nz, a.nunits,
                                                               part_score, part_key);

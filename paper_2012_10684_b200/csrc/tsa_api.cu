@@ -903,7 +903,11 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
     a.units = units;
     a.unit_begin = unit_begin;
     a.nunits = unit_end - unit_begin;
-    a.ss = k == 3 ? 2 : 4;  // CTAs sharing a slice (k = 3 slices are small)
+    // CTAs sharing a slice: with the exact bounds most items are dropped
+    // cheaply, so fewer table copies win (profiles/r2zq: c3 ss 1/2/4 = 283/288/309
+    // us, c4 ss 2/4/8 = 221/232/251 us)
+    a.ss = k == 3 ? 1 : 2;
+    if (const char *e = getenv("TSA_TRI_SS")) a.ss = std::max(1, std::min(kTriSS, atoi(e)));  // A/B
     a.TS = tsa::tri_slice_stride(bins);
     a.ccur = w.ccur;
     a.item_score = w.item_score;

@@ -223,7 +223,7 @@ tsa_status tsa_label(const tsa_problem *p, const int32_t *thresholds,
  * device in slabs, runs tsa_segment per slab and copies thresholds, objective,
  * status and (if labels_host != NULL) labels back: compute on stream0,
  * copy-out on stream1, copy-in on a stream the call creates and destroys,
- * ordered by events over two device buffers, so the H2D and D2H copy engines
+ * ordered by events over three device slab buffers, so the H2D and D2H copy engines
  * and the kernels run concurrently.  Device scratch (dev_buf, dev_bytes) comes from the
  * caller: tsa_segment_host_scratch_size() bytes.  Blocks until done. */
 size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab_slices);

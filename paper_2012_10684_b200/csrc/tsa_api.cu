@@ -1946,11 +1946,17 @@ static size_t small_bytes(const tsa_problem *p) {
   return c.off;
 }
 
+// device slab buffers of tsa_segment_host: with two, the copy-in of slab i+2
+// waited for slab i's labels to leave, i.e. for slab i's compute -- a bubble
+// of one compute latency per slab on the H2D engine; three keep both copy
+// engines streaming
+constexpr int kHostBufs = 3;
+
 size_t tsa_segment_host_scratch_size(const tsa_problem *p, int64_t slab) {
   if (tsa_validate(p) != TSA_OK || slab <= 0) return 0;
   slab = std::min(slab, p->nz);
   tsa_problem sp;
-  return 2 * slab_bytes(p, slab, &sp) + small_bytes(p);
+  return (size_t)kHostBufs * slab_bytes(p, slab, &sp) + small_bytes(p);
 }
 
 tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, double *obj_h,
@@ -1961,17 +1967,17 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   slab = std::min(slab, p->nz);
   tsa_problem sp;
   const size_t per = slab_bytes(p, slab, &sp);
-  if (dev_bytes < 2 * per + small_bytes(p)) return set_error(TSA_ERR_WORKSPACE, "device scratch too small");
+  if (dev_bytes < kHostBufs * per + small_bytes(p)) return set_error(TSA_ERR_WORKSPACE, "device scratch too small");
   const size_t esz = p->dtype == TSA_U8 ? 1 : 2;
   const int64_t n = p->nx * p->ny;
-  Carve cs{reinterpret_cast<char *>(dev_buf) + 2 * per};
+  Carve cs{reinterpret_cast<char *>(dev_buf) + kHostBufs * per};
   int32_t *thr_all = cs.take<int32_t>((size_t)p->nz * p->k);
   double *obj_all = cs.take<double>((size_t)p->nz);
   int32_t *sts_all = cs.take<int32_t>((size_t)p->nz);
   // Three streams: copy-in on a stream of this call (created and destroyed
   // here: the call blocks anyway), compute on stream0, copy-out on stream1.
-  // Two device buffers: slab i+2 may overwrite buffer i%2 once slab i's labels
-  // left (ev_free); slab i is computed once it arrived (ev_in) and its labels
+  // kHostBufs device buffers: slab i+3 may overwrite buffer i%3 once slab i's
+  // labels left (ev_free); slab i is computed once it arrived (ev_in) and its labels
   // leave once it is computed (ev_done) -- so the H2D engine streams slab i+1
   // while the kernels run on slab i and the D2H engine drains slab i-1.
   // Thresholds, objective and status stay on the device for the whole volume
@@ -1981,8 +1987,8 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   // c1's single 256^2 slice is latency-bound)
   const bool own_in = p->nz > slab;
   if (own_in) TSA_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-  cudaEvent_t ev_done[2], ev_free[2], ev_in[2], ev_start;
-  for (int b = 0; b < 2; b++) {
+  cudaEvent_t ev_done[kHostBufs], ev_free[kHostBufs], ev_in[kHostBufs], ev_start;
+  for (int b = 0; b < kHostBufs; b++) {
     TSA_CUDA(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
     TSA_CUDA(cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming));
     TSA_CUDA(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming));
@@ -1994,7 +2000,7 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   tsa_status rc = TSA_OK;
   for (int64_t z0 = 0, i = 0; z0 < p->nz && rc == TSA_OK; z0 += slab, i++) {
     const int64_t nzs = std::min(slab, p->nz - z0);
-    const int b = (int)(i & 1);
+    const int b = (int)(i % kHostBufs);
     Carve c{reinterpret_cast<char *>(dev_buf) + b * per};
     char *vol = c.take<char>((size_t)slab * n * esz);
     uint8_t *lab = c.take<uint8_t>((size_t)slab * n);
@@ -2007,7 +2013,8 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
     char *ws = c.take<char>(0);
     const size_t wsb = tsa_workspace_size(&q);
     const char *src = reinterpret_cast<const char *>(p->volume) + (size_t)z0 * n * esz;
-    if (i >= 2 && cudaStreamWaitEvent(cin, ev_free[b], 0) != cudaSuccess) rc = set_error(TSA_ERR_CUDA, "wait ev_free");
+    if (i >= kHostBufs && cudaStreamWaitEvent(cin, ev_free[b], 0) != cudaSuccess)
+      rc = set_error(TSA_ERR_CUDA, "wait ev_free");
     if (rc == TSA_OK && cudaMemcpyAsync(vol, src, (size_t)nzs * n * esz, cudaMemcpyHostToDevice, cin) != cudaSuccess)
       rc = set_error(TSA_ERR_CUDA, "H2D");
     if (rc == TSA_OK && (cudaEventRecord(ev_in[b], cin) != cudaSuccess ||
@@ -2038,7 +2045,7 @@ tsa_status tsa_segment_host(const tsa_problem *p, int64_t slab, int32_t *thr_h, 
   }
   const cudaError_t e0 = cudaStreamSynchronize(comp), e1 = cudaStreamSynchronize(cout),
                     e2 = own_in ? cudaStreamSynchronize(cin) : cudaSuccess;
-  for (int b = 0; b < 2; b++) {
+  for (int b = 0; b < kHostBufs; b++) {
     cudaEventDestroy(ev_done[b]);
     cudaEventDestroy(ev_free[b]);
     cudaEventDestroy(ev_in[b]);

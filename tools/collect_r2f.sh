@@ -2,13 +2,16 @@
 # Round-2 evidence on the GPU box (gpurun): bench lines for every workload,
 # the reference arm, ncu launch lists and compact exports (details / raw /
 # hot SASS lines) of --set full captures of the dominant kernels.
-# Usage: tools/collect_r2.sh <tag>     (writes gpurun_out/<tag>/)
+# Final round-2 sweep: also the GPU test suite, smoke() and compute-sanitizer.
+# Usage: tools/collect_r2f.sh <tag>     (writes gpurun_out/<tag>/)
 set -u
 TAG=${1:-r2}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT /tmp/ncu
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/gpu.txt
 nproc > $OUT/host.txt; lscpu | grep "Model name" >> $OUT/host.txt
+timeout 2400 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $OUT/smoke.log 2>&1; echo "rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench_c5.jsonl 2> $OUT/bench_c5.err
 timeout 600 python bench.py --workload c1 --steps 2000 --warmup 20 > $OUT/bench_c1.jsonl 2> $OUT/bench_c1.err
 timeout 600 python bench.py --workload c2 --steps 2000 --warmup 20 > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err
@@ -48,4 +51,5 @@ prof tri_c4 k_search_tri $P c4 --reps 2
 prof tri_c3 k_search_tri $P c3 --reps 2
 prof hist_c2 k_hist_part $P c2 --reps 2
 prof mid_c2 k_mid $P c2 --reps 2
+timeout 1800 bash tools/sanitize.sh $OUT/sanitizer > $OUT/sanitize.log 2>&1; echo "rc=$?" >> $OUT/sanitize.log
 du -sh $OUT

@@ -1104,7 +1104,7 @@ def run_1d(args, cfg, rank, world, dev):
     tri = k >= 3 and bins <= 512 and args.enumeration == "canonical"  # + k_fold_slots
     # + k_k2_seed: the bounded k = 2 search (q < 1, TSA_K2_PRUNE not 0), fused
     # into k_scan_seed (replacing k_scan) unless TSA_K2_FUSE=0
-    seed = k == 2 and args.enumeration != "dp" and qs[0] < 1 and os.environ.get("TSA_K2_PRUNE", "1")[:1] != "0"
+    seed = k == 2 and args.enumeration == "canonical" and qs[0] < 1 and os.environ.get("TSA_K2_PRUNE", "1")[:1] != "0"
     seed_kernel = seed and os.environ.get("TSA_K2_FUSE", "1")[:1] == "0"
     # staged step with labels: k_decide + labels + k_finalize_phi (split finalize)
     split = not sweep and os.environ.get("TSA_SPLIT_FINALIZE", "1")[:1] != "0"

@@ -1466,9 +1466,9 @@ __device__ __forceinline__ double k2_term(const Luts &l, const Tab &tab, uint32_
 // ck16[b0+1] the same over rows b0..b0+15, checked first for every 16 rows
 // (two 16-byte loads per check instead of the group's eight row loads: the
 // first pruned version was L1-bound, ncu 93 % L1/TEX throughput).
-template <int MODE, int DEG, bool NC = true, bool PRUNE = false>
+template <int MODE, int DEG, bool NC = true, bool PRUNE = false, class Tab = SpPair>
 __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
-                                        const int lane, const Luts &l, const SpPair &tab, double &best,
+                                        const int lane, const Luts &l, const Tab &tab, double &best,
                                         uint64_t &bestkey, const K2Row *ck4 = nullptr,
                                         const K2Row *ck16 = nullptr) {
   static_assert(!PRUNE || MODE == PROD_MAX, "k = 2 pruning bounds the product form with q < 1");

@@ -811,7 +811,9 @@ static tsa_status search_impl(const uint32_t *hist, int32_t *slice_status, int64
 
   // the pruned k = 2 search (q < 1): tables, seed and bound records in one
   // kernel (k_scan_seed); else k_scan (+ k_k2_seed below when unfused)
-  const bool k2_prune = k == 2 && mode == tsa::PROD_MAX && enumeration != TSA_ENUM_DP && k2_prune_enabled();
+  // (canonical only: FULL positions include empty bins, where the bound's
+  // class-size factor n(a, b0)^-q is undefined for an empty first row)
+  const bool k2_prune = k == 2 && mode == tsa::PROD_MAX && enumeration == TSA_ENUM_CANONICAL && k2_prune_enabled();
   const bool fuse_seed = k2_prune && k2_fuse_enabled();
   if (fuse_seed) {
     tsa::SearchArgs ss = {};

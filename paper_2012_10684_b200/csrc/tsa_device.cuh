@@ -125,6 +125,7 @@ struct Luts {
 struct SpGlobal {
   const double *sp;
   const double *p2s = nullptr;  // shared copy of Luts::p2 (k2_term users only)
+  const double *k1q = nullptr;  // (the pruned k = 2 search only; unused here)
   __device__ __forceinline__ double2 jr(uint32_t j) const { return make_double2(sp[j], sp[kSN + j]); }
   __device__ __forceinline__ double p2(int s) const { return p2s[s]; }
 };

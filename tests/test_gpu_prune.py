@@ -177,3 +177,16 @@ def test_k2_many_bins_unstaged_seed(q):
     vol = torch.from_numpy(np.stack(slices)).to(DEV)
     _same(_run(vol, 4096, q, True, pipeline="staged"), _run(vol, 4096, q, False, pipeline="staged"),
           f"many bins q={q}")
+
+
+@pytest.mark.parametrize("q", [0.5, 0.8])
+def test_k2_full_enumeration_equals_canonical(q):
+    """FULL enumeration (positions = every bin, empty ones included; the
+    unpruned kernel) against the pruned canonical search, L = 256 with ~90
+    non-empty bins and L = 4096 (12-bit): the same thresholds and objective."""
+    for name, nz in (("c2", 6), ("c5", 2)):
+        cfg = phantom.CONFIGS[name]
+        vol = torch.from_numpy(phantom.make_volume(cfg, nz=nz, z_first=150)).to(DEV)
+        a = _run(vol, cfg.bins, q, True, pipeline="staged")
+        b = _run(vol, cfg.bins, q, True, pipeline="staged", enumeration="full")
+        _same(a, b, f"{name} full vs canonical q={q}")

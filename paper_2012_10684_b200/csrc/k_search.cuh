@@ -551,6 +551,9 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return j * (j + 1) / 2 + 
 constexpr int kTriMaxRows = 128;                 // positions staged in static shared memory
 constexpr int kTriCum = 512 + 2;                 // item prefix sums, one per t_{k-1} (M <= bins <= 512)
 constexpr int kTri3Cols = 96;                    // k = 3: last thresholds per item (3 per lane)
+#ifndef TSA_TRI_SEED_PASSES
+#define TSA_TRI_SEED_PASSES 3  // coordinate-ascent rounds of the k >= 3 seed (tri_seed)
+#endif
 #ifndef TSA_TRI4_Q
 #define TSA_TRI4_Q 16
 #endif
@@ -819,7 +822,7 @@ __device__ double tri_seed(const int M, const double *Tt, const double *asz) {
 #pragma unroll
   for (int j = 1; j < K; j++) t[j] = max(t[j], t[j - 1] + 1);  // strictly increasing
   double best = val(t);
-  for (int pass = 0; pass < 3; pass++) {
+  for (int pass = 0; pass < TSA_TRI_SEED_PASSES; pass++) {
 #pragma unroll
     for (int j = 0; j < K; j++) {
       const int lo = j == 0 ? 0 : t[j - 1] + 1, hi = j == K - 1 ? M - 2 : t[j + 1] - 1;
@@ -1679,6 +1682,9 @@ __device__ __forceinline__ double k2_value(const K2Row *rz, const int a, const i
 }
 
 constexpr int kK2SeedRows = 1024;  // rows staged in shared memory (32 KB)
+#ifndef TSA_K2_SEED_GRID
+#define TSA_K2_SEED_GRID 32  // side of the seed's coarse grid of (a, b)
+#endif
 
 // The per-slice body (k_k2_seed, and k_scan_seed after the slice's tables):
 // srow = shared staging for up to `cap` rows; the early return is CTA-uniform.
@@ -1730,22 +1736,23 @@ __device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, cons
     warp_argmax(v, key);
     return key;  // every warp reduces the same entries: block-uniform
   };
-  const int S = (M - 1 + 31) / 32;
+  constexpr int GS = TSA_K2_SEED_GRID, GU = (GS * GS + 255) / 256;  // grid side, points per thread
+  const int S = (M - 1 + GS - 1) / GS;
   double v = -CUDART_INF;
   uint64_t key = kKeyNone;
-  {  // grid: 1024 points, 4 per thread, independent (their loads overlap)
-    double x[4];
-    uint64_t kx[4];
+  {  // grid: GS x GS points, independent (their loads overlap)
+    double x[GU];
+    uint64_t kx[GU];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < GU; u++) {
       const int e = threadIdx.x + u * 256;
-      const int a = S * (e >> 5), b = S * (e & 31);
-      const bool ok = e < 1024 && a < b && b <= M - 2;
+      const int a = S * (e / GS), b = S * (e % GS);
+      const bool ok = e < GS * GS && a < b && b <= M - 2;
       x[u] = ok ? k2_value<MODE, DEG>(rz, a, b, g.luts, tab) : -CUDART_INF;
       kx[u] = ok ? (((uint64_t)a << 16) | (uint64_t)b) : kKeyNone;
     }
 #pragma unroll
-    for (int u = 0; u < 4; u++)
+    for (int u = 0; u < GU; u++)
       if (better(x[u], kx[u], v, key)) {
         v = x[u];
         key = kx[u];

@@ -32,19 +32,8 @@ namespace tsa {
 // debug builds only (tools/fused_trace.py): per-task (type, z, smid, t0, t1)
 __device__ unsigned long long g_trace[5 * 65536];
 __device__ int g_trace_n;
-__device__ unsigned long long g_mphase[8 * 4096];  // per slice: 8 phase timestamps of its M task
-#define TSA_MPHASE(z, i) \
-  if (threadIdx.x == 0 && (z) < 4096) g_mphase[8 * (z) + (i)] = gtimer();
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 #endif
-
-#ifndef TSA_TRACE
-#define TSA_MPHASE(z, i)
-#endif
+// TSA_MPHASE / g_mphase / gtimer: tsa_device.cuh
 
 struct FusedArgs {
   const uint8_t *vol;
@@ -232,7 +221,7 @@ __device__ void fused_mid(const FusedArgs &g, int z, char *smem) {
   __shared__ int s_status, s_M;
   __shared__ double s_red[32], s_P[kKMax + 1], s_S[kKMax + 1];
   __shared__ uint64_t s_key[32];
-  __shared__ __align__(16) double s_scan[96];
+  __shared__ __align__(16) double s_scan[128];  // build_tables scratch: 1 KB
   __shared__ double s_p2[32];  // Luts::p2 for the class terms (synchronised below)
   stage_p2(g.luts, s_p2);
   TSA_MPHASE(z, 0)

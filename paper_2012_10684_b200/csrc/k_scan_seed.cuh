@@ -13,6 +13,7 @@ namespace tsa {
 template <int DEG>
 __global__ void __launch_bounds__(kTableThreads) k_scan_seed(ScanArgs g, SearchArgs sa, int smem_bytes) {
   extern __shared__ __align__(16) double wsh[];
+  TSA_MPHASE(blockIdx.x, 0)
   uint32_t *hs = reinterpret_cast<uint32_t *>(wsh + g.L + 128);
   const uint4 *h4 = reinterpret_cast<const uint4 *>(g.hist + (int64_t)blockIdx.x * g.L);
   if ((g.L & 3) == 0 && (reinterpret_cast<uintptr_t>(g.hist) & 15) == 0)
@@ -20,9 +21,12 @@ __global__ void __launch_bounds__(kTableThreads) k_scan_seed(ScanArgs g, SearchA
   else
     for (int i = threadIdx.x; i < g.L; i += blockDim.x) hs[i] = g.hist[(int64_t)blockIdx.x * g.L + i];
   __syncthreads();
+  TSA_MPHASE(blockIdx.x, 1)
   scan_slice<PROD_MAX>(g, blockIdx.x, hs, wsh);
   __syncthreads();  // the slice's rows / M / status are written (global, this CTA)
+  TSA_MPHASE(blockIdx.x, 2)
   k2_seed_body<PROD_MAX, DEG>(sa, blockIdx.x, reinterpret_cast<K2Row *>(wsh), smem_bytes / (int)sizeof(K2Row));
+  TSA_MPHASE(blockIdx.x, 7)
 }
 
 }  // namespace tsa

@@ -1703,6 +1703,7 @@ __device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, cons
   __shared__ double s_p2[32];
   if (threadIdx.x < 32) s_p2[threadIdx.x] = g.luts.p2[threadIdx.x];
   __syncthreads();
+  TSA_MPHASE(z, 3)
   // bound records of the search (k2_tile PRUNE): entry e = b0 + 1 covers rows
   // b0 .. b0+3 (chk4) / b0 .. b0+15 (chk16), clipped to the slice's last row
   // M-1 (records reaching past it are never read)
@@ -1758,7 +1759,9 @@ __device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, cons
         key = kx[u];
       }
   }
+  TSA_MPHASE(z, 4)
   key = reduce(v, key);
+  TSA_MPHASE(z, 5)
   int ta = key == kKeyNone ? 0 : (int)(key >> 16), tb = key == kKeyNone ? 1 : (int)(key & 0xffff);
   for (int pass = 0; pass < 2; pass++) {
     const bool move_a = pass == 0;
@@ -1779,6 +1782,7 @@ __device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, cons
     ta = (int)(key >> 16);
     tb = (int)(key & 0xffff);
   }
+  TSA_MPHASE(z, 6)
   if (threadIdx.x == 0) g.seed[z] = k2_value<MODE, DEG>(rz, ta, tb, g.luts, tab);
 }
 

@@ -122,6 +122,21 @@ struct Luts {
 // p2(s): 2^(-s q) (Luts::p2) from a shared-memory copy -- the k = 2 kernels
 // index it per lane, and a lane-divergent index into the kernel-parameter
 // copy serialises in the constant cache (ncu: LDC in the k = 2 hot loop).
+#ifdef TSA_TRACE
+// debug builds only: 8 phase timestamps per slice of a per-slice kernel
+// (k_mid: tools/fused_trace.py; k_scan_seed: tools/scan_trace.py)
+__device__ unsigned long long g_mphase[8 * 4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TSA_MPHASE(z, i) \
+  if (threadIdx.x == 0 && (z) < 4096) g_mphase[8 * (z) + (i)] = gtimer();
+#else
+#define TSA_MPHASE(z, i)
+#endif
+
 struct SpGlobal {
   const double *sp;
   const double *p2s = nullptr;  // shared copy of Luts::p2 (k2_term users only)

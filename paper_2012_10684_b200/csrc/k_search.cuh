@@ -47,7 +47,7 @@ struct SearchArgs {
   int ss;                            // k_search_tri: CTA entries per slice
   int32_t *ccur;                     // k_search_tri: [nz] per-slice chunk counters, zeroed
   double *seed;                      // [nz] seed scores of the pruned k = 2 search (k_k2_seed)
-  K2Row *chk;                        // [2][nz][RE] bound records of the pruned k = 2 search (k_k2_seed)
+  K2Chk *chk;                        // [2][nz][RE] bound records of the pruned k = 2 search (k_k2_seed)
   int64_t TS;                        // k_tri_tables / k_search_tri: doubles per slice region (tri_slice_stride)
 };
 
@@ -1464,16 +1464,17 @@ __device__ __forceinline__ double k2_term(const Luts &l, const Tab &tab, uint32_
 // it is neither the argmax nor tied with it: the result is the exhaustive
 // search's, bit for bit.  The first 32 columns (lanes with a >= b) and the
 // last partial group are always evaluated.
-// The bound's inputs come from per-slice records (k_k2_seed): ck4[b0+1] =
-// {W at row b0+3, max Asuf over rows b0..b0+3, C at row b0} for a group and
+// The bound's inputs come from per-slice records (k_k2_seed, K2Chk: one
+// 16-byte load): ck4[b0+1] = {W at row b0+3 rounded up, max Asuf over rows
+// b0..b0+3 rounded up to float, C at row b0} for a group and
 // ck16[b0+1] the same over rows b0..b0+15, checked first for every 16 rows
 // (two 16-byte loads per check instead of the group's eight row loads: the
 // first pruned version was L1-bound, ncu 93 % L1/TEX throughput).
 template <int MODE, int DEG, bool NC = true, bool PRUNE = false, class Tab = SpPair>
 __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int i, const int blo, const int bhi,
                                         const int lane, const Luts &l, const Tab &tab, double &best,
-                                        uint64_t &bestkey, const K2Row *ck4 = nullptr,
-                                        const K2Row *ck16 = nullptr) {
+                                        uint64_t &bestkey, const K2Chk *ck4 = nullptr,
+                                        const K2Chk *ck16 = nullptr) {
   static_assert(!PRUNE || MODE == PROD_MAX, "k = 2 pruning bounds the product form with q < 1");
   const double ident = MODE == SUM ? 0.0 : 1.0;
   const int a = 32 * i + lane;
@@ -1502,20 +1503,21 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
   // sum_{i in C} c_i^q <= k^(1-q) (sum c_i)^q, k = #bins of C (q < 1), bounds
   // the middle class term by k^(1-q) <= kmax^(1-q), kmax = b0 + span - 1 - a
   // (tab.k1q, one shared load), and the smaller bound is used.
-  auto live_xy = [&](const double2 x, const double2 y, const bool chk, const int b0, const int span) -> bool {
-    uint32_t j, rr, n = (uint32_t)__double2loint(y.y) - Ca;
+  // x = the record as {wub, (amax float bits | c << 32)} (K2Chk)
+  auto live_xy = [&](const double2 x, const bool chk, const int b0, const int span) -> bool {
+    uint32_t j, rr, n = (uint32_t)__double2hiint(x.y) - Ca;
     if (chk && a >= b0) n = nfirst;
     int s;
     nsplit_idx(n, j, s, rr);
+    const double amax = (double)__int_as_float(__double2loint(x.y));
     const double ipub = __dmul_rn(tab.jr(j).x, tab.p2(s));
-    double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(dd_diff(x.x, x.y, Wah, Wal), y.x));
+    double bound = __dmul_rn(__dmul_rn(preub, ipub), __dmul_rn(dd_diff(x.x, 0.0, Wah, Wal), amax));
     const int kmax = b0 + span - 1 - a;
-    if (kmax < kK1Q) bound = fmin(bound, __dmul_rn(__dmul_rn(preub, tab.k1q[max(kmax, 0)]), y.x));
+    if (kmax < kK1Q) bound = fmin(bound, __dmul_rn(__dmul_rn(preub, tab.k1q[max(kmax, 0)]), amax));
     return __any_sync(0xffffffffu, (!chk || a < b0 + span - 1) && bound >= best);
   };
-  auto live = [&](const K2Row *ck, const bool chk, const int b0) -> bool {
-    return live_xy(ldrow<NC>(reinterpret_cast<const double2 *>(ck)),
-                   ldrow<NC>(reinterpret_cast<const double2 *>(ck) + 1), chk, b0, kK2Rows);
+  auto live = [&](const K2Chk *ck, const bool chk, const int b0) -> bool {
+    return live_xy(ldrow<NC>(reinterpret_cast<const double2 *>(ck)), chk, b0, kK2Rows);
   };
   // chkd: the group's bound was already checked (PRUNE) by the caller
   auto group = [&](const int b0, const bool chk, const bool chkd = false) {
@@ -1563,23 +1565,16 @@ __device__ __forceinline__ void k2_tile(const K2Row *rz, const int M, const int 
     // records one 16-row block ahead (their L1/L2 latency was the top stall);
     // inside a live block the four group records are loaded together
     double2 nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 1));
-    double2 ny = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 1) + 1);
     for (; b0 + 15 <= bend; b0 += 16) {
-      const double2 x = nx, y = ny;
-      if (b0 + 31 <= bend) {
-        nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17));
-        ny = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17) + 1);
-      }
-      if (live_xy(x, y, false, b0, 16)) {
-        double2 gx[4], gy[4];
+      const double2 x = nx;
+      if (b0 + 31 <= bend) nx = ldrow<NC>(reinterpret_cast<const double2 *>(ck16 + b0 + 17));
+      if (live_xy(x, false, b0, 16)) {
+        double2 gx[4];
 #pragma unroll
-        for (int g = 0; g < 4; g++) {
-          gx[g] = ldrow<NC>(reinterpret_cast<const double2 *>(ck4 + b0 + 4 * g + 1));
-          gy[g] = ldrow<NC>(reinterpret_cast<const double2 *>(ck4 + b0 + 4 * g + 1) + 1);
-        }
+        for (int g = 0; g < 4; g++) gx[g] = ldrow<NC>(reinterpret_cast<const double2 *>(ck4 + b0 + 4 * g + 1));
         unsigned lv = 0;
 #pragma unroll
-        for (int g = 0; g < 4; g++) lv |= live_xy(gx[g], gy[g], false, b0 + 4 * g, kK2Rows) ? 1u << g : 0u;
+        for (int g = 0; g < 4; g++) lv |= live_xy(gx[g], false, b0 + 4 * g, kK2Rows) ? 1u << g : 0u;
 #pragma unroll 1
         for (int g = 0; g < 4; g++)
           if (lv >> g & 1u) group(b0 + 4 * g, false, true);
@@ -1646,7 +1641,7 @@ __global__ void __launch_bounds__(256, TSA_K2_MINB) k_search_k2(SearchArgs g) {
     uint64_t bestkey = kKeyNone;
     if (g.status[z] == kOK && 32 * i <= M - 3 && bhi >= 32 * i + 1 && blo <= M - 2) {
       if (PRUNE) best = g.seed[z];
-      const K2Row *ck = PRUNE ? g.chk + (size_t)z * g.RE : nullptr;
+      const K2Chk *ck = PRUNE ? g.chk + (size_t)z * g.RE : nullptr;
       k2_tile<MODE, DEG, true, PRUNE>(g.rows + (size_t)z * g.RE, M, i, blo, bhi, lane, l, tab, best, bestkey, ck,
                                       PRUNE ? ck + (size_t)g.nz * g.RE : nullptr);
       warp_argmax(best, bestkey);
@@ -1708,15 +1703,16 @@ __device__ void k2_seed_body(const SearchArgs &g, const int z, K2Row *srow, cons
   // b0 .. b0+3 (chk4) / b0 .. b0+15 (chk16), clipped to the slice's last row
   // M-1 (records reaching past it are never read)
   {
-    K2Row *c4 = g.chk + (size_t)z * g.RE, *c16 = c4 + (size_t)g.nz * g.RE;
+    K2Chk *c4 = g.chk + (size_t)z * g.RE, *c16 = c4 + (size_t)g.nz * g.RE;
     for (int e = 1 + threadIdx.x; e <= M - 1; e += blockDim.x) {
       const int e4 = min(e + 3, M - 1), e16 = min(e + 15, M - 1);
       double m4 = rz[e].as, m16;
       for (int x = e + 1; x <= e4; x++) m4 = fmax(m4, rz[x].as);
       m16 = m4;
       for (int x = e4 + 1; x <= e16; x++) m16 = fmax(m16, rz[x].as);
-      c4[e] = K2Row{rz[e4].wh, rz[e4].wl, m4, rz[e].c, 0};
-      c16[e] = K2Row{rz[e16].wh, rz[e16].wl, m16, rz[e].c, 0};
+      // upper bounds: W rounded up from its dd (hi + lo), Asuf max rounded up to float
+      c4[e] = K2Chk{__dadd_ru(rz[e4].wh, rz[e4].wl), __double2float_ru(m4), rz[e].c};
+      c16[e] = K2Chk{__dadd_ru(rz[e16].wh, rz[e16].wl), __double2float_ru(m16), rz[e].c};
     }
   }
   const SpGlobal tab{g.luts.sp, s_p2};

@@ -140,7 +140,7 @@ struct SearchWs {
   tsa::K2Row *rows = nullptr;    // [nz][k2_row_stride] packed positions (k = 2)
   int32_t *ccur = nullptr;       // [nz] per-slice chunk counters (k_search_tri)
   double *seed = nullptr;        // [nz] seed scores of the pruned k = 2 search
-  tsa::K2Row *chk = nullptr;     // [2][nz][k2_row_stride] bound records of the pruned k = 2 search
+  tsa::K2Chk *chk = nullptr;     // [2][nz][k2_row_stride] bound records of the pruned k = 2 search
 };
 
 constexpr int kTriSS = 8;  // k_search_tri: CTA entries per slice
@@ -184,7 +184,7 @@ size_t carve_search(Carve &c, SearchWs &w, int64_t nz, int64_t N, int32_t bins, 
     w.item_key = c.take<uint64_t>((size_t)k2_blocks(bins) * tsa::k2_tiles(bins) * nz);
     w.rows = c.take<tsa::K2Row>(nz * (size_t)k2_row_stride(bins) + kPad);
     w.seed = c.take<double>(nz);
-    w.chk = c.take<tsa::K2Row>(2 * nz * (size_t)k2_row_stride(bins) + kPad);
+    w.chk = c.take<tsa::K2Chk>(2 * nz * (size_t)k2_row_stride(bins) + kPad);
   }
   if (use_rtable(bins, k, objective) && enumeration != TSA_ENUM_DP) {
     // (k_search_tri regions: tri_slice_stride(bins) doubles per slice)

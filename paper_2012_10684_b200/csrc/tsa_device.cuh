@@ -103,6 +103,15 @@ struct __align__(16) K2Row {
   int32_t bin;
 };
 
+// Bound record of the pruned k = 2 search (k2_tile PRUNE, one 16-byte load):
+// wub >= the exact W (dd hi + lo, rounded up) at the record's last row, amax
+// >= max Asuf over its rows (rounded up to float), c = C at its first row.
+struct __align__(16) K2Chk {
+  double wub;
+  float amax;
+  uint32_t c;
+};
+
 struct Luts {
   const double *sp;  // [kSN] j^-q (ln j at q == 1) | [kSN] 1/j; entry j = 0: NaN
   double p2[32];     // 2^(-s q) (q == 1: ln 2^s), s = 0..31, from the host (kernel parameter:

@@ -53,7 +53,7 @@ constexpr int kTableThreads = 256;
 __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q, int shannon,
                                              double *wsh, uint32_t *C, double *Whi, double *Wlo,
                                              int32_t *Bin, char *scratch, int &m_out,
-                                             uint32_t &n_out) {
+                                             uint32_t &n_out, const int zt = 1 << 30) {
   // exactly kTableThreads threads do the work whatever the block size (>= it),
   // so every kernel produces bit-identical tables
   const int tid = threadIdx.x, T = kTableThreads;
@@ -69,6 +69,7 @@ __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q,
     }
   }
   __syncthreads();
+  TSA_SPHASE(zt, 1)
   uint32_t m_l = 0, n_l = 0;
   dd w_l = {0.0, 0.0};
   for (int i = i0; i < i1; i++) {
@@ -81,7 +82,9 @@ __device__ __forceinline__ void build_tables(const uint32_t *h, int L, double q,
   }
   uint32_t m_ex, n_ex, m_tot, n_tot;
   dd w_ex;
+  TSA_SPHASE(zt, 2)
   block_scan_mnw(m_l, n_l, w_l, m_ex, n_ex, w_ex, m_tot, n_tot, scratch, T);
+  TSA_SPHASE(zt, 3)
   if (tid == 0) {
     C[0] = 0;
     Whi[0] = 0.0;
@@ -127,7 +130,9 @@ __device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h
   int32_t *cBin = g.cBin + z * E;
   int m;
   uint32_t ntot;
-  build_tables(h, L, g.q, g.shannon, wsh, cC, cWhi, cWlo, cBin, scratch, m, ntot);
+  TSA_SPHASE(z, 0)
+  build_tables(h, L, g.q, g.shannon, wsh, cC, cWhi, cWlo, cBin, scratch, m, ntot, (int)z);
+  TSA_SPHASE(z, 4)
   int status = g.status[z];
   if (status == kOK && m < g.k + 1) status = kNoValidSplit;
   __syncthreads();
@@ -175,11 +180,13 @@ __device__ void scan_slice(const ScanArgs &g, const int64_t z, const uint32_t *h
   double *Asuf = g.Asuf + z * L;
   const int32_t *tBin = g.full ? g.fBin + z * E : cBin;
   K2Row *rows = g.rows ? g.rows + z * g.RE : nullptr;
+  TSA_SPHASE(z, 5)
   for (int i = tid; i <= M - 2; i += blockDim.x) {
     const double as = class_term<MODE>(t, g.luts, i + 1, M - 1, s_p2);
     Asuf[i] = as;
     if (rows) rows[i + 1] = K2Row{tWhi[i + 1], tWlo[i + 1], as, tC[i + 1], tBin[i + 1]};
   }
+  TSA_SPHASE(z, 6)
 }
 
 template <int MODE>

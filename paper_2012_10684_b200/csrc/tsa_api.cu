@@ -2071,6 +2071,10 @@ int tsa_debug_trace(unsigned long long *host, int max_entries) {
   cudaMemcpyToSymbol(tsa::g_trace_n, &zero, sizeof(int));
   return n;
 }
+int tsa_debug_sphase(unsigned long long *host, int nz) {
+  cudaMemcpyFromSymbol(host, tsa::g_sphase, sizeof(unsigned long long) * 8 * std::min(nz, 4096));
+  return 0;
+}
 int tsa_debug_mphase(unsigned long long *host, int nz) {
   cudaMemcpyFromSymbol(host, tsa::g_mphase, sizeof(unsigned long long) * 8 * std::min(nz, 4096));
   return 0;

@@ -142,8 +142,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TSA_MPHASE(z, i) \
   if (threadIdx.x == 0 && (z) < 4096) g_mphase[8 * (z) + (i)] = gtimer();
+// inside the table build (scan_slice / build_tables): tools/scan_trace.py
+__device__ unsigned long long g_sphase[8 * 4096];
+#define TSA_SPHASE(z, i) \
+  if (threadIdx.x == 0 && (z) < 4096) g_sphase[8 * (z) + (i)] = gtimer();
 #else
 #define TSA_MPHASE(z, i)
+#define TSA_SPHASE(z, i)
 #endif
 
 struct SpGlobal {

@@ -32,3 +32,11 @@ print(f"{name}: kernel span {(ph[:, 7].max() - t0) / 1e3:.1f} us, CTA duration m
 print("  phases (mean us):", ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))))
 st = (ph[:, 0] - t0) / 1e3
 print("  CTA start times (us) percentiles 0/25/50/75/100:", np.percentile(st, [0, 25, 50, 75, 100]).round(1))
+
+lib.tsa_debug_sphase.argtypes = [ctypes.c_void_p, ctypes.c_int]
+sp = np.zeros(8 * 4096, np.uint64)
+lib.tsa_debug_sphase(sp.ctypes.data, cfg.nz)
+sp = sp[: 8 * cfg.nz].reshape(cfg.nz, 8).astype(np.int64)
+d = np.diff(sp[:, :7], axis=1) / 1e3
+names = ["pow (all bins, lane-strided)", "per-thread prefix", "block scan", "table writes", "status/M", "Asuf + rows"]
+print("  table phases (mean us):", ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))))
